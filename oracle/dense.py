@@ -1,0 +1,142 @@
+"""Tiny-size dense definitions in numpy (TEST INFRASTRUCTURE ONLY; see oracle/__init__.py).
+
+These are the plain definitions written out densely -- usable only for small n -- and
+serve to pin the C oracle:
+
+* ``dense_L``            Eq. L as a dense matrix.
+* ``series_Z``           Eq. PX as an explicit power series.
+* ``neumann_Z``          Lemma 1's gamma -> infinity limit (1-alpha)(I - alpha L L^T)^{-1} X
+                         (proof).
+* ``msa_matrix``         Eq. s: the exact MSA matrix S.
+* ``obj1``               Eq. obj1 for one partition.
+* ``best_partition``     brute force over all partitions into <= k clusters (n <= 10).
+* ``sin_theta``          robust sin of the largest principal angle.
+* ``ari``                adjusted Rand index for label comparisons.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def dense_B(n, m, rowptr, col, val=None):
+    B = np.zeros((n, m))
+    for u in range(n):
+        for e in range(rowptr[u], rowptr[u + 1]):
+            B[u, col[e]] += 1.0 if val is None else float(val[e])
+    return B
+
+
+def dense_L(B):
+    du, dv = B.sum(1), B.sum(0)
+    su = np.where(du > 0, 1.0 / np.sqrt(np.where(du > 0, du, 1.0)), 0.0)
+    sv = np.where(dv > 0, 1.0 / np.sqrt(np.where(dv > 0, dv, 1.0)), 0.0)
+    return su[:, None] * B * sv[None, :]
+
+
+def series_Z(L, X, alpha, T):
+    """(1-alpha) sum_{r=0}^{T} alpha^r (L L^T)^r X, with the dense matrix power."""
+    M = L @ L.T
+    out = np.zeros_like(X, dtype=np.float64)
+    P = np.eye(M.shape[0])
+    c = (1.0 - alpha) if alpha < 1.0 else 1.0
+    for r in range(T + 1):
+        out += c * (alpha ** r) * (P @ X)
+        P = P @ M
+    return out
+
+
+def neumann_Z(L, X, alpha):
+    M = L @ L.T
+    return (1.0 - alpha) * np.linalg.solve(np.eye(M.shape[0]) - alpha * M, X)
+
+
+def rownorm(Z):
+    nr = np.linalg.norm(Z, axis=1, keepdims=True)
+    return np.where(nr > 0, Z / np.where(nr > 0, nr, 1.0), 0.0)
+
+
+def msa_matrix(Zhat):
+    """Eq. s: s(i,j) = e^{z_i.z_j} / (sqrt(sum_l e^{z_i.z_l}) sqrt(sum_l e^{z_j.z_l}))."""
+    K = np.exp(Zhat @ Zhat.T)
+    rs = K.sum(1)
+    return K / np.sqrt(np.outer(rs, rs))
+
+
+def obj1(S, labels):
+    """Eq. obj1: sum_l (1/|C_l|) sum_{i in C_l, j not in C_l} s(u_i, u_j)."""
+    labels = np.asarray(labels)
+    tot = 0.0
+    for c in np.unique(labels):
+        inn = labels == c
+        tot += S[np.ix_(inn, ~inn)].sum() / inn.sum()
+    return tot
+
+
+def partitions(n, k):
+    """All set partitions of range(n) into at most k blocks (restricted-growth strings)."""
+    a = [0] * n
+
+    def rec(i, mx):
+        if i == n:
+            yield tuple(a)
+            return
+        for v in range(min(mx + 2, k)):
+            a[i] = v
+            yield from rec(i + 1, max(mx, v))
+
+    if n == 0:
+        yield ()
+        return
+    a[0] = 0
+    yield from rec(1, 0)
+
+
+def best_partition(S, k, exact_k=True):
+    """Brute-force minimiser of Eq. obj1 over partitions into k (or <= k) non-empty blocks."""
+    n = S.shape[0]
+    best, arg, allv = math.inf, None, []
+    for p in partitions(n, k):
+        if exact_k and len(set(p)) != k:
+            continue
+        v = obj1(S, p)
+        allv.append((v, p))
+        if v < best:
+            best, arg = v, p
+    allv.sort()
+    return arg, best, allv
+
+
+def orth(A):
+    q, _ = np.linalg.qr(np.asarray(A, dtype=np.float64))
+    return q
+
+
+def sin_theta(A, B):
+    """Robust sin(max principal angle) between span(A) and span(B):
+    ||Q_B - Q_A (Q_A^T Q_B)||_2 after fp64 Householder orthonormalisation."""
+    qa, qb = orth(A), orth(B)
+    return float(np.linalg.norm(qb - qa @ (qa.T @ qb), 2))
+
+
+def ari(a, b):
+    """Adjusted Rand index (Hubert & Arabie) from the contingency table."""
+    a, b = np.asarray(a), np.asarray(b)
+    ua, ia = np.unique(a, return_inverse=True)
+    ub, ib = np.unique(b, return_inverse=True)
+    ct = np.zeros((ua.size, ub.size), np.int64)
+    np.add.at(ct, (ia, ib), 1)
+
+    def c2(x):
+        x = np.asarray(x, np.float64)
+        return (x * (x - 1) / 2).sum()
+
+    n = a.size
+    s_ij, s_a, s_b = c2(ct), c2(ct.sum(1)), c2(ct.sum(0))
+    tot = n * (n - 1) / 2
+    exp = s_a * s_b / tot if tot > 0 else 0.0
+    mx = 0.5 * (s_a + s_b)
+    if mx == exp:
+        return 1.0
+    return float((s_ij - exp) / (mx - exp))
