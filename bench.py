@@ -1,0 +1,297 @@
+#!/usr/bin/env python
+"""bench.py -- the TPO hot path (arXiv 2405.11922) on B200: one step = one whole pass of
+propagate -> Haar Q -> features -> exact top-k -> ONMF + NCI over BASELINE.json's
+configs[1] ("small") by default, through libtpo's C-ABI (tpo_run).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config small]
+
+Prints ONE JSON line (rank 0).  `value` is the whole-step throughput in MSA-propagation work
+units (2 * nnz * d * T multiply-adds per step, i.e. nnz*d per SpMM) per second with inputs
+resident in HBM; `ms_per_step` is the end-to-end TPO time per step.  `e2e` is the same
+metric with host inputs copied in and labels copied out inside the timed region.
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def propagation_bytes(n, m, nnz, d):
+    """SURVEY.md §8(d) compulsory bytes per hop (unit weights): Z read (SpMM-1), X read and
+    Z write (SpMM-2), the V-side block written and read, int32 indices of both CSRs, int64
+    row pointers, and the two degree-scale vectors."""
+    return 4 * (3 * n * d + 2 * m * d) + 2 * 4 * nnz + 8 * (n + m + 2) + 4 * (n + m)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                for nm, v in zip(names, f[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, g, ws, rank):
+    """The fp64 oracle as it stands, on a bounded sample: one propagation hop (a1-a3) over the
+    full graph per step (the stages a5-a9 are excluded: the oracle's D x D Jacobi alone would
+    take minutes at D = 2000)."""
+    if rank != 0:
+        return
+    from oracle import core as O
+    O.lib()
+    cores = len(os.sched_getaffinity(0))
+    units = 2 * g.nnz * g.d * 1
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, 1)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = units * len(times) / tot
+    unit = "nnz*d/s"
+    sample = f"oracle_propagate over the full {g.name} graph, 1 of T={g.T} hops per step (a1-a3 only)"
+    line = {"impl": "reference", "metric": metric_name(), "value": value, "unit": unit, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(g, args, ws),
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def metric_name():
+    return "MSA propagation nnz*d/s over the end-to-end TPO step"
+
+
+def config_dict(g, args, ws):
+    return {"workload": f"{g.name} planted ABG (BASELINE.json configs[{['tiny','small','medium','large','xl'].index(g.name)}])",
+            "n_u": g.n, "n_v": g.m, "nnz": g.nnz, "d": g.d, "k": g.k, "alpha": g.alpha, "T": g.T, "Tf": args.tf,
+            "Tg": args.tg, "eig": "exact", "seed": 0, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+            "l2": "256 MiB L2 flush between timed steps; inputs also exceed L2"}
+
+
+def cpu_baseline_sample(g):
+    from oracle import core as O
+    O.lib()
+    t0 = time.perf_counter()
+    O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, 1)
+    dt = time.perf_counter() - t0
+    return {"value": 2 * g.nnz * g.d / dt, "unit": "nnz*d/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "oracle",
+            "sample": f"oracle_propagate, 1 of T={g.T} hops over the full {g.name} graph ({dt:.1f} s; a5-a9 excluded)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="small")
+    ap.add_argument("--tf", type=int, default=5)
+    ap.add_argument("--tg", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+
+    from synth import make_config
+    g = make_config(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, g, ws, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2405_11922_b200 as T
+    from paper_2405_11922_b200._lib import lib
+
+    L = lib()
+    dg = T.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, device=dev)
+    X = torch.from_numpy(g.X).to(dev)
+    runner = T.Runner(dg, g.d, g.k, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return runner(X, g.alpha, g.T, g.G, args.tf, args.tg)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # --- timed region: device-resident inputs ------------------------------------------
+    stage = np.zeros(4)
+    times = []
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.tpo_launch_count()
+    with ClockSampler(local) as cs:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            stage += runner.timings
+    torch.cuda.synchronize()
+    launches = L.tpo_launch_count() - launches0
+    tot_ms = float(sum(times))
+    if ws > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        tot_ms = float(t.item())
+    units = 2.0 * g.nnz * g.d * g.T
+    value = ws * units * args.steps / (tot_ms / 1e3)
+    ms_step = tot_ms / args.steps
+    stage_ms = stage / args.steps
+
+    # --- end to end through the public API with host buffers ----------------------------
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hX, hBr, hBc, hTr, hTc = pin(g.X), pin(g.B_rowptr), pin(g.B_col), pin(g.Bt_rowptr), pin(g.Bt_col)
+        h2d = sum(t.numel() * t.element_size() for t in (hX, hBr, hBc, hTr, hTc))
+        d2h = g.n * 4
+        hlab = torch.empty(g.n, dtype=torch.int32).pin_memory()
+        et = []
+        for it in range(max(2, args.steps // 2) + 1):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dg2 = T.DeviceGraph(g.n, g.m, g.nnz, dg.B_rowptr, dg.B_col, dg.Bt_rowptr, dg.Bt_col)
+            dg2.B_rowptr.copy_(hBr, non_blocking=True)
+            dg2.B_col.copy_(hBc, non_blocking=True)
+            dg2.Bt_rowptr.copy_(hTr, non_blocking=True)
+            dg2.Bt_col.copy_(hTc, non_blocking=True)
+            X.copy_(hX, non_blocking=True)
+            lab = runner(X, g.alpha, g.T, g.G, args.tf, args.tg)
+            hlab.copy_(lab, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if it > 0:
+                et.append(e0.elapsed_time(e1))
+        e2e_ms = float(np.mean(et))
+        if ws > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": ws * units / (e2e_ms / 1e3), "unit": "nnz*d/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # --- roofline of the propagation (the paper's dominant cost) --
+    pk, src = peaks()
+    bytes_hop = propagation_bytes(g.n, g.m, g.nnz, g.d)
+    prop_ms = stage_ms[0]
+    achieved = bytes_hop * g.T / (prop_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("bytes_per_hop")
+        except Exception:
+            traffic = None
+    roof = {"kernel": "spmm_kernel pair (one hop: SpMM-1 V side + SpMM-2 U side, fix-ups, per-call schedule)",
+            "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": src,
+            "algorithmic_bytes_per_hop": bytes_hop, "hops": g.T, "propagate_ms": prop_ms}
+
+    line = {"metric": metric_name(), "value": value, "unit": "nnz*d/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": config_dict(g, args, ws),
+            "stages_ms": {"propagate": stage_ms[0], "features": stage_ms[1], "topk_eig": stage_ms[2],
+                          "cluster": stage_ms[3]},
+            "tpo_seconds": ms_step / 1e3,
+            "propagation_nnz_d_per_s": 2.0 * g.nnz * g.d * g.T / (prop_ms / 1e3),
+            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": cs.summary()}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(g)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

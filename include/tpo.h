@@ -1,0 +1,188 @@
+/*
+ * tpo.h -- C-ABI of libtpo, the B200 (sm_100a) implementation of the TPO hot path
+ * ("Effective Clustering on Large Attributed Bipartite Graphs", arXiv 2405.11922).
+ *
+ * Citations are PAPER.md line numbers of the paper's LaTeX source plus the equation /
+ * algorithm label; "R<n>" names a reading of a silent or garbled passage listed in
+ * DESIGN.md ("Readings").
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - Pointers are DEVICE pointers unless marked (host).  Dense matrices are row-major.
+ *    Dense float/double device buffers must be 16-byte aligned.
+ *  - Ownership: the caller allocates and owns every buffer; the library never frees
+ *    caller memory and keeps no pointer after a call returns.  The only objects the
+ *    library owns are the opaque communicator handles of tpo_comm_create.
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls enqueue on it and return without synchronising, except those marked [sync],
+ *    which copy small fp64 matrices to the host, factor them there and copy back; [sync]
+ *    calls return after their work has completed.
+ *  - Workspace: calls that take (ws, ws_bytes) have a size query tpo_<name>_ws(...);
+ *    a smaller ws_bytes returns TPO_ENOMEM.  ws must be 256-byte aligned.
+ *  - Errors: the int return is 0 (TPO_OK) or a negative TPO_E* code; no C++ exception
+ *    crosses the ABI.  tpo_last_error() returns a thread-local message describing the
+ *    last failure.  On error the contents of output buffers are unspecified.
+ *  - Determinism: no floating-point atomics; every cross-thread reduction has a fixed
+ *    order, so identical inputs give bitwise-identical outputs on the same GPU model.
+ *  - Thread safety: concurrent calls on different streams with disjoint buffers are
+ *    allowed; the only global mutable state is thread-local (last-error slot, launch count).
+ */
+#ifndef TPO_H
+#define TPO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPO_ABI_VERSION 1
+
+enum {
+    TPO_OK = 0,
+    TPO_EINVAL = -1,    /* bad shape, null pointer, range, alignment, unknown mode       */
+    TPO_ECUDA = -2,     /* a CUDA runtime call or kernel launch failed                     */
+    TPO_ENOMEM = -3,    /* ws_bytes below the size query                                   */
+    TPO_ENCCL = -4,     /* an NCCL call failed (multi-GPU entry points)                    */
+    TPO_ENUMERIC = -5   /* non-SPD Gram in CholeskyQR, zero singular value, non-finite     */
+};
+
+/* Sparse bipartite adjacency B_U or its transpose, in CSR.
+ * row_ptr: int64 [n_rows+1] (device), monotone, row_ptr[0] = 0, row_ptr[n_rows] = nnz;
+ * col_idx: int32 [nnz] (device), each < n_cols; val: fp32 [nnz] (device) non-negative edge
+ * weights w(u_i, v_j), or NULL for unit weights.  Duplicate (row, col) pairs must have
+ * been merged by the caller. */
+typedef struct tpo_csr {
+    int64_t n_rows, n_cols, nnz;
+    const int64_t *row_ptr;
+    const int32_t *col_idx;
+    const float *val;
+} tpo_csr_t;
+
+int tpo_abi_version(void);
+const char *tpo_last_error(void);
+/* Number of CUDA kernels this library has launched from the calling host thread (monotone
+ * thread-local counter; for launch accounting in benchmarks). */
+uint64_t tpo_launch_count(void);
+
+/* ---------------------------------------------------------------------------------------
+ * a1-a3  MSA propagation.  Lemma 1 / Eq. PX truncated at gamma = T
+ * hops, with L = D_U^{-1/2} B D_V^{-1/2} (Eq. L) and the
+ * hop update of Eq. update-Z bracketed as L (L^T Z):
+ *      Z_0 = c X ;   Z <- c X + alpha * L (L^T Z)   (T times),   c = 1 - alpha  (R1;
+ *      c = 1 when alpha = 1), then Zhat[i] = Z[i] / ||Z[i]|| (Eq. Z),
+ *      zero rows stay zero (R4).  D_U, D_V are the weighted degrees,
+ *      1/sqrt(0) := 0 (R3).
+ *   B  : n_u x n_v CSR;  Bt: the same edges as an n_v x n_u CSR (B^T).
+ *   X  : n_u x d fp32 (input, not modified).  d >= 4, d % 4 == 0.
+ *   Z  : n_u x d fp32 out (raw Z, prefactor c); also used as the iterate in place.
+ *   Zhat: n_u x d fp32 out, or NULL.
+ *   alpha in [0, 1], T >= 0.
+ * Workspace: tpo_propagate_ws(n_u, n_v, nnz, d).
+ * Errors: TPO_EINVAL (shapes of B/Bt/X disagree, Bt.nnz != B.nnz, alpha/T/d out of range,
+ * null or misaligned pointers), TPO_ENOMEM, TPO_ECUDA.
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_propagate_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d);
+int tpo_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d,
+                  float alpha, int32_t T, float *Z, float *Zhat,
+                  void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a4  Haar rotation, Alg. 1 L6-7: Q = the Q factor of the QR
+ * decomposition of the d x d Gaussian matrix G, sign-fixed so that diag(R) > 0, which
+ * makes Q Haar-distributed and unique.  Host-only, fp64.
+ *   G: (host) d x d fp64 in;  Q: (host) d x d fp64 out.  Errors: TPO_EINVAL.
+ * --------------------------------------------------------------------------------------- */
+int tpo_haar_q(const double *G, int64_t d, double *Q);
+
+/* ---------------------------------------------------------------------------------------
+ * a5  Random features (Alg. 1 L8-9; Eq. R-prime; Eq. Ri 466-468):
+ *      Zo = sqrt(d) * Zhat * Q^T ;  R' = sqrt(e/d) * ( sin(Zo) || cos(Zo) )   (n x 2d,
+ *      sin in columns [0,d), cos in [d,2d));  r = sum_i R'[i] (fp64);
+ *      dinv[i] = 1 / sqrt(max(R'[i] . r, 1e-12))   (R6)     so that R = diag(dinv) R'.
+ *   Zhat: n x d fp32;  Q: d x d fp32 (from tpo_haar_q);  Rp: n x 2d fp32 out;
+ *   dinv: n fp32 out;  r_out: 2d fp64 out (device) or NULL.
+ * Workspace: tpo_features_ws(n, d).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA.
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_features_ws(int64_t n, int64_t d);
+int tpo_features(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp,
+                 float *dinv, double *r_out, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a6  Implicit affinity product: out = S~ Y with S~ = R R^T = diag(dinv) R' R'^T diag(dinv)
+ * (R R^T approximates the MSA matrix S, Theorem 1); evaluated as
+ * dinv . (R' (R'^T (dinv . Y))) so the n x n matrix is never formed.
+ *   Rp: n x D fp32;  dinv: n fp32;  Y: n x b fp32;  out: n x b fp32 out (may not alias Y).
+ *   The D x b intermediate R'^T (dinv . Y) is reduced across the GPU in fp64.
+ * Workspace: tpo_affinity_matvec_ws(n, D, b).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA.
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_affinity_matvec_ws(int64_t n, int64_t D, int64_t b);
+int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D,
+                        const float *Y, int64_t b, float *out, void *ws, size_t ws_bytes,
+                        void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a7  Top-k singular triplets of R = diag(dinv) R' -- "the top-k left and right singular
+ * vectors of R" and its top-k singular values (Eq. init-HY).
+ *   mode TPO_EIG_EXACT (R7): the exact top-k.  Gram G = R^T R (D x D, fp64 cross-block
+ *     sums), host fp64 symmetric eigensolve, Gamma = R Psi Sigma^{-1}, CholeskyQR2 polish
+ *     when ||Gamma^T Gamma - I||_max > 1e-6.  Equivalent to block subspace iteration on
+ *     S~ with a full-rank block (b = D), which converges in one step.
+ *   mode TPO_EIG_HALKO: the randomised truncated SVD the paper cites (Halko et al.,
+ *     PAPER.md:574) with b = k + p columns, q power iterations, orthonormalisation by
+ *     CholeskyQR2, Rayleigh-Ritz on the host.  Omega (D x b fp32) is its Gaussian test
+ *     matrix.  An approximation of the EXACT result (exact only when it has converged).
+ *   Both modes apply the sign rule R8 (column sums of Gamma >= 0).
+ *   Rp: n x D fp32;  dinv: n fp32;  1 <= k <= min(n, D) (HALKO: k + p <= min(n, D)).
+ *   Gamma: n x k fp32 out;  sigma: (host) k fp64 out, descending;  Psi: D x k fp32 out.
+ * [sync].  Workspace: tpo_topk_eig_ws(n, D, k, mode, p).
+ * Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC (sigma_k == 0, non-SPD Gram).
+ * --------------------------------------------------------------------------------------- */
+enum { TPO_EIG_EXACT = 0, TPO_EIG_HALKO = 1 };
+size_t tpo_topk_eig_ws(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p);
+int tpo_topk_eig(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k,
+                 int32_t mode, int32_t p, int32_t q, const float *Omega,
+                 float *Gamma, double *sigma, float *Psi, void *ws, size_t ws_bytes,
+                 void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * a8-a9  Discretisation: greedy orthogonal NMF (Alg. 2, Eqs. update-Q /
+ * update-Y PAPER.md:553-560, products bracketed as PAPER.md:564), initialised from the
+ * top-k triplets (Eq. init-HY) with the R9 clamps
+ *     Ups = max(Gamma,0)+eps, H = max(Psi Sigma,0)+eps, eps = 1e-12,
+ *     H   <- H   . max(R^T Ups,0) / (H (Ups^T Ups) + eps)
+ *     Ups <- Ups . sqrt( max(R H,0) / (max(Ups (Ups^T (R H)),0) + eps) ),
+ * T_f times (H first), then NCI generation (Alg. 3): Phi = I; T_g times
+ * l*_i = argmax_l Ups[i].Phi[:,l] (Eq. ell-ast, ties -> smallest l), Y one-hot with unit
+ * columns (Eqs. Y-update, y-norm), Phi = Ups^T Y; early stop on a
+ * repeated labelling (R10).  All arithmetic fp64.
+ *   Rp: n x D fp32;  dinv: n fp32;  Gamma: n x k fp32;  sigma: (host) k fp64;
+ *   Psi: D x k fp32;  Tf >= 0, Tg >= 1;  labels: n int32 out in [0,k);
+ *   iters_used: (host) int32 out, iterations of Alg. 3 actually run (may be NULL).
+ * [sync].  Workspace: tpo_cluster_ws(n, D, k).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA.
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_cluster_ws(int64_t n, int64_t D, int32_t k);
+int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k,
+                const float *Gamma, const double *sigma, const float *Psi, int32_t Tf,
+                int32_t Tg, int32_t *labels, int32_t *iters_used, void *ws,
+                size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Whole hot path (Fig. overview): propagate -> Haar Q from G -> features ->
+ * top-k (mode) -> cluster.  G: (host) d x d fp64.  Omega: D x (k+p) fp32 (HALKO only, else
+ * NULL).  labels: n int32 out.  timings_ms: (host) 4 doubles out {propagate, features,
+ * topk, cluster} measured with CUDA events on `stream`, or NULL.
+ * [sync].  Workspace: tpo_run_ws(n_u, n_v, nnz, d, k, mode, p).
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, int32_t mode,
+                  int32_t p);
+int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha,
+            int32_t T, int32_t k, const double *G, int32_t eig_mode, const float *Omega,
+            int32_t p, int32_t q, int32_t Tf, int32_t Tg, int32_t *labels,
+            double *timings_ms, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPO_H */

@@ -1,0 +1,9 @@
+"""B200-native (sm_100a) implementation of the TPO hot path (arXiv 2405.11922).
+
+The product is libtpo.so (C-ABI in include/tpo.h, CUDA sources in csrc/); this package is
+its thin Python binding.  There is no CPU fallback: importing the binding functions needs
+the built library (`python -m paper_2405_11922_b200.build`).
+"""
+from .tpo import (DeviceGraph, Runner, affinity_matvec, cluster, features, haar_q,  # noqa: F401
+                  propagate, run, to_device_graph, topk_eig)
+from ._lib import TPO_EIG_EXACT, TPO_EIG_HALKO, TpoError, lib  # noqa: F401

@@ -1,0 +1,84 @@
+"""ctypes loader of the in-tree libtpo.so (the C-ABI of include/tpo.h).
+
+Loading fails loudly: there is no CPU fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtpo.so")
+
+# exported symbols, as declared in include/tpo.h
+SYMBOLS = [
+    "tpo_abi_version", "tpo_last_error", "tpo_launch_count",
+    "tpo_propagate_ws", "tpo_propagate", "tpo_haar_q",
+    "tpo_features_ws", "tpo_features",
+    "tpo_affinity_matvec_ws", "tpo_affinity_matvec",
+    "tpo_topk_eig_ws", "tpo_topk_eig",
+    "tpo_cluster_ws", "tpo_cluster",
+    "tpo_run_ws", "tpo_run",
+]
+
+TPO_OK, TPO_EINVAL, TPO_ECUDA, TPO_ENOMEM, TPO_ENCCL, TPO_ENUMERIC = 0, -1, -2, -3, -4, -5
+TPO_EIG_EXACT, TPO_EIG_HALKO = 0, 1
+_NAMES = {-1: "TPO_EINVAL", -2: "TPO_ECUDA", -3: "TPO_ENOMEM", -4: "TPO_ENCCL", -5: "TPO_ENUMERIC"}
+
+
+class TpoError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class CSR(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("val", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtpo.so not built at {LIB_PATH}: run `python -m paper_2405_11922_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    i64, i32, sz, vp, f32, dbl = C.c_int64, C.c_int32, C.c_size_t, C.c_void_p, C.c_float, C.c_double
+    P = C.POINTER(CSR)
+    L.tpo_abi_version.restype = C.c_int
+    L.tpo_last_error.restype = C.c_char_p
+    L.tpo_launch_count.restype = C.c_uint64
+    L.tpo_propagate_ws.argtypes = [i64, i64, i64, i64]
+    L.tpo_propagate_ws.restype = sz
+    L.tpo_propagate.argtypes = [P, P, vp, i64, f32, i32, vp, vp, vp, sz, vp]
+    L.tpo_haar_q.argtypes = [vp, i64, vp]
+    L.tpo_features_ws.argtypes = [i64, i64]
+    L.tpo_features_ws.restype = sz
+    L.tpo_features.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, sz, vp]
+    L.tpo_affinity_matvec_ws.argtypes = [i64, i64, i64]
+    L.tpo_affinity_matvec_ws.restype = sz
+    L.tpo_affinity_matvec.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, sz, vp]
+    L.tpo_topk_eig_ws.argtypes = [i64, i64, i32, i32, i32]
+    L.tpo_topk_eig_ws.restype = sz
+    L.tpo_topk_eig.argtypes = [vp, vp, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.tpo_cluster_ws.argtypes = [i64, i64, i32]
+    L.tpo_cluster_ws.restype = sz
+    L.tpo_cluster.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.tpo_run_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32]
+    L.tpo_run_ws.restype = sz
+    L.tpo_run.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+    for name in ["tpo_propagate", "tpo_haar_q", "tpo_features", "tpo_affinity_matvec", "tpo_topk_eig",
+                 "tpo_cluster", "tpo_run"]:
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int):
+    if rc != TPO_OK:
+        raise TpoError(rc, lib().tpo_last_error().decode())

@@ -1,0 +1,261 @@
+// a8-a9: discretisation -- greedy orthogonal NMF (Alg. 2) and NCI
+// generation (Alg. 3), fp64 arithmetic (R11), deterministic reductions.
+//
+// Per ONMF iteration (H first, then Ups; brackets of PAPER.md:564):
+//   RtU = R'^T (dinv . Ups), UtU = Ups^T Ups             (split-over-rows fp64 products)
+//   H   <- H . max(RtU,0) / (H UtU + eps)                 (h_update_kernel)
+//   RH  = dinv . (R' H);  M = Ups^T RH                    (row-tiled product, split product)
+//   Ups <- Ups . sqrt(max(RH,0) / (max(Ups M,0) + eps))   (ups_update_kernel, warp per row)
+// Per NCI iteration (all on device, no host round trip; a device flag freezes the loop at
+// the label fix-point, R10):
+//   assign_kernel: l* = argmax_l Ups[i] . Phi[:,l] (ties -> smallest l), changed flag
+//   count + per-cluster row sums (fixed row ranges per block, fixed-order reduction)
+//   Phi[:,l] = sum_{i in C_l} Ups[i] / sqrt(|C_l|)
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+namespace {
+
+constexpr double EPS = 1e-12;   // R9
+
+__global__ void init_factors_kernel(const float *__restrict__ Gamma, int64_t n, const float *__restrict__ Psi,
+                                    const double *__restrict__ sig, int64_t D, int k, double *__restrict__ U,
+                                    double *__restrict__ H) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n * k) {
+        const double g = (double)Gamma[i];
+        U[i] = (g > 0.0 ? g : 0.0) + EPS;
+    }
+    if (i < D * k) {
+        const double h = (double)Psi[i] * sig[i % k];
+        H[i] = (h > 0.0 ? h : 0.0) + EPS;
+    }
+}
+
+// Hn[j,l] = H[j,l] * max(RtU[j,l],0) / ((H UtU)[j,l] + eps)
+__global__ void h_update_kernel(const double *__restrict__ H, const double *__restrict__ RtU,
+                                const double *__restrict__ UtU, int64_t D, int k, double *__restrict__ Hn) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= D * k) return;
+    const int64_t j = i / k;
+    const int l = (int)(i - j * k);
+    double s = 0.0;
+    for (int a = 0; a < k; ++a) s = __dadd_rn(s, __dmul_rn(H[j * k + a], UtU[(int64_t)a * k + l]));
+    const double num = RtU[i] > 0.0 ? RtU[i] : 0.0;
+    Hn[i] = __dmul_rn(H[i], num) / __dadd_rn(s, EPS);
+}
+
+// Ups[i,l] *= sqrt(max(RH[i,l],0) / (max((Ups M)[i,l],0) + eps)); warp per row, the old row
+// staged in shared memory (k <= 128).
+__global__ void __launch_bounds__(256) ups_update_kernel(double *__restrict__ U, const double *__restrict__ RH,
+                                                         const double *__restrict__ M, int64_t n, int k) {
+    __shared__ double rowbuf[8][128];
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (row >= n) return;
+    double *u = U + row * k;
+    double *ub = rowbuf[w];
+    for (int l = lane; l < k; l += 32) ub[l] = u[l];
+    __syncwarp();
+    for (int l = lane; l < k; l += 32) {
+        double s = 0.0;
+        for (int a = 0; a < k; ++a) s = __dadd_rn(s, __dmul_rn(ub[a], M[(int64_t)a * k + l]));
+        const double r = RH[row * k + l];
+        const double num = r > 0.0 ? r : 0.0;
+        const double den = __dadd_rn(s > 0.0 ? s : 0.0, EPS);
+        u[l] = __dmul_rn(ub[l], sqrt(num / den));
+    }
+}
+
+struct NciState {
+    int32_t *changed;     // [0]: labels changed in the current iteration
+    int32_t *done;        // [0]: fix-point reached (freezes the remaining iterations)
+    int32_t *iters;       // [0]: iterations run
+};
+
+// l* = argmax_l sum_a Ups[i,a] Phi[a,l]; warp per row, Phi and the row in smem.
+__global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
+                                                     int64_t n, int k, int32_t *__restrict__ labels, NciState s) {
+    if (*s.done) return;
+    extern __shared__ double phs[];
+    __shared__ double rowbuf[8][128];
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) phs[i] = Phi[i];
+    __syncthreads();
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (row >= n) return;
+    double *ub = rowbuf[w];
+    for (int l = lane; l < k; l += 32) ub[l] = U[row * k + l];
+    __syncwarp();
+    double best = 0.0;
+    int arg = 0x7fffffff;
+    for (int l = lane; l < k; l += 32) {
+        double sc = 0.0;
+        for (int a = 0; a < k; ++a) sc = __dadd_rn(sc, __dmul_rn(ub[a], phs[a * k + l]));
+        if (arg == 0x7fffffff || sc > best) { best = sc; arg = l; }
+    }
+    // warp argmax: larger score wins; equal scores -> smaller index
+    for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (oa != 0x7fffffff && (arg == 0x7fffffff || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
+    }
+    if (lane == 0) {
+        if (labels[row] != arg) *s.changed = 1;
+        labels[row] = arg;
+    }
+}
+
+__global__ void nci_step_kernel(NciState s, int32_t *__restrict__ counts, int k) {
+    // runs after assign: advance the iteration counter, freeze on a fix-point
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        if (!*s.done) {
+            *s.iters += 1;
+            if (!*s.changed) *s.done = 1;
+            *s.changed = 0;
+        }
+    }
+    (void)counts; (void)k;
+}
+
+// per-block cluster sums over a fixed row range: part[b][l][a] = sum_{i in range, label l} U[i,a]
+// and per-block counts cpart[b][l].  Thread a (lanes over columns) walks the rows in order.
+__global__ void cluster_sums_kernel(const double *__restrict__ U, const int32_t *__restrict__ labels, int64_t n,
+                                    int k, int64_t rows_per_block, double *__restrict__ part,
+                                    int64_t *__restrict__ cpart, const int32_t *__restrict__ done) {
+    if (*done) return;
+    extern __shared__ double acc[];          // [k][k]
+    int64_t *cnt = reinterpret_cast<int64_t *>(acc + (size_t)k * k);
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) acc[i] = 0.0;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
+    const int a = threadIdx.x;
+    if (a < k) {
+        for (int64_t i = r0; i < r1; ++i) {
+            const int l = labels[i];
+            acc[(int64_t)l * k + a] += U[i * k + a];
+            if (a == 0) cnt[l] += 1;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) part[blockIdx.x * (int64_t)k * k + i] = acc[i];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) cpart[blockIdx.x * (int64_t)k + i] = cnt[i];
+}
+
+// Phi[a,l] = (sum_b part[b][l][a]) / sqrt(count_l)   (zero column for an empty cluster)
+__global__ void phi_kernel(const double *__restrict__ part, const int64_t *__restrict__ cpart, int64_t nb, int k,
+                           double *__restrict__ Phi, const int32_t *__restrict__ done) {
+    if (*done) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k * k) return;
+    const int l = i / k, a = i - l * k;
+    double s = 0.0;
+    int64_t c = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        s += part[b * (int64_t)k * k + (int64_t)l * k + a];
+        c += cpart[b * (int64_t)k + l];
+    }
+    Phi[(int64_t)a * k + l] = c > 0 ? s / sqrt((double)c) : 0.0;
+}
+
+__global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void eye_kernel(double *P, int k) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k * k) P[i] = (i / k == i % k) ? 1.0 : 0.0;
+}
+
+int64_t cluster_rows_per_block(int64_t n) { return std::max<int64_t>(64, cdiv(std::max<int64_t>(n, 1), 4 * 148)); }
+
+}  // namespace
+
+size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
+    Arena ar(nullptr, 0);
+    ar.take<double>(n * k);          // Ups
+    ar.take<double>(n * k);          // RH
+    ar.take<double>(D * k * 2);      // H, Hn
+    ar.take<double>(D * k);          // RtU
+    ar.take<double>(k * k * 3);      // UtU, M, Phi
+    ar.take<double>(k);
+    ar.take<int32_t>(8);
+    const int64_t nb = cdiv(std::max<int64_t>(n, 1), cluster_rows_per_block(n));
+    ar.take<double>(nb * k * k);
+    ar.take<int64_t>(nb * k);
+    return ar.off + std::max(tsgemm_ws(n, D, k), tsgemm_ws(n, k, k)) + 4096;
+}
+
+void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
+                  const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
+                  int32_t *iters_used, Arena &ar, cudaStream_t st) {
+    double *U = ar.take<double>(n * k);
+    double *RH = ar.take<double>(n * k);
+    double *H = ar.take<double>(D * k), *Hn = ar.take<double>(D * k);
+    double *RtU = ar.take<double>(D * k);
+    double *UtU = ar.take<double>(k * k), *M = ar.take<double>(k * k), *Phi = ar.take<double>(k * k);
+    double *sig = ar.take<double>(k);
+    int32_t *flags = ar.take<int32_t>(8);
+    const int64_t rpb = cluster_rows_per_block(n);
+    const int64_t nb = cdiv(std::max<int64_t>(n, 1), rpb);
+    double *part = ar.take<double>(nb * k * k);
+    int64_t *cpart = ar.take<int64_t>(nb * k);
+    const size_t mark = ar.off;
+
+    TPO_CUDA(cudaMemcpyAsync(sig, sigma, sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    const int64_t mx = std::max(n, D) * k;
+    init_factors_kernel<<<cdiv(mx, 256), 256, 0, st>>>(Gamma, n, Psi, sig, D, k, U, H);
+    TPO_LAUNCH_CHECK();
+    for (int t = 0; t < Tf; ++t) {
+        tsgemm_AtB_f32f64(Rp, D, dinv, U, k, n, D, k, RtU, ar, st);
+        ar.off = mark;
+        tsgemm_AtB_f64f64(U, k, U, k, n, k, k, UtU, ar, st);
+        ar.off = mark;
+        h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
+        TPO_LAUNCH_CHECK();
+        std::swap(H, Hn);
+        tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
+        tsgemm_AtB_f64f64(U, k, RH, k, n, k, k, M, ar, st);
+        ar.off = mark;
+        ups_update_kernel<<<cdiv(n * 32, 256), 256, 0, st>>>(U, RH, M, n, k);
+        TPO_LAUNCH_CHECK();
+    }
+    // Alg. 3
+    NciState s{flags, flags + 1, flags + 2};
+    TPO_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 8, st));
+    fill_i32<<<cdiv(n, 256), 256, 0, st>>>(labels, n, -1);
+    TPO_LAUNCH_CHECK();
+    eye_kernel<<<cdiv(k * k, 256), 256, 0, st>>>(Phi, k);
+    TPO_LAUNCH_CHECK();
+    const size_t phi_smem = sizeof(double) * k * k;
+    const size_t sum_smem = sizeof(double) * k * k + sizeof(int64_t) * k;
+    if (phi_smem > 48 * 1024)
+        TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));
+    if (sum_smem > 48 * 1024)
+        TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
+    const int sum_threads = (int)std::max<int64_t>(32, cdiv(k, 32) * 32);
+    for (int t = 0; t < Tg; ++t) {
+        assign_kernel<<<cdiv(n * 32, 256), 256, phi_smem, st>>>(U, Phi, n, k, labels, s);
+        TPO_LAUNCH_CHECK();
+        nci_step_kernel<<<1, 32, 0, st>>>(s, nullptr, k);
+        TPO_LAUNCH_CHECK();
+        if (t == Tg - 1) break;                       // the last Phi update is never used
+        cluster_sums_kernel<<<nb, sum_threads, sum_smem, st>>>(U, labels, n, k, rpb, part, cpart, s.done);
+        TPO_LAUNCH_CHECK();
+        phi_kernel<<<cdiv(k * k, 256), 256, 0, st>>>(part, cpart, nb, k, Phi, s.done);
+        TPO_LAUNCH_CHECK();
+    }
+    int32_t it = 0;
+    TPO_CUDA(cudaMemcpyAsync(&it, s.iters, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    if (iters_used) *iters_used = it;
+}
+
+}  // namespace tpo

@@ -1,0 +1,321 @@
+// a6-a7: implicit affinity product and the top-k singular triplets of R = diag(dinv) R'
+// ("the top-k left and right singular vectors of R", Eq. init-HY).
+//
+// EXACT mode (R7): Gram G = R^T R (D x D, fp64 sums) once, then block subspace iteration
+// with Rayleigh-Ritz on G (the D x D image of the implicit n x n affinity S~ = R R^T:
+// both share their nonzero spectrum) until the top-k Ritz residuals fall below 1e-9 lambda_1;
+// with a full-rank block (b = D) this is one Rayleigh-Ritz step, i.e. a dense eigensolve.
+// Then Gamma = R Psi Sigma^{-1} and a CholeskyQR2 polish if ||Gamma^T Gamma - I||_max > 1e-6.
+// HALKO mode: the randomised truncated SVD the paper cites, q power steps.
+// Both modes end with the sign rule R8.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+
+void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int64_t p, int64_t q, double *out,
+                  int64_t ldo, cudaStream_t st);
+
+namespace {
+
+// Column statistics of an n x k fp32 matrix: sum (fp64), sum |x| (fp64), argmax |x| (first
+// index).  One block per column, fixed-order tree reduction.
+__global__ void colstats_kernel(const float *__restrict__ A, int64_t n, int k, double *__restrict__ out_sum,
+                                double *__restrict__ out_abs, int64_t *__restrict__ out_arg) {
+    __shared__ double ss[256], sa[256], sm[256];
+    __shared__ int64_t si[256];
+    const int c = blockIdx.x, t = threadIdx.x;
+    double s = 0.0, a = 0.0, best = -1.0;
+    int64_t bi = 0;
+    for (int64_t i = t; i < n; i += 256) {
+        const double v = (double)A[i * k + c];
+        s += v;
+        a += fabs(v);
+        if (fabs(v) > best) { best = fabs(v); bi = i; }
+    }
+    ss[t] = s; sa[t] = a; sm[t] = best; si[t] = bi;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (t < o) {
+            ss[t] += ss[t + o];
+            sa[t] += sa[t + o];
+            if (sm[t + o] > sm[t] || (sm[t + o] == sm[t] && si[t + o] < si[t])) { sm[t] = sm[t + o]; si[t] = si[t + o]; }
+        }
+        __syncthreads();
+    }
+    if (t == 0) { out_sum[c] = ss[0]; out_abs[c] = sa[0]; out_arg[c] = si[0]; }
+}
+
+__global__ void flip_cols_f32(float *__restrict__ A, int64_t n, int k, const int *__restrict__ sgn) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * k) return;
+    if (sgn[i % k] < 0) A[i] = -A[i];
+}
+
+__global__ void cast_f64_f32(const double *__restrict__ a, int64_t len, float *__restrict__ b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < len) b[i] = (float)a[i];
+}
+
+template <class T>
+T *to_dev(Arena &ar, const std::vector<T> &h, cudaStream_t st) {
+    T *d = ar.take<T>(h.size());
+    TPO_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+template <class T>
+std::vector<T> to_host(const T *d, size_t len, cudaStream_t st) {
+    std::vector<T> h(len);
+    TPO_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(T) * len, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+
+// splitmix64 -> uniform in [-1, 1): the deterministic start block of the subspace iteration
+double start_entry(uint64_t i) {
+    uint64_t z = i + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// CholeskyQR2 of a device fp64 matrix V (rows x b) in place (tmp: rows x b).
+void cholqr2_f64(double *V, double *tmp, int64_t rows, int64_t b, Arena &ar, cudaStream_t st) {
+    for (int pass = 0; pass < 2; ++pass) {
+        const size_t mark = ar.off;
+        double *g = ar.take<double>(b * b);
+        tsgemm_AtB_f64f64(V, b, V, b, rows, b, b, g, ar, st);
+        std::vector<double> gh = to_host(g, b * b, st), C(b * b), Ci(b * b);
+        if (!host_cholesky_upper(b, gh.data(), C.data()))
+            throw Error(TPO_ENUMERIC, "CholeskyQR2: Gram matrix not positive definite");
+        host_upper_inverse(b, C.data(), Ci.data());
+        double *ci = to_dev(ar, Ci, st);
+        tsgemm_AW_dd(V, b, ci, rows, b, b, tmp, b, st);
+        TPO_CUDA(cudaMemcpyAsync(V, tmp, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        ar.off = mark;
+    }
+}
+
+// Top-k eigenpairs of the symmetric D x D device matrix G: lam (host, k), Psi64 (device D x k).
+void gram_topk(const double *G, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64, Arena &ar,
+               cudaStream_t st) {
+    const int64_t b = std::min<int64_t>(D, k + std::max<int64_t>(k, 16));
+    if (b >= D) {       // full-rank block: a single Rayleigh-Ritz step = dense eigensolve
+        std::vector<double> gh = to_host(G, D * D, st), w(D), V(D * k);
+        host_sym_eig_top(D, gh.data(), k, w.data(), V.data());
+        lam.assign(w.begin(), w.begin() + k);
+        TPO_CUDA(cudaMemcpyAsync(Psi64, V.data(), sizeof(double) * D * k, cudaMemcpyHostToDevice, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    std::vector<double> v0(D * b);
+    for (int64_t i = 0; i < D * b; ++i) v0[i] = start_entry((uint64_t)i);
+    double *V = to_dev(ar, v0, st);
+    double *W = ar.take<double>(D * b);
+    double *T = ar.take<double>(D * b);
+    cholqr2_f64(V, T, D, b, ar, st);
+    const int max_it = 5000, rr_every = 4;
+    double lam1 = 0.0;
+    std::vector<double> H, WtW, E(b * b), w(b);
+    for (int it = 0; it < max_it; ++it) {
+        tsgemm_AW_dd(G, D, V, D, D, b, W, b, st);                 // W = G V
+        const bool rr = (it % rr_every) == rr_every - 1 || it == max_it - 1;
+        if (!rr) {
+            TPO_CUDA(cudaMemcpyAsync(V, W, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
+            cholqr2_f64(V, T, D, b, ar, st);
+            continue;
+        }
+        const size_t mark = ar.off;
+        double *h = ar.take<double>(b * b), *ww = ar.take<double>(b * b);
+        tsgemm_AtB_f64f64(V, b, W, b, D, b, b, h, ar, st);       // H = V^T G V
+        tsgemm_AtB_f64f64(W, b, W, b, D, b, b, ww, ar, st);      // W^T W
+        H = to_host(h, b * b, st);
+        WtW = to_host(ww, b * b, st);
+        host_sym_eig_top(b, H.data(), b, w.data(), E.data());
+        lam1 = std::max(lam1, fabs(w[0]));
+        double rmax = 0.0;
+        for (int l = 0; l < k; ++l) {          // ||G v_l - lam_l v_l||^2 = e^T W^T W e - lam^2
+            double s = 0.0;
+            for (int64_t a = 0; a < b; ++a) {
+                double t = 0.0;
+                for (int64_t c = 0; c < b; ++c) t += WtW[a * b + c] * E[c * b + l];
+                s += E[a * b + l] * t;
+            }
+            rmax = std::max(rmax, sqrt(std::max(s - w[l] * w[l], 0.0)));
+        }
+        double *e = to_dev(ar, E, st);
+        if (rmax <= 1e-9 * lam1 || it == max_it - 1) {
+            std::vector<double> Ek(b * k);
+            for (int64_t a = 0; a < b; ++a)
+                for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * b + l];
+            double *ek = to_dev(ar, Ek, st);
+            tsgemm_AW_dd(V, b, ek, D, b, k, Psi64, k, st);           // Ritz vectors
+            lam.assign(w.begin(), w.begin() + k);
+            TPO_CUDA(cudaStreamSynchronize(st));
+            ar.off = mark;
+            return;
+        }
+        tsgemm_AW_dd(W, b, e, D, b, b, V, b, st);                    // V <- G V E (Ritz-rotated)
+        cholqr2_f64(V, T, D, b, ar, st);
+        ar.off = mark;
+    }
+}
+
+// Sign rule R8 on (Gamma, Psi): sum_i Gamma[i,l] >= 0, else (near-zero sums) the sign of the
+// largest-magnitude entry.  Flips are applied to both factors.
+void apply_sign_rule(float *Gamma, int64_t n, int k, float *Psi, int64_t D, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    double *s = ar.take<double>(k), *a = ar.take<double>(k);
+    int64_t *arg = ar.take<int64_t>(k);
+    colstats_kernel<<<k, 256, 0, st>>>(Gamma, n, k, s, a, arg);
+    TPO_LAUNCH_CHECK();
+    std::vector<double> hs = to_host(s, k, st), ha = to_host(a, k, st);
+    std::vector<int64_t> harg = to_host(arg, k, st);
+    std::vector<int> sg(k, 1);
+    bool any = false;
+    for (int l = 0; l < k; ++l) {
+        if (fabs(hs[l]) < 1e-6 * ha[l]) {
+            float v;
+            TPO_CUDA(cudaMemcpy(&v, Gamma + harg[l] * k + l, sizeof(float), cudaMemcpyDeviceToHost));
+            sg[l] = v < 0.f ? -1 : 1;
+        } else {
+            sg[l] = hs[l] < 0.0 ? -1 : 1;
+        }
+        any |= sg[l] < 0;
+    }
+    if (any) {
+        int *dsg = to_dev(ar, sg, st);
+        flip_cols_f32<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
+        TPO_LAUNCH_CHECK();
+        flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
+        TPO_LAUNCH_CHECK();
+        TPO_CUDA(cudaStreamSynchronize(st));
+    }
+    ar.off = mark;
+}
+
+// CholeskyQR2 polish of the fp32 n x k Gamma when its Gram is off identity by > 1e-6.
+void polish_gamma(float *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    double *g = ar.take<double>((size_t)k * k);
+    float *tmp = nullptr;
+    for (int pass = 0; pass < 3; ++pass) {
+        tsgemm_AtB_f32f32(Gamma, k, nullptr, Gamma, k, nullptr, n, k, k, g, ar, st);
+        std::vector<double> gh = to_host(g, (size_t)k * k, st);
+        double dev = 0.0;
+        for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b) dev = std::max(dev, fabs(gh[a * k + b] - (a == b ? 1.0 : 0.0)));
+        if (dev <= 1e-6 || pass == 2) break;
+        std::vector<double> C((size_t)k * k), Ci((size_t)k * k);
+        if (!host_cholesky_upper(k, gh.data(), C.data()))
+            throw Error(TPO_ENUMERIC, "CholeskyQR2 polish: Gamma^T Gamma not positive definite");
+        host_upper_inverse(k, C.data(), Ci.data());
+        double *ci = to_dev(ar, Ci, st);
+        if (!tmp) tmp = ar.take<float>((size_t)n * k);
+        tsgemm_AW_f32(Gamma, k, nullptr, ci, n, k, k, tmp, k, st);
+        TPO_CUDA(cudaMemcpyAsync(Gamma, tmp, sizeof(float) * n * k, cudaMemcpyDeviceToDevice, st));
+    }
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
+// Gamma = diag(rs) A Psi64 diag(1/sigma), Psi (fp32 out) = Psi64.
+void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
+                    const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st) {
+    std::vector<double> ph = to_host(Psi64, (size_t)D * k, st);
+    for (int64_t j = 0; j < D; ++j)
+        for (int l = 0; l < k; ++l) ph[j * k + l] /= sig[l];
+    double *w = to_dev(ar, ph, st);
+    tsgemm_AW_f32(Rp, D, dinv, w, n, D, k, Gamma, k, st);
+    cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
+    TPO_LAUNCH_CHECK();
+    polish_gamma(Gamma, n, k, ar, st);
+    apply_sign_rule(Gamma, n, k, Psi, D, ar, st);
+}
+
+}  // namespace
+
+size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p) {
+    const int64_t b = std::min<int64_t>(D, k + std::max<int64_t>(k, 16));
+    const int64_t bh = k + p;
+    size_t s = 0;
+    s += align_up(sizeof(double) * D * D) + gram_ws(n, D);
+    s += 3 * align_up(sizeof(double) * D * std::max(b, bh)) + 8 * align_up(sizeof(double) * b * b + 8);
+    s += 2 * align_up(sizeof(double) * D * k) + tsgemm_ws(n, k, k) + align_up(sizeof(float) * n * k);
+    if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
+    return s + 64 * 256;
+}
+
+void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p,
+                   int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi, Arena &ar,
+                   cudaStream_t st) {
+    std::vector<double> lam;
+    double *Psi64 = ar.take<double>(D * k);
+    if (mode == TPO_EIG_EXACT) {
+        double *G = ar.take<double>(D * D);
+        const size_t mark = ar.off;
+        gram_weighted(Rp, dinv, n, D, G, ar, st);
+        ar.off = mark;
+        gram_topk(G, D, k, lam, Psi64, ar, st);
+    } else {
+        // Halko randomised SVD: Y = orth(R Omega); q x Y = orth(R (R^T Y)); B = R^T Y;
+        // Rayleigh-Ritz through the eigendecomposition of B^T B = Y^T R R^T Y.
+        const int64_t b = k + p;
+        std::vector<float> om = to_host(Omega, D * b, st);
+        std::vector<double> omd(om.begin(), om.end());
+        double *Om = to_dev(ar, omd, st);
+        double *Y = ar.take<double>(n * b), *T = ar.take<double>(n * b), *Bm = ar.take<double>(D * b);
+        tsgemm_AW_f64(Rp, D, dinv, Om, n, D, b, Y, b, st);
+        cholqr2_f64(Y, T, n, b, ar, st);
+        for (int it = 0; it < q; ++it) {
+            const size_t mark = ar.off;
+            tsgemm_AtB_f32f64(Rp, D, dinv, Y, b, n, D, b, Bm, ar, st);
+            ar.off = mark;
+            tsgemm_AW_f64(Rp, D, dinv, Bm, n, D, b, Y, b, st);
+            cholqr2_f64(Y, T, n, b, ar, st);
+        }
+        const size_t mark = ar.off;
+        tsgemm_AtB_f32f64(Rp, D, dinv, Y, b, n, D, b, Bm, ar, st);     // B = R^T Y (D x b)
+        double *g = ar.take<double>(b * b);
+        tsgemm_AtB_f64f64(Bm, b, Bm, b, D, b, b, g, ar, st);           // B^T B (b x b)
+        std::vector<double> gh = to_host(g, b * b, st), w(b), E(b * b);
+        host_sym_eig_top(b, gh.data(), b, w.data(), E.data());
+        lam.assign(w.begin(), w.begin() + k);
+        std::vector<double> Ek(b * k);
+        for (int64_t a = 0; a < b; ++a)
+            for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * b + l];
+        double *ek = to_dev(ar, Ek, st);
+        // Psi = B E_k Sigma^{-1} (right singular vectors); Gamma follows from Psi below.
+        tsgemm_AW_dd(Bm, b, ek, D, b, k, Psi64, k, st);
+        std::vector<double> ps = to_host(Psi64, D * k, st);
+        for (int64_t j = 0; j < D; ++j)
+            for (int l = 0; l < k; ++l) ps[j * k + l] /= sqrt(std::max(w[l], 1e-300));
+        TPO_CUDA(cudaMemcpyAsync(Psi64, ps.data(), sizeof(double) * D * k, cudaMemcpyHostToDevice, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        ar.off = mark;
+    }
+    std::vector<double> sig(k);
+    for (int l = 0; l < k; ++l) {
+        sig[l] = sqrt(std::max(lam[l], 0.0));
+        if (!(sig[l] > 0.0)) throw Error(TPO_ENUMERIC, "top-k: sigma_k is zero (rank(R) < k)");
+        sigma[l] = sig[l];
+    }
+    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st);
+}
+
+// a6: out = dinv . R' (R'^T (dinv . Y)), the D x b intermediate summed in fp64.
+void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b,
+                          float *out, Arena &ar, cudaStream_t st) {
+    double *W = ar.take<double>(D * b);
+    tsgemm_AtB_f32f32(Rp, D, dinv, Y, b, nullptr, n, D, b, W, ar, st);
+    tsgemm_AW_f32(Rp, D, dinv, W, n, D, b, out, b, st);
+}
+
+}  // namespace tpo

@@ -1,0 +1,212 @@
+// Host fp64 small dense linear algebra of libtpo (d x d, b x b, k x k matrices only).
+//   * QR by classical Gram-Schmidt with one re-orthogonalisation pass (CGS2): R has a
+//     positive diagonal by construction, which is the sign convention of the Haar
+//     rotation (Alg. 1 L7; unique QR with diag(R) > 0).
+//   * Symmetric eigensolver: Householder tridiagonalisation + implicit-shift QL with
+//     eigenvector accumulation (EISPACK tred2/tql2 scheme), used for the Rayleigh-Ritz
+//     matrices of the subspace iteration (b x b) and for D x D when b = D.
+//   * Cholesky (upper) and triangular inverse for CholeskyQR2.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+
+void host_qr_positive(int64_t rows, int64_t cols, const double *A, double *Q, double *R) {
+    // Q (rows x cols) row-major; columns built one by one.
+    std::vector<double> q((size_t)rows * cols, 0.0), r((size_t)cols * cols, 0.0), v(rows);
+    for (int64_t j = 0; j < cols; ++j) {
+        for (int64_t i = 0; i < rows; ++i) v[i] = A[i * cols + j];
+        for (int pass = 0; pass < 2; ++pass) {
+            std::vector<double> c(j, 0.0);
+            for (int64_t p = 0; p < j; ++p) {
+                double s = 0.0;
+                for (int64_t i = 0; i < rows; ++i) s += q[i * cols + p] * v[i];
+                c[p] = s;
+            }
+            for (int64_t p = 0; p < j; ++p) {
+                for (int64_t i = 0; i < rows; ++i) v[i] -= c[p] * q[i * cols + p];
+                r[p * cols + j] += c[p];
+            }
+        }
+        double nr = 0.0;
+        for (int64_t i = 0; i < rows; ++i) nr += v[i] * v[i];
+        nr = sqrt(nr);
+        if (!(nr > 0.0)) throw Error(TPO_ENUMERIC, "QR: rank-deficient input");
+        r[j * cols + j] = nr;
+        for (int64_t i = 0; i < rows; ++i) q[i * cols + j] = v[i] / nr;
+    }
+    memcpy(Q, q.data(), sizeof(double) * q.size());
+    if (R) memcpy(R, r.data(), sizeof(double) * r.size());
+}
+
+namespace {
+
+// Householder reduction of symmetric a (n x n, row-major, overwritten by the orthogonal
+// transform Z with Z^T A Z = tridiag(d, e)); e[i] couples i-1 and i, e[0] = 0.
+void tridiagonalise(int n, std::vector<double> &a, std::vector<double> &d, std::vector<double> &e) {
+    auto A = [&](int i, int j) -> double & { return a[(size_t)i * n + j]; };
+    for (int i = n - 1; i > 0; --i) {
+        const int l = i - 1;
+        double h = 0.0, scale = 0.0;
+        if (l > 0) {
+            for (int k = 0; k <= l; ++k) scale += fabs(A(i, k));
+            if (scale == 0.0) {
+                e[i] = A(i, l);
+            } else {
+                for (int k = 0; k <= l; ++k) {
+                    A(i, k) /= scale;
+                    h += A(i, k) * A(i, k);
+                }
+                double f = A(i, l);
+                double g = (f >= 0.0) ? -sqrt(h) : sqrt(h);
+                e[i] = scale * g;
+                h -= f * g;
+                A(i, l) = f - g;
+                f = 0.0;
+                for (int j = 0; j <= l; ++j) {
+                    A(j, i) = A(i, j) / h;
+                    g = 0.0;
+                    for (int k = 0; k <= j; ++k) g += A(j, k) * A(i, k);
+                    for (int k = j + 1; k <= l; ++k) g += A(k, j) * A(i, k);
+                    e[j] = g / h;
+                    f += e[j] * A(i, j);
+                }
+                const double hh = f / (h + h);
+                for (int j = 0; j <= l; ++j) {
+                    f = A(i, j);
+                    e[j] = g = e[j] - hh * f;
+                    for (int k = 0; k <= j; ++k) A(j, k) -= (f * e[k] + g * A(i, k));
+                }
+            }
+        } else {
+            e[i] = A(i, l);
+        }
+        d[i] = h;
+    }
+    d[0] = 0.0;
+    e[0] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const int l = i - 1;
+        if (d[i] != 0.0) {
+            for (int j = 0; j <= l; ++j) {
+                double g = 0.0;
+                for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
+                for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
+            }
+        }
+        d[i] = A(i, i);
+        A(i, i) = 1.0;
+        for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
+    }
+}
+
+// Implicit-shift QL on the tridiagonal (d, e), accumulating rotations into z (n x n).
+void tridiag_ql(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> &z) {
+    for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+    e[n - 1] = 0.0;
+    for (int l = 0; l < n; ++l) {
+        int iter = 0, m;
+        do {
+            for (m = l; m < n - 1; ++m) {
+                const double dd = fabs(d[m]) + fabs(d[m + 1]);
+                if (fabs(e[m]) <= 1e-300 || fabs(e[m]) + dd == dd) break;
+            }
+            if (m != l) {
+                if (iter++ == 200) throw Error(TPO_ENUMERIC, "tridiagonal QL did not converge");
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? fabs(r) : -fabs(r)));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int i;
+                for (i = m - 1; i >= l; --i) {
+                    double f = s * e[i];
+                    const double b = c * e[i];
+                    e[i + 1] = (r = hypot(f, g));
+                    if (r == 0.0) {
+                        d[i + 1] -= p;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    s = f / r;
+                    c = g / r;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    d[i + 1] = g + (p = s * r);
+                    g = c * r - b;
+                    for (int k = 0; k < n; ++k) {
+                        f = z[(size_t)k * n + i + 1];
+                        z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * f;
+                        z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * f;
+                    }
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= p;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
+    }
+}
+
+}  // namespace
+
+void host_sym_eig_top(int64_t D, const double *Ain, int64_t nvec, double *w, double *V) {
+    const int n = (int)D;
+    std::vector<double> a(Ain, Ain + (size_t)n * n), d(n), e(n);
+    // symmetrise defensively (inputs are symmetric up to rounding of the reduction)
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < i; ++j) {
+            const double s = 0.5 * (a[(size_t)i * n + j] + a[(size_t)j * n + i]);
+            a[(size_t)i * n + j] = a[(size_t)j * n + i] = s;
+        }
+    if (n == 1) {
+        w[0] = a[0];
+        if (nvec > 0) V[0] = 1.0;
+        return;
+    }
+    tridiagonalise(n, a, d, e);
+    tridiag_ql(n, d, e, a);
+    std::vector<int> ord(n);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return d[x] > d[y]; });
+    for (int i = 0; i < n; ++i) w[i] = d[ord[i]];
+    for (int64_t c = 0; c < nvec; ++c)
+        for (int r = 0; r < n; ++r) V[(size_t)r * nvec + c] = a[(size_t)r * n + ord[c]];
+}
+
+bool host_cholesky_upper(int64_t k, const double *A, double *C) {
+    for (int64_t i = 0; i < k * k; ++i) C[i] = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+        double s = A[j * k + j];
+        for (int64_t p = 0; p < j; ++p) s -= C[p * k + j] * C[p * k + j];
+        if (!(s > 0.0) || !std::isfinite(s)) return false;
+        const double cjj = sqrt(s);
+        C[j * k + j] = cjj;
+        for (int64_t i = j + 1; i < k; ++i) {
+            double t = A[j * k + i];
+            for (int64_t p = 0; p < j; ++p) t -= C[p * k + j] * C[p * k + i];
+            C[j * k + i] = t / cjj;
+        }
+    }
+    return true;
+}
+
+void host_upper_inverse(int64_t k, const double *C, double *Ci) {
+    for (int64_t i = 0; i < k * k; ++i) Ci[i] = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+        Ci[j * k + j] = 1.0 / C[j * k + j];
+        for (int64_t i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t p = i + 1; p <= j; ++p) s += C[i * k + p] * Ci[p * k + j];
+            Ci[i * k + j] = -s / C[i * k + i];
+        }
+    }
+}
+
+}  // namespace tpo

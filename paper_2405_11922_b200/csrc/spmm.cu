@@ -1,0 +1,452 @@
+// a1-a3: MSA propagation (Lemma 1 / Eq. PX; hop update Eq. update-Z,
+// PAPER.md:454, bracketed L (L^T Z) as PAPER.md:456) on sm_100a.
+//
+// Data layout and fusion:
+//   * The iterate is kept pre-scaled, P = s_u . Z (s_u = D_U^{-1/2}), in the caller's Z
+//     buffer, so that neither SpMM gathers a per-edge scale:
+//        SpMM-1 (rows of B^T, V side):   Q[v] = s_v[v]^2 * sum_{u in N(v)} w_uv P[u]
+//        SpMM-2 (rows of B,   U side):   Z[u] = c X[u] + alpha s_u[u] sum_{v in N(u)} w_uv Q[v]
+//                                         P[u] = s_u[u] Z[u]      (hops 1..T-1)
+//     which is Z <- c X + alpha L (L^T Z) with L = D_U^{-1/2} B D_V^{-1/2} (Eq. L).
+//     The last hop writes Z and fuses the row L2 normalisation (Eq. Z) when d <= 128.
+//   * One warp gathers one 128-float column slice of a CSR row with 128-bit loads
+//     (lane l owns float4 column l of the slice); 8 neighbour rows are in flight per warp.
+//   * Power-law rows are split into chunks of CHUNK edges.  Rows with <= CHUNK edges are
+//     one work item finished in place; longer rows write per-chunk partial sums that a
+//     fix-up kernel adds in chunk order (deterministic: no float atomics anywhere).
+#include "tpo_internal.cuh"
+
+namespace tpo {
+namespace {
+
+constexpr int CHUNK = 512;           // edges per work item of a long row
+constexpr int WPB = 8;               // warps per block
+constexpr int UNR = 8;               // neighbour rows in flight per warp
+
+enum Epi { EPI_V = 0, EPI_U = 1, EPI_FINAL = 2 };
+
+struct Sched {
+    int64_t *offsets;      // [n_rows+1] packed exclusive scan: (items << 32) | slots
+    int4 *items;           // {row, chunk, slot or -1, nchunks}
+    int4 *slots;           // {row, chunk, nchunks, first slot}
+    int64_t max_items, max_slots;
+};
+
+__device__ __forceinline__ int64_t packed_total(const int64_t *offsets, int64_t n) { return offsets[n]; }
+
+// ---------------------------------------------------------------------------------------
+// degrees -> scales (a1).  s = 1/sqrt(sum of weights), 1/sqrt(0) := 0 (R3).
+// ---------------------------------------------------------------------------------------
+__global__ void degree_scale_kernel(const int64_t *__restrict__ rowptr, const float *__restrict__ val,
+                                    int64_t n, float *__restrict__ s) {
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const int64_t b = rowptr[row], e = rowptr[row + 1];
+    double deg;
+    if (val == nullptr) {
+        deg = (double)(e - b);
+    } else {
+        double acc = 0.0;
+        for (int64_t i = b + lane; i < e; i += 32) acc += (double)val[i];
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        deg = acc;
+    }
+    if (lane == 0) s[row] = deg > 0.0 ? (float)(1.0 / sqrt(deg)) : 0.0f;
+}
+
+// ---------------------------------------------------------------------------------------
+// Work schedule: items per row, packed exclusive scan, fill.
+// ---------------------------------------------------------------------------------------
+__global__ void sched_count_kernel(const int64_t *__restrict__ rowptr, int64_t n, int64_t *__restrict__ cnt) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t len = rowptr[r + 1] - rowptr[r];
+    const int64_t nch = len <= CHUNK ? 1 : (len + CHUNK - 1) / CHUNK;
+    const int64_t sl = len <= CHUNK ? 0 : nch;
+    cnt[r] = (nch << 32) | sl;
+}
+
+constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_TILE = SCAN_T * SCAN_I;
+
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t *sh, int64_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        sh[lane + 32] = w;   // inclusive warp totals
+    }
+    __syncthreads();
+    const int64_t before = (wid ? sh[32 + wid - 1] : 0) + x - v;
+    total = sh[32 + (blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void scan_tile_sums(const int64_t *__restrict__ in, int64_t n, int64_t *__restrict__ sums) {
+    __shared__ int64_t sh[64];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_I;
+    int64_t s = 0;
+    for (int i = 0; i < SCAN_I; ++i) s += (base + i < n) ? in[base + i] : 0;
+    int64_t tot;
+    block_exclusive_scan(s, sh, tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void scan_sums_single(int64_t *__restrict__ sums, int64_t nb) {
+    __shared__ int64_t sh[64];
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_T) {
+        const int64_t i = b0 + threadIdx.x;
+        const int64_t v = i < nb ? sums[i] : 0;
+        int64_t tot;
+        const int64_t ex = block_exclusive_scan(v, sh, tot);
+        if (i < nb) sums[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+__global__ void scan_apply(const int64_t *__restrict__ in, int64_t n, const int64_t *__restrict__ sums,
+                           int64_t *__restrict__ out, int64_t *__restrict__ out_total) {
+    __shared__ int64_t sh[64];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_I;
+    int64_t v[SCAN_I], s = 0;
+    for (int i = 0; i < SCAN_I; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        s += v[i];
+    }
+    int64_t tot;
+    int64_t run = block_exclusive_scan(s, sh, tot) + sums[blockIdx.x];
+    for (int i = 0; i < SCAN_I; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) *out_total = run;
+}
+
+__global__ void sched_fill_kernel(const int64_t *__restrict__ rowptr, const int64_t *__restrict__ offsets,
+                                  int64_t n, int4 *__restrict__ items, int4 *__restrict__ slots) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t len = rowptr[r + 1] - rowptr[r];
+    const int nch = len <= CHUNK ? 1 : (int)((len + CHUNK - 1) / CHUNK);
+    const int64_t off = offsets[r];
+    const int64_t it0 = off >> 32;
+    const int sl0 = (int)(off & 0xffffffffLL);
+    if (nch == 1) {
+        items[it0] = make_int4((int)r, 0, -1, 1);
+        return;
+    }
+    for (int j = 0; j < nch; ++j) {
+        items[it0 + j] = make_int4((int)r, j, sl0 + j, nch);
+        slots[sl0 + j] = make_int4((int)r, j, nch, sl0);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Gather SpMM + fused epilogues.
+// ---------------------------------------------------------------------------------------
+struct SpmmArgs {
+    const int64_t *rowptr;
+    const int32_t *col;
+    const float *val;
+    const float4 *src;        // gathered operand, row stride d4 float4
+    int d4, nslices;
+    Sched sch;
+    int64_t n_rows;
+    float4 *partials;         // [slots][d4]
+    // epilogue
+    const float *scale;       // s_v (EPI_V) or s_u (EPI_U / EPI_FINAL)
+    const float4 *X;
+    float c, alpha;
+    float4 *out;              // Q (EPI_V), P (EPI_U), Z (EPI_FINAL)
+    float4 *out_hat;          // Zhat (EPI_FINAL, fused when nslices == 1), else null
+};
+
+__device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {
+    a.x = fmaf(w, v.x, a.x); a.y = fmaf(w, v.y, a.y); a.z = fmaf(w, v.z, a.z); a.w = fmaf(w, v.w, a.w);
+    return a;
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 v) {
+    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    return a;
+}
+
+template <bool WEIGHTED>
+__device__ __forceinline__ float4 gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, int c4, bool act) {
+    const int lane = threadIdx.x & 31;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 *__restrict__ src = a.src + c4;
+    const int64_t d4 = a.d4;
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+        const int cnt = (int)(end - e0 < 32 ? end - e0 : 32);
+        const int mycol = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
+        float myw = 1.f;
+        if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
+        int j = 0;
+        for (; j + UNR <= cnt; j += UNR) {
+            float4 v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int c = __shfl_sync(0xffffffffu, mycol, j + u);
+                v[u] = act ? __ldg(src + (int64_t)c * d4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                if (WEIGHTED) acc = f4fma(__shfl_sync(0xffffffffu, myw, j + u), v[u], acc);
+                else acc = f4add(acc, v[u]);
+            }
+        }
+        for (; j < cnt; ++j) {
+            const int c = __shfl_sync(0xffffffffu, mycol, j);
+            const float4 v = act ? __ldg(src + (int64_t)c * d4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (WEIGHTED) acc = f4fma(__shfl_sync(0xffffffffu, myw, j), v, acc);
+            else acc = f4add(acc, v);
+        }
+    }
+    return acc;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc) {
+    const int64_t o = row * (int64_t)a.d4 + c4;
+    if (EPI == EPI_V) {
+        const float s = a.scale[row];
+        const float s2 = s * s;
+        if (act) a.out[o] = make_float4(acc.x * s2, acc.y * s2, acc.z * s2, acc.w * s2);
+        return;
+    }
+    const float su = a.scale[row];
+    const float g = a.alpha * su;
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+        const float4 x = __ldg(a.X + o);
+        z.x = fmaf(a.c, x.x, g * acc.x);
+        z.y = fmaf(a.c, x.y, g * acc.y);
+        z.z = fmaf(a.c, x.z, g * acc.z);
+        z.w = fmaf(a.c, x.w, g * acc.w);
+    }
+    if (EPI == EPI_U) {
+        if (act) a.out[o] = make_float4(su * z.x, su * z.y, su * z.z, su * z.w);
+        return;
+    }
+    // EPI_FINAL
+    if (act) a.out[o] = z;
+    if (a.out_hat != nullptr) {            // only when nslices == 1: the warp owns the row
+        float ss = z.x * z.x + z.y * z.y + z.z * z.z + z.w * z.w;
+        for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;
+        if (act) a.out_hat[o] = make_float4(z.x * inv, z.y * inv, z.z * inv, z.w * inv);
+    }
+}
+
+template <int EPI, bool WEIGHTED>
+__global__ void __launch_bounds__(WPB * 32) spmm_kernel(SpmmArgs a) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
+    const int64_t n_items = tot >> 32;
+    const int64_t item = gw / a.nslices;
+    const int slice = (int)(gw - item * a.nslices);
+    if (item >= n_items) return;
+    const int4 it = a.sch.items[item];
+    const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];
+    const int64_t beg = rb + (int64_t)it.y * CHUNK;
+    const int64_t end = it.w == 1 ? re : min(re, beg + CHUNK);
+    const int c4 = slice * 32 + lane;
+    const bool act = c4 < a.d4;
+    const float4 acc = gather_rows<WEIGHTED>(a, beg, end, c4, act);
+    if (it.z >= 0) {
+        if (act) a.partials[(int64_t)it.z * a.d4 + c4] = acc;
+        return;
+    }
+    epilogue<EPI>(a, it.x, c4, act, acc);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(WPB * 32) fixup_kernel(SpmmArgs a) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
+    const int64_t n_slots = tot & 0xffffffffLL;
+    const int64_t slot = gw / a.nslices;
+    const int slice = (int)(gw - slot * a.nslices);
+    if (slot >= n_slots) return;
+    const int4 s = a.sch.slots[slot];
+    if (s.y != 0) return;                       // the warp of chunk 0 finishes the row
+    const int c4 = slice * 32 + lane;
+    const bool act = c4 < a.d4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+        const float4 *p = a.partials + (int64_t)slot * a.d4 + c4;
+        int j = 0;
+        for (; j + 4 <= s.z; j += 4) {
+            float4 v0 = p[(int64_t)(j + 0) * a.d4], v1 = p[(int64_t)(j + 1) * a.d4];
+            float4 v2 = p[(int64_t)(j + 2) * a.d4], v3 = p[(int64_t)(j + 3) * a.d4];
+            acc = f4add(acc, v0); acc = f4add(acc, v1); acc = f4add(acc, v2); acc = f4add(acc, v3);
+        }
+        for (; j < s.z; ++j) acc = f4add(acc, p[(int64_t)j * a.d4]);
+    }
+    epilogue<EPI>(a, s.x, c4, act, acc);
+}
+
+// P0 = s_u . (c X) for T >= 1; for T == 0, Z = c X (and Zhat = rownorm, see below).
+__global__ void init_scaled_kernel(const float4 *__restrict__ X, const float *__restrict__ su, int64_t n, int d4,
+                                   float c, int scale_rows, float4 *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * d4) return;
+    const int64_t row = i / d4;
+    const float s = scale_rows ? su[row] * c : c;
+    const float4 x = X[i];
+    out[i] = make_float4(s * x.x, s * x.y, s * x.z, s * x.w);
+}
+
+// Zhat = Z / ||Z|| row-wise (warp per row), zero rows stay zero (R4).
+__global__ void rownorm_kernel(const float4 *__restrict__ Z, int64_t n, int d4, float4 *__restrict__ Zh) {
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const float4 *z = Z + row * d4;
+    float ss = 0.f;
+    for (int j = lane; j < d4; j += 32) {
+        const float4 v = z[j];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;
+    for (int j = lane; j < d4; j += 32) {
+        const float4 v = z[j];
+        Zh[row * d4 + j] = make_float4(v.x * inv, v.y * inv, v.z * inv, v.w * inv);
+    }
+}
+
+struct SchedBufs {
+    Sched s;
+    int64_t *cnt, *tilesums;
+};
+
+SchedBufs sched_alloc(Arena &ar, int64_t n_rows, int64_t nnz) {
+    SchedBufs b;
+    b.s.max_items = n_rows + nnz / CHUNK + 1;
+    b.s.max_slots = 2 * (nnz / CHUNK) + 1;
+    b.s.offsets = ar.take<int64_t>(n_rows + 1);
+    b.s.items = ar.take<int4>(b.s.max_items);
+    b.s.slots = ar.take<int4>(b.s.max_slots);
+    b.cnt = ar.take<int64_t>(n_rows + 1);
+    b.tilesums = ar.take<int64_t>(cdiv(n_rows + 1, SCAN_TILE) + 1);
+    return b;
+}
+
+void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream_t st) {
+    const int T = 256;
+    sched_count_kernel<<<cdiv(n_rows, T), T, 0, st>>>(rowptr, n_rows, b.cnt);
+    TPO_LAUNCH_CHECK();
+    const int64_t nb = cdiv(n_rows, SCAN_TILE);
+    scan_tile_sums<<<nb, SCAN_T, 0, st>>>(b.cnt, n_rows, b.tilesums);
+    TPO_LAUNCH_CHECK();
+    scan_sums_single<<<1, SCAN_T, 0, st>>>(b.tilesums, nb);
+    TPO_LAUNCH_CHECK();
+    scan_apply<<<nb, SCAN_T, 0, st>>>(b.cnt, n_rows, b.tilesums, b.s.offsets, b.s.offsets + n_rows);
+    TPO_LAUNCH_CHECK();
+    sched_fill_kernel<<<cdiv(n_rows, T), T, 0, st>>>(rowptr, b.s.offsets, n_rows, b.s.items, b.s.slots);
+    TPO_LAUNCH_CHECK();
+}
+
+template <int EPI>
+void spmm_launch(const SpmmArgs &a, int64_t max_items, int64_t max_slots, bool weighted, cudaStream_t st) {
+    const int64_t warps = max_items * a.nslices;
+    const int64_t blocks = cdiv(warps, WPB);
+    if (weighted) spmm_kernel<EPI, true><<<blocks, WPB * 32, 0, st>>>(a);
+    else spmm_kernel<EPI, false><<<blocks, WPB * 32, 0, st>>>(a);
+    TPO_LAUNCH_CHECK();
+    const int64_t fw = max_slots * a.nslices;
+    fixup_kernel<EPI><<<cdiv(fw, WPB), WPB * 32, 0, st>>>(a);
+    TPO_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
+    Arena ar(nullptr, 0);
+    ar.take<float>(n_v * d);                      // Q (V-side block)
+    ar.take<float>(n_u);
+    ar.take<float>(n_v);
+    sched_alloc(ar, n_u, nnz);
+    sched_alloc(ar, n_v, nnz);
+    ar.take<float>((2 * (nnz / CHUNK) + 1) * d);  // partials (shared by both SpMMs)
+    return ar.off + 256;
+}
+
+void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
+                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st) {
+    const int64_t n = B.n_rows, m = B.n_cols, nnz = B.nnz;
+    const int d4 = (int)(d / 4);
+    const float c = alpha < 1.0f ? 1.0f - alpha : 1.0f;    // R1
+    float *Qv = ar.take<float>(m * d);
+    float *su = ar.take<float>(n);
+    float *sv = ar.take<float>(m);
+    SchedBufs sb = sched_alloc(ar, n, nnz);
+    SchedBufs sbt = sched_alloc(ar, m, nnz);
+    float *partials = ar.take<float>((2 * (nnz / CHUNK) + 1) * d);
+
+    const int TB = 256;
+    if (n > 0) degree_scale_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>(B.row_ptr, B.val, n, su);
+    TPO_LAUNCH_CHECK();
+    if (m > 0) degree_scale_kernel<<<cdiv(m * 32, TB), TB, 0, st>>>(Bt.row_ptr, Bt.val, m, sv);
+    TPO_LAUNCH_CHECK();
+    if (n == 0) return;
+    if (T == 0) {
+        init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 0, (float4 *)Z);
+        TPO_LAUNCH_CHECK();
+        if (Zhat) rownorm_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>((const float4 *)Z, n, d4, (float4 *)Zhat);
+        TPO_LAUNCH_CHECK();
+        return;
+    }
+    sched_build(sb, B.row_ptr, n, st);
+    if (m > 0) sched_build(sbt, Bt.row_ptr, m, st);
+    init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 1, (float4 *)Z);
+    TPO_LAUNCH_CHECK();
+
+    const int nslices = (d4 + 31) / 32;
+    for (int t = 0; t < T; ++t) {
+        const bool last = (t == T - 1);
+        if (m > 0) {
+            SpmmArgs a{};
+            a.rowptr = Bt.row_ptr; a.col = Bt.col_idx; a.val = Bt.val;
+            a.src = (const float4 *)Z; a.d4 = d4; a.nslices = nslices;
+            a.sch = sbt.s; a.n_rows = m; a.partials = (float4 *)partials;
+            a.scale = sv; a.out = (float4 *)Qv;
+            spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
+        } else {
+            TPO_CUDA(cudaMemsetAsync(Qv, 0, 0, st));
+        }
+        SpmmArgs a{};
+        a.rowptr = B.row_ptr; a.col = B.col_idx; a.val = B.val;
+        a.src = (const float4 *)Qv; a.d4 = d4; a.nslices = nslices;
+        a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
+        a.scale = su; a.X = (const float4 *)X; a.c = c; a.alpha = alpha;
+        a.out = (float4 *)Z;
+        if (last) {
+            a.out_hat = (nslices == 1 && Zhat) ? (float4 *)Zhat : nullptr;
+            spmm_launch<EPI_FINAL>(a, sb.s.max_items, sb.s.max_slots, B.val != nullptr, st);
+            if (Zhat && nslices > 1) {
+                rownorm_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>((const float4 *)Z, n, d4, (float4 *)Zhat);
+                TPO_LAUNCH_CHECK();
+            }
+        } else {
+            spmm_launch<EPI_U>(a, sb.s.max_items, sb.s.max_slots, B.val != nullptr, st);
+        }
+    }
+}
+
+}  // namespace tpo

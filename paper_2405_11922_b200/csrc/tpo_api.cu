@@ -1,0 +1,253 @@
+// C-ABI entry points of libtpo (include/tpo.h): argument validation, workspace carving,
+// error translation.  All arithmetic lives in the module files.
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+
+size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d);
+size_t features_ws_bytes(int64_t n, int64_t d);
+size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p);
+size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k);
+
+namespace {
+thread_local std::string g_last_error;
+thread_local uint64_t g_launches = 0;
+}
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+void count_launch() { ++g_launches; }
+
+int sm_count() {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return v;
+}
+
+namespace {
+
+void check_ptr(const void *p, const char *name, bool need_align = true) {
+    TPO_REQUIRE(p != nullptr, std::string(name) + " is NULL");
+    if (need_align) TPO_REQUIRE(aligned16(p), std::string(name) + " is not 16-byte aligned");
+}
+
+void check_csr(const tpo_csr_t *A, const char *name) {
+    TPO_REQUIRE(A != nullptr, std::string(name) + " is NULL");
+    TPO_REQUIRE(A->n_rows >= 0 && A->n_cols >= 0 && A->nnz >= 0, std::string(name) + ": negative size");
+    TPO_REQUIRE(A->n_rows < (int64_t(1) << 31) && A->n_cols < (int64_t(1) << 31), std::string(name) + ": more than 2^31-1 rows/cols");
+    TPO_REQUIRE(A->row_ptr != nullptr, std::string(name) + ".row_ptr is NULL");
+    TPO_REQUIRE(A->nnz == 0 || A->col_idx != nullptr, std::string(name) + ".col_idx is NULL");
+}
+
+void check_ws(void *ws, size_t have, size_t need) {
+    if (have < need) throw Error(TPO_ENOMEM, "workspace too small: " + std::to_string(have) + " < " + std::to_string(need));
+    TPO_REQUIRE(ws != nullptr || need == 0, "ws is NULL");
+    TPO_REQUIRE((reinterpret_cast<uintptr_t>(ws) & 255u) == 0, "ws is not 256-byte aligned");
+}
+
+void check_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T,
+                     const float *Z, const float *Zhat) {
+    check_csr(B, "B");
+    check_csr(Bt, "Bt");
+    TPO_REQUIRE(B->n_rows == Bt->n_cols && B->n_cols == Bt->n_rows, "Bt is not shaped as the transpose of B");
+    TPO_REQUIRE(B->nnz == Bt->nnz, "B.nnz != Bt.nnz");
+    TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+    TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
+    TPO_REQUIRE(T >= 0, "T must be >= 0");
+    if (B->n_rows > 0) {
+        check_ptr(X, "X");
+        check_ptr(Z, "Z");
+    }
+    if (Zhat) check_ptr(Zhat, "Zhat");
+}
+
+}  // namespace
+}  // namespace tpo
+
+using namespace tpo;
+
+extern "C" {
+
+int tpo_abi_version(void) { return TPO_ABI_VERSION; }
+
+const char *tpo_last_error(void) { return tpo::g_last_error.c_str(); }
+
+uint64_t tpo_launch_count(void) { return tpo::g_launches; }
+
+size_t tpo_propagate_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
+    return propagate_ws_bytes(n_u, n_v, nnz, d);
+}
+
+int tpo_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T,
+                  float *Z, float *Zhat, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        check_propagate(B, Bt, X, d, alpha, T, Z, Zhat);
+        check_ws(ws, ws_bytes, tpo_propagate_ws(B->n_rows, B->n_cols, B->nnz, d));
+        Arena ar(ws, ws_bytes);
+        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zhat, ar, as_stream(stream));
+    });
+}
+
+int tpo_haar_q(const double *G, int64_t d, double *Q) {
+    return guarded([&] {
+        TPO_REQUIRE(G != nullptr && Q != nullptr, "G and Q must be host pointers");
+        TPO_REQUIRE(d >= 1, "d must be >= 1");
+        host_qr_positive(d, d, G, Q, nullptr);
+    });
+}
+
+size_t tpo_features_ws(int64_t n, int64_t d) { return features_ws_bytes(n, d); }
+
+int tpo_features(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv, double *r_out,
+                 void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 0, "n must be >= 0");
+        TPO_REQUIRE(d >= 1 && d <= 8192, "d must lie in [1, 8192]");
+        if (n > 0) {
+            check_ptr(Zhat, "Zhat");
+            check_ptr(Rp, "Rp");
+            check_ptr(dinv, "dinv");
+        }
+        check_ptr(Q, "Q");
+        check_ws(ws, ws_bytes, tpo_features_ws(n, d));
+        Arena ar(ws, ws_bytes);
+        features_impl(Zhat, n, d, Q, Rp, dinv, r_out, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_affinity_matvec_ws(int64_t n, int64_t D, int64_t b) {
+    return align_up(sizeof(double) * D * b) + tsgemm_ws(n, D, b) + 1024;
+}
+
+int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b,
+                        float *out, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && D >= 1 && b >= 1, "n, D, b must be >= 1");
+        check_ptr(Rp, "Rp");
+        check_ptr(dinv, "dinv");
+        check_ptr(Y, "Y");
+        check_ptr(out, "out");
+        TPO_REQUIRE(out != Y, "out may not alias Y");
+        check_ws(ws, ws_bytes, tpo_affinity_matvec_ws(n, D, b));
+        Arena ar(ws, ws_bytes);
+        affinity_matvec_impl(Rp, dinv, n, D, Y, b, out, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_topk_eig_ws(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p) {
+    return topk_eig_ws_bytes(n, D, k, mode, p);
+}
+
+int tpo_topk_eig(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p,
+                 int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi, void *ws, size_t ws_bytes,
+                 void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(mode == TPO_EIG_EXACT || mode == TPO_EIG_HALKO, "unknown eig mode");
+        TPO_REQUIRE(n >= 1 && D >= 1, "n and D must be >= 1");
+        TPO_REQUIRE(k >= 1 && k <= n && k <= D, "k must lie in [1, min(n, D)]");
+        TPO_REQUIRE(k <= 128, "k must be <= 128");
+        if (mode == TPO_EIG_HALKO) {
+            TPO_REQUIRE(p >= 0 && q >= 0, "p and q must be >= 0");
+            TPO_REQUIRE(k + p <= n && k + p <= D, "k + p must be <= min(n, D)");
+            check_ptr(Omega, "Omega");
+        }
+        check_ptr(Rp, "Rp");
+        check_ptr(dinv, "dinv");
+        check_ptr(Gamma, "Gamma");
+        check_ptr(Psi, "Psi");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        check_ws(ws, ws_bytes, tpo_topk_eig_ws(n, D, k, mode, p));
+        Arena ar(ws, ws_bytes);
+        cudaStream_t st = as_stream(stream);
+        topk_eig_impl(Rp, dinv, n, D, k, mode, p, q, Omega, Gamma, sigma, Psi, ar, st);
+        TPO_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+size_t tpo_cluster_ws(int64_t n, int64_t D, int32_t k) { return cluster_ws_bytes(n, D, k); }
+
+int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
+                const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels, int32_t *iters_used,
+                void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && D >= 1, "n and D must be >= 1");
+        TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= D, "k must lie in [1, min(n, D, 128)]");
+        TPO_REQUIRE(Tf >= 0 && Tg >= 1, "need Tf >= 0 and Tg >= 1");
+        check_ptr(Rp, "Rp");
+        check_ptr(dinv, "dinv");
+        check_ptr(Gamma, "Gamma");
+        check_ptr(Psi, "Psi");
+        check_ptr(labels, "labels");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        check_ws(ws, ws_bytes, tpo_cluster_ws(n, D, k));
+        Arena ar(ws, ws_bytes);
+        cluster_impl(Rp, dinv, n, D, k, Gamma, sigma, Psi, Tf, Tg, labels, iters_used, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, int32_t mode, int32_t p) {
+    const int64_t D = 2 * d;
+    size_t s = 0;
+    s += 2 * align_up(sizeof(float) * n_u * d);          // Z, Zhat
+    s += align_up(sizeof(float) * n_u * D) + align_up(sizeof(float) * n_u);   // Rp, dinv
+    s += align_up(sizeof(float) * d * d);                // Q
+    s += align_up(sizeof(float) * n_u * k) + align_up(sizeof(float) * D * k);   // Gamma, Psi
+    size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d), tpo_features_ws(n_u, d)),
+                            std::max(tpo_topk_eig_ws(n_u, D, k, mode, p), tpo_cluster_ws(n_u, D, k)));
+    return s + stage + 8 * 256;
+}
+
+int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T, int32_t k,
+            const double *G, int32_t eig_mode, const float *Omega, int32_t p, int32_t q, int32_t Tf, int32_t Tg,
+            int32_t *labels, double *timings_ms, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        check_propagate(B, Bt, X, d, alpha, T, X, nullptr);
+        TPO_REQUIRE(G != nullptr, "G (host) is NULL");
+        const int64_t n = B->n_rows, D = 2 * d;
+        TPO_REQUIRE(n >= 1, "empty U side");
+        TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= D, "k must lie in [1, min(n, 2d, 128)]");
+        check_ptr(labels, "labels");
+        check_ws(ws, ws_bytes, tpo_run_ws(n, B->n_cols, B->nnz, d, k, eig_mode, p));
+        cudaStream_t st = as_stream(stream);
+        Arena ar(ws, ws_bytes);
+        float *Z = ar.take<float>(n * d), *Zh = ar.take<float>(n * d);
+        float *Rp = ar.take<float>(n * D), *dinv = ar.take<float>(n);
+        float *Qd = ar.take<float>(d * d);
+        float *Gamma = ar.take<float>(n * k), *Psi = ar.take<float>(D * k);
+        const size_t mark = ar.off;
+        cudaEvent_t ev[5];
+        for (auto &e : ev) TPO_CUDA(cudaEventCreate(&e));
+        TPO_CUDA(cudaEventRecord(ev[0], st));
+        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st);
+        ar.off = mark;
+        TPO_CUDA(cudaEventRecord(ev[1], st));
+        std::vector<double> Qh((size_t)d * d);
+        host_qr_positive(d, d, G, Qh.data(), nullptr);
+        std::vector<float> Qf(Qh.begin(), Qh.end());
+        TPO_CUDA(cudaMemcpyAsync(Qd, Qf.data(), sizeof(float) * d * d, cudaMemcpyHostToDevice, st));
+        features_impl(Zh, n, d, Qd, Rp, dinv, nullptr, ar, st);
+        ar.off = mark;
+        TPO_CUDA(cudaEventRecord(ev[2], st));
+        std::vector<double> sig(k);
+        topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st);
+        ar.off = mark;
+        TPO_CUDA(cudaEventRecord(ev[3], st));
+        cluster_impl(Rp, dinv, n, D, k, Gamma, sig.data(), Psi, Tf, Tg, labels, nullptr, ar, st);
+        TPO_CUDA(cudaEventRecord(ev[4], st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        if (timings_ms)
+            for (int i = 0; i < 4; ++i) {
+                float ms = 0.f;
+                TPO_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                timings_ms[i] = ms;
+            }
+        for (auto &e : ev) cudaEventDestroy(e);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// Internal helpers of libtpo (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <exception>
+#include <string>
+
+#include "../../include/tpo.h"
+
+namespace tpo {
+
+// Thread-local last error message (the only global mutable state of the library).
+void set_error(const std::string &msg);
+
+struct Error : public std::exception {
+    int code;
+    std::string msg;
+    Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+    const char *what() const noexcept override { return msg.c_str(); }
+};
+
+#define TPO_REQUIRE(cond, msg)                                                   \
+    do {                                                                         \
+        if (!(cond)) throw ::tpo::Error(TPO_EINVAL, std::string(__func__) + ": " + (msg)); \
+    } while (0)
+
+#define TPO_CUDA(call)                                                           \
+    do {                                                                         \
+        cudaError_t _e = (call);                                                 \
+        if (_e != cudaSuccess)                                                   \
+            throw ::tpo::Error(TPO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+// Every kernel launch is followed by TPO_LAUNCH_CHECK(), which also counts it (thread-local
+// counter read by tpo_launch_count(); used by bench.py's gpu_launches).
+void count_launch();
+#define TPO_LAUNCH_CHECK()            \
+    do {                              \
+        ::tpo::count_launch();        \
+        TPO_CUDA(cudaGetLastError()); \
+    } while (0)
+
+// Runs f(); converts exceptions into TPO error codes + the last-error message.
+template <class F>
+int guarded(F &&f) {
+    try {
+        f();
+        return TPO_OK;
+    } catch (const Error &e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::exception &e) {
+        set_error(std::string("internal: ") + e.what());
+        return TPO_ECUDA;
+    } catch (...) {
+        set_error("internal: unknown exception");
+        return TPO_ECUDA;
+    }
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Bump allocator over the caller's workspace.
+struct Arena {
+    char *base;
+    size_t cap, off = 0;
+    bool dry;                       // dry run: only measures
+    Arena(void *b, size_t c) : base(static_cast<char *>(b)), cap(c), dry(b == nullptr) {}
+    template <class T>
+    T *take(size_t count) {
+        size_t bytes = align_up(count * sizeof(T) + 1);
+        size_t at = off;
+        off += bytes;
+        if (dry) return nullptr;
+        if (off > cap) throw Error(TPO_ENOMEM, "workspace too small: need at least " + std::to_string(off) + " bytes");
+        return reinterpret_cast<T *>(base + at);
+    }
+};
+
+inline cudaStream_t as_stream(void *s) { return static_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// ----------------------------------------------------------------------------------------
+// Module entry points (implemented in the .cu files; called by tpo_api.cu)
+// ----------------------------------------------------------------------------------------
+void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
+                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st);
+void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv,
+                   double *r_out, Arena &ar, cudaStream_t st);
+void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y,
+                          int64_t b, float *out, Arena &ar, cudaStream_t st);
+void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode,
+                   int32_t p, int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi,
+                   Arena &ar, cudaStream_t st);
+void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
+                  const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
+                  int32_t *iters_used, Arena &ar, cudaStream_t st);
+
+// ----------------------------------------------------------------------------------------
+// Dense building blocks (dense.cu)
+// ----------------------------------------------------------------------------------------
+// out[p x q] (fp64, device) = sum_i (rs[i] * A[i, :])^T B[i, :], A fp32 n x p (lda), B fp32 or
+// fp64 n x q; deterministic split over rows with a fixed-order fp64 reduction.
+void tsgemm_AtB_f32f32(const float *A, int64_t lda, const float *rsA, const float *Bm, int64_t ldb,
+                       const float *rsB, int64_t n, int64_t p, int64_t q, double *out, Arena &ar,
+                       cudaStream_t st);
+void tsgemm_AtB_f32f64(const float *A, int64_t lda, const float *rsA, const double *Bm, int64_t ldb,
+                       int64_t n, int64_t p, int64_t q, double *out, Arena &ar, cudaStream_t st);
+void tsgemm_AtB_f64f64(const double *A, int64_t lda, const double *Bm, int64_t ldb, int64_t n, int64_t p,
+                       int64_t q, double *out, Arena &ar, cudaStream_t st);
+// Out[n x q] = rs[i] * (A[i, :] W) with A fp32 n x p, W fp64 p x q; output fp32 or fp64.
+void tsgemm_AW_f32(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p,
+                   int64_t q, float *out, int64_t ldo, cudaStream_t st);
+void tsgemm_AW_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p,
+                   int64_t q, double *out, int64_t ldo, cudaStream_t st);
+// Symmetric Gram G = sum_i w_i^2 A[i]^T A[i] (D x D fp64, full matrix written).
+void gram_weighted(const float *A, const float *w, int64_t n, int64_t D, double *G, Arena &ar,
+                   cudaStream_t st);
+size_t gram_ws(int64_t n, int64_t D);
+size_t tsgemm_ws(int64_t n, int64_t p, int64_t q);
+
+// ----------------------------------------------------------------------------------------
+// Host fp64 dense linear algebra (host_linalg.cpp)
+// ----------------------------------------------------------------------------------------
+void host_qr_positive(int64_t rows, int64_t cols, const double *A, double *Q, double *R);
+// Symmetric eigendecomposition: all eigenvalues (descending) in w, the eigenvectors of the
+// top `nvec` eigenvalues in the columns of V (D x nvec, row-major).
+void host_sym_eig_top(int64_t D, const double *A, int64_t nvec, double *w, double *V);
+// Cholesky A = C^T C (upper C), returns false if not SPD.
+bool host_cholesky_upper(int64_t k, const double *A, double *C);
+// Inverse of an upper-triangular matrix.
+void host_upper_inverse(int64_t k, const double *C, double *Ci);
+
+}  // namespace tpo

@@ -1,0 +1,199 @@
+"""Python binding of libtpo (include/tpo.h): argument marshalling only.
+
+PyTorch provides device memory and streams; every step of the hot path runs in the CUDA
+library.  Function names follow the C-ABI: propagate, haar_q, features, affinity_matvec,
+topk_eig, cluster, run.  Tensors must be CUDA tensors of the documented dtype and be
+contiguous; outputs are allocated here unless passed in.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from ._lib import CSR, TPO_EIG_EXACT, TPO_EIG_HALKO, check, lib  # noqa: F401
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _need(t, dtype, name, shape=None):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+@dataclass
+class DeviceGraph:
+    """CSR(B) (n_u x n_v) and CSR(B^T) (n_v x n_u) of one ABG on the device."""
+    n_u: int
+    n_v: int
+    nnz: int
+    B_rowptr: torch.Tensor
+    B_col: torch.Tensor
+    Bt_rowptr: torch.Tensor
+    Bt_col: torch.Tensor
+    B_val: Optional[torch.Tensor] = None
+    Bt_val: Optional[torch.Tensor] = None
+
+    def csr(self):
+        B = CSR(self.n_u, self.n_v, self.nnz, self.B_rowptr.data_ptr(), self.B_col.data_ptr(),
+                None if self.B_val is None else self.B_val.data_ptr())
+        Bt = CSR(self.n_v, self.n_u, self.nnz, self.Bt_rowptr.data_ptr(), self.Bt_col.data_ptr(),
+                 None if self.Bt_val is None else self.Bt_val.data_ptr())
+        return B, Bt
+
+
+def to_device_graph(n_u, n_v, B_rowptr, B_col, Bt_rowptr, Bt_col, B_val=None, Bt_val=None,
+                    device="cuda", non_blocking=False) -> DeviceGraph:
+    def dev(a, dt):
+        if a is None:
+            return None
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(device=device, dtype=dt, non_blocking=non_blocking).contiguous()
+    return DeviceGraph(int(n_u), int(n_v), int(len(B_col)), dev(B_rowptr, torch.int64), dev(B_col, torch.int32),
+                       dev(Bt_rowptr, torch.int64), dev(Bt_col, torch.int32),
+                       dev(B_val, torch.float32), dev(Bt_val, torch.float32))
+
+
+def propagate(g: DeviceGraph, X: torch.Tensor, alpha: float, T: int, Z=None, Zhat=None, want_zhat=True,
+              stream=None):
+    """a1-a3 (tpo_propagate): returns (Z, Zhat)."""
+    n, d = X.shape
+    _need(X, torch.float32, "X", (g.n_u, d))
+    Z = torch.empty_like(X) if Z is None else _need(Z, torch.float32, "Z", X.shape)
+    if want_zhat:
+        Zhat = torch.empty_like(X) if Zhat is None else _need(Zhat, torch.float32, "Zhat", X.shape)
+    else:
+        Zhat = None
+    L = lib()
+    nbytes = L.tpo_propagate_ws(g.n_u, g.n_v, g.nnz, d)
+    ws = _ws(nbytes, X.device)
+    B, Bt = g.csr()
+    check(L.tpo_propagate(C.byref(B), C.byref(Bt), _ptr(X), d, float(alpha), int(T), _ptr(Z), _ptr(Zhat),
+                          _ptr(ws), ws.numel(), _stream(stream)))
+    return Z, Zhat
+
+
+def haar_q(G: np.ndarray) -> np.ndarray:
+    """a4 (tpo_haar_q, host): Q of the positive-diagonal QR of the Gaussian G."""
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    d = G.shape[0]
+    Q = np.empty((d, d), np.float64)
+    check(lib().tpo_haar_q(G.ctypes.data_as(C.c_void_p), d, Q.ctypes.data_as(C.c_void_p)))
+    return Q
+
+
+def features(Zhat: torch.Tensor, Q: torch.Tensor, Rp=None, dinv=None, want_r=False, stream=None):
+    """a5 (tpo_features): returns (Rp, dinv, r or None)."""
+    n, d = Zhat.shape
+    _need(Zhat, torch.float32, "Zhat")
+    _need(Q, torch.float32, "Q", (d, d))
+    Rp = torch.empty((n, 2 * d), dtype=torch.float32, device=Zhat.device) if Rp is None else Rp
+    dinv = torch.empty(n, dtype=torch.float32, device=Zhat.device) if dinv is None else dinv
+    r = torch.empty(2 * d, dtype=torch.float64, device=Zhat.device) if want_r else None
+    L = lib()
+    ws = _ws(L.tpo_features_ws(n, d), Zhat.device)
+    check(L.tpo_features(_ptr(Zhat), n, d, _ptr(Q), _ptr(Rp), _ptr(dinv), _ptr(r), _ptr(ws), ws.numel(),
+                         _stream(stream)))
+    return Rp, dinv, r
+
+
+def affinity_matvec(Rp: torch.Tensor, dinv: torch.Tensor, Y: torch.Tensor, out=None, stream=None):
+    """a6 (tpo_affinity_matvec): dinv . R'(R'^T (dinv . Y))."""
+    n, D = Rp.shape
+    _need(Rp, torch.float32, "Rp")
+    _need(dinv, torch.float32, "dinv", (n,))
+    _need(Y, torch.float32, "Y")
+    b = Y.shape[1]
+    out = torch.empty_like(Y) if out is None else out
+    L = lib()
+    ws = _ws(L.tpo_affinity_matvec_ws(n, D, b), Rp.device)
+    check(L.tpo_affinity_matvec(_ptr(Rp), _ptr(dinv), n, D, _ptr(Y), b, _ptr(out), _ptr(ws), ws.numel(),
+                                _stream(stream)))
+    return out
+
+
+def topk_eig(Rp: torch.Tensor, dinv: torch.Tensor, k: int, mode: int = TPO_EIG_EXACT, p: int = 10, q: int = 2,
+             Omega: Optional[torch.Tensor] = None, stream=None):
+    """a7 (tpo_topk_eig): returns (Gamma [n,k] fp32, sigma np.float64[k], Psi [D,k] fp32)."""
+    n, D = Rp.shape
+    _need(Rp, torch.float32, "Rp")
+    _need(dinv, torch.float32, "dinv", (n,))
+    if mode == TPO_EIG_HALKO:
+        _need(Omega, torch.float32, "Omega", (D, k + p))
+    Gamma = torch.empty((n, k), dtype=torch.float32, device=Rp.device)
+    Psi = torch.empty((D, k), dtype=torch.float32, device=Rp.device)
+    sigma = np.zeros(k, np.float64)
+    L = lib()
+    ws = _ws(L.tpo_topk_eig_ws(n, D, k, mode, p), Rp.device)
+    check(L.tpo_topk_eig(_ptr(Rp), _ptr(dinv), n, D, int(k), int(mode), int(p), int(q), _ptr(Omega), _ptr(Gamma),
+                         sigma.ctypes.data_as(C.c_void_p), _ptr(Psi), _ptr(ws), ws.numel(), _stream(stream)))
+    return Gamma, sigma, Psi
+
+
+def cluster(Rp: torch.Tensor, dinv: torch.Tensor, Gamma: torch.Tensor, sigma: np.ndarray, Psi: torch.Tensor,
+            Tf: int = 5, Tg: int = 20, labels=None, stream=None):
+    """a8-a9 (tpo_cluster): returns (labels int32 [n], iterations of Alg. 3 run)."""
+    n, D = Rp.shape
+    k = Gamma.shape[1]
+    _need(Rp, torch.float32, "Rp")
+    _need(dinv, torch.float32, "dinv", (n,))
+    _need(Gamma, torch.float32, "Gamma", (n, k))
+    _need(Psi, torch.float32, "Psi", (D, k))
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+    labels = torch.empty(n, dtype=torch.int32, device=Rp.device) if labels is None else labels
+    it = C.c_int32(0)
+    L = lib()
+    ws = _ws(L.tpo_cluster_ws(n, D, k), Rp.device)
+    check(L.tpo_cluster(_ptr(Rp), _ptr(dinv), n, D, int(k), _ptr(Gamma), sigma.ctypes.data_as(C.c_void_p), _ptr(Psi),
+                        int(Tf), int(Tg), _ptr(labels), C.byref(it), _ptr(ws), ws.numel(), _stream(stream)))
+    return labels, int(it.value)
+
+
+class Runner:
+    """Whole hot path (tpo_run) with a workspace kept across calls."""
+
+    def __init__(self, g: DeviceGraph, d: int, k: int, mode: int = TPO_EIG_EXACT, p: int = 10, device="cuda"):
+        self.g, self.d, self.k, self.mode, self.p = g, d, k, mode, p
+        self.ws = _ws(lib().tpo_run_ws(g.n_u, g.n_v, g.nnz, d, k, mode, p), device)
+        self.labels = torch.empty(g.n_u, dtype=torch.int32, device=device)
+        self.timings = np.zeros(4, np.float64)
+
+    def __call__(self, X: torch.Tensor, alpha: float, T: int, G: np.ndarray, Tf: int = 5, Tg: int = 20,
+                 q: int = 2, Omega: Optional[torch.Tensor] = None, stream=None):
+        _need(X, torch.float32, "X", (self.g.n_u, self.d))
+        G = np.ascontiguousarray(G, dtype=np.float64)
+        B, Bt = self.g.csr()
+        check(lib().tpo_run(C.byref(B), C.byref(Bt), _ptr(X), self.d, float(alpha), int(T), int(self.k),
+                            G.ctypes.data_as(C.c_void_p), int(self.mode), _ptr(Omega), int(self.p), int(q), int(Tf),
+                            int(Tg), _ptr(self.labels), self.timings.ctypes.data_as(C.c_void_p), _ptr(self.ws),
+                            self.ws.numel(), _stream(stream)))
+        return self.labels
+
+
+def run(g: DeviceGraph, X: torch.Tensor, alpha: float, T: int, k: int, G: np.ndarray, mode=TPO_EIG_EXACT,
+        Tf=5, Tg=20, p=10, q=2, Omega=None):
+    """Whole hot path (tpo_run): returns (labels, timings_ms[4])."""
+    r = Runner(g, X.shape[1], k, mode, p, X.device)
+    labels = r(X, alpha, T, G, Tf, Tg, q, Omega)
+    return labels, r.timings.copy()

@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances (north_star): propagated Z within 1e-5 relative Frobenius;
+features / affinity products within 1e-5 relative Frobenius (fp32 storage); top-k subspace
+sin(max principal angle) <= 1e-4 against the oracle's exact top-k; cluster labels bit-exact
+given identical eigen inputs; end-to-end ARI(GPU, oracle) >= 0.999.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import core as O  # noqa: E402
+from oracle import dense as DN  # noqa: E402
+from synth import csr_from_edges, make_config, planted_abg, random_unit_rows  # noqa: E402
+
+
+def relF(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def tpo():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_11922_b200 import build
+    build.build()
+    import paper_2405_11922_b200 as T
+    return T
+
+
+def dev_graph(T, g):
+    return T.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, g.B_val, g.Bt_val)
+
+
+def hub_graph(seed=0, weighted=False, n=1500, m=900, d=8):
+    """Random edges plus a V hub of degree 1400 and a U hub of degree 700 (> the 512-edge chunk),
+    isolated U rows 3 and 4, isolated V 7."""
+    rng = np.random.default_rng(seed)
+    u = rng.integers(0, n, 9000)
+    v = rng.integers(0, m, 9000)
+    u = np.concatenate([u, np.arange(1400) + 5, np.full(700, 11)])
+    v = np.concatenate([v, np.full(1400, 13), rng.permutation(m)[:700]])
+    keep = (u != 3) & (u != 4) & (v != 7)
+    key = np.unique(u[keep].astype(np.int64) * m + v[keep])
+    u, v = key // m, key % m
+    w = (rng.random(u.shape[0]).astype(np.float32) + 0.5) if weighted else None
+    B_rowptr, B_col, Bt_rowptr, Bt_col, B_val, Bt_val = csr_from_edges(u, v, n, m, w)
+    X = random_unit_rows(n, d, seed=seed + 1)
+    return dict(n=n, m=m, B_rowptr=B_rowptr, B_col=B_col, Bt_rowptr=Bt_rowptr, Bt_col=Bt_col, B_val=B_val,
+                Bt_val=Bt_val, X=X)
+
+
+class G:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+# ------------------------------------------------------------------------------------------
+# a1-a3 propagation
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("d,T,alpha,weighted", [(4, 3, 0.5, False), (132, 3, 0.5, False), (128, 5, 0.9, True),
+                                                (300, 2, 0.6, False), (8, 0, 0.5, False), (12, 4, 0.0, False),
+                                                (16, 3, 1.0, True)])
+def test_propagate_planted(tpo, d, T, alpha, weighted):
+    g = planted_abg(3001, 2005, 5, d, deg=("zipf", 1.3, 120), p_in=0.6, pop=("zipf", 1.2), x=("gaussian", 1.0),
+                    seed=d + T, weighted=weighted)
+    Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, alpha, T, g.B_val)
+    Z, Zh = tpo.propagate(dev_graph(tpo, g), torch.from_numpy(g.X).cuda(), alpha, T)
+    assert relF(Z.cpu().numpy(), Zo) <= 1e-5
+    assert relF(Zh.cpu().numpy(), Zho) <= 1e-5
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("d", [8, 128, 136])
+def test_propagate_hubs_isolated(tpo, weighted, d):
+    """Rows longer than one 512-edge chunk (fix-up path), isolated U and V nodes (R3)."""
+    h = hub_graph(seed=d, weighted=weighted, d=d)
+    g = G(**h)
+    Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, 0.5, 3, g.B_val)
+    dg = tpo.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, g.B_val, g.Bt_val)
+    Z, Zh = tpo.propagate(dg, torch.from_numpy(g.X).cuda(), 0.5, 3)
+    Z, Zh = Z.cpu().numpy(), Zh.cpu().numpy()
+    assert relF(Z, Zo) <= 1e-5 and relF(Zh, Zho) <= 1e-5
+    for u in (3, 4):   # isolated U keeps X-hat
+        assert np.allclose(Zh[u], g.X[u] / np.linalg.norm(g.X[u]), atol=1e-6)
+    # run twice: bitwise identical (no float atomics)
+    Z2, Zh2 = tpo.propagate(dg, torch.from_numpy(g.X).cuda(), 0.5, 3)
+    assert np.array_equal(Z, Z2.cpu().numpy()) and np.array_equal(Zh, Zh2.cpu().numpy())
+
+
+def test_propagate_empty_graph(tpo):
+    """nnz = 0: every node is isolated, Z = (1 - alpha) X."""
+    n, m, d = 37, 5, 8
+    rp = np.zeros(n + 1, np.int64)
+    rpt = np.zeros(m + 1, np.int64)
+    X = random_unit_rows(n, d, seed=3)
+    dg = tpo.to_device_graph(n, m, rp, np.zeros(0, np.int32), rpt, np.zeros(0, np.int32))
+    Z, Zh = tpo.propagate(dg, torch.from_numpy(X).cuda(), 0.25, 4)
+    assert np.allclose(Z.cpu().numpy(), 0.75 * X, atol=1e-7)
+
+
+def test_propagate_sqrt_degree_closed_form_full_size(tpo):
+    """P2 at the bench configuration's graph (BASELINE configs[1], 'small'): x = sqrt(D_U) is a
+    fixed point of L L^T, so Z_T = (1 - alpha^{T+1}) x."""
+    g = make_config("small")
+    du = np.diff(g.B_rowptr).astype(np.float64)
+    X = np.repeat(np.sqrt(du)[:, None], 8, axis=1).astype(np.float32)
+    Z, _ = tpo.propagate(dev_graph(tpo, g), torch.from_numpy(X).cuda(), g.alpha, g.T)
+    exp = (1 - g.alpha ** (g.T + 1)) * X.astype(np.float64)
+    assert relF(Z.cpu().numpy(), exp) <= 1e-5
+
+
+@pytest.mark.slow
+def test_propagate_full_small_vs_oracle(tpo):
+    """Full-size parity on BASELINE configs[1] ('small': 50k x 80k, ~1M edges, d = 1000, T = 5)."""
+    g = make_config("small")
+    Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, g.T)
+    Z, Zh = tpo.propagate(dev_graph(tpo, g), torch.from_numpy(g.X).cuda(), g.alpha, g.T)
+    assert relF(Z.cpu().numpy(), Zo) <= 1e-5
+    assert relF(Zh.cpu().numpy(), Zho) <= 1e-5
+
+
+# ------------------------------------------------------------------------------------------
+# a4-a5 features
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,d", [(3001, 12), (1000, 132), (777, 300), (130, 4)])
+def test_features(tpo, n, d):
+    Zh = random_unit_rows(n, d, seed=d, zero_rows=(5,))
+    Q = O.haar_q(np.random.default_rng(d).standard_normal((d, d))).astype(np.float32)
+    Rpo, dvo, ro = O.features(Zh, Q)
+    Rp, dv, r = tpo.features(torch.from_numpy(Zh).cuda(), torch.from_numpy(Q).cuda(), want_r=True)
+    assert relF(Rp.cpu().numpy(), Rpo) <= 1e-5
+    assert relF(dv.cpu().numpy(), dvo) <= 1e-5
+    assert relF(r.cpu().numpy(), ro) <= 1e-5
+    Rp2, dv2, _ = tpo.features(torch.from_numpy(Zh).cuda(), torch.from_numpy(Q).cuda())
+    assert torch.equal(Rp, Rp2) and torch.equal(dv, dv2)
+
+
+# ------------------------------------------------------------------------------------------
+# a6-a7 implicit affinity and top-k
+# ------------------------------------------------------------------------------------------
+
+def oracle_features_of(g):
+    Z, Zh = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, g.T, g.B_val)
+    Q = O.haar_q(g.G)
+    Rp, dinv, _ = O.features(Zh.astype(np.float32), Q.astype(np.float32))
+    return Rp.astype(np.float32), dinv.astype(np.float32)
+
+
+@pytest.fixture(scope="module")
+def tiny_feats():
+    g = make_config("tiny")
+    Rp, dinv = oracle_features_of(g)
+    return g, Rp, dinv
+
+
+def test_affinity_matvec(tpo, tiny_feats):
+    g, Rp, dinv = tiny_feats
+    Y = np.random.default_rng(1).standard_normal((g.n, 15)).astype(np.float32)
+    out_o = O.affinity_matvec(Rp, dinv, Y)
+    out = tpo.affinity_matvec(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), torch.from_numpy(Y).cuda())
+    assert relF(out.cpu().numpy(), out_o) <= 1e-5
+    # F5: S~ (1/dinv) = 1/dinv
+    v = (1.0 / dinv)[:, None].astype(np.float32)
+    o2 = tpo.affinity_matvec(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), torch.from_numpy(v).cuda())
+    assert relF(o2.cpu().numpy(), v) <= 1e-5
+
+
+@pytest.fixture(scope="module")
+def tiny_topk(tiny_feats):
+    g, Rp, dinv = tiny_feats
+    return O.topk(Rp, dinv, g.k)
+
+
+def test_topk_exact_tiny(tpo, tiny_feats, tiny_topk):
+    g, Rp, dinv = tiny_feats
+    Gmo, so, Pso, lam = tiny_topk
+    Gm, s, Ps = tpo.topk_eig(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), g.k)
+    Gm, Ps = Gm.cpu().numpy(), Ps.cpu().numpy()
+    assert DN.sin_theta(Gm, Gmo) <= 1e-4
+    assert DN.sin_theta(Ps, Pso) <= 1e-4
+    assert np.allclose(s, so, rtol=1e-5)
+    assert abs(s[0] - 1.0) < 1e-5                                   # F5 / E5
+    assert np.max(np.abs(Gm.astype(np.float64).T @ Gm - np.eye(g.k))) <= 1e-6   # E2
+    assert np.all(Gm.astype(np.float64).sum(0) >= 0)                 # R8
+
+
+def test_topk_planted_svd(tpo):
+    """E8: R' = U diag(s) V^T with dinv = 1 -> Gamma = U[:, :k], sigma = s[:k]."""
+    rng = np.random.default_rng(3)
+    n, D, k = 2500, 48, 6
+    U, _ = np.linalg.qr(rng.standard_normal((n, D)))
+    V, _ = np.linalg.qr(rng.standard_normal((D, D)))
+    sig = np.geomspace(3.0, 0.05, D)
+    Rp = ((U * sig) @ V.T).astype(np.float32)
+    Gm, s, Ps = tpo.topk_eig(torch.from_numpy(Rp).cuda(), torch.ones(n, device="cuda"), k)
+    assert np.allclose(s, sig[:k], rtol=1e-5)
+    assert DN.sin_theta(Gm.cpu().numpy(), U[:, :k]) <= 1e-4
+    assert DN.sin_theta(Ps.cpu().numpy(), V[:, :k]) <= 1e-4
+
+
+# ------------------------------------------------------------------------------------------
+# a8-a9 discretisation
+# ------------------------------------------------------------------------------------------
+
+def test_cluster_bit_exact_given_eigen_inputs(tpo, tiny_feats, tiny_topk):
+    """D4: identical fp32 (R', dinv, Gamma, Psi) and fp64 sigma -> identical labels."""
+    g, Rp, dinv = tiny_feats
+    Gmo, so, Pso, _ = tiny_topk
+    Gm32, Ps32 = Gmo.astype(np.float32), Pso.astype(np.float32)
+    lab_o, it_o, U_o = O.cluster(Rp, dinv, Gm32, so, Ps32, 5, 20)
+    lab, it = tpo.cluster(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), torch.from_numpy(Gm32).cuda(), so,
+                          torch.from_numpy(Ps32).cuda(), 5, 20)
+    lab = lab.cpu().numpy()
+    assert it == it_o
+    assert np.array_equal(lab, lab_o)
+
+
+@pytest.mark.parametrize("Tf,Tg", [(0, 1), (1, 3), (7, 30)])
+def test_cluster_iterations(tpo, Tf, Tg):
+    g = planted_abg(1200, 1200, 4, 16, deg=("poisson", 8.0), p_in=0.85, x=("gaussian", 1.0), alpha=0.5, T=3, seed=5)
+    Rp, dinv = oracle_features_of(g)
+    Gmo, so, Pso, _ = O.topk(Rp, dinv, g.k)
+    Gm32, Ps32 = Gmo.astype(np.float32), Pso.astype(np.float32)
+    lab_o, it_o, _ = O.cluster(Rp, dinv, Gm32, so, Ps32, Tf, Tg)
+    lab, it = tpo.cluster(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), torch.from_numpy(Gm32).cuda(), so,
+                          torch.from_numpy(Ps32).cuda(), Tf, Tg)
+    assert it == it_o and np.array_equal(lab.cpu().numpy(), lab_o)
+
+
+# ------------------------------------------------------------------------------------------
+# end to end
+# ------------------------------------------------------------------------------------------
+
+def test_run_tiny_end_to_end(tpo, tiny_topk):
+    g = make_config("tiny")
+    res = O.run(g)
+    labels, tm = tpo.run(dev_graph(tpo, g), torch.from_numpy(g.X).cuda(), g.alpha, g.T, g.k, g.G)
+    labels = labels.cpu().numpy()
+    assert DN.ari(labels, res["labels"]) >= 0.999
+    assert labels.min() >= 0 and labels.max() < g.k
+    assert np.all(tm > 0)
