@@ -95,6 +95,13 @@ int tpo_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64
  *   G: (host) d x d fp64 in;  Q: (host) d x d fp64 out.  Errors: TPO_EINVAL.
  * --------------------------------------------------------------------------------------- */
 int tpo_haar_q(const double *G, int64_t d, double *Q);
+/* The same factor computed on the device (block Gram-Schmidt with re-orthogonalisation over
+ * 64-column panels, each panel by CholeskyQR2; the QR with diag(R) > 0 is unique, so this is
+ * the Q of tpo_haar_q up to rounding), written as fp32 for tpo_features.
+ *   G: (host) d x d fp64;  Q: d x d fp32 out (device).  [sync].
+ * Workspace: tpo_haar_q_dev_ws(d).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC. */
+size_t tpo_haar_q_dev_ws(int64_t d);
+int tpo_haar_q_dev(const double *G, int64_t d, float *Q, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * a5  Random features (Alg. 1 L8-9; Eq. R-prime; Eq. Ri 466-468):

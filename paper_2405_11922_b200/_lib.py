@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "libtpo.so")
 # exported symbols, as declared in include/tpo.h
 SYMBOLS = [
     "tpo_abi_version", "tpo_last_error", "tpo_launch_count",
-    "tpo_propagate_ws", "tpo_propagate", "tpo_haar_q",
+    "tpo_propagate_ws", "tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev_ws", "tpo_haar_q_dev",
     "tpo_features_ws", "tpo_features",
     "tpo_affinity_matvec_ws", "tpo_affinity_matvec",
     "tpo_topk_eig_ws", "tpo_topk_eig",
@@ -57,6 +57,9 @@ def lib():
     L.tpo_propagate_ws.restype = sz
     L.tpo_propagate.argtypes = [P, P, vp, i64, f32, i32, vp, vp, vp, sz, vp]
     L.tpo_haar_q.argtypes = [vp, i64, vp]
+    L.tpo_haar_q_dev_ws.argtypes = [i64]
+    L.tpo_haar_q_dev_ws.restype = sz
+    L.tpo_haar_q_dev.argtypes = [vp, i64, vp, vp, sz, vp]
     L.tpo_features_ws.argtypes = [i64, i64]
     L.tpo_features_ws.restype = sz
     L.tpo_features.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, sz, vp]
@@ -72,7 +75,7 @@ def lib():
     L.tpo_run_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32]
     L.tpo_run_ws.restype = sz
     L.tpo_run.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
-    for name in ["tpo_propagate", "tpo_haar_q", "tpo_features", "tpo_affinity_matvec", "tpo_topk_eig",
+    for name in ["tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_topk_eig",
                  "tpo_cluster", "tpo_run"]:
         getattr(L, name).restype = C.c_int
     _lib = L

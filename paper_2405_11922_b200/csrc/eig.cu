@@ -240,7 +240,54 @@ void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, in
     apply_sign_rule(Gamma, n, k, Psi, D, ar, st);
 }
 
+__global__ void copy2d_kernel(const double *__restrict__ src, int64_t lds, double *__restrict__ dst, int64_t ldd,
+                              int64_t rows, int64_t cols, const double *__restrict__ sub, int64_t ldsub) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * cols) return;
+    const int64_t r = i / cols, c = i - r * cols;
+    double v = src[r * lds + c];
+    if (sub) v -= sub[r * ldsub + c];
+    dst[r * ldd + c] = v;
+}
+
 }  // namespace
+
+size_t haar_q_ws_bytes(int64_t d) {
+    const int64_t bw = std::min<int64_t>(64, d);
+    return 3 * align_up(sizeof(double) * d * d) + 4 * align_up(sizeof(double) * d * bw) +
+           tsgemm_ws(d, d, bw) + 16 * align_up(sizeof(double) * bw * bw + 8) + 8192;
+}
+
+// Alg. 1 L6-7 on the device: Q of the unique QR (diag(R) > 0) of the d x d Gaussian G by
+// block classical Gram-Schmidt with re-orthogonalisation (BCGS2) over 64-column panels, each
+// panel orthonormalised by CholeskyQR2.  R is block upper triangular with upper triangular,
+// positive-diagonal blocks, so Q is the same unique factor the host routine returns.
+void haar_q_device(const double *G_host, int64_t d, float *Q_out, Arena &ar, cudaStream_t st) {
+    const int64_t bw = std::min<int64_t>(64, d);
+    double *A = ar.take<double>(d * d), *Q = ar.take<double>(d * d);
+    double *P = ar.take<double>(d * bw), *T = ar.take<double>(d * bw), *Cm = ar.take<double>(d * bw);
+    TPO_CUDA(cudaMemcpyAsync(A, G_host, sizeof(double) * d * d, cudaMemcpyHostToDevice, st));
+    for (int64_t j0 = 0; j0 < d; j0 += bw) {
+        const int64_t w = std::min<int64_t>(bw, d - j0);
+        copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(A + j0, d, P, w, d, w, nullptr, 0);
+        TPO_LAUNCH_CHECK();
+        if (j0 > 0) {
+            for (int pass = 0; pass < 2; ++pass) {
+                const size_t mark = ar.off;
+                tsgemm_AtB_f64f64(Q, d, P, w, d, j0, w, Cm, ar, st);        // C = Q_<j^T P
+                ar.off = mark;
+                tsgemm_AW_dd(Q, d, Cm, d, j0, w, T, w, st);                 // T = Q_<j C
+                copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(P, w, P, w, d, w, T, w);   // P -= T
+                TPO_LAUNCH_CHECK();
+            }
+        }
+        cholqr2_f64(P, T, d, w, ar, st);
+        copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(P, w, Q + j0, d, d, w, nullptr, 0);
+        TPO_LAUNCH_CHECK();
+    }
+    cast_f64_f32<<<cdiv(d * d, 256), 256, 0, st>>>(Q, d * d, Q_out);
+    TPO_LAUNCH_CHECK();
+}
 
 size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p) {
     const int64_t b = std::min<int64_t>(D, k + std::max<int64_t>(k, 16));

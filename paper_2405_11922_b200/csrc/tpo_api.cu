@@ -101,6 +101,21 @@ int tpo_haar_q(const double *G, int64_t d, double *Q) {
     });
 }
 
+size_t tpo_haar_q_dev_ws(int64_t d) { return haar_q_ws_bytes(d); }
+
+int tpo_haar_q_dev(const double *G, int64_t d, float *Q, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(G != nullptr, "G (host) is NULL");
+        TPO_REQUIRE(d >= 1, "d must be >= 1");
+        check_ptr(Q, "Q");
+        check_ws(ws, ws_bytes, tpo_haar_q_dev_ws(d));
+        Arena ar(ws, ws_bytes);
+        cudaStream_t st = as_stream(stream);
+        haar_q_device(G, d, Q, ar, st);
+        TPO_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 size_t tpo_features_ws(int64_t n, int64_t d) { return features_ws_bytes(n, d); }
 
 int tpo_features(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv, double *r_out,
@@ -197,7 +212,8 @@ size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, i
     s += align_up(sizeof(float) * n_u * D) + align_up(sizeof(float) * n_u);   // Rp, dinv
     s += align_up(sizeof(float) * d * d);                // Q
     s += align_up(sizeof(float) * n_u * k) + align_up(sizeof(float) * D * k);   // Gamma, Psi
-    size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d), tpo_features_ws(n_u, d)),
+    size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d),
+                                     std::max(tpo_features_ws(n_u, d), haar_q_ws_bytes(d))),
                             std::max(tpo_topk_eig_ws(n_u, D, k, mode, p), tpo_cluster_ws(n_u, D, k)));
     return s + stage + 8 * 256;
 }
@@ -226,10 +242,8 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
         propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[1], st));
-        std::vector<double> Qh((size_t)d * d);
-        host_qr_positive(d, d, G, Qh.data(), nullptr);
-        std::vector<float> Qf(Qh.begin(), Qh.end());
-        TPO_CUDA(cudaMemcpyAsync(Qd, Qf.data(), sizeof(float) * d * d, cudaMemcpyHostToDevice, st));
+        haar_q_device(G, d, Qd, ar, st);
+        ar.off = mark;
         features_impl(Zh, n, d, Qd, Rp, dinv, nullptr, ar, st);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[2], st));

@@ -102,6 +102,9 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
                   int32_t *iters_used, Arena &ar, cudaStream_t st);
 
+void haar_q_device(const double *G_host, int64_t d, float *Q_out, Arena &ar, cudaStream_t st);
+size_t haar_q_ws_bytes(int64_t d);
+
 // ----------------------------------------------------------------------------------------
 // Dense building blocks (dense.cu)
 // ----------------------------------------------------------------------------------------
@@ -119,6 +122,8 @@ void tsgemm_AW_f32(const float *A, int64_t lda, const float *rs, const double *W
                    int64_t q, float *out, int64_t ldo, cudaStream_t st);
 void tsgemm_AW_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p,
                    int64_t q, double *out, int64_t ldo, cudaStream_t st);
+void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int64_t p, int64_t q, double *out,
+                  int64_t ldo, cudaStream_t st);
 // Symmetric Gram G = sum_i w_i^2 A[i]^T A[i] (D x D fp64, full matrix written).
 void gram_weighted(const float *A, const float *w, int64_t n, int64_t D, double *G, Arena &ar,
                    cudaStream_t st);

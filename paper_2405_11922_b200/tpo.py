@@ -103,6 +103,17 @@ def haar_q(G: np.ndarray) -> np.ndarray:
     return Q
 
 
+def haar_q_dev(G: np.ndarray, device="cuda", stream=None) -> torch.Tensor:
+    """a4 on the device (tpo_haar_q_dev): fp32 Q of the positive-diagonal QR of G."""
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    d = G.shape[0]
+    Q = torch.empty((d, d), dtype=torch.float32, device=device)
+    L = lib()
+    ws = _ws(L.tpo_haar_q_dev_ws(d), Q.device)
+    check(L.tpo_haar_q_dev(G.ctypes.data_as(C.c_void_p), d, _ptr(Q), _ptr(ws), ws.numel(), _stream(stream)))
+    return Q
+
+
 def features(Zhat: torch.Tensor, Q: torch.Tensor, Rp=None, dinv=None, want_r=False, stream=None):
     """a5 (tpo_features): returns (Rp, dinv, r or None)."""
     n, d = Zhat.shape

@@ -130,7 +130,21 @@ def test_propagate_full_small_vs_oracle(tpo):
 
 
 # ------------------------------------------------------------------------------------------
-# a4-a5 features
+# a4-a5 Haar rotation and features
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("d", [1, 12, 64, 65, 300, 1000])
+def test_haar_q_device(tpo, d):
+    """Device BCGS2 + CholeskyQR2 panels vs the oracle's Householder QR (unique positive QR)."""
+    G = np.random.default_rng(d).standard_normal((d, d))
+    Q = tpo.haar_q_dev(G).cpu().numpy()
+    Qo = O.haar_q(G)
+    assert np.max(np.abs(Q - Qo)) <= 1e-5
+    assert np.linalg.norm(Q.astype(np.float64).T @ Q - np.eye(d), 2) <= 1e-5
+
+
+# ------------------------------------------------------------------------------------------
+# features
 # ------------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n,d", [(3001, 12), (1000, 132), (777, 300), (130, 4)])
