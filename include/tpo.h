@@ -147,6 +147,14 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
  * Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC (sigma_k == 0, non-SPD Gram).
  * --------------------------------------------------------------------------------------- */
 enum { TPO_EIG_EXACT = 0, TPO_EIG_HALKO = 1 };
+/* a7 step 1 on its own: G = R^T R = R'^T diag(dinv^2) R' (D x D fp64 out, full symmetric
+ * matrix), the Gram of the exact mode.  tcgen05 kind::tf32 with 3xTF32 splitting of R
+ * (fp32-accurate products), fp32 accumulation over 256-row segments, fp64 across segments.
+ *   Rp: n x D fp32, D % 4 == 0;  dinv: n fp32;  G: D x D fp64 out (device).
+ * Workspace: tpo_gram_ws(n, D).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA. */
+size_t tpo_gram_ws(int64_t n, int64_t D);
+int tpo_gram(const float *Rp, const float *dinv, int64_t n, int64_t D, double *G, void *ws,
+             size_t ws_bytes, void *stream);
 size_t tpo_topk_eig_ws(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p);
 int tpo_topk_eig(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k,
                  int32_t mode, int32_t p, int32_t q, const float *Omega,

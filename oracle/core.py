@@ -40,6 +40,7 @@ def lib():
         L.oracle_features.argtypes = [i64, i64, vp, vp, vp, vp, vp]
         L.oracle_affinity_matvec.argtypes = [i64, i64, vp, vp, vp, i64, vp]
         L.oracle_sym_eig.argtypes = [i64, vp, vp, vp]
+        L.oracle_gram.argtypes = [i64, i64, vp, vp, vp]
         L.oracle_topk.argtypes = [i64, i64, vp, vp, i32, vp, vp, vp, vp]
         L.oracle_topk.restype = C.c_int
         L.oracle_onmf.argtypes = [i64, i64, i32, vp, vp, vp, vp, vp, i32, vp, vp]
@@ -113,6 +114,15 @@ def sym_eig(A):
     w, V = np.zeros(D), np.zeros((D, D))
     lib().oracle_sym_eig(D, _p(A), _p(w), _p(V))
     return w, V
+
+
+def gram(Rp, dinv):
+    """G = R^T R, R = diag(dinv) R' (step 1 of topk)."""
+    Rp, dinv = _c(Rp, np.float32), _c(dinv, np.float32)
+    n, D = Rp.shape
+    G = np.zeros((D, D))
+    lib().oracle_gram(n, D, _p(Rp), _p(dinv), _p(G))
+    return G
 
 
 def topk(Rp, dinv, k):

@@ -300,9 +300,9 @@ static int sign_rule(int64_t n, int64_t k, const double *Gamma, int64_t l) {
  * Gamma: n x k, sigma: k, Psi: D x k (doubles).  Returns 0, or -5 if sigma_k == 0.
  * Optionally returns all D eigenvalues of G (descending) in lam_all.
  * ------------------------------------------------------------------------------------ */
-int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_t k,
-                double *Gamma, double *sigma, double *Psi, double *lam_all) {
-    double *G = dalloc((size_t)(D * D));
+/* G = R^T R with R = diag(dinv) R' (fp64 products of the widened fp32 inputs), step 1 of
+ * oracle_topk; exported on its own for the parity test of the GPU Gram. */
+void oracle_gram(int64_t n, int64_t D, const float *Rp, const float *dinv, double *G) {
 #pragma omp parallel for schedule(static)
     for (int64_t a = 0; a < D; ++a)
         for (int64_t b = a; b < D; ++b) {
@@ -314,6 +314,12 @@ int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_
             G[a * D + b] = s;
             G[b * D + a] = s;
         }
+}
+
+int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_t k,
+                double *Gamma, double *sigma, double *Psi, double *lam_all) {
+    double *G = dalloc((size_t)(D * D));
+    oracle_gram(n, D, Rp, dinv, G);
     double *w = dalloc((size_t)D), *V = dalloc((size_t)(D * D));
     jacobi_eig(D, G, w, V);
     int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (size_t)D);

@@ -16,7 +16,7 @@ SYMBOLS = [
     "tpo_propagate_ws", "tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev_ws", "tpo_haar_q_dev",
     "tpo_features_ws", "tpo_features",
     "tpo_affinity_matvec_ws", "tpo_affinity_matvec",
-    "tpo_topk_eig_ws", "tpo_topk_eig",
+    "tpo_gram_ws", "tpo_gram", "tpo_topk_eig_ws", "tpo_topk_eig",
     "tpo_cluster_ws", "tpo_cluster",
     "tpo_run_ws", "tpo_run",
 ]
@@ -66,6 +66,9 @@ def lib():
     L.tpo_affinity_matvec_ws.argtypes = [i64, i64, i64]
     L.tpo_affinity_matvec_ws.restype = sz
     L.tpo_affinity_matvec.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, sz, vp]
+    L.tpo_gram_ws.argtypes = [i64, i64]
+    L.tpo_gram_ws.restype = sz
+    L.tpo_gram.argtypes = [vp, vp, i64, i64, vp, vp, sz, vp]
     L.tpo_topk_eig_ws.argtypes = [i64, i64, i32, i32, i32]
     L.tpo_topk_eig_ws.restype = sz
     L.tpo_topk_eig.argtypes = [vp, vp, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
@@ -75,7 +78,7 @@ def lib():
     L.tpo_run_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32]
     L.tpo_run_ws.restype = sz
     L.tpo_run.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
-    for name in ["tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_topk_eig",
+    for name in ["tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_gram", "tpo_topk_eig",
                  "tpo_cluster", "tpo_run"]:
         getattr(L, name).restype = C.c_int
     _lib = L

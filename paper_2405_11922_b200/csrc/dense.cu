@@ -222,10 +222,5 @@ void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int6
     TPO_LAUNCH_CHECK();
 }
 
-size_t gram_ws(int64_t n, int64_t D) { return tsgemm_ws(n, D, D); }
-
-void gram_weighted(const float *A, const float *w, int64_t n, int64_t D, double *G, Arena &ar, cudaStream_t st) {
-    atb_run<float, float>(A, D, w, A, D, w, n, D, D, G, ar, st);
-}
 
 }  // namespace tpo

@@ -293,7 +293,7 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
     const int64_t b = std::min<int64_t>(D, k + std::max<int64_t>(k, 16));
     const int64_t bh = k + p;
     size_t s = 0;
-    s += align_up(sizeof(double) * D * D) + gram_ws(n, D);
+    s += align_up(sizeof(double) * D * D) + gram_tc_ws(n, D);
     s += 3 * align_up(sizeof(double) * D * std::max(b, bh)) + 8 * align_up(sizeof(double) * b * b + 8);
     s += 2 * align_up(sizeof(double) * D * k) + tsgemm_ws(n, k, k) + align_up(sizeof(float) * n * k);
     if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
@@ -308,7 +308,7 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
     if (mode == TPO_EIG_EXACT) {
         double *G = ar.take<double>(D * D);
         const size_t mark = ar.off;
-        gram_weighted(Rp, dinv, n, D, G, ar, st);
+        gram_tc(Rp, dinv, n, D, G, ar, st);
         ar.off = mark;
         gram_topk(G, D, k, lam, Psi64, ar, st);
     } else {

@@ -1,0 +1,376 @@
+// a7 step 1: Gram G = R^T R = R'^T diag(dinv^2) R' (D x D) on the 5th-generation tensor cores.
+//
+// R = dinv . R' is first split into TF32 halves (R = R_hi + R_lo, R_hi = rna-tf32(R), both
+// stored fp32), then each 128 x 128 upper-triangular output tile accumulates
+//      R_lo^T R_hi + R_hi^T R_lo + R_hi^T R_hi          ("3xTF32", fp32-accurate products)
+// with tcgen05.mma kind::tf32 (both operands MN-major straight out of row-major R, staged by
+// TMA with 128-byte swizzle), fp32 accumulators in TMEM.  Every SEG k-blocks (256 rows) the
+// accumulator is drained by 8 epilogue warps into fp64 registers (double-buffered TMEM, so
+// the MMAs of the next segment overlap the drain), and the fp64 tile partials of the row
+// splits are summed in split order by a second kernel (deterministic, no atomics).
+//
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 MMA issuer (+ TMEM owner),
+// warps 2..9 epilogue (TMEM lane quarter = warp % 4, column half = (warp - 2) / 4).
+#include <cuda.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+namespace {
+
+constexpr int TILE = 128;          // output tile (M = N = 128)
+constexpr int KB = 32;             // rows per k-block (4 MMAs of K = 8)
+constexpr int STAGES = 3;
+constexpr int SEG = 8;             // k-blocks per fp32 accumulation segment (256 rows)
+constexpr int SLAB = 32 * KB * 4;  // one 32-column x 32-row fp32 slab (4 KB)
+constexpr int OPER = 4 * SLAB;     // one 128-column operand tile (16 KB)
+constexpr int STAGE_BYTES = 4 * OPER;   // A_hi, A_lo, B_hi, B_lo
+constexpr int NTHREADS = 320;
+constexpr int TMEM_COLS = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    uint64_t spins = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.b32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (++spins > (1ull << 31)) __trap();     // watchdog: never hang the GPU
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor: MN-major operand, 128-byte swizzle; LBO = byte stride between
+// 32-element (128 B) MN slabs, SBO = byte stride between 8-row K groups; version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, A and B MN-major, M x N.
+constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+            tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+struct GramArgs {
+    int n_tiles;        // T = ceil(D / 128)
+    int ksplit;         // row splits
+    int64_t rows_per;   // rows per split (multiple of KB)
+    int64_t n;
+    double *part;       // [ksplit][pairs][128][128]
+};
+
+__device__ __forceinline__ void pair_of(int p, int T, int &ta, int &tb) {
+    int a = 0;
+    while (p >= T - a) { p -= T - a; ++a; }
+    ta = a;
+    tb = a + p;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+gram_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo, GramArgs g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    const int pairs = g.n_tiles * (g.n_tiles + 1) / 2;
+    const int split = blockIdx.x % g.ksplit;
+    const int pidx = blockIdx.x / g.ksplit;
+    int ta, tb;
+    pair_of(pidx, g.n_tiles, ta, tb);
+    const bool diag = (ta == tb);
+    const int64_t r0 = (int64_t)split * g.rows_per;
+    const int64_t r1 = min(g.n, r0 + g.rows_per);
+    const int nkb = r1 > r0 ? (int)((r1 - r0 + KB - 1) / KB) : 0;
+    const int nseg = (nkb + SEG - 1) / SEG;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&bars[s]), 1);
+            mbar_init(smem_u32(&bars[STAGES + s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bars[2 * STAGES + b]), 1);
+            mbar_init(smem_u32(&bars[2 * STAGES + 2 + b]), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_lo) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            const uint32_t bytes = diag ? 2 * OPER : 4 * OPER;
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % STAGES, j = kb / STAGES;
+                if (j > 0) mbar_wait(smem_u32(&bars[STAGES + s]), (j - 1) & 1);
+                const uint32_t full = smem_u32(&bars[s]);
+                mbar_expect_tx(full, bytes);
+                const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+                const int y = (int)(r0 + (int64_t)kb * KB);
+                for (int c = 0; c < 4; ++c) {
+                    tma_load_2d(base + 0 * OPER + c * SLAB, &map_hi, full, ta * TILE + 32 * c, y);
+                    tma_load_2d(base + 1 * OPER + c * SLAB, &map_lo, full, ta * TILE + 32 * c, y);
+                    if (!diag) {
+                        tma_load_2d(base + 2 * OPER + c * SLAB, &map_hi, full, tb * TILE + 32 * c, y);
+                        tma_load_2d(base + 3 * OPER + c * SLAB, &map_lo, full, tb * TILE + 32 * c, y);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = idesc_tf32(TILE, TILE);
+        for (int seg = 0; seg < nseg; ++seg) {
+            const int buf = seg & 1, use = seg >> 1;
+            if (use > 0) mbar_wait(smem_u32(&bars[2 * STAGES + 2 + buf]), (use - 1) & 1);
+            fence_after();
+            const uint32_t tmem_d = tmem_base + buf * TILE;
+            const int kb0 = seg * SEG, kb1 = min(nkb, kb0 + SEG);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                const int s = kb % STAGES, j = kb / STAGES;
+                mbar_wait(smem_u32(&bars[s]), j & 1);
+                fence_after();
+                if (lane == 0) {
+                    const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+                    const uint32_t ahi = base, alo = base + OPER;
+                    const uint32_t bhi = diag ? ahi : base + 2 * OPER, blo = diag ? alo : base + 3 * OPER;
+#pragma unroll
+                    for (int kk = 0; kk < KB / 8; ++kk) {
+                        const uint32_t off = kk * 1024;
+                        const uint64_t dAhi = umma_desc(ahi + off, SLAB, 1024);
+                        const uint64_t dAlo = umma_desc(alo + off, SLAB, 1024);
+                        const uint64_t dBhi = umma_desc(bhi + off, SLAB, 1024);
+                        const uint64_t dBlo = umma_desc(blo + off, SLAB, 1024);
+                        const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
+                        mma_tf32(tmem_d, dAlo, dBhi, idesc, first);
+                        mma_tf32(tmem_d, dAhi, dBlo, idesc, 1u);
+                        mma_tf32(tmem_d, dAhi, dBhi, idesc, 1u);
+                    }
+                    mma_commit(smem_u32(&bars[STAGES + s]));          // frees the smem stage
+                    if (kb == kb1 - 1) mma_commit(smem_u32(&bars[2 * STAGES + buf]));   // segment done
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- epilogue: TMEM -> fp64 registers ----------------
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        double acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+        for (int seg = 0; seg < nseg; ++seg) {
+            const int buf = seg & 1, use = seg >> 1;
+            mbar_wait(smem_u32(&bars[2 * STAGES + buf]), use & 1);
+            fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + buf * TILE + 64 * h;
+            float v[32];
+            tmem_ld32(taddr, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
+            tmem_ld32(taddr + 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[32 + i] += (double)v[i];
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars[2 * STAGES + 2 + buf]));
+        }
+        double *out = g.part + (((int64_t)split * pairs + pidx) * TILE + (32 * q + lane)) * TILE + 64 * h;
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) *reinterpret_cast<double2 *>(out + i) = make_double2(acc[i], acc[i + 1]);
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// G[a][b] = sum_s part[s][pair(min tile, max tile)][..]; lower triangle mirrored from the upper.
+__global__ void gram_reduce_kernel(const double *__restrict__ part, int D, int T, int ksplit, double *__restrict__ G) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)D * D) return;
+    int a = (int)(i / D), b = (int)(i - (int64_t)a * D);
+    if (a > b) { const int t = a; a = b; b = t; }
+    const int ta = a / TILE, tb = b / TILE;
+    const int pidx = ta * T - ta * (ta - 1) / 2 + (tb - ta);
+    const int64_t pairs = (int64_t)T * (T + 1) / 2;
+    const int64_t off = ((int64_t)pidx * TILE + (a - ta * TILE)) * TILE + (b - tb * TILE);
+    double s = 0.0;
+    for (int k = 0; k < ksplit; ++k) s += part[k * pairs * TILE * TILE + off];
+    G[i] = s;
+}
+
+// R_hi = rna-tf32(dinv . R'), R_lo = dinv . R' - R_hi   (fp32 bit patterns)
+__global__ void split_tf32_kernel(const float4 *__restrict__ Rp, const float *__restrict__ dinv, int64_t n, int D4,
+                                  float4 *__restrict__ hi, float4 *__restrict__ lo) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * D4) return;
+    const float s = dinv[i / D4];
+    const float4 x = Rp[i];
+    float v[4] = {x.x * s, x.y * s, x.z * s, x.w * s}, h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint32_t t;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v[j]));
+        h[j] = __uint_as_float(t);
+        l[j] = v[j] - h[j];
+    }
+    hi[i] = make_float4(h[0], h[1], h[2], h[3]);
+    lo[i] = make_float4(l[0], l[1], l[2], l[3]);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw Error(TPO_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+    return fn;
+}
+
+CUtensorMap make_map(const float *base, int64_t n, int64_t D) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)D * sizeof(float)};
+    const cuuint32_t box[2] = {32, KB};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(TPO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+struct GramPlan {
+    int T, pairs, ksplit;
+    int64_t rows_per;
+};
+
+GramPlan plan(int64_t n, int64_t D) {
+    GramPlan p;
+    p.T = (int)cdiv(D, TILE);
+    p.pairs = p.T * (p.T + 1) / 2;
+    const int64_t kblocks = std::max<int64_t>(1, cdiv(n, KB));
+    int64_t ks = std::max<int64_t>(1, 148 / p.pairs);
+    ks = std::min<int64_t>(ks, kblocks);
+    p.rows_per = cdiv(kblocks, ks) * KB;
+    p.ksplit = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(n, 1), p.rows_per));
+    return p;
+}
+
+}  // namespace
+
+size_t gram_tc_ws(int64_t n, int64_t D) {
+    const GramPlan p = plan(n, D);
+    return 2 * align_up(sizeof(float) * n * D) + align_up(sizeof(double) * p.ksplit * p.pairs * TILE * TILE) + 1024;
+}
+
+// G (D x D fp64, device) = R'^T diag(dinv^2) R'.  Requires D % 4 == 0 (TMA row pitch).
+void gram_tc(const float *Rp, const float *dinv, int64_t n, int64_t D, double *G, Arena &ar, cudaStream_t st) {
+    const GramPlan p = plan(n, D);
+    float *hi = ar.take<float>(n * D), *lo = ar.take<float>(n * D);
+    double *part = ar.take<double>((size_t)p.ksplit * p.pairs * TILE * TILE);
+    split_tf32_kernel<<<cdiv(n * (D / 4), 256), 256, 0, st>>>((const float4 *)Rp, dinv, n, (int)(D / 4),
+                                                            (float4 *)hi, (float4 *)lo);
+    TPO_LAUNCH_CHECK();
+    const CUtensorMap mh = make_map(hi, n, D), ml = make_map(lo, n, D);
+    const size_t smem = STAGES * STAGE_BYTES + 1024 + 256;
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    GramArgs a{p.T, p.ksplit, p.rows_per, n, part};
+    gram_tc_kernel<<<p.pairs * p.ksplit, NTHREADS, smem, st>>>(mh, ml, a);
+    TPO_LAUNCH_CHECK();
+    gram_reduce_kernel<<<cdiv(D * D, 256), 256, 0, st>>>(part, (int)D, p.T, p.ksplit, G);
+    TPO_LAUNCH_CHECK();
+}
+
+}  // namespace tpo

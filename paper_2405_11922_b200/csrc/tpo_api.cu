@@ -154,6 +154,21 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
     });
 }
 
+size_t tpo_gram_ws(int64_t n, int64_t D) { return gram_tc_ws(n, D) + 1024; }
+
+int tpo_gram(const float *Rp, const float *dinv, int64_t n, int64_t D, double *G, void *ws, size_t ws_bytes,
+             void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && D >= 4 && D % 4 == 0, "need n >= 1 and D a positive multiple of 4");
+        check_ptr(Rp, "Rp");
+        check_ptr(dinv, "dinv");
+        check_ptr(G, "G");
+        check_ws(ws, ws_bytes, tpo_gram_ws(n, D));
+        Arena ar(ws, ws_bytes);
+        gram_tc(Rp, dinv, n, D, G, ar, as_stream(stream));
+    });
+}
+
 size_t tpo_topk_eig_ws(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p) {
     return topk_eig_ws_bytes(n, D, k, mode, p);
 }

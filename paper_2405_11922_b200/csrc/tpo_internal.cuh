@@ -125,9 +125,9 @@ void tsgemm_AW_f64(const float *A, int64_t lda, const float *rs, const double *W
 void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int64_t p, int64_t q, double *out,
                   int64_t ldo, cudaStream_t st);
 // Symmetric Gram G = sum_i w_i^2 A[i]^T A[i] (D x D fp64, full matrix written).
-void gram_weighted(const float *A, const float *w, int64_t n, int64_t D, double *G, Arena &ar,
-                   cudaStream_t st);
-size_t gram_ws(int64_t n, int64_t D);
+// tcgen05 3xTF32 Gram with fp64 segment accumulation (gram_tc.cu).
+void gram_tc(const float *Rp, const float *dinv, int64_t n, int64_t D, double *G, Arena &ar, cudaStream_t st);
+size_t gram_tc_ws(int64_t n, int64_t D);
 size_t tsgemm_ws(int64_t n, int64_t p, int64_t q);
 
 // ----------------------------------------------------------------------------------------

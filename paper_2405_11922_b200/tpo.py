@@ -144,6 +144,18 @@ def affinity_matvec(Rp: torch.Tensor, dinv: torch.Tensor, Y: torch.Tensor, out=N
     return out
 
 
+def gram(Rp: torch.Tensor, dinv: torch.Tensor, stream=None) -> torch.Tensor:
+    """a7 step 1 (tpo_gram): G = R'^T diag(dinv^2) R' as a D x D fp64 tensor."""
+    n, D = Rp.shape
+    _need(Rp, torch.float32, "Rp")
+    _need(dinv, torch.float32, "dinv", (n,))
+    G = torch.empty((D, D), dtype=torch.float64, device=Rp.device)
+    L = lib()
+    ws = _ws(L.tpo_gram_ws(n, D), Rp.device)
+    check(L.tpo_gram(_ptr(Rp), _ptr(dinv), n, D, _ptr(G), _ptr(ws), ws.numel(), _stream(stream)))
+    return G
+
+
 def topk_eig(Rp: torch.Tensor, dinv: torch.Tensor, k: int, mode: int = TPO_EIG_EXACT, p: int = 10, q: int = 2,
              Omega: Optional[torch.Tensor] = None, stream=None):
     """a7 (tpo_topk_eig): returns (Gamma [n,k] fp32, sigma np.float64[k], Psi [D,k] fp32)."""

@@ -178,6 +178,22 @@ def tiny_feats():
     return g, Rp, dinv
 
 
+@pytest.mark.parametrize("n,D", [(2000, 600), (777, 136), (5003, 256), (40, 8)])
+def test_gram_tcgen05(tpo, n, D):
+    """tcgen05 3xTF32 Gram vs the oracle's fp64 Gram (ragged row / column tails, diagonal and
+    off-diagonal 128 x 128 tiles, several row splits)."""
+    Zh = random_unit_rows(n, D // 2, seed=n)
+    Q = O.haar_q(np.random.default_rng(D).standard_normal((D // 2, D // 2))).astype(np.float32)
+    Rp, dinv, _ = O.features(Zh, Q)
+    Rp, dinv = Rp.astype(np.float32), dinv.astype(np.float32)
+    Go = O.gram(Rp, dinv)
+    G = tpo.gram(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda()).cpu().numpy()
+    assert np.array_equal(G, G.T)
+    assert np.max(np.abs(G - Go)) <= 2e-6 * np.max(np.abs(Go))
+    G2 = tpo.gram(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda()).cpu().numpy()
+    assert np.array_equal(G, G2)
+
+
 def test_affinity_matvec(tpo, tiny_feats):
     g, Rp, dinv = tiny_feats
     Y = np.random.default_rng(1).standard_normal((g.n, 15)).astype(np.float32)
