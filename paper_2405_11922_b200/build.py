@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(log)
     if force or _stale(OUT, objs):
         tmp = OUT + f".{os.getpid()}.tmp"
-        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread",
+                                                               "-Xlinker", "--no-undefined"]
         subprocess.check_call(cmd)
         os.replace(tmp, OUT)
     return OUT

@@ -4,8 +4,8 @@
 // stored fp32), then each 128 x 128 upper-triangular output tile accumulates
 //      R_lo^T R_hi + R_hi^T R_lo + R_hi^T R_hi          ("3xTF32", fp32-accurate products)
 // with tcgen05.mma kind::tf32 (both operands MN-major straight out of row-major R, staged by
-// TMA with 128-byte swizzle), fp32 accumulators in TMEM.  Every SEG k-blocks (256 rows) the
-// accumulator is drained by 8 epilogue warps into fp64 registers (double-buffered TMEM, so
+// TMA with the 128-byte / 32-byte-atom swizzle), fp32 accumulators in TMEM.  Every SEG k-blocks (128 rows) the
+// accumulator (every SEG k-blocks = 128 rows) is drained by 8 epilogue warps into fp64 registers (double-buffered TMEM, so
 // the MMAs of the next segment overlap the drain), and the fp64 tile partials of the row
 // splits are summed in split order by a second kernel (deterministic, no atomics).
 //
@@ -25,7 +25,7 @@ namespace {
 constexpr int TILE = 128;          // output tile (M = N = 128)
 constexpr int KB = 32;             // rows per k-block (4 MMAs of K = 8)
 constexpr int STAGES = 3;
-constexpr int SEG = 8;             // k-blocks per fp32 accumulation segment (256 rows)
+constexpr int SEG = 4;             // k-blocks per fp32 accumulation segment (128 rows)
 constexpr int SLAB = 32 * KB * 4;  // one 32-column x 32-row fp32 slab (4 KB)
 constexpr int OPER = 4 * SLAB;     // one 128-column operand tile (16 KB)
 constexpr int STAGE_BYTES = 4 * OPER;   // A_hi, A_lo, B_hi, B_lo
@@ -66,15 +66,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-// UMMA shared-memory descriptor: MN-major operand, 128-byte swizzle; LBO = byte stride between
-// 32-element (128 B) MN slabs, SBO = byte stride between 8-row K groups; version 1 (sm_100).
+// UMMA shared-memory descriptor for a 32-bit MN-major operand.  32-bit MN-major operands use the
+// "128-byte swizzle with 32-byte atomicity" layout (descriptor layout type 1, TMA mode
+// SWIZZLE_128B_ATOM_32B): 128-byte rows, 32-byte chunks XOR-swizzled over 4-row atoms.
+// LBO = byte stride between 32-element (128 B) MN slabs, SBO = byte stride between 4-row K
+// atoms (512 B); version 1 (sm_100).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = 0;
     d |= (uint64_t)((addr & 0x3FFFF) >> 4);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
+    d |= (uint64_t)1 << 61;     // SWIZZLE_128B_BASE32B
     return d;
 }
 
@@ -112,6 +115,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ float *g_gram_dbg = nullptr;   // debug dump (set by tpo__gram_debug), normally null
 
 struct GramArgs {
     int n_tiles;        // T = ceil(D / 128)
@@ -206,6 +211,12 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant
                 const int s = kb % STAGES, j = kb / STAGES;
                 mbar_wait(smem_u32(&bars[s]), j & 1);
                 fence_after();
+                if (g_gram_dbg && blockIdx.x == 0 && kb == 0) {
+                    const float *st0 = reinterpret_cast<const float *>(smem);
+                    g_gram_dbg[lane] = st0[lane];
+                    g_gram_dbg[32 + lane] = st0[OPER / 4 + lane];
+                    g_gram_dbg[64 + lane] = st0[32 + lane];
+                }
                 if (lane == 0) {
                     const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
                     const uint32_t ahi = base, alo = base + OPER;
@@ -213,10 +224,10 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant
 #pragma unroll
                     for (int kk = 0; kk < KB / 8; ++kk) {
                         const uint32_t off = kk * 1024;
-                        const uint64_t dAhi = umma_desc(ahi + off, SLAB, 1024);
-                        const uint64_t dAlo = umma_desc(alo + off, SLAB, 1024);
-                        const uint64_t dBhi = umma_desc(bhi + off, SLAB, 1024);
-                        const uint64_t dBlo = umma_desc(blo + off, SLAB, 1024);
+                        const uint64_t dAhi = umma_desc(ahi + off, SLAB, 512);
+                        const uint64_t dAlo = umma_desc(alo + off, SLAB, 512);
+                        const uint64_t dBhi = umma_desc(bhi + off, SLAB, 512);
+                        const uint64_t dBlo = umma_desc(blo + off, SLAB, 512);
                         const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
                         mma_tf32(tmem_d, dAlo, dBhi, idesc, first);
                         mma_tf32(tmem_d, dAhi, dBlo, idesc, 1u);
@@ -241,6 +252,13 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant
             const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + buf * TILE + 64 * h;
             float v[32];
             tmem_ld32(taddr, v);
+            if (g_gram_dbg && blockIdx.x == 0 && seg == 0 && warp == 2 && lane == 0)
+                for (int i = 0; i < 32; ++i) g_gram_dbg[96 + i] = v[i];
+            if (g_gram_dbg && blockIdx.x == 0 && seg == 0 && warp == 2 && lane == 0) {
+                g_gram_dbg[128] = __uint_as_float(tmem_base);
+                g_gram_dbg[129] = (float)nkb;
+                g_gram_dbg[130] = (float)nseg;
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
             tmem_ld32(taddr + 32, v);
@@ -322,7 +340,7 @@ CUtensorMap make_map(const float *base, int64_t n, int64_t D) {
     const cuuint32_t box[2] = {32, KB};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(TPO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return m;
@@ -346,6 +364,8 @@ GramPlan plan(int64_t n, int64_t D) {
 }
 
 }  // namespace
+
+void gram_debug_set(float *p) { TPO_CUDA(cudaMemcpyToSymbol(g_gram_dbg, &p, sizeof(p))); }
 
 size_t gram_tc_ws(int64_t n, int64_t D) {
     const GramPlan p = plan(n, D);

@@ -11,6 +11,7 @@ namespace tpo {
 
 size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d);
 size_t features_ws_bytes(int64_t n, int64_t d);
+void gram_debug_set(float *p);
 size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p);
 size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k);
 
@@ -153,6 +154,9 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
         affinity_matvec_impl(Rp, dinv, n, D, Y, b, out, ar, as_stream(stream));
     });
 }
+
+// undocumented debugging hook (not part of include/tpo.h)
+int tpo__gram_debug(float *p) { return guarded([&] { tpo::gram_debug_set(p); }); }
 
 size_t tpo_gram_ws(int64_t n, int64_t D) { return gram_tc_ws(n, D) + 1024; }
 
