@@ -148,20 +148,26 @@ __global__ void cluster_sums_kernel(const double *__restrict__ U, const int32_t 
     for (int i = threadIdx.x; i < k; i += blockDim.x) cpart[blockIdx.x * (int64_t)k + i] = cnt[i];
 }
 
-// Phi[a,l] = (sum_b part[b][l][a]) / sqrt(count_l)   (zero column for an empty cluster)
+// Phi[a,l] = (sum_b part[b][l][a]) / sqrt(count_l)   (zero column for an empty cluster);
+// one warp per entry, lanes stride the blocks, fixed shuffle tree.
 __global__ void phi_kernel(const double *__restrict__ part, const int64_t *__restrict__ cpart, int64_t nb, int k,
                            double *__restrict__ Phi, const int32_t *__restrict__ done) {
     if (*done) return;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= k * k) return;
-    const int l = i / k, a = i - l * k;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= (int64_t)k * k) return;
+    const int l = (int)(wid / k), a = (int)(wid - (int64_t)l * k);
     double s = 0.0;
     int64_t c = 0;
-    for (int64_t b = 0; b < nb; ++b) {
+    for (int64_t b = lane; b < nb; b += 32) {
         s += part[b * (int64_t)k * k + (int64_t)l * k + a];
         c += cpart[b * (int64_t)k + l];
     }
-    Phi[(int64_t)a * k + l] = c > 0 ? s / sqrt((double)c) : 0.0;
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) Phi[(int64_t)a * k + l] = c > 0 ? s / sqrt((double)c) : 0.0;
 }
 
 __global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
@@ -249,7 +255,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         if (t == Tg - 1) break;                       // the last Phi update is never used
         cluster_sums_kernel<<<nb, sum_threads, sum_smem, st>>>(U, labels, n, k, rpb, part, cpart, s.done);
         TPO_LAUNCH_CHECK();
-        phi_kernel<<<cdiv(k * k, 256), 256, 0, st>>>(part, cpart, nb, k, Phi, s.done);
+        phi_kernel<<<cdiv((int64_t)k * k * 32, 256), 256, 0, st>>>(part, cpart, nb, k, Phi, s.done);
         TPO_LAUNCH_CHECK();
     }
     int32_t it = 0;

@@ -1,14 +1,17 @@
 // Tall-skinny dense products of the solver (a6-a8) with fp64 accumulation and a fixed-order
-// cross-block reduction (no atomics): the products R'^T Y, Y^T Y, R' W of the implicit
-// affinity (never form the n x n matrix) and of Alg. 2.
+// cross-block reduction (no atomics): R'^T Y, Y^T Y and R' W of the implicit affinity
+// (the n x n matrix is never formed) and of Alg. 2, whose right-hand sides
+// have q = k or b <= a few hundred columns.
 //
-//   atb:  out[p x q] = sum_i (ra_i A[i,:])^T (rb_i B[i,:])   rows split over a grid of
-//         row groups; each block accumulates its rows in registers (fp64), writes one
-//         partial, and a reduction kernel adds the partials in group order.
-//   aw:   out[i, :] = r_i A[i, :] W                            (row tiles x column tiles)
-//
-// Both use a 64 x 64 output tile per 256-thread block, a 4 x 4 register micro-tile per
-// thread, and a 16-deep smem k-slab.  Operands are widened to fp64 when staged.
+//   atb:  out[p x q] = sum_i (ra_i A[i,:])^T (rb_i B[i,:])
+//         Thread owns TA columns of A (coalesced global loads) and a QT-wide chunk of B
+//         (staged in smem, read as broadcasts); rows are split over a grid of row groups and
+//         each block writes one fp64 partial that reduce_groups_kernel adds in group order.
+//   aw:   out[i, :] = r_i A[i, :] W
+//         A warp owns RW = 4 rows and a QT-wide chunk of W; lanes stride the reduction
+//         dimension (coalesced loads of A), W is staged transposed in smem, and the lane
+//         partials are combined by a fixed shuffle tree.
+// Operands are widened to fp64 before multiplying.
 #include <algorithm>
 
 #include "tpo_internal.cuh"
@@ -16,68 +19,80 @@
 namespace tpo {
 namespace {
 
-constexpr int TM = 64, TK = 16, NT = 256;
+constexpr int NT = 256;
+constexpr int TA = 2;          // A columns per thread in atb
+constexpr int PT = NT * TA;    // A columns per block in atb
+constexpr int QT = 16;         // q chunk (both kernels)
+constexpr int RC = 32;         // rows per smem chunk in atb
+constexpr int RW = 4;          // rows per warp in aw
+constexpr int JT = 128;        // reduction-dimension tile in aw
 
 template <class T>
-__device__ __forceinline__ double ld_wide(const T *p) { return (double)(*p); }
+__device__ __forceinline__ double wide(T x) { return (double)x; }
 
 // ----------------------------------------------------------------------------------------
-// atb: partial[g][a][b] = sum over rows i in group g of (ra_i A[i,a]) (rb_i B[i,b])
+// atb
 // ----------------------------------------------------------------------------------------
-template <class TA, class TB>
-__global__ void __launch_bounds__(NT) atb_kernel(const TA *__restrict__ A, int64_t lda, const float *__restrict__ ra,
-                                                 const TB *__restrict__ B, int64_t ldb, const float *__restrict__ rb,
+template <class TAt, class TBt>
+__global__ void __launch_bounds__(NT) atb_kernel(const TAt *__restrict__ A, int64_t lda, const float *__restrict__ ra,
+                                                 const TBt *__restrict__ B, int64_t ldb, const float *__restrict__ rb,
                                                  int64_t n, int p, int q, int64_t rows_per_group,
                                                  double *__restrict__ part) {
-    __shared__ double As[TK][TM];
-    __shared__ double Bs[TK][TM];
-    const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
-    const int a0 = blockIdx.x * TM, b0 = blockIdx.y * TM;
+    __shared__ __align__(16) double Bs[RC][QT];
+    __shared__ double Sa[RC];
+    const int t = threadIdx.x;
+    const int a0 = blockIdx.x * PT, b0 = blockIdx.y * QT;
     const int64_t g = blockIdx.z;
     const int64_t r_beg = g * rows_per_group, r_end = min(n, r_beg + rows_per_group);
-    double acc[4][4];
+    double acc[TA][QT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TA; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    // staging: 16 rows x 64 cols per operand = 1024 values, 4 per thread
-    const int lr = t >> 4, lc = (t & 15) * 4;
-    for (int64_t r0 = r_beg; r0 < r_end; r0 += TK) {
-        const int64_t row = r0 + lr;
-        const bool rv = row < r_end;
-        const double sa = (rv && ra) ? (double)ra[row] : 1.0;
-        const double sb = (rv && rb) ? (double)rb[row] : 1.0;
+        for (int j = 0; j < QT; ++j) acc[i][j] = 0.0;
+    int col[TA];
+    bool cv[TA];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int ca = a0 + lc + c, cb = b0 + lc + c;
-            As[lr][lc + c] = (rv && ca < p) ? sa * ld_wide(A + row * lda + ca) : 0.0;
-            Bs[lr][lc + c] = (rv && cb < q) ? sb * ld_wide(B + row * ldb + cb) : 0.0;
+    for (int i = 0; i < TA; ++i) {
+        col[i] = a0 + t + NT * i;
+        cv[i] = col[i] < p;
+    }
+    for (int64_t r0 = r_beg; r0 < r_end; r0 += RC) {
+        const int rows = (int)(r_end - r0 < RC ? r_end - r0 : RC);
+        for (int e = t; e < RC * QT; e += NT) {
+            const int r = e / QT, c = e - r * QT;
+            double v = 0.0;
+            if (r < rows && b0 + c < q) {
+                v = wide(B[(r0 + r) * ldb + b0 + c]);
+                if (rb) v *= (double)rb[r0 + r];
+            }
+            Bs[r][c] = v;
         }
+        if (t < RC) Sa[t] = (t < rows) ? (ra ? (double)ra[r0 + t] : 1.0) : 0.0;
         __syncthreads();
+#pragma unroll 4
+        for (int r = 0; r < rows; ++r) {
+            double av[TA];
 #pragma unroll
-        for (int r = 0; r < TK; ++r) {
-            double av[4], bv[4];
+            for (int i = 0; i < TA; ++i) av[i] = cv[i] ? Sa[r] * wide(A[(r0 + r) * lda + col[i]]) : 0.0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[r][i * 16 + ty];
+            for (int j = 0; j < QT; j += 2) {
+                const double2 bv = *reinterpret_cast<const double2 *>(&Bs[r][j]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bs[r][j * 16 + tx];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+                for (int i = 0; i < TA; ++i) {
+                    acc[i][j] = fma(av[i], bv.x, acc[i][j]);
+                    acc[i][j + 1] = fma(av[i], bv.y, acc[i][j + 1]);
+                }
+            }
         }
         __syncthreads();
     }
     double *out = part + g * (int64_t)p * q;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int a = a0 + i * 16 + ty;
-        if (a >= p) continue;
+    for (int i = 0; i < TA; ++i) {
+        if (!cv[i]) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int b = b0 + j * 16 + tx;
-            if (b < q) out[(int64_t)a * q + b] = acc[i][j];
-        }
+        for (int j = 0; j < QT; ++j)
+            if (b0 + j < q) out[(int64_t)col[i] * q + b0 + j] = acc[i][j];
     }
 }
 
@@ -90,62 +105,66 @@ __global__ void reduce_groups_kernel(const double *__restrict__ part, int64_t G,
 }
 
 // ----------------------------------------------------------------------------------------
-// aw: out[i, b] = r_i sum_a A[i, a] W[a, b]    (A n x p, W p x q fp64)
+// aw
 // ----------------------------------------------------------------------------------------
-template <class TA, class TO>
-__global__ void __launch_bounds__(NT) aw_kernel(const TA *__restrict__ A, int64_t lda, const float *__restrict__ rs,
+template <class TAt, class TO>
+__global__ void __launch_bounds__(NT) aw_kernel(const TAt *__restrict__ A, int64_t lda, const float *__restrict__ rs,
                                                 const double *__restrict__ W, int64_t n, int p, int q,
                                                 TO *__restrict__ out, int64_t ldo) {
-    __shared__ double As[TK][TM];   // As[kk][row]
-    __shared__ double Ws[TK][TM];   // Ws[kk][col]
-    const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
-    const int64_t i0 = (int64_t)blockIdx.x * TM;
-    const int b0 = blockIdx.y * TM;
-    double acc[4][4];
+    __shared__ double Ws[QT][JT + 1];   // transposed W tile: Ws[c][j]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t row0 = ((int64_t)blockIdx.x * (NT / 32) + w) * RW;
+    const int b0 = blockIdx.y * QT;
+    double acc[RW][QT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int r = 0; r < RW; ++r)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    // A staging: 64 rows x 16 k: thread loads row (t >> 2), k (t & 3) * 4 .. +3
-    const int ar = t >> 2, ak = (t & 3) * 4;
-    // W staging: 16 k x 64 cols: thread loads k (t >> 4), cols (t & 15) * 4 .. +3
-    const int wk = t >> 4, wc = (t & 15) * 4;
-    for (int k0 = 0; k0 < p; k0 += TK) {
-        const int64_t row = i0 + ar;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int kk = k0 + ak + c;
-            As[ak + c][ar] = (row < n && kk < p) ? ld_wide(A + row * lda + kk) : 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int kk = k0 + wk, col = b0 + wc + c;
-            Ws[wk][wc + c] = (kk < p && col < q) ? W[(int64_t)kk * q + col] : 0.0;
+        for (int c = 0; c < QT; ++c) acc[r][c] = 0.0;
+    for (int j0 = 0; j0 < p; j0 += JT) {
+        for (int e = threadIdx.x; e < QT * JT; e += NT) {
+            const int c = e / JT, j = e - c * JT;
+            Ws[c][j] = (j0 + j < p && b0 + c < q) ? W[(int64_t)(j0 + j) * q + b0 + c] : 0.0;
         }
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < TK; ++r) {
-            double av[4], bv[4];
+        for (int jj = 0; jj < JT / 32; ++jj) {
+            const int j = jj * 32 + lane;
+            double av[RW];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[r][i * 16 + ty];
+            for (int r = 0; r < RW; ++r) {
+                const int64_t row = row0 + r;
+                av[r] = (row < n && j0 + j < p) ? wide(A[row * lda + j0 + j]) : 0.0;
+            }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Ws[r][j * 16 + tx];
+            for (int c = 0; c < QT; ++c) {
+                const double wv = Ws[c][j];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+                for (int r = 0; r < RW; ++r) acc[r][c] = fma(av[r], wv, acc[r][c]);
+            }
         }
         __syncthreads();
     }
+    // fixed shuffle tree over the lanes
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t row = i0 + i * 16 + ty;
-        if (row >= n) continue;
-        const double s = rs ? (double)rs[row] : 1.0;
+    for (int r = 0; r < RW; ++r)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int b = b0 + j * 16 + tx;
-            if (b < q) out[row * ldo + b] = (TO)(s * acc[i][j]);
+        for (int c = 0; c < QT; ++c) {
+            double v = acc[r][c];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc[r][c] = v;
+        }
+    if (lane < QT) {
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            const int64_t row = row0 + r;
+            if (row >= n || b0 + lane >= q) continue;
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < QT; ++c)
+                if (c == lane) v = acc[r][c];
+            const double s = rs ? (double)rs[row] : 1.0;
+            out[row * ldo + b0 + lane] = (TO)(s * v);
         }
     }
 }
@@ -154,31 +173,42 @@ __global__ void __launch_bounds__(NT) aw_kernel(const TA *__restrict__ A, int64_
 // total (a fixed constant, so workspace queries need no device).
 constexpr int64_t kBlocksTarget = 4 * 148;
 int64_t atb_rows_per_group(int64_t n, int64_t p, int64_t q) {
-    const int64_t tiles = cdiv(p, TM) * cdiv(q, TM);
+    const int64_t tiles = cdiv(p, PT) * cdiv(q, QT);
     const int64_t want = std::max<int64_t>(1, cdiv(kBlocksTarget, tiles));
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(want, cdiv(n, 4 * TK)));
-    return cdiv(cdiv(std::max<int64_t>(n, 1), G), TK) * TK;
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(want, cdiv(std::max<int64_t>(n, 1), 4 * RC)));
+    return cdiv(cdiv(std::max<int64_t>(n, 1), G), RC) * RC;
 }
 
-template <class TA, class TB>
-void atb_run(const TA *A, int64_t lda, const float *ra, const TB *B, int64_t ldb, const float *rb, int64_t n,
+template <class TAt, class TBt>
+void atb_run(const TAt *A, int64_t lda, const float *ra, const TBt *B, int64_t ldb, const float *rb, int64_t n,
              int64_t p, int64_t q, double *out, Arena &ar, cudaStream_t st) {
-    const int64_t tp = cdiv(p, TM), tq = cdiv(q, TM);
-    const int64_t rpg = atb_rows_per_group(n, p, q);
-    const int64_t Gr = std::max<int64_t>(1, cdiv(n, rpg));
     if (n == 0) {
         TPO_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * p * q, st));
         return;
     }
+    const int64_t rpg = atb_rows_per_group(n, p, q);
+    const int64_t Gr = std::max<int64_t>(1, cdiv(n, rpg));
+    const dim3 grid(cdiv(p, PT), cdiv(q, QT), Gr);
     if (Gr == 1) {
-        atb_kernel<TA, TB><<<dim3(tp, tq, 1), NT, 0, st>>>(A, lda, ra, B, ldb, rb, n, (int)p, (int)q, rpg, out);
+        atb_kernel<TAt, TBt><<<grid, NT, 0, st>>>(A, lda, ra, B, ldb, rb, n, (int)p, (int)q, rpg, out);
         TPO_LAUNCH_CHECK();
         return;
     }
+    const size_t mark = ar.off;
     double *part = ar.take<double>(Gr * p * q);
-    atb_kernel<TA, TB><<<dim3(tp, tq, Gr), NT, 0, st>>>(A, lda, ra, B, ldb, rb, n, (int)p, (int)q, rpg, part);
+    atb_kernel<TAt, TBt><<<grid, NT, 0, st>>>(A, lda, ra, B, ldb, rb, n, (int)p, (int)q, rpg, part);
     TPO_LAUNCH_CHECK();
     reduce_groups_kernel<<<cdiv(p * q, 256), 256, 0, st>>>(part, Gr, p * q, out);
+    TPO_LAUNCH_CHECK();
+    ar.off = mark;
+}
+
+template <class TAt, class TO>
+void aw_run(const TAt *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q, TO *out,
+            int64_t ldo, cudaStream_t st) {
+    if (n == 0 || q == 0) return;
+    const dim3 grid(cdiv(n, (NT / 32) * RW), cdiv(q, QT));
+    aw_kernel<TAt, TO><<<grid, NT, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
     TPO_LAUNCH_CHECK();
 }
 
@@ -204,23 +234,15 @@ void tsgemm_AtB_f64f64(const double *A, int64_t lda, const double *Bm, int64_t l
 
 void tsgemm_AW_f32(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q,
                    float *out, int64_t ldo, cudaStream_t st) {
-    if (n == 0) return;
-    aw_kernel<float, float><<<dim3(cdiv(n, TM), cdiv(q, TM)), NT, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
-    TPO_LAUNCH_CHECK();
+    aw_run<float, float>(A, lda, rs, W, n, p, q, out, ldo, st);
 }
 void tsgemm_AW_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q,
                    double *out, int64_t ldo, cudaStream_t st) {
-    if (n == 0) return;
-    aw_kernel<float, double><<<dim3(cdiv(n, TM), cdiv(q, TM)), NT, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
-    TPO_LAUNCH_CHECK();
+    aw_run<float, double>(A, lda, rs, W, n, p, q, out, ldo, st);
 }
-// fp64 A (used on the D x D Gram inside the subspace iteration)
 void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int64_t p, int64_t q, double *out,
                   int64_t ldo, cudaStream_t st) {
-    if (n == 0) return;
-    aw_kernel<double, double><<<dim3(cdiv(n, TM), cdiv(q, TM)), NT, 0, st>>>(A, lda, nullptr, W, n, (int)p, (int)q, out, ldo);
-    TPO_LAUNCH_CHECK();
+    aw_run<double, double>(A, lda, nullptr, W, n, p, q, out, ldo, st);
 }
-
 
 }  // namespace tpo

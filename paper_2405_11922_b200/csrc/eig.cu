@@ -125,7 +125,11 @@ void gram_topk(const double *G, int64_t D, int32_t k, std::vector<double> &lam, 
     double lam1 = 0.0;
     std::vector<double> H, WtW, E(b * b), w(b);
     for (int it = 0; it < max_it; ++it) {
-        tsgemm_AW_dd(G, D, V, D, D, b, W, b, st);                 // W = G V
+        {   // W = G V = G^T V (G symmetric): rows of G split over the grid
+            const size_t m2 = ar.off;
+            tsgemm_AtB_f64f64(G, D, V, b, D, D, b, W, ar, st);
+            ar.off = m2;
+        }
         const bool rr = (it % rr_every) == rr_every - 1 || it == max_it - 1;
         if (!rr) {
             TPO_CUDA(cudaMemcpyAsync(V, W, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
