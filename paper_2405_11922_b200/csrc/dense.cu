@@ -107,21 +107,32 @@ __global__ void reduce_groups_kernel(const double *__restrict__ part, int64_t G,
 // ----------------------------------------------------------------------------------------
 // aw
 // ----------------------------------------------------------------------------------------
-template <class TAt, class TO>
+template <class TAt, class TO, int QW>
 __global__ void __launch_bounds__(NT) aw_kernel(const TAt *__restrict__ A, int64_t lda, const float *__restrict__ rs,
                                                 const double *__restrict__ W, int64_t n, int p, int q,
                                                 TO *__restrict__ out, int64_t ldo) {
-    __shared__ double Ws[QT][JT + 1];   // transposed W tile: Ws[c][j]
+    __shared__ double Ws[QW][JT + 1];   // transposed W tile: Ws[c][j]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t row0 = ((int64_t)blockIdx.x * (NT / 32) + w) * RW;
-    const int b0 = blockIdx.y * QT;
-    double acc[RW][QT];
+    const int b0 = blockIdx.y * QW;
+    double acc[RW][QW];
 #pragma unroll
     for (int r = 0; r < RW; ++r)
 #pragma unroll
-        for (int c = 0; c < QT; ++c) acc[r][c] = 0.0;
+        for (int c = 0; c < QW; ++c) acc[r][c] = 0.0;
     for (int j0 = 0; j0 < p; j0 += JT) {
-        for (int e = threadIdx.x; e < QT * JT; e += NT) {
+        // issue all loads of A for this tile first (RW x JT/32 per lane in flight)
+        double av[JT / 32][RW];
+#pragma unroll
+        for (int jj = 0; jj < JT / 32; ++jj) {
+            const int j = j0 + jj * 32 + lane;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const int64_t row = row0 + r;
+                av[jj][r] = (row < n && j < p) ? wide(A[row * lda + j]) : 0.0;
+            }
+        }
+        for (int e = threadIdx.x; e < QW * JT; e += NT) {
             const int c = e / JT, j = e - c * JT;
             Ws[c][j] = (j0 + j < p && b0 + c < q) ? W[(int64_t)(j0 + j) * q + b0 + c] : 0.0;
         }
@@ -129,17 +140,11 @@ __global__ void __launch_bounds__(NT) aw_kernel(const TAt *__restrict__ A, int64
 #pragma unroll
         for (int jj = 0; jj < JT / 32; ++jj) {
             const int j = jj * 32 + lane;
-            double av[RW];
 #pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                const int64_t row = row0 + r;
-                av[r] = (row < n && j0 + j < p) ? wide(A[row * lda + j0 + j]) : 0.0;
-            }
-#pragma unroll
-            for (int c = 0; c < QT; ++c) {
+            for (int c = 0; c < QW; ++c) {
                 const double wv = Ws[c][j];
 #pragma unroll
-                for (int r = 0; r < RW; ++r) acc[r][c] = fma(av[r], wv, acc[r][c]);
+                for (int r = 0; r < RW; ++r) acc[r][c] = fma(av[jj][r], wv, acc[r][c]);
             }
         }
         __syncthreads();
@@ -148,20 +153,20 @@ __global__ void __launch_bounds__(NT) aw_kernel(const TAt *__restrict__ A, int64
 #pragma unroll
     for (int r = 0; r < RW; ++r)
 #pragma unroll
-        for (int c = 0; c < QT; ++c) {
+        for (int c = 0; c < QW; ++c) {
             double v = acc[r][c];
 #pragma unroll
             for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             acc[r][c] = v;
         }
-    if (lane < QT) {
+    if (lane < QW) {
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
             const int64_t row = row0 + r;
             if (row >= n || b0 + lane >= q) continue;
             double v = 0.0;
 #pragma unroll
-            for (int c = 0; c < QT; ++c)
+            for (int c = 0; c < QW; ++c)
                 if (c == lane) v = acc[r][c];
             const double s = rs ? (double)rs[row] : 1.0;
             out[row * ldo + b0 + lane] = (TO)(s * v);
@@ -207,8 +212,13 @@ template <class TAt, class TO>
 void aw_run(const TAt *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q, TO *out,
             int64_t ldo, cudaStream_t st) {
     if (n == 0 || q == 0) return;
-    const dim3 grid(cdiv(n, (NT / 32) * RW), cdiv(q, QT));
-    aw_kernel<TAt, TO><<<grid, NT, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
+    if (q <= 8) {
+        const dim3 grid(cdiv(n, (NT / 32) * RW), cdiv(q, 8));
+        aw_kernel<TAt, TO, 8><<<grid, NT, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
+    } else {
+        const dim3 grid(cdiv(n, (NT / 32) * RW), cdiv(q, QT));
+        aw_kernel<TAt, TO, QT><<<grid, NT, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
+    }
     TPO_LAUNCH_CHECK();
 }
 

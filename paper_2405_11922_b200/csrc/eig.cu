@@ -56,6 +56,11 @@ __global__ void flip_cols_f32(float *__restrict__ A, int64_t n, int k, const int
     if (sgn[i % k] < 0) A[i] = -A[i];
 }
 
+__global__ void fill_f64(double *p, int64_t n, double v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
 __global__ void cast_f64_f32(const double *__restrict__ a, int64_t len, float *__restrict__ b) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < len) b[i] = (float)a[i];
@@ -85,16 +90,22 @@ double start_entry(uint64_t i) {
     return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
 }
 
-// CholeskyQR2 of a device fp64 matrix V (rows x b) in place (tmp: rows x b).
+// CholeskyQR2 of a device fp64 matrix V (rows x b) in place (tmp: rows x b).  Each pass
+// factors the column-equilibrated Gram S G S = C^T C (S = diag(G_ii^-1/2)), so V <- V S C^-1.
 void cholqr2_f64(double *V, double *tmp, int64_t rows, int64_t b, Arena &ar, cudaStream_t st) {
     for (int pass = 0; pass < 2; ++pass) {
         const size_t mark = ar.off;
         double *g = ar.take<double>(b * b);
         tsgemm_AtB_f64f64(V, b, V, b, rows, b, b, g, ar, st);
-        std::vector<double> gh = to_host(g, b * b, st), C(b * b), Ci(b * b);
+        std::vector<double> gh = to_host(g, b * b, st), C(b * b), Ci(b * b), sc(b);
+        for (int64_t i = 0; i < b; ++i) sc[i] = gh[i * b + i] > 0.0 ? 1.0 / sqrt(gh[i * b + i]) : 0.0;
+        for (int64_t i = 0; i < b; ++i)
+            for (int64_t j = 0; j < b; ++j) gh[i * b + j] *= sc[i] * sc[j];
         if (!host_cholesky_upper(b, gh.data(), C.data()))
             throw Error(TPO_ENUMERIC, "CholeskyQR2: Gram matrix not positive definite");
         host_upper_inverse(b, C.data(), Ci.data());
+        for (int64_t i = 0; i < b; ++i)
+            for (int64_t j = 0; j < b; ++j) Ci[i * b + j] *= sc[i];
         double *ci = to_dev(ar, Ci, st);
         tsgemm_AW_dd(V, b, ci, rows, b, b, tmp, b, st);
         TPO_CUDA(cudaMemcpyAsync(V, tmp, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, st));
@@ -103,11 +114,58 @@ void cholqr2_f64(double *V, double *tmp, int64_t rows, int64_t b, Arena &ar, cud
     }
 }
 
-// Top-k eigenpairs of the symmetric D x D device matrix G: lam (host, k), Psi64 (device D x k).
-void gram_topk(const double *G, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64, Arena &ar,
-               cudaStream_t st) {
-    const int64_t b = std::min<int64_t>(D, k + std::max<int64_t>(k, 16));
-    if (b >= D) {       // full-rank block: a single Rayleigh-Ritz step = dense eigensolve
+// Gd = G - u u^T (deflation of the trivial eigenpair, see gram_topk)
+__global__ void deflate_kernel(const double *__restrict__ G, const double *__restrict__ u, int64_t D,
+                               double *__restrict__ Gd) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= D * D) return;
+    const int64_t a = i / D, b = i - a * D;
+    Gd[i] = G[i] - u[a] * u[b];
+}
+
+// out = s1 * GY - s2 * Y1 - (Y0 ? Y0 : 0): one step of the Chebyshev three-term recurrence
+__global__ void cheb_kernel(const double *__restrict__ GY, const double *__restrict__ Y1,
+                            const double *__restrict__ Y0, int64_t len, double s1, double s2,
+                            double *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    double v = s1 * GY[i] - s2 * Y1[i];
+    if (Y0) v -= Y0[i];
+    out[i] = v;
+}
+
+// V[i, j] -= u[i] c[j]   (c = u^T V): keeps the block orthogonal to the deflated direction
+__global__ void project_out_kernel(double *__restrict__ V, const double *__restrict__ u, const double *__restrict__ c,
+                                   int64_t D, int b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= D * b) return;
+    const int64_t r = i / b;
+    V[i] -= u[r] * c[i - r * b];
+}
+
+// Z = [u | V]  (D x (b+1))
+__global__ void stack_kernel(const double *__restrict__ u, const double *__restrict__ V, int64_t D, int b,
+                             double *__restrict__ Z) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= D * (b + 1)) return;
+    const int64_t r = i / (b + 1), c = i - r * (b + 1);
+    Z[i] = c == 0 ? u[r] : V[r * b + c - 1];
+}
+
+// Top-k eigenpairs of the symmetric D x D device matrix G = R^T R: lam (host, k), Psi64
+// (device D x k).  u (device, unit norm) is the known top eigenvector r/||r|| of the trivial
+// pair lambda = 1 (G r = R'^T 1 = r, since R'[i].r = dinv_i^-2).
+//  * b + 1 >= D: one Rayleigh-Ritz step with the full basis = dense eigensolve on the host.
+//  * otherwise Chebyshev-filtered block subspace iteration (degree m) on the deflated
+//    Gd = G - u u^T with a block V (D x b) kept orthogonal to u, and after every filter a
+//    Rayleigh-Ritz step with the FULL G on span([u, V]); stop when the top-k Ritz residuals
+//    ||G z - theta z|| fall below 1e-9 theta_1.  The filter damps [0, theta_min] (theta_min
+//    = smallest Ritz value of the block) and amplifies the wanted end of the spectrum; the
+//    deflation keeps the lambda = 1 direction from swamping the block.
+void gram_topk(const double *G, const double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
+               Arena &ar, cudaStream_t st) {
+    const int64_t b = std::min<int64_t>(D - 1, k + std::max<int64_t>(k, 16));
+    if (b + 1 >= D || D <= 64) {
         std::vector<double> gh = to_host(G, D * D, st), w(D), V(D * k);
         host_sym_eig_top(D, gh.data(), k, w.data(), V.data());
         lam.assign(w.begin(), w.begin() + k);
@@ -115,59 +173,77 @@ void gram_topk(const double *G, int64_t D, int32_t k, std::vector<double> &lam, 
         TPO_CUDA(cudaStreamSynchronize(st));
         return;
     }
+    const int64_t bz = b + 1;
+    double *Gd = ar.take<double>(D * D);
+    double *V = ar.take<double>(D * b), *T = ar.take<double>(D * b);
+    double *Y0 = ar.take<double>(D * b), *Y1 = ar.take<double>(D * b), *GY = ar.take<double>(D * b);
+    double *Z = ar.take<double>(D * bz), *W = ar.take<double>(D * bz);
+    double *cvec = ar.take<double>(b);
+    deflate_kernel<<<cdiv(D * D, 256), 256, 0, st>>>(G, u, D, Gd);
+    TPO_LAUNCH_CHECK();
     std::vector<double> v0(D * b);
     for (int64_t i = 0; i < D * b; ++i) v0[i] = start_entry((uint64_t)i);
-    double *V = to_dev(ar, v0, st);
-    double *W = ar.take<double>(D * b);
-    double *T = ar.take<double>(D * b);
-    cholqr2_f64(V, T, D, b, ar, st);
-    const int max_it = 5000, rr_every = 4;
-    double lam1 = 0.0;
-    std::vector<double> H, WtW, E(b * b), w(b);
-    for (int it = 0; it < max_it; ++it) {
-        {   // W = G V = G^T V (G symmetric): rows of G split over the grid
-            const size_t m2 = ar.off;
-            tsgemm_AtB_f64f64(G, D, V, b, D, D, b, W, ar, st);
-            ar.off = m2;
-        }
-        const bool rr = (it % rr_every) == rr_every - 1 || it == max_it - 1;
-        if (!rr) {
-            TPO_CUDA(cudaMemcpyAsync(V, W, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
-            cholqr2_f64(V, T, D, b, ar, st);
-            continue;
-        }
-        const size_t mark = ar.off;
-        double *h = ar.take<double>(b * b), *ww = ar.take<double>(b * b);
-        tsgemm_AtB_f64f64(V, b, W, b, D, b, b, h, ar, st);       // H = V^T G V
-        tsgemm_AtB_f64f64(W, b, W, b, D, b, b, ww, ar, st);      // W^T W
-        H = to_host(h, b * b, st);
-        WtW = to_host(ww, b * b, st);
-        host_sym_eig_top(b, H.data(), b, w.data(), E.data());
-        lam1 = std::max(lam1, fabs(w[0]));
-        double rmax = 0.0;
-        for (int l = 0; l < k; ++l) {          // ||G v_l - lam_l v_l||^2 = e^T W^T W e - lam^2
-            double s = 0.0;
-            for (int64_t a = 0; a < b; ++a) {
-                double t = 0.0;
-                for (int64_t c = 0; c < b; ++c) t += WtW[a * b + c] * E[c * b + l];
-                s += E[a * b + l] * t;
+    TPO_CUDA(cudaMemcpyAsync(V, v0.data(), sizeof(double) * D * b, cudaMemcpyHostToDevice, st));
+    auto orth_against_u = [&]() {
+        const size_t m2 = ar.off;
+        tsgemm_AtB_f64f64(u, 1, V, b, D, 1, b, cvec, ar, st);
+        ar.off = m2;
+        project_out_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(V, u, cvec, D, (int)b);
+        TPO_LAUNCH_CHECK();
+        cholqr2_f64(V, T, D, b, ar, st);
+    };
+    orth_against_u();
+    const int m = 8, max_rounds = 60;
+    std::vector<double> w(bz), E(bz * bz);
+    double bnd = 0.0;
+    for (int round = 0; round <= max_rounds; ++round) {
+        if (round > 0) {   // Chebyshev filter p_m(Gd) V, damping [0, bnd]
+            const double c = 0.5 * bnd, e = 0.5 * bnd;
+            TPO_CUDA(cudaMemcpyAsync(Y0, V, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
+            tsgemm_AW_dd(Gd, D, Y0, D, D, b, GY, b, st);
+            cheb_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(GY, Y0, nullptr, D * b, 1.0 / e, c / e, Y1);
+            TPO_LAUNCH_CHECK();
+            for (int j = 2; j <= m; ++j) {
+                tsgemm_AW_dd(Gd, D, Y1, D, D, b, GY, b, st);
+                cheb_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(GY, Y1, Y0, D * b, 2.0 / e, 2.0 * c / e, Y0);
+                TPO_LAUNCH_CHECK();
+                std::swap(Y0, Y1);
             }
-            rmax = std::max(rmax, sqrt(std::max(s - w[l] * w[l], 0.0)));
+            TPO_CUDA(cudaMemcpyAsync(V, Y1, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
+            orth_against_u();
         }
-        double *e = to_dev(ar, E, st);
-        if (rmax <= 1e-9 * lam1 || it == max_it - 1) {
-            std::vector<double> Ek(b * k);
-            for (int64_t a = 0; a < b; ++a)
-                for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * b + l];
+        // Rayleigh-Ritz with the full G on Z = [u, V]
+        stack_kernel<<<cdiv(D * bz, 256), 256, 0, st>>>(u, V, D, (int)b, Z);
+        TPO_LAUNCH_CHECK();
+        tsgemm_AW_dd(G, D, Z, D, D, bz, W, bz, st);
+        const size_t mark = ar.off;
+        double *h = ar.take<double>(bz * bz), *ww = ar.take<double>(bz * bz);
+        tsgemm_AtB_f64f64(Z, bz, W, bz, D, bz, bz, h, ar, st);
+        tsgemm_AtB_f64f64(W, bz, W, bz, D, bz, bz, ww, ar, st);
+        std::vector<double> H = to_host(h, bz * bz, st), WtW = to_host(ww, bz * bz, st);
+        host_sym_eig_top(bz, H.data(), bz, w.data(), E.data());
+        double rmax = 0.0;
+        for (int l = 0; l < k; ++l) {          // ||G z_l - w_l z_l||^2 = e^T W^T W e - w_l^2
+            double s2 = 0.0;
+            for (int64_t a = 0; a < bz; ++a) {
+                double t = 0.0;
+                for (int64_t c = 0; c < bz; ++c) t += WtW[a * bz + c] * E[c * bz + l];
+                s2 += E[a * bz + l] * t;
+            }
+            rmax = std::max(rmax, sqrt(std::max(s2 - w[l] * w[l], 0.0)));
+        }
+        if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
+            std::vector<double> Ek(bz * k);
+            for (int64_t a = 0; a < bz; ++a)
+                for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * bz + l];
             double *ek = to_dev(ar, Ek, st);
-            tsgemm_AW_dd(V, b, ek, D, b, k, Psi64, k, st);           // Ritz vectors
+            tsgemm_AW_dd(Z, bz, ek, D, bz, k, Psi64, k, st);          // Ritz vectors
             lam.assign(w.begin(), w.begin() + k);
             TPO_CUDA(cudaStreamSynchronize(st));
             ar.off = mark;
             return;
         }
-        tsgemm_AW_dd(W, b, e, D, b, b, V, b, st);                    // V <- G V E (Ritz-rotated)
-        cholqr2_f64(V, T, D, b, ar, st);
+        bnd = std::max(w[bz - 1], 1e-6 * fabs(w[0]));
         ar.off = mark;
     }
 }
@@ -298,7 +374,8 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
     const int64_t bh = k + p;
     size_t s = 0;
     s += align_up(sizeof(double) * D * D) + gram_tc_ws(n, D);
-    s += 3 * align_up(sizeof(double) * D * std::max(b, bh)) + 8 * align_up(sizeof(double) * b * b + 8);
+    s += align_up(sizeof(double) * D * D) + align_up(sizeof(double) * (n + D + 64));
+    s += 8 * align_up(sizeof(double) * D * (std::max(b, bh) + 1)) + 8 * align_up(sizeof(double) * (b + 1) * (b + 1) + 8);
     s += 2 * align_up(sizeof(double) * D * k) + tsgemm_ws(n, k, k) + align_up(sizeof(float) * n * k);
     if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
     return s + 64 * 256;
@@ -311,10 +388,25 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
     double *Psi64 = ar.take<double>(D * k);
     if (mode == TPO_EIG_EXACT) {
         double *G = ar.take<double>(D * D);
+        double *u = ar.take<double>(D);
         const size_t mark = ar.off;
         gram_tc(Rp, dinv, n, D, G, ar, st);
         ar.off = mark;
-        gram_topk(G, D, k, lam, Psi64, ar, st);
+        {   // u = r / ||r||, r = R'^T 1 (the top eigenvector of the trivial pair)
+            double *ones = ar.take<double>(n);
+            fill_f64<<<cdiv(n, 256), 256, 0, st>>>(ones, n, 1.0);
+            TPO_LAUNCH_CHECK();
+            tsgemm_AtB_f32f64(Rp, D, nullptr, ones, 1, n, D, 1, u, ar, st);
+            std::vector<double> uh = to_host(u, D, st);
+            double nr = 0.0;
+            for (double x : uh) nr += x * x;
+            nr = sqrt(nr);
+            if (!(nr > 0.0)) throw Error(TPO_ENUMERIC, "top-k: R' has zero column sums");
+            for (double &x : uh) x /= nr;
+            TPO_CUDA(cudaMemcpyAsync(u, uh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, st));
+            ar.off = mark;
+        }
+        gram_topk(G, u, D, k, lam, Psi64, ar, st);
     } else {
         // Halko randomised SVD: Y = orth(R Omega); q x Y = orth(R (R^T Y)); B = R^T Y;
         // Rayleigh-Ritz through the eigendecomposition of B^T B = Y^T R R^T Y.
