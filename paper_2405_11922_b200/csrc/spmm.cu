@@ -11,6 +11,8 @@
 //     The last hop writes Z and fuses the row L2 normalisation (Eq. Z) when d <= 128.
 //   * One warp gathers one 128-float column slice of a CSR row with 128-bit loads
 //     (lane l owns float4 column l of the slice); 8 neighbour rows are in flight per warp.
+//     Work is ordered slice-major, so for d > 128 the rows gathered at any time come from one
+//     128-column slice of the dense operand (a slice of the V-side block is m x 512 B).
 //   * Power-law rows are split into chunks of CHUNK edges.  Rows with <= CHUNK edges are
 //     one work item finished in place; longer rows write per-chunk partial sums that a
 //     fix-up kernel adds in chunk order (deterministic: no float atomics anywhere).
@@ -256,8 +258,10 @@ __global__ void __launch_bounds__(WPB * 32) spmm_kernel(SpmmArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
     const int64_t n_items = tot >> 32;
-    const int64_t item = gw / a.nslices;
-    const int slice = (int)(gw - item * a.nslices);
+    // slice-major order: concurrently running warps work on the same 128-column slice, so the
+    // gathered working set is one slice of the dense operand (L2-resident for d > 128)
+    const int slice = (int)(gw / a.sch.max_items);
+    const int64_t item = gw - (int64_t)slice * a.sch.max_items;
     if (item >= n_items) return;
     const int4 it = a.sch.items[item];
     const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];
@@ -279,8 +283,8 @@ __global__ void __launch_bounds__(WPB * 32) fixup_kernel(SpmmArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
     const int64_t n_slots = tot & 0xffffffffLL;
-    const int64_t slot = gw / a.nslices;
-    const int slice = (int)(gw - slot * a.nslices);
+    const int slice = (int)(gw / a.sch.max_slots);
+    const int64_t slot = gw - (int64_t)slice * a.sch.max_slots;
     if (slot >= n_slots) return;
     const int4 s = a.sch.slots[slot];
     if (s.y != 0) return;                       // the warp of chunk 0 finishes the row
