@@ -13,15 +13,18 @@
 //     (lane l owns float4 column l of the slice); 8 neighbour rows are in flight per warp.
 //     Work is ordered slice-major, so for d > 128 the rows gathered at any time come from one
 //     128-column slice of the dense operand (a slice of the V-side block is m x 512 B).
-//   * Power-law rows are split into chunks of CHUNK edges.  Rows with <= CHUNK edges are
-//     one work item finished in place; longer rows write per-chunk partial sums that a
-//     fix-up kernel adds in chunk order (deterministic: no float atomics anywhere).
+//   * Work items: consecutive short rows are grouped into row blocks of about CHUNK edges
+//     (a new block starts where floor(row_ptr / CHUNK) changes), processed by one warp as a
+//     single edge stream -- 8 gathers in flight regardless of row boundaries, rows flushed
+//     through the epilogue as the stream crosses them (empty rows included).  Rows longer
+//     than CHUNK edges are split into CHUNK-edge items that write partial sums, added in
+//     chunk order by a fix-up kernel (deterministic: no float atomics anywhere).
 #include "tpo_internal.cuh"
 
 namespace tpo {
 namespace {
 
-constexpr int CHUNK = 512;           // edges per work item of a long row
+constexpr int CHUNK = 256;           // edges per long-row chunk; also the row-block grouping grain
 constexpr int WPB = 8;               // warps per block
 constexpr int UNR = 8;               // neighbour rows in flight per warp
 
@@ -60,13 +63,22 @@ __global__ void degree_scale_kernel(const int64_t *__restrict__ rowptr, const fl
 // ---------------------------------------------------------------------------------------
 // Work schedule: items per row, packed exclusive scan, fill.
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ bool row_is_long(const int64_t *rowptr, int64_t r) {
+    return rowptr[r + 1] - rowptr[r] > CHUNK;
+}
+// A short row starts a row block at row 0, after a long row, or where floor(rowptr / CHUNK)
+// changes.  Packed count: (items << 32) | slots.
 __global__ void sched_count_kernel(const int64_t *__restrict__ rowptr, int64_t n, int64_t *__restrict__ cnt) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int64_t len = rowptr[r + 1] - rowptr[r];
-    const int64_t nch = len <= CHUNK ? 1 : (len + CHUNK - 1) / CHUNK;
-    const int64_t sl = len <= CHUNK ? 0 : nch;
-    cnt[r] = (nch << 32) | sl;
+    if (len > CHUNK) {
+        const int64_t nch = (len + CHUNK - 1) / CHUNK;
+        cnt[r] = (nch << 32) | nch;
+        return;
+    }
+    const bool start = r == 0 || row_is_long(rowptr, r - 1) || (rowptr[r] / CHUNK != rowptr[r - 1] / CHUNK);
+    cnt[r] = start ? (int64_t(1) << 32) : 0;
 }
 
 constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_TILE = SCAN_T * SCAN_I;
@@ -136,22 +148,25 @@ __global__ void scan_apply(const int64_t *__restrict__ in, int64_t n, const int6
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) *out_total = run;
 }
 
+// items: {row, chunk, slot, nchunks} for long-row chunks; {first row, 0, -1, 0} for a row
+// block (its rows end where the next item starts).
 __global__ void sched_fill_kernel(const int64_t *__restrict__ rowptr, const int64_t *__restrict__ offsets,
                                   int64_t n, int4 *__restrict__ items, int4 *__restrict__ slots) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= n) return;
-    const int64_t len = rowptr[r + 1] - rowptr[r];
-    const int nch = len <= CHUNK ? 1 : (int)((len + CHUNK - 1) / CHUNK);
-    const int64_t off = offsets[r];
+    const int64_t off = offsets[r], nxt = (r + 1 < n) ? offsets[r + 1] : offsets[n];
     const int64_t it0 = off >> 32;
-    const int sl0 = (int)(off & 0xffffffffLL);
-    if (nch == 1) {
-        items[it0] = make_int4((int)r, 0, -1, 1);
+    const int nit = (int)((nxt >> 32) - it0);
+    if (nit == 0) return;
+    const int64_t len = rowptr[r + 1] - rowptr[r];
+    if (len <= CHUNK) {
+        items[it0] = make_int4((int)r, 0, -1, 0);
         return;
     }
-    for (int j = 0; j < nch; ++j) {
-        items[it0 + j] = make_int4((int)r, j, sl0 + j, nch);
-        slots[sl0 + j] = make_int4((int)r, j, nch, sl0);
+    const int sl0 = (int)(off & 0xffffffffLL);
+    for (int j = 0; j < nit; ++j) {
+        items[it0 + j] = make_int4((int)r, j, sl0 + j, nit);
+        slots[sl0 + j] = make_int4((int)r, j, nit, sl0);
     }
 }
 
@@ -219,41 +234,106 @@ __device__ __forceinline__ float4 gather_rows(const SpmmArgs &a, int64_t beg, in
     return acc;
 }
 
+// Epilogue of one output row from its gathered sum `acc`; x (this lane's float4 of X[row])
+// and s (the row's degree scale) are preloaded by the caller.
 template <int EPI>
-__device__ __forceinline__ void epilogue(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc) {
+__device__ __forceinline__ void epilogue_v(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc, float4 x,
+                                           float s) {
     const int64_t o = row * (int64_t)a.d4 + c4;
     if (EPI == EPI_V) {
-        const float s = a.scale[row];
         const float s2 = s * s;
         if (act) a.out[o] = make_float4(acc.x * s2, acc.y * s2, acc.z * s2, acc.w * s2);
         return;
     }
-    const float su = a.scale[row];
-    const float g = a.alpha * su;
-    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (act) {
-        const float4 x = __ldg(a.X + o);
-        z.x = fmaf(a.c, x.x, g * acc.x);
-        z.y = fmaf(a.c, x.y, g * acc.y);
-        z.z = fmaf(a.c, x.z, g * acc.z);
-        z.w = fmaf(a.c, x.w, g * acc.w);
-    }
+    const float g = a.alpha * s;
+    float4 z;
+    z.x = fmaf(a.c, x.x, g * acc.x);
+    z.y = fmaf(a.c, x.y, g * acc.y);
+    z.z = fmaf(a.c, x.z, g * acc.z);
+    z.w = fmaf(a.c, x.w, g * acc.w);
     if (EPI == EPI_U) {
-        if (act) a.out[o] = make_float4(su * z.x, su * z.y, su * z.z, su * z.w);
+        if (act) a.out[o] = make_float4(s * z.x, s * z.y, s * z.z, s * z.w);
         return;
     }
     // EPI_FINAL
     if (act) a.out[o] = z;
     if (a.out_hat != nullptr) {            // only when nslices == 1: the warp owns the row
-        float ss = z.x * z.x + z.y * z.y + z.z * z.z + z.w * z.w;
+        float ss = act ? z.x * z.x + z.y * z.y + z.z * z.z + z.w * z.w : 0.f;
         for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
         const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;
         if (act) a.out_hat[o] = make_float4(z.x * inv, z.y * inv, z.z * inv, z.w * inv);
     }
 }
 
+template <int EPI>
+__device__ __forceinline__ float4 load_x(const SpmmArgs &a, int64_t row, int c4, bool act) {
+    if (EPI == EPI_V || !act) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return __ldg(a.X + row * (int64_t)a.d4 + c4);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc) {
+    epilogue_v<EPI>(a, row, c4, act, acc, load_x<EPI>(a, row, c4, act), a.scale[row]);
+}
+
+// One warp streams the edges of rows [r0, r1) (all short) for one column slice, flushing each
+// row through the epilogue as the stream crosses its end; empty rows are flushed with 0.
 template <int EPI, bool WEIGHTED>
-__global__ void __launch_bounds__(WPB * 32) spmm_kernel(SpmmArgs a) {
+__device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0, int64_t r1, int c4, bool act) {
+    const int lane = threadIdx.x & 31;
+    const float4 *__restrict__ src = a.src + c4;
+    const int64_t d4 = a.d4;
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t rb = r0; rb < r1; rb += 32) {
+        const int nb = (int)(r1 - rb < 32 ? r1 - rb : 32);
+        const int64_t my_end = lane < nb ? a.rowptr[rb + 1 + lane] : 0;     // end of row rb + lane
+        const float my_s = lane < nb ? a.scale[rb + lane] : 0.f;
+        const int64_t e_beg = a.rowptr[rb];
+        const int64_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+        int cur = 0;
+        int64_t cur_end = __shfl_sync(0xffffffffu, my_end, 0);
+        float4 xcur = load_x<EPI>(a, rb, c4, act);
+        float4 acc = zero;
+        for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
+            const int cnt = (int)(e_end - e0 < 32 ? e_end - e0 : 32);
+            const int mycol = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
+            float myw = 1.f;
+            if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
+            for (int j = 0; j < cnt; j += UNR) {
+                float4 v[UNR];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const int jj = j + u < 31 ? j + u : 31;
+                    const int c = __shfl_sync(0xffffffffu, mycol, jj);
+                    v[u] = (act && j + u < cnt) ? __ldg(src + (int64_t)c * d4) : zero;
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    if (j + u >= cnt) break;
+                    const int64_t e = e0 + j + u;
+                    while (e >= cur_end) {               // warp-uniform: flush finished rows
+                        epilogue_v<EPI>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
+                        acc = zero;
+                        ++cur;
+                        cur_end = __shfl_sync(0xffffffffu, my_end, cur);
+                        xcur = load_x<EPI>(a, rb + cur, c4, act);
+                    }
+                    if (WEIGHTED) acc = f4fma(__shfl_sync(0xffffffffu, myw, j + u), v[u], acc);
+                    else acc = f4add(acc, v[u]);
+                }
+            }
+        }
+        while (cur < nb) {                               // last row of the batch and empty rows
+            epilogue_v<EPI>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
+            acc = zero;
+            ++cur;
+            if (cur < nb) xcur = load_x<EPI>(a, rb + cur, c4, act);
+        }
+    }
+}
+
+template <int EPI, bool WEIGHTED>
+__global__ void __launch_bounds__(WPB * 32, 4) spmm_kernel(SpmmArgs a) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
@@ -264,17 +344,18 @@ __global__ void __launch_bounds__(WPB * 32) spmm_kernel(SpmmArgs a) {
     const int64_t item = gw - (int64_t)slice * a.sch.max_items;
     if (item >= n_items) return;
     const int4 it = a.sch.items[item];
-    const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];
-    const int64_t beg = rb + (int64_t)it.y * CHUNK;
-    const int64_t end = it.w == 1 ? re : min(re, beg + CHUNK);
     const int c4 = slice * 32 + lane;
     const bool act = c4 < a.d4;
-    const float4 acc = gather_rows<WEIGHTED>(a, beg, end, c4, act);
-    if (it.z >= 0) {
-        if (act) a.partials[(int64_t)it.z * a.d4 + c4] = acc;
+    if (it.w == 0) {                                     // row block
+        const int64_t r1 = item + 1 < n_items ? (int64_t)a.sch.items[item + 1].x : a.n_rows;
+        process_row_block<EPI, WEIGHTED>(a, it.x, r1, c4, act);
         return;
     }
-    epilogue<EPI>(a, it.x, c4, act, acc);
+    const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];   // chunk of a long row
+    const int64_t beg = rb + (int64_t)it.y * CHUNK;
+    const int64_t end = min(re, beg + CHUNK);
+    const float4 acc = gather_rows<WEIGHTED>(a, beg, end, c4, act);
+    if (act) a.partials[(int64_t)it.z * a.d4 + c4] = acc;
 }
 
 template <int EPI>
@@ -341,7 +422,7 @@ struct SchedBufs {
 
 SchedBufs sched_alloc(Arena &ar, int64_t n_rows, int64_t nnz) {
     SchedBufs b;
-    b.s.max_items = n_rows + nnz / CHUNK + 1;
+    b.s.max_items = n_rows + 2 * (nnz / CHUNK) + 1;
     b.s.max_slots = 2 * (nnz / CHUNK) + 1;
     b.s.offsets = ar.take<int64_t>(n_rows + 1);
     b.s.items = ar.take<int4>(b.s.max_items);
