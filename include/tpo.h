@@ -108,7 +108,8 @@ int tpo_haar_q_dev(const double *G, int64_t d, float *Q, void *ws, size_t ws_byt
  *      Zo = sqrt(d) * Zhat * Q^T ;  R' = sqrt(e/d) * ( sin(Zo) || cos(Zo) )   (n x 2d,
  *      sin in columns [0,d), cos in [d,2d));  r = sum_i R'[i] (fp64);
  *      dinv[i] = 1 / sqrt(max(R'[i] . r, 1e-12))   (R6)     so that R = diag(dinv) R'.
- *   Zhat: n x d fp32;  Q: d x d fp32 (from tpo_haar_q);  Rp: n x 2d fp32 out;
+ *   Zhat: n x d fp32, d % 4 == 0;  Q: d x d fp32 (from tpo_haar_q);  Rp: n x 2d fp32 out;
+ *   The GEMM Zhat Q^T runs on tcgen05 with 3xTF32 splitting (fp32-accurate products).
  *   dinv: n fp32 out;  r_out: 2d fp64 out (device) or NULL.
  * Workspace: tpo_features_ws(n, d).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA.
  * --------------------------------------------------------------------------------------- */

@@ -111,6 +111,33 @@ __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ 
     }
 }
 
+// Small-k variant (k <= 16): one thread per row, the row of Ups in registers, Phi in smem
+// (same arithmetic and summation order as assign_kernel).
+template <int KM>
+__global__ void __launch_bounds__(256) assign_small_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
+                                                           int64_t n, int k, int32_t *__restrict__ labels, NciState s) {
+    if (*s.done) return;
+    __shared__ double phs[KM * KM];
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) phs[i] = Phi[i];
+    __syncthreads();
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    double u[KM];
+#pragma unroll
+    for (int a = 0; a < KM; ++a) u[a] = a < k ? U[row * k + a] : 0.0;
+    double best = 0.0;
+    int arg = 0;
+    for (int l = 0; l < k; ++l) {
+        double sc = 0.0;
+#pragma unroll
+        for (int a = 0; a < KM; ++a)
+            if (a < k) sc = __dadd_rn(sc, __dmul_rn(u[a], phs[a * k + l]));
+        if (l == 0 || sc > best) { best = sc; arg = l; }
+    }
+    if (labels[row] != arg) *s.changed = 1;
+    labels[row] = arg;
+}
+
 __global__ void nci_step_kernel(NciState s, int32_t *__restrict__ counts, int k) {
     // runs after assign: advance the iteration counter, freeze on a fix-point
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -248,7 +275,10 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
     const int sum_threads = (int)std::max<int64_t>(32, cdiv(k, 32) * 32);
     for (int t = 0; t < Tg; ++t) {
-        assign_kernel<<<cdiv(n * 32, 256), 256, phi_smem, st>>>(U, Phi, n, k, labels, s);
+        if (k <= 16)
+            assign_small_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+        else
+            assign_kernel<<<cdiv(n * 32, 256), 256, phi_smem, st>>>(U, Phi, n, k, labels, s);
         TPO_LAUNCH_CHECK();
         nci_step_kernel<<<1, 32, 0, st>>>(s, nullptr, k);
         TPO_LAUNCH_CHECK();

@@ -174,6 +174,177 @@ __global__ void __launch_bounds__(NT) aw_kernel(const TAt *__restrict__ A, int64
     }
 }
 
+
+// ----------------------------------------------------------------------------------------
+// Streaming variants for a fp32 A with 16-byte aligned rows (R' products): A slabs are staged
+// into shared memory with cp.async (double buffered), each thread owns a 4 x 4 register tile
+// (4 rows/columns of A strided by 32, 4 columns of the skinny side), fp64 FMA.
+// ----------------------------------------------------------------------------------------
+constexpr int SN = 128;        // threads
+constexpr int SR = 128;        // rows (aw) or A columns (atb) per block
+constexpr int SK = 32;         // slab depth
+constexpr int SP = 36;         // smem pitch (floats) of an A slab row: conflict-free, 16 B aligned
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// out[i, b0 + c] = rs_i * sum_j A[i, j] W[j, b0 + c]
+template <class TO, int QW>
+__global__ void __launch_bounds__(SN) aw_stream_kernel(const float *__restrict__ A, int64_t lda,
+                                                       const float *__restrict__ rs, const double *__restrict__ W,
+                                                       int64_t n, int p, int q, TO *__restrict__ out, int64_t ldo) {
+    constexpr int CW = QW / 4;
+    __shared__ __align__(16) float As[2][SR * SP];
+    __shared__ __align__(16) double Ws[2][SK * QW];
+    const int t = threadIdx.x, rg = t >> 2, cg = t & 3;
+    const int64_t i0 = (int64_t)blockIdx.x * SR;
+    const int b0 = blockIdx.y * QW;
+    const int nslab = (p + SK - 1) / SK;
+    double acc[4][CW];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+    auto load = [&](int s, int buf) {
+        const int k0 = s * SK;
+#pragma unroll
+        for (int m = 0; m < (SR * SK / 4) / SN; ++m) {
+            const int ch = t + SN * m, row = ch >> 3, kc = (ch & 7) * 4;
+            const int64_t gi = i0 + row;
+            const bool ok = gi < n && k0 + kc < p;
+            cp_async16(&As[buf][row * SP + kc], ok ? (const void *)(A + gi * lda + k0 + kc) : (const void *)A, ok);
+        }
+        cp_async_commit();
+        for (int e = t; e < SK * QW; e += SN) {
+            const int kk = e / QW, c = e - kk * QW;
+            Ws[buf][e] = (k0 + kk < p && b0 + c < q) ? W[(int64_t)(k0 + kk) * q + b0 + c] : 0.0;
+        }
+    };
+    load(0, 0);
+    for (int s = 0; s < nslab; ++s) {
+        const int buf = s & 1;
+        if (s + 1 < nslab) {
+            load(s + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *a = As[buf];
+        const double *w = Ws[buf];
+#pragma unroll 8
+        for (int kk = 0; kk < SK; ++kk) {
+            double av[4], wv[CW];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) av[r] = (double)a[(rg + 32 * r) * SP + kk];
+#pragma unroll
+            for (int c = 0; c < CW; ++c) wv[c] = w[kk * QW + cg * CW + c];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], wv[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t row = i0 + rg + 32 * r;
+        if (row >= n) continue;
+        const double sc = rs ? (double)rs[row] : 1.0;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            const int col = b0 + cg * CW + c;
+            if (col < q) out[row * ldo + col] = (TO)(sc * acc[r][c]);
+        }
+    }
+}
+
+// part[g][a][b0 + c] = sum over the rows of group g of (ra_i A[i, a]) B[i, b0 + c]
+template <class TBt, int QW>
+__global__ void __launch_bounds__(SN) atb_stream_kernel(const float *__restrict__ A, int64_t lda,
+                                                        const float *__restrict__ ra, const TBt *__restrict__ B,
+                                                        int64_t ldb, int64_t n, int p, int q, int64_t rows_per_group,
+                                                        double *__restrict__ part) {
+    constexpr int CW = QW / 4;
+    __shared__ __align__(16) float As[2][SK * (SR + 4)];     // As[row][a], pitch SR + 4
+    __shared__ __align__(16) double Bs[2][SK * QW];
+    constexpr int AP = SR + 4;
+    const int t = threadIdx.x, ag = t >> 2, bg = t & 3;
+    const int a0 = blockIdx.x * SR, b0 = blockIdx.y * QW;
+    const int64_t g = blockIdx.z;
+    const int64_t r_beg = g * rows_per_group, r_end = min(n, r_beg + rows_per_group);
+    const int nslab = r_end > r_beg ? (int)((r_end - r_beg + SK - 1) / SK) : 0;
+    double acc[4][CW];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+    auto load = [&](int s, int buf) {
+        const int64_t k0 = r_beg + (int64_t)s * SK;
+#pragma unroll
+        for (int m = 0; m < (SR * SK / 4) / SN; ++m) {
+            const int ch = t + SN * m, row = ch >> 5, ac = (ch & 31) * 4;
+            const int64_t gi = k0 + row;
+            const bool ok = gi < r_end && a0 + ac < p;
+            cp_async16(&As[buf][row * AP + ac], ok ? (const void *)(A + gi * lda + a0 + ac) : (const void *)A, ok);
+        }
+        cp_async_commit();
+        for (int e = t; e < SK * QW; e += SN) {
+            const int kk = e / QW, c = e - kk * QW;
+            const int64_t gi = k0 + kk;
+            double v = 0.0;
+            if (gi < r_end && b0 + c < q) {
+                v = (double)B[gi * ldb + b0 + c];
+                if (ra) v *= (double)ra[gi];
+            }
+            Bs[buf][e] = v;
+        }
+    };
+    if (nslab > 0) load(0, 0);
+    for (int s = 0; s < nslab; ++s) {
+        const int buf = s & 1;
+        if (s + 1 < nslab) {
+            load(s + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *a = As[buf];
+        const double *b = Bs[buf];
+#pragma unroll 8
+        for (int kk = 0; kk < SK; ++kk) {
+            double av[4], bv[CW];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) av[r] = (double)a[kk * AP + ag + 32 * r];
+#pragma unroll
+            for (int c = 0; c < CW; ++c) bv[c] = b[kk * QW + bg * CW + c];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], bv[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+    double *o = part + g * (int64_t)p * q;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int a = a0 + ag + 32 * r;
+        if (a >= p) continue;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            const int col = b0 + bg * CW + c;
+            if (col < q) o[(int64_t)a * q + col] = acc[r][c];
+        }
+    }
+}
+
 // Row groups of the split-over-rows products: about 4 blocks per SM of a 148-SM B200 in
 // total (a fixed constant, so workspace queries need no device).
 constexpr int64_t kBlocksTarget = 4 * 148;
@@ -235,20 +406,59 @@ void tsgemm_AtB_f32f32(const float *A, int64_t lda, const float *rsA, const floa
 }
 void tsgemm_AtB_f32f64(const float *A, int64_t lda, const float *rsA, const double *Bm, int64_t ldb, int64_t n,
                        int64_t p, int64_t q, double *out, Arena &ar, cudaStream_t st) {
-    atb_run<float, double>(A, lda, rsA, Bm, ldb, nullptr, n, p, q, out, ar, st);
+    if (n == 0 || lda % 4 != 0 || (reinterpret_cast<uintptr_t>(A) & 15u) != 0 || q > 16) {
+        atb_run<float, double>(A, lda, rsA, Bm, ldb, nullptr, n, p, q, out, ar, st);
+        return;
+    }
+    const int QW = q <= 8 ? 8 : 16;
+    const int64_t tiles = cdiv(p, SR) * cdiv(q, QW);
+    const int64_t want = std::max<int64_t>(1, cdiv(kBlocksTarget, tiles));
+    const int64_t G0 = std::max<int64_t>(1, std::min<int64_t>(want, cdiv(n, 4 * SK)));
+    const int64_t rpg = cdiv(cdiv(n, G0), SK) * SK;
+    const int64_t Gr = std::max<int64_t>(1, cdiv(n, rpg));
+    const size_t mark = ar.off;
+    double *part = Gr == 1 ? out : ar.take<double>(Gr * p * q);
+    const dim3 grid(cdiv(p, SR), cdiv(q, QW), Gr);
+    if (QW == 8)
+        atb_stream_kernel<double, 8><<<grid, SN, 0, st>>>(A, lda, rsA, Bm, ldb, n, (int)p, (int)q, rpg, part);
+    else
+        atb_stream_kernel<double, 16><<<grid, SN, 0, st>>>(A, lda, rsA, Bm, ldb, n, (int)p, (int)q, rpg, part);
+    TPO_LAUNCH_CHECK();
+    if (Gr > 1) {
+        reduce_groups_kernel<<<cdiv(p * q, 256), 256, 0, st>>>(part, Gr, p * q, out);
+        TPO_LAUNCH_CHECK();
+    }
+    ar.off = mark;
 }
 void tsgemm_AtB_f64f64(const double *A, int64_t lda, const double *Bm, int64_t ldb, int64_t n, int64_t p,
                        int64_t q, double *out, Arena &ar, cudaStream_t st) {
     atb_run<double, double>(A, lda, nullptr, Bm, ldb, nullptr, n, p, q, out, ar, st);
 }
 
+template <class TO>
+void aw_f32_run(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q, TO *out,
+                int64_t ldo, cudaStream_t st) {
+    if (n == 0 || q == 0) return;
+    if (lda % 4 != 0 || (reinterpret_cast<uintptr_t>(A) & 15u) != 0) {
+        aw_run<float, TO>(A, lda, rs, W, n, p, q, out, ldo, st);
+        return;
+    }
+    if (q <= 8) {
+        aw_stream_kernel<TO, 8><<<dim3(cdiv(n, SR), cdiv(q, 8)), SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
+    } else {
+        aw_stream_kernel<TO, 16><<<dim3(cdiv(n, SR), cdiv(q, 16)), SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out,
+                                                                               ldo);
+    }
+    TPO_LAUNCH_CHECK();
+}
+
 void tsgemm_AW_f32(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q,
                    float *out, int64_t ldo, cudaStream_t st) {
-    aw_run<float, float>(A, lda, rs, W, n, p, q, out, ldo, st);
+    aw_f32_run<float>(A, lda, rs, W, n, p, q, out, ldo, st);
 }
 void tsgemm_AW_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q,
                    double *out, int64_t ldo, cudaStream_t st) {
-    aw_run<float, double>(A, lda, rs, W, n, p, q, out, ldo, st);
+    aw_f32_run<double>(A, lda, rs, W, n, p, q, out, ldo, st);
 }
 void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int64_t p, int64_t q, double *out,
                   int64_t ldo, cudaStream_t st) {

@@ -363,7 +363,205 @@ GramPlan plan(int64_t n, int64_t D) {
     return p;
 }
 
+
+// =========================================================================================
+// a5 on the tensor cores: Zo = sqrt(d) Zhat Q^T with 3xTF32 (K-major operands: Zhat rows and
+// Q rows are both contiguous along the reduction index l), fp32 accumulation in TMEM over
+// the d-term dot products, epilogue R' = sqrt(e/d) (sin Zo || cos Zo) straight from TMEM.
+// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..5 epilogue (lane quarter = warp % 4).
+// =========================================================================================
+constexpr int FT_M = 128, FT_N = 128, FT_KB = 32, FT_STAGES = 3;
+constexpr int FT_OPER = FT_M * FT_KB * 4;          // 16 KB: 128 rows x 32 fp32 (128 B rows)
+constexpr int FT_STAGE = 4 * FT_OPER;              // A_hi, A_lo, B_hi, B_lo
+constexpr int FT_THREADS = 192;
+
+// K-major operand, 128-byte swizzle: 8-row x 128-byte atoms stacked along M/N at SBO = 1 KB.
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;                       // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;             // SBO
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
+    return d;
+}
+
+constexpr uint32_t idesc_tf32_kmajor(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(FT_THREADS, 1)
+features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_constant__ CUtensorMap mz_lo,
+                   const __grid_constant__ CUtensorMap mq_hi, const __grid_constant__ CUtensorMap mq_lo, int64_t n,
+                   int d, float *__restrict__ Rp) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + FT_STAGES * FT_STAGE);   // full[S], empty[S], tfull
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * FT_STAGES + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i0 = (int64_t)blockIdx.x * FT_M;
+    const int j0 = blockIdx.y * FT_N;
+    const int nkb = (d + FT_KB - 1) / FT_KB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < FT_STAGES; ++s) {
+            mbar_init(smem_u32(&bars[s]), 1);
+            mbar_init(smem_u32(&bars[FT_STAGES + s]), 1);
+        }
+        mbar_init(smem_u32(&bars[2 * FT_STAGES]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(FT_N)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % FT_STAGES, j = kb / FT_STAGES;
+                if (j > 0) mbar_wait(smem_u32(&bars[FT_STAGES + s]), (j - 1) & 1);
+                const uint32_t full = smem_u32(&bars[s]);
+                mbar_expect_tx(full, FT_STAGE);
+                const uint32_t base = smem_u32(smem + s * FT_STAGE);
+                tma_load_2d(base + 0 * FT_OPER, &mz_hi, full, kb * FT_KB, (int)i0);
+                tma_load_2d(base + 1 * FT_OPER, &mz_lo, full, kb * FT_KB, (int)i0);
+                tma_load_2d(base + 2 * FT_OPER, &mq_hi, full, kb * FT_KB, j0);
+                tma_load_2d(base + 3 * FT_OPER, &mq_lo, full, kb * FT_KB, j0);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_tf32_kmajor(FT_M, FT_N);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % FT_STAGES, j = kb / FT_STAGES;
+            mbar_wait(smem_u32(&bars[s]), j & 1);
+            fence_after();
+            if (lane == 0) {
+                const uint32_t base = smem_u32(smem + s * FT_STAGE);
+#pragma unroll
+                for (int kk = 0; kk < FT_KB / 8; ++kk) {
+                    const uint32_t off = kk * 32;        // 8 fp32 of K inside the 128-byte atom
+                    const uint64_t ah = umma_desc_kmajor(base + off), al = umma_desc_kmajor(base + FT_OPER + off);
+                    const uint64_t bh = umma_desc_kmajor(base + 2 * FT_OPER + off);
+                    const uint64_t bl = umma_desc_kmajor(base + 3 * FT_OPER + off);
+                    mma_tf32(tmem_base, al, bh, idesc, (kb | kk) ? 1u : 0u);
+                    mma_tf32(tmem_base, ah, bl, idesc, 1u);
+                    mma_tf32(tmem_base, ah, bh, idesc, 1u);
+                }
+                mma_commit(smem_u32(&bars[FT_STAGES + s]));
+                if (kb == nkb - 1) mma_commit(smem_u32(&bars[2 * FT_STAGES]));
+            }
+            __syncwarp();
+        }
+    } else {
+        const int q = warp & 3;
+        mbar_wait(smem_u32(&bars[2 * FT_STAGES]), 0);
+        fence_after();
+        const int64_t row = i0 + 32 * q + lane;
+        const float sd = sqrtf((float)d);
+        const float amp = (float)sqrt(exp(1.0) / (double)d);
+        const int64_t D = 2 * (int64_t)d;
+#pragma unroll 1
+        for (int c = 0; c < FT_N / 32; ++c) {
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + 32 * c, v);
+            const int jb = j0 + 32 * c;
+            if (row >= n) continue;
+            float *ps = Rp + row * D + jb, *pc = Rp + row * D + d + jb;
+            if (jb + 32 <= d) {
+#pragma unroll
+                for (int t = 0; t < 32; t += 4) {
+                    float s0, c0, s1, c1, s2, c2, s3, c3;
+                    sincosf(sd * v[t], &s0, &c0);
+                    sincosf(sd * v[t + 1], &s1, &c1);
+                    sincosf(sd * v[t + 2], &s2, &c2);
+                    sincosf(sd * v[t + 3], &s3, &c3);
+                    *reinterpret_cast<float4 *>(ps + t) = make_float4(amp * s0, amp * s1, amp * s2, amp * s3);
+                    *reinterpret_cast<float4 *>(pc + t) = make_float4(amp * c0, amp * c1, amp * c2, amp * c3);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    if (jb + t < d) {
+                        float sn, cs;
+                        sincosf(sd * v[t], &sn, &cs);
+                        ps[t] = amp * sn;
+                        pc[t] = amp * cs;
+                    }
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(FT_N) : "memory");
+    }
+}
+
+// hi = rna-tf32(x), lo = x - hi   (plain split, no row scale)
+__global__ void split_plain_kernel(const float4 *__restrict__ x, int64_t len4, float4 *__restrict__ hi,
+                                   float4 *__restrict__ lo) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= len4) return;
+    const float4 v4 = x[i];
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    float h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint32_t t;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v[j]));
+        h[j] = __uint_as_float(t);
+        l[j] = v[j] - h[j];
+    }
+    hi[i] = make_float4(h[0], h[1], h[2], h[3]);
+    lo[i] = make_float4(l[0], l[1], l[2], l[3]);
+}
+
+CUtensorMap make_map_kmajor(const float *base, int64_t rows, int64_t K, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * sizeof(float)};
+    const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(TPO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
 }  // namespace
+
+size_t features_tc_ws(int64_t n, int64_t d) {
+    return 2 * align_up(sizeof(float) * n * d) + 2 * align_up(sizeof(float) * d * d) + 1024;
+}
+
+// R'[:, 0:d] = sqrt(e/d) sin(sqrt(d) Zhat Q^T), R'[:, d:2d] = sqrt(e/d) cos(...)   (d % 4 == 0)
+void features_tc(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, Arena &ar, cudaStream_t st) {
+    float *zh = ar.take<float>(n * d), *zl = ar.take<float>(n * d);
+    float *qh = ar.take<float>(d * d), *ql = ar.take<float>(d * d);
+    split_plain_kernel<<<cdiv(n * d / 4, 256), 256, 0, st>>>((const float4 *)Zhat, n * d / 4, (float4 *)zh,
+                                                           (float4 *)zl);
+    TPO_LAUNCH_CHECK();
+    split_plain_kernel<<<cdiv(d * d / 4, 256), 256, 0, st>>>((const float4 *)Q, d * d / 4, (float4 *)qh, (float4 *)ql);
+    TPO_LAUNCH_CHECK();
+    const CUtensorMap a_hi = make_map_kmajor(zh, n, d, FT_M), a_lo = make_map_kmajor(zl, n, d, FT_M);
+    const CUtensorMap b_hi = make_map_kmajor(qh, d, d, FT_N), b_lo = make_map_kmajor(ql, d, d, FT_N);
+    const size_t smem = FT_STAGES * FT_STAGE + 1024 + 256;
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(features_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    const dim3 grid(cdiv(n, FT_M), cdiv(d, FT_N));
+    features_tc_kernel<<<grid, FT_THREADS, smem, st>>>(a_hi, a_lo, b_hi, b_lo, n, (int)d, Rp);
+    TPO_LAUNCH_CHECK();
+}
 
 void gram_debug_set(float *p) { TPO_CUDA(cudaMemcpyToSymbol(g_gram_dbg, &p, sizeof(p))); }
 

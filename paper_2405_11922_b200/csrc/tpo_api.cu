@@ -123,7 +123,7 @@ int tpo_features(const float *Zhat, int64_t n, int64_t d, const float *Q, float 
                  void *ws, size_t ws_bytes, void *stream) {
     return guarded([&] {
         TPO_REQUIRE(n >= 0, "n must be >= 0");
-        TPO_REQUIRE(d >= 1 && d <= 8192, "d must lie in [1, 8192]");
+        TPO_REQUIRE(d >= 4 && d <= 8192 && d % 4 == 0, "d must be a multiple of 4 in [4, 8192]");
         if (n > 0) {
             check_ptr(Zhat, "Zhat");
             check_ptr(Rp, "Rp");

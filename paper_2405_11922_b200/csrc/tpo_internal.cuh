@@ -128,6 +128,9 @@ void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int6
 // tcgen05 3xTF32 Gram with fp64 segment accumulation (gram_tc.cu).
 void gram_tc(const float *Rp, const float *dinv, int64_t n, int64_t D, double *G, Arena &ar, cudaStream_t st);
 size_t gram_tc_ws(int64_t n, int64_t D);
+// R' = sqrt(e/d) (sin || cos)(sqrt(d) Zhat Q^T) on tcgen05 (3xTF32), R' only (gram_tc.cu).
+void features_tc(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, Arena &ar, cudaStream_t st);
+size_t features_tc_ws(int64_t n, int64_t d);
 size_t tsgemm_ws(int64_t n, int64_t p, int64_t q);
 
 // ----------------------------------------------------------------------------------------
