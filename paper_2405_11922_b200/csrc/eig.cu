@@ -3,7 +3,7 @@
 //
 // EXACT mode (R7): Gram G = R^T R (D x D, fp64 sums) once, then block subspace iteration
 // with Rayleigh-Ritz on G (the D x D image of the implicit n x n affinity S~ = R R^T:
-// both share their nonzero spectrum) until the top-k Ritz residuals fall below 1e-9 lambda_1;
+// both share their nonzero spectrum) until the top-k Ritz residuals fall below 1e-10 lambda_1;
 // with a full-rank block (b = D) this is one Rayleigh-Ritz step, i.e. a dense eigensolve.
 // Then Gamma = R Psi Sigma^{-1} and a CholeskyQR2 polish if ||Gamma^T Gamma - I||_max > 1e-6.
 // HALKO mode: the randomised truncated SVD the paper cites, q power steps.
@@ -143,6 +143,25 @@ __global__ void project_out_kernel(double *__restrict__ V, const double *__restr
     V[i] -= u[r] * c[i - r * b];
 }
 
+// res[l] = || GX[:, l] - w[l] X[:, l] ||  (one block per column, fixed tree)
+__global__ void residual_kernel(const double *__restrict__ GX, const double *__restrict__ X,
+                                const double *__restrict__ w, int64_t D, int k, double *__restrict__ res) {
+    __shared__ double sh[256];
+    const int l = blockIdx.x;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < D; i += 256) {
+        const double r = GX[i * k + l] - w[l] * X[i * k + l];
+        acc += r * r;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) res[l] = sqrt(sh[0]);
+}
+
 // Z = [u | V]  (D x (b+1))
 __global__ void stack_kernel(const double *__restrict__ u, const double *__restrict__ V, int64_t D, int b,
                              double *__restrict__ Z) {
@@ -159,7 +178,7 @@ __global__ void stack_kernel(const double *__restrict__ u, const double *__restr
 //  * otherwise Chebyshev-filtered block subspace iteration (degree m) on the deflated
 //    Gd = G - u u^T with a block V (D x b) kept orthogonal to u, and after every filter a
 //    Rayleigh-Ritz step with the FULL G on span([u, V]); stop when the top-k Ritz residuals
-//    ||G z - theta z|| fall below 1e-9 theta_1.  The filter damps [0, theta_min] (theta_min
+//    ||G z - theta z|| (computed explicitly) fall below 1e-10 theta_1.  The filter damps [0, theta_min] (theta_min
 //    = smallest Ritz value of the block) and amplifies the wanted end of the spectrum; the
 //    deflation keeps the lambda = 1 direction from swamping the block.
 void gram_topk(const double *G, const double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
@@ -217,29 +236,25 @@ void gram_topk(const double *G, const double *u, int64_t D, int32_t k, std::vect
         TPO_LAUNCH_CHECK();
         tsgemm_AW_dd(G, D, Z, D, D, bz, W, bz, st);
         const size_t mark = ar.off;
-        double *h = ar.take<double>(bz * bz), *ww = ar.take<double>(bz * bz);
+        double *h = ar.take<double>(bz * bz);
         tsgemm_AtB_f64f64(Z, bz, W, bz, D, bz, bz, h, ar, st);
-        tsgemm_AtB_f64f64(W, bz, W, bz, D, bz, bz, ww, ar, st);
-        std::vector<double> H = to_host(h, bz * bz, st), WtW = to_host(ww, bz * bz, st);
+        std::vector<double> H = to_host(h, bz * bz, st);
         host_sym_eig_top(bz, H.data(), bz, w.data(), E.data());
+        // explicit residuals r_l = ||G x_l - w_l x_l|| of the top-k Ritz pairs (x = Z e, G x = W e)
+        std::vector<double> Ek(bz * k), wk(w.begin(), w.begin() + k);
+        for (int64_t a = 0; a < bz; ++a)
+            for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * bz + l];
+        double *ek = to_dev(ar, Ek, st), *dw = to_dev(ar, wk, st);
+        double *gx = ar.take<double>(D * k), *res = ar.take<double>(k);
+        tsgemm_AW_dd(Z, bz, ek, D, bz, k, Psi64, k, st);              // Ritz vectors x
+        tsgemm_AW_dd(W, bz, ek, D, bz, k, gx, k, st);                 // G x
+        residual_kernel<<<k, 256, 0, st>>>(gx, Psi64, dw, D, k, res);
+        TPO_LAUNCH_CHECK();
+        const std::vector<double> rh = to_host(res, k, st);
         double rmax = 0.0;
-        for (int l = 0; l < k; ++l) {          // ||G z_l - w_l z_l||^2 = e^T W^T W e - w_l^2
-            double s2 = 0.0;
-            for (int64_t a = 0; a < bz; ++a) {
-                double t = 0.0;
-                for (int64_t c = 0; c < bz; ++c) t += WtW[a * bz + c] * E[c * bz + l];
-                s2 += E[a * bz + l] * t;
-            }
-            rmax = std::max(rmax, sqrt(std::max(s2 - w[l] * w[l], 0.0)));
-        }
-        if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
-            std::vector<double> Ek(bz * k);
-            for (int64_t a = 0; a < bz; ++a)
-                for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * bz + l];
-            double *ek = to_dev(ar, Ek, st);
-            tsgemm_AW_dd(Z, bz, ek, D, bz, k, Psi64, k, st);          // Ritz vectors
+        for (int l = 0; l < k; ++l) rmax = std::max(rmax, rh[l]);
+        if (rmax <= 1e-10 * fabs(w[0]) || round == max_rounds) {
             lam.assign(w.begin(), w.begin() + k);
-            TPO_CUDA(cudaStreamSynchronize(st));
             ar.off = mark;
             return;
         }
