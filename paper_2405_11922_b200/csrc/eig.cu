@@ -114,13 +114,13 @@ void cholqr2_f64(double *V, double *tmp, int64_t rows, int64_t b, Arena &ar, cud
     }
 }
 
-// Gd = G - u u^T (deflation of the trivial eigenpair, see gram_topk)
-__global__ void deflate_kernel(const double *__restrict__ G, const double *__restrict__ u, int64_t D,
+// Gd = G - lam u u^T (deflation of the top eigenpair, see gram_topk)
+__global__ void deflate_kernel(const double *__restrict__ G, const double *__restrict__ u, double lam, int64_t D,
                                double *__restrict__ Gd) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= D * D) return;
     const int64_t a = i / D, b = i - a * D;
-    Gd[i] = G[i] - u[a] * u[b];
+    Gd[i] = G[i] - lam * u[a] * u[b];
 }
 
 // out = s1 * GY - s2 * Y1 - (Y0 ? Y0 : 0): one step of the Chebyshev three-term recurrence
@@ -181,7 +181,7 @@ __global__ void stack_kernel(const double *__restrict__ u, const double *__restr
 //    ||G z - theta z|| (computed explicitly) fall below 1e-10 theta_1.  The filter damps [0, theta_min] (theta_min
 //    = smallest Ritz value of the block) and amplifies the wanted end of the spectrum; the
 //    deflation keeps the lambda = 1 direction from swamping the block.
-void gram_topk(const double *G, const double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
+void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
                Arena &ar, cudaStream_t st) {
     const int64_t b = std::min<int64_t>(D - 1, k + std::max<int64_t>(k, 16));
     if (b + 1 >= D || D <= 64) {
@@ -198,7 +198,26 @@ void gram_topk(const double *G, const double *u, int64_t D, int32_t k, std::vect
     double *Y0 = ar.take<double>(D * b), *Y1 = ar.take<double>(D * b), *GY = ar.take<double>(D * b);
     double *Z = ar.take<double>(D * bz), *W = ar.take<double>(D * bz);
     double *cvec = ar.take<double>(b);
-    deflate_kernel<<<cdiv(D * D, 256), 256, 0, st>>>(G, u, D, Gd);
+    // u = r/||r|| is the top eigenvector of the exact Gram; refine it to the top eigenvector of
+    // the computed G by a few power steps (rate lambda_2 / lambda_1 ~ 0.03), then deflate
+    // Gd = G - lambda_1 u u^T with lambda_1 = u^T G u.
+    double lam1 = 1.0;
+    {
+        double *gu = Y0;
+        std::vector<double> uh;
+        for (int it = 0; it < 6; ++it) {
+            tsgemm_AW_dd(G, D, u, D, D, 1, gu, 1, st);
+            std::vector<double> g = to_host(gu, D, st);
+            if (uh.empty()) uh = to_host(u, D, st);
+            double nr = 0.0, ray = 0.0;
+            for (int64_t i = 0; i < D; ++i) { nr += g[i] * g[i]; ray += g[i] * uh[i]; }
+            nr = sqrt(nr);
+            lam1 = ray;
+            for (int64_t i = 0; i < D; ++i) uh[i] = g[i] / nr;
+            TPO_CUDA(cudaMemcpyAsync(const_cast<double *>(u), uh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, st));
+        }
+    }
+    deflate_kernel<<<cdiv(D * D, 256), 256, 0, st>>>(G, u, lam1, D, Gd);
     TPO_LAUNCH_CHECK();
     std::vector<double> v0(D * b);
     for (int64_t i = 0; i < D * b; ++i) v0[i] = start_entry((uint64_t)i);
