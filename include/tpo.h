@@ -89,6 +89,38 @@ int tpo_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64
                   void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * a1-a3 sharded across GPUs (one process per GPU).  The rank owns the
+ * contiguous U slice [u0, u1) (n_p rows): Bp = those rows of B (global V column ids) and
+ * Btp = Bp^T (m x n_p, local U column ids).  The CALLER runs the collectives:
+ *    deg_v <- all-reduce(sum) of the shard partials        (once)
+ *    per hop:  Qpart = tpo_shard_vside(Btp, P)              (m x d, raw sums B_p^T P_p)
+ *              Qslice = reduce-scatter(sum) of Qpart over V
+ *              tpo_shard_vscale(Qslice, s_v slice)          (Q[v] *= s_v[v]^2)
+ *              Q = all-gather(Qslice)                        (m x d)
+ *              tpo_shard_uside(Bp, Q, ...)                   (P, or Z and Zhat at the last hop)
+ * which reproduces tpo_propagate on the full graph (the sum of the shard partials of
+ * B^T (s_u . Z) over ranks is the full product).  T = 0 needs no exchange: Z = (1-alpha) X.
+ *   tpo_shard_degrees: deg_u (n_p fp64 out) weighted row sums of Bp; deg_v (m fp64 out) the
+ *     shard's partial V degrees (row sums of Btp).
+ *   tpo_shard_start: s_u = deg_u^-1/2, s_v = deg_v^-1/2 (global deg_v; 1/sqrt(0) := 0), fp32;
+ *     Pp = s_u . (1 - alpha) Xp (n_p x d), the pre-scaled iterate.
+ *   tpo_shard_uside: last = 0 -> Zp <- P = s_u . (c Xp + alpha s_u . B_p Q);
+ *     last = 1 -> Zp <- Z = c Xp + alpha s_u . B_p Q, Zhat_p <- rownorm(Z) (may be NULL).
+ * Workspace of vside / uside: tpo_shard_ws(rows of the CSR, nnz, d).
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_shard_ws(int64_t n_rows, int64_t nnz, int64_t d);
+int tpo_shard_degrees(const tpo_csr_t *Bp, const tpo_csr_t *Btp, double *deg_u, double *deg_v,
+                      void *stream);
+int tpo_shard_start(const double *deg_u, const double *deg_v, int64_t n_p, int64_t m, const float *Xp,
+                    int64_t d, float alpha, float *s_u, float *s_v, float *Pp, void *stream);
+int tpo_shard_vside(const tpo_csr_t *Btp, const float *Pp, int64_t d, float *Qpart, void *ws,
+                    size_t ws_bytes, void *stream);
+int tpo_shard_vscale(float *Q, const float *s_v, int64_t rows, int64_t d, void *stream);
+int tpo_shard_uside(const tpo_csr_t *Bp, const float *Q, const float *Xp, int64_t d, float alpha,
+                    const float *s_u, int32_t last, float *Zp, float *Zhat_p, void *ws,
+                    size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * a4  Haar rotation, Alg. 1 L6-7: Q = the Q factor of the QR
  * decomposition of the d x d Gaussian matrix G, sign-fixed so that diag(R) > 0, which
  * makes Q Haar-distributed and unique.  Host-only, fp64.

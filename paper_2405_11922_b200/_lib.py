@@ -13,7 +13,8 @@ LIB_PATH = os.path.join(HERE, "libtpo.so")
 # exported symbols, as declared in include/tpo.h
 SYMBOLS = [
     "tpo_abi_version", "tpo_last_error", "tpo_launch_count",
-    "tpo_propagate_ws", "tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev_ws", "tpo_haar_q_dev",
+    "tpo_propagate_ws", "tpo_propagate",
+    "tpo_shard_ws", "tpo_shard_degrees", "tpo_shard_start", "tpo_shard_vside", "tpo_shard_vscale", "tpo_shard_uside", "tpo_haar_q", "tpo_haar_q_dev_ws", "tpo_haar_q_dev",
     "tpo_features_ws", "tpo_features",
     "tpo_affinity_matvec_ws", "tpo_affinity_matvec",
     "tpo_gram_ws", "tpo_gram", "tpo_topk_eig_ws", "tpo_topk_eig",
@@ -56,6 +57,13 @@ def lib():
     L.tpo_propagate_ws.argtypes = [i64, i64, i64, i64]
     L.tpo_propagate_ws.restype = sz
     L.tpo_propagate.argtypes = [P, P, vp, i64, f32, i32, vp, vp, vp, sz, vp]
+    L.tpo_shard_ws.argtypes = [i64, i64, i64]
+    L.tpo_shard_ws.restype = sz
+    L.tpo_shard_degrees.argtypes = [P, P, vp, vp, vp]
+    L.tpo_shard_start.argtypes = [vp, vp, i64, i64, vp, i64, f32, vp, vp, vp, vp]
+    L.tpo_shard_vside.argtypes = [P, vp, i64, vp, vp, sz, vp]
+    L.tpo_shard_vscale.argtypes = [vp, vp, i64, i64, vp]
+    L.tpo_shard_uside.argtypes = [P, vp, vp, i64, f32, vp, i32, vp, vp, vp, sz, vp]
     L.tpo_haar_q.argtypes = [vp, i64, vp]
     L.tpo_haar_q_dev_ws.argtypes = [i64]
     L.tpo_haar_q_dev_ws.restype = sz
@@ -78,7 +86,8 @@ def lib():
     L.tpo_run_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32]
     L.tpo_run_ws.restype = sz
     L.tpo_run.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
-    for name in ["tpo_propagate", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_gram", "tpo_topk_eig",
+    for name in ["tpo_propagate", "tpo_shard_degrees", "tpo_shard_start", "tpo_shard_vside", "tpo_shard_vscale",
+                 "tpo_shard_uside", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_gram", "tpo_topk_eig",
                  "tpo_cluster", "tpo_run"]:
         getattr(L, name).restype = C.c_int
     _lib = L

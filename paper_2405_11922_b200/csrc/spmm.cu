@@ -28,7 +28,7 @@ constexpr int CHUNK = 256;           // edges per long-row chunk; also the row-b
 constexpr int WPB = 8;               // warps per block
 constexpr int UNR = 8;               // neighbour rows in flight per warp
 
-enum Epi { EPI_V = 0, EPI_U = 1, EPI_FINAL = 2 };
+enum Epi { EPI_V = 0, EPI_U = 1, EPI_FINAL = 2, EPI_RAW = 3 };
 
 struct Sched {
     int64_t *offsets;      // [n_rows+1] packed exclusive scan: (items << 32) | slots
@@ -58,6 +58,38 @@ __global__ void degree_scale_kernel(const int64_t *__restrict__ rowptr, const fl
         deg = acc;
     }
     if (lane == 0) s[row] = deg > 0.0 ? (float)(1.0 / sqrt(deg)) : 0.0f;
+}
+
+// weighted degrees in fp64 (sharded path: the V-side sums are all-reduced across ranks)
+__global__ void degree_kernel(const int64_t *__restrict__ rowptr, const float *__restrict__ val, int64_t n,
+                              double *__restrict__ deg) {
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const int64_t b = rowptr[row], e = rowptr[row + 1];
+    double acc = 0.0;
+    if (val == nullptr) {
+        acc = lane == 0 ? (double)(e - b) : 0.0;
+    } else {
+        for (int64_t i = b + lane; i < e; i += 32) acc += (double)val[i];
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) deg[row] = acc;
+}
+
+__global__ void inv_sqrt_kernel(const double *__restrict__ deg, int64_t n, float *__restrict__ s) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) s[i] = deg[i] > 0.0 ? (float)(1.0 / sqrt(deg[i])) : 0.0f;
+}
+
+// Q[r] *= s[r]^2 (the V-side scale of a reduce-scattered slice)
+__global__ void vscale_kernel(float4 *__restrict__ Q, const float *__restrict__ s, int64_t rows, int d4) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * d4) return;
+    const float v = s[i / d4];
+    const float s2 = v * v;
+    float4 q = Q[i];
+    Q[i] = make_float4(q.x * s2, q.y * s2, q.z * s2, q.w * s2);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -240,6 +272,10 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_v(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc, float4 x,
                                            float s) {
     const int64_t o = row * (int64_t)a.d4 + c4;
+    if (EPI == EPI_RAW) {
+        if (act) a.out[o] = acc;
+        return;
+    }
     if (EPI == EPI_V) {
         const float s2 = s * s;
         if (act) a.out[o] = make_float4(acc.x * s2, acc.y * s2, acc.z * s2, acc.w * s2);
@@ -267,13 +303,13 @@ __device__ __forceinline__ void epilogue_v(const SpmmArgs &a, int64_t row, int c
 
 template <int EPI>
 __device__ __forceinline__ float4 load_x(const SpmmArgs &a, int64_t row, int c4, bool act) {
-    if (EPI == EPI_V || !act) return make_float4(0.f, 0.f, 0.f, 0.f);
+    if (EPI == EPI_V || EPI == EPI_RAW || !act) return make_float4(0.f, 0.f, 0.f, 0.f);
     return __ldg(a.X + row * (int64_t)a.d4 + c4);
 }
 
 template <int EPI>
 __device__ __forceinline__ void epilogue(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc) {
-    epilogue_v<EPI>(a, row, c4, act, acc, load_x<EPI>(a, row, c4, act), a.scale[row]);
+    epilogue_v<EPI>(a, row, c4, act, acc, load_x<EPI>(a, row, c4, act), EPI == EPI_RAW ? 0.f : a.scale[row]);
 }
 
 // One warp streams the edges of rows [r0, r1) (all short) for one column slice, flushing each
@@ -287,7 +323,7 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int nb = (int)(r1 - rb < 32 ? r1 - rb : 32);
         const int64_t my_end = lane < nb ? a.rowptr[rb + 1 + lane] : 0;     // end of row rb + lane
-        const float my_s = lane < nb ? a.scale[rb + lane] : 0.f;
+        const float my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
         const int64_t e_beg = a.rowptr[rb];
         const int64_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
         int cur = 0;
@@ -531,6 +567,86 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
         } else {
             spmm_launch<EPI_U>(a, sb.s.max_items, sb.s.max_slots, B.val != nullptr, st);
         }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Sharded propagation pieces (U rows split across ranks; collectives done by the caller).
+// ------------------------------------------------------------------------------------------
+size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d) {
+    Arena ar(nullptr, 0);
+    sched_alloc(ar, n_rows, nnz);
+    ar.take<float>((2 * (nnz / CHUNK) + 1) * d);
+    return ar.off + 256;
+}
+
+void shard_degrees_impl(const tpo_csr_t &Bp, const tpo_csr_t &Btp, double *deg_u, double *deg_v, cudaStream_t st) {
+    const int TB = 256;
+    if (Bp.n_rows > 0) degree_kernel<<<cdiv(Bp.n_rows * 32, TB), TB, 0, st>>>(Bp.row_ptr, Bp.val, Bp.n_rows, deg_u);
+    TPO_LAUNCH_CHECK();
+    if (Btp.n_rows > 0) degree_kernel<<<cdiv(Btp.n_rows * 32, TB), TB, 0, st>>>(Btp.row_ptr, Btp.val, Btp.n_rows, deg_v);
+    TPO_LAUNCH_CHECK();
+}
+
+void shard_start_impl(const double *deg_u, const double *deg_v, int64_t n_p, int64_t m, const float *Xp, int64_t d,
+                      float alpha, float *s_u, float *s_v, float *Pp, cudaStream_t st) {
+    const int TB = 256;
+    const float c = alpha < 1.0f ? 1.0f - alpha : 1.0f;
+    if (n_p > 0) inv_sqrt_kernel<<<cdiv(n_p, TB), TB, 0, st>>>(deg_u, n_p, s_u);
+    TPO_LAUNCH_CHECK();
+    if (m > 0) inv_sqrt_kernel<<<cdiv(m, TB), TB, 0, st>>>(deg_v, m, s_v);
+    TPO_LAUNCH_CHECK();
+    const int d4 = (int)(d / 4);
+    if (n_p > 0) init_scaled_kernel<<<cdiv(n_p * d4, TB), TB, 0, st>>>((const float4 *)Xp, s_u, n_p, d4, c, 1, (float4 *)Pp);
+    TPO_LAUNCH_CHECK();
+}
+
+void shard_vside_impl(const tpo_csr_t &Btp, const float *Pp, int64_t d, float *Qpart, Arena &ar, cudaStream_t st) {
+    const int64_t m = Btp.n_rows;
+    if (m == 0) return;
+    const int d4 = (int)(d / 4);
+    SchedBufs sb = sched_alloc(ar, m, Btp.nnz);
+    float *partials = ar.take<float>((2 * (Btp.nnz / CHUNK) + 1) * d);
+    sched_build(sb, Btp.row_ptr, m, st);
+    SpmmArgs a{};
+    a.rowptr = Btp.row_ptr; a.col = Btp.col_idx; a.val = Btp.val;
+    a.src = (const float4 *)Pp; a.d4 = d4; a.nslices = (d4 + 31) / 32;
+    a.sch = sb.s; a.n_rows = m; a.partials = (float4 *)partials;
+    a.out = (float4 *)Qpart;
+    spmm_launch<EPI_RAW>(a, sb.s.max_items, sb.s.max_slots, Btp.val != nullptr, st);
+}
+
+void shard_vscale_impl(float *Q, const float *s_v, int64_t rows, int64_t d, cudaStream_t st) {
+    const int d4 = (int)(d / 4);
+    if (rows == 0) return;
+    vscale_kernel<<<cdiv(rows * d4, 256), 256, 0, st>>>((float4 *)Q, s_v, rows, d4);
+    TPO_LAUNCH_CHECK();
+}
+
+void shard_uside_impl(const tpo_csr_t &Bp, const float *Q, const float *Xp, int64_t d, float alpha, const float *s_u,
+                      bool last, float *Zp, float *Zhat_p, Arena &ar, cudaStream_t st) {
+    const int64_t n = Bp.n_rows;
+    if (n == 0) return;
+    const int d4 = (int)(d / 4);
+    const int nslices = (d4 + 31) / 32;
+    SchedBufs sb = sched_alloc(ar, n, Bp.nnz);
+    float *partials = ar.take<float>((2 * (Bp.nnz / CHUNK) + 1) * d);
+    sched_build(sb, Bp.row_ptr, n, st);
+    SpmmArgs a{};
+    a.rowptr = Bp.row_ptr; a.col = Bp.col_idx; a.val = Bp.val;
+    a.src = (const float4 *)Q; a.d4 = d4; a.nslices = nslices;
+    a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
+    a.scale = s_u; a.X = (const float4 *)Xp; a.c = alpha < 1.0f ? 1.0f - alpha : 1.0f; a.alpha = alpha;
+    a.out = (float4 *)Zp;
+    if (last) {
+        a.out_hat = (nslices == 1 && Zhat_p) ? (float4 *)Zhat_p : nullptr;
+        spmm_launch<EPI_FINAL>(a, sb.s.max_items, sb.s.max_slots, Bp.val != nullptr, st);
+        if (Zhat_p && nslices > 1) {
+            rownorm_kernel<<<cdiv(n * 32, 256), 256, 0, st>>>((const float4 *)Zp, n, d4, (float4 *)Zhat_p);
+            TPO_LAUNCH_CHECK();
+        }
+    } else {
+        spmm_launch<EPI_U>(a, sb.s.max_items, sb.s.max_slots, Bp.val != nullptr, st);
     }
 }
 

@@ -94,6 +94,79 @@ int tpo_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64
     });
 }
 
+size_t tpo_shard_ws(int64_t n_rows, int64_t nnz, int64_t d) { return shard_spmm_ws_bytes(n_rows, nnz, d); }
+
+int tpo_shard_degrees(const tpo_csr_t *Bp, const tpo_csr_t *Btp, double *deg_u, double *deg_v, void *stream) {
+    return guarded([&] {
+        check_csr(Bp, "Bp");
+        check_csr(Btp, "Btp");
+        TPO_REQUIRE(Bp->n_rows == Btp->n_cols && Bp->n_cols == Btp->n_rows && Bp->nnz == Btp->nnz,
+                    "Btp is not shaped as the transpose of Bp");
+        if (Bp->n_rows) TPO_REQUIRE(deg_u != nullptr, "deg_u is NULL");
+        if (Btp->n_rows) TPO_REQUIRE(deg_v != nullptr, "deg_v is NULL");
+        shard_degrees_impl(*Bp, *Btp, deg_u, deg_v, as_stream(stream));
+    });
+}
+
+int tpo_shard_start(const double *deg_u, const double *deg_v, int64_t n_p, int64_t m, const float *Xp, int64_t d,
+                    float alpha, float *s_u, float *s_v, float *Pp, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && m >= 0, "negative size");
+        TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
+        if (n_p) {
+            check_ptr(Xp, "Xp");
+            check_ptr(Pp, "Pp");
+            TPO_REQUIRE(deg_u && s_u, "deg_u / s_u is NULL");
+        }
+        if (m) TPO_REQUIRE(deg_v && s_v, "deg_v / s_v is NULL");
+        shard_start_impl(deg_u, deg_v, n_p, m, Xp, d, alpha, s_u, s_v, Pp, as_stream(stream));
+    });
+}
+
+int tpo_shard_vside(const tpo_csr_t *Btp, const float *Pp, int64_t d, float *Qpart, void *ws, size_t ws_bytes,
+                    void *stream) {
+    return guarded([&] {
+        check_csr(Btp, "Btp");
+        TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        if (Btp->n_rows) check_ptr(Qpart, "Qpart");
+        if (Btp->n_cols) check_ptr(Pp, "Pp");
+        check_ws(ws, ws_bytes, tpo_shard_ws(Btp->n_rows, Btp->nnz, d));
+        Arena ar(ws, ws_bytes);
+        shard_vside_impl(*Btp, Pp, d, Qpart, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_vscale(float *Q, const float *s_v, int64_t rows, int64_t d, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(rows >= 0 && d >= 4 && d % 4 == 0, "bad shape");
+        if (rows) {
+            check_ptr(Q, "Q");
+            TPO_REQUIRE(s_v != nullptr, "s_v is NULL");
+        }
+        shard_vscale_impl(Q, s_v, rows, d, as_stream(stream));
+    });
+}
+
+int tpo_shard_uside(const tpo_csr_t *Bp, const float *Q, const float *Xp, int64_t d, float alpha, const float *s_u,
+                    int32_t last, float *Zp, float *Zhat_p, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        check_csr(Bp, "Bp");
+        TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
+        if (Bp->n_rows) {
+            check_ptr(Xp, "Xp");
+            check_ptr(Zp, "Zp");
+            TPO_REQUIRE(s_u != nullptr, "s_u is NULL");
+        }
+        if (Bp->n_cols) check_ptr(Q, "Q");
+        if (Zhat_p) check_ptr(Zhat_p, "Zhat_p");
+        check_ws(ws, ws_bytes, tpo_shard_ws(Bp->n_rows, Bp->nnz, d));
+        Arena ar(ws, ws_bytes);
+        shard_uside_impl(*Bp, Q, Xp, d, alpha, s_u, last != 0, Zp, Zhat_p, ar, as_stream(stream));
+    });
+}
+
 int tpo_haar_q(const double *G, int64_t d, double *Q) {
     return guarded([&] {
         TPO_REQUIRE(G != nullptr && Q != nullptr, "G and Q must be host pointers");

@@ -91,6 +91,15 @@ int sm_count();
 // ----------------------------------------------------------------------------------------
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
                     int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st);
+// sharded propagation pieces (spmm.cu)
+size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d);
+void shard_degrees_impl(const tpo_csr_t &Bp, const tpo_csr_t &Btp, double *deg_u, double *deg_v, cudaStream_t st);
+void shard_start_impl(const double *deg_u, const double *deg_v, int64_t n_p, int64_t m, const float *Xp, int64_t d,
+                      float alpha, float *s_u, float *s_v, float *Pp, cudaStream_t st);
+void shard_vside_impl(const tpo_csr_t &Btp, const float *Pp, int64_t d, float *Qpart, Arena &ar, cudaStream_t st);
+void shard_vscale_impl(float *Q, const float *s_v, int64_t rows, int64_t d, cudaStream_t st);
+void shard_uside_impl(const tpo_csr_t &Bp, const float *Q, const float *Xp, int64_t d, float alpha, const float *s_u,
+                      bool last, float *Zp, float *Zhat_p, Arena &ar, cudaStream_t st);
 void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv,
                    double *r_out, Arena &ar, cudaStream_t st);
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y,
