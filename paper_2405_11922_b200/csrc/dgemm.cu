@@ -1,0 +1,250 @@
+// Small and medium fp64 dense products of the host-sized linear algebra (Haar rotation of
+// Alg. 1 L6-7; the D x D eigen-iteration of a7; CholeskyQR2), plus the
+// device Cholesky-inverse that keeps CholeskyQR2 free of host round trips.
+//
+//   dgemm:     C = beta C + alpha op(A) B, row-major, op(A) = A (M x K) or A^T (A is K x M).
+//              64 x 64 output tile per CTA, 16-deep K slabs staged in shared memory, each
+//              thread owns a 4 x 4 register tile strided by 16 (conflict-free smem reads,
+//              coalesced stores).  When the grid of output tiles cannot fill the GPU the K
+//              range is split; each split writes an fp64 partial and splitk_reduce adds them
+//              in split order (deterministic: no atomics).
+//   chol_inv:  one CTA; for the b x b Gram g (b <= 112) of CholeskyQR: S = diag(g)^{-1/2},
+//              S g S = C^T C (upper C), writes Ci = S C^{-1} so that V <- V Ci has orthonormal
+//              columns; a non-SPD or non-finite pivot sets *flag (checked by the caller at its
+//              next synchronisation point -> TPO_ENUMERIC).
+#include <algorithm>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, NTH = 256;
+
+// BNT = 64 (4 x 4 register tile per thread) or 32 (2 x 4, for skinny right-hand sides).
+// The next K slab is prefetched into registers while the current one is multiplied.
+template <bool TA, int BNT>
+__global__ void __launch_bounds__(NTH) dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
+                                                    const double *__restrict__ A, int64_t lda,
+                                                    const double *__restrict__ B, int64_t ldb, double beta,
+                                                    double *__restrict__ C, int64_t ldc, int64_t kchunk,
+                                                    double *__restrict__ part) {
+    constexpr int TXN = BNT / 4, TYN = NTH / TXN, RM = BM / TYN;
+    constexpr int NA = (BK * BM) / NTH, NB = (BK * BNT) / NTH;
+    __shared__ double As[BK][BM + 1];
+    __shared__ double Bs[BK][BNT + 1];
+    const int t = threadIdx.x, tx = t % TXN, ty = t / TXN;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BNT;
+    const int64_t k0 = (int64_t)blockIdx.z * kchunk, k1 = min(K, k0 + kchunk);
+    double acc[RM][4];
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    double ra[NA], rb[NB];
+    auto fetch = [&](int64_t kk) {
+#pragma unroll
+        for (int r = 0; r < NA; ++r) {
+            const int i = t + r * NTH;
+            int k, m;
+            if (TA) { k = i / BM; m = i % BM; } else { m = i / BK; k = i % BK; }
+            const int64_t gk = kk + k, gm = m0 + m;
+            ra[r] = (gk < k1 && gm < M) ? (TA ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+            const int i = t + r * NTH;
+            const int k = i / BNT, nn = i % BNT;
+            const int64_t gk = kk + k, gn = n0 + nn;
+            rb[r] = (gk < k1 && gn < N) ? B[gk * ldb + gn] : 0.0;
+        }
+    };
+    if (k0 < k1) fetch(k0);
+    for (int64_t kk = k0; kk < k1; kk += BK) {
+#pragma unroll
+        for (int r = 0; r < NA; ++r) {
+            const int i = t + r * NTH;
+            if (TA) As[i / BM][i % BM] = ra[r]; else As[i % BK][i / BK] = ra[r];
+        }
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+            const int i = t + r * NTH;
+            Bs[i / BNT][i % BNT] = rb[r];
+        }
+        __syncthreads();
+        if (kk + BK < k1) fetch(kk + BK);
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+            double av[RM], bv[4];
+#pragma unroll
+            for (int i = 0; i < RM; ++i) av[i] = As[k][ty + TYN * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[k][tx + TXN * j];
+#pragma unroll
+            for (int i = 0; i < RM; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+        const int64_t gm = m0 + ty + TYN * i;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gn = n0 + tx + TXN * j;
+            if (gn >= N) continue;
+            if (part) {
+                part[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+            } else {
+                const double v = alpha * acc[i][j];
+                C[gm * ldc + gn] = beta == 0.0 ? v : fma(beta, C[gm * ldc + gn], v);
+            }
+        }
+    }
+}
+
+__global__ void splitk_reduce_kernel(const double *__restrict__ part, int64_t S, int64_t M, int64_t N, double alpha,
+                                     double beta, double *__restrict__ C, int64_t ldc) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M * N) return;
+    double s = 0.0;
+    for (int64_t z = 0; z < S; ++z) s += part[z * M * N + i];
+    const int64_t r = i / N, c = i - r * N;
+    const double v = alpha * s;
+    C[r * ldc + c] = beta == 0.0 ? v : fma(beta, C[r * ldc + c], v);
+}
+
+int64_t splits_for(int64_t M, int64_t N, int64_t K) {
+    const int64_t tiles = cdiv(M, BM) * cdiv(N, N <= 32 ? 32 : BN);
+    const int64_t want = cdiv(2 * 148, tiles);
+    return std::max<int64_t>(1, std::min<int64_t>(want, cdiv(K, 4 * BK)));
+}
+
+// ---------------------------------------------------------------------------------------
+// chol_inv (one CTA of TPR threads per row, two b x b matrices in shared memory, b <= CI_MAX)
+//   Cholesky by Schur complements: step j updates rows r > j of the upper triangle with
+//   A[r][c] -= A[j][r] A[j][c] / A[j][j]; row j is final after step j (one barrier per step)
+//   and is scaled by 1/sqrt(A[j][j]) at the end.
+//   Inverse X = C^{-1} by back substitution on unscaled rows: for j = b-1 .. 0,
+//   X[r][c] -= C[r][j] X[j][c] / C[j][j] for r < j, c >= j (one barrier per step); row j
+//   is final once step j starts, and every row is divided by its pivot at the end.
+// ---------------------------------------------------------------------------------------
+constexpr int CI_MAX = 112;
+constexpr int TPR = 4;     // threads per row
+
+__global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__restrict__ g, int b,
+                                                                double *__restrict__ Ci, int *__restrict__ flag) {
+    extern __shared__ double sm[];
+    const int p = b + 1, t = threadIdx.x, nt = blockDim.x;
+    const int my_r = t / TPR, my_q = t % TPR;        // row owned, column phase
+    double *U = sm;                      // b x b (pitch p): equilibrated Gram -> Cholesky factor
+    double *X = sm + b * p;              // b x b (pitch p): inverse
+    double *sc = X + b * p;              // b: equilibration
+    double *pinv = sc + b;               // b: 1 / pivot
+    for (int i = t; i < b; i += nt) {
+        const double d = g[(int64_t)i * b + i];
+        sc[i] = (d > 0.0 && isfinite(d)) ? rsqrt(d) : 0.0;
+    }
+    __syncthreads();
+    for (int i = t; i < b * b; i += nt) {
+        const int r = i / b, c = i - r * b;
+        U[r * p + c] = c >= r ? g[i] * sc[r] * sc[c] : 0.0;
+        X[r * p + c] = r == c ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < b - 1; ++j) {
+        if (my_r > j && my_r < b) {
+            const double d = U[j * p + j];
+            const double f = (d > 0.0 && isfinite(d)) ? U[j * p + my_r] / d : 0.0;
+            for (int c = my_r + my_q; c < b; c += TPR) U[my_r * p + c] -= f * U[j * p + c];
+        }
+        __syncthreads();
+    }
+    int bad = 0;
+    if (my_r < b) {                                  // C[r][c] = A_r[r][c] / sqrt(A_r[r][r])
+        const double d = U[my_r * p + my_r];
+        const bool ok = d > 0.0 && isfinite(d);
+        bad = !ok;
+        const double s = ok ? rsqrt(d) : 1.0;
+        for (int c = my_r + 1 + my_q; c < b; c += TPR) U[my_r * p + c] *= s;
+    }
+    __syncthreads();
+    if (my_r < b && my_q == 0) {
+        const double d = U[my_r * p + my_r];
+        const double cd = (d > 0.0 && isfinite(d)) ? sqrt(d) : 1.0;
+        U[my_r * p + my_r] = cd;
+        pinv[my_r] = 1.0 / cd;
+    }
+    __syncthreads();
+    for (int j = b - 1; j > 0; --j) {
+        if (my_r < j) {
+            const double f = U[my_r * p + j] * pinv[j];
+            for (int c = j + my_q; c < b; c += TPR) X[my_r * p + c] -= f * X[j * p + c];
+        }
+        __syncthreads();
+    }
+    for (int i = t; i < b * b; i += nt) {
+        const int r = i / b, c = i - r * b;
+        Ci[i] = c >= r ? X[r * p + c] * pinv[r] * sc[r] : 0.0;
+    }
+    bad = __syncthreads_or(bad);
+    if (t == 0) {
+        bool z = false;
+        for (int i = 0; i < b; ++i) z |= sc[i] == 0.0;
+        if ((bad || z) && flag) *flag = 1;
+    }
+}
+
+}  // namespace
+
+// Bound for every K and every M' <= M, N' <= N: S <= 296 / tiles + 1 and M N <= 4096 tiles,
+// so the split-K partials hold at most 296 * 4096 + M N doubles.
+size_t dgemm_ws(int64_t M, int64_t N, int64_t K) {
+    (void)K;
+    return align_up(sizeof(double) * (size_t)(2 * 148 * BM * BN + 2 * M * N) + 1) + 256;
+}
+
+void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, const double *B,
+           int64_t ldb, double beta, double *C, int64_t ldc, Arena &ar, cudaStream_t st) {
+    if (M <= 0 || N <= 0) return;
+    if (K <= 0) {   // empty sum: C = beta C
+        splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(nullptr, 0, M, N, alpha, beta, C, ldc);
+        TPO_LAUNCH_CHECK();
+        return;
+    }
+    const int64_t S = splits_for(M, N, K);
+    const int64_t kchunk = cdiv(cdiv(K, S), BK) * BK;
+    const int64_t Sr = cdiv(K, kchunk);
+    const bool skinny = N <= 32;
+    const dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, skinny ? 32 : BN), (unsigned)Sr);
+    const size_t mark = ar.off;
+    double *part = Sr > 1 ? ar.take<double>(Sr * M * N) : nullptr;
+    if (transA && skinny)
+        dgemm_kernel<true, 32><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
+    else if (transA)
+        dgemm_kernel<true, 64><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
+    else if (skinny)
+        dgemm_kernel<false, 32><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
+    else
+        dgemm_kernel<false, 64><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
+    TPO_LAUNCH_CHECK();
+    if (Sr > 1) {
+        splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(part, Sr, M, N, alpha, beta, C, ldc);
+        TPO_LAUNCH_CHECK();
+    }
+    ar.off = mark;
+}
+
+void chol_inv_device(const double *g, int64_t b, double *Ci, int *flag, cudaStream_t st) {
+    TPO_REQUIRE(b >= 1 && b <= CI_MAX, "chol_inv: block width out of range");
+    const size_t smem = sizeof(double) * (size_t)(2 * b * (b + 1) + 2 * b);
+    if (smem > 48 * 1024)
+        TPO_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = (int)cdiv(b * TPR, 32) * 32;
+    chol_inv_kernel<<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
+    TPO_LAUNCH_CHECK();
+}
+
+}  // namespace tpo

@@ -92,35 +92,94 @@ double start_entry(uint64_t i) {
 
 // CholeskyQR2 of a device fp64 matrix V (rows x b) in place (tmp: rows x b).  Each pass
 // factors the column-equilibrated Gram S G S = C^T C (S = diag(G_ii^-1/2)), so V <- V S C^-1.
-void cholqr2_f64(double *V, double *tmp, int64_t rows, int64_t b, Arena &ar, cudaStream_t st) {
+// For b <= 112 everything stays on the device (dgemm + one-CTA chol_inv); a failed
+// factorisation sets *flag, which the caller checks at its next synchronisation point.
+void cholqr2_f64(double *V, double *tmp, int64_t rows, int64_t b, int *flag, Arena &ar, cudaStream_t st) {
     for (int pass = 0; pass < 2; ++pass) {
         const size_t mark = ar.off;
         double *g = ar.take<double>(b * b);
-        tsgemm_AtB_f64f64(V, b, V, b, rows, b, b, g, ar, st);
-        std::vector<double> gh = to_host(g, b * b, st), C(b * b), Ci(b * b), sc(b);
-        for (int64_t i = 0; i < b; ++i) sc[i] = gh[i * b + i] > 0.0 ? 1.0 / sqrt(gh[i * b + i]) : 0.0;
-        for (int64_t i = 0; i < b; ++i)
-            for (int64_t j = 0; j < b; ++j) gh[i * b + j] *= sc[i] * sc[j];
-        if (!host_cholesky_upper(b, gh.data(), C.data()))
-            throw Error(TPO_ENUMERIC, "CholeskyQR2: Gram matrix not positive definite");
-        host_upper_inverse(b, C.data(), Ci.data());
-        for (int64_t i = 0; i < b; ++i)
-            for (int64_t j = 0; j < b; ++j) Ci[i * b + j] *= sc[i];
-        double *ci = to_dev(ar, Ci, st);
-        tsgemm_AW_dd(V, b, ci, rows, b, b, tmp, b, st);
+        dgemm(true, b, b, rows, 1.0, V, b, V, b, 0.0, g, b, ar, st);
+        double *ci = ar.take<double>(b * b);
+        if (b <= 112) {
+            chol_inv_device(g, b, ci, flag, st);
+        } else {
+            std::vector<double> gh = to_host(g, b * b, st), C(b * b), Ci(b * b), sc(b);
+            for (int64_t i = 0; i < b; ++i) sc[i] = gh[i * b + i] > 0.0 ? 1.0 / sqrt(gh[i * b + i]) : 0.0;
+            for (int64_t i = 0; i < b; ++i)
+                for (int64_t j = 0; j < b; ++j) gh[i * b + j] *= sc[i] * sc[j];
+            if (!host_cholesky_upper(b, gh.data(), C.data()))
+                throw Error(TPO_ENUMERIC, "CholeskyQR2: Gram matrix not positive definite");
+            host_upper_inverse(b, C.data(), Ci.data());
+            for (int64_t i = 0; i < b; ++i)
+                for (int64_t j = 0; j < b; ++j) Ci[i * b + j] *= sc[i];
+            TPO_CUDA(cudaMemcpyAsync(ci, Ci.data(), sizeof(double) * b * b, cudaMemcpyHostToDevice, st));
+            TPO_CUDA(cudaStreamSynchronize(st));
+        }
+        dgemm(false, rows, b, b, 1.0, V, b, ci, b, 0.0, tmp, b, ar, st);
         TPO_CUDA(cudaMemcpyAsync(V, tmp, sizeof(double) * rows * b, cudaMemcpyDeviceToDevice, st));
-        TPO_CUDA(cudaStreamSynchronize(st));
         ar.off = mark;
     }
 }
 
+// Reads the device failure flag of the CholeskyQR steps (synchronises the stream).
+void check_flag(const int *flag, cudaStream_t st, const char *what) {
+    int h = 0;
+    TPO_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    if (h) throw Error(TPO_ENUMERIC, std::string(what) + ": Gram matrix not positive definite");
+}
+
 // Gd = G - lam u u^T (deflation of the top eigenpair, see gram_topk)
-__global__ void deflate_kernel(const double *__restrict__ G, const double *__restrict__ u, double lam, int64_t D,
-                               double *__restrict__ Gd) {
+__global__ void deflate_kernel(const double *__restrict__ G, const double *__restrict__ u,
+                               const double *__restrict__ lam, int64_t D, double *__restrict__ Gd) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= D * D) return;
     const int64_t a = i / D, b = i - a * D;
-    Gd[i] = G[i] - lam * u[a] * u[b];
+    Gd[i] = G[i] - (*lam) * u[a] * u[b];
+}
+
+// u = r / ||r|| (one CTA, fixed-order tree); *zero = 1 when r = 0.
+__global__ void __launch_bounds__(1024) unit_vec_kernel(const double *__restrict__ r, double *__restrict__ u,
+                                                        int64_t D, int *__restrict__ zero) {
+    __shared__ double s1[1024];
+    const int t = threadIdx.x;
+    double nr = 0.0;
+    for (int64_t i = t; i < D; i += 1024) nr += r[i] * r[i];
+    s1[t] = nr;
+    __syncthreads();
+    for (int o = 512; o; o >>= 1) {
+        if (t < o) s1[t] += s1[t + o];
+        __syncthreads();
+    }
+    if (!(s1[0] > 0.0)) {
+        if (t == 0) *zero = 1;
+        return;
+    }
+    const double inv = 1.0 / sqrt(s1[0]);
+    for (int64_t i = t; i < D; i += 1024) u[i] = r[i] * inv;
+}
+
+// One power step finished on the device (one CTA, fixed-order tree): given gu = G u,
+// lam = gu . u (Rayleigh quotient, u unit), u <- gu / ||gu||.
+__global__ void __launch_bounds__(1024) power_step_kernel(const double *__restrict__ gu, double *__restrict__ u,
+                                                          int64_t D, double *__restrict__ lam) {
+    __shared__ double s1[1024], s2[1024];
+    const int t = threadIdx.x;
+    double nr = 0.0, ray = 0.0;
+    for (int64_t i = t; i < D; i += 1024) {
+        nr += gu[i] * gu[i];
+        ray += gu[i] * u[i];
+    }
+    s1[t] = nr;
+    s2[t] = ray;
+    __syncthreads();
+    for (int o = 512; o; o >>= 1) {
+        if (t < o) { s1[t] += s1[t + o]; s2[t] += s2[t + o]; }
+        __syncthreads();
+    }
+    const double inv = 1.0 / sqrt(s1[0]);
+    for (int64_t i = t; i < D; i += 1024) u[i] = gu[i] * inv;
+    if (t == 0) *lam = s2[0];
 }
 
 // out = s1 * GY - s2 * Y1 - (Y0 ? Y0 : 0): one step of the Chebyshev three-term recurrence
@@ -201,21 +260,13 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     // u = r/||r|| is the top eigenvector of the exact Gram; refine it to the top eigenvector of
     // the computed G by a few power steps (rate lambda_2 / lambda_1 ~ 0.03), then deflate
     // Gd = G - lambda_1 u u^T with lambda_1 = u^T G u.
-    double lam1 = 1.0;
-    {
-        double *gu = Y0;
-        std::vector<double> uh;
-        for (int it = 0; it < 6; ++it) {
-            tsgemm_AW_dd(G, D, u, D, D, 1, gu, 1, st);
-            std::vector<double> g = to_host(gu, D, st);
-            if (uh.empty()) uh = to_host(u, D, st);
-            double nr = 0.0, ray = 0.0;
-            for (int64_t i = 0; i < D; ++i) { nr += g[i] * g[i]; ray += g[i] * uh[i]; }
-            nr = sqrt(nr);
-            lam1 = ray;
-            for (int64_t i = 0; i < D; ++i) uh[i] = g[i] / nr;
-            TPO_CUDA(cudaMemcpyAsync(const_cast<double *>(u), uh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, st));
-        }
+    double *lam1 = ar.take<double>(1);
+    int *flag = ar.take<int>(1);
+    TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    for (int it = 0; it < 6; ++it) {
+        dgemm(false, D, 1, D, 1.0, G, D, u, 1, 0.0, Y0, 1, ar, st);
+        power_step_kernel<<<1, 1024, 0, st>>>(Y0, u, D, lam1);
+        TPO_LAUNCH_CHECK();
     }
     deflate_kernel<<<cdiv(D * D, 256), 256, 0, st>>>(G, u, lam1, D, Gd);
     TPO_LAUNCH_CHECK();
@@ -224,11 +275,11 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     TPO_CUDA(cudaMemcpyAsync(V, v0.data(), sizeof(double) * D * b, cudaMemcpyHostToDevice, st));
     auto orth_against_u = [&]() {
         const size_t m2 = ar.off;
-        tsgemm_AtB_f64f64(u, 1, V, b, D, 1, b, cvec, ar, st);
+        dgemm(true, 1, b, D, 1.0, u, 1, V, b, 0.0, cvec, b, ar, st);
         ar.off = m2;
         project_out_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(V, u, cvec, D, (int)b);
         TPO_LAUNCH_CHECK();
-        cholqr2_f64(V, T, D, b, ar, st);
+        cholqr2_f64(V, T, D, b, flag, ar, st);
     };
     orth_against_u();
     const int m = 8, max_rounds = 60;
@@ -238,11 +289,11 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         if (round > 0) {   // Chebyshev filter p_m(Gd) V, damping [0, bnd]
             const double c = 0.5 * bnd, e = 0.5 * bnd;
             TPO_CUDA(cudaMemcpyAsync(Y0, V, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
-            tsgemm_AW_dd(Gd, D, Y0, D, D, b, GY, b, st);
+            dgemm(false, D, b, D, 1.0, Gd, D, Y0, b, 0.0, GY, b, ar, st);
             cheb_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(GY, Y0, nullptr, D * b, 1.0 / e, c / e, Y1);
             TPO_LAUNCH_CHECK();
             for (int j = 2; j <= m; ++j) {
-                tsgemm_AW_dd(Gd, D, Y1, D, D, b, GY, b, st);
+                dgemm(false, D, b, D, 1.0, Gd, D, Y1, b, 0.0, GY, b, ar, st);
                 cheb_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(GY, Y1, Y0, D * b, 2.0 / e, 2.0 * c / e, Y0);
                 TPO_LAUNCH_CHECK();
                 std::swap(Y0, Y1);
@@ -253,10 +304,10 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         // Rayleigh-Ritz with the full G on Z = [u, V]
         stack_kernel<<<cdiv(D * bz, 256), 256, 0, st>>>(u, V, D, (int)b, Z);
         TPO_LAUNCH_CHECK();
-        tsgemm_AW_dd(G, D, Z, D, D, bz, W, bz, st);
+        dgemm(false, D, bz, D, 1.0, G, D, Z, bz, 0.0, W, bz, ar, st);
         const size_t mark = ar.off;
         double *h = ar.take<double>(bz * bz);
-        tsgemm_AtB_f64f64(Z, bz, W, bz, D, bz, bz, h, ar, st);
+        dgemm(true, bz, bz, D, 1.0, Z, bz, W, bz, 0.0, h, bz, ar, st);
         std::vector<double> H = to_host(h, bz * bz, st);
         host_sym_eig_top(bz, H.data(), bz, w.data(), E.data());
         // explicit residuals r_l = ||G x_l - w_l x_l|| of the top-k Ritz pairs (x = Z e, G x = W e)
@@ -265,14 +316,15 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
             for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * bz + l];
         double *ek = to_dev(ar, Ek, st), *dw = to_dev(ar, wk, st);
         double *gx = ar.take<double>(D * k), *res = ar.take<double>(k);
-        tsgemm_AW_dd(Z, bz, ek, D, bz, k, Psi64, k, st);              // Ritz vectors x
-        tsgemm_AW_dd(W, bz, ek, D, bz, k, gx, k, st);                 // G x
+        dgemm(false, D, k, bz, 1.0, Z, bz, ek, k, 0.0, Psi64, k, ar, st);   // Ritz vectors x
+        dgemm(false, D, k, bz, 1.0, W, bz, ek, k, 0.0, gx, k, ar, st);      // G x
         residual_kernel<<<k, 256, 0, st>>>(gx, Psi64, dw, D, k, res);
         TPO_LAUNCH_CHECK();
         const std::vector<double> rh = to_host(res, k, st);
         double rmax = 0.0;
         for (int l = 0; l < k; ++l) rmax = std::max(rmax, rh[l]);
         if (rmax <= 1e-10 * fabs(w[0]) || round == max_rounds) {
+            check_flag(flag, st, "top-k subspace iteration (CholeskyQR2)");
             lam.assign(w.begin(), w.begin() + k);
             ar.off = mark;
             return;
@@ -368,39 +420,37 @@ __global__ void copy2d_kernel(const double *__restrict__ src, int64_t lds, doubl
 
 size_t haar_q_ws_bytes(int64_t d) {
     const int64_t bw = std::min<int64_t>(64, d);
-    return 3 * align_up(sizeof(double) * d * d) + 4 * align_up(sizeof(double) * d * bw) +
-           tsgemm_ws(d, d, bw) + 16 * align_up(sizeof(double) * bw * bw + 8) + 8192;
+    return 2 * align_up(sizeof(double) * d * d) + 3 * align_up(sizeof(double) * d * bw) +
+           2 * align_up(sizeof(double) * bw * bw + 8) + dgemm_ws(d, bw, d) + 8192;
 }
 
 // Alg. 1 L6-7 on the device: Q of the unique QR (diag(R) > 0) of the d x d Gaussian G by
 // block classical Gram-Schmidt with re-orthogonalisation (BCGS2) over 64-column panels, each
 // panel orthonormalised by CholeskyQR2.  R is block upper triangular with upper triangular,
-// positive-diagonal blocks, so Q is the same unique factor the host routine returns.
+// positive-diagonal blocks, so Q is the same unique factor the host routine returns.  No
+// host round trip until the final failure-flag check.
 void haar_q_device(const double *G_host, int64_t d, float *Q_out, Arena &ar, cudaStream_t st) {
     const int64_t bw = std::min<int64_t>(64, d);
     double *A = ar.take<double>(d * d), *Q = ar.take<double>(d * d);
     double *P = ar.take<double>(d * bw), *T = ar.take<double>(d * bw), *Cm = ar.take<double>(d * bw);
+    int *flag = ar.take<int>(1);
+    TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
     TPO_CUDA(cudaMemcpyAsync(A, G_host, sizeof(double) * d * d, cudaMemcpyHostToDevice, st));
     for (int64_t j0 = 0; j0 < d; j0 += bw) {
         const int64_t w = std::min<int64_t>(bw, d - j0);
         copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(A + j0, d, P, w, d, w, nullptr, 0);
         TPO_LAUNCH_CHECK();
-        if (j0 > 0) {
-            for (int pass = 0; pass < 2; ++pass) {
-                const size_t mark = ar.off;
-                tsgemm_AtB_f64f64(Q, d, P, w, d, j0, w, Cm, ar, st);        // C = Q_<j^T P
-                ar.off = mark;
-                tsgemm_AW_dd(Q, d, Cm, d, j0, w, T, w, st);                 // T = Q_<j C
-                copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(P, w, P, w, d, w, T, w);   // P -= T
-                TPO_LAUNCH_CHECK();
-            }
+        for (int pass = 0; j0 > 0 && pass < 2; ++pass) {
+            dgemm(true, j0, w, d, 1.0, Q, d, P, w, 0.0, Cm, w, ar, st);     // C = Q_<j^T P
+            dgemm(false, d, w, j0, -1.0, Q, d, Cm, w, 1.0, P, w, ar, st);   // P -= Q_<j C
         }
-        cholqr2_f64(P, T, d, w, ar, st);
+        cholqr2_f64(P, T, d, w, flag, ar, st);
         copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(P, w, Q + j0, d, d, w, nullptr, 0);
         TPO_LAUNCH_CHECK();
     }
     cast_f64_f32<<<cdiv(d * d, 256), 256, 0, st>>>(Q, d * d, Q_out);
     TPO_LAUNCH_CHECK();
+    check_flag(flag, st, "Haar rotation (panel CholeskyQR2)");
 }
 
 size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p) {
@@ -412,12 +462,13 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
     s += 8 * align_up(sizeof(double) * D * (std::max(b, bh) + 1)) + 8 * align_up(sizeof(double) * (b + 1) * (b + 1) + 8);
     s += 2 * align_up(sizeof(double) * D * k) + tsgemm_ws(n, k, k) + align_up(sizeof(float) * n * k);
     if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
+    s += dgemm_ws(std::max(n, D), std::max(b, bh) + 1, 0) + 2 * align_up(sizeof(double) * (std::max(b, bh) + 1) * (std::max(b, bh) + 1));
     return s + 64 * 256;
 }
 
 void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p,
                    int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi, Arena &ar,
-                   cudaStream_t st) {
+                   cudaStream_t st, const double *r_colsum) {
     std::vector<double> lam;
     double *Psi64 = ar.take<double>(D * k);
     if (mode == TPO_EIG_EXACT) {
@@ -427,17 +478,19 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
         gram_tc(Rp, dinv, n, D, G, ar, st);
         ar.off = mark;
         {   // u = r / ||r||, r = R'^T 1 (the top eigenvector of the trivial pair)
-            double *ones = ar.take<double>(n);
-            fill_f64<<<cdiv(n, 256), 256, 0, st>>>(ones, n, 1.0);
+            double *r = const_cast<double *>(r_colsum);
+            if (!r) {
+                r = ar.take<double>(D);
+                colsum_f64(Rp, n, D, r, ar, st);
+            }
+            int *zflag = ar.take<int>(1);
+            TPO_CUDA(cudaMemsetAsync(zflag, 0, sizeof(int), st));
+            unit_vec_kernel<<<1, 1024, 0, st>>>(r, u, D, zflag);
             TPO_LAUNCH_CHECK();
-            tsgemm_AtB_f32f64(Rp, D, nullptr, ones, 1, n, D, 1, u, ar, st);
-            std::vector<double> uh = to_host(u, D, st);
-            double nr = 0.0;
-            for (double x : uh) nr += x * x;
-            nr = sqrt(nr);
-            if (!(nr > 0.0)) throw Error(TPO_ENUMERIC, "top-k: R' has zero column sums");
-            for (double &x : uh) x /= nr;
-            TPO_CUDA(cudaMemcpyAsync(u, uh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, st));
+            int zh = 0;
+            TPO_CUDA(cudaMemcpyAsync(&zh, zflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+            TPO_CUDA(cudaStreamSynchronize(st));
+            if (zh) throw Error(TPO_ENUMERIC, "top-k: R' has zero column sums");
             ar.off = mark;
         }
         gram_topk(G, u, D, k, lam, Psi64, ar, st);
@@ -449,15 +502,18 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
         std::vector<double> omd(om.begin(), om.end());
         double *Om = to_dev(ar, omd, st);
         double *Y = ar.take<double>(n * b), *T = ar.take<double>(n * b), *Bm = ar.take<double>(D * b);
+        int *flag = ar.take<int>(1);
+        TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
         tsgemm_AW_f64(Rp, D, dinv, Om, n, D, b, Y, b, st);
-        cholqr2_f64(Y, T, n, b, ar, st);
+        cholqr2_f64(Y, T, n, b, flag, ar, st);
         for (int it = 0; it < q; ++it) {
             const size_t mark = ar.off;
             tsgemm_AtB_f32f64(Rp, D, dinv, Y, b, n, D, b, Bm, ar, st);
             ar.off = mark;
             tsgemm_AW_f64(Rp, D, dinv, Bm, n, D, b, Y, b, st);
-            cholqr2_f64(Y, T, n, b, ar, st);
+            cholqr2_f64(Y, T, n, b, flag, ar, st);
         }
+        check_flag(flag, st, "randomised SVD (CholeskyQR2)");
         const size_t mark = ar.off;
         tsgemm_AtB_f32f64(Rp, D, dinv, Y, b, n, D, b, Bm, ar, st);     // B = R^T Y (D x b)
         double *g = ar.take<double>(b * b);

@@ -65,7 +65,25 @@ int row_groups_for(int64_t n, int d) {
     return (int)std::max<int64_t>(1, std::min<int64_t>({want, row_tiles, (int64_t)ROW_GROUPS_MAX * 4}));
 }
 
+void colsum_run(const float *Rp, int64_t n, int D, int G, double *part, double *r, cudaStream_t st) {
+    const int64_t rows_per = cdiv(n, G);
+    colsum_part_kernel<<<dim3(G, cdiv(D, 256)), 256, 0, st>>>(Rp, n, D, rows_per, part);
+    TPO_LAUNCH_CHECK();
+    colsum_reduce_kernel<<<cdiv(D, 256), 256, 0, st>>>(part, G, D, r);
+    TPO_LAUNCH_CHECK();
+}
+
 }  // namespace
+
+// r = sum_i R'[i] (fp64, deterministic), the same routine tpo_features uses.
+void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cudaStream_t st) {
+    const int G = row_groups_for(n, (int)(D / 2));
+    const size_t mark = ar.off;
+    double *part = ar.take<double>((size_t)G * D);
+    if (n == 0) TPO_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * D, st));
+    else colsum_run(Rp, n, (int)D, G, part, r, st);
+    ar.off = mark;
+}
 
 size_t features_ws_bytes(int64_t n, int64_t d) {
     Arena ar(nullptr, 0);
@@ -89,11 +107,7 @@ void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, floa
         features_tc(Zhat, n, d, Q, Rp, ar, st);
         ar.off = mark;
     }
-    const int64_t rows_per = cdiv(n, G);
-    colsum_part_kernel<<<dim3(G, cdiv(D, 256)), 256, 0, st>>>(Rp, n, D, rows_per, part);
-    TPO_LAUNCH_CHECK();
-    colsum_reduce_kernel<<<cdiv(D, 256), 256, 0, st>>>(part, G, D, r);
-    TPO_LAUNCH_CHECK();
+    colsum_run(Rp, n, D, G, part, r, st);
     const int TB = 256;
     dinv_kernel<<<cdiv(n * 32, TB), TB, sizeof(double) * D, st>>>(Rp, n, D, r, dinv);
     TPO_LAUNCH_CHECK();

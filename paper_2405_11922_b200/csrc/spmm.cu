@@ -19,6 +19,10 @@
 //     through the epilogue as the stream crosses them (empty rows included).  Rows longer
 //     than CHUNK edges are split into CHUNK-edge items that write partial sums, added in
 //     chunk order by a fix-up kernel (deterministic: no float atomics anywhere).
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "tpo_internal.cuh"
 
 namespace tpo {
@@ -210,7 +214,8 @@ struct SpmmArgs {
     const int32_t *col;
     const float *val;
     const float4 *src;        // gathered operand, row stride d4 float4
-    int d4, nslices;
+    int d4, nslices;          // nslices: 32-float4 slices (fix-up granularity)
+    int ngroups;              // column groups of SL slices (gather granularity)
     Sched sch;
     int64_t n_rows;
     float4 *partials;         // [slots][d4]
@@ -231,11 +236,15 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 v) {
     return a;
 }
 
-template <bool WEIGHTED>
-__device__ __forceinline__ float4 gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, int c4, bool act) {
+// One warp gathers the SL float4 columns c4[0..SL) (stride 32) of the CSR rows in edges
+// [beg, end) into acc[].
+template <bool WEIGHTED, int SL>
+__device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, const int (&c4)[SL],
+                                            const bool (&act)[SL], float4 (&acc)[SL]) {
     const int lane = threadIdx.x & 31;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 *__restrict__ src = a.src + c4;
+    constexpr int U = UNR / SL > 0 ? UNR / SL : 1;
+#pragma unroll
+    for (int s = 0; s < SL; ++s) acc[s] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t d4 = a.d4;
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
         const int cnt = (int)(end - e0 < 32 ? end - e0 : 32);
@@ -243,27 +252,31 @@ __device__ __forceinline__ float4 gather_rows(const SpmmArgs &a, int64_t beg, in
         float myw = 1.f;
         if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
         int j = 0;
-        for (; j + UNR <= cnt; j += UNR) {
-            float4 v[UNR];
+        for (; j + U <= cnt; j += U) {
+            float4 v[U][SL];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int c = __shfl_sync(0xffffffffu, mycol, j + u);
-                v[u] = act ? __ldg(src + (int64_t)c * d4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u = 0; u < U; ++u) {
+                const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, j + u) * d4;
+#pragma unroll
+                for (int s = 0; s < SL; ++s) v[u][s] = act[s] ? __ldg(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                if (WEIGHTED) acc = f4fma(__shfl_sync(0xffffffffu, myw, j + u), v[u], acc);
-                else acc = f4add(acc, v[u]);
+            for (int u = 0; u < U; ++u) {
+                const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, j + u) : 1.f;
+#pragma unroll
+                for (int s = 0; s < SL; ++s) acc[s] = WEIGHTED ? f4fma(w, v[u][s], acc[s]) : f4add(acc[s], v[u][s]);
             }
         }
         for (; j < cnt; ++j) {
-            const int c = __shfl_sync(0xffffffffu, mycol, j);
-            const float4 v = act ? __ldg(src + (int64_t)c * d4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (WEIGHTED) acc = f4fma(__shfl_sync(0xffffffffu, myw, j), v, acc);
-            else acc = f4add(acc, v);
+            const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, j) * d4;
+            const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, j) : 1.f;
+#pragma unroll
+            for (int s = 0; s < SL; ++s) {
+                const float4 v = act[s] ? __ldg(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
+                acc[s] = WEIGHTED ? f4fma(w, v, acc[s]) : f4add(acc[s], v);
+            }
         }
     }
-    return acc;
 }
 
 // Epilogue of one output row from its gathered sum `acc`; x (this lane's float4 of X[row])
@@ -312,12 +325,29 @@ __device__ __forceinline__ void epilogue(const SpmmArgs &a, int64_t row, int c4,
     epilogue_v<EPI>(a, row, c4, act, acc, load_x<EPI>(a, row, c4, act), EPI == EPI_RAW ? 0.f : a.scale[row]);
 }
 
-// One warp streams the edges of rows [r0, r1) (all short) for one column slice, flushing each
-// row through the epilogue as the stream crosses its end; empty rows are flushed with 0.
-template <int EPI, bool WEIGHTED>
-__device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0, int64_t r1, int c4, bool act) {
+// Epilogue of one output row over the warp's SL column slices; the fused row normalisation
+// (EPI_FINAL with out_hat) is only used when one slice covers the whole row (nslices == 1).
+template <int EPI, int SL>
+__device__ __forceinline__ void epilogue_sl(const SpmmArgs &a, int64_t row, const int (&c4)[SL], const bool (&act)[SL],
+                                            const float4 (&acc)[SL], const float4 (&x)[SL], float s) {
+#pragma unroll
+    for (int q = 0; q < SL; ++q) epilogue_v<EPI>(a, row, c4[q], act[q], acc[q], x[q], s);
+}
+
+template <int EPI, int SL>
+__device__ __forceinline__ void load_x_sl(const SpmmArgs &a, int64_t row, const int (&c4)[SL], const bool (&act)[SL],
+                                          float4 (&x)[SL]) {
+#pragma unroll
+    for (int q = 0; q < SL; ++q) x[q] = load_x<EPI>(a, row, c4[q], act[q]);
+}
+
+// One warp streams the edges of rows [r0, r1) (all short) for its SL column slices, flushing
+// each row through the epilogue as the stream crosses its end; empty rows are flushed with 0.
+template <int EPI, bool WEIGHTED, int SL>
+__device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0, int64_t r1, const int (&c4)[SL],
+                                                  const bool (&act)[SL]) {
     const int lane = threadIdx.x & 31;
-    const float4 *__restrict__ src = a.src + c4;
+    constexpr int U = UNR / SL > 0 ? UNR / SL : 1;
     const int64_t d4 = a.d4;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t rb = r0; rb < r1; rb += 32) {
@@ -328,70 +358,84 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
         const int64_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
         int cur = 0;
         int64_t cur_end = __shfl_sync(0xffffffffu, my_end, 0);
-        float4 xcur = load_x<EPI>(a, rb, c4, act);
-        float4 acc = zero;
+        float4 xcur[SL], acc[SL];
+        load_x_sl<EPI, SL>(a, rb, c4, act, xcur);
+#pragma unroll
+        for (int q = 0; q < SL; ++q) acc[q] = zero;
         for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
             const int cnt = (int)(e_end - e0 < 32 ? e_end - e0 : 32);
             const int mycol = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
             float myw = 1.f;
             if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
-            for (int j = 0; j < cnt; j += UNR) {
-                float4 v[UNR];
+            for (int j = 0; j < cnt; j += U) {
+                float4 v[U][SL];
 #pragma unroll
-                for (int u = 0; u < UNR; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const int jj = j + u < 31 ? j + u : 31;
-                    const int c = __shfl_sync(0xffffffffu, mycol, jj);
-                    v[u] = (act && j + u < cnt) ? __ldg(src + (int64_t)c * d4) : zero;
+                    const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, jj) * d4;
+#pragma unroll
+                    for (int q = 0; q < SL; ++q) v[u][q] = (act[q] && j + u < cnt) ? __ldg(a.src + c4[q] + ro) : zero;
                 }
 #pragma unroll
-                for (int u = 0; u < UNR; ++u) {
+                for (int u = 0; u < U; ++u) {
                     if (j + u >= cnt) break;
                     const int64_t e = e0 + j + u;
                     while (e >= cur_end) {               // warp-uniform: flush finished rows
-                        epilogue_v<EPI>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
-                        acc = zero;
+                        epilogue_sl<EPI, SL>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
+#pragma unroll
+                        for (int q = 0; q < SL; ++q) acc[q] = zero;
                         ++cur;
                         cur_end = __shfl_sync(0xffffffffu, my_end, cur);
-                        xcur = load_x<EPI>(a, rb + cur, c4, act);
+                        load_x_sl<EPI, SL>(a, rb + cur, c4, act, xcur);
                     }
-                    if (WEIGHTED) acc = f4fma(__shfl_sync(0xffffffffu, myw, j + u), v[u], acc);
-                    else acc = f4add(acc, v[u]);
+                    const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, j + u) : 1.f;
+#pragma unroll
+                    for (int q = 0; q < SL; ++q) acc[q] = WEIGHTED ? f4fma(w, v[u][q], acc[q]) : f4add(acc[q], v[u][q]);
                 }
             }
         }
         while (cur < nb) {                               // last row of the batch and empty rows
-            epilogue_v<EPI>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
-            acc = zero;
+            epilogue_sl<EPI, SL>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
+#pragma unroll
+            for (int q = 0; q < SL; ++q) acc[q] = zero;
             ++cur;
-            if (cur < nb) xcur = load_x<EPI>(a, rb + cur, c4, act);
+            if (cur < nb) load_x_sl<EPI, SL>(a, rb + cur, c4, act, xcur);
         }
     }
 }
 
-template <int EPI, bool WEIGHTED>
-__global__ void __launch_bounds__(WPB * 32, 4) spmm_kernel(SpmmArgs a) {
+template <int EPI, bool WEIGHTED, int SL, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
     const int64_t n_items = tot >> 32;
-    // slice-major order: concurrently running warps work on the same 128-column slice, so the
-    // gathered working set is one slice of the dense operand (L2-resident for d > 128)
-    const int slice = (int)(gw / a.sch.max_items);
-    const int64_t item = gw - (int64_t)slice * a.sch.max_items;
+    // group-major order: concurrently running warps work on the same column group, so the
+    // gathered working set is one group of the dense operand (L2-resident for d > 128 SL)
+    const int grp = (int)(gw / a.sch.max_items);
+    const int64_t item = gw - (int64_t)grp * a.sch.max_items;
     if (item >= n_items) return;
     const int4 it = a.sch.items[item];
-    const int c4 = slice * 32 + lane;
-    const bool act = c4 < a.d4;
+    int c4[SL];
+    bool act[SL];
+#pragma unroll
+    for (int q = 0; q < SL; ++q) {
+        c4[q] = (grp * SL + q) * 32 + lane;
+        act[q] = c4[q] < a.d4;
+    }
     if (it.w == 0) {                                     // row block
         const int64_t r1 = item + 1 < n_items ? (int64_t)a.sch.items[item + 1].x : a.n_rows;
-        process_row_block<EPI, WEIGHTED>(a, it.x, r1, c4, act);
+        process_row_block<EPI, WEIGHTED, SL>(a, it.x, r1, c4, act);
         return;
     }
     const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];   // chunk of a long row
     const int64_t beg = rb + (int64_t)it.y * CHUNK;
     const int64_t end = min(re, beg + CHUNK);
-    const float4 acc = gather_rows<WEIGHTED>(a, beg, end, c4, act);
-    if (act) a.partials[(int64_t)it.z * a.d4 + c4] = acc;
+    float4 acc[SL];
+    gather_rows<WEIGHTED, SL>(a, beg, end, c4, act, acc);
+#pragma unroll
+    for (int q = 0; q < SL; ++q)
+        if (act[q]) a.partials[(int64_t)it.z * a.d4 + c4[q]] = acc[q];
 }
 
 template <int EPI>
@@ -483,13 +527,39 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
     TPO_LAUNCH_CHECK();
 }
 
+// Column slices per warp (SL): more slices amortise the index load / shuffle / address work
+// of an edge over more bytes, fewer keep the gathered working set (SL x 512 B per row) small.
+// MINB: resident blocks per SM the register budget is sized for.  Encoded as SL * 10 + MINB.
+int spmm_variant(int nslices) {
+    int v = nslices >= 2 ? 23 : 14;      // measured best on small (d = 1000) and medium (d = 256)
+    if (const char *e = getenv("TPO_SPMM_VARIANT")) v = atoi(e);
+    int sl = v / 10;
+    if (sl != 1 && sl != 2 && sl != 4 && sl != 8) v = 14, sl = 1;
+    while (sl > 1 && sl > nslices) sl /= 2;
+    return sl * 10 + v % 10;
+}
+
+template <int EPI, bool W>
+void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
+    const int sl = var / 10;
+    a.ngroups = (a.nslices + sl - 1) / sl;
+    const int64_t blocks = cdiv(max_items * a.ngroups, WPB);
+    switch (var) {
+        case 13: spmm_kernel<EPI, W, 1, 3><<<blocks, WPB * 32, 0, st>>>(a); break;
+        case 23: spmm_kernel<EPI, W, 2, 3><<<blocks, WPB * 32, 0, st>>>(a); break;
+        case 22: spmm_kernel<EPI, W, 2, 2><<<blocks, WPB * 32, 0, st>>>(a); break;
+        case 42: spmm_kernel<EPI, W, 4, 2><<<blocks, WPB * 32, 0, st>>>(a); break;
+        case 82: spmm_kernel<EPI, W, 8, 2><<<blocks, WPB * 32, 0, st>>>(a); break;
+        default: a.ngroups = a.nslices; spmm_kernel<EPI, W, 1, 4><<<cdiv(max_items * a.nslices, WPB), WPB * 32, 0, st>>>(a); break;
+    }
+    TPO_LAUNCH_CHECK();
+}
+
 template <int EPI>
 void spmm_launch(const SpmmArgs &a, int64_t max_items, int64_t max_slots, bool weighted, cudaStream_t st) {
-    const int64_t warps = max_items * a.nslices;
-    const int64_t blocks = cdiv(warps, WPB);
-    if (weighted) spmm_kernel<EPI, true><<<blocks, WPB * 32, 0, st>>>(a);
-    else spmm_kernel<EPI, false><<<blocks, WPB * 32, 0, st>>>(a);
-    TPO_LAUNCH_CHECK();
+    const int var = spmm_variant(a.nslices);
+    if (weighted) spmm_launch_sl<EPI, true>(a, max_items, var, st);
+    else spmm_launch_sl<EPI, false>(a, max_items, var, st);
     const int64_t fw = max_slots * a.nslices;
     fixup_kernel<EPI><<<cdiv(fw, WPB), WPB * 32, 0, st>>>(a);
     TPO_LAUNCH_CHECK();

@@ -304,8 +304,9 @@ size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, i
     s += align_up(sizeof(float) * n_u * D) + align_up(sizeof(float) * n_u);   // Rp, dinv
     s += align_up(sizeof(float) * d * d);                // Q
     s += align_up(sizeof(float) * n_u * k) + align_up(sizeof(float) * D * k);   // Gamma, Psi
-    size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d),
-                                     std::max(tpo_features_ws(n_u, d), haar_q_ws_bytes(d))),
+    s += align_up(sizeof(double) * D);                                           // r
+    s += align_up(haar_q_ws_bytes(d));                   // Haar Q runs beside the propagation
+    size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d), tpo_features_ws(n_u, d)),
                             std::max(tpo_topk_eig_ws(n_u, D, k, mode, p), tpo_cluster_ws(n_u, D, k)));
     return s + stage + 8 * 256;
 }
@@ -327,20 +328,45 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
         float *Rp = ar.take<float>(n * D), *dinv = ar.take<float>(n);
         float *Qd = ar.take<float>(d * d);
         float *Gamma = ar.take<float>(n * k), *Psi = ar.take<float>(D * k);
+        double *r = ar.take<double>(D);
+        const size_t haar_bytes = align_up(haar_q_ws_bytes(d));
+        Arena har(ar.dry ? nullptr : ar.base + ar.off, haar_bytes);
+        ar.take<char>(haar_bytes - 256);
         const size_t mark = ar.off;
-        cudaEvent_t ev[5];
-        for (auto &e : ev) TPO_CUDA(cudaEventCreate(&e));
+        struct Res {   // events and the side stream, released on every exit path
+            cudaEvent_t ev[5] = {}, fork = nullptr, join = nullptr;
+            cudaStream_t side = nullptr;
+            ~Res() {
+                for (auto &e : ev) if (e) cudaEventDestroy(e);
+                if (fork) cudaEventDestroy(fork);
+                if (join) cudaEventDestroy(join);
+                if (side) cudaStreamDestroy(side);
+            }
+        } res;
+        cudaEvent_t *ev = res.ev;
+        for (int i = 0; i < 5; ++i) TPO_CUDA(cudaEventCreate(&ev[i]));
+        TPO_CUDA(cudaEventCreateWithFlags(&res.fork, cudaEventDisableTiming));
+        TPO_CUDA(cudaEventCreateWithFlags(&res.join, cudaEventDisableTiming));
+        int lo = 0, hi = 0;   // highest priority: the latency-bound Haar chain interleaves with the SpMMs
+        TPO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        TPO_CUDA(cudaStreamCreateWithPriority(&res.side, cudaStreamNonBlocking, hi));
+        cudaEvent_t fork = res.fork, join = res.join;
+        cudaStream_t side = res.side;
         TPO_CUDA(cudaEventRecord(ev[0], st));
+        TPO_CUDA(cudaEventRecord(fork, st));
         propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[1], st));
-        haar_q_device(G, d, Qd, ar, st);
-        ar.off = mark;
-        features_impl(Zh, n, d, Qd, Rp, dinv, nullptr, ar, st);
+        // Alg. 1 L6-7 depends only on G: it runs on a side stream beside the propagation
+        TPO_CUDA(cudaStreamWaitEvent(side, fork, 0));
+        haar_q_device(G, d, Qd, har, side);
+        TPO_CUDA(cudaEventRecord(join, side));
+        TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
+        features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[2], st));
         std::vector<double> sig(k);
-        topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st);
+        topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st, r);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[3], st));
         cluster_impl(Rp, dinv, n, D, k, Gamma, sig.data(), Psi, Tf, Tg, labels, nullptr, ar, st);
@@ -352,7 +378,6 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
                 TPO_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
                 timings_ms[i] = ms;
             }
-        for (auto &e : ev) cudaEventDestroy(e);
     });
 }
 

@@ -104,9 +104,11 @@ void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, floa
                    double *r_out, Arena &ar, cudaStream_t st);
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y,
                           int64_t b, float *out, Arena &ar, cudaStream_t st);
+// r_colsum: r = sum_i R'[i] (2d fp64, device) from tpo_features, or NULL to recompute it.
 void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode,
                    int32_t p, int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi,
-                   Arena &ar, cudaStream_t st);
+                   Arena &ar, cudaStream_t st, const double *r_colsum = nullptr);
+void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cudaStream_t st);
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
                   int32_t *iters_used, Arena &ar, cudaStream_t st);
@@ -141,6 +143,14 @@ size_t gram_tc_ws(int64_t n, int64_t D);
 void features_tc(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, Arena &ar, cudaStream_t st);
 size_t features_tc_ws(int64_t n, int64_t d);
 size_t tsgemm_ws(int64_t n, int64_t p, int64_t q);
+// fp64 C = beta C + alpha op(A) B (row-major; op(A) = A^T when transA, A is then K x M);
+// deterministic split-K (dgemm.cu).  Workspace <= dgemm_ws(M, N, K).
+void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda,
+           const double *B, int64_t ldb, double beta, double *C, int64_t ldc, Arena &ar, cudaStream_t st);
+size_t dgemm_ws(int64_t M, int64_t N, int64_t K);
+// Ci = S C^{-1} for the b x b Gram g (S g S = C^T C, S = diag(g)^{-1/2}), b <= 128; one CTA;
+// a failed pivot sets *flag (device int) instead of throwing (dgemm.cu).
+void chol_inv_device(const double *g, int64_t b, double *Ci, int *flag, cudaStream_t st);
 
 // ----------------------------------------------------------------------------------------
 // Host fp64 dense linear algebra (host_linalg.cpp)
