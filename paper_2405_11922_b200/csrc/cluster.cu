@@ -223,7 +223,7 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     const int64_t nb = cdiv(std::max<int64_t>(n, 1), cluster_rows_per_block(n));
     ar.take<double>(nb * k * k);
     ar.take<int64_t>(nb * k);
-    return ar.off + std::max(tsgemm_ws(n, D, k), dgemm_ws(k, k, n)) + 4096;
+    return ar.off + std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)) + 4096;
 }
 
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
@@ -247,14 +247,14 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     init_factors_kernel<<<cdiv(mx, 256), 256, 0, st>>>(Gamma, n, Psi, sig, D, k, U, H);
     TPO_LAUNCH_CHECK();
     for (int t = 0; t < Tf; ++t) {
-        tsgemm_AtB_f32f64(Rp, D, dinv, U, k, n, D, k, RtU, ar, st);
+        onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
         ar.off = mark;
         dgemm(true, k, k, n, 1.0, U, k, U, k, 0.0, UtU, k, ar, st);
         ar.off = mark;
         h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
         TPO_LAUNCH_CHECK();
         std::swap(H, Hn);
-        tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
+        onmf_rh(Rp, n, D, dinv, H, k, RH, st);
         dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;
         ups_update_kernel<<<cdiv(n * 32, 256), 256, 0, st>>>(U, RH, M, n, k);

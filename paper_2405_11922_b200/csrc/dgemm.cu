@@ -132,7 +132,7 @@ int64_t splits_for(int64_t M, int64_t N, int64_t K) {
 //   is final once step j starts, and every row is divided by its pivot at the end.
 // ---------------------------------------------------------------------------------------
 constexpr int CI_MAX = 112;
-constexpr int TPR = 4;     // threads per row
+constexpr int TPR = 8;     // threads per row
 
 __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__restrict__ g, int b,
                                                                 double *__restrict__ Ci, int *__restrict__ flag) {
@@ -154,11 +154,22 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
         X[r * p + c] = r == c ? 1.0 : 0.0;
     }
     __syncthreads();
+    if (t == 0) {
+        const double d = U[0];
+        pinv[0] = (d > 0.0 && isfinite(d)) ? 1.0 / d : 0.0;
+    }
+    __syncthreads();
     for (int j = 0; j < b - 1; ++j) {
         if (my_r > j && my_r < b) {
-            const double d = U[j * p + j];
-            const double f = (d > 0.0 && isfinite(d)) ? U[j * p + my_r] / d : 0.0;
-            for (int c = my_r + my_q; c < b; c += TPR) U[my_r * p + c] -= f * U[j * p + c];
+            const double f = U[j * p + my_r] * pinv[j];
+            const double *uj = U + j * p;
+            double *ur = U + my_r * p;
+#pragma unroll 4
+            for (int c = my_r + my_q; c < b; c += TPR) ur[c] -= f * uj[c];
+            if (my_r == j + 1 && my_q == 0) {            // next pivot is final now: 1 / A_{j+1}[j+1][j+1]
+                const double d = ur[my_r];
+                pinv[my_r] = (d > 0.0 && isfinite(d)) ? 1.0 / d : 0.0;
+            }
         }
         __syncthreads();
     }
@@ -181,7 +192,10 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
     for (int j = b - 1; j > 0; --j) {
         if (my_r < j) {
             const double f = U[my_r * p + j] * pinv[j];
-            for (int c = j + my_q; c < b; c += TPR) X[my_r * p + c] -= f * X[j * p + c];
+            const double *xj = X + j * p;
+            double *xr = X + my_r * p;
+#pragma unroll 4
+            for (int c = j + my_q; c < b; c += TPR) xr[c] -= f * xj[c];
         }
         __syncthreads();
     }

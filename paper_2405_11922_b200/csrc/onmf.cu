@@ -1,0 +1,282 @@
+// a8: the two passes over R' of one greedy-orthogonal-NMF iteration (Alg. 2, PAPER.md:536-547;
+// products bracketed as PAPER.md:564 so the n x n affinity is never formed), fp64 arithmetic
+// (R11) with fp32 R' widened on load:
+//
+//   onmf_rtu:  RtU[a, l] = sum_i R'[i, a] (dinv_i Ups[i, l])          (D x k, reduce over n)
+//              grid = (row groups, column blocks, k chunks); a thread owns CPT columns of R'
+//              (coalesced loads, 4 rows in flight) and KC columns of Ups (dinv.Ups staged in
+//              shared memory, read as broadcasts): CPT x KC fp64 accumulators.  Each CTA writes
+//              an fp64 partial; onmf_reduce adds the row groups in order (deterministic).
+//   onmf_rh:   RH[i, l] = dinv_i sum_a R'[i, a] H[a, l]                (n x k)
+//              H (D x KC chunk) staged in shared memory; a warp owns RPW rows, lanes split the
+//              a-dimension (coalesced), RPW x KC accumulators per lane, fixed shuffle tree.
+//
+// Both are fp64-FMA bound on B200 (64 DFMA/clk/SM): n D k FMAs per pass.
+#include <algorithm>
+
+#include "tpo_internal.cuh"
+
+namespace tpo {
+namespace {
+
+constexpr int NT = 256;
+constexpr int RT = 64;                      // rows of dinv.Ups staged per tile (onmf_rtu)
+
+template <int CPT, int KC>
+__global__ void __launch_bounds__(NT) onmf_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
+                                                      const float *__restrict__ dinv,
+                                                      const double *__restrict__ U, int k, int64_t rows_per,
+                                                      double *__restrict__ part) {
+    __shared__ double Ys[RT][KC];
+    const int t = threadIdx.x;
+    const int64_t g = blockIdx.x;
+    const int a0 = blockIdx.y * (NT * CPT);
+    const int k0 = blockIdx.z * KC;
+    const int kc = min(KC, k - k0);
+    const int64_t r0 = g * rows_per, r1 = min(n, r0 + rows_per);
+    int col[CPT];
+    bool cv[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        col[c] = a0 + t + NT * c;
+        cv[c] = col[c] < D;
+    }
+    double acc[CPT][KC];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int l = 0; l < KC; ++l) acc[c][l] = 0.0;
+    for (int64_t tb = r0; tb < r1; tb += RT) {
+        const int rows = (int)min((int64_t)RT, r1 - tb);
+        __syncthreads();
+        for (int e = t; e < RT * KC; e += NT) {
+            const int r = e / KC, l = e - r * KC;
+            double v = 0.0;
+            if (r < rows && l < kc) v = (double)dinv[tb + r] * U[(tb + r) * k + k0 + l];
+            Ys[r][l] = v;
+        }
+        __syncthreads();
+        int r = 0;
+        for (; r + 4 <= rows; r += 4) {
+            float rv[4][CPT];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) rv[u][c] = cv[c] ? __ldg(Rp + (tb + r + u) * D + col[c]) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+#pragma unroll
+                for (int l = 0; l < KC; ++l) {
+                    const double y = Ys[r + u][l];
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) acc[c][l] = fma((double)rv[u][c], y, acc[c][l]);
+                }
+            }
+        }
+        for (; r < rows; ++r) {
+            float rv[CPT];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) rv[c] = cv[c] ? __ldg(Rp + (tb + r) * D + col[c]) : 0.f;
+#pragma unroll
+            for (int l = 0; l < KC; ++l) {
+                const double y = Ys[r][l];
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) acc[c][l] = fma((double)rv[c], y, acc[c][l]);
+            }
+        }
+    }
+    // part[g][a][l] (the chunk's columns only)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (!cv[c]) continue;
+#pragma unroll
+        for (int l = 0; l < KC; ++l)
+            if (l < kc) part[(g * D + col[c]) * (int64_t)k + k0 + l] = acc[c][l];
+    }
+}
+
+__global__ void onmf_reduce_kernel(const double *__restrict__ part, int64_t G, int64_t len, double *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    double s = 0.0;
+    for (int64_t g = 0; g < G; ++g) s += part[g * len + i];
+    out[i] = s;
+}
+
+template <int RPW, int KC>
+__global__ void __launch_bounds__(NT) onmf_rh_kernel(const float *__restrict__ Rp, int64_t n, int D,
+                                                     const float *__restrict__ dinv, const double *__restrict__ H,
+                                                     int k, double *__restrict__ RH) {
+    extern __shared__ double Hs[];          // [D][KC]
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int k0 = blockIdx.y * KC;
+    const int kc = min(KC, k - k0);
+    for (int e = t; e < D * KC; e += NT) {
+        const int a = e / KC, l = e - a * KC;
+        Hs[e] = l < kc ? H[(int64_t)a * k + k0 + l] : 0.0;
+    }
+    __syncthreads();
+    const int64_t rows_per_block = (int64_t)(NT / 32) * RPW;
+    for (int64_t rb = (int64_t)blockIdx.x * rows_per_block + w * RPW; rb < n; rb += (int64_t)gridDim.x * rows_per_block) {
+        double acc[RPW][KC];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r)
+#pragma unroll
+            for (int l = 0; l < KC; ++l) acc[r][l] = 0.0;
+        bool rv_ok[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) rv_ok[r] = rb + r < n;
+        for (int a = lane; a < D; a += 32) {
+            float rv[RPW];
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) rv[r] = rv_ok[r] ? __ldg(Rp + (rb + r) * D + a) : 0.f;
+            const double *h = Hs + a * KC;
+#pragma unroll
+            for (int l = 0; l < KC; ++l) {
+                const double hv = h[l];
+#pragma unroll
+                for (int r = 0; r < RPW; ++r) acc[r][l] = fma((double)rv[r], hv, acc[r][l]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r)
+#pragma unroll
+            for (int l = 0; l < KC; ++l)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) acc[r][l] += __shfl_xor_sync(0xffffffffu, acc[r][l], o);
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                if (!rv_ok[r]) continue;
+                const double s = (double)dinv[rb + r];
+#pragma unroll
+                for (int l = 0; l < KC; ++l)
+                    if (l < kc) RH[(rb + r) * k + k0 + l] = s * acc[r][l];
+            }
+        }
+    }
+}
+
+// k-chunk widths that are instantiated (a chunk is padded up to the next one)
+constexpr int KCS[] = {2, 4, 5, 8, 10, 12, 16, 20, 25, 32, 50};
+
+int pick_kc(int need) {
+    for (int v : KCS)
+        if (v >= need) return v;
+    return 50;
+}
+
+struct RtuPlan {
+    int kc, nkc, cpt, ncb;
+    int64_t G, rows_per;
+};
+
+RtuPlan rtu_plan(int64_t n, int D, int k) {
+    RtuPlan p;
+    p.nkc = (k + 49) / 50;
+    p.kc = pick_kc((k + p.nkc - 1) / p.nkc);
+    const int want = (D + NT - 1) / NT;                 // columns per thread to cover D in one block
+    const int cap = std::max(1, std::min(8, 96 / p.kc));  // CPT x KC accumulators <= 96
+    int cpt = 1;
+    while (cpt < want && cpt * 2 <= cap) cpt *= 2;
+    p.cpt = cpt;
+    p.ncb = (D + NT * cpt - 1) / (NT * cpt);
+    const int64_t tiles = (int64_t)p.ncb * p.nkc;
+    const int64_t want_g = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
+    p.G = std::max<int64_t>(1, std::min<int64_t>(want_g, (std::max<int64_t>(n, 1) + RT - 1) / RT));
+    p.rows_per = cdiv(cdiv(std::max<int64_t>(n, 1), p.G), 4) * 4;
+    p.G = cdiv(std::max<int64_t>(n, 1), p.rows_per);
+    return p;
+}
+
+template <int KC>
+void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float *dinv, const double *U, int k,
+                double *part, cudaStream_t st) {
+    const dim3 grid((unsigned)p.G, (unsigned)p.ncb, (unsigned)p.nkc);
+    // only CPT x KC <= 96 is planned (rtu_plan); the other combinations are not instantiated
+    constexpr int C8 = 8 * KC <= 96 ? 8 : 1, C4 = 4 * KC <= 96 ? 4 : 1, C2 = 2 * KC <= 96 ? 2 : 1;
+    switch (p.cpt) {
+        case 1: onmf_rtu_kernel<1, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        case 2: onmf_rtu_kernel<C2, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        case 4: onmf_rtu_kernel<C4, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        default: onmf_rtu_kernel<C8, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+    }
+    TPO_LAUNCH_CHECK();
+}
+
+template <int KC>
+void launch_rh(int rpw, int nkc, const float *Rp, int64_t n, int D, const float *dinv, const double *H, int k, double *RH,
+               cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)D * KC;
+    const int64_t rows_per_block = (NT / 32) * rpw;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, rows_per_block), 148 * 8));
+    const dim3 grid(gx, (unsigned)nkc);
+    constexpr int R4 = 4 * KC <= 64 ? 4 : 1, R2 = 2 * KC <= 64 ? 2 : 1;
+    switch (rpw) {
+        case 1:
+            TPO_CUDA(cudaFuncSetAttribute(onmf_rh_kernel<1, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            onmf_rh_kernel<1, KC><<<grid, NT, smem, st>>>(Rp, n, D, dinv, H, k, RH);
+            break;
+        case 2:
+            TPO_CUDA(cudaFuncSetAttribute(onmf_rh_kernel<R2, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            onmf_rh_kernel<R2, KC><<<grid, NT, smem, st>>>(Rp, n, D, dinv, H, k, RH);
+            break;
+        default:
+            TPO_CUDA(cudaFuncSetAttribute(onmf_rh_kernel<R4, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            onmf_rh_kernel<R4, KC><<<grid, NT, smem, st>>>(Rp, n, D, dinv, H, k, RH);
+            break;
+    }
+    TPO_LAUNCH_CHECK();
+}
+
+#define TPO_KC_SWITCH(kc, F, ...)                      \
+    switch (kc) {                                      \
+        case 2: F<2>(__VA_ARGS__); break;              \
+        case 4: F<4>(__VA_ARGS__); break;              \
+        case 5: F<5>(__VA_ARGS__); break;              \
+        case 8: F<8>(__VA_ARGS__); break;              \
+        case 10: F<10>(__VA_ARGS__); break;            \
+        case 12: F<12>(__VA_ARGS__); break;            \
+        case 16: F<16>(__VA_ARGS__); break;            \
+        case 20: F<20>(__VA_ARGS__); break;            \
+        case 25: F<25>(__VA_ARGS__); break;            \
+        case 32: F<32>(__VA_ARGS__); break;            \
+        default: F<50>(__VA_ARGS__); break;            \
+    }
+
+}  // namespace
+
+size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k) {
+    const RtuPlan p = rtu_plan(n, (int)D, k);
+    return align_up(sizeof(double) * (size_t)(p.G * D * k) + 1) + 256;
+}
+
+// RtU = R'^T (dinv . U)   (D x k, fp64)
+void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
+              cudaStream_t st) {
+    const RtuPlan p = rtu_plan(n, (int)D, k);
+    const size_t mark = ar.off;
+    double *part = ar.take<double>(p.G * D * k);
+    TPO_KC_SWITCH(p.kc, launch_rtu, p, Rp, n, (int)D, dinv, U, k, part, st);
+    onmf_reduce_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(part, p.G, D * k, RtU);
+    TPO_LAUNCH_CHECK();
+    ar.off = mark;
+}
+
+// RH = dinv . (R' H)   (n x k, fp64); H: D x k fp64
+void onmf_rh(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *H, int k, double *RH,
+             cudaStream_t st) {
+    // the H chunk lives in shared memory: D * kc * 8 bytes <= 200 KB
+    TPO_REQUIRE((size_t)D * 2 * 8 <= 200 * 1024, "ONMF: D too large for the shared-memory H chunk");
+    int nkc = 1;
+    while (true) {
+        const int kc = pick_kc((k + nkc - 1) / nkc);
+        if ((size_t)D * kc * 8 <= 200 * 1024 && kc >= (k + nkc - 1) / nkc) break;
+        ++nkc;
+    }
+    const int kc = pick_kc((k + nkc - 1) / nkc);
+    const int rpw = 4 * kc <= 64 ? 4 : (2 * kc <= 64 ? 2 : 1);
+    TPO_KC_SWITCH(kc, launch_rh, rpw, nkc, Rp, n, (int)D, dinv, H, k, RH, st);
+}
+
+}  // namespace tpo
