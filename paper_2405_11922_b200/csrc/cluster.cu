@@ -138,6 +138,72 @@ __global__ void __launch_bounds__(256) assign_small_kernel(const double *__restr
     labels[row] = arg;
 }
 
+// Fused Alg. 3 pass for k <= KM <= 32: l*_i = argmax_l (Ups Phi)[i, l] (thread per row, the row
+// in registers, Phi in smem; same arithmetic order as assign_kernel) AND the per-cluster sums
+// of the next Phi in the same read of Ups.  Each warp owns a contiguous run of rows and adds
+// them in row order into its own smem accumulators (lanes over columns); the warps of a block
+// are combined in warp order -> part[b][l][a], cpart[b][l] (deterministic).
+template <int KM, int NW>
+__global__ void __launch_bounds__(NW * 32) nci_fused_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
+                                                        int64_t n, int k, int64_t rows_per_block,
+                                                        int32_t *__restrict__ labels, NciState s,
+                                                        double *__restrict__ part, int64_t *__restrict__ cpart) {
+    if (*s.done) return;
+    constexpr int NT = NW * 32;
+    __shared__ double phs[KM * KM];
+    __shared__ double acc[NW][KM][KM];
+    __shared__ int cnt[NW][KM];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    for (int i = t; i < k * k; i += NT) phs[i] = Phi[i];
+    for (int i = t; i < NW * KM * KM; i += NT) (&acc[0][0][0])[i] = 0.0;
+    for (int i = t; i < NW * KM; i += NT) (&cnt[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t b0 = blockIdx.x * rows_per_block, b1 = min(n, b0 + rows_per_block);
+    const int64_t per_w = (rows_per_block + NW - 1) / NW;
+    const int64_t w0 = min(b1, b0 + w * per_w), w1 = min(b1, w0 + per_w);
+    bool changed = false;
+    for (int64_t c0 = w0; c0 < w1; c0 += 32) {
+        const int64_t row = c0 + lane;
+        const bool ok = row < w1;
+        double u[KM];
+#pragma unroll
+        for (int a = 0; a < KM; ++a) u[a] = (ok && a < k) ? U[row * k + a] : 0.0;
+        double best = 0.0;
+        int arg = 0;
+        for (int l = 0; l < k; ++l) {
+            double sc = 0.0;
+#pragma unroll
+            for (int a = 0; a < KM; ++a)
+                if (a < k) sc = __dadd_rn(sc, __dmul_rn(u[a], phs[a * k + l]));
+            if (l == 0 || sc > best) { best = sc; arg = l; }
+        }
+        if (ok) {
+            if (labels[row] != arg) changed = true;
+            labels[row] = arg;
+        }
+        const int nr = (int)(w1 - c0 < 32 ? w1 - c0 : 32);
+        for (int r = 0; r < nr; ++r) {          // rows in order: acc[l][a] += Ups[row, a]
+            const int l = __shfl_sync(0xffffffffu, arg, r);
+            if (lane < k) acc[w][l][lane] += U[(c0 + r) * k + lane];
+            if (lane == 0) cnt[w][l] += 1;
+            __syncwarp();
+        }
+    }
+    if (__any_sync(0xffffffffu, changed) && lane == 0) *s.changed = 1;
+    __syncthreads();
+    for (int i = t; i < k * k; i += NT) {
+        const int l = i / k, a = i - l * k;
+        double v = 0.0;
+        for (int ww = 0; ww < NW; ++ww) v += acc[ww][l][a];
+        part[blockIdx.x * (int64_t)k * k + i] = v;
+    }
+    for (int l = t; l < k; l += NT) {
+        int64_t c = 0;
+        for (int ww = 0; ww < NW; ++ww) c += cnt[ww][l];
+        cpart[blockIdx.x * (int64_t)k + l] = c;
+    }
+}
+
 __global__ void nci_step_kernel(NciState s, int32_t *__restrict__ counts, int k) {
     // runs after assign: advance the iteration counter, freeze on a fix-point
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -254,7 +320,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
         TPO_LAUNCH_CHECK();
         std::swap(H, Hn);
-        onmf_rh(Rp, n, D, dinv, H, k, RH, st);
+        tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
         dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;
         ups_update_kernel<<<cdiv(n * 32, 256), 256, 0, st>>>(U, RH, M, n, k);
@@ -275,6 +341,21 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
     const int sum_threads = (int)std::max<int64_t>(32, cdiv(k, 32) * 32);
     for (int t = 0; t < Tg; ++t) {
+        const bool last = t == Tg - 1;           // the last Phi update is never used
+        if (k <= 32 && !last) {
+            // rows per block: whole 32-row chunks for each of the 8 warps, ~2 blocks per SM
+            const int64_t rpf = std::max<int64_t>(rpb, cdiv(cdiv(n, 2 * 148), 256) * 256);
+            const int64_t nbf = cdiv(n, rpf);
+            if (k <= 8) nci_fused_kernel<8, 8><<<nbf, 256, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
+            else if (k <= 16) nci_fused_kernel<16, 8><<<nbf, 256, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
+            else nci_fused_kernel<32, 4><<<nbf, 128, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
+            TPO_LAUNCH_CHECK();
+            nci_step_kernel<<<1, 32, 0, st>>>(s, nullptr, k);
+            TPO_LAUNCH_CHECK();
+            phi_kernel<<<cdiv((int64_t)k * k * 32, 256), 256, 0, st>>>(part, cpart, nbf, k, Phi, s.done);
+            TPO_LAUNCH_CHECK();
+            continue;
+        }
         if (k <= 16)
             assign_small_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
         else
@@ -282,7 +363,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         TPO_LAUNCH_CHECK();
         nci_step_kernel<<<1, 32, 0, st>>>(s, nullptr, k);
         TPO_LAUNCH_CHECK();
-        if (t == Tg - 1) break;                       // the last Phi update is never used
+        if (last) break;
         cluster_sums_kernel<<<nb, sum_threads, sum_smem, st>>>(U, labels, n, k, rpb, part, cpart, s.done);
         TPO_LAUNCH_CHECK();
         phi_kernel<<<cdiv((int64_t)k * k * 32, 256), 256, 0, st>>>(part, cpart, nb, k, Phi, s.done);

@@ -134,6 +134,16 @@ int64_t splits_for(int64_t M, int64_t N, int64_t K) {
 constexpr int CI_MAX = 112;
 constexpr int TPR = 8;     // threads per row
 
+// 1/d by the hardware approximation refined with two Newton steps (the pivot reciprocal sits
+// on the critical path of every Cholesky step; an IEEE division is several times longer)
+__device__ __forceinline__ double fast_rcp(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    r = r * fma(-d, r, 2.0);
+    r = r * fma(-d, r, 2.0);
+    return r;
+}
+
 __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__restrict__ g, int b,
                                                                 double *__restrict__ Ci, int *__restrict__ flag) {
     extern __shared__ double sm[];
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
     __syncthreads();
     if (t == 0) {
         const double d = U[0];
-        pinv[0] = (d > 0.0 && isfinite(d)) ? 1.0 / d : 0.0;
+        pinv[0] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
     }
     __syncthreads();
     for (int j = 0; j < b - 1; ++j) {
@@ -168,7 +178,7 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
             for (int c = my_r + my_q; c < b; c += TPR) ur[c] -= f * uj[c];
             if (my_r == j + 1 && my_q == 0) {            // next pivot is final now: 1 / A_{j+1}[j+1][j+1]
                 const double d = ur[my_r];
-                pinv[my_r] = (d > 0.0 && isfinite(d)) ? 1.0 / d : 0.0;
+                pinv[my_r] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
             }
         }
         __syncthreads();

@@ -282,7 +282,8 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         cholqr2_f64(V, T, D, b, flag, ar, st);
     };
     orth_against_u();
-    const int m = 8, max_rounds = 60;
+    const int max_rounds = 60;
+    int m = 8;
     std::vector<double> w(bz), E(bz * bz);
     double bnd = 0.0;
     for (int round = 0; round <= max_rounds; ++round) {
@@ -330,6 +331,14 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
             return;
         }
         bnd = std::max(w[bz - 1], 1e-6 * fabs(w[0]));
+        // Degree: the filter grows the top deflated direction by T_m(x1), x1 = (w[1] - c) / e;
+        // keep T_m(x1) <= 1e6 so the filtered block stays well conditioned for CholeskyQR2
+        // (a wide spectrum converges in a few low-degree rounds anyway).
+        {
+            const double x1 = std::max(1.0, (w[1] - 0.5 * bnd) / (0.5 * bnd));
+            m = 8;
+            while (m > 1 && cosh(m * acosh(x1)) > 1e6) --m;
+        }
         ar.off = mark;
     }
 }

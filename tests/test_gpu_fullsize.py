@@ -8,8 +8,11 @@ GPU stage, so each stage is compared on identical inputs.  Tolerances are north_
 Z / R' within 1e-5 relative Frobenius, top-k subspace sin(theta_max) <= 1e-4, labels
 bit-exact given identical eigen inputs.
 
-The xl config (10M x 4M, 300M edges) is checked by the closed form only, and only when
-TPO_TEST_XL=1 (its generation alone needs tens of GB of host memory).
+To bound the oracle's time (its plain fp64 propagation runs ~40 s per hop on the large graph),
+the large config's staged inputs use T = 1 hop (same graph, same d, same kernels and launch
+configuration; its T = 8 propagation is pinned by the P2 closed form at full size) and its
+discretisation runs T_f = 1.  The xl config (10M x 4M, 300M edges) is checked by the closed form
+only, and only when TPO_TEST_XL=1 (its generation alone needs tens of GB of host memory).
 """
 import os
 
@@ -45,19 +48,23 @@ def tpo():
 _CACHE = {}
 
 
+STAGE_T = {"medium": None, "large": 1}     # None: the config's own T
+
+
 def staged(name):
     """Generate the config once and run the oracle stage by stage (cached per module)."""
     if name in _CACHE:
         return _CACHE[name]
     g = make_config(name)
-    Z, Zh = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, g.T, g.B_val)
+    T = g.T if STAGE_T[name] is None else STAGE_T[name]
+    Z, Zh = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, T, g.B_val)
     Q = O.haar_q(g.G).astype(np.float32)
     Zh32 = Zh.astype(np.float32)
     Rp, dinv, r = O.features(Zh32, Q)
     Rp32, dinv32 = Rp.astype(np.float32), dinv.astype(np.float32)
     del Rp
     Gm, s, Ps, lam = O.topk(Rp32, dinv32, g.k)
-    _CACHE[name] = dict(g=g, Z=Z, Zh=Zh, Q=Q, Zh32=Zh32, Rp32=Rp32, dinv=dinv, r=r, dinv32=dinv32, Gm=Gm, s=s,
+    _CACHE[name] = dict(g=g, T=T, Z=Z, Zh=Zh, Q=Q, Zh32=Zh32, Rp32=Rp32, dinv=dinv, r=r, dinv32=dinv32, Gm=Gm, s=s,
                         Ps=Ps, lam=lam)
     return _CACHE[name]
 
@@ -73,7 +80,7 @@ CFGS = ["medium", "large"]
 def test_propagate_full_vs_oracle(tpo, name):
     st = staged(name)
     g = st["g"]
-    Z, Zh = tpo.propagate(dev_graph(tpo, g), torch.from_numpy(g.X).cuda(), g.alpha, g.T)
+    Z, Zh = tpo.propagate(dev_graph(tpo, g), torch.from_numpy(g.X).cuda(), g.alpha, st["T"])
     assert relF(Z.cpu().numpy(), st["Z"]) <= 1e-5
     assert relF(Zh.cpu().numpy(), st["Zh"]) <= 1e-5
 
@@ -118,10 +125,10 @@ def test_topk_full_vs_oracle(tpo, name):
     assert np.all(Gm.astype(np.float64).sum(0) >= 0)                              # R8
 
 
-@pytest.mark.parametrize("name,Tf,Tg", [("medium", 5, 20), ("large", 2, 20)])
+@pytest.mark.parametrize("name,Tf,Tg", [("medium", 5, 20), ("large", 1, 20)])
 def test_cluster_full_bit_exact(tpo, name, Tf, Tg):
     """D4 at full size: identical fp32 (R', dinv, Gamma, Psi) and fp64 sigma -> identical labels and
-    the same number of Alg. 3 iterations (large runs T_f = 2 to bound the oracle's time)."""
+    the same number of Alg. 3 iterations (large runs T_f = 1 to bound the oracle's time)."""
     st = staged(name)
     Gm32, Ps32 = st["Gm"].astype(np.float32), st["Ps"].astype(np.float32)
     lab_o, it_o, _ = O.cluster(st["Rp32"], st["dinv32"], Gm32, st["s"], Ps32, Tf, Tg)
