@@ -443,11 +443,17 @@ void aw_f32_run(const float *A, int64_t lda, const float *rs, const double *W, i
         aw_run<float, TO>(A, lda, rs, W, n, p, q, out, ldo, st);
         return;
     }
-    if (q <= 8) {
-        aw_stream_kernel<TO, 8><<<dim3(cdiv(n, SR), cdiv(q, 8)), SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo);
-    } else {
-        aw_stream_kernel<TO, 16><<<dim3(cdiv(n, SR), cdiv(q, 16)), SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out,
-                                                                               ldo);
+    // q chunk width QW (a multiple of 4, <= 24: static smem) fitted to q: little padding for any k
+    const int64_t nch = cdiv(q, 24);
+    const int QW = (int)(cdiv(cdiv(q, nch), 4) * 4);
+    const dim3 grid((unsigned)cdiv(n, SR), (unsigned)cdiv(q, QW));
+    switch (QW) {
+        case 4: aw_stream_kernel<TO, 4><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
+        case 8: aw_stream_kernel<TO, 8><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
+        case 12: aw_stream_kernel<TO, 12><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
+        case 16: aw_stream_kernel<TO, 16><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
+        case 20: aw_stream_kernel<TO, 20><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
+        default: aw_stream_kernel<TO, 24><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
     }
     TPO_LAUNCH_CHECK();
 }

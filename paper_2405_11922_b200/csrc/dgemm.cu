@@ -169,15 +169,27 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
         pinv[0] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
     }
     __syncthreads();
+    constexpr int PER = (CI_MAX + TPR - 1) / TPR;   // columns a thread owns in one row
     for (int j = 0; j < b - 1; ++j) {
         if (my_r > j && my_r < b) {
             const double f = U[j * p + my_r] * pinv[j];
             const double *uj = U + j * p;
             double *ur = U + my_r * p;
-#pragma unroll 4
-            for (int c = my_r + my_q; c < b; c += TPR) ur[c] -= f * uj[c];
+            // all loads first (U rows alias: keep the compiler from ordering loads after stores)
+            double xv[PER], yv[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int c = my_r + my_q + TPR * q;
+                xv[q] = c < b ? ur[c] : 0.0;
+                yv[q] = c < b ? uj[c] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int c = my_r + my_q + TPR * q;
+                if (c < b) ur[c] = xv[q] - f * yv[q];
+            }
             if (my_r == j + 1 && my_q == 0) {            // next pivot is final now: 1 / A_{j+1}[j+1][j+1]
-                const double d = ur[my_r];
+                const double d = xv[0] - f * yv[0];
                 pinv[my_r] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
             }
         }
@@ -204,8 +216,18 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
             const double f = U[my_r * p + j] * pinv[j];
             const double *xj = X + j * p;
             double *xr = X + my_r * p;
-#pragma unroll 4
-            for (int c = j + my_q; c < b; c += TPR) xr[c] -= f * xj[c];
+            double xv[PER], yv[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int c = j + my_q + TPR * q;
+                xv[q] = c < b ? xr[c] : 0.0;
+                yv[q] = c < b ? xj[c] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int c = j + my_q + TPR * q;
+                if (c < b) xr[c] = xv[q] - f * yv[q];
+            }
         }
         __syncthreads();
     }

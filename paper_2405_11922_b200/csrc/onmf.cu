@@ -23,7 +23,7 @@ constexpr int NT = 256;
 constexpr int RT = 64;                      // rows of dinv.Ups staged per tile (onmf_rtu)
 
 template <int CPT, int KC>
-__global__ void __launch_bounds__(NT) onmf_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
+__global__ void __launch_bounds__(NT, 2) onmf_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
                                                       const float *__restrict__ dinv,
                                                       const double *__restrict__ U, int k, int64_t rows_per,
                                                       double *__restrict__ part) {
@@ -95,12 +95,17 @@ __global__ void __launch_bounds__(NT) onmf_rtu_kernel(const float *__restrict__ 
     }
 }
 
+// out[i] = sum_g part[g][i]: 8 independent partial sums (g mod 8) combined in a fixed order
 __global__ void onmf_reduce_kernel(const double *__restrict__ part, int64_t G, int64_t len, double *__restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= len) return;
-    double s = 0.0;
-    for (int64_t g = 0; g < G; ++g) s += part[g * len + i];
-    out[i] = s;
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t g = 0;
+    for (; g + 8 <= G; g += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] += part[(g + j) * len + i];
+    for (; g < G; ++g) s[g & 7] += part[g * len + i];
+    out[i] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 template <int RPW, int KC>
@@ -176,13 +181,13 @@ RtuPlan rtu_plan(int64_t n, int D, int k) {
     p.nkc = (k + 49) / 50;
     p.kc = pick_kc((k + p.nkc - 1) / p.nkc);
     const int want = (D + NT - 1) / NT;                 // columns per thread to cover D in one block
-    const int cap = std::max(1, std::min(8, 96 / p.kc));  // CPT x KC accumulators <= 96
+    const int cap = std::max(1, std::min(8, 48 / p.kc));  // CPT x KC accumulators <= 48: 2 CTAs / SM
     int cpt = 1;
     while (cpt < want && cpt * 2 <= cap) cpt *= 2;
     p.cpt = cpt;
     p.ncb = (D + NT * cpt - 1) / (NT * cpt);
     const int64_t tiles = (int64_t)p.ncb * p.nkc;
-    const int64_t want_g = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
+    const int64_t want_g = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);   // one wave at 2 CTAs / SM
     p.G = std::max<int64_t>(1, std::min<int64_t>(want_g, (std::max<int64_t>(n, 1) + RT - 1) / RT));
     p.rows_per = cdiv(cdiv(std::max<int64_t>(n, 1), p.G), 4) * 4;
     p.G = cdiv(std::max<int64_t>(n, 1), p.rows_per);
@@ -193,8 +198,8 @@ template <int KC>
 void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float *dinv, const double *U, int k,
                 double *part, cudaStream_t st) {
     const dim3 grid((unsigned)p.G, (unsigned)p.ncb, (unsigned)p.nkc);
-    // only CPT x KC <= 96 is planned (rtu_plan); the other combinations are not instantiated
-    constexpr int C8 = 8 * KC <= 96 ? 8 : 1, C4 = 4 * KC <= 96 ? 4 : 1, C2 = 2 * KC <= 96 ? 2 : 1;
+    // only CPT x KC <= 48 (or CPT = 1) is planned (rtu_plan); the other combinations are not instantiated
+    constexpr int C8 = 8 * KC <= 48 ? 8 : 1, C4 = 4 * KC <= 48 ? 4 : 1, C2 = 2 * KC <= 48 ? 2 : 1;
     switch (p.cpt) {
         case 1: onmf_rtu_kernel<1, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
         case 2: onmf_rtu_kernel<C2, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
