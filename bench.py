@@ -267,13 +267,29 @@ def main():
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("bytes_per_hop")
+            traffic = json.load(open(tf)).get("bytes_per_hop") * g.T      # per launch of the T-hop loop
         except Exception:
             traffic = None
+    gather = None
+    gc = os.path.join(ROOT, "profiles", "gather_ceilings.json")
+    if os.path.exists(gc):
+        try:
+            ceil = json.load(open(gc))
+            gbytes = 2.0 * g.nnz * g.d * 4        # every edge reads a d-wide fp32 row, both SpMMs
+            ach = gbytes * g.T / (prop_ms / 1e3) / 1e9
+            # the gathered table per column group: L2-resident when it fits in 126 MB
+            sl = 2 if g.d > 128 else 1
+            table_mb = max(g.n, g.m) * min(g.d, 128 * sl) * 4 / 2**20
+            pk_g = ceil["l2_resident_gbs"] if table_mb <= 96 else ceil["dram_gbs"]
+            gather = {"achieved": ach, "ceiling": pk_g, "unit": "GB/s", "frac": ach / pk_g,
+                      "gathered_bytes_per_hop": gbytes, "table_mb_per_column_group": table_mb,
+                      "ceiling_source": "profiles/gather_ceilings.json (measured gather probe)"}
+        except Exception:
+            gather = None
     roof = {"kernel": "spmm_kernel pair (one hop: SpMM-1 V side + SpMM-2 U side, fix-ups, per-call schedule)",
             "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": src,
-            "algorithmic_bytes_per_hop": bytes_hop, "hops": g.T, "propagate_ms": prop_ms}
+            "algorithmic_bytes_per_hop": bytes_hop, "hops": g.T, "propagate_ms": prop_ms, "gather": gather}
 
     line = {"metric": metric_name(), "value": value, "unit": "nnz*d/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

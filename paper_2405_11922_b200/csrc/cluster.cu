@@ -51,24 +51,37 @@ __global__ void h_update_kernel(const double *__restrict__ H, const double *__re
 }
 
 // Ups[i,l] *= sqrt(max(RH[i,l],0) / (max((Ups M)[i,l],0) + eps)); warp per row, the old row
-// staged in shared memory (k <= 128).
+// and M (k x k) staged in shared memory (k <= 128).
 __global__ void __launch_bounds__(256) ups_update_kernel(double *__restrict__ U, const double *__restrict__ RH,
                                                          const double *__restrict__ M, int64_t n, int k) {
-    __shared__ double rowbuf[8][128];
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    extern __shared__ double msh[];                  // [k * k]
+    __shared__ __align__(16) double rowbuf[8][4][128];
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) msh[i] = M[i];
+    __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (row >= n) return;
-    double *u = U + row * k;
-    double *ub = rowbuf[w];
-    for (int l = lane; l < k; l += 32) ub[l] = u[l];
-    __syncwarp();
-    for (int l = lane; l < k; l += 32) {
-        double s = 0.0;
-        for (int a = 0; a < k; ++a) s = __dadd_rn(s, __dmul_rn(ub[a], M[(int64_t)a * k + l]));
-        const double r = RH[row * k + l];
-        const double num = r > 0.0 ? r : 0.0;
-        const double den = __dadd_rn(s > 0.0 ? s : 0.0, EPS);
-        u[l] = __dmul_rn(ub[l], sqrt(num / den));
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * 4; r0 < n; r0 += (int64_t)gridDim.x * 8 * 4) {
+        const int nr = (int)(n - r0 < 4 ? n - r0 : 4);
+        double (*ub)[128] = rowbuf[w];
+        for (int r = 0; r < 4; ++r)
+            for (int l = lane; l < k; l += 32) ub[r][l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
+        __syncwarp();
+        for (int l = lane; l < k; l += 32) {
+            double sv[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int a = 0; a < k; ++a) {
+                const double m = msh[a * k + l];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) sv[r] = __dadd_rn(sv[r], __dmul_rn(ub[r][a], m));
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (r >= nr) continue;
+                const double rv = RH[(r0 + r) * k + l];
+                const double num = rv > 0.0 ? rv : 0.0;
+                const double den = __dadd_rn(sv[r] > 0.0 ? sv[r] : 0.0, EPS);
+                U[(r0 + r) * k + l] = __dmul_rn(ub[r][l], sqrt(num / den));
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -79,36 +92,60 @@ struct NciState {
 };
 
 // l* = argmax_l sum_a Ups[i,a] Phi[a,l]; warp per row, Phi and the row in smem.
+constexpr int AR = 4;     // rows per warp per pass (assign_kernel, ups_update_kernel)
+
 __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
                                                      int64_t n, int k, int32_t *__restrict__ labels, NciState s) {
     if (*s.done) return;
     extern __shared__ double phs[];
-    __shared__ double rowbuf[8][128];
+    __shared__ __align__(16) double rowbuf[8][AR][128];
     for (int i = threadIdx.x; i < k * k; i += blockDim.x) phs[i] = Phi[i];
     __syncthreads();
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (row >= n) return;
-    double *ub = rowbuf[w];
-    for (int l = lane; l < k; l += 32) ub[l] = U[row * k + l];
-    __syncwarp();
-    double best = 0.0;
-    int arg = 0x7fffffff;
-    for (int l = lane; l < k; l += 32) {
-        double sc = 0.0;
-        for (int a = 0; a < k; ++a) sc = __dadd_rn(sc, __dmul_rn(ub[a], phs[a * k + l]));
-        if (arg == 0x7fffffff || sc > best) { best = sc; arg = l; }
+    bool changed = false;
+    // AR rows per warp at a time: each Phi element read from smem serves AR rows
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * AR; r0 < n; r0 += (int64_t)gridDim.x * 8 * AR) {
+        const int nr = (int)(n - r0 < AR ? n - r0 : AR);
+        double (*ub)[128] = rowbuf[w];
+        for (int r = 0; r < AR; ++r)
+            for (int l = lane; l < k; l += 32) ub[r][l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
+        __syncwarp();
+        double best[AR];
+        int arg[AR];
+#pragma unroll
+        for (int r = 0; r < AR; ++r) { best[r] = 0.0; arg[r] = 0x7fffffff; }
+        for (int l = lane; l < k; l += 32) {
+            double sc[AR];
+#pragma unroll
+            for (int r = 0; r < AR; ++r) sc[r] = 0.0;
+            for (int a = 0; a < k; ++a) {
+                const double ph = phs[a * k + l];
+#pragma unroll
+                for (int r = 0; r < AR; ++r) sc[r] = __dadd_rn(sc[r], __dmul_rn(ub[r][a], ph));
+            }
+#pragma unroll
+            for (int r = 0; r < AR; ++r)
+                if (arg[r] == 0x7fffffff || sc[r] > best[r]) { best[r] = sc[r]; arg[r] = l; }
+        }
+#pragma unroll
+        for (int r = 0; r < AR; ++r) {
+            // warp argmax: larger score wins; equal scores -> smaller index
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best[r], o);
+                const int oa = __shfl_xor_sync(0xffffffffu, arg[r], o);
+                if (oa != 0x7fffffff && (arg[r] == 0x7fffffff || ob > best[r] || (ob == best[r] && oa < arg[r]))) {
+                    best[r] = ob;
+                    arg[r] = oa;
+                }
+            }
+            if (lane == 0 && r < nr) {
+                if (labels[r0 + r] != arg[r]) changed = true;
+                labels[r0 + r] = arg[r];
+            }
+        }
+        __syncwarp();
     }
-    // warp argmax: larger score wins; equal scores -> smaller index
-    for (int o = 16; o; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-        if (oa != 0x7fffffff && (arg == 0x7fffffff || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
-    }
-    if (lane == 0) {
-        if (labels[row] != arg) *s.changed = 1;
-        labels[row] = arg;
-    }
+    if (changed) *s.changed = 1;
 }
 
 // Small-k variant (k <= 16): one thread per row, the row of Ups in registers, Phi in smem
@@ -216,29 +253,62 @@ __global__ void nci_step_kernel(NciState s, int32_t *__restrict__ counts, int k)
     (void)counts; (void)k;
 }
 
-// per-block cluster sums over a fixed row range: part[b][l][a] = sum_{i in range, label l} U[i,a]
-// and per-block counts cpart[b][l].  Thread a (lanes over columns) walks the rows in order.
+// Per-block cluster sums over a fixed row range (k > 32 path): grid (blocks, 32-column chunks);
+// each warp owns a contiguous run of the block's rows and adds them in row order into its own
+// smem accumulators acc[w][l][lane] (lane = column of the chunk); warps are combined in order
+// -> part[b][l][a], cpart[b][l] (deterministic, no atomics).
 __global__ void cluster_sums_kernel(const double *__restrict__ U, const int32_t *__restrict__ labels, int64_t n,
-                                    int k, int64_t rows_per_block, double *__restrict__ part,
+                                    int k, int64_t rows_per_block, int nw, double *__restrict__ part,
                                     int64_t *__restrict__ cpart, const int32_t *__restrict__ done) {
     if (*done) return;
-    extern __shared__ double acc[];          // [k][k]
-    int64_t *cnt = reinterpret_cast<int64_t *>(acc + (size_t)k * k);
-    for (int i = threadIdx.x; i < k * k; i += blockDim.x) acc[i] = 0.0;
-    for (int i = threadIdx.x; i < k; i += blockDim.x) cnt[i] = 0;
+    extern __shared__ double sh[];
+    double *acc = sh;                                          // [nw][k][32]
+    int *cnt = reinterpret_cast<int *>(acc + (size_t)nw * k * 32);   // [nw][k]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nt = blockDim.x;
+    for (int i = threadIdx.x; i < nw * k * 32; i += nt) acc[i] = 0.0;
+    for (int i = threadIdx.x; i < nw * k; i += nt) cnt[i] = 0;
     __syncthreads();
-    const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
-    const int a = threadIdx.x;
-    if (a < k) {
-        for (int64_t i = r0; i < r1; ++i) {
-            const int l = labels[i];
-            acc[(int64_t)l * k + a] += U[i * k + a];
-            if (a == 0) cnt[l] += 1;
+    const int a = blockIdx.y * 32 + lane;
+    const bool act = a < k;
+    const int64_t b0 = blockIdx.x * rows_per_block, b1 = min(n, b0 + rows_per_block);
+    const int64_t per_w = (rows_per_block + nw - 1) / nw;
+    const int64_t w0 = min(b1, b0 + w * per_w), w1 = min(b1, w0 + per_w);
+    double *my = acc + (size_t)w * k * 32 + lane;
+    int *myc = cnt + w * k;
+    int64_t i = w0;
+    for (; i + 4 <= w1; i += 4) {
+        int l[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            l[u] = labels[i + u];
+            v[u] = act ? U[(i + u) * k + a] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            my[l[u] * 32] += v[u];
+            if (lane == 0 && blockIdx.y == 0) myc[l[u]] += 1;
         }
     }
+    for (; i < w1; ++i) {
+        const int l = labels[i];
+        my[l * 32] += act ? U[i * k + a] : 0.0;
+        if (lane == 0 && blockIdx.y == 0) myc[l] += 1;
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < k * k; i += blockDim.x) part[blockIdx.x * (int64_t)k * k + i] = acc[i];
-    for (int i = threadIdx.x; i < k; i += blockDim.x) cpart[blockIdx.x * (int64_t)k + i] = cnt[i];
+    for (int e = threadIdx.x; e < k * 32; e += nt) {
+        const int l = e / 32, c = e % 32, col = blockIdx.y * 32 + c;
+        if (col >= k) continue;
+        double v = 0.0;
+        for (int ww = 0; ww < nw; ++ww) v += acc[((size_t)ww * k + l) * 32 + c];
+        part[blockIdx.x * (int64_t)k * k + (int64_t)l * k + col] = v;
+    }
+    if (blockIdx.y == 0)
+        for (int l = threadIdx.x; l < k; l += nt) {
+            int64_t c = 0;
+            for (int ww = 0; ww < nw; ++ww) c += cnt[ww * k + l];
+            cpart[blockIdx.x * (int64_t)k + l] = c;
+        }
 }
 
 // Phi[a,l] = (sum_b part[b][l][a]) / sqrt(count_l)   (zero column for an empty cluster);
@@ -312,6 +382,9 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const int64_t mx = std::max(n, D) * k;
     init_factors_kernel<<<cdiv(mx, 256), 256, 0, st>>>(Gamma, n, Psi, sig, D, k, U, H);
     TPO_LAUNCH_CHECK();
+    const size_t ups_smem = sizeof(double) * k * k;
+    // static rowbuf (32 KB) + dynamic M: opt in whenever the total passes the 48 KB default
+    TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
     for (int t = 0; t < Tf; ++t) {
         onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
         ar.off = mark;
@@ -323,7 +396,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
         dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;
-        ups_update_kernel<<<cdiv(n * 32, 256), 256, 0, st>>>(U, RH, M, n, k);
+        ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 32), 148 * 8), 256, ups_smem, st>>>(U, RH, M, n, k);
         TPO_LAUNCH_CHECK();
     }
     // Alg. 3
@@ -334,18 +407,16 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     eye_kernel<<<cdiv(k * k, 256), 256, 0, st>>>(Phi, k);
     TPO_LAUNCH_CHECK();
     const size_t phi_smem = sizeof(double) * k * k;
-    const size_t sum_smem = sizeof(double) * k * k + sizeof(int64_t) * k;
-    if (phi_smem > 48 * 1024)
-        TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));
-    if (sum_smem > 48 * 1024)
-        TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
-    const int sum_threads = (int)std::max<int64_t>(32, cdiv(k, 32) * 32);
+    const int sum_nw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / ((int64_t)k * (32 * 8 + 4))));
+    const size_t sum_smem = (size_t)sum_nw * k * (32 * sizeof(double) + sizeof(int));
+    TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));
+    TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
+    // rows per block for the sums / fused passes: whole 32-row runs per warp, ~2 blocks per SM
+    const int64_t rpf = std::max<int64_t>(rpb, cdiv(cdiv(n, 2 * 148), 256) * 256);
+    const int64_t nbf = cdiv(n, rpf);
     for (int t = 0; t < Tg; ++t) {
         const bool last = t == Tg - 1;           // the last Phi update is never used
         if (k <= 32 && !last) {
-            // rows per block: whole 32-row chunks for each of the 8 warps, ~2 blocks per SM
-            const int64_t rpf = std::max<int64_t>(rpb, cdiv(cdiv(n, 2 * 148), 256) * 256);
-            const int64_t nbf = cdiv(n, rpf);
             if (k <= 8) nci_fused_kernel<8, 8><<<nbf, 256, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
             else if (k <= 16) nci_fused_kernel<16, 8><<<nbf, 256, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
             else nci_fused_kernel<32, 4><<<nbf, 128, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
@@ -359,14 +430,16 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         if (k <= 16)
             assign_small_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
         else
-            assign_kernel<<<cdiv(n * 32, 256), 256, phi_smem, st>>>(U, Phi, n, k, labels, s);
+            assign_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * AR), 148 * 8), 256, phi_smem, st>>>(U, Phi, n, k,
+                                                                                                  labels, s);
         TPO_LAUNCH_CHECK();
         nci_step_kernel<<<1, 32, 0, st>>>(s, nullptr, k);
         TPO_LAUNCH_CHECK();
         if (last) break;
-        cluster_sums_kernel<<<nb, sum_threads, sum_smem, st>>>(U, labels, n, k, rpb, part, cpart, s.done);
+        cluster_sums_kernel<<<dim3((unsigned)nbf, (unsigned)cdiv(k, 32)), sum_nw * 32, sum_smem, st>>>(
+            U, labels, n, k, rpf, sum_nw, part, cpart, s.done);
         TPO_LAUNCH_CHECK();
-        phi_kernel<<<cdiv((int64_t)k * k * 32, 256), 256, 0, st>>>(part, cpart, nb, k, Phi, s.done);
+        phi_kernel<<<cdiv((int64_t)k * k * 32, 256), 256, 0, st>>>(part, cpart, nbf, k, Phi, s.done);
         TPO_LAUNCH_CHECK();
     }
     int32_t it = 0;

@@ -22,32 +22,75 @@ void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int6
 
 namespace {
 
-// Column statistics of an n x k fp32 matrix: sum (fp64), sum |x| (fp64), argmax |x| (first
-// index).  One block per column, fixed-order tree reduction.
-__global__ void colstats_kernel(const float *__restrict__ A, int64_t n, int k, double *__restrict__ out_sum,
-                                double *__restrict__ out_abs, int64_t *__restrict__ out_arg) {
-    __shared__ double ss[256], sa[256], sm[256];
-    __shared__ int64_t si[256];
-    const int c = blockIdx.x, t = threadIdx.x;
+// Column statistics of an n x k fp64 matrix: sum, sum |x|, argmax |x| (first index).  Stage 1:
+// a block per fixed row range, warps own contiguous sub-ranges (rows in order), lanes own
+// columns; warps are combined in order.  Stage 2 combines the blocks in order (strict '>'
+// keeps the smallest index among equal magnitudes).  Deterministic.
+constexpr int CS_WARPS = 8;
+__global__ void __launch_bounds__(CS_WARPS * 32) colstats_part_kernel(const double *__restrict__ A, int64_t n, int k,
+                                                                      int64_t rows_per, double *__restrict__ ps,
+                                                                      double *__restrict__ pa, double *__restrict__ pm,
+                                                                      int64_t *__restrict__ pi) {
+    __shared__ double ss[CS_WARPS][128], sa[CS_WARPS][128], smx[CS_WARPS][128];
+    __shared__ int64_t si[CS_WARPS][128];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t b0 = blockIdx.x * rows_per, b1 = min(n, b0 + rows_per);
+    const int64_t per_w = (rows_per + CS_WARPS - 1) / CS_WARPS;
+    const int64_t w0 = min(b1, b0 + w * per_w), w1 = min(b1, w0 + per_w);
+    for (int c = lane; c < k; c += 32) {
+        double s = 0.0, a = 0.0, best = -1.0;
+        int64_t bi = 0;
+        for (int64_t i = w0; i < w1; ++i) {
+            const double v = A[i * k + c];
+            s += v;
+            a += fabs(v);
+            if (fabs(v) > best) { best = fabs(v); bi = i; }
+        }
+        ss[w][c] = s; sa[w][c] = a; smx[w][c] = best; si[w][c] = bi;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += CS_WARPS * 32) {
+        double s = 0.0, a = 0.0, best = -1.0;
+        int64_t bi = 0;
+        for (int ww = 0; ww < CS_WARPS; ++ww) {
+            s += ss[ww][c];
+            a += sa[ww][c];
+            if (smx[ww][c] > best) { best = smx[ww][c]; bi = si[ww][c]; }
+        }
+        ps[blockIdx.x * (int64_t)k + c] = s;
+        pa[blockIdx.x * (int64_t)k + c] = a;
+        pm[blockIdx.x * (int64_t)k + c] = best;
+        pi[blockIdx.x * (int64_t)k + c] = bi;
+    }
+}
+
+__global__ void colstats_final_kernel(const double *__restrict__ ps, const double *__restrict__ pa,
+                                      const double *__restrict__ pm, const int64_t *__restrict__ pi, int64_t G, int k,
+                                      double *__restrict__ out_sum, double *__restrict__ out_abs,
+                                      int64_t *__restrict__ out_arg) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
     double s = 0.0, a = 0.0, best = -1.0;
     int64_t bi = 0;
-    for (int64_t i = t; i < n; i += 256) {
-        const double v = (double)A[i * k + c];
-        s += v;
-        a += fabs(v);
-        if (fabs(v) > best) { best = fabs(v); bi = i; }
+    for (int64_t g = 0; g < G; ++g) {
+        s += ps[g * k + c];
+        a += pa[g * k + c];
+        if (pm[g * k + c] > best) { best = pm[g * k + c]; bi = pi[g * k + c]; }
     }
-    ss[t] = s; sa[t] = a; sm[t] = best; si[t] = bi;
-    __syncthreads();
-    for (int o = 128; o; o >>= 1) {
-        if (t < o) {
-            ss[t] += ss[t + o];
-            sa[t] += sa[t + o];
-            if (sm[t + o] > sm[t] || (sm[t + o] == sm[t] && si[t + o] < si[t])) { sm[t] = sm[t + o]; si[t] = si[t + o]; }
-        }
-        __syncthreads();
-    }
-    if (t == 0) { out_sum[c] = ss[0]; out_abs[c] = sa[0]; out_arg[c] = si[0]; }
+    out_sum[c] = s;
+    out_abs[c] = a;
+    out_arg[c] = bi;
+}
+
+__global__ void flip_cols_f64(double *__restrict__ A, int64_t n, int k, const int *__restrict__ sgn) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * k) return;
+    if (sgn[i % k] < 0) A[i] = -A[i];
+}
+
+__global__ void cast_f64_f32_k(const double *__restrict__ a, int64_t len, float *__restrict__ b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < len) b[i] = (float)a[i];
 }
 
 __global__ void flip_cols_f32(float *__restrict__ A, int64_t n, int k, const int *__restrict__ sgn) {
@@ -344,12 +387,18 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
 }
 
 // Sign rule R8 on (Gamma, Psi): sum_i Gamma[i,l] >= 0, else (near-zero sums) the sign of the
-// largest-magnitude entry.  Flips are applied to both factors.
-void apply_sign_rule(float *Gamma, int64_t n, int k, float *Psi, int64_t D, Arena &ar, cudaStream_t st) {
+// largest-magnitude entry.  Flips are applied to both factors (Gamma fp64 here).
+void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Arena &ar, cudaStream_t st) {
     const size_t mark = ar.off;
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(2 * 148, cdiv(n, 64)));
+    const int64_t rows_per = cdiv(n, G);
+    double *ps = ar.take<double>(G * k), *pa = ar.take<double>(G * k), *pm = ar.take<double>(G * k);
+    int64_t *pi = ar.take<int64_t>(G * k);
     double *s = ar.take<double>(k), *a = ar.take<double>(k);
     int64_t *arg = ar.take<int64_t>(k);
-    colstats_kernel<<<k, 256, 0, st>>>(Gamma, n, k, s, a, arg);
+    colstats_part_kernel<<<G, CS_WARPS * 32, 0, st>>>(Gamma, n, k, rows_per, ps, pa, pm, pi);
+    TPO_LAUNCH_CHECK();
+    colstats_final_kernel<<<cdiv(k, 128), 128, 0, st>>>(ps, pa, pm, pi, G, k, s, a, arg);
     TPO_LAUNCH_CHECK();
     std::vector<double> hs = to_host(s, k, st), ha = to_host(a, k, st);
     std::vector<int64_t> harg = to_host(arg, k, st);
@@ -357,9 +406,9 @@ void apply_sign_rule(float *Gamma, int64_t n, int k, float *Psi, int64_t D, Aren
     bool any = false;
     for (int l = 0; l < k; ++l) {
         if (fabs(hs[l]) < 1e-6 * ha[l]) {
-            float v;
-            TPO_CUDA(cudaMemcpy(&v, Gamma + harg[l] * k + l, sizeof(float), cudaMemcpyDeviceToHost));
-            sg[l] = v < 0.f ? -1 : 1;
+            double v;
+            TPO_CUDA(cudaMemcpy(&v, Gamma + harg[l] * k + l, sizeof(double), cudaMemcpyDeviceToHost));
+            sg[l] = v < 0.0 ? -1 : 1;
         } else {
             sg[l] = hs[l] < 0.0 ? -1 : 1;
         }
@@ -367,7 +416,7 @@ void apply_sign_rule(float *Gamma, int64_t n, int k, float *Psi, int64_t D, Aren
     }
     if (any) {
         int *dsg = to_dev(ar, sg, st);
-        flip_cols_f32<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
+        flip_cols_f64<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
         TPO_LAUNCH_CHECK();
         flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
         TPO_LAUNCH_CHECK();
@@ -376,43 +425,54 @@ void apply_sign_rule(float *Gamma, int64_t n, int k, float *Psi, int64_t D, Aren
     ar.off = mark;
 }
 
-// CholeskyQR2 polish of the fp32 n x k Gamma when its Gram is off identity by > 1e-6.
-void polish_gamma(float *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
+// CholeskyQR polish of the fp64 n x k Gamma while its Gram is off identity by > 1e-6 (at most
+// two corrections): G = Gamma^T Gamma (dgemm), Ci = S C^{-1} (chol_inv), Gamma <- Gamma Ci.
+void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
     const size_t mark = ar.off;
-    double *g = ar.take<double>((size_t)k * k);
-    float *tmp = nullptr;
+    double *g = ar.take<double>((size_t)k * k), *ci = ar.take<double>((size_t)k * k);
+    double *tmp = nullptr;
+    int *flag = ar.take<int>(1);
+    TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
     for (int pass = 0; pass < 3; ++pass) {
-        tsgemm_AtB_f32f32(Gamma, k, nullptr, Gamma, k, nullptr, n, k, k, g, ar, st);
+        dgemm(true, k, k, n, 1.0, Gamma, k, Gamma, k, 0.0, g, k, ar, st);
         std::vector<double> gh = to_host(g, (size_t)k * k, st);
         double dev = 0.0;
         for (int a = 0; a < k; ++a)
             for (int b = 0; b < k; ++b) dev = std::max(dev, fabs(gh[a * k + b] - (a == b ? 1.0 : 0.0)));
         if (dev <= 1e-6 || pass == 2) break;
-        std::vector<double> C((size_t)k * k), Ci((size_t)k * k);
-        if (!host_cholesky_upper(k, gh.data(), C.data()))
-            throw Error(TPO_ENUMERIC, "CholeskyQR2 polish: Gamma^T Gamma not positive definite");
-        host_upper_inverse(k, C.data(), Ci.data());
-        double *ci = to_dev(ar, Ci, st);
-        if (!tmp) tmp = ar.take<float>((size_t)n * k);
-        tsgemm_AW_f32(Gamma, k, nullptr, ci, n, k, k, tmp, k, st);
-        TPO_CUDA(cudaMemcpyAsync(Gamma, tmp, sizeof(float) * n * k, cudaMemcpyDeviceToDevice, st));
+        if (k <= 112) {
+            chol_inv_device(g, k, ci, flag, st);
+        } else {
+            std::vector<double> C((size_t)k * k), Ci((size_t)k * k);
+            if (!host_cholesky_upper(k, gh.data(), C.data()))
+                throw Error(TPO_ENUMERIC, "CholeskyQR2 polish: Gamma^T Gamma not positive definite");
+            host_upper_inverse(k, C.data(), Ci.data());
+            TPO_CUDA(cudaMemcpyAsync(ci, Ci.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
+        }
+        if (!tmp) tmp = ar.take<double>((size_t)n * k);
+        dgemm(false, n, k, k, 1.0, Gamma, k, ci, k, 0.0, tmp, k, ar, st);
+        TPO_CUDA(cudaMemcpyAsync(Gamma, tmp, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
     }
-    TPO_CUDA(cudaStreamSynchronize(st));
+    check_flag(flag, st, "CholeskyQR2 polish of Gamma");
     ar.off = mark;
 }
 
-// Gamma = diag(rs) A Psi64 diag(1/sigma), Psi (fp32 out) = Psi64.
+// Gamma = diag(dinv) R' Psi64 diag(1/sigma) in fp64, polished and sign-fixed, then rounded to
+// fp32; Psi (fp32 out) = Psi64.
 void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
                     const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st) {
     std::vector<double> ph = to_host(Psi64, (size_t)D * k, st);
     for (int64_t j = 0; j < D; ++j)
         for (int l = 0; l < k; ++l) ph[j * k + l] /= sig[l];
     double *w = to_dev(ar, ph, st);
-    tsgemm_AW_f32(Rp, D, dinv, w, n, D, k, Gamma, k, st);
+    double *G64 = ar.take<double>((size_t)n * k);
+    tsgemm_AW_f64(Rp, D, dinv, w, n, D, k, G64, k, st);
     cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
     TPO_LAUNCH_CHECK();
-    polish_gamma(Gamma, n, k, ar, st);
-    apply_sign_rule(Gamma, n, k, Psi, D, ar, st);
+    polish_gamma(G64, n, k, ar, st);
+    apply_sign_rule(G64, n, k, Psi, D, ar, st);
+    cast_f64_f32_k<<<cdiv(n * k, 256), 256, 0, st>>>(G64, n * k, Gamma);
+    TPO_LAUNCH_CHECK();
 }
 
 __global__ void copy2d_kernel(const double *__restrict__ src, int64_t lds, double *__restrict__ dst, int64_t ldd,
@@ -469,7 +529,8 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
     s += align_up(sizeof(double) * D * D) + gram_tc_ws(n, D);
     s += align_up(sizeof(double) * D * D) + align_up(sizeof(double) * (n + D + 64));
     s += 8 * align_up(sizeof(double) * D * (std::max(b, bh) + 1)) + 8 * align_up(sizeof(double) * (b + 1) * (b + 1) + 8);
-    s += 2 * align_up(sizeof(double) * D * k) + tsgemm_ws(n, k, k) + align_up(sizeof(float) * n * k);
+    s += 2 * align_up(sizeof(double) * D * k) + 2 * align_up(sizeof(double) * n * k) + dgemm_ws(n, k, k) +
+         4 * align_up(sizeof(double) * 2 * 148 * k) + 8 * align_up(sizeof(double) * k * k);
     if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
     s += dgemm_ws(std::max(n, D), std::max(b, bh) + 1, 0) + 2 * align_up(sizeof(double) * (std::max(b, bh) + 1) * (std::max(b, bh) + 1));
     return s + 64 * 256;

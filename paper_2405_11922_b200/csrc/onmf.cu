@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(NT) onmf_rh_kernel(const float *__restrict__ R
 }
 
 // k-chunk widths that are instantiated (a chunk is padded up to the next one)
-constexpr int KCS[] = {2, 4, 5, 8, 10, 12, 16, 20, 25, 32, 50};
+constexpr int KCS[] = {2, 4, 5, 8, 10, 12, 16, 20, 26, 32, 50};
 
 int pick_kc(int need) {
     for (int v : KCS)
@@ -178,10 +178,12 @@ struct RtuPlan {
 
 RtuPlan rtu_plan(int64_t n, int D, int k) {
     RtuPlan p;
-    p.nkc = (k + 49) / 50;
+    // k chunks of <= 26 columns: each broadcast smem read of dinv.Ups feeds CPT FMAs, so a thread
+    // owns >= 2 columns of R' whenever D allows (CPT x KC <= 64 accumulators: 2 CTAs / SM)
+    p.nkc = (k + 25) / 26;
     p.kc = pick_kc((k + p.nkc - 1) / p.nkc);
     const int want = (D + NT - 1) / NT;                 // columns per thread to cover D in one block
-    const int cap = std::max(1, std::min(8, 48 / p.kc));  // CPT x KC accumulators <= 48: 2 CTAs / SM
+    const int cap = std::max(1, std::min(8, 64 / p.kc));
     int cpt = 1;
     while (cpt < want && cpt * 2 <= cap) cpt *= 2;
     p.cpt = cpt;
@@ -198,8 +200,8 @@ template <int KC>
 void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float *dinv, const double *U, int k,
                 double *part, cudaStream_t st) {
     const dim3 grid((unsigned)p.G, (unsigned)p.ncb, (unsigned)p.nkc);
-    // only CPT x KC <= 48 (or CPT = 1) is planned (rtu_plan); the other combinations are not instantiated
-    constexpr int C8 = 8 * KC <= 48 ? 8 : 1, C4 = 4 * KC <= 48 ? 4 : 1, C2 = 2 * KC <= 48 ? 2 : 1;
+    // only CPT x KC <= 64 (or CPT = 1) is planned (rtu_plan); the other combinations are not instantiated
+    constexpr int C8 = 8 * KC <= 64 ? 8 : 1, C4 = 4 * KC <= 64 ? 4 : 1, C2 = 2 * KC <= 64 ? 2 : 1;
     switch (p.cpt) {
         case 1: onmf_rtu_kernel<1, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
         case 2: onmf_rtu_kernel<C2, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
@@ -244,7 +246,7 @@ void launch_rh(int rpw, int nkc, const float *Rp, int64_t n, int D, const float 
         case 12: F<12>(__VA_ARGS__); break;            \
         case 16: F<16>(__VA_ARGS__); break;            \
         case 20: F<20>(__VA_ARGS__); break;            \
-        case 25: F<25>(__VA_ARGS__); break;            \
+        case 26: F<26>(__VA_ARGS__); break;            \
         case 32: F<32>(__VA_ARGS__); break;            \
         default: F<50>(__VA_ARGS__); break;            \
     }

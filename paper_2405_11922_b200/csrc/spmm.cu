@@ -29,6 +29,7 @@ namespace tpo {
 namespace {
 
 constexpr int CHUNK = 256;           // edges per long-row chunk; also the row-block grouping grain
+constexpr int kCounters = 64;        // persistent-warp work counters zeroed together
 constexpr int WPB = 8;               // warps per block
 constexpr int UNR = 8;               // neighbour rows in flight per warp
 
@@ -225,6 +226,9 @@ struct SpmmArgs {
     float c, alpha;
     float4 *out;              // Q (EPI_V), P (EPI_U), Z (EPI_FINAL)
     float4 *out_hat;          // Zhat (EPI_FINAL, fused when nslices == 1), else null
+    unsigned long long *work; // persistent-warp work counter of this launch (zeroed)
+    int reserve_sms;          // SMs left free (blocks placed on them exit) for concurrent side-stream work
+    int smid_limit;           // = SMs - reserve_sms, set at launch
 };
 
 __device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {
@@ -404,17 +408,10 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
     }
 }
 
-template <int EPI, bool WEIGHTED, int SL, int MINB>
-__global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+// One work unit: item `item` of the schedule for column group `grp`.
+template <int EPI, bool WEIGHTED, int SL>
+__device__ __forceinline__ void spmm_unit(const SpmmArgs &a, int grp, int64_t item, int64_t n_items) {
     const int lane = threadIdx.x & 31;
-    const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
-    const int64_t n_items = tot >> 32;
-    // group-major order: concurrently running warps work on the same column group, so the
-    // gathered working set is one group of the dense operand (L2-resident for d > 128 SL)
-    const int grp = (int)(gw / a.sch.max_items);
-    const int64_t item = gw - (int64_t)grp * a.sch.max_items;
-    if (item >= n_items) return;
     const int4 it = a.sch.items[item];
     int c4[SL];
     bool act[SL];
@@ -436,6 +433,31 @@ __global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
 #pragma unroll
     for (int q = 0; q < SL; ++q)
         if (act[q]) a.partials[(int64_t)it.z * a.d4 + c4[q]] = acc[q];
+}
+
+// Persistent warps: the grid is the resident capacity (SMs x MINB blocks); each warp takes the
+// next work unit from a device counter (*a.work, zeroed before the launch).  Units are ordered
+// group-major, so concurrently running warps work on the same column group (its gathered
+// working set stays L2-resident) -- and no block holds its slot while one slow warp finishes.
+// Which warp runs a unit does not change its result (each unit is computed by one warp in a
+// fixed order), so results stay deterministic.
+template <int EPI, bool WEIGHTED, int SL, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    if ((int)smid >= a.smid_limit) return;            // a reserved SM: leave it to the side stream
+    const int lane = threadIdx.x & 31;
+    const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
+    const int64_t n_items = tot >> 32;
+    const int64_t units = n_items * a.ngroups;
+    while (true) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(a.work, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if ((int64_t)u >= units) return;
+        const int grp = (int)((int64_t)u / n_items);
+        spmm_unit<EPI, WEIGHTED, SL>(a, grp, (int64_t)u - (int64_t)grp * n_items, n_items);
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -609,6 +631,13 @@ __global__ void __launch_bounds__(WPB * 32) fixup_kernel(SpmmArgs a) {
     if (act) {
         const float4 *p = a.partials + (int64_t)slot * a.d4 + c4;
         int j = 0;
+        for (; j + 16 <= s.z; j += 16) {               // 16 loads in flight, added in chunk order
+            float4 v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = p[(int64_t)(j + u) * a.d4];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc = f4add(acc, v[u]);
+        }
         for (; j + 4 <= s.z; j += 4) {
             float4 v0 = p[(int64_t)(j + 0) * a.d4], v1 = p[(int64_t)(j + 1) * a.d4];
             float4 v2 = p[(int64_t)(j + 2) * a.d4], v3 = p[(int64_t)(j + 3) * a.d4];
@@ -687,6 +716,7 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
 int spmm_variant(int nslices) {
     int v = nslices >= 2 ? 23 : 14;      // measured best on small (d = 1000) and medium (d = 256)
     if (const char *e = getenv("TPO_SPMM_VARIANT")) v = atoi(e);
+    if (v < 1000 && v != 13 && v != 14 && v != 22 && v != 23 && v != 42 && v != 82) v = 14;
     if (v >= 1000) {                     // cp.async ring variants: 1000 + SL * 100 + RING
         int sl = (v - 1000) / 100, ring = v % 100;
         if (sl != 1 && sl != 2 && sl != 4) sl = 1;
@@ -729,13 +759,20 @@ void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
         TPO_LAUNCH_CHECK();
         return;
     }
+    // persistent warps: at most the resident capacity (SMs x MINB blocks of WPB warps)
+    const int minb = var % 10;
+    const int nsm = sm_count();
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)nsm * minb));
+    // the reserve applies only to a full-capacity grid (blocks on every SM, so the blocks of the
+    // non-reserved SMs exist and drain the work queue); a smaller grid keeps every block
+    a.smid_limit = (int64_t)grid == (int64_t)nsm * minb ? std::max(1, nsm - std::max(0, a.reserve_sms)) : (1 << 30);
     switch (var) {
-        case 13: spmm_kernel<EPI, W, 1, 3><<<blocks, WPB * 32, 0, st>>>(a); break;
-        case 23: spmm_kernel<EPI, W, 2, 3><<<blocks, WPB * 32, 0, st>>>(a); break;
-        case 22: spmm_kernel<EPI, W, 2, 2><<<blocks, WPB * 32, 0, st>>>(a); break;
-        case 42: spmm_kernel<EPI, W, 4, 2><<<blocks, WPB * 32, 0, st>>>(a); break;
-        case 82: spmm_kernel<EPI, W, 8, 2><<<blocks, WPB * 32, 0, st>>>(a); break;
-        default: a.ngroups = a.nslices; spmm_kernel<EPI, W, 1, 4><<<cdiv(max_items * a.nslices, WPB), WPB * 32, 0, st>>>(a); break;
+        case 13: spmm_kernel<EPI, W, 1, 3><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 23: spmm_kernel<EPI, W, 2, 3><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 22: spmm_kernel<EPI, W, 2, 2><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 42: spmm_kernel<EPI, W, 4, 2><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 82: spmm_kernel<EPI, W, 8, 2><<<grid, WPB * 32, 0, st>>>(a); break;
+        default: spmm_kernel<EPI, W, 1, 4><<<grid, WPB * 32, 0, st>>>(a); break;
     }
     TPO_LAUNCH_CHECK();
 }
@@ -760,11 +797,12 @@ size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
     sched_alloc(ar, n_u, nnz);
     sched_alloc(ar, n_v, nnz);
     ar.take<float>((2 * (nnz / CHUNK) + 1) * d);  // partials (shared by both SpMMs)
+    ar.take<unsigned long long>(kCounters);       // persistent-warp work counters
     return ar.off + 256;
 }
 
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
-                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st) {
+                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms) {
     const int64_t n = B.n_rows, m = B.n_cols, nnz = B.nnz;
     const int d4 = (int)(d / 4);
     const float c = alpha < 1.0f ? 1.0f - alpha : 1.0f;    // R1
@@ -774,6 +812,12 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     SchedBufs sb = sched_alloc(ar, n, nnz);
     SchedBufs sbt = sched_alloc(ar, m, nnz);
     float *partials = ar.take<float>((2 * (nnz / CHUNK) + 1) * d);
+    unsigned long long *work = ar.take<unsigned long long>(kCounters);
+    int launches = 0;
+    auto counter = [&]() {        // a zeroed counter per SpMM launch (the pool is re-zeroed when it wraps)
+        if (launches % kCounters == 0) TPO_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) * kCounters, st));
+        return work + (launches++ % kCounters);
+    };
 
     const int TB = 256;
     if (n > 0) degree_scale_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>(B.row_ptr, B.val, n, su);
@@ -801,7 +845,7 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
             a.rowptr = Bt.row_ptr; a.col = Bt.col_idx; a.val = Bt.val;
             a.src = (const float4 *)Z; a.d4 = d4; a.nslices = nslices;
             a.sch = sbt.s; a.n_rows = m; a.partials = (float4 *)partials;
-            a.scale = sv; a.out = (float4 *)Qv;
+            a.scale = sv; a.out = (float4 *)Qv; a.work = counter(); a.reserve_sms = reserve_sms;
             spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
         } else {
             TPO_CUDA(cudaMemsetAsync(Qv, 0, 0, st));
@@ -811,7 +855,7 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
         a.src = (const float4 *)Qv; a.d4 = d4; a.nslices = nslices;
         a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
         a.scale = su; a.X = (const float4 *)X; a.c = c; a.alpha = alpha;
-        a.out = (float4 *)Z;
+        a.out = (float4 *)Z; a.work = counter(); a.reserve_sms = reserve_sms;
         if (last) {
             a.out_hat = (nslices == 1 && Zhat) ? (float4 *)Zhat : nullptr;
             spmm_launch<EPI_FINAL>(a, sb.s.max_items, sb.s.max_slots, B.val != nullptr, st);
@@ -832,6 +876,7 @@ size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d) {
     Arena ar(nullptr, 0);
     sched_alloc(ar, n_rows, nnz);
     ar.take<float>((2 * (nnz / CHUNK) + 1) * d);
+    ar.take<unsigned long long>(1);
     return ar.off + 256;
 }
 
@@ -868,6 +913,8 @@ void shard_vside_impl(const tpo_csr_t &Btp, const float *Pp, int64_t d, float *Q
     a.src = (const float4 *)Pp; a.d4 = d4; a.nslices = (d4 + 31) / 32;
     a.sch = sb.s; a.n_rows = m; a.partials = (float4 *)partials;
     a.out = (float4 *)Qpart;
+    a.work = ar.take<unsigned long long>(1);
+    TPO_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
     spmm_launch<EPI_RAW>(a, sb.s.max_items, sb.s.max_slots, Btp.val != nullptr, st);
 }
 
@@ -893,6 +940,8 @@ void shard_uside_impl(const tpo_csr_t &Bp, const float *Q, const float *Xp, int6
     a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
     a.scale = s_u; a.X = (const float4 *)Xp; a.c = alpha < 1.0f ? 1.0f - alpha : 1.0f; a.alpha = alpha;
     a.out = (float4 *)Zp;
+    a.work = ar.take<unsigned long long>(1);
+    TPO_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
     if (last) {
         a.out_hat = (nslices == 1 && Zhat_p) ? (float4 *)Zhat_p : nullptr;
         spmm_launch<EPI_FINAL>(a, sb.s.max_items, sb.s.max_slots, Bp.val != nullptr, st);

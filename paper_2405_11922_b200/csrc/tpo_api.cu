@@ -311,6 +311,9 @@ size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, i
     return s + stage + 8 * 256;
 }
 
+// SMs left to the Haar rotation while the (persistent) propagation kernels run beside it
+constexpr int kHaarReserveSms = 8;
+
 int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T, int32_t k,
             const double *G, int32_t eig_mode, const float *Omega, int32_t p, int32_t q, int32_t Tf, int32_t Tg,
             int32_t *labels, double *timings_ms, void *ws, size_t ws_bytes, void *stream) {
@@ -354,7 +357,7 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
         cudaStream_t side = res.side;
         TPO_CUDA(cudaEventRecord(ev[0], st));
         TPO_CUDA(cudaEventRecord(fork, st));
-        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st);
+        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, kHaarReserveSms);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[1], st));
         // Alg. 1 L6-7 depends only on G: it runs on a side stream beside the propagation

@@ -89,8 +89,10 @@ int sm_count();
 // ----------------------------------------------------------------------------------------
 // Module entry points (implemented in the .cu files; called by tpo_api.cu)
 // ----------------------------------------------------------------------------------------
+// reserve_sms: SMs' worth of block slots the persistent SpMM grids leave free (tpo_run keeps
+// a few for the Haar rotation running beside the propagation on a side stream).
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
-                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st);
+                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms = 0);
 // sharded propagation pieces (spmm.cu)
 size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d);
 void shard_degrees_impl(const tpo_csr_t &Bp, const tpo_csr_t &Btp, double *deg_u, double *deg_v, cudaStream_t st);

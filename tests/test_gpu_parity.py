@@ -270,6 +270,21 @@ def test_cluster_iterations(tpo, Tf, Tg):
     assert it == it_o and np.array_equal(lab.cpu().numpy(), lab_o)
 
 
+@pytest.mark.parametrize("k,Tf,Tg", [(40, 3, 20), (50, 2, 10)])
+def test_cluster_bit_exact_k_over_32(tpo, k, Tf, Tg):
+    """The k > 32 discretisation path (warp-per-row assign with 4 rows per warp, column-chunked
+    cluster sums, smem-staged M in the Upsilon update): labels bit-exact vs the oracle."""
+    g = planted_abg(6000, 4000, k, 48, deg=("poisson", 10.0), p_in=0.8, x=("gaussian", 1.0), alpha=0.5, T=2,
+                    seed=k)
+    Rp, dinv = oracle_features_of(g)
+    Gmo, so, Pso, _ = O.topk(Rp, dinv, k)
+    Gm32, Ps32 = Gmo.astype(np.float32), Pso.astype(np.float32)
+    lab_o, it_o, _ = O.cluster(Rp, dinv, Gm32, so, Ps32, Tf, Tg)
+    lab, it = tpo.cluster(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), torch.from_numpy(Gm32).cuda(), so,
+                          torch.from_numpy(Ps32).cuda(), Tf, Tg)
+    assert it == it_o and np.array_equal(lab.cpu().numpy(), lab_o)
+
+
 # ------------------------------------------------------------------------------------------
 # end to end
 # ------------------------------------------------------------------------------------------
