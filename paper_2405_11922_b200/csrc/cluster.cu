@@ -92,13 +92,13 @@ struct NciState {
 };
 
 // l* = argmax_l sum_a Ups[i,a] Phi[a,l]; warp per row, Phi and the row in smem.
-constexpr int AR = 4;     // rows per warp per pass (assign_kernel, ups_update_kernel)
+constexpr int AR = 8;     // rows per warp per pass (assign_kernel)
 
 __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
                                                      int64_t n, int k, int32_t *__restrict__ labels, NciState s) {
     if (*s.done) return;
-    extern __shared__ double phs[];
-    __shared__ __align__(16) double rowbuf[8][AR][128];
+    extern __shared__ __align__(16) double phs[];         // [k * k] then rowbuf [8][AR][k]
+    double *rowbuf_all = phs + k * k;
     for (int i = threadIdx.x; i < k * k; i += blockDim.x) phs[i] = Phi[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -106,9 +106,9 @@ __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ 
     // AR rows per warp at a time: each Phi element read from smem serves AR rows
     for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * AR; r0 < n; r0 += (int64_t)gridDim.x * 8 * AR) {
         const int nr = (int)(n - r0 < AR ? n - r0 : AR);
-        double (*ub)[128] = rowbuf[w];
+        double *ubw = rowbuf_all + (size_t)w * AR * k;
         for (int r = 0; r < AR; ++r)
-            for (int l = lane; l < k; l += 32) ub[r][l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
+            for (int l = lane; l < k; l += 32) ubw[r * k + l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
         __syncwarp();
         double best[AR];
         int arg[AR];
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ 
             for (int a = 0; a < k; ++a) {
                 const double ph = phs[a * k + l];
 #pragma unroll
-                for (int r = 0; r < AR; ++r) sc[r] = __dadd_rn(sc[r], __dmul_rn(ub[r][a], ph));
+                for (int r = 0; r < AR; ++r) sc[r] = __dadd_rn(sc[r], __dmul_rn(ubw[r * k + a], ph));
             }
 #pragma unroll
             for (int r = 0; r < AR; ++r)
@@ -406,7 +406,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     TPO_LAUNCH_CHECK();
     eye_kernel<<<cdiv(k * k, 256), 256, 0, st>>>(Phi, k);
     TPO_LAUNCH_CHECK();
-    const size_t phi_smem = sizeof(double) * k * k;
+    const size_t phi_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * AR * k);
     const int sum_nw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / ((int64_t)k * (32 * 8 + 4))));
     const size_t sum_smem = (size_t)sum_nw * k * (32 * sizeof(double) + sizeof(int));
     TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));

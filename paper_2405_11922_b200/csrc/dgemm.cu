@@ -23,7 +23,7 @@ constexpr int BM = 64, BN = 64, BK = 16, NTH = 256;
 
 // BNT = 64 (4 x 4 register tile per thread) or 32 (2 x 4, for skinny right-hand sides).
 // The next K slab is prefetched into registers while the current one is multiplied.
-template <bool TA, int BNT>
+template <bool TA, int BNT, int BK = 16>
 __global__ void __launch_bounds__(NTH) dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
                                                     const double *__restrict__ A, int64_t lda,
                                                     const double *__restrict__ B, int64_t ldb, double beta,
@@ -114,6 +114,60 @@ __global__ void splitk_reduce_kernel(const double *__restrict__ part, int64_t S,
     const int64_t r = i / N, c = i - r * N;
     const double v = alpha * s;
     C[r * ldc + c] = beta == 0.0 ? v : fma(beta, C[r * ldc + c], v);
+}
+
+// Tall-skinny transposed product C = alpha A^T B + beta C for M, N <= 64 and large K (the
+// k x k Grams of the solver): a block per fixed K range stages 32-row slabs of A and B in
+// shared memory and each thread accumulates (m, n) pairs; the block partials are summed in
+// block order by splitk_reduce_kernel (deterministic).
+constexpr int TS_ROWS = 32, TS_MAX = 64;
+__global__ void __launch_bounds__(256) tsgram_kernel(int64_t M, int64_t N, int64_t K, const double *__restrict__ A,
+                                                     int64_t lda, const double *__restrict__ B, int64_t ldb,
+                                                     int64_t rows_per, double *__restrict__ part) {
+    __shared__ double As[TS_ROWS][TS_MAX + 1];
+    __shared__ double Bs[TS_ROWS][TS_MAX + 1];
+    const int t = threadIdx.x;
+    const int64_t r0 = blockIdx.x * rows_per, r1 = min(K, r0 + rows_per);
+    const int pairs = (int)(M * N);
+    constexpr int NQ = (TS_MAX * TS_MAX) / 256;
+    double acc[NQ];
+    int mq[NQ], cq[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        acc[q] = 0.0;
+        const int pidx = min(t + 256 * q, pairs - 1);      // clamped: out-of-range pairs are not stored
+        mq[q] = pidx / (int)N;
+        cq[q] = pidx - mq[q] * (int)N;
+    }
+    const int nq = (pairs - t + 255) / 256;                 // pairs this thread owns
+    for (int64_t rb = r0; rb < r1; rb += TS_ROWS) {
+        const int rows = (int)min((int64_t)TS_ROWS, r1 - rb);
+        __syncthreads();
+        for (int e = t; e < TS_ROWS * M; e += 256) {
+            const int r = e / (int)M, m = e - r * (int)M;
+            As[r][m] = r < rows ? A[(rb + r) * lda + m] : 0.0;
+        }
+        for (int e = t; e < TS_ROWS * N; e += 256) {
+            const int r = e / (int)N, c = e - r * (int)N;
+            Bs[r][c] = r < rows ? B[(rb + r) * ldb + c] : 0.0;
+        }
+        __syncthreads();
+        if (nq >= NQ) {
+            for (int r = 0; r < TS_ROWS; ++r)
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) acc[q] = fma(As[r][mq[q]], Bs[r][cq[q]], acc[q]);
+        } else {
+            for (int r = 0; r < TS_ROWS; ++r)
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    if (q < nq) acc[q] = fma(As[r][mq[q]], Bs[r][cq[q]], acc[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < (TS_MAX * TS_MAX) / 256; ++q) {
+        const int pidx = t + 256 * q;
+        if (pidx < pairs) part[blockIdx.x * (int64_t)pairs + pidx] = acc[q];
+    }
 }
 
 int64_t splits_for(int64_t M, int64_t N, int64_t K) {
@@ -260,6 +314,19 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
         TPO_LAUNCH_CHECK();
         return;
     }
+    if (transA && M <= TS_MAX && N <= TS_MAX && K >= 2048) {
+        const int64_t G = std::max<int64_t>(1, std::min<int64_t>(2 * 148, cdiv(K, 256)));
+        const int64_t rows_per = cdiv(cdiv(K, G), TS_ROWS) * TS_ROWS;
+        const int64_t Gr = cdiv(K, rows_per);
+        const size_t mark = ar.off;
+        double *part = ar.take<double>(Gr * M * N);
+        tsgram_kernel<<<(unsigned)Gr, 256, 0, st>>>(M, N, K, A, lda, B, ldb, rows_per, part);
+        TPO_LAUNCH_CHECK();
+        splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(part, Gr, M, N, alpha, beta, C, ldc);
+        TPO_LAUNCH_CHECK();
+        ar.off = mark;
+        return;
+    }
     const int64_t S = splits_for(M, N, K);
     const int64_t kchunk = cdiv(cdiv(K, S), BK) * BK;
     const int64_t Sr = cdiv(K, kchunk);
@@ -272,7 +339,7 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
     else if (transA)
         dgemm_kernel<true, 64><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
     else if (skinny)
-        dgemm_kernel<false, 32><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
+        dgemm_kernel<false, 32, 32><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
     else
         dgemm_kernel<false, 64><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
     TPO_LAUNCH_CHECK();

@@ -64,22 +64,36 @@ __global__ void __launch_bounds__(CS_WARPS * 32) colstats_part_kernel(const doub
     }
 }
 
+// warp per column: lanes stride the block partials, fixed shuffle tree for the sums; the
+// argmax keeps the larger magnitude, ties -> smaller row index (order independent)
 __global__ void colstats_final_kernel(const double *__restrict__ ps, const double *__restrict__ pa,
                                       const double *__restrict__ pm, const int64_t *__restrict__ pi, int64_t G, int k,
                                       double *__restrict__ out_sum, double *__restrict__ out_abs,
                                       int64_t *__restrict__ out_arg) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (c >= k) return;
     double s = 0.0, a = 0.0, best = -1.0;
-    int64_t bi = 0;
-    for (int64_t g = 0; g < G; ++g) {
+    int64_t bi = INT64_MAX;
+    for (int64_t g = lane; g < G; g += 32) {
         s += ps[g * k + c];
         a += pa[g * k + c];
-        if (pm[g * k + c] > best) { best = pm[g * k + c]; bi = pi[g * k + c]; }
+        const double m = pm[g * k + c];
+        const int64_t i = pi[g * k + c];
+        if (m > best || (m == best && i < bi)) { best = m; bi = i; }
     }
-    out_sum[c] = s;
-    out_abs[c] = a;
-    out_arg[c] = bi;
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        const double om = __shfl_xor_sync(0xffffffffu, best, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (om > best || (om == best && oi < bi)) { best = om; bi = oi; }
+    }
+    if (lane == 0) {
+        out_sum[c] = s;
+        out_abs[c] = a;
+        out_arg[c] = bi;
+    }
 }
 
 __global__ void flip_cols_f64(double *__restrict__ A, int64_t n, int k, const int *__restrict__ sgn) {
@@ -398,7 +412,7 @@ void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Are
     int64_t *arg = ar.take<int64_t>(k);
     colstats_part_kernel<<<G, CS_WARPS * 32, 0, st>>>(Gamma, n, k, rows_per, ps, pa, pm, pi);
     TPO_LAUNCH_CHECK();
-    colstats_final_kernel<<<cdiv(k, 128), 128, 0, st>>>(ps, pa, pm, pi, G, k, s, a, arg);
+    colstats_final_kernel<<<cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ps, pa, pm, pi, G, k, s, a, arg);
     TPO_LAUNCH_CHECK();
     std::vector<double> hs = to_host(s, k, st), ha = to_host(a, k, st);
     std::vector<int64_t> harg = to_host(arg, k, st);

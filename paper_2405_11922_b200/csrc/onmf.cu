@@ -19,18 +19,19 @@
 namespace tpo {
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 256;                     // onmf_rh block
+constexpr int NTR = 128;                    // onmf_rtu block: 128 threads x CPT columns
 constexpr int RT = 64;                      // rows of dinv.Ups staged per tile (onmf_rtu)
 
 template <int CPT, int KC>
-__global__ void __launch_bounds__(NT, 2) onmf_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
+__global__ void __launch_bounds__(NTR, 4) onmf_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
                                                       const float *__restrict__ dinv,
                                                       const double *__restrict__ U, int k, int64_t rows_per,
                                                       double *__restrict__ part) {
     __shared__ double Ys[RT][KC];
     const int t = threadIdx.x;
     const int64_t g = blockIdx.x;
-    const int a0 = blockIdx.y * (NT * CPT);
+    const int a0 = blockIdx.y * (NTR * CPT);
     const int k0 = blockIdx.z * KC;
     const int kc = min(KC, k - k0);
     const int64_t r0 = g * rows_per, r1 = min(n, r0 + rows_per);
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(NT, 2) onmf_rtu_kernel(const float *__restrict
     bool cv[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-        col[c] = a0 + t + NT * c;
+        col[c] = a0 + t + NTR * c;
         cv[c] = col[c] < D;
     }
     double acc[CPT][KC];
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(NT, 2) onmf_rtu_kernel(const float *__restrict
     for (int64_t tb = r0; tb < r1; tb += RT) {
         const int rows = (int)min((int64_t)RT, r1 - tb);
         __syncthreads();
-        for (int e = t; e < RT * KC; e += NT) {
+        for (int e = t; e < RT * KC; e += NTR) {
             const int r = e / KC, l = e - r * KC;
             double v = 0.0;
             if (r < rows && l < kc) v = (double)dinv[tb + r] * U[(tb + r) * k + k0 + l];
@@ -182,14 +183,14 @@ RtuPlan rtu_plan(int64_t n, int D, int k) {
     // owns >= 2 columns of R' whenever D allows (CPT x KC <= 64 accumulators: 2 CTAs / SM)
     p.nkc = (k + 25) / 26;
     p.kc = pick_kc((k + p.nkc - 1) / p.nkc);
-    const int want = (D + NT - 1) / NT;                 // columns per thread to cover D in one block
+    const int want = (D + NTR - 1) / NTR;               // columns per thread to cover D in one block
     const int cap = std::max(1, std::min(8, 64 / p.kc));
     int cpt = 1;
     while (cpt < want && cpt * 2 <= cap) cpt *= 2;
     p.cpt = cpt;
-    p.ncb = (D + NT * cpt - 1) / (NT * cpt);
+    p.ncb = (D + NTR * cpt - 1) / (NTR * cpt);
     const int64_t tiles = (int64_t)p.ncb * p.nkc;
-    const int64_t want_g = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);   // one wave at 2 CTAs / SM
+    const int64_t want_g = std::max<int64_t>(1, (4 * 148 + tiles - 1) / tiles);   // one wave at 4 CTAs / SM
     p.G = std::max<int64_t>(1, std::min<int64_t>(want_g, (std::max<int64_t>(n, 1) + RT - 1) / RT));
     p.rows_per = cdiv(cdiv(std::max<int64_t>(n, 1), p.G), 4) * 4;
     p.G = cdiv(std::max<int64_t>(n, 1), p.rows_per);
@@ -203,10 +204,10 @@ void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float
     // only CPT x KC <= 64 (or CPT = 1) is planned (rtu_plan); the other combinations are not instantiated
     constexpr int C8 = 8 * KC <= 64 ? 8 : 1, C4 = 4 * KC <= 64 ? 4 : 1, C2 = 2 * KC <= 64 ? 2 : 1;
     switch (p.cpt) {
-        case 1: onmf_rtu_kernel<1, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
-        case 2: onmf_rtu_kernel<C2, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
-        case 4: onmf_rtu_kernel<C4, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
-        default: onmf_rtu_kernel<C8, KC><<<grid, NT, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        case 1: onmf_rtu_kernel<1, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        case 2: onmf_rtu_kernel<C2, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        case 4: onmf_rtu_kernel<C4, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        default: onmf_rtu_kernel<C8, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
     }
     TPO_LAUNCH_CHECK();
 }
