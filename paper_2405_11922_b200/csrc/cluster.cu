@@ -23,6 +23,15 @@ namespace {
 
 constexpr double EPS = 1e-12;   // R9
 
+// u[l] for a runtime l from a register array (an unrolled select keeps u in registers)
+template <int KM>
+__device__ __forceinline__ double u_at(const double (&u)[KM], int l) {
+    double v = 0.0;
+#pragma unroll
+    for (int a = 0; a < KM; ++a) v = a == l ? u[a] : v;
+    return v;
+}
+
 __global__ void init_factors_kernel(const float *__restrict__ Gamma, int64_t n, const float *__restrict__ Psi,
                                     const double *__restrict__ sig, int64_t D, int k, double *__restrict__ U,
                                     double *__restrict__ H) {
@@ -52,36 +61,77 @@ __global__ void h_update_kernel(const double *__restrict__ H, const double *__re
 
 // Ups[i,l] *= sqrt(max(RH[i,l],0) / (max((Ups M)[i,l],0) + eps)); warp per row, the old row
 // and M (k x k) staged in shared memory (k <= 128).
+constexpr int UR = 8;     // rows per warp per pass (ups_update_kernel)
+
 __global__ void __launch_bounds__(256) ups_update_kernel(double *__restrict__ U, const double *__restrict__ RH,
                                                          const double *__restrict__ M, int64_t n, int k) {
-    extern __shared__ double msh[];                  // [k * k]
-    __shared__ __align__(16) double rowbuf[8][4][128];
+    extern __shared__ __align__(16) double msh[];    // [k * k] then rowbuf [8][UR][k]
+    double *rowbuf_all = msh + k * k;
     for (int i = threadIdx.x; i < k * k; i += blockDim.x) msh[i] = M[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * 4; r0 < n; r0 += (int64_t)gridDim.x * 8 * 4) {
-        const int nr = (int)(n - r0 < 4 ? n - r0 : 4);
-        double (*ub)[128] = rowbuf[w];
-        for (int r = 0; r < 4; ++r)
-            for (int l = lane; l < k; l += 32) ub[r][l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * UR; r0 < n; r0 += (int64_t)gridDim.x * 8 * UR) {
+        const int nr = (int)(n - r0 < UR ? n - r0 : UR);
+        double *ubw = rowbuf_all + (size_t)w * UR * k;
+        for (int r = 0; r < UR; ++r)
+            for (int l = lane; l < k; l += 32) ubw[r * k + l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
         __syncwarp();
         for (int l = lane; l < k; l += 32) {
-            double sv[4] = {0.0, 0.0, 0.0, 0.0};
+            double sv[UR];
+#pragma unroll
+            for (int r = 0; r < UR; ++r) sv[r] = 0.0;
             for (int a = 0; a < k; ++a) {
                 const double m = msh[a * k + l];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) sv[r] = __dadd_rn(sv[r], __dmul_rn(ub[r][a], m));
+                for (int r = 0; r < UR; ++r) sv[r] = __dadd_rn(sv[r], __dmul_rn(ubw[r * k + a], m));
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < UR; ++r) {
                 if (r >= nr) continue;
                 const double rv = RH[(r0 + r) * k + l];
                 const double num = rv > 0.0 ? rv : 0.0;
                 const double den = __dadd_rn(sv[r] > 0.0 ? sv[r] : 0.0, EPS);
-                U[(r0 + r) * k + l] = __dmul_rn(ub[r][l], sqrt(num / den));
+                U[(r0 + r) * k + l] = __dmul_rn(ubw[r * k + l], sqrt(num / den));
             }
         }
         __syncwarp();
+    }
+}
+
+// The same update, thread per row with the old row in registers (k <= KM <= 64) and M read
+// as shared-memory broadcasts; per (row, l) the same operation order as ups_update_kernel.
+template <int KM>
+__global__ void __launch_bounds__(256) ups_update_reg_kernel(double *__restrict__ U, const double *__restrict__ RH,
+                                                             const double *__restrict__ M, int64_t n, int k) {
+    __shared__ double msh[KM * KM];
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) msh[i] = M[i];
+    __syncthreads();
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    double u[KM];
+#pragma unroll
+    for (int a = 0; a < KM; ++a) u[a] = a < k ? U[row * k + a] : 0.0;
+    int l = 0;
+    for (; l + 1 < k; l += 2) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < KM; ++a)
+            if (a < k) {
+                s0 = __dadd_rn(s0, __dmul_rn(u[a], msh[a * k + l]));
+                s1 = __dadd_rn(s1, __dmul_rn(u[a], msh[a * k + l + 1]));
+            }
+        const double r0 = RH[row * k + l], r1 = RH[row * k + l + 1];
+        U[row * k + l] = __dmul_rn(u_at(u, l), sqrt((r0 > 0.0 ? r0 : 0.0) / __dadd_rn(s0 > 0.0 ? s0 : 0.0, EPS)));
+        U[row * k + l + 1] =
+            __dmul_rn(u_at(u, l + 1), sqrt((r1 > 0.0 ? r1 : 0.0) / __dadd_rn(s1 > 0.0 ? s1 : 0.0, EPS)));
+    }
+    for (; l < k; ++l) {
+        double s0 = 0.0;
+#pragma unroll
+        for (int a = 0; a < KM; ++a)
+            if (a < k) s0 = __dadd_rn(s0, __dmul_rn(u[a], msh[a * k + l]));
+        const double r0 = RH[row * k + l];
+        U[row * k + l] = __dmul_rn(u_at(u, l), sqrt((r0 > 0.0 ? r0 : 0.0) / __dadd_rn(s0 > 0.0 ? s0 : 0.0, EPS)));
     }
 }
 
@@ -164,7 +214,19 @@ __global__ void __launch_bounds__(256) assign_small_kernel(const double *__restr
     for (int a = 0; a < KM; ++a) u[a] = a < k ? U[row * k + a] : 0.0;
     double best = 0.0;
     int arg = 0;
-    for (int l = 0; l < k; ++l) {
+    int l = 0;
+    for (; l + 1 < k; l += 2) {                 // two scores at once (independent chains)
+        double sc0 = 0.0, sc1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < KM; ++a)
+            if (a < k) {
+                sc0 = __dadd_rn(sc0, __dmul_rn(u[a], phs[a * k + l]));
+                sc1 = __dadd_rn(sc1, __dmul_rn(u[a], phs[a * k + l + 1]));
+            }
+        if (l == 0 || sc0 > best) { best = sc0; arg = l; }
+        if (sc1 > best) { best = sc1; arg = l + 1; }
+    }
+    for (; l < k; ++l) {
         double sc = 0.0;
 #pragma unroll
         for (int a = 0; a < KM; ++a)
@@ -382,8 +444,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const int64_t mx = std::max(n, D) * k;
     init_factors_kernel<<<cdiv(mx, 256), 256, 0, st>>>(Gamma, n, Psi, sig, D, k, U, H);
     TPO_LAUNCH_CHECK();
-    const size_t ups_smem = sizeof(double) * k * k;
-    // static rowbuf (32 KB) + dynamic M: opt in whenever the total passes the 48 KB default
+    const size_t ups_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * UR * k);
     TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
     for (int t = 0; t < Tf; ++t) {
         onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
@@ -396,7 +457,15 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
         dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;
-        ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 32), 148 * 8), 256, ups_smem, st>>>(U, RH, M, n, k);
+        if (k <= 16)
+            ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
+        else if (k <= 32)
+            ups_update_reg_kernel<32><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
+        else if (k <= 64)
+            ups_update_reg_kernel<64><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
+        else
+            ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * UR), 148 * 8), 256, ups_smem, st>>>(U, RH, M,
+                                                                                                          n, k);
         TPO_LAUNCH_CHECK();
     }
     // Alg. 3
@@ -429,6 +498,10 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         }
         if (k <= 16)
             assign_small_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+        else if (k <= 32)
+            assign_small_kernel<32><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+        else if (k <= 64)
+            assign_small_kernel<64><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
         else
             assign_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * AR), 148 * 8), 256, phi_smem, st>>>(U, Phi, n, k,
                                                                                                   labels, s);

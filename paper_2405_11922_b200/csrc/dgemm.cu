@@ -109,65 +109,45 @@ __global__ void splitk_reduce_kernel(const double *__restrict__ part, int64_t S,
                                      double beta, double *__restrict__ C, int64_t ldc) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= M * N) return;
-    double s = 0.0;
-    for (int64_t z = 0; z < S; ++z) s += part[z * M * N + i];
+    // 8 independent partial sums (split z mod 8) combined in a fixed order: deterministic and
+    // 8 loads in flight
+    double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t z = 0;
+    for (; z + 8 <= S; z += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s8[j] += part[(z + j) * M * N + i];
+    for (; z < S; ++z) s8[z & 7] += part[z * M * N + i];
+    const double s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
     const int64_t r = i / N, c = i - r * N;
     const double v = alpha * s;
     C[r * ldc + c] = beta == 0.0 ? v : fma(beta, C[r * ldc + c], v);
 }
 
-// Tall-skinny transposed product C = alpha A^T B + beta C for M, N <= 64 and large K (the
-// k x k Grams of the solver): a block per fixed K range stages 32-row slabs of A and B in
-// shared memory and each thread accumulates (m, n) pairs; the block partials are summed in
-// block order by splitk_reduce_kernel (deterministic).
-constexpr int TS_ROWS = 32, TS_MAX = 64;
-__global__ void __launch_bounds__(256) tsgram_kernel(int64_t M, int64_t N, int64_t K, const double *__restrict__ A,
-                                                     int64_t lda, const double *__restrict__ B, int64_t ldb,
-                                                     int64_t rows_per, double *__restrict__ part) {
-    __shared__ double As[TS_ROWS][TS_MAX + 1];
-    __shared__ double Bs[TS_ROWS][TS_MAX + 1];
-    const int t = threadIdx.x;
-    const int64_t r0 = blockIdx.x * rows_per, r1 = min(K, r0 + rows_per);
-    const int pairs = (int)(M * N);
-    constexpr int NQ = (TS_MAX * TS_MAX) / 256;
-    double acc[NQ];
-    int mq[NQ], cq[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        acc[q] = 0.0;
-        const int pidx = min(t + 256 * q, pairs - 1);      // clamped: out-of-range pairs are not stored
-        mq[q] = pidx / (int)N;
-        cq[q] = pidx - mq[q] * (int)N;
+// The same sum, one warp per output (lanes stride the splits, fixed shuffle tree): for few
+// outputs and many splits.
+__global__ void splitk_reduce_warp_kernel(const double *__restrict__ part, int64_t S, int64_t M, int64_t N,
+                                          double alpha, double beta, double *__restrict__ C, int64_t ldc) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= M * N) return;
+    double s = 0.0;
+    for (int64_t z = lane; z < S; z += 32) s += part[z * M * N + i];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        const int64_t r = i / N, c = i - r * N;
+        const double v = alpha * s;
+        C[r * ldc + c] = beta == 0.0 ? v : fma(beta, C[r * ldc + c], v);
     }
-    const int nq = (pairs - t + 255) / 256;                 // pairs this thread owns
-    for (int64_t rb = r0; rb < r1; rb += TS_ROWS) {
-        const int rows = (int)min((int64_t)TS_ROWS, r1 - rb);
-        __syncthreads();
-        for (int e = t; e < TS_ROWS * M; e += 256) {
-            const int r = e / (int)M, m = e - r * (int)M;
-            As[r][m] = r < rows ? A[(rb + r) * lda + m] : 0.0;
-        }
-        for (int e = t; e < TS_ROWS * N; e += 256) {
-            const int r = e / (int)N, c = e - r * (int)N;
-            Bs[r][c] = r < rows ? B[(rb + r) * ldb + c] : 0.0;
-        }
-        __syncthreads();
-        if (nq >= NQ) {
-            for (int r = 0; r < TS_ROWS; ++r)
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) acc[q] = fma(As[r][mq[q]], Bs[r][cq[q]], acc[q]);
-        } else {
-            for (int r = 0; r < TS_ROWS; ++r)
-#pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    if (q < nq) acc[q] = fma(As[r][mq[q]], Bs[r][cq[q]], acc[q]);
-        }
+}
+
+void splitk_reduce(const double *part, int64_t S, int64_t M, int64_t N, double alpha, double beta, double *C,
+                   int64_t ldc, cudaStream_t st) {
+    if (S >= 64 && M * N <= 16384) {
+        splitk_reduce_warp_kernel<<<cdiv(M * N * 32, 256), 256, 0, st>>>(part, S, M, N, alpha, beta, C, ldc);
+    } else {
+        splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(part, S, M, N, alpha, beta, C, ldc);
     }
-#pragma unroll
-    for (int q = 0; q < (TS_MAX * TS_MAX) / 256; ++q) {
-        const int pidx = t + 256 * q;
-        if (pidx < pairs) part[blockIdx.x * (int64_t)pairs + pidx] = acc[q];
-    }
+    TPO_LAUNCH_CHECK();
 }
 
 int64_t splits_for(int64_t M, int64_t N, int64_t K) {
@@ -198,6 +178,7 @@ __device__ __forceinline__ double fast_rcp(double d) {
     return r;
 }
 
+template <int PER>      // columns of a row a thread owns: ceil(b / TPR) <= PER
 __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__restrict__ g, int b,
                                                                 double *__restrict__ Ci, int *__restrict__ flag) {
     extern __shared__ double sm[];
@@ -223,7 +204,6 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
         pinv[0] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
     }
     __syncthreads();
-    constexpr int PER = (CI_MAX + TPR - 1) / TPR;   // columns a thread owns in one row
     for (int j = 0; j < b - 1; ++j) {
         if (my_r > j && my_r < b) {
             const double f = U[j * p + my_r] * pinv[j];
@@ -314,19 +294,6 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
         TPO_LAUNCH_CHECK();
         return;
     }
-    if (transA && M <= TS_MAX && N <= TS_MAX && K >= 2048) {
-        const int64_t G = std::max<int64_t>(1, std::min<int64_t>(2 * 148, cdiv(K, 256)));
-        const int64_t rows_per = cdiv(cdiv(K, G), TS_ROWS) * TS_ROWS;
-        const int64_t Gr = cdiv(K, rows_per);
-        const size_t mark = ar.off;
-        double *part = ar.take<double>(Gr * M * N);
-        tsgram_kernel<<<(unsigned)Gr, 256, 0, st>>>(M, N, K, A, lda, B, ldb, rows_per, part);
-        TPO_LAUNCH_CHECK();
-        splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(part, Gr, M, N, alpha, beta, C, ldc);
-        TPO_LAUNCH_CHECK();
-        ar.off = mark;
-        return;
-    }
     const int64_t S = splits_for(M, N, K);
     const int64_t kchunk = cdiv(cdiv(K, S), BK) * BK;
     const int64_t Sr = cdiv(K, kchunk);
@@ -343,20 +310,23 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
     else
         dgemm_kernel<false, 64><<<grid, NTH, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, part);
     TPO_LAUNCH_CHECK();
-    if (Sr > 1) {
-        splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(part, Sr, M, N, alpha, beta, C, ldc);
-        TPO_LAUNCH_CHECK();
-    }
+    if (Sr > 1) splitk_reduce(part, Sr, M, N, alpha, beta, C, ldc, st);
     ar.off = mark;
 }
 
 void chol_inv_device(const double *g, int64_t b, double *Ci, int *flag, cudaStream_t st) {
     TPO_REQUIRE(b >= 1 && b <= CI_MAX, "chol_inv: block width out of range");
     const size_t smem = sizeof(double) * (size_t)(2 * b * (b + 1) + 2 * b);
-    if (smem > 48 * 1024)
-        TPO_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int threads = (int)cdiv(b * TPR, 32) * 32;
-    chol_inv_kernel<<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
+    if (b <= 32) {
+        chol_inv_kernel<4><<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
+    } else if (b <= 64) {
+        TPO_CUDA(cudaFuncSetAttribute(chol_inv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        chol_inv_kernel<8><<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
+    } else {
+        TPO_CUDA(cudaFuncSetAttribute(chol_inv_kernel<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        chol_inv_kernel<14><<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
+    }
     TPO_LAUNCH_CHECK();
 }
 

@@ -242,11 +242,11 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 v) {
 
 // One warp gathers the SL float4 columns c4[0..SL) (stride 32) of the CSR rows in edges
 // [beg, end) into acc[].
-template <bool WEIGHTED, int SL>
+template <bool WEIGHTED, int SL, int UE>
 __device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, const int (&c4)[SL],
                                             const bool (&act)[SL], float4 (&acc)[SL]) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = UNR / SL > 0 ? UNR / SL : 1;
+    constexpr int U = UE;
 #pragma unroll
     for (int s = 0; s < SL; ++s) acc[s] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t d4 = a.d4;
@@ -347,11 +347,11 @@ __device__ __forceinline__ void load_x_sl(const SpmmArgs &a, int64_t row, const 
 
 // One warp streams the edges of rows [r0, r1) (all short) for its SL column slices, flushing
 // each row through the epilogue as the stream crosses its end; empty rows are flushed with 0.
-template <int EPI, bool WEIGHTED, int SL>
+template <int EPI, bool WEIGHTED, int SL, int UE>
 __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0, int64_t r1, const int (&c4)[SL],
                                                   const bool (&act)[SL]) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = UNR / SL > 0 ? UNR / SL : 1;
+    constexpr int U = UE;
     const int64_t d4 = a.d4;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t rb = r0; rb < r1; rb += 32) {
@@ -409,7 +409,7 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
 }
 
 // One work unit: item `item` of the schedule for column group `grp`.
-template <int EPI, bool WEIGHTED, int SL>
+template <int EPI, bool WEIGHTED, int SL, int UE>
 __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, int grp, int64_t item, int64_t n_items) {
     const int lane = threadIdx.x & 31;
     const int4 it = a.sch.items[item];
@@ -422,14 +422,14 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, int grp, int64_t it
     }
     if (it.w == 0) {                                     // row block
         const int64_t r1 = item + 1 < n_items ? (int64_t)a.sch.items[item + 1].x : a.n_rows;
-        process_row_block<EPI, WEIGHTED, SL>(a, it.x, r1, c4, act);
+        process_row_block<EPI, WEIGHTED, SL, UE>(a, it.x, r1, c4, act);
         return;
     }
     const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];   // chunk of a long row
     const int64_t beg = rb + (int64_t)it.y * CHUNK;
     const int64_t end = min(re, beg + CHUNK);
     float4 acc[SL];
-    gather_rows<WEIGHTED, SL>(a, beg, end, c4, act, acc);
+    gather_rows<WEIGHTED, SL, UE>(a, beg, end, c4, act, acc);
 #pragma unroll
     for (int q = 0; q < SL; ++q)
         if (act[q]) a.partials[(int64_t)it.z * a.d4 + c4[q]] = acc[q];
@@ -441,7 +441,7 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, int grp, int64_t it
 // working set stays L2-resident) -- and no block holds its slot while one slow warp finishes.
 // Which warp runs a unit does not change its result (each unit is computed by one warp in a
 // fixed order), so results stay deterministic.
-template <int EPI, bool WEIGHTED, int SL, int MINB>
+template <int EPI, bool WEIGHTED, int SL, int MINB, int UE = (UNR / SL > 0 ? UNR / SL : 1)>
 __global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
     unsigned smid;
     asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
         u = __shfl_sync(0xffffffffu, u, 0);
         if ((int64_t)u >= units) return;
         const int grp = (int)((int64_t)u / n_items);
-        spmm_unit<EPI, WEIGHTED, SL>(a, grp, (int64_t)u - (int64_t)grp * n_items, n_items);
+        spmm_unit<EPI, WEIGHTED, SL, UE>(a, grp, (int64_t)u - (int64_t)grp * n_items, n_items);
     }
 }
 
@@ -716,7 +716,14 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
 int spmm_variant(int nslices) {
     int v = nslices >= 2 ? 23 : 14;      // measured best on small (d = 1000) and medium (d = 256)
     if (const char *e = getenv("TPO_SPMM_VARIANT")) v = atoi(e);
-    if (v < 1000 && v != 13 && v != 14 && v != 22 && v != 23 && v != 42 && v != 82) v = 14;
+    if (v < 1000 && v != 13 && v != 14 && v != 22 && v != 23 && v != 42 && v != 82 && v != 24 && v != 148 &&
+        v != 228 && v != 238 && v != 138)
+        v = 14;
+    if (v >= 100 && v < 1000) {          // SL * 100 + MINB * 10 + edges-in-flight code (8 -> 8 edges)
+        const int sl = v / 100;
+        if (sl > nslices) v = 14;
+        return v;
+    }
     if (v >= 1000) {                     // cp.async ring variants: 1000 + SL * 100 + RING
         int sl = (v - 1000) / 100, ring = v % 100;
         if (sl != 1 && sl != 2 && sl != 4) sl = 1;
@@ -733,7 +740,7 @@ int spmm_variant(int nslices) {
 
 template <int EPI, bool W>
 void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
-    const int sl = var >= 1000 ? (var - 1000) / 100 : var / 10;
+    const int sl = var >= 1000 ? (var - 1000) / 100 : (var >= 100 ? var / 100 : var / 10);
     a.ngroups = (a.nslices + sl - 1) / sl;
     const int64_t blocks = cdiv(max_items * a.ngroups, WPB);
     if (var >= 1000) {
@@ -760,7 +767,7 @@ void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
         return;
     }
     // persistent warps: at most the resident capacity (SMs x MINB blocks of WPB warps)
-    const int minb = var % 10;
+    const int minb = var >= 100 ? (var / 10) % 10 : var % 10;
     const int nsm = sm_count();
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)nsm * minb));
     // the reserve applies only to a full-capacity grid (blocks on every SM, so the blocks of the
@@ -772,6 +779,11 @@ void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
         case 22: spmm_kernel<EPI, W, 2, 2><<<grid, WPB * 32, 0, st>>>(a); break;
         case 42: spmm_kernel<EPI, W, 4, 2><<<grid, WPB * 32, 0, st>>>(a); break;
         case 82: spmm_kernel<EPI, W, 8, 2><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 24: spmm_kernel<EPI, W, 2, 4><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 148: spmm_kernel<EPI, W, 1, 4, 8><<<grid, WPB * 32, 0, st>>>(a); break;       // = 14
+        case 138: spmm_kernel<EPI, W, 1, 3, 12><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 228: spmm_kernel<EPI, W, 2, 2, 8><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 238: spmm_kernel<EPI, W, 2, 3, 6><<<grid, WPB * 32, 0, st>>>(a); break;
         default: spmm_kernel<EPI, W, 1, 4><<<grid, WPB * 32, 0, st>>>(a); break;
     }
     TPO_LAUNCH_CHECK();
