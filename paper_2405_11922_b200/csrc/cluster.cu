@@ -459,10 +459,6 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         ar.off = mark;
         if (k <= 16)
             ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
-        else if (k <= 32)
-            ups_update_reg_kernel<32><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
-        else if (k <= 64)
-            ups_update_reg_kernel<64><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
         else
             ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * UR), 148 * 8), 256, ups_smem, st>>>(U, RH, M,
                                                                                                           n, k);

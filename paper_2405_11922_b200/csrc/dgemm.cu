@@ -277,6 +277,169 @@ __global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Blocked chol_inv (one CTA of 256 threads, 16 x 16 blocks, b <= CI_MAX): the same factor and
+// inverse as chol_inv_kernel with O(b / 16) block barriers instead of O(b) steps.
+//   Cholesky (upper, S g S = U^T U), per block column J = [j0, je):
+//     (1) warp 0 factors the diagonal block (warp-synchronous right-looking steps),
+//     (2) panel: U[J, c] <- U_JJ^{-T} U[J, c] for c >= je (thread per column, forward subst.),
+//     (3) trailing: U[r][c] -= sum_{i in J} U[i][r] U[i][c] for je <= r <= c.
+//   Inverse X = U^{-1}: warp w inverts diagonal block w (column per lane, back substitution),
+//     then block rows I from the bottom: T[i][c] = sum_{l=ie}^{c} U[i][l] X[l][c] (c >= ie),
+//     X[i][c] = -sum_{l=i}^{ie-1} X_II[i][l] T[l][c].
+// ---------------------------------------------------------------------------------------
+constexpr int CB = 16;
+
+__global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double *__restrict__ g, int b,
+                                                           double *__restrict__ Ci, int *__restrict__ flag) {
+    extern __shared__ double sm[];
+    const int p = b + 1, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    double *U = sm;                      // b x b (pitch p)
+    double *X = sm + b * p;              // b x b (pitch p): inverse, then T scratch rows
+    double *sc = X + b * p;              // b
+    double *T = sc + b;                  // CB x b scratch
+    double *rd = T + CB * b;             // b: 1 / U[i][i] (no fp64 divisions on the dependency chains)
+    __shared__ int bad;
+    if (t == 0) bad = 0;
+    for (int i = t; i < b; i += 256) {
+        const double d = g[(int64_t)i * b + i];
+        sc[i] = (d > 0.0 && isfinite(d)) ? rsqrt(d) : 0.0;
+    }
+    __syncthreads();
+    for (int i = t; i < b * b; i += 256) {
+        const int r = i / b, c = i - r * b;
+        U[r * p + c] = c >= r ? g[i] * sc[r] * sc[c] : 0.0;
+        X[r * p + c] = 0.0;
+    }
+    __syncthreads();
+    const int nb = (b + CB - 1) / CB;
+    for (int J = 0; J < nb; ++J) {
+        const int j0 = J * CB, je = min(b, j0 + CB);
+        if (w == 0) {                                    // (1) diagonal block, warp-synchronous
+            for (int j = j0; j < je; ++j) {
+                double d = U[j * p + j];
+                const bool ok = d > 0.0 && isfinite(d);
+                if (!ok) d = 1.0;
+                double inv = rsqrt(d);
+                inv = inv * fma(-0.5 * d * inv, inv, 1.5);      // one Newton step: full fp64 accuracy
+                const double piv = d * inv;
+                __syncwarp();
+                if (lane == 0) {
+                    if (!ok) bad = 1;
+                    U[j * p + j] = piv;
+                    rd[j] = inv;
+                }
+                const int c1 = j + 1 + lane;
+                if (c1 < je) U[j * p + c1] *= inv;
+                __syncwarp();
+                // trailing pairs (r, c), j < r <= c < je: lane owns column j+1+(lane&15) and every
+                // other row from j+1+(lane>>4); all loads are issued before the stores
+                const int cc = j + 1 + (lane & 15), rp = lane >> 4;
+                if (cc < je) {
+                    const double ujc = U[j * p + cc];
+                    double uj[CB / 2], ur[CB / 2];
+#pragma unroll
+                    for (int m = 0; m < CB / 2; ++m) {
+                        const int r = j + 1 + rp + 2 * m;
+                        const bool v = r <= cc;
+                        uj[m] = v ? U[j * p + r] : 0.0;
+                        ur[m] = v ? U[r * p + cc] : 0.0;
+                    }
+#pragma unroll
+                    for (int m = 0; m < CB / 2; ++m) {
+                        const int r = j + 1 + rp + 2 * m;
+                        if (r <= cc) U[r * p + cc] = ur[m] - uj[m] * ujc;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        for (int c = je + t; c < b; c += 256) {         // (2) panel: forward substitution per column
+            double x[CB];
+#pragma unroll
+            for (int ii = 0; ii < CB; ++ii) x[ii] = j0 + ii < je ? U[(j0 + ii) * p + c] : 0.0;
+#pragma unroll
+            for (int ii = 0; ii < CB; ++ii) {
+                const int i = j0 + ii;
+                if (i >= je) break;
+                double v = x[ii];
+#pragma unroll
+                for (int ll = 0; ll < ii; ++ll) v -= U[(j0 + ll) * p + i] * x[ll];
+                x[ii] = v * rd[i];
+            }
+#pragma unroll
+            for (int ii = 0; ii < CB; ++ii)
+                if (j0 + ii < je) U[(j0 + ii) * p + c] = x[ii];
+        }
+        __syncthreads();
+        const int w2 = b - je;                            // (3) trailing update, 16 threads per row
+        for (int rr = t / 16; rr < w2; rr += 16) {
+            const int r = je + rr;
+            for (int c = r + (t & 15); c < b; c += 16) {
+                double v = U[r * p + c];
+                for (int i = j0; i < je; ++i) v -= U[i * p + r] * U[i * p + c];
+                U[r * p + c] = v;
+            }
+        }
+        __syncthreads();
+    }
+    // inverse of the diagonal blocks: warp w handles blocks w, w + 8, ...; lane = column,
+    // the column's entries kept in registers while it is solved bottom-up
+    for (int I = w; I < nb; I += 8) {
+        const int i0 = I * CB, ie = min(b, i0 + CB);
+        const int jj = lane, j = i0 + jj;
+        if (lane < CB && j < ie) {
+            double x[CB];
+#pragma unroll
+            for (int ii = 0; ii < CB; ++ii) x[ii] = 0.0;
+#pragma unroll
+            for (int ii = CB - 1; ii >= 0; --ii) {
+                if (ii > jj) continue;
+                const int i = i0 + ii;
+                if (ii == jj) { x[ii] = rd[i]; continue; }
+                double s2 = 0.0;
+#pragma unroll
+                for (int ll = ii + 1; ll < CB; ++ll)
+                    if (ll <= jj) s2 += U[i * p + i0 + ll] * x[ll];
+                x[ii] = -s2 * rd[i];
+            }
+#pragma unroll
+            for (int ii = 0; ii < CB; ++ii)
+                if (ii <= jj) X[(i0 + ii) * p + j] = x[ii];
+        }
+    }
+    __syncthreads();
+    for (int I = nb - 2; I >= 0; --I) {                  // off-diagonal block rows, bottom up
+        const int i0 = I * CB, ie = min(b, i0 + CB), wc = b - ie;
+        for (int e = t; e < CB * wc; e += 256) {          // T[i][c] = sum_{l=ie}^{c} U[i][l] X[l][c]
+            const int ii = e / wc, c = ie + e % wc, i = i0 + ii;
+            double s = 0.0;
+            if (i < ie)
+                for (int l = ie; l <= c; ++l) s += U[i * p + l] * X[l * p + c];
+            T[ii * b + c] = s;
+        }
+        __syncthreads();
+        for (int e = t; e < CB * wc; e += 256) {          // X[i][c] = -sum_{l=i}^{ie-1} X[i][l] T[l][c]
+            const int ii = e / wc, c = ie + e % wc, i = i0 + ii;
+            if (i >= ie) continue;
+            double s = 0.0;
+            for (int l = i; l < ie; ++l) s += X[i * p + l] * T[(l - i0) * b + c];
+            X[i * p + c] = -s;
+        }
+        __syncthreads();
+    }
+    for (int i = t; i < b * b; i += 256) {
+        const int r = i / b, c = i - r * b;
+        Ci[i] = c >= r ? X[r * p + c] * sc[r] : 0.0;
+    }
+    if (t == 0) {
+        bool z = false;
+        for (int i = 0; i < b; ++i) z |= sc[i] == 0.0;
+        if ((bad || z) && flag) *flag = 1;
+    }
+}
+
 }  // namespace
 
 // Bound for every K and every M' <= M, N' <= N: S <= 296 / tiles + 1 and M N <= 4096 tiles,
@@ -316,17 +479,9 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
 
 void chol_inv_device(const double *g, int64_t b, double *Ci, int *flag, cudaStream_t st) {
     TPO_REQUIRE(b >= 1 && b <= CI_MAX, "chol_inv: block width out of range");
-    const size_t smem = sizeof(double) * (size_t)(2 * b * (b + 1) + 2 * b);
-    const int threads = (int)cdiv(b * TPR, 32) * 32;
-    if (b <= 32) {
-        chol_inv_kernel<4><<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
-    } else if (b <= 64) {
-        TPO_CUDA(cudaFuncSetAttribute(chol_inv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        chol_inv_kernel<8><<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
-    } else {
-        TPO_CUDA(cudaFuncSetAttribute(chol_inv_kernel<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        chol_inv_kernel<14><<<1, threads, smem, st>>>(g, (int)b, Ci, flag);
-    }
+    const size_t smem = sizeof(double) * (size_t)(2 * b * (b + 1) + 2 * b + CB * b);
+    TPO_CUDA(cudaFuncSetAttribute(chol_inv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    chol_inv_blk_kernel<<<1, 256, smem, st>>>(g, (int)b, Ci, flag);
     TPO_LAUNCH_CHECK();
 }
 
