@@ -356,25 +356,21 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int nb = (int)(r1 - rb < 32 ? r1 - rb : 32);
-        // edge offsets relative to the batch's first edge fit in 32 bits (a row block spans
-        // about CHUNK edges; short rows only): fewer live 64-bit registers in the hot loop
-        const int64_t e_beg = a.rowptr[rb];
-        const int my_end = lane < nb ? (int)(a.rowptr[rb + 1 + lane] - e_beg) : 0;   // end of row rb + lane
+        const int64_t my_end = lane < nb ? a.rowptr[rb + 1 + lane] : 0;     // end of row rb + lane
         const float my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
-        const int e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
-        const int32_t *colp = a.col + e_beg;
-        const float *valp = WEIGHTED ? a.val + e_beg : nullptr;
+        const int64_t e_beg = a.rowptr[rb];
+        const int64_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
         int cur = 0;
-        int cur_end = __shfl_sync(0xffffffffu, my_end, 0);
+        int64_t cur_end = __shfl_sync(0xffffffffu, my_end, 0);
         float4 xcur[SL], acc[SL];
         load_x_sl<EPI, SL>(a, rb, c4, act, xcur);
 #pragma unroll
         for (int q = 0; q < SL; ++q) acc[q] = zero;
-        for (int e0 = 0; e0 < e_end; e0 += 32) {
-            const int cnt = e_end - e0 < 32 ? e_end - e0 : 32;
-            const int mycol = lane < cnt ? __ldg(colp + e0 + lane) : 0;
+        for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
+            const int cnt = (int)(e_end - e0 < 32 ? e_end - e0 : 32);
+            const int mycol = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
             float myw = 1.f;
-            if (WEIGHTED) myw = lane < cnt ? __ldg(valp + e0 + lane) : 0.f;
+            if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
             for (int j = 0; j < cnt; j += U) {
                 float4 v[U][SL];
 #pragma unroll
@@ -387,7 +383,7 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     if (j + u >= cnt) break;
-                    const int e = e0 + j + u;
+                    const int64_t e = e0 + j + u;
                     while (e >= cur_end) {               // warp-uniform: flush finished rows
                         epilogue_sl<EPI, SL>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
 #pragma unroll
