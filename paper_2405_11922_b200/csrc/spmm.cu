@@ -30,6 +30,9 @@ namespace {
 
 constexpr int CHUNK = 256;           // edges per long-row chunk; also the row-block grouping grain
 constexpr int kCounters = 64;        // persistent-warp work counters zeroed together
+#ifndef TPO_L2_HINTS
+#define TPO_L2_HINTS 1
+#endif
 constexpr int WPB = 8;               // warps per block
 constexpr int UNR = 8;               // neighbour rows in flight per warp
 
@@ -242,6 +245,36 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 v) {
 
 // One warp gathers the SL float4 columns c4[0..SL) (stride 32) of the CSR rows in edges
 // [beg, end) into acc[].
+// L2 residency hints.  The gathered operand is re-read by many edges: loads carry an
+// evict_last cache policy; the outputs (and X) are touched once per hop: streaming stores /
+// loads (evict-first), so they do not push the gathered column group out of L2.
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float4 ld_keep(const float4 *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 gather_ld(const float4 *p) {
+#if TPO_L2_HINTS
+    return ld_keep(p, l2_keep_policy());
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) {
+#if TPO_L2_HINTS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 template <bool WEIGHTED, int SL, int UE>
 __device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, const int (&c4)[SL],
                                             const bool (&act)[SL], float4 (&acc)[SL]) {
@@ -262,7 +295,7 @@ __device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int6
             for (int u = 0; u < U; ++u) {
                 const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, j + u) * d4;
 #pragma unroll
-                for (int s = 0; s < SL; ++s) v[u][s] = act[s] ? __ldg(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int s = 0; s < SL; ++s) v[u][s] = act[s] ? gather_ld(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -276,7 +309,7 @@ __device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int6
             const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, j) : 1.f;
 #pragma unroll
             for (int s = 0; s < SL; ++s) {
-                const float4 v = act[s] ? __ldg(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v = act[s] ? gather_ld(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
                 acc[s] = WEIGHTED ? f4fma(w, v, acc[s]) : f4add(acc[s], v);
             }
         }
@@ -290,12 +323,12 @@ __device__ __forceinline__ void epilogue_v(const SpmmArgs &a, int64_t row, int c
                                            float s) {
     const int64_t o = row * (int64_t)a.d4 + c4;
     if (EPI == EPI_RAW) {
-        if (act) a.out[o] = acc;
+        if (act) st_stream(a.out + o, acc);
         return;
     }
     if (EPI == EPI_V) {
         const float s2 = s * s;
-        if (act) a.out[o] = make_float4(acc.x * s2, acc.y * s2, acc.z * s2, acc.w * s2);
+        if (act) st_stream(a.out + o, make_float4(acc.x * s2, acc.y * s2, acc.z * s2, acc.w * s2));
         return;
     }
     const float g = a.alpha * s;
@@ -305,23 +338,27 @@ __device__ __forceinline__ void epilogue_v(const SpmmArgs &a, int64_t row, int c
     z.z = fmaf(a.c, x.z, g * acc.z);
     z.w = fmaf(a.c, x.w, g * acc.w);
     if (EPI == EPI_U) {
-        if (act) a.out[o] = make_float4(s * z.x, s * z.y, s * z.z, s * z.w);
+        if (act) st_stream(a.out + o, make_float4(s * z.x, s * z.y, s * z.z, s * z.w));
         return;
     }
     // EPI_FINAL
-    if (act) a.out[o] = z;
+    if (act) st_stream(a.out + o, z);
     if (a.out_hat != nullptr) {            // only when nslices == 1: the warp owns the row
         float ss = act ? z.x * z.x + z.y * z.y + z.z * z.z + z.w * z.w : 0.f;
         for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
         const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;
-        if (act) a.out_hat[o] = make_float4(z.x * inv, z.y * inv, z.z * inv, z.w * inv);
+        if (act) st_stream(a.out_hat + o, make_float4(z.x * inv, z.y * inv, z.z * inv, z.w * inv));
     }
 }
 
 template <int EPI>
 __device__ __forceinline__ float4 load_x(const SpmmArgs &a, int64_t row, int c4, bool act) {
     if (EPI == EPI_V || EPI == EPI_RAW || !act) return make_float4(0.f, 0.f, 0.f, 0.f);
+#if TPO_L2_HINTS
+    return __ldcs(a.X + row * (int64_t)a.d4 + c4);
+#else
     return __ldg(a.X + row * (int64_t)a.d4 + c4);
+#endif
 }
 
 template <int EPI>
@@ -378,7 +415,7 @@ __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0,
                     const int jj = j + u < 31 ? j + u : 31;
                     const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, jj) * d4;
 #pragma unroll
-                    for (int q = 0; q < SL; ++q) v[u][q] = (act[q] && j + u < cnt) ? __ldg(a.src + c4[q] + ro) : zero;
+                    for (int q = 0; q < SL; ++q) v[u][q] = (act[q] && j + u < cnt) ? gather_ld(a.src + c4[q] + ro) : zero;
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
