@@ -148,6 +148,71 @@ def cpu_baseline_sample(g):
             "sample": f"oracle_propagate, 1 of T={g.T} hops over the full {g.name} graph ({dt:.1f} s; a5-a9 excluded)"}
 
 
+def run_sharded(args, g, ws, rank, local, dev):
+    """One graph, U rows split over the ranks: sharded propagation (NCCL
+    reduce-scatter / all-gather of the V-side block per hop) and the sharded solver (fp64
+    partials all-reduced); every rank computes the Haar rotation from G (replicated)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2405_11922_b200 as T
+    from paper_2405_11922_b200._lib import lib
+    from paper_2405_11922_b200.sharded import (GpuShardOps, GpuSolverOps, TorchCollectives, propagate_sharded,
+                                               shard_graph, solve_sharded)
+    if ws == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    coll = TorchCollectives()
+    sh = shard_graph(g.n, g.m, g.B_rowptr, g.B_col, rank, ws, g.B_val)
+    ops = GpuShardOps(sh, dev, g.d)
+    sops = GpuSolverOps(sh.n_p, g.d, g.k, dev)
+    Xp = torch.from_numpy(g.X[sh.u0:sh.u1]).to(dev)
+    L = lib()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        Q = T.haar_q_dev(g.G, device=dev)
+        _, Zh = propagate_sharded(ops, coll, Xp, g.alpha, g.T)
+        lab, _ = solve_sharded(sops, coll, Zh, Q, sh.u0, args.tf, args.tg)
+        return lab
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.tpo_launch_count()
+    times = []
+    stream = torch.cuda.current_stream()
+    with ClockSampler(local) as cs:
+        for _ in range(args.steps):
+            flush.zero_()
+            dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = L.tpo_launch_count() - launches0
+    t = torch.tensor([float(sum(times))], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    tot_ms = float(t.item())
+    units = 2.0 * g.nnz * g.d * g.T
+    cfg = config_dict(g, args, ws)
+    cfg["parallelism"] = f"U-rows sharded over {ws} rank(s) (NCCL RS/AG per hop, all-reduced solver partials)"
+    line = {"metric": metric_name(), "value": units * args.steps / (tot_ms / 1e3), "unit": "nnz*d/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic", "config": cfg,
+            "e2e": None, "gpu_launches": int(launches), "clocks": cs.summary(), "mode": "sharded"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -159,6 +224,10 @@ def main():
     ap.add_argument("--tg", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="N > 1: independent replicas (weak scaling, default) or one graph with its U rows "
+                         "sharded across the ranks (strong scaling: NCCL reduce-scatter / all-gather per hop, "
+                         "all-reduced solver partials)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
 
@@ -177,6 +246,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     import paper_2405_11922_b200 as T
     from paper_2405_11922_b200._lib import lib
+
+    if args.mode == "sharded":
+        run_sharded(args, g, ws, rank, local, dev)
+        return
 
     L = lib()
     dg = T.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, device=dev)

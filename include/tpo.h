@@ -217,6 +217,79 @@ int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_
                 size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * a5-a9 sharded across GPUs: the rank owns the contiguous U rows [u0, u1)
+ * (n_p rows) of Zhat / R' / dinv / Gamma / Ups / labels; the CALLER all-reduces (sum) the
+ * marked partials between the calls (NCCL on GPUs via torch.distributed), so the replicated
+ * D x D / D x k / k x k quantities are identical on every rank:
+ *   tpo_shard_features  R'_p = features of Zhat_p (Eqs. R-prime) and
+ *                       r_part = sum_{i in p} R'[i] (2d fp64)                   -> all-reduce r
+ *   tpo_shard_dinv      dinv_p[i] = 1/sqrt(max(R'[i] . r, 1e-12)) (Eq. Ri, 466-468; R6)
+ *   tpo_gram            G_part = R_p^T R_p (D x D fp64)                          -> all-reduce G
+ *   tpo_eig_from_gram   Psi64 (D x k fp64), sigma (host) = the exact top-k of R from the
+ *                       global Gram (Eq. init-HY; R7) [sync]
+ *   tpo_shard_gamma     Gamma64_p = diag(dinv_p) R'_p Psi64 diag(1/sigma) (n_p x k fp64) [sync]
+ *   tpo_shard_atb64     out = A_p^T B_p (k x k fp64; A_p, B_p n_p x k fp64)      -> all-reduce
+ *                       (Gamma^T Gamma for the CholeskyQR polish; Ups^T Ups, Ups^T RH in Alg. 2)
+ *   tpo_shard_apply_chol X_p <- X_p S C^{-1} for the global Gram g = S^-1 C^T C S^-1 [sync]
+ *   tpo_shard_colstats  per-column sum, sum|x|, max|x| and its GLOBAL row index (row0 = u0)
+ *                       of Gamma64_p: sums -> all-reduce; (max, index) -> all-gather, the
+ *                       caller keeps the largest magnitude, ties -> smallest index (R8) [sync]
+ *   tpo_shard_gamma_final flips the columns with signs[l] < 0 (host int32 k) in Gamma64_p and
+ *                       Psi (Psi = fp32 copy of Psi64 when Psi64 != NULL), rounds Gamma_p to
+ *                       fp32 [sync]
+ *   tpo_shard_onmf_init Ups_p = max(Gamma_p,0)+eps, H = max(Psi Sigma,0)+eps (R9) [sync]
+ *   tpo_shard_onmf_rtu  RtU_part = R'_p^T (dinv_p . Ups_p) (D x k fp64)          -> all-reduce
+ *   tpo_onmf_h_update   H <- H . max(RtU,0) / (H UtU + eps) (Eq. update-Q) [sync]
+ *   tpo_shard_onmf_rh   RH_p = dinv_p . (R'_p H) (n_p x k fp64)
+ *   tpo_shard_onmf_u_update Ups_p <- Ups_p . sqrt(max(RH_p,0) / (max(Ups_p M,0) + eps))
+ *                       (Eq. update-Y; M = all-reduced Ups^T RH)
+ *   tpo_shard_nci_assign labels_p = argmax_l (Ups_p Phi)[i, l] (Eq. ell-ast, PAPER.md:625-627,
+ *                       ties -> smallest l); *changed (device int32, zeroed by the caller) set
+ *                       to 1 when a label changes; sums[l][a] = sum_{i in C_l, i in p} Ups[i,a]
+ *                       (k x k fp64) and counts[l] (k fp64)             -> all-reduce all three [sync]
+ *   tpo_nci_phi         Phi[a][l] = sums[l][a] / sqrt(counts[l]) (empty -> 0)
+ * Pointers are device pointers except those marked (host).  Workspace: tpo_shard_solver_ws
+ * (n_p, d, k) bytes serve every call that takes one.  Errors: TPO_EINVAL (shapes, null or
+ * misaligned pointers), TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC (non-SPD Gram, sigma_k == 0).
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_shard_solver_ws(int64_t n_p, int64_t d, int32_t k);
+int tpo_shard_features(const float *Zhat_p, int64_t n_p, int64_t d, const float *Q, float *Rp_p,
+                       double *r_part, void *ws, size_t ws_bytes, void *stream);
+int tpo_shard_dinv(const float *Rp_p, int64_t n_p, int64_t D, const double *r, float *dinv_p,
+                   void *stream);
+int tpo_eig_from_gram(const double *G, const double *r, int64_t D, int32_t k, double *Psi64,
+                      double *sigma, void *ws, size_t ws_bytes, void *stream);
+int tpo_shard_gamma(const float *Rp_p, const float *dinv_p, int64_t n_p, int64_t D, int32_t k,
+                    const double *Psi64, const double *sigma, double *Gamma64_p, void *ws,
+                    size_t ws_bytes, void *stream);
+int tpo_shard_atb64(const double *A_p, const double *B_p, int64_t n_p, int32_t k, double *out,
+                    void *ws, size_t ws_bytes, void *stream);
+int tpo_shard_apply_chol(double *X_p, int64_t n_p, int32_t k, const double *g, void *ws,
+                         size_t ws_bytes, void *stream);
+int tpo_shard_colstats(const double *A_p, int64_t n_p, int32_t k, int64_t row0, double *sum,
+                       double *abs_sum, double *maxabs, int64_t *argmax, void *ws, size_t ws_bytes,
+                       void *stream);
+int tpo_shard_gamma_final(double *Gamma64_p, int64_t n_p, int32_t k, const int32_t *signs,
+                          const double *Psi64, int64_t D, float *Psi, float *Gamma_p, void *ws,
+                          size_t ws_bytes, void *stream);
+int tpo_shard_onmf_init(const float *Gamma_p, int64_t n_p, const float *Psi, const double *sigma,
+                        int64_t D, int32_t k, double *U_p, double *H, void *ws, size_t ws_bytes,
+                        void *stream);
+int tpo_shard_onmf_rtu(const float *Rp_p, const float *dinv_p, const double *U_p, int64_t n_p,
+                       int64_t D, int32_t k, double *RtU_part, void *ws, size_t ws_bytes,
+                       void *stream);
+int tpo_onmf_h_update(double *H, const double *RtU, const double *UtU, int64_t D, int32_t k,
+                      void *ws, size_t ws_bytes, void *stream);
+int tpo_shard_onmf_rh(const float *Rp_p, const float *dinv_p, const double *H, int64_t n_p,
+                      int64_t D, int32_t k, double *RH_p, void *stream);
+int tpo_shard_onmf_u_update(double *U_p, const double *RH_p, const double *M, int64_t n_p,
+                            int32_t k, void *stream);
+int tpo_shard_nci_assign(const double *U_p, const double *Phi, int64_t n_p, int32_t k,
+                         int32_t *labels_p, int32_t *changed, double *sums, double *counts,
+                         void *ws, size_t ws_bytes, void *stream);
+int tpo_nci_phi(const double *sums, const double *counts, int32_t k, double *Phi, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * Whole hot path (Fig. overview): propagate -> Haar Q from G -> features ->
  * top-k (mode) -> cluster.  G: (host) d x d fp64.  Omega: D x (k+p) fp32 (HALKO only, else
  * NULL).  labels: n int32 out.  timings_ms: (host) 4 doubles out {propagate, features,

@@ -20,6 +20,10 @@ SYMBOLS = [
     "tpo_gram_ws", "tpo_gram", "tpo_topk_eig_ws", "tpo_topk_eig",
     "tpo_cluster_ws", "tpo_cluster",
     "tpo_run_ws", "tpo_run",
+    "tpo_shard_solver_ws", "tpo_shard_features", "tpo_shard_dinv", "tpo_eig_from_gram", "tpo_shard_gamma",
+    "tpo_shard_atb64", "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final",
+    "tpo_shard_onmf_init", "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh",
+    "tpo_shard_onmf_u_update", "tpo_shard_nci_assign", "tpo_nci_phi",
 ]
 
 TPO_OK, TPO_EINVAL, TPO_ECUDA, TPO_ENOMEM, TPO_ENCCL, TPO_ENUMERIC = 0, -1, -2, -3, -4, -5
@@ -86,6 +90,28 @@ def lib():
     L.tpo_run_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32]
     L.tpo_run_ws.restype = sz
     L.tpo_run.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+    L.tpo_shard_solver_ws.argtypes = [i64, i64, i32]
+    L.tpo_shard_solver_ws.restype = sz
+    L.tpo_shard_features.argtypes = [vp, i64, i64, vp, vp, vp, vp, sz, vp]
+    L.tpo_shard_dinv.argtypes = [vp, i64, i64, vp, vp, vp]
+    L.tpo_eig_from_gram.argtypes = [vp, vp, i64, i32, vp, vp, vp, sz, vp]
+    L.tpo_shard_gamma.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp, sz, vp]
+    L.tpo_shard_atb64.argtypes = [vp, vp, i64, i32, vp, vp, sz, vp]
+    L.tpo_shard_apply_chol.argtypes = [vp, i64, i32, vp, vp, sz, vp]
+    L.tpo_shard_colstats.argtypes = [vp, i64, i32, i64, vp, vp, vp, vp, vp, sz, vp]
+    L.tpo_shard_gamma_final.argtypes = [vp, i64, i32, vp, vp, i64, vp, vp, vp, sz, vp]
+    L.tpo_shard_onmf_init.argtypes = [vp, i64, vp, vp, i64, i32, vp, vp, vp, sz, vp]
+    L.tpo_shard_onmf_rtu.argtypes = [vp, vp, vp, i64, i64, i32, vp, vp, sz, vp]
+    L.tpo_onmf_h_update.argtypes = [vp, vp, vp, i64, i32, vp, sz, vp]
+    L.tpo_shard_onmf_rh.argtypes = [vp, vp, vp, i64, i64, i32, vp, vp]
+    L.tpo_shard_onmf_u_update.argtypes = [vp, vp, vp, i64, i32, vp]
+    L.tpo_shard_nci_assign.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.tpo_nci_phi.argtypes = [vp, vp, i32, vp, vp]
+    for name in ["tpo_shard_features", "tpo_shard_dinv", "tpo_eig_from_gram", "tpo_shard_gamma", "tpo_shard_atb64",
+                 "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final", "tpo_shard_onmf_init",
+                 "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh", "tpo_shard_onmf_u_update",
+                 "tpo_shard_nci_assign", "tpo_nci_phi"]:
+        getattr(L, name).restype = C.c_int
     for name in ["tpo_propagate", "tpo_shard_degrees", "tpo_shard_start", "tpo_shard_vside", "tpo_shard_vscale",
                  "tpo_shard_uside", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_gram", "tpo_topk_eig",
                  "tpo_cluster", "tpo_run"]:

@@ -409,6 +409,121 @@ int64_t cluster_rows_per_block(int64_t n) { return std::max<int64_t>(64, cdiv(st
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------
+// Pieces of Alg. 2 / Alg. 3 for the row-sharded solver (the caller all-reduces partials).
+// ---------------------------------------------------------------------------------------
+void onmf_init(const float *Gamma, int64_t n, const float *Psi, const double *sigma_host, int64_t D, int k, double *U,
+               double *H, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    double *sig = ar.take<double>(k);
+    TPO_CUDA(cudaMemcpyAsync(sig, sigma_host, sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    const int64_t mx = std::max(n, D) * k;
+    init_factors_kernel<<<cdiv(std::max<int64_t>(mx, 1), 256), 256, 0, st>>>(Gamma, n, Psi, sig, D, k, U, H);
+    TPO_LAUNCH_CHECK();
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
+void onmf_h_update(double *H, const double *RtU, const double *UtU, int64_t D, int k, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    double *Hn = ar.take<double>(D * k);
+    h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
+    TPO_LAUNCH_CHECK();
+    TPO_CUDA(cudaMemcpyAsync(H, Hn, sizeof(double) * D * k, cudaMemcpyDeviceToDevice, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
+void onmf_u_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st) {
+    if (n == 0) return;
+    if (k <= 16) {
+        ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
+    } else {
+        const size_t ups_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * UR * k);
+        TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
+        ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * UR), 148 * 8), 256, ups_smem, st>>>(U, RH, M, n, k);
+    }
+    TPO_LAUNCH_CHECK();
+}
+
+// sums[l][a] = sum over the block partials, counts[l] (fp64) -- fixed order
+__global__ void sums_reduce_kernel(const double *__restrict__ part, const int64_t *__restrict__ cpart, int64_t nb,
+                                   int k, double *__restrict__ sums, double *__restrict__ counts) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < (int64_t)k * k) {
+        double s = 0.0;
+        for (int64_t b = 0; b < nb; ++b) s += part[b * (int64_t)k * k + i];
+        sums[i] = s;
+    }
+    if (i < k) {
+        int64_t c = 0;
+        for (int64_t b = 0; b < nb; ++b) c += cpart[b * (int64_t)k + i];
+        counts[i] = (double)c;
+    }
+}
+
+// Phi[a][l] = sums[l][a] / sqrt(counts[l]) (zero column for an empty cluster)
+__global__ void phi_from_sums_kernel(const double *__restrict__ sums, const double *__restrict__ counts, int k,
+                                     double *__restrict__ Phi) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k * k) return;
+    const int l = i / k, a = i - l * k;
+    Phi[(int64_t)a * k + l] = counts[l] > 0.0 ? sums[i] / sqrt(counts[l]) : 0.0;
+}
+
+size_t nci_assign_part_ws(int64_t n, int k) {
+    const int64_t nb = cdiv(std::max<int64_t>(n, 1), std::max<int64_t>(256, cdiv(cdiv(std::max<int64_t>(n, 1), 2 * 148), 256) * 256));
+    return align_up(sizeof(double) * nb * k * k) + align_up(sizeof(int64_t) * nb * k) + 4 * 256;
+}
+
+// Alg. 3 assign on the shard's rows with the current Phi: labels, changed flag (device int,
+// set to 1 when a label changes; the caller zeroes it), and the shard's cluster sums / counts.
+void nci_assign_part(const double *U, const double *Phi, int64_t n, int k, int32_t *labels, int32_t *changed,
+                     double *sums, double *counts, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    int32_t *zero = ar.take<int32_t>(2);
+    TPO_CUDA(cudaMemsetAsync(zero, 0, sizeof(int32_t) * 2, st));
+    NciState s{changed, zero, zero + 1};
+    const int64_t rpf = std::max<int64_t>(256, cdiv(cdiv(std::max<int64_t>(n, 1), 2 * 148), 256) * 256);
+    const int64_t nbf = cdiv(std::max<int64_t>(n, 1), rpf);
+    double *part = ar.take<double>(nbf * k * k);
+    int64_t *cpart = ar.take<int64_t>(nbf * k);
+    if (n == 0) {
+        TPO_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * nbf * k * k, st));
+        TPO_CUDA(cudaMemsetAsync(cpart, 0, sizeof(int64_t) * nbf * k, st));
+    } else if (k <= 32) {
+        if (k <= 8) nci_fused_kernel<8, 8><<<nbf, 256, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
+        else if (k <= 16) nci_fused_kernel<16, 8><<<nbf, 256, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
+        else nci_fused_kernel<32, 4><<<nbf, 128, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
+        TPO_LAUNCH_CHECK();
+    } else {
+        if (k <= 64) {
+            assign_small_kernel<64><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+        } else {
+            const size_t phi_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * AR * k);
+            TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));
+            assign_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * AR), 148 * 8), 256, phi_smem, st>>>(U, Phi, n, k,
+                                                                                                  labels, s);
+        }
+        TPO_LAUNCH_CHECK();
+        const int sum_nw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / ((int64_t)k * (32 * 8 + 4))));
+        const size_t sum_smem = (size_t)sum_nw * k * (32 * sizeof(double) + sizeof(int));
+        TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
+        cluster_sums_kernel<<<dim3((unsigned)nbf, (unsigned)cdiv(k, 32)), sum_nw * 32, sum_smem, st>>>(
+            U, labels, n, k, rpf, sum_nw, part, cpart, s.done);
+        TPO_LAUNCH_CHECK();
+    }
+    sums_reduce_kernel<<<cdiv((int64_t)k * k, 256), 256, 0, st>>>(part, cpart, nbf, k, sums, counts);
+    TPO_LAUNCH_CHECK();
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
+void nci_phi(const double *sums, const double *counts, int k, double *Phi, cudaStream_t st) {
+    phi_from_sums_kernel<<<cdiv(k * k, 256), 256, 0, st>>>(sums, counts, k, Phi);
+    TPO_LAUNCH_CHECK();
+}
+
 size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     Arena ar(nullptr, 0);
     ar.take<double>(n * k);          // Ups

@@ -550,6 +550,135 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
     return s + 64 * 256;
 }
 
+// ---------------------------------------------------------------------------------------
+// Pieces of the exact top-k for the row-sharded solver (the caller all-reduces partials).
+// ---------------------------------------------------------------------------------------
+size_t eig_from_gram_ws(int64_t D, int32_t k) {
+    const int64_t b = std::min<int64_t>(D, k + std::max<int64_t>(k, 16));
+    return align_up(sizeof(double) * D * D) + 8 * align_up(sizeof(double) * D * (b + 1)) +
+           8 * align_up(sizeof(double) * (b + 1) * (b + 1) + 8) + dgemm_ws(D, b + 1, 0) + 2 * align_up(sizeof(double) * D) +
+           64 * 256;
+}
+
+// Psi64 (D x k) and sigma (host, k) of the top-k eigenpairs of the global Gram G = R^T R, with
+// u = r / ||r|| the known top direction (the same routine tpo_topk_eig runs after its Gram).
+void eig_from_gram(const double *G, const double *r, int64_t D, int32_t k, double *Psi64, double *sigma, Arena &ar,
+                   cudaStream_t st) {
+    double *u = ar.take<double>(D);
+    int *zflag = ar.take<int>(1);
+    TPO_CUDA(cudaMemsetAsync(zflag, 0, sizeof(int), st));
+    unit_vec_kernel<<<1, 1024, 0, st>>>(r, u, D, zflag);
+    TPO_LAUNCH_CHECK();
+    int zh = 0;
+    TPO_CUDA(cudaMemcpyAsync(&zh, zflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    if (zh) throw Error(TPO_ENUMERIC, "top-k: R' has zero column sums");
+    std::vector<double> lam;
+    gram_topk(G, u, D, k, lam, Psi64, ar, st);
+    for (int l = 0; l < k; ++l) {
+        sigma[l] = sqrt(std::max(lam[l], 0.0));
+        if (!(sigma[l] > 0.0)) throw Error(TPO_ENUMERIC, "top-k: sigma_k is zero (rank(R) < k)");
+    }
+}
+
+// G64 = diag(dinv) R' Psi64 diag(1/sigma) on the given rows (fp64)
+void gamma_rows(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
+                const double *sigma, double *G64, Arena &ar, cudaStream_t st) {
+    std::vector<double> ph = to_host(Psi64, (size_t)D * k, st);
+    for (int64_t j = 0; j < D; ++j)
+        for (int l = 0; l < k; ++l) ph[j * k + l] /= sigma[l];
+    const size_t mark = ar.off;
+    double *w = to_dev(ar, ph, st);
+    if (n > 0) tsgemm_AW_f64(Rp, D, dinv, w, n, D, k, G64, k, st);
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
+// X <- X S C^{-1} for the global k x k Gram g = S^{-1} C^T C S^{-1} (one CholeskyQR step)
+void apply_chol(double *X, int64_t n, int k, const double *g, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    double *ci = ar.take<double>((size_t)k * k);
+    int *flag = ar.take<int>(1);
+    TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    if (k <= 112) {
+        chol_inv_device(g, k, ci, flag, st);
+    } else {
+        std::vector<double> gh = to_host(g, (size_t)k * k, st), C((size_t)k * k), Ci((size_t)k * k);
+        if (!host_cholesky_upper(k, gh.data(), C.data()))
+            throw Error(TPO_ENUMERIC, "CholeskyQR: Gram not positive definite");
+        host_upper_inverse(k, C.data(), Ci.data());
+        TPO_CUDA(cudaMemcpyAsync(ci, Ci.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
+    }
+    if (n > 0) {
+        double *tmp = ar.take<double>((size_t)n * k);
+        dgemm(false, n, k, k, 1.0, X, k, ci, k, 0.0, tmp, k, ar, st);
+        TPO_CUDA(cudaMemcpyAsync(X, tmp, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
+    }
+    check_flag(flag, st, "CholeskyQR of Gamma");
+    ar.off = mark;
+}
+
+// per-column sum, sum |x|, max |x| and its (global: + row0) row index over the given rows
+void colstats_rows(const double *A, int64_t n, int k, int64_t row0, double *sum, double *abs_sum, double *maxabs,
+                   int64_t *argmax, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(2 * 148, cdiv(std::max<int64_t>(n, 1), 64)));
+    const int64_t rows_per = cdiv(std::max<int64_t>(n, 1), G);
+    double *ps = ar.take<double>(G * k), *pa = ar.take<double>(G * k), *pm = ar.take<double>(G * k);
+    int64_t *pi = ar.take<int64_t>(G * k);
+    if (n == 0) {
+        fill_f64<<<cdiv(G * k, 256), 256, 0, st>>>(ps, G * k, 0.0);
+        fill_f64<<<cdiv(G * k, 256), 256, 0, st>>>(pa, G * k, 0.0);
+        fill_f64<<<cdiv(G * k, 256), 256, 0, st>>>(pm, G * k, -1.0);
+        TPO_LAUNCH_CHECK();
+        TPO_CUDA(cudaMemsetAsync(pi, 0, sizeof(int64_t) * G * k, st));
+    } else {
+        colstats_part_kernel<<<G, CS_WARPS * 32, 0, st>>>(A, n, k, rows_per, ps, pa, pm, pi);
+        TPO_LAUNCH_CHECK();
+    }
+    colstats_final_kernel<<<cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ps, pa, pm, pi, G, k, sum, abs_sum, argmax);
+    TPO_LAUNCH_CHECK();
+    // max |x| per column: the value at the argmax (read back through the same partials)
+    std::vector<double> hpm = to_host(pm, (size_t)(G * k), st);
+    std::vector<int64_t> hpi = to_host(pi, (size_t)(G * k), st);
+    std::vector<double> mx(k, -1.0);
+    std::vector<int64_t> ai(k, INT64_MAX);
+    for (int64_t g = 0; g < G; ++g)
+        for (int c = 0; c < k; ++c) {
+            const double m = hpm[g * k + c];
+            const int64_t i = hpi[g * k + c];
+            if (m > mx[c] || (m == mx[c] && i < ai[c])) { mx[c] = m; ai[c] = i; }
+        }
+    for (int c = 0; c < k; ++c) ai[c] = ai[c] == INT64_MAX ? row0 : ai[c] + row0;
+    TPO_CUDA(cudaMemcpyAsync(maxabs, mx.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    TPO_CUDA(cudaMemcpyAsync(argmax, ai.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
+// flip the columns with signs_host[l] < 0 in G64 (n x k) and Psi (D x k, fp32; from Psi64 when
+// given), then round G64 to fp32 Gamma
+void gamma_final(double *G64, int64_t n, int k, const int *signs_host, float *Psi, const double *Psi64, int64_t D,
+                 float *Gamma, Arena &ar, cudaStream_t st) {
+    const size_t mark = ar.off;
+    std::vector<int> sg(signs_host, signs_host + k);
+    int *dsg = to_dev(ar, sg, st);
+    if (Psi64) {
+        cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
+        TPO_LAUNCH_CHECK();
+    }
+    flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
+    TPO_LAUNCH_CHECK();
+    if (n > 0) {
+        flip_cols_f64<<<cdiv(n * k, 256), 256, 0, st>>>(G64, n, k, dsg);
+        TPO_LAUNCH_CHECK();
+        cast_f64_f32_k<<<cdiv(n * k, 256), 256, 0, st>>>(G64, n * k, Gamma);
+        TPO_LAUNCH_CHECK();
+    }
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+}
+
 void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p,
                    int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi, Arena &ar,
                    cudaStream_t st, const double *r_colsum) {

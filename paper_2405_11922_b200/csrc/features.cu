@@ -85,6 +85,29 @@ void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cud
     ar.off = mark;
 }
 
+// dinv from a given (global) r: the per-row half of tpo_features (sharded path)
+void dinv_from_r(const float *Rp, int64_t n, int64_t D, const double *r, float *dinv, cudaStream_t st) {
+    if (n == 0) return;
+    dinv_kernel<<<cdiv(n * 32, 256), 256, sizeof(double) * D, st>>>(Rp, n, (int)D, r, dinv);
+    TPO_LAUNCH_CHECK();
+}
+
+// R' of the given rows and their fp64 column sums (the shard's partial r)
+void features_part(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, double *r_part, Arena &ar,
+                   cudaStream_t st) {
+    const int64_t D = 2 * d;
+    if (n == 0) {
+        TPO_CUDA(cudaMemsetAsync(r_part, 0, sizeof(double) * D, st));
+        return;
+    }
+    {
+        const size_t mark = ar.off;
+        features_tc(Zhat, n, d, Q, Rp, ar, st);
+        ar.off = mark;
+    }
+    colsum_f64(Rp, n, D, r_part, ar, st);
+}
+
 size_t features_ws_bytes(int64_t n, int64_t d) {
     Arena ar(nullptr, 0);
     ar.take<double>((size_t)row_groups_for(n, (int)d) * 2 * d);

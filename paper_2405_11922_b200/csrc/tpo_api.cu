@@ -311,6 +311,197 @@ size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, i
     return s + stage + 8 * 256;
 }
 
+// ------------------------------------------------------------------------------------------
+// Row-sharded solver pieces (a5-a9); the caller all-reduces the partials between calls.
+// ------------------------------------------------------------------------------------------
+size_t tpo_shard_solver_ws(int64_t n_p, int64_t d, int32_t k) {
+    const int64_t D = 2 * d;
+    size_t s = features_ws_bytes(n_p, d);
+    s = std::max(s, eig_from_gram_ws(D, k));
+    s = std::max(s, nci_assign_part_ws(n_p, k));
+    s = std::max(s, onmf_ws_bytes(n_p, D, k));
+    s = std::max(s, dgemm_ws(std::max<int64_t>(n_p, k), k, n_p) + align_up(sizeof(double) * (size_t)(n_p * k + k * k)));
+    return s + 64 * 256 + align_up(sizeof(double) * (size_t)(D * k + 4 * 2 * 148 * k));
+}
+
+int tpo_shard_features(const float *Zhat_p, int64_t n_p, int64_t d, const float *Q, float *Rp_p, double *r_part,
+                       void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && d >= 4 && d % 4 == 0, "bad n_p / d");
+        check_ptr(Q, "Q");
+        check_ptr(r_part, "r_part");
+        if (n_p > 0) { check_ptr(Zhat_p, "Zhat_p"); check_ptr(Rp_p, "Rp_p"); }
+        Arena ar(ws, ws_bytes);
+        features_part(Zhat_p, n_p, d, Q, Rp_p, r_part, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_dinv(const float *Rp_p, int64_t n_p, int64_t D, const double *r, float *dinv_p, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && D >= 1, "bad n_p / D");
+        check_ptr(r, "r");
+        if (n_p > 0) { check_ptr(Rp_p, "Rp_p"); check_ptr(dinv_p, "dinv_p", false); }
+        dinv_from_r(Rp_p, n_p, D, r, dinv_p, as_stream(stream));
+    });
+}
+
+int tpo_eig_from_gram(const double *G, const double *r, int64_t D, int32_t k, double *Psi64, double *sigma,
+                      void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(D >= 1 && k >= 1 && k <= D && k <= 128, "need 1 <= k <= min(D, 128)");
+        check_ptr(G, "G");
+        check_ptr(r, "r");
+        check_ptr(Psi64, "Psi64");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        check_ws(ws, ws_bytes, eig_from_gram_ws(D, k));
+        Arena ar(ws, ws_bytes);
+        eig_from_gram(G, r, D, k, Psi64, sigma, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_gamma(const float *Rp_p, const float *dinv_p, int64_t n_p, int64_t D, int32_t k, const double *Psi64,
+                    const double *sigma, double *Gamma64_p, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && D >= 1 && k >= 1, "bad shapes");
+        check_ptr(Psi64, "Psi64");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        if (n_p > 0) { check_ptr(Rp_p, "Rp_p"); check_ptr(dinv_p, "dinv_p", false); check_ptr(Gamma64_p, "Gamma64_p"); }
+        Arena ar(ws, ws_bytes);
+        gamma_rows(Rp_p, dinv_p, n_p, D, k, Psi64, sigma, Gamma64_p, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_atb64(const double *A_p, const double *B_p, int64_t n_p, int32_t k, double *out, void *ws,
+                    size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1, "bad shapes");
+        check_ptr(out, "out");
+        cudaStream_t st = as_stream(stream);
+        if (n_p == 0) {
+            TPO_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * k * k, st));
+            return;
+        }
+        check_ptr(A_p, "A_p");
+        check_ptr(B_p, "B_p");
+        Arena ar(ws, ws_bytes);
+        dgemm(true, k, k, n_p, 1.0, A_p, k, B_p, k, 0.0, out, k, ar, st);
+    });
+}
+
+int tpo_shard_apply_chol(double *X_p, int64_t n_p, int32_t k, const double *g, void *ws, size_t ws_bytes,
+                         void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1, "bad shapes");
+        check_ptr(g, "g");
+        if (n_p > 0) check_ptr(X_p, "X_p");
+        Arena ar(ws, ws_bytes);
+        apply_chol(X_p, n_p, k, g, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_colstats(const double *A_p, int64_t n_p, int32_t k, int64_t row0, double *sum, double *abs_sum,
+                       double *maxabs, int64_t *argmax, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && k <= 128, "bad shapes");
+        check_ptr(sum, "sum"); check_ptr(abs_sum, "abs_sum"); check_ptr(maxabs, "maxabs"); check_ptr(argmax, "argmax");
+        if (n_p > 0) check_ptr(A_p, "A_p");
+        Arena ar(ws, ws_bytes);
+        colstats_rows(A_p, n_p, k, row0, sum, abs_sum, maxabs, argmax, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_gamma_final(double *Gamma64_p, int64_t n_p, int32_t k, const int32_t *signs, const double *Psi64,
+                          int64_t D, float *Psi, float *Gamma_p, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && D >= 1, "bad shapes");
+        TPO_REQUIRE(signs != nullptr, "signs (host) is NULL");
+        check_ptr(Psi, "Psi");
+        if (n_p > 0) { check_ptr(Gamma64_p, "Gamma64_p"); check_ptr(Gamma_p, "Gamma_p"); }
+        Arena ar(ws, ws_bytes);
+        gamma_final(Gamma64_p, n_p, k, reinterpret_cast<const int *>(signs), Psi, Psi64, D, Gamma_p, ar,
+                    as_stream(stream));
+    });
+}
+
+int tpo_shard_onmf_init(const float *Gamma_p, int64_t n_p, const float *Psi, const double *sigma, int64_t D, int32_t k,
+                        double *U_p, double *H, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && D >= 1, "bad shapes");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        check_ptr(Psi, "Psi"); check_ptr(H, "H");
+        if (n_p > 0) { check_ptr(Gamma_p, "Gamma_p"); check_ptr(U_p, "U_p"); }
+        Arena ar(ws, ws_bytes);
+        onmf_init(Gamma_p, n_p, Psi, sigma, D, k, U_p, H, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_onmf_rtu(const float *Rp_p, const float *dinv_p, const double *U_p, int64_t n_p, int64_t D, int32_t k,
+                       double *RtU_part, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && D >= 1, "bad shapes");
+        check_ptr(RtU_part, "RtU_part");
+        cudaStream_t st = as_stream(stream);
+        if (n_p == 0) {
+            TPO_CUDA(cudaMemsetAsync(RtU_part, 0, sizeof(double) * D * k, st));
+            return;
+        }
+        check_ptr(Rp_p, "Rp_p"); check_ptr(dinv_p, "dinv_p", false); check_ptr(U_p, "U_p");
+        Arena ar(ws, ws_bytes);
+        onmf_rtu(Rp_p, n_p, D, dinv_p, U_p, k, RtU_part, ar, st);
+    });
+}
+
+int tpo_onmf_h_update(double *H, const double *RtU, const double *UtU, int64_t D, int32_t k, void *ws,
+                      size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(D >= 1 && k >= 1, "bad shapes");
+        check_ptr(H, "H"); check_ptr(RtU, "RtU"); check_ptr(UtU, "UtU");
+        Arena ar(ws, ws_bytes);
+        onmf_h_update(H, RtU, UtU, D, k, ar, as_stream(stream));
+    });
+}
+
+int tpo_shard_onmf_rh(const float *Rp_p, const float *dinv_p, const double *H, int64_t n_p, int64_t D, int32_t k,
+                      double *RH_p, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && D >= 1, "bad shapes");
+        check_ptr(H, "H");
+        if (n_p == 0) return;
+        check_ptr(Rp_p, "Rp_p"); check_ptr(dinv_p, "dinv_p", false); check_ptr(RH_p, "RH_p");
+        tsgemm_AW_f64(Rp_p, D, dinv_p, H, n_p, D, k, RH_p, k, as_stream(stream));
+    });
+}
+
+int tpo_shard_onmf_u_update(double *U_p, const double *RH_p, const double *M, int64_t n_p, int32_t k, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && k <= 128, "bad shapes");
+        check_ptr(M, "M");
+        if (n_p == 0) return;
+        check_ptr(U_p, "U_p"); check_ptr(RH_p, "RH_p");
+        onmf_u_update(U_p, RH_p, M, n_p, k, as_stream(stream));
+    });
+}
+
+int tpo_shard_nci_assign(const double *U_p, const double *Phi, int64_t n_p, int32_t k, int32_t *labels_p,
+                         int32_t *changed, double *sums, double *counts, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n_p >= 0 && k >= 1 && k <= 128, "bad shapes");
+        check_ptr(Phi, "Phi"); check_ptr(changed, "changed", false); check_ptr(sums, "sums"); check_ptr(counts, "counts");
+        if (n_p > 0) { check_ptr(U_p, "U_p"); check_ptr(labels_p, "labels_p", false); }
+        check_ws(ws, ws_bytes, nci_assign_part_ws(n_p, k));
+        Arena ar(ws, ws_bytes);
+        nci_assign_part(U_p, Phi, n_p, k, labels_p, changed, sums, counts, ar, as_stream(stream));
+    });
+}
+
+int tpo_nci_phi(const double *sums, const double *counts, int32_t k, double *Phi, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(k >= 1, "bad k");
+        check_ptr(sums, "sums"); check_ptr(counts, "counts"); check_ptr(Phi, "Phi");
+        nci_phi(sums, counts, k, Phi, as_stream(stream));
+    });
+}
+
 // SMs left to the Haar rotation while the (persistent) propagation kernels run beside it
 constexpr int kHaarReserveSms = 8;
 

@@ -116,6 +116,32 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
                   int32_t *iters_used, Arena &ar, cudaStream_t st);
 
 void haar_q_device(const double *G_host, int64_t d, float *Q_out, Arena &ar, cudaStream_t st);
+
+// Pieces of a5-a9 for the row-sharded solver (the caller all-reduces the
+// partials between them).  features.cu:
+void features_part(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, double *r_part, Arena &ar,
+                   cudaStream_t st);
+void dinv_from_r(const float *Rp, int64_t n, int64_t D, const double *r, float *dinv, cudaStream_t st);
+// eig.cu: top-k of a given (global) Gram; Gamma pieces on the shard's rows
+void eig_from_gram(const double *G, const double *r, int64_t D, int32_t k, double *Psi64, double *sigma, Arena &ar,
+                   cudaStream_t st);
+size_t eig_from_gram_ws(int64_t D, int32_t k);
+void gamma_rows(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
+                const double *sigma, double *G64, Arena &ar, cudaStream_t st);
+void apply_chol(double *X, int64_t n, int k, const double *g, Arena &ar, cudaStream_t st);
+void colstats_rows(const double *A, int64_t n, int k, int64_t row0, double *sum, double *abs_sum, double *maxabs,
+                   int64_t *argmax, Arena &ar, cudaStream_t st);
+void gamma_final(double *G64, int64_t n, int k, const int *signs_host, float *Psi, const double *Psi64, int64_t D,
+                 float *Gamma, Arena &ar, cudaStream_t st);
+// cluster.cu
+void onmf_init(const float *Gamma, int64_t n, const float *Psi, const double *sigma_host, int64_t D, int k, double *U,
+               double *H, Arena &ar, cudaStream_t st);
+void onmf_h_update(double *H, const double *RtU, const double *UtU, int64_t D, int k, Arena &ar, cudaStream_t st);
+void onmf_u_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);
+void nci_assign_part(const double *U, const double *Phi, int64_t n, int k, int32_t *labels, int32_t *changed,
+                     double *sums, double *counts, Arena &ar, cudaStream_t st);
+size_t nci_assign_part_ws(int64_t n, int k);
+void nci_phi(const double *sums, const double *counts, int k, double *Phi, cudaStream_t st);
 size_t haar_q_ws_bytes(int64_t d);
 
 // ----------------------------------------------------------------------------------------

@@ -105,6 +105,15 @@ class TorchCollectives:
             parts = list(out.chunk(self.world, dim=0))
             self.dist.all_gather(parts, inp.contiguous(), group=self.group)
 
+    def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
+        """(world, *t.shape): every rank's copy of t."""
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        if self.backend == "nccl":
+            self.dist.all_gather_into_tensor(out.view(-1), t.contiguous().view(-1), group=self.group)
+        else:
+            self.dist.all_gather([out[r] for r in range(self.world)], t.contiguous(), group=self.group)
+        return out
+
 
 class GpuShardOps:
     """Local compute of one shard through libtpo's tpo_shard_* entry points (device tensors)."""
@@ -207,3 +216,200 @@ def propagate_sharded(ops, coll, Xp: torch.Tensor, alpha: float, T: int, want_zh
         last = t == T - 1
         ops.uside(Q, Xp, alpha, s_u, last, Z, Zhat if last else None)
     return Z, Zhat
+
+
+# ------------------------------------------------------------------------------------------
+# a5-a9 on row shards ("an all-reduce of the d x k Gram matrices"): every
+# D x D, D x k and k x k quantity is the all-reduced sum of the shards' partials, so each rank
+# holds the same replicated factors; the n-row quantities stay on their rank.
+# ------------------------------------------------------------------------------------------
+class GpuSolverOps:
+    """Local compute of the sharded solver through libtpo's tpo_shard_* solver entry points."""
+
+    def __init__(self, n_p: int, d: int, k: int, device):
+        self.n_p, self.d, self.k, self.D = n_p, d, k, 2 * d
+        self.device = torch.device(device)
+        nb = lib().tpo_shard_solver_ws(n_p, d, k)
+        nb = max(nb, lib().tpo_gram_ws(max(n_p, 1), self.D))
+        self.ws = torch.empty(max(int(nb), 256), dtype=torch.uint8, device=self.device)
+
+    @staticmethod
+    def _p(t):
+        return None if t is None else C.c_void_p(t.data_ptr())
+
+    def _st(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _z(self, *shape, dtype=torch.float64):
+        return torch.zeros(shape, dtype=dtype, device=self.device)
+
+    def _ws(self):
+        return self._p(self.ws), self.ws.numel()
+
+    def features(self, Zhat_p, Q):
+        Rp = torch.empty(self.n_p, self.D, dtype=torch.float32, device=self.device)
+        r = self._z(self.D)
+        check(lib().tpo_shard_features(self._p(Zhat_p), self.n_p, self.d, self._p(Q), self._p(Rp), self._p(r),
+                                       *self._ws(), self._st()))
+        return Rp, r
+
+    def dinv(self, Rp, r):
+        dv = torch.empty(self.n_p, dtype=torch.float32, device=self.device)
+        check(lib().tpo_shard_dinv(self._p(Rp), self.n_p, self.D, self._p(r), self._p(dv), self._st()))
+        return dv
+
+    def gram(self, Rp, dinv):
+        G = self._z(self.D, self.D)
+        if self.n_p > 0:
+            check(lib().tpo_gram(self._p(Rp), self._p(dinv), self.n_p, self.D, self._p(G), *self._ws(), self._st()))
+        return G
+
+    def eig(self, G, r):
+        Psi64 = self._z(self.D, self.k)
+        sig = np.zeros(self.k)
+        check(lib().tpo_eig_from_gram(self._p(G), self._p(r), self.D, self.k, self._p(Psi64),
+                                      sig.ctypes.data_as(C.c_void_p), *self._ws(), self._st()))
+        return Psi64, sig
+
+    def gamma(self, Rp, dinv, Psi64, sigma):
+        G64 = self._z(self.n_p, self.k)
+        sig = np.ascontiguousarray(sigma, np.float64)
+        check(lib().tpo_shard_gamma(self._p(Rp), self._p(dinv), self.n_p, self.D, self.k, self._p(Psi64),
+                                    sig.ctypes.data_as(C.c_void_p), self._p(G64), *self._ws(), self._st()))
+        return G64
+
+    def atb(self, A, B):
+        out = self._z(self.k, self.k)
+        check(lib().tpo_shard_atb64(self._p(A), self._p(B), self.n_p, self.k, self._p(out), *self._ws(), self._st()))
+        return out
+
+    def apply_chol(self, X, g):
+        check(lib().tpo_shard_apply_chol(self._p(X), self.n_p, self.k, self._p(g), *self._ws(), self._st()))
+
+    def colstats(self, G64, row0):
+        s, a, v = self._z(self.k), self._z(self.k), self._z(self.k)
+        i = torch.zeros(self.k, dtype=torch.int64, device=self.device)
+        check(lib().tpo_shard_colstats(self._p(G64), self.n_p, self.k, int(row0), self._p(s), self._p(a), self._p(v),
+                                       self._p(i), *self._ws(), self._st()))
+        return s, a, v, i
+
+    def gamma_final(self, G64, signs, Psi64):
+        Psi = torch.empty(self.D, self.k, dtype=torch.float32, device=self.device)
+        Gm = torch.empty(self.n_p, self.k, dtype=torch.float32, device=self.device)
+        sg = np.ascontiguousarray(signs, np.int32)
+        check(lib().tpo_shard_gamma_final(self._p(G64), self.n_p, self.k, sg.ctypes.data_as(C.c_void_p),
+                                          self._p(Psi64), self.D, self._p(Psi), self._p(Gm), *self._ws(), self._st()))
+        return Psi, Gm
+
+    def onmf_init(self, Gamma_p, Psi, sigma):
+        U, H = self._z(self.n_p, self.k), self._z(self.D, self.k)
+        sig = np.ascontiguousarray(sigma, np.float64)
+        check(lib().tpo_shard_onmf_init(self._p(Gamma_p), self.n_p, self._p(Psi), sig.ctypes.data_as(C.c_void_p),
+                                        self.D, self.k, self._p(U), self._p(H), *self._ws(), self._st()))
+        return U, H
+
+    def rtu(self, Rp, dinv, U):
+        out = self._z(self.D, self.k)
+        check(lib().tpo_shard_onmf_rtu(self._p(Rp), self._p(dinv), self._p(U), self.n_p, self.D, self.k,
+                                       self._p(out), *self._ws(), self._st()))
+        return out
+
+    def h_update(self, H, RtU, UtU):
+        check(lib().tpo_onmf_h_update(self._p(H), self._p(RtU), self._p(UtU), self.D, self.k, *self._ws(), self._st()))
+
+    def rh(self, Rp, dinv, H):
+        out = self._z(self.n_p, self.k)
+        check(lib().tpo_shard_onmf_rh(self._p(Rp), self._p(dinv), self._p(H), self.n_p, self.D, self.k, self._p(out),
+                                      self._st()))
+        return out
+
+    def u_update(self, U, RH, M):
+        check(lib().tpo_shard_onmf_u_update(self._p(U), self._p(RH), self._p(M), self.n_p, self.k, self._st()))
+
+    def nci_assign(self, U, Phi, labels):
+        changed = torch.zeros(1, dtype=torch.int32, device=self.device)
+        sums, counts = self._z(self.k, self.k), self._z(self.k)
+        check(lib().tpo_shard_nci_assign(self._p(U), self._p(Phi), self.n_p, self.k, self._p(labels), self._p(changed),
+                                         self._p(sums), self._p(counts), *self._ws(), self._st()))
+        return changed, sums, counts
+
+    def phi(self, sums, counts):
+        Phi = self._z(self.k, self.k)
+        check(lib().tpo_nci_phi(self._p(sums), self._p(counts), self.k, self._p(Phi), self._st()))
+        return Phi
+
+    def eye(self):
+        return torch.eye(self.k, dtype=torch.float64, device=self.device)
+
+    def labels(self):
+        return torch.full((self.n_p,), -1, dtype=torch.int32, device=self.device)
+
+
+def _sign_rule(s, a, vals, idxs):
+    """R8 from the global column statistics: sum >= 0, else (near-zero sums) the sign of the
+    largest-magnitude entry, the smallest global row index among equal magnitudes.  vals/idxs:
+    per rank (world x k) signed value at the rank's argmax and its global row index."""
+    k = s.shape[0]
+    signs = np.ones(k, np.int32)
+    for l in range(k):
+        if abs(s[l]) < 1e-6 * a[l]:
+            best, bi, bv = -1.0, None, 0.0
+            for r in range(vals.shape[0]):
+                m, i = abs(vals[r, l]), idxs[r, l]
+                if m > best or (m == best and i < bi):
+                    best, bi, bv = m, i, vals[r, l]
+            signs[l] = -1 if bv < 0 else 1
+        else:
+            signs[l] = -1 if s[l] < 0 else 1
+    return signs
+
+
+def solve_sharded(ops, coll, Zhat_p, Q, row0: int, Tf: int = 5, Tg: int = 20):
+    """a5-a9 on this rank's rows (features -> exact top-k -> ONMF -> NCI), the same steps as
+    tpo_run with the fp64 partials all-reduced in between.  Returns (labels_p, Alg. 3 iterations)."""
+    Rp, r = ops.features(Zhat_p, Q)
+    coll.allreduce_sum(r)                                    # r = sum_i R'[i]
+    dinv = ops.dinv(Rp, r)
+    G = ops.gram(Rp, dinv)
+    coll.allreduce_sum(G)                                    # G = R^T R
+    Psi64, sigma = ops.eig(G, r)                             # replicated (identical G on every rank)
+    G64 = ops.gamma(Rp, dinv, Psi64, sigma)
+    k = sigma.shape[0]
+    eye = torch.eye(k, dtype=torch.float64, device=G64.device)
+    for p in range(3):                                       # CholeskyQR polish while ||G^T G - I|| > 1e-6
+        g = ops.atb(G64, G64)
+        coll.allreduce_sum(g)
+        if float((g - eye).abs().max()) <= 1e-6 or p == 2:
+            break
+        ops.apply_chol(G64, g)
+    s, a, v, i = ops.colstats(G64, row0)
+    coll.allreduce_sum(s)
+    coll.allreduce_sum(a)
+    vals = coll.all_gather_rows(v)
+    idxs = coll.all_gather_rows(i)
+    signs = _sign_rule(s.cpu().numpy(), a.cpu().numpy(), vals.cpu().numpy(), idxs.cpu().numpy())
+    Psi, Gamma_p = ops.gamma_final(G64, signs, Psi64)
+    U, H = ops.onmf_init(Gamma_p, Psi, sigma)                # Alg. 2
+    for t in range(Tf):
+        RtU = ops.rtu(Rp, dinv, U)
+        coll.allreduce_sum(RtU)
+        UtU = ops.atb(U, U)
+        coll.allreduce_sum(UtU)
+        ops.h_update(H, RtU, UtU)
+        RH = ops.rh(Rp, dinv, H)
+        M = ops.atb(U, RH)
+        coll.allreduce_sum(M)
+        ops.u_update(U, RH, M)
+    Phi = ops.eye()                                          # Alg. 3
+    labels = ops.labels()
+    iters = 0
+    for t in range(Tg):
+        changed, sums, counts = ops.nci_assign(U, Phi, labels)
+        coll.allreduce_sum(changed)
+        iters += 1
+        if int(changed.item()) == 0 or t == Tg - 1:
+            break
+        coll.allreduce_sum(sums)
+        coll.allreduce_sum(counts)
+        Phi = ops.phi(sums, counts)
+    return labels, iters
