@@ -400,8 +400,18 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     }
 }
 
+// signs of R8 from the column statistics, on the device (no host round trip)
+__global__ void sign_rule_kernel(const double *__restrict__ s, const double *__restrict__ a,
+                                 const int64_t *__restrict__ arg, const double *__restrict__ Gamma, int k,
+                                 int *__restrict__ sgn) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= k) return;
+    if (fabs(s[l]) < 1e-6 * a[l]) sgn[l] = Gamma[arg[l] * k + l] < 0.0 ? -1 : 1;
+    else sgn[l] = s[l] < 0.0 ? -1 : 1;
+}
+
 // Sign rule R8 on (Gamma, Psi): sum_i Gamma[i,l] >= 0, else (near-zero sums) the sign of the
-// largest-magnitude entry.  Flips are applied to both factors (Gamma fp64 here).
+// largest-magnitude entry (smallest index among ties).  Flips are applied to both factors.
 void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Arena &ar, cudaStream_t st) {
     const size_t mark = ar.off;
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(2 * 148, cdiv(n, 64)));
@@ -410,60 +420,57 @@ void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Are
     int64_t *pi = ar.take<int64_t>(G * k);
     double *s = ar.take<double>(k), *a = ar.take<double>(k);
     int64_t *arg = ar.take<int64_t>(k);
+    int *dsg = ar.take<int>(k);
     colstats_part_kernel<<<G, CS_WARPS * 32, 0, st>>>(Gamma, n, k, rows_per, ps, pa, pm, pi);
     TPO_LAUNCH_CHECK();
     colstats_final_kernel<<<cdiv((int64_t)k * 32, 256), 256, 0, st>>>(ps, pa, pm, pi, G, k, s, a, arg);
     TPO_LAUNCH_CHECK();
-    std::vector<double> hs = to_host(s, k, st), ha = to_host(a, k, st);
-    std::vector<int64_t> harg = to_host(arg, k, st);
-    std::vector<int> sg(k, 1);
-    bool any = false;
-    for (int l = 0; l < k; ++l) {
-        if (fabs(hs[l]) < 1e-6 * ha[l]) {
-            double v;
-            TPO_CUDA(cudaMemcpy(&v, Gamma + harg[l] * k + l, sizeof(double), cudaMemcpyDeviceToHost));
-            sg[l] = v < 0.0 ? -1 : 1;
-        } else {
-            sg[l] = hs[l] < 0.0 ? -1 : 1;
-        }
-        any |= sg[l] < 0;
-    }
-    if (any) {
-        int *dsg = to_dev(ar, sg, st);
-        flip_cols_f64<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
-        TPO_LAUNCH_CHECK();
-        flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
-        TPO_LAUNCH_CHECK();
-        TPO_CUDA(cudaStreamSynchronize(st));
-    }
+    sign_rule_kernel<<<cdiv(k, 128), 128, 0, st>>>(s, a, arg, Gamma, k, dsg);
+    TPO_LAUNCH_CHECK();
+    flip_cols_f64<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
+    TPO_LAUNCH_CHECK();
+    flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
+    TPO_LAUNCH_CHECK();
     ar.off = mark;
 }
 
+// ci <- I when the Gram g is already within 1e-6 of I (then X ci = X exactly): the polish
+// decision taken on the device
+__global__ void polish_select_kernel(const double *__restrict__ g, int k, double *__restrict__ ci) {
+    __shared__ int need;
+    if (threadIdx.x == 0) need = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+        const double dv = fabs(g[i] - ((i / k) == (i % k) ? 1.0 : 0.0));
+        if (!(dv <= 1e-6)) need = 1;
+    }
+    __syncthreads();
+    if (need) return;
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) ci[i] = (i / k) == (i % k) ? 1.0 : 0.0;
+}
+
 // CholeskyQR polish of the fp64 n x k Gamma while its Gram is off identity by > 1e-6 (at most
-// two corrections): G = Gamma^T Gamma (dgemm), Ci = S C^{-1} (chol_inv), Gamma <- Gamma Ci.
+// two corrections): G = Gamma^T Gamma (dgemm), Ci = S C^{-1} (chol_inv), Gamma <- Gamma Ci, with
+// Ci replaced by I on the device when the Gram is already within 1e-6 of I.
 void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
     const size_t mark = ar.off;
     double *g = ar.take<double>((size_t)k * k), *ci = ar.take<double>((size_t)k * k);
-    double *tmp = nullptr;
+    double *tmp = ar.take<double>((size_t)n * k);
     int *flag = ar.take<int>(1);
     TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    for (int pass = 0; pass < 3; ++pass) {
+    for (int pass = 0; pass < 2; ++pass) {
         dgemm(true, k, k, n, 1.0, Gamma, k, Gamma, k, 0.0, g, k, ar, st);
-        std::vector<double> gh = to_host(g, (size_t)k * k, st);
-        double dev = 0.0;
-        for (int a = 0; a < k; ++a)
-            for (int b = 0; b < k; ++b) dev = std::max(dev, fabs(gh[a * k + b] - (a == b ? 1.0 : 0.0)));
-        if (dev <= 1e-6 || pass == 2) break;
         if (k <= 112) {
             chol_inv_device(g, k, ci, flag, st);
         } else {
-            std::vector<double> C((size_t)k * k), Ci((size_t)k * k);
+            std::vector<double> gh = to_host(g, (size_t)k * k, st), C((size_t)k * k), Ci((size_t)k * k);
             if (!host_cholesky_upper(k, gh.data(), C.data()))
                 throw Error(TPO_ENUMERIC, "CholeskyQR2 polish: Gamma^T Gamma not positive definite");
             host_upper_inverse(k, C.data(), Ci.data());
             TPO_CUDA(cudaMemcpyAsync(ci, Ci.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
         }
-        if (!tmp) tmp = ar.take<double>((size_t)n * k);
+        polish_select_kernel<<<1, 256, 0, st>>>(g, k, ci);
+        TPO_LAUNCH_CHECK();
         dgemm(false, n, k, k, 1.0, Gamma, k, ci, k, 0.0, tmp, k, ar, st);
         TPO_CUDA(cudaMemcpyAsync(Gamma, tmp, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
     }
@@ -471,14 +478,22 @@ void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
     ar.off = mark;
 }
 
+// Psi / sigma column scaling on the device
+__global__ void scale_cols_kernel(const double *__restrict__ A, int64_t rows, int k, const double *__restrict__ sig,
+                                  double *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * k) return;
+    out[i] = A[i] / sig[i % k];
+}
+
 // Gamma = diag(dinv) R' Psi64 diag(1/sigma) in fp64, polished and sign-fixed, then rounded to
 // fp32; Psi (fp32 out) = Psi64.
 void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
                     const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st) {
-    std::vector<double> ph = to_host(Psi64, (size_t)D * k, st);
-    for (int64_t j = 0; j < D; ++j)
-        for (int l = 0; l < k; ++l) ph[j * k + l] /= sig[l];
-    double *w = to_dev(ar, ph, st);
+    double *sd = to_dev(ar, sig, st);
+    double *w = ar.take<double>((size_t)D * k);
+    scale_cols_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D, k, sd, w);
+    TPO_LAUNCH_CHECK();
     double *G64 = ar.take<double>((size_t)n * k);
     tsgemm_AW_f64(Rp, D, dinv, w, n, D, k, G64, k, st);
     cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
@@ -487,6 +502,7 @@ void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, in
     apply_sign_rule(G64, n, k, Psi, D, ar, st);
     cast_f64_f32_k<<<cdiv(n * k, 256), 256, 0, st>>>(G64, n * k, Gamma);
     TPO_LAUNCH_CHECK();
+    TPO_CUDA(cudaStreamSynchronize(st));
 }
 
 __global__ void copy2d_kernel(const double *__restrict__ src, int64_t lds, double *__restrict__ dst, int64_t ldd,
