@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ 
 // Small-k variant (k <= 16): one thread per row, the row of Ups in registers, Phi in smem
 // (same arithmetic and summation order as assign_kernel).
 template <int KM>
-__global__ void __launch_bounds__(256) assign_small_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
+__global__ void __launch_bounds__(128) assign_small_kernel(const double *__restrict__ U, const double *__restrict__ Phi,
                                                            int64_t n, int k, int32_t *__restrict__ labels, NciState s) {
     if (*s.done) return;
     __shared__ double phs[KM * KM];
@@ -215,16 +215,21 @@ __global__ void __launch_bounds__(256) assign_small_kernel(const double *__restr
     double best = 0.0;
     int arg = 0;
     int l = 0;
-    for (; l + 1 < k; l += 2) {                 // two scores at once (independent chains)
-        double sc0 = 0.0, sc1 = 0.0;
+    for (; l + 3 < k; l += 4) {                 // four scores at once (independent chains)
+        double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0, sc3 = 0.0;
 #pragma unroll
         for (int a = 0; a < KM; ++a)
             if (a < k) {
-                sc0 = __dadd_rn(sc0, __dmul_rn(u[a], phs[a * k + l]));
-                sc1 = __dadd_rn(sc1, __dmul_rn(u[a], phs[a * k + l + 1]));
+                const double ua = u[a];
+                sc0 = __dadd_rn(sc0, __dmul_rn(ua, phs[a * k + l]));
+                sc1 = __dadd_rn(sc1, __dmul_rn(ua, phs[a * k + l + 1]));
+                sc2 = __dadd_rn(sc2, __dmul_rn(ua, phs[a * k + l + 2]));
+                sc3 = __dadd_rn(sc3, __dmul_rn(ua, phs[a * k + l + 3]));
             }
         if (l == 0 || sc0 > best) { best = sc0; arg = l; }
         if (sc1 > best) { best = sc1; arg = l + 1; }
+        if (sc2 > best) { best = sc2; arg = l + 2; }
+        if (sc3 > best) { best = sc3; arg = l + 3; }
     }
     for (; l < k; ++l) {
         double sc = 0.0;
@@ -498,7 +503,7 @@ void nci_assign_part(const double *U, const double *Phi, int64_t n, int k, int32
         TPO_LAUNCH_CHECK();
     } else {
         if (k <= 64) {
-            assign_small_kernel<64><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+            assign_small_kernel<64><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
         } else {
             const size_t phi_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * AR * k);
             TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));
@@ -608,11 +613,11 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
             continue;
         }
         if (k <= 16)
-            assign_small_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+            assign_small_kernel<16><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
         else if (k <= 32)
-            assign_small_kernel<32><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+            assign_small_kernel<32><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
         else if (k <= 64)
-            assign_small_kernel<64><<<cdiv(n, 256), 256, 0, st>>>(U, Phi, n, k, labels, s);
+            assign_small_kernel<64><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
         else
             assign_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * AR), 148 * 8), 256, phi_smem, st>>>(U, Phi, n, k,
                                                                                                   labels, s);
