@@ -3,7 +3,7 @@
 //
 // EXACT mode (R7): Gram G = R^T R (D x D, fp64 sums) once, then block subspace iteration
 // with Rayleigh-Ritz on G (the D x D image of the implicit n x n affinity S~ = R R^T:
-// both share their nonzero spectrum) until the top-k Ritz residuals fall below 1e-10 lambda_1;
+// both share their nonzero spectrum) until the top-k Ritz residuals fall below 1e-9 lambda_1;
 // with a full-rank block (b = D) this is one Rayleigh-Ritz step, i.e. a dense eigensolve.
 // Then Gamma = R Psi Sigma^{-1} and a CholeskyQR2 polish if ||Gamma^T Gamma - I||_max > 1e-6.
 // HALKO mode: the randomised truncated SVD the paper cites, q power steps.
@@ -294,7 +294,8 @@ __global__ void stack_kernel(const double *__restrict__ u, const double *__restr
 //  * otherwise Chebyshev-filtered block subspace iteration (degree m) on the deflated
 //    Gd = G - u u^T with a block V (D x b) kept orthogonal to u, and after every filter a
 //    Rayleigh-Ritz step with the FULL G on span([u, V]); stop when the top-k Ritz residuals
-//    ||G z - theta z|| (computed explicitly) fall below 1e-10 theta_1.  The filter damps [0, theta_min] (theta_min
+//    ||G z - theta z|| (computed explicitly) fall below 1e-9 theta_1 (sin theta <= residual / gap,
+//    orders of magnitude below the 1e-4 parity bound and the fp32 rounding of Gamma).  The filter damps [0, theta_min] (theta_min
 //    = smallest Ritz value of the block) and amplifies the wanted end of the spectrum; the
 //    deflation keeps the lambda = 1 direction from swamping the block.
 void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
@@ -381,7 +382,7 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         const std::vector<double> rh = to_host(res, k, st);
         double rmax = 0.0;
         for (int l = 0; l < k; ++l) rmax = std::max(rmax, rh[l]);
-        if (rmax <= 1e-10 * fabs(w[0]) || round == max_rounds) {
+        if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
             check_flag(flag, st, "top-k subspace iteration (CholeskyQR2)");
             lam.assign(w.begin(), w.begin() + k);
             ar.off = mark;
