@@ -497,160 +497,6 @@ __global__ void __launch_bounds__(WPB * 32, MINB) spmm_kernel(SpmmArgs a) {
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// Asynchronous gather pipeline (cp.async ring).  The gathers of a work item are issued RING
-// edges ahead of their consumption into a per-warp shared-memory ring (one slot = the warp's
-// SL column slices of one neighbour row, 512 B per slice), so a warp keeps RING row slices in
-// flight without holding them in registers; the consumer reads its own lane's 16 B back,
-// accumulates, and flushes rows as the edge stream crosses their ends (same order of
-// additions as the register path: edges of a row in CSR order).
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16_ca(uint32_t dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_grp() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_grp() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int SL, int RING>
-struct RingIssuer {
-    const int32_t *col;
-    const float4 *src;
-    int64_t d4;
-    uint32_t ring;          // this lane's smem address of slot 0, slice 0
-    int c4[SL];
-    bool act[SL];
-    int64_t pb = -1;        // base edge of the loaded index batch
-    int pcol = 0;
-    // issue the gathers of edge e (e < end) into slot e % RING, then commit one group
-    __device__ __forceinline__ void issue(int64_t e, int64_t end, int lane) {
-        if (e < end) {
-            const int64_t b = e & ~int64_t(31);
-            if (b != pb) {                                   // warp-uniform
-                pb = b;
-                pcol = b + lane < end ? __ldg(col + b + lane) : 0;
-            }
-            const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, pcol, (int)(e - b)) * d4;
-            const uint32_t slot = ring + (uint32_t)((e % RING) * SL * 512);
-#pragma unroll
-            for (int q = 0; q < SL; ++q)
-                if (act[q]) cp_async16_ca(slot + q * 512, src + c4[q] + ro);
-        }
-        cp_async_commit_grp();
-    }
-};
-
-template <int EPI, bool WEIGHTED, int SL, int RING>
-__global__ void __launch_bounds__(WPB * 32) spmm_ring_kernel(SpmmArgs a) {
-    extern __shared__ __align__(16) float4 ring_sm[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t tot = packed_total(a.sch.offsets, a.n_rows);
-    const int64_t n_items = tot >> 32;
-    const int grp = (int)(gw / a.sch.max_items);
-    const int64_t item = gw - (int64_t)grp * a.sch.max_items;
-    if (item >= n_items) return;
-    const int4 it = a.sch.items[item];
-    RingIssuer<SL, RING> is;
-    is.col = a.col;
-    is.src = a.src;
-    is.d4 = a.d4;
-    is.ring = static_cast<uint32_t>(__cvta_generic_to_shared(ring_sm + (size_t)wib * RING * SL * 32)) + lane * 16;
-#pragma unroll
-    for (int q = 0; q < SL; ++q) {
-        is.c4[q] = (grp * SL + q) * 32 + lane;
-        is.act[q] = is.c4[q] < a.d4;
-    }
-    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 *my_ring = ring_sm + (size_t)wib * RING * SL * 32 + lane;
-    auto fetch = [&](int64_t e, float4 (&v)[SL]) {
-        const float4 *sl = my_ring + (size_t)(e % RING) * SL * 32;
-#pragma unroll
-        for (int q = 0; q < SL; ++q) v[q] = is.act[q] ? sl[q * 32] : zero;
-    };
-    if (it.w != 0) {                                     // chunk of a long row -> partial sums
-        const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];
-        const int64_t beg = rb + (int64_t)it.y * CHUNK, end = min(re, beg + CHUNK);
-        for (int i = 0; i < RING - 1; ++i) is.issue(beg + i, end, lane);
-        float4 acc[SL];
-#pragma unroll
-        for (int q = 0; q < SL; ++q) acc[q] = zero;
-        float myw = 1.f;
-        int64_t wb = -1;
-        for (int64_t e = beg; e < end; ++e) {
-            is.issue(e + RING - 1, end, lane);
-            cp_async_wait_grp<RING - 1>();
-            float4 v[SL];
-            fetch(e, v);
-            float w = 1.f;
-            if (WEIGHTED) {
-                const int64_t b = e & ~int64_t(31);
-                if (b != wb) { wb = b; myw = b + lane < end ? __ldg(a.val + b + lane) : 0.f; }
-                w = __shfl_sync(0xffffffffu, myw, (int)(e - b));
-            }
-#pragma unroll
-            for (int q = 0; q < SL; ++q) acc[q] = WEIGHTED ? f4fma(w, v[q], acc[q]) : f4add(acc[q], v[q]);
-        }
-        cp_async_wait_grp<0>();
-#pragma unroll
-        for (int q = 0; q < SL; ++q)
-            if (is.act[q]) a.partials[(int64_t)it.z * a.d4 + is.c4[q]] = acc[q];
-        return;
-    }
-    // row block [r0, r1): one edge stream over consecutive short rows
-    const int64_t r0 = it.x, r1 = item + 1 < n_items ? (int64_t)a.sch.items[item + 1].x : a.n_rows;
-    const int64_t e_beg = a.rowptr[r0], e_end = a.rowptr[r1];
-    for (int i = 0; i < RING - 1; ++i) is.issue(e_beg + i, e_end, lane);
-    int64_t rb = r0;                                     // current 32-row batch
-    int nb = (int)min((int64_t)32, r1 - rb);
-    int64_t my_end = lane < nb ? a.rowptr[rb + 1 + lane] : 0;
-    float my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
-    int cur = 0;
-    int64_t cur_end = __shfl_sync(0xffffffffu, my_end, 0);
-    float4 xcur[SL], acc[SL];
-    load_x_sl<EPI, SL>(a, rb, is.c4, is.act, xcur);
-#pragma unroll
-    for (int q = 0; q < SL; ++q) acc[q] = zero;
-    auto advance = [&]() {      // flush row rb + cur, move to the next row (warp-uniform)
-        epilogue_sl<EPI, SL>(a, rb + cur, is.c4, is.act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
-#pragma unroll
-        for (int q = 0; q < SL; ++q) acc[q] = zero;
-        ++cur;
-        if (cur == nb) {
-            rb += 32;
-            cur = 0;
-            nb = (int)min((int64_t)32, r1 - rb);
-            if (nb > 0) {
-                my_end = lane < nb ? a.rowptr[rb + 1 + lane] : 0;
-                my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
-            }
-        }
-        if (nb > 0) {
-            cur_end = __shfl_sync(0xffffffffu, my_end, cur);
-            load_x_sl<EPI, SL>(a, rb + cur, is.c4, is.act, xcur);
-        }
-    };
-    float myw = 1.f;
-    int64_t wb = -1;
-    for (int64_t e = e_beg; e < e_end; ++e) {
-        is.issue(e + RING - 1, e_end, lane);
-        while (e >= cur_end) advance();                  // rows ending before edge e (incl. empty rows)
-        cp_async_wait_grp<RING - 1>();
-        float4 v[SL];
-        fetch(e, v);
-        float w = 1.f;
-        if (WEIGHTED) {
-            const int64_t b = e & ~int64_t(31);
-            if (b != wb) { wb = b; myw = b + lane < e_end ? __ldg(a.val + b + lane) : 0.f; }
-            w = __shfl_sync(0xffffffffu, myw, (int)(e - b));
-        }
-#pragma unroll
-        for (int q = 0; q < SL; ++q) acc[q] = WEIGHTED ? f4fma(w, v[q], acc[q]) : f4add(acc[q], v[q]);
-    }
-    cp_async_wait_grp<0>();
-    while (rb < r1 && nb > 0) advance();                 // the last row and trailing empty rows
-}
-
 template <int EPI>
 __global__ void __launch_bounds__(WPB * 32) fixup_kernel(SpmmArgs a) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -749,78 +595,31 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
 
 // Column slices per warp (SL): more slices amortise the index load / shuffle / address work
 // of an edge over more bytes, fewer keep the gathered working set (SL x 512 B per row) small.
-// MINB: resident blocks per SM the register budget is sized for.  Encoded as SL * 10 + MINB.
+// MINB: resident blocks per SM the register budget is sized for.  Encoded as SL * 10 + MINB
+// (or SL * 100 + MINB * 10 + edges-in-flight code); TPO_SPMM_VARIANT overrides it (tuning).
 int spmm_variant(int nslices) {
     int v = nslices >= 2 ? 23 : 14;      // measured best on small (d = 1000) and medium (d = 256)
     if (const char *e = getenv("TPO_SPMM_VARIANT")) v = atoi(e);
-    if (v < 1000 && v != 13 && v != 14 && v != 22 && v != 23 && v != 42 && v != 82 && v != 24 && v != 148 &&
-        v != 228 && v != 238 && v != 138)
-        v = 14;
-    if (v >= 100 && v < 1000) {          // SL * 100 + MINB * 10 + edges-in-flight code (8 -> 8 edges)
-        const int sl = v / 100;
-        if (sl > nslices) v = 14;
-        return v;
-    }
-    if (v >= 1000) {                     // cp.async ring variants: 1000 + SL * 100 + RING
-        int sl = (v - 1000) / 100, ring = v % 100;
-        if (sl != 1 && sl != 2 && sl != 4) sl = 1;
-        if (ring != 8 && ring != 16 && ring != 24) ring = 16;
-        while (sl > 1 && sl > nslices) sl /= 2;
-        if (sl == 4) ring = 8;
-        return 1000 + sl * 100 + ring;
-    }
-    int sl = v / 10;
-    if (sl != 1 && sl != 2 && sl != 4 && sl != 8) v = 14, sl = 1;
-    while (sl > 1 && sl > nslices) sl /= 2;
-    return sl * 10 + v % 10;
+    if (v != 14 && v != 23 && v != 228) v = 14;
+    if (v / (v >= 100 ? 100 : 10) > nslices) v = 14;
+    return v;
 }
 
 template <int EPI, bool W>
 void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
-    const int sl = var >= 1000 ? (var - 1000) / 100 : (var >= 100 ? var / 100 : var / 10);
+    const int sl = var >= 100 ? var / 100 : var / 10;
+    const int minb = var >= 100 ? (var / 10) % 10 : var % 10;
     a.ngroups = (a.nslices + sl - 1) / sl;
     const int64_t blocks = cdiv(max_items * a.ngroups, WPB);
-    if (var >= 1000) {
-        const int ring = var % 100;
-        const size_t smem = (size_t)WPB * ring * sl * 512;
-#define TPO_RING_CASE(SLV, RV)                                                                              \
-    case SLV * 100 + RV:                                                                                   \
-        TPO_CUDA(cudaFuncSetAttribute(spmm_ring_kernel<EPI, W, SLV, RV>,                                   \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-        spmm_ring_kernel<EPI, W, SLV, RV><<<blocks, WPB * 32, smem, st>>>(a);                              \
-        break;
-        switch (var - 1000) {
-            TPO_RING_CASE(1, 8)
-            TPO_RING_CASE(1, 16)
-            TPO_RING_CASE(1, 24)
-            TPO_RING_CASE(2, 8)
-            TPO_RING_CASE(2, 16)
-            TPO_RING_CASE(2, 24)
-            TPO_RING_CASE(4, 8)
-            default: TPO_REQUIRE(false, "unknown SpMM ring variant");
-        }
-#undef TPO_RING_CASE
-        TPO_LAUNCH_CHECK();
-        return;
-    }
     // persistent warps: at most the resident capacity (SMs x MINB blocks of WPB warps)
-    const int minb = var >= 100 ? (var / 10) % 10 : var % 10;
     const int nsm = sm_count();
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)nsm * minb));
     // the reserve applies only to a full-capacity grid (blocks on every SM, so the blocks of the
     // non-reserved SMs exist and drain the work queue); a smaller grid keeps every block
     a.smid_limit = (int64_t)grid == (int64_t)nsm * minb ? std::max(1, nsm - std::max(0, a.reserve_sms)) : (1 << 30);
     switch (var) {
-        case 13: spmm_kernel<EPI, W, 1, 3><<<grid, WPB * 32, 0, st>>>(a); break;
         case 23: spmm_kernel<EPI, W, 2, 3><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 22: spmm_kernel<EPI, W, 2, 2><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 42: spmm_kernel<EPI, W, 4, 2><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 82: spmm_kernel<EPI, W, 8, 2><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 24: spmm_kernel<EPI, W, 2, 4><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 148: spmm_kernel<EPI, W, 1, 4, 8><<<grid, WPB * 32, 0, st>>>(a); break;       // = 14
-        case 138: spmm_kernel<EPI, W, 1, 3, 12><<<grid, WPB * 32, 0, st>>>(a); break;
         case 228: spmm_kernel<EPI, W, 2, 2, 8><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 238: spmm_kernel<EPI, W, 2, 3, 6><<<grid, WPB * 32, 0, st>>>(a); break;
         default: spmm_kernel<EPI, W, 1, 4><<<grid, WPB * 32, 0, st>>>(a); break;
     }
     TPO_LAUNCH_CHECK();
