@@ -291,7 +291,8 @@ int tpo_nci_phi(const double *sums, const double *counts, int32_t k, double *Phi
 
 /* ---------------------------------------------------------------------------------------
  * Whole hot path (Fig. overview): propagate -> Haar Q from G -> features ->
- * top-k (mode) -> cluster.  G: (host) d x d fp64.  Omega: D x (k+p) fp32 (HALKO only, else
+ * top-k (mode) -> cluster.  G: d x d fp64 on the DEVICE (the Gaussian input of Alg. 1 L6,
+ * resident like X; the Haar QR of Alg. 1 L7 runs inside the call, beside the propagation).  Omega: D x (k+p) fp32 (HALKO only, else
  * NULL).  labels: n int32 out.  timings_ms: (host) 4 doubles out {propagate, features,
  * topk, cluster} measured with CUDA events on `stream`, or NULL.
  * [sync].  Workspace: tpo_run_ws(n_u, n_v, nnz, d, k, mode, p).

@@ -12,6 +12,9 @@ serve to pin the C oracle:
 * ``best_partition``     brute force over all partitions into <= k clusters (n <= 10).
 * ``sin_theta``          robust sin of the largest principal angle.
 * ``ari``                adjusted Rand index for label comparisons.
+* ``halko_topk``         the randomised truncated SVD the paper cites for the top-k (Halko et
+                         al., p = 10, q = 2 at SPEC.md:143), replayed
+                         step by step with Householder QR (Halko mode).
 """
 from __future__ import annotations
 
@@ -140,3 +143,29 @@ def ari(a, b):
     if mx == exp:
         return 1.0
     return float((s_ij - exp) / (mx - exp))
+
+
+def sign_rule(Gm, Ps):
+    """R8: flip each pair so that sum_i Gamma[i, l] >= 0; when |sum| < 1e-6 ||.||_1 use
+    the sign of the largest-magnitude entry (smallest index among ties)."""
+    Gm, Ps = Gm.copy(), Ps.copy()
+    for l in range(Gm.shape[1]):
+        s, a = Gm[:, l].sum(), np.abs(Gm[:, l]).sum()
+        sg = (-1.0 if Gm[np.argmax(np.abs(Gm[:, l])), l] < 0 else 1.0) if abs(s) < 1e-6 * a else (-1.0 if s < 0 else 1.0)
+        Gm[:, l] *= sg
+        Ps[:, l] *= sg
+    return Gm, Ps
+
+
+def halko_topk(Rp, dinv, k, p, q, Omega):
+    """Randomised truncated SVD of R = diag(dinv) R' (Halko, Martinsson and Tropp):
+    Y = orth(R Omega) with Omega (D x (k+p)) given; q times Y = orth(R (R^T Y)); then the SVD
+    Y^T R = U S V^T gives Gamma = Y U[:, :k], sigma = S[:k], Psi = V[:, :k]; sign rule R8.
+    fp64 throughout, Householder QR (numpy/LAPACK) for orth.  Returns (Gamma, sigma, Psi)."""
+    R = np.asarray(dinv, np.float64)[:, None] * np.asarray(Rp, np.float64)
+    Y, _ = np.linalg.qr(R @ np.asarray(Omega, np.float64))
+    for _ in range(q):
+        Y, _ = np.linalg.qr(R @ (R.T @ Y))
+    U, S, Vt = np.linalg.svd(Y.T @ R, full_matrices=False)
+    Gm, Ps = sign_rule(Y @ U[:, :k], Vt[:k].T)
+    return Gm, S[:k].copy(), Ps

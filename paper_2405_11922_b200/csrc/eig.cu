@@ -9,6 +9,7 @@
 // HALKO mode: the randomised truncated SVD the paper cites, q power steps.
 // Both modes end with the sign rule R8.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -489,14 +490,20 @@ __global__ void scale_cols_kernel(const double *__restrict__ A, int64_t rows, in
 
 // Gamma = diag(dinv) R' Psi64 diag(1/sigma) in fp64, polished and sign-fixed, then rounded to
 // fp32; Psi (fp32 out) = Psi64.
+// Gamma_in (optional, n x k fp64): the left factor when the mode already has it (Halko: Y E_k);
+// otherwise Gamma = R Psi Sigma^{-1} (exact mode: the same factor, the block being full rank).
 void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
-                    const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st) {
-    double *sd = to_dev(ar, sig, st);
-    double *w = ar.take<double>((size_t)D * k);
-    scale_cols_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D, k, sd, w);
-    TPO_LAUNCH_CHECK();
-    double *G64 = ar.take<double>((size_t)n * k);
-    tsgemm_AW_f64(Rp, D, dinv, w, n, D, k, G64, k, st);
+                    const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st,
+                    double *Gamma_in = nullptr) {
+    double *G64 = Gamma_in;
+    if (!G64) {
+        double *sd = to_dev(ar, sig, st);
+        double *w = ar.take<double>((size_t)D * k);
+        scale_cols_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D, k, sd, w);
+        TPO_LAUNCH_CHECK();
+        G64 = ar.take<double>((size_t)n * k);
+        tsgemm_AW_f64(Rp, D, dinv, w, n, D, k, G64, k, st);
+    }
     cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
     TPO_LAUNCH_CHECK();
     polish_gamma(G64, n, k, ar, st);
@@ -518,8 +525,19 @@ __global__ void copy2d_kernel(const double *__restrict__ src, int64_t lds, doubl
 
 }  // namespace
 
+// panel width of the device Haar QR (<= 112, the one-CTA Cholesky-inverse limit);
+// TPO_HAAR_PANEL overrides (tuning)
+int64_t haar_panel(int64_t d) {
+    int64_t bw = 64;
+    if (const char *e = getenv("TPO_HAAR_PANEL")) {
+        const int64_t v = atoll(e);
+        if (v >= 16 && v <= 112) bw = v;
+    }
+    return std::min<int64_t>(bw, d);
+}
+
 size_t haar_q_ws_bytes(int64_t d) {
-    const int64_t bw = std::min<int64_t>(64, d);
+    const int64_t bw = std::min<int64_t>(112, d);
     return 2 * align_up(sizeof(double) * d * d) + 3 * align_up(sizeof(double) * d * bw) +
            2 * align_up(sizeof(double) * bw * bw + 8) + dgemm_ws(d, bw, d) + 8192;
 }
@@ -529,13 +547,14 @@ size_t haar_q_ws_bytes(int64_t d) {
 // panel orthonormalised by CholeskyQR2.  R is block upper triangular with upper triangular,
 // positive-diagonal blocks, so Q is the same unique factor the host routine returns.  No
 // host round trip until the final failure-flag check.
-void haar_q_device(const double *G_host, int64_t d, float *Q_out, Arena &ar, cudaStream_t st) {
-    const int64_t bw = std::min<int64_t>(64, d);
+void haar_q_device(const double *G, bool G_on_device, int64_t d, float *Q_out, Arena &ar, cudaStream_t st) {
+    const int64_t bw = haar_panel(d);
     double *A = ar.take<double>(d * d), *Q = ar.take<double>(d * d);
     double *P = ar.take<double>(d * bw), *T = ar.take<double>(d * bw), *Cm = ar.take<double>(d * bw);
     int *flag = ar.take<int>(1);
     TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    TPO_CUDA(cudaMemcpyAsync(A, G_host, sizeof(double) * d * d, cudaMemcpyHostToDevice, st));
+    TPO_CUDA(cudaMemcpyAsync(A, G, sizeof(double) * d * d, G_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             st));
     for (int64_t j0 = 0; j0 < d; j0 += bw) {
         const int64_t w = std::min<int64_t>(bw, d - j0);
         copy2d_kernel<<<cdiv(d * w, 256), 256, 0, st>>>(A + j0, d, P, w, d, w, nullptr, 0);
@@ -701,6 +720,7 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
                    cudaStream_t st, const double *r_colsum) {
     std::vector<double> lam;
     double *Psi64 = ar.take<double>(D * k);
+    double *halko_gamma = nullptr;              // Halko mode: Gamma = Y E_k
     if (mode == TPO_EIG_EXACT) {
         double *G = ar.take<double>(D * D);
         double *u = ar.take<double>(D);
@@ -755,14 +775,16 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
         for (int64_t a = 0; a < b; ++a)
             for (int l = 0; l < k; ++l) Ek[a * k + l] = E[a * b + l];
         double *ek = to_dev(ar, Ek, st);
-        // Psi = B E_k Sigma^{-1} (right singular vectors); Gamma follows from Psi below.
+        // Y^T R = U S V^T with U = E, S^2 = w: Psi = V_k = B E_k S_k^{-1} (right singular vectors),
+        // Gamma = Y U_k (left singular vectors of the rank-b approximation Y Y^T R, Halko et al.)
         tsgemm_AW_dd(Bm, b, ek, D, b, k, Psi64, k, st);
         std::vector<double> ps = to_host(Psi64, D * k, st);
         for (int64_t j = 0; j < D; ++j)
             for (int l = 0; l < k; ++l) ps[j * k + l] /= sqrt(std::max(w[l], 1e-300));
         TPO_CUDA(cudaMemcpyAsync(Psi64, ps.data(), sizeof(double) * D * k, cudaMemcpyHostToDevice, st));
+        halko_gamma = ar.take<double>(n * k);
+        dgemm(false, n, k, b, 1.0, Y, b, ek, k, 0.0, halko_gamma, k, ar, st);
         TPO_CUDA(cudaStreamSynchronize(st));
-        ar.off = mark;
     }
     std::vector<double> sig(k);
     for (int l = 0; l < k; ++l) {
@@ -770,7 +792,7 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
         if (!(sig[l] > 0.0)) throw Error(TPO_ENUMERIC, "top-k: sigma_k is zero (rank(R) < k)");
         sigma[l] = sig[l];
     }
-    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st);
+    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st, halko_gamma);
 }
 
 // a6: out = dinv . R' (R'^T (dinv . Y)), the D x b intermediate summed in fp64.

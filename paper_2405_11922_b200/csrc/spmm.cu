@@ -650,7 +650,8 @@ size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
 }
 
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
-                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms) {
+                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms,
+                    int reserve_launches) {
     const int64_t n = B.n_rows, m = B.n_cols, nnz = B.nnz;
     const int d4 = (int)(d / 4);
     const float c = alpha < 1.0f ? 1.0f - alpha : 1.0f;    // R1
@@ -693,7 +694,9 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
             a.rowptr = Bt.row_ptr; a.col = Bt.col_idx; a.val = Bt.val;
             a.src = (const float4 *)Z; a.d4 = d4; a.nslices = nslices;
             a.sch = sbt.s; a.n_rows = m; a.partials = (float4 *)partials;
-            a.scale = sv; a.out = (float4 *)Qv; a.work = counter(); a.reserve_sms = reserve_sms;
+            a.scale = sv; a.out = (float4 *)Qv;
+            a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
+            a.work = counter();
             spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
         } else {
             TPO_CUDA(cudaMemsetAsync(Qv, 0, 0, st));
@@ -703,7 +706,9 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
         a.src = (const float4 *)Qv; a.d4 = d4; a.nslices = nslices;
         a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
         a.scale = su; a.X = (const float4 *)X; a.c = c; a.alpha = alpha;
-        a.out = (float4 *)Z; a.work = counter(); a.reserve_sms = reserve_sms;
+        a.out = (float4 *)Z;
+        a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
+        a.work = counter();
         if (last) {
             a.out_hat = (nslices == 1 && Zhat) ? (float4 *)Zhat : nullptr;
             spmm_launch<EPI_FINAL>(a, sb.s.max_items, sb.s.max_slots, B.val != nullptr, st);

@@ -5,6 +5,9 @@
 #include <string>
 #include <vector>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "tpo_internal.cuh"
 
 namespace tpo {
@@ -185,7 +188,7 @@ int tpo_haar_q_dev(const double *G, int64_t d, float *Q, void *ws, size_t ws_byt
         check_ws(ws, ws_bytes, tpo_haar_q_dev_ws(d));
         Arena ar(ws, ws_bytes);
         cudaStream_t st = as_stream(stream);
-        haar_q_device(G, d, Q, ar, st);
+        haar_q_device(G, false, d, Q, ar, st);
         TPO_CUDA(cudaStreamSynchronize(st));
     });
 }
@@ -502,15 +505,23 @@ int tpo_nci_phi(const double *sums, const double *counts, int32_t k, double *Phi
     });
 }
 
-// SMs left to the Haar rotation while the (persistent) propagation kernels run beside it
-constexpr int kHaarReserveSms = 8;
+// SMs left to the Haar rotation while the first (persistent) propagation kernels run beside
+// it; TPO_HAAR_RESERVE="sms,launches" overrides (tuning)
+static void haar_reserve(int &sms, int &launches) {
+    sms = 8;
+    launches = 1 << 30;
+    if (const char *e = getenv("TPO_HAAR_RESERVE")) {
+        int a = 0, b = 0;
+        if (sscanf(e, "%d,%d", &a, &b) == 2 && a >= 0 && b >= 0) { sms = a; launches = b; }
+    }
+}
 
 int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T, int32_t k,
             const double *G, int32_t eig_mode, const float *Omega, int32_t p, int32_t q, int32_t Tf, int32_t Tg,
             int32_t *labels, double *timings_ms, void *ws, size_t ws_bytes, void *stream) {
     return guarded([&] {
         check_propagate(B, Bt, X, d, alpha, T, X, nullptr);
-        TPO_REQUIRE(G != nullptr, "G (host) is NULL");
+        check_ptr(G, "G");
         const int64_t n = B->n_rows, D = 2 * d;
         TPO_REQUIRE(n >= 1, "empty U side");
         TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= D, "k must lie in [1, min(n, 2d, 128)]");
@@ -548,12 +559,14 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
         cudaStream_t side = res.side;
         TPO_CUDA(cudaEventRecord(ev[0], st));
         TPO_CUDA(cudaEventRecord(fork, st));
-        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, kHaarReserveSms);
+        int res_sms = 0, res_launches = 0;
+        haar_reserve(res_sms, res_launches);
+        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, res_sms, res_launches);
         ar.off = mark;
         TPO_CUDA(cudaEventRecord(ev[1], st));
         // Alg. 1 L6-7 depends only on G: it runs on a side stream beside the propagation
         TPO_CUDA(cudaStreamWaitEvent(side, fork, 0));
-        haar_q_device(G, d, Qd, har, side);
+        haar_q_device(G, true, d, Qd, har, side);
         TPO_CUDA(cudaEventRecord(join, side));
         TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
         features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);

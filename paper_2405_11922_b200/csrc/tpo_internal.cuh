@@ -89,10 +89,11 @@ int sm_count();
 // ----------------------------------------------------------------------------------------
 // Module entry points (implemented in the .cu files; called by tpo_api.cu)
 // ----------------------------------------------------------------------------------------
-// reserve_sms: SMs' worth of block slots the persistent SpMM grids leave free (tpo_run keeps
-// a few for the Haar rotation running beside the propagation on a side stream).
+// reserve_sms: SMs the persistent SpMM grids of the first reserve_launches SpMM launches leave
+// free (tpo_run keeps some for the Haar rotation running beside the propagation on a side stream).
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
-                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms = 0);
+                    int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms = 0,
+                    int reserve_launches = 1 << 30);
 // sharded propagation pieces (spmm.cu)
 size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d);
 void shard_degrees_impl(const tpo_csr_t &Bp, const tpo_csr_t &Btp, double *deg_u, double *deg_v, cudaStream_t st);
@@ -115,7 +116,8 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
                   int32_t *iters_used, Arena &ar, cudaStream_t st);
 
-void haar_q_device(const double *G_host, int64_t d, float *Q_out, Arena &ar, cudaStream_t st);
+// G: d x d fp64, on the device when G_on_device, else host memory
+void haar_q_device(const double *G, bool G_on_device, int64_t d, float *Q_out, Arena &ar, cudaStream_t st);
 
 // Pieces of a5-a9 for the row-sharded solver (the caller all-reduces the
 // partials between them).  features.cu:

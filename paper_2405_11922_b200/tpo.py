@@ -202,13 +202,16 @@ class Runner:
         self.labels = torch.empty(g.n_u, dtype=torch.int32, device=device)
         self.timings = np.zeros(4, np.float64)
 
-    def __call__(self, X: torch.Tensor, alpha: float, T: int, G: np.ndarray, Tf: int = 5, Tg: int = 20,
+    def __call__(self, X: torch.Tensor, alpha: float, T: int, G, Tf: int = 5, Tg: int = 20,
                  q: int = 2, Omega: Optional[torch.Tensor] = None, stream=None):
+        """G: the d x d fp64 Gaussian of Alg. 1 L6, a device tensor (numpy arrays are uploaded)."""
         _need(X, torch.float32, "X", (self.g.n_u, self.d))
-        G = np.ascontiguousarray(G, dtype=np.float64)
+        if not isinstance(G, torch.Tensor):
+            G = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float64)).to(X.device)
+        _need(G, torch.float64, "G", (self.d, self.d))
         B, Bt = self.g.csr()
         check(lib().tpo_run(C.byref(B), C.byref(Bt), _ptr(X), self.d, float(alpha), int(T), int(self.k),
-                            G.ctypes.data_as(C.c_void_p), int(self.mode), _ptr(Omega), int(self.p), int(q), int(Tf),
+                            _ptr(G), int(self.mode), _ptr(Omega), int(self.p), int(q), int(Tf),
                             int(Tg), _ptr(self.labels), self.timings.ctypes.data_as(C.c_void_p), _ptr(self.ws),
                             self.ws.numel(), _stream(stream)))
         return self.labels

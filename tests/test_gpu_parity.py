@@ -241,6 +241,24 @@ def test_topk_planted_svd(tpo):
     assert DN.sin_theta(Ps.cpu().numpy(), V[:, :k]) <= 1e-4
 
 
+def test_topk_halko_mode_vs_oracle(tpo, tiny_feats):
+    """TPO_EIG_HALKO (the paper-cited rSVD, p = 10, q = 2) vs the same algorithm in the oracle with
+    the same Omega (same-algorithm parity; orth by CholeskyQR2 on the GPU,
+    Householder in the oracle -- the same subspaces)."""
+    g, Rp, dinv = tiny_feats
+    k, p, q = g.k, 10, 2
+    Om = np.random.default_rng(7).standard_normal((Rp.shape[1], k + p)).astype(np.float32)
+    Gmo, so, Pso = DN.halko_topk(Rp, dinv, k, p, q, Om)
+    Gm, s, Ps = tpo.topk_eig(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), k, mode=tpo.TPO_EIG_HALKO,
+                             p=p, q=q, Omega=torch.from_numpy(Om).cuda())
+    Gm, Ps = Gm.cpu().numpy(), Ps.cpu().numpy()
+    assert np.allclose(s, so, rtol=1e-5)
+    assert DN.sin_theta(Gm, Gmo) <= 1e-4
+    assert DN.sin_theta(Ps, Pso) <= 1e-4
+    assert np.max(np.abs(Gm.astype(np.float64).T @ Gm - np.eye(k))) <= 1e-6
+    assert np.all(Gm.astype(np.float64).sum(0) >= 0)
+
+
 # ------------------------------------------------------------------------------------------
 # a8-a9 discretisation
 # ------------------------------------------------------------------------------------------

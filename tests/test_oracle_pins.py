@@ -418,3 +418,45 @@ def test_end_to_end_tiny_planted():
     assert abs(res["sigma"][0] - 1.0) < 1e-6
     assert np.linalg.norm(res["Gamma"].T @ res["Gamma"] - np.eye(3)) < 1e-10
     assert DN.ari(res["labels"], g.truth) > 0.5
+
+
+# ------------------------------------------------------------------------------------------
+# Halko mode oracle (oracle/dense.halko_topk): the randomised truncated SVD PAPER.md:574 cites
+# ------------------------------------------------------------------------------------------
+
+def _planted_svd(n, D, sig, seed):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, D)))
+    V, _ = np.linalg.qr(rng.standard_normal((D, D)))
+    return U, V, (U * sig) @ V.T
+
+
+def test_halko_exact_when_rank_fits_the_block():
+    """rank(R) <= b = k + p: range(R Omega) = range(R), so the rSVD is the exact SVD (textbook
+    property of the range finder) -- pins Gamma = Y U, Psi = V, sigma = S."""
+    n, D, k, p = 400, 30, 4, 6
+    sig = np.concatenate([np.geomspace(4.0, 0.5, 8), np.zeros(D - 8)])     # rank 8 <= b = 10
+    U, V, Rp = _planted_svd(n, D, sig, 1)
+    Om = np.random.default_rng(2).standard_normal((D, k + p))
+    Gm, s, Ps = DN.halko_topk(Rp, np.ones(n), k, p, 0, Om)
+    assert np.allclose(s, sig[:k], rtol=1e-12)
+    assert DN.sin_theta(Gm, U[:, :k]) < 1e-10 and DN.sin_theta(Ps, V[:, :k]) < 1e-10
+    assert np.all(Gm.sum(0) >= 0)                                          # R8
+    assert np.allclose(Gm * s, (Rp @ Ps), atol=1e-10)                      # R Psi = Gamma Sigma
+
+
+def test_halko_power_iterations_converge_to_the_exact_top_k():
+    """Full-rank R with a gap after k: q power steps drive sin(theta) to the exact top-k down by
+    (sigma_{b+1} / sigma_k)^{2q+1} (Halko et al., Thm. 9.1 flavour); at q = 6 it is exact to 1e-8."""
+    n, D, k, p = 500, 60, 5, 5
+    sig = np.concatenate([np.linspace(3.0, 2.0, k), np.geomspace(0.5, 0.01, D - k)])
+    U, V, Rp = _planted_svd(n, D, sig, 3)
+    Om = np.random.default_rng(4).standard_normal((D, k + p))
+    errs = []
+    for q in (0, 1, 2, 6):
+        Gm, s, Ps = DN.halko_topk(Rp, np.ones(n), k, p, q, Om)
+        errs.append(DN.sin_theta(Ps, V[:, :k]))
+    assert errs[0] > errs[1] > errs[2] > errs[3]
+    assert errs[3] < 1e-8
+    Gm, s, _ = DN.halko_topk(Rp, np.ones(n), k, p, 6, Om)
+    assert np.allclose(s, sig[:k], rtol=1e-10)
