@@ -390,29 +390,39 @@ constexpr uint32_t idesc_tf32_kmajor(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Persistent: grid = min(tiles, SMs); a CTA walks the 128 x 128 output tiles t = blockIdx.x +
+// i * gridDim.x (row tile = t / ncol, so the concurrently running CTAs share A row tiles in
+// L2).  Two TMEM accumulators (2 x 128 columns): the MMA warp fills buffer i & 1 while the four
+// epilogue warps drain the other one (sincos + stores), so the epilogue overlaps the MMAs.
+// Barriers: full[s] / empty[s] per smem stage (TMA <-> MMA), tfull[a] (MMA commit -> epilogue),
+// tempty[a] (4 epilogue warps -> MMA).
 __global__ void __launch_bounds__(FT_THREADS, 1)
 features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_constant__ CUtensorMap mz_lo,
                    const __grid_constant__ CUtensorMap mq_hi, const __grid_constant__ CUtensorMap mq_lo, int64_t n,
                    int d, float *__restrict__ Rp) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + FT_STAGES * FT_STAGE);   // full[S], empty[S], tfull
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * FT_STAGES + 1);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + FT_STAGES * FT_STAGE);   // full[S], empty[S], tfull[2], tempty[2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * FT_STAGES + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t i0 = (int64_t)blockIdx.x * FT_M;
-    const int j0 = blockIdx.y * FT_N;
     const int nkb = (d + FT_KB - 1) / FT_KB;
+    const int ncol = (d + FT_N - 1) / FT_N;
+    const int64_t nrow = (n + FT_M - 1) / FT_M;
+    const int64_t ntiles = nrow * ncol;
     if (threadIdx.x == 0) {
         for (int s = 0; s < FT_STAGES; ++s) {
             mbar_init(smem_u32(&bars[s]), 1);
             mbar_init(smem_u32(&bars[FT_STAGES + s]), 1);
         }
-        mbar_init(smem_u32(&bars[2 * FT_STAGES]), 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(smem_u32(&bars[2 * FT_STAGES + a]), 1);
+            mbar_init(smem_u32(&bars[2 * FT_STAGES + 2 + a]), 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(FT_N)
+                     "r"(2 * FT_N)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -422,85 +432,112 @@ features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_const
     const uint32_t tmem_base = *tmem_slot;
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % FT_STAGES, j = kb / FT_STAGES;
-                if (j > 0) mbar_wait(smem_u32(&bars[FT_STAGES + s]), (j - 1) & 1);
-                const uint32_t full = smem_u32(&bars[s]);
-                mbar_expect_tx(full, FT_STAGE);
-                const uint32_t base = smem_u32(smem + s * FT_STAGE);
-                tma_load_2d(base + 0 * FT_OPER, &mz_hi, full, kb * FT_KB, (int)i0);
-                tma_load_2d(base + 1 * FT_OPER, &mz_lo, full, kb * FT_KB, (int)i0);
-                tma_load_2d(base + 2 * FT_OPER, &mq_hi, full, kb * FT_KB, j0);
-                tma_load_2d(base + 3 * FT_OPER, &mq_lo, full, kb * FT_KB, j0);
+            int64_t g = 0;                                   // k-blocks issued by this CTA
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t i0 = (t / ncol) * FT_M;
+                const int j0 = (int)(t % ncol) * FT_N;
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = (int)(g % FT_STAGES);
+                    const int64_t j = g / FT_STAGES;
+                    if (j > 0) mbar_wait(smem_u32(&bars[FT_STAGES + s]), (uint32_t)((j - 1) & 1));
+                    const uint32_t full = smem_u32(&bars[s]);
+                    mbar_expect_tx(full, FT_STAGE);
+                    const uint32_t base = smem_u32(smem + s * FT_STAGE);
+                    tma_load_2d(base + 0 * FT_OPER, &mz_hi, full, kb * FT_KB, (int)i0);
+                    tma_load_2d(base + 1 * FT_OPER, &mz_lo, full, kb * FT_KB, (int)i0);
+                    tma_load_2d(base + 2 * FT_OPER, &mq_hi, full, kb * FT_KB, j0);
+                    tma_load_2d(base + 3 * FT_OPER, &mq_lo, full, kb * FT_KB, j0);
+                }
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t idesc = idesc_tf32_kmajor(FT_M, FT_N);
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % FT_STAGES, j = kb / FT_STAGES;
-            mbar_wait(smem_u32(&bars[s]), j & 1);
-            fence_after();
-            if (lane == 0) {
-                const uint32_t base = smem_u32(smem + s * FT_STAGE);
-#pragma unroll
-                for (int kk = 0; kk < FT_KB / 8; ++kk) {
-                    const uint32_t off = kk * 32;        // 8 fp32 of K inside the 128-byte atom
-                    const uint64_t ah = umma_desc_kmajor(base + off), al = umma_desc_kmajor(base + FT_OPER + off);
-                    const uint64_t bh = umma_desc_kmajor(base + 2 * FT_OPER + off);
-                    const uint64_t bl = umma_desc_kmajor(base + 3 * FT_OPER + off);
-                    mma_tf32(tmem_base, al, bh, idesc, (kb | kk) ? 1u : 0u);
-                    mma_tf32(tmem_base, ah, bl, idesc, 1u);
-                    mma_tf32(tmem_base, ah, bh, idesc, 1u);
-                }
-                mma_commit(smem_u32(&bars[FT_STAGES + s]));
-                if (kb == nkb - 1) mma_commit(smem_u32(&bars[2 * FT_STAGES]));
+        int64_t g = 0;
+        int i = 0;                                           // tiles of this CTA
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int a = i & 1;
+            if (i >= 2) {                                    // the epilogue drained this buffer (tile i - 2)
+                mbar_wait(smem_u32(&bars[2 * FT_STAGES + 2 + a]), (uint32_t)(((i >> 1) - 1) & 1));
+                fence_after();
             }
-            __syncwarp();
+            const uint32_t acc = tmem_base + (uint32_t)(a * FT_N);
+            for (int kb = 0; kb < nkb; ++kb, ++g) {
+                const int s = (int)(g % FT_STAGES);
+                const int64_t j = g / FT_STAGES;
+                mbar_wait(smem_u32(&bars[s]), (uint32_t)(j & 1));
+                fence_after();
+                if (lane == 0) {
+                    const uint32_t base = smem_u32(smem + s * FT_STAGE);
+#pragma unroll
+                    for (int kk = 0; kk < FT_KB / 8; ++kk) {
+                        const uint32_t off = kk * 32;        // 8 fp32 of K inside the 128-byte atom
+                        const uint64_t ah = umma_desc_kmajor(base + off), al = umma_desc_kmajor(base + FT_OPER + off);
+                        const uint64_t bh = umma_desc_kmajor(base + 2 * FT_OPER + off);
+                        const uint64_t bl = umma_desc_kmajor(base + 3 * FT_OPER + off);
+                        mma_tf32(acc, al, bh, idesc, (kb | kk) ? 1u : 0u);
+                        mma_tf32(acc, ah, bl, idesc, 1u);
+                        mma_tf32(acc, ah, bh, idesc, 1u);
+                    }
+                    mma_commit(smem_u32(&bars[FT_STAGES + s]));
+                    if (kb == nkb - 1) mma_commit(smem_u32(&bars[2 * FT_STAGES + a]));
+                }
+                __syncwarp();
+            }
         }
     } else {
         const int q = warp & 3;
-        mbar_wait(smem_u32(&bars[2 * FT_STAGES]), 0);
-        fence_after();
-        const int64_t row = i0 + 32 * q + lane;
         const float sd = sqrtf((float)d);
         const float amp = (float)sqrt(exp(1.0) / (double)d);
         const int64_t D = 2 * (int64_t)d;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int a = i & 1;
+            const int64_t i0 = (t / ncol) * FT_M;
+            const int j0 = (int)(t % ncol) * FT_N;
+            mbar_wait(smem_u32(&bars[2 * FT_STAGES + a]), (uint32_t)((i >> 1) & 1));
+            fence_after();
+            const int64_t row = i0 + 32 * q + lane;
 #pragma unroll 1
-        for (int c = 0; c < FT_N / 32; ++c) {
-            float v[32];
-            tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + 32 * c, v);
-            const int jb = j0 + 32 * c;
-            if (row >= n) continue;
-            float *ps = Rp + row * D + jb, *pc = Rp + row * D + d + jb;
-            if (jb + 32 <= d) {
+            for (int c = 0; c < FT_N / 32; ++c) {
+                float v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * FT_N) + 32 * c, v);
+                const int jb = j0 + 32 * c;
+                if (row >= n) continue;
+                float *ps = Rp + row * D + jb, *pc = Rp + row * D + d + jb;
+                if (jb + 32 <= d) {
 #pragma unroll
-                for (int t = 0; t < 32; t += 4) {
-                    float s0, c0, s1, c1, s2, c2, s3, c3;
-                    sincosf(sd * v[t], &s0, &c0);
-                    sincosf(sd * v[t + 1], &s1, &c1);
-                    sincosf(sd * v[t + 2], &s2, &c2);
-                    sincosf(sd * v[t + 3], &s3, &c3);
-                    *reinterpret_cast<float4 *>(ps + t) = make_float4(amp * s0, amp * s1, amp * s2, amp * s3);
-                    *reinterpret_cast<float4 *>(pc + t) = make_float4(amp * c0, amp * c1, amp * c2, amp * c3);
-                }
-            } else {
+                    for (int tt = 0; tt < 32; tt += 4) {
+                        float s0, c0, s1, c1, s2, c2, s3, c3;
+                        sincosf(sd * v[tt], &s0, &c0);
+                        sincosf(sd * v[tt + 1], &s1, &c1);
+                        sincosf(sd * v[tt + 2], &s2, &c2);
+                        sincosf(sd * v[tt + 3], &s3, &c3);
+                        *reinterpret_cast<float4 *>(ps + tt) = make_float4(amp * s0, amp * s1, amp * s2, amp * s3);
+                        *reinterpret_cast<float4 *>(pc + tt) = make_float4(amp * c0, amp * c1, amp * c2, amp * c3);
+                    }
+                } else {
 #pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    if (jb + t < d) {
-                        float sn, cs;
-                        sincosf(sd * v[t], &sn, &cs);
-                        ps[t] = amp * sn;
-                        pc[t] = amp * cs;
+                    for (int tt = 0; tt < 32; ++tt) {
+                        if (jb + tt < d) {
+                            float sn, cs;
+                            sincosf(sd * v[tt], &sn, &cs);
+                            ps[tt] = amp * sn;
+                            pc[tt] = amp * cs;
+                        }
                     }
                 }
             }
+            fence_before();                                  // TMEM reads done before the MMA reuses it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars[2 * FT_STAGES + 2 + a]));
         }
     }
     fence_before();
     __syncthreads();
     if (warp == 1) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(FT_N) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * FT_N)
+                     : "memory");
     }
 }
 
@@ -558,7 +595,8 @@ void features_tc(const float *Zhat, int64_t n, int64_t d, const float *Q, float 
     std::call_once(once, [&] {
         cudaFuncSetAttribute(features_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
-    const dim3 grid(cdiv(n, FT_M), cdiv(d, FT_N));
+    const int64_t tiles = cdiv(n, FT_M) * cdiv(d, FT_N);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count()));
     features_tc_kernel<<<grid, FT_THREADS, smem, st>>>(a_hi, a_lo, b_hi, b_lo, n, (int)d, Rp);
     TPO_LAUNCH_CHECK();
 }

@@ -508,7 +508,7 @@ int tpo_nci_phi(const double *sums, const double *counts, int32_t k, double *Phi
 // SMs left to the Haar rotation while the first (persistent) propagation kernels run beside
 // it; TPO_HAAR_RESERVE="sms,launches" overrides (tuning)
 static void haar_reserve(int &sms, int &launches) {
-    sms = 8;
+    sms = 16;
     launches = 1 << 30;
     if (const char *e = getenv("TPO_HAAR_RESERVE")) {
         int a = 0, b = 0;
