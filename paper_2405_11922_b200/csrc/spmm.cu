@@ -234,12 +234,31 @@ struct SpmmArgs {
     int smid_limit;           // = SMs - reserve_sms, set at launch
 };
 
+// Packed fp32x2 arithmetic (FADD2 / FFMA2 on sm_100a): two lanes of a float4 per instruction,
+// each lane rounded exactly as the scalar operation.
+__device__ __forceinline__ unsigned long long pk(float x, float y) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ void upk(unsigned long long r, float &x, float &y) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
 __device__ __forceinline__ float4 f4fma(float w, float4 v, float4 a) {
-    a.x = fmaf(w, v.x, a.x); a.y = fmaf(w, v.y, a.y); a.z = fmaf(w, v.z, a.z); a.w = fmaf(w, v.w, a.w);
+    const unsigned long long ww = pk(w, w);
+    unsigned long long lo = pk(a.x, a.y), hi = pk(a.z, a.w);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(lo) : "l"(ww), "l"(pk(v.x, v.y)));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(hi) : "l"(ww), "l"(pk(v.z, v.w)));
+    upk(lo, a.x, a.y);
+    upk(hi, a.z, a.w);
     return a;
 }
 __device__ __forceinline__ float4 f4add(float4 a, float4 v) {
-    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    unsigned long long lo = pk(a.x, a.y), hi = pk(a.z, a.w);
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(lo) : "l"(pk(v.x, v.y)));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(hi) : "l"(pk(v.z, v.w)));
+    upk(lo, a.x, a.y);
+    upk(hi, a.z, a.w);
     return a;
 }
 
@@ -267,6 +286,12 @@ __device__ __forceinline__ float4 gather_ld(const float4 *p) {
     return __ldg(p);
 #endif
 }
+// base + ro float4 in one IMAD.WIDE.U32
+__device__ __forceinline__ const float4 *row_addr(const float4 *base, uint32_t ro) {
+    const float4 *p;
+    asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(p) : "r"(ro), "l"(base));
+    return p;
+}
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) {
 #if TPO_L2_HINTS
     __stcs(p, v);
@@ -275,42 +300,35 @@ __device__ __forceinline__ void st_stream(float4 *p, float4 v) {
 #endif
 }
 
+// Loads are unconditional: lanes past the end of an edge batch hold a valid (clamped) column
+// and inactive column lanes read a clamped in-range address (`base`); neither is accumulated
+// or stored.  Row offsets col * d4 are 32-bit (every gathered table has < 2^31 float4).
 template <bool WEIGHTED, int SL, int UE>
-__device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, const int (&c4)[SL],
-                                            const bool (&act)[SL], float4 (&acc)[SL]) {
+__device__ __forceinline__ void gather_rows(const SpmmArgs &a, int64_t beg, int64_t end, const float4 *const (&base)[SL],
+                                            float4 (&acc)[SL]) {
     const int lane = threadIdx.x & 31;
     constexpr int U = UE;
 #pragma unroll
     for (int s = 0; s < SL; ++s) acc[s] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int64_t d4 = a.d4;
+    const uint32_t d4 = (uint32_t)a.d4;
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
         const int cnt = (int)(end - e0 < 32 ? end - e0 : 32);
-        const int mycol = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
-        float myw = 1.f;
-        if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
-        int j = 0;
-        for (; j + U <= cnt; j += U) {
+        const uint32_t myoff = (uint32_t)__ldg(a.col + e0 + (lane < cnt ? lane : 0)) * d4;
+        // weight 0 past the batch end (the clamped row is read but adds +0)
+        const float myw = lane < cnt ? (WEIGHTED ? __ldg(a.val + e0 + lane) : 1.f) : 0.f;
+        for (int j = 0; j < cnt; j += U) {
             float4 v[U][SL];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, j + u) * d4;
+                const uint32_t ro = __shfl_sync(0xffffffffu, myoff, j + u);
 #pragma unroll
-                for (int s = 0; s < SL; ++s) v[u][s] = act[s] ? gather_ld(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int s = 0; s < SL; ++s) v[u][s] = gather_ld(row_addr(base[s], ro));
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, j + u) : 1.f;
+                const float w = __shfl_sync(0xffffffffu, myw, j + u);
 #pragma unroll
-                for (int s = 0; s < SL; ++s) acc[s] = WEIGHTED ? f4fma(w, v[u][s], acc[s]) : f4add(acc[s], v[u][s]);
-            }
-        }
-        for (; j < cnt; ++j) {
-            const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, j) * d4;
-            const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, j) : 1.f;
-#pragma unroll
-            for (int s = 0; s < SL; ++s) {
-                const float4 v = act[s] ? gather_ld(a.src + c4[s] + ro) : make_float4(0.f, 0.f, 0.f, 0.f);
-                acc[s] = WEIGHTED ? f4fma(w, v, acc[s]) : f4add(acc[s], v);
+                for (int s = 0; s < SL; ++s) acc[s] = f4fma(w, v[u][s], acc[s]);
             }
         }
     }
@@ -386,41 +404,41 @@ __device__ __forceinline__ void load_x_sl(const SpmmArgs &a, int64_t row, const 
 // each row through the epilogue as the stream crosses its end; empty rows are flushed with 0.
 template <int EPI, bool WEIGHTED, int SL, int UE>
 __device__ __forceinline__ void process_row_block(const SpmmArgs &a, int64_t r0, int64_t r1, const int (&c4)[SL],
-                                                  const bool (&act)[SL]) {
+                                                  const bool (&act)[SL], const float4 *const (&base)[SL]) {
     const int lane = threadIdx.x & 31;
     constexpr int U = UE;
-    const int64_t d4 = a.d4;
+    const uint32_t d4 = (uint32_t)a.d4;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t rb = r0; rb < r1; rb += 32) {
         const int nb = (int)(r1 - rb < 32 ? r1 - rb : 32);
-        const int64_t my_end = lane < nb ? a.rowptr[rb + 1 + lane] : 0;     // end of row rb + lane
-        const float my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
         const int64_t e_beg = a.rowptr[rb];
-        const int64_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+        // edge positions relative to e_beg (a batch of <= 32 short rows has <= 32 * CHUNK edges)
+        const int my_end = lane < nb ? (int)(a.rowptr[rb + 1 + lane] - e_beg) : 0;   // end of row rb + lane
+        const float my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
+        const int n_e = __shfl_sync(0xffffffffu, my_end, nb - 1);
         int cur = 0;
-        int64_t cur_end = __shfl_sync(0xffffffffu, my_end, 0);
+        int cur_end = __shfl_sync(0xffffffffu, my_end, 0);
         float4 xcur[SL], acc[SL];
         load_x_sl<EPI, SL>(a, rb, c4, act, xcur);
 #pragma unroll
         for (int q = 0; q < SL; ++q) acc[q] = zero;
-        for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
-            const int cnt = (int)(e_end - e0 < 32 ? e_end - e0 : 32);
-            const int mycol = lane < cnt ? __ldg(a.col + e0 + lane) : 0;
+        for (int k0 = 0; k0 < n_e; k0 += 32) {
+            const int cnt = n_e - k0 < 32 ? n_e - k0 : 32;
+            const uint32_t myoff = (uint32_t)__ldg(a.col + e_beg + k0 + (lane < cnt ? lane : 0)) * d4;
             float myw = 1.f;
-            if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e0 + lane) : 0.f;
+            if (WEIGHTED) myw = lane < cnt ? __ldg(a.val + e_beg + k0 + lane) : 0.f;
             for (int j = 0; j < cnt; j += U) {
                 float4 v[U][SL];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int jj = j + u < 31 ? j + u : 31;
-                    const int64_t ro = (int64_t)__shfl_sync(0xffffffffu, mycol, jj) * d4;
+                    const uint32_t ro = __shfl_sync(0xffffffffu, myoff, j + u);
 #pragma unroll
-                    for (int q = 0; q < SL; ++q) v[u][q] = (act[q] && j + u < cnt) ? gather_ld(a.src + c4[q] + ro) : zero;
+                    for (int q = 0; q < SL; ++q) v[u][q] = gather_ld(row_addr(base[q], ro));
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     if (j + u >= cnt) break;
-                    const int64_t e = e0 + j + u;
+                    const int e = k0 + j + u;
                     while (e >= cur_end) {               // warp-uniform: flush finished rows
                         epilogue_sl<EPI, SL>(a, rb + cur, c4, act, acc, xcur, __shfl_sync(0xffffffffu, my_s, cur));
 #pragma unroll
@@ -452,21 +470,23 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, int grp, int64_t it
     const int4 it = a.sch.items[item];
     int c4[SL];
     bool act[SL];
+    const float4 *base[SL];
 #pragma unroll
     for (int q = 0; q < SL; ++q) {
         c4[q] = (grp * SL + q) * 32 + lane;
         act[q] = c4[q] < a.d4;
+        base[q] = a.src + (act[q] ? c4[q] : a.d4 - 1);
     }
     if (it.w == 0) {                                     // row block
         const int64_t r1 = item + 1 < n_items ? (int64_t)a.sch.items[item + 1].x : a.n_rows;
-        process_row_block<EPI, WEIGHTED, SL, UE>(a, it.x, r1, c4, act);
+        process_row_block<EPI, WEIGHTED, SL, UE>(a, it.x, r1, c4, act, base);
         return;
     }
     const int64_t rb = a.rowptr[it.x], re = a.rowptr[it.x + 1];   // chunk of a long row
     const int64_t beg = rb + (int64_t)it.y * CHUNK;
     const int64_t end = min(re, beg + CHUNK);
     float4 acc[SL];
-    gather_rows<WEIGHTED, SL, UE>(a, beg, end, c4, act, acc);
+    gather_rows<WEIGHTED, SL, UE>(a, beg, end, base, acc);
 #pragma unroll
     for (int q = 0; q < SL; ++q)
         if (act[q]) a.partials[(int64_t)it.z * a.d4 + c4[q]] = acc[q];
