@@ -65,16 +65,18 @@ constexpr int UR = 8;     // rows per warp per pass (ups_update_kernel)
 
 __global__ void __launch_bounds__(256) ups_update_kernel(double *__restrict__ U, const double *__restrict__ RH,
                                                          const double *__restrict__ M, int64_t n, int k) {
-    extern __shared__ __align__(16) double msh[];    // [k * k] then rowbuf [8][UR][k]
-    double *rowbuf_all = msh + k * k;
+    extern __shared__ __align__(16) double msh[];    // [k * k] then rowbuf [8][k][UR] (rows innermost)
+    double *rowbuf_all = msh + ((k * k + 1) & ~1);   // 16-byte aligned row buffers
     for (int i = threadIdx.x; i < k * k; i += blockDim.x) msh[i] = M[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int64_t r0 = ((int64_t)blockIdx.x * 8 + w) * UR; r0 < n; r0 += (int64_t)gridDim.x * 8 * UR) {
         const int nr = (int)(n - r0 < UR ? n - r0 : UR);
         double *ubw = rowbuf_all + (size_t)w * UR * k;
-        for (int r = 0; r < UR; ++r)
-            for (int l = lane; l < k; l += 32) ubw[r * k + l] = r < nr ? U[(r0 + r) * k + l] : 0.0;
+        for (int e = lane; e < UR * k; e += 32) {        // coalesced read of the UR rows, stored [a][r]
+            const int r = e / k, a = e - r * k;
+            ubw[a * UR + r] = r < nr ? U[r0 * k + e] : 0.0;
+        }
         __syncwarp();
         for (int l = lane; l < k; l += 32) {
             double sv[UR];
@@ -82,16 +84,23 @@ __global__ void __launch_bounds__(256) ups_update_kernel(double *__restrict__ U,
             for (int r = 0; r < UR; ++r) sv[r] = 0.0;
             for (int a = 0; a < k; ++a) {
                 const double m = msh[a * k + l];
+                double uv[UR];
 #pragma unroll
-                for (int r = 0; r < UR; ++r) sv[r] = __dadd_rn(sv[r], __dmul_rn(ubw[r * k + a], m));
+                for (int r = 0; r < UR; r += 2) {
+                    const double2 v2 = *reinterpret_cast<const double2 *>(ubw + a * UR + r);
+                    uv[r] = v2.x;
+                    uv[r + 1] = v2.y;
+                }
+#pragma unroll
+                for (int r = 0; r < UR; ++r) sv[r] = fma(uv[r], m, sv[r]);
             }
 #pragma unroll
             for (int r = 0; r < UR; ++r) {
                 if (r >= nr) continue;
                 const double rv = RH[(r0 + r) * k + l];
                 const double num = rv > 0.0 ? rv : 0.0;
-                const double den = __dadd_rn(sv[r] > 0.0 ? sv[r] : 0.0, EPS);
-                U[(r0 + r) * k + l] = __dmul_rn(ubw[r * k + l], sqrt(num / den));
+                const double den = (sv[r] > 0.0 ? sv[r] : 0.0) + EPS;
+                U[(r0 + r) * k + l] = ubw[l * UR + r] * sqrt(num / den);
             }
         }
         __syncwarp();
@@ -99,7 +108,8 @@ __global__ void __launch_bounds__(256) ups_update_kernel(double *__restrict__ U,
 }
 
 // The same update, thread per row with the old row in registers (k <= KM <= 64) and M read
-// as shared-memory broadcasts; per (row, l) the same operation order as ups_update_kernel.
+// as shared-memory broadcasts; per (row, l) the same operation order (fma chain over a) as
+// ups_update_kernel.
 template <int KM>
 __global__ void __launch_bounds__(256) ups_update_reg_kernel(double *__restrict__ U, const double *__restrict__ RH,
                                                              const double *__restrict__ M, int64_t n, int k) {
@@ -117,8 +127,8 @@ __global__ void __launch_bounds__(256) ups_update_reg_kernel(double *__restrict_
 #pragma unroll
         for (int a = 0; a < KM; ++a)
             if (a < k) {
-                s0 = __dadd_rn(s0, __dmul_rn(u[a], msh[a * k + l]));
-                s1 = __dadd_rn(s1, __dmul_rn(u[a], msh[a * k + l + 1]));
+                s0 = fma(u[a], msh[a * k + l], s0);
+                s1 = fma(u[a], msh[a * k + l + 1], s1);
             }
         const double r0 = RH[row * k + l], r1 = RH[row * k + l + 1];
         U[row * k + l] = __dmul_rn(u_at(u, l), sqrt((r0 > 0.0 ? r0 : 0.0) / __dadd_rn(s0 > 0.0 ? s0 : 0.0, EPS)));
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(256) ups_update_reg_kernel(double *__restrict_
         double s0 = 0.0;
 #pragma unroll
         for (int a = 0; a < KM; ++a)
-            if (a < k) s0 = __dadd_rn(s0, __dmul_rn(u[a], msh[a * k + l]));
+            if (a < k) s0 = fma(u[a], msh[a * k + l], s0);
         const double r0 = RH[row * k + l];
         U[row * k + l] = __dmul_rn(u_at(u, l), sqrt((r0 > 0.0 ? r0 : 0.0) / __dadd_rn(s0 > 0.0 ? s0 : 0.0, EPS)));
     }
@@ -444,7 +454,7 @@ void onmf_u_update(double *U, const double *RH, const double *M, int64_t n, int 
     if (k <= 16) {
         ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
     } else {
-        const size_t ups_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * UR * k);
+        const size_t ups_smem = sizeof(double) * ((size_t)k * k + 1 + (size_t)8 * UR * k);
         TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
         ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * UR), 148 * 8), 256, ups_smem, st>>>(U, RH, M, n, k);
     }
@@ -564,7 +574,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const int64_t mx = std::max(n, D) * k;
     init_factors_kernel<<<cdiv(mx, 256), 256, 0, st>>>(Gamma, n, Psi, sig, D, k, U, H);
     TPO_LAUNCH_CHECK();
-    const size_t ups_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * UR * k);
+    const size_t ups_smem = sizeof(double) * ((size_t)k * k + 1 + (size_t)8 * UR * k);
     TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
     for (int t = 0; t < Tf; ++t) {
         onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
