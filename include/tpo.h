@@ -304,6 +304,20 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
             int32_t p, int32_t q, int32_t Tf, int32_t Tg, int32_t *labels,
             double *timings_ms, void *ws, size_t ws_bytes, void *stream);
 
+/* The same path end to end from HOST inputs: B, Bt (row_ptr, col_idx, val), X and G are host
+ * pointers (pinned memory lets the copies run asynchronously), labels a host int32 array of
+ * n_u.  Inside the call the inputs are copied to device buffers carved from the workspace --
+ * G first, on the Haar side stream, so the Haar QR of Alg. 1 L7 runs while the CSRs and X
+ * are still being copied (no SMs are held back for it) -- then the path runs as tpo_run and the
+ * labels are copied back.  Omega (HALKO only) stays a device pointer.  timings_ms[0] includes
+ * the input copies.  [sync].  Workspace: tpo_run_host_ws(..., weighted = B->val != NULL). */
+size_t tpo_run_host_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, int32_t mode,
+                       int32_t p, int32_t weighted);
+int tpo_run_host(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha,
+                 int32_t T, int32_t k, const double *G, int32_t eig_mode, const float *Omega,
+                 int32_t p, int32_t q, int32_t Tf, int32_t Tg, int32_t *labels,
+                 double *timings_ms, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

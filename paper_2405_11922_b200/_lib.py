@@ -19,7 +19,7 @@ SYMBOLS = [
     "tpo_affinity_matvec_ws", "tpo_affinity_matvec",
     "tpo_gram_ws", "tpo_gram", "tpo_topk_eig_ws", "tpo_topk_eig",
     "tpo_cluster_ws", "tpo_cluster",
-    "tpo_run_ws", "tpo_run",
+    "tpo_run_ws", "tpo_run", "tpo_run_host_ws", "tpo_run_host",
     "tpo_shard_solver_ws", "tpo_shard_features", "tpo_shard_dinv", "tpo_eig_from_gram", "tpo_shard_gamma",
     "tpo_shard_atb64", "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final",
     "tpo_shard_onmf_init", "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh",
@@ -90,6 +90,9 @@ def lib():
     L.tpo_run_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32]
     L.tpo_run_ws.restype = sz
     L.tpo_run.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+    L.tpo_run_host_ws.argtypes = [i64, i64, i64, i64, i32, i32, i32, i32]
+    L.tpo_run_host_ws.restype = sz
+    L.tpo_run_host.argtypes = [P, P, vp, i64, f32, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp, sz, vp]
     L.tpo_shard_solver_ws.argtypes = [i64, i64, i32]
     L.tpo_shard_solver_ws.restype = sz
     L.tpo_shard_features.argtypes = [vp, i64, i64, vp, vp, vp, vp, sz, vp]
@@ -114,7 +117,7 @@ def lib():
         getattr(L, name).restype = C.c_int
     for name in ["tpo_propagate", "tpo_shard_degrees", "tpo_shard_start", "tpo_shard_vside", "tpo_shard_vscale",
                  "tpo_shard_uside", "tpo_haar_q", "tpo_haar_q_dev", "tpo_features", "tpo_affinity_matvec", "tpo_gram", "tpo_topk_eig",
-                 "tpo_cluster", "tpo_run"]:
+                 "tpo_cluster", "tpo_run", "tpo_run_host"]:
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -516,75 +516,161 @@ static void haar_reserve(int &sms, int &launches) {
     }
 }
 
+// The whole path on device inputs (B, Bt, X, G).  The Haar side stream starts after `g_ready`
+// (recorded on `st` once G is on the device); with `haar_first` its kernels are queued before
+// the propagation's (host inputs: the Haar QR runs while the CSRs and X are still being copied).
+struct RunRes {   // events and the Haar side stream, created before the timed start, released on every exit
+    cudaEvent_t ev[5] = {}, join = nullptr, g_ready = nullptr;
+    cudaStream_t side = nullptr;
+    RunRes() {
+        for (auto &e : ev) TPO_CUDA(cudaEventCreate(&e));
+        TPO_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+        TPO_CUDA(cudaEventCreateWithFlags(&g_ready, cudaEventDisableTiming));
+        int lo = 0, hi = 0;   // highest priority: the latency-bound Haar chain interleaves with the SpMMs
+        TPO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        TPO_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+    }
+    ~RunRes() {
+        for (auto &e : ev) if (e) cudaEventDestroy(e);
+        if (join) cudaEventDestroy(join);
+        if (g_ready) cudaEventDestroy(g_ready);
+        if (side) cudaStreamDestroy(side);
+    }
+};
+
+static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T,
+                     int32_t k, const double *G, bool haar_first, cudaEvent_t g_ready, int32_t eig_mode,
+                     const float *Omega, int32_t p, int32_t q, int32_t Tf, int32_t Tg, int32_t *labels,
+                     double *timings_ms, Arena &ar, cudaStream_t st, RunRes &res, int res_sms, int res_launches) {
+    const int64_t n = B->n_rows, D = 2 * d;
+    float *Z = ar.take<float>(n * d), *Zh = ar.take<float>(n * d);
+    float *Rp = ar.take<float>(n * D), *dinv = ar.take<float>(n);
+    float *Qd = ar.take<float>(d * d);
+    float *Gamma = ar.take<float>(n * k), *Psi = ar.take<float>(D * k);
+    double *r = ar.take<double>(D);
+    const size_t haar_bytes = align_up(haar_q_ws_bytes(d));
+    Arena har(ar.dry ? nullptr : ar.base + ar.off, haar_bytes);
+    ar.take<char>(haar_bytes - 256);
+    const size_t mark = ar.off;
+    cudaEvent_t *ev = res.ev;
+    cudaEvent_t join = res.join;
+    cudaStream_t side = res.side;
+    // Alg. 1 L6-7 depends only on G: it runs on a side stream beside the propagation.  With
+    // device inputs the propagation is queued first, so its persistent kernels take their SMs
+    // (all but the reserved ones) before the Haar kernels arrive.
+    auto haar = [&] {
+        TPO_CUDA(cudaStreamWaitEvent(side, g_ready, 0));
+        haar_q_device(G, true, d, Qd, har, side);
+        TPO_CUDA(cudaEventRecord(join, side));
+    };
+    if (haar_first) haar();
+    propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, res_sms, res_launches);
+    ar.off = mark;
+    if (!haar_first) haar();
+    TPO_CUDA(cudaEventRecord(ev[1], st));
+    TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
+    features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
+    ar.off = mark;
+    TPO_CUDA(cudaEventRecord(ev[2], st));
+    std::vector<double> sig(k);
+    topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st, r);
+    ar.off = mark;
+    TPO_CUDA(cudaEventRecord(ev[3], st));
+    cluster_impl(Rp, dinv, n, D, k, Gamma, sig.data(), Psi, Tf, Tg, labels, nullptr, ar, st);
+    TPO_CUDA(cudaEventRecord(ev[4], st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    if (timings_ms)
+        for (int i = 0; i < 4; ++i) {
+            float ms = 0.f;
+            TPO_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            timings_ms[i] = ms;
+        }
+}
+
+static void check_run(const tpo_csr_t *B, int64_t d, int32_t k) {
+    const int64_t n = B->n_rows, D = 2 * d;
+    TPO_REQUIRE(n >= 1, "empty U side");
+    TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= D, "k must lie in [1, min(n, 2d, 128)]");
+}
+
 int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T, int32_t k,
             const double *G, int32_t eig_mode, const float *Omega, int32_t p, int32_t q, int32_t Tf, int32_t Tg,
             int32_t *labels, double *timings_ms, void *ws, size_t ws_bytes, void *stream) {
     return guarded([&] {
         check_propagate(B, Bt, X, d, alpha, T, X, nullptr);
         check_ptr(G, "G");
-        const int64_t n = B->n_rows, D = 2 * d;
-        TPO_REQUIRE(n >= 1, "empty U side");
-        TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= D, "k must lie in [1, min(n, 2d, 128)]");
+        check_run(B, d, k);
         check_ptr(labels, "labels");
-        check_ws(ws, ws_bytes, tpo_run_ws(n, B->n_cols, B->nnz, d, k, eig_mode, p));
+        check_ws(ws, ws_bytes, tpo_run_ws(B->n_rows, B->n_cols, B->nnz, d, k, eig_mode, p));
         cudaStream_t st = as_stream(stream);
         Arena ar(ws, ws_bytes);
-        float *Z = ar.take<float>(n * d), *Zh = ar.take<float>(n * d);
-        float *Rp = ar.take<float>(n * D), *dinv = ar.take<float>(n);
-        float *Qd = ar.take<float>(d * d);
-        float *Gamma = ar.take<float>(n * k), *Psi = ar.take<float>(D * k);
-        double *r = ar.take<double>(D);
-        const size_t haar_bytes = align_up(haar_q_ws_bytes(d));
-        Arena har(ar.dry ? nullptr : ar.base + ar.off, haar_bytes);
-        ar.take<char>(haar_bytes - 256);
-        const size_t mark = ar.off;
-        struct Res {   // events and the side stream, released on every exit path
-            cudaEvent_t ev[5] = {}, fork = nullptr, join = nullptr;
-            cudaStream_t side = nullptr;
-            ~Res() {
-                for (auto &e : ev) if (e) cudaEventDestroy(e);
-                if (fork) cudaEventDestroy(fork);
-                if (join) cudaEventDestroy(join);
-                if (side) cudaStreamDestroy(side);
-            }
-        } res;
-        cudaEvent_t *ev = res.ev;
-        for (int i = 0; i < 5; ++i) TPO_CUDA(cudaEventCreate(&ev[i]));
-        TPO_CUDA(cudaEventCreateWithFlags(&res.fork, cudaEventDisableTiming));
-        TPO_CUDA(cudaEventCreateWithFlags(&res.join, cudaEventDisableTiming));
-        int lo = 0, hi = 0;   // highest priority: the latency-bound Haar chain interleaves with the SpMMs
-        TPO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        TPO_CUDA(cudaStreamCreateWithPriority(&res.side, cudaStreamNonBlocking, hi));
-        cudaEvent_t fork = res.fork, join = res.join;
-        cudaStream_t side = res.side;
-        TPO_CUDA(cudaEventRecord(ev[0], st));
-        TPO_CUDA(cudaEventRecord(fork, st));
+        RunRes res;
+        TPO_CUDA(cudaEventRecord(res.ev[0], st));
         int res_sms = 0, res_launches = 0;
         haar_reserve(res_sms, res_launches);
-        propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, res_sms, res_launches);
-        ar.off = mark;
-        TPO_CUDA(cudaEventRecord(ev[1], st));
-        // Alg. 1 L6-7 depends only on G: it runs on a side stream beside the propagation
-        TPO_CUDA(cudaStreamWaitEvent(side, fork, 0));
-        haar_q_device(G, true, d, Qd, har, side);
-        TPO_CUDA(cudaEventRecord(join, side));
-        TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
-        features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
-        ar.off = mark;
-        TPO_CUDA(cudaEventRecord(ev[2], st));
-        std::vector<double> sig(k);
-        topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st, r);
-        ar.off = mark;
-        TPO_CUDA(cudaEventRecord(ev[3], st));
-        cluster_impl(Rp, dinv, n, D, k, Gamma, sig.data(), Psi, Tf, Tg, labels, nullptr, ar, st);
-        TPO_CUDA(cudaEventRecord(ev[4], st));
+        run_body(B, Bt, X, d, alpha, T, k, G, false, res.ev[0], eig_mode, Omega, p, q, Tf, Tg, labels, timings_ms, ar,
+                 st, res, res_sms, res_launches);
+    });
+}
+
+size_t tpo_run_host_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, int32_t mode, int32_t p,
+                       int32_t weighted) {
+    size_t s = align_up(sizeof(int64_t) * (n_u + 1)) + align_up(sizeof(int64_t) * (n_v + 1));
+    s += 2 * align_up(sizeof(int32_t) * nnz);
+    if (weighted) s += 2 * align_up(sizeof(float) * nnz);
+    s += align_up(sizeof(float) * n_u * d) + align_up(sizeof(double) * d * d) + align_up(sizeof(int32_t) * n_u);
+    return s + tpo_run_ws(n_u, n_v, nnz, d, k, mode, p) + 8 * 256;
+}
+
+int tpo_run_host(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T,
+                 int32_t k, const double *G, int32_t eig_mode, const float *Omega, int32_t p, int32_t q, int32_t Tf,
+                 int32_t Tg, int32_t *labels, double *timings_ms, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        check_propagate(B, Bt, X, d, alpha, T, X, nullptr);
+        TPO_REQUIRE(G != nullptr, "G is NULL");
+        TPO_REQUIRE(labels != nullptr, "labels is NULL");
+        TPO_REQUIRE((B->val == nullptr) == (Bt->val == nullptr), "B and Bt must both carry weights or neither");
+        check_run(B, d, k);
+        const int64_t n = B->n_rows, m = B->n_cols, nnz = B->nnz;
+        const int weighted = B->val != nullptr;
+        check_ws(ws, ws_bytes, tpo_run_host_ws(n, m, nnz, d, k, eig_mode, p, weighted));
+        cudaStream_t st = as_stream(stream);
+        Arena ar(ws, ws_bytes);
+        int64_t *brp = ar.take<int64_t>(n + 1), *trp = ar.take<int64_t>(m + 1);
+        int32_t *bci = ar.take<int32_t>(nnz), *tci = ar.take<int32_t>(nnz);
+        float *bv = weighted ? ar.take<float>(nnz) : nullptr, *tv = weighted ? ar.take<float>(nnz) : nullptr;
+        float *Xd = ar.take<float>(n * d);
+        double *Gd = ar.take<double>(d * d);
+        int32_t *lab = ar.take<int32_t>(n);
+        RunRes res;
+        TPO_CUDA(cudaEventRecord(res.ev[0], st));
+        // inputs in the order the path consumes them: G (the Haar QR starts as soon as it lands;
+        // the copy engine serves the copies in issue order), the CSRs (degrees, schedules), X
+        auto h2d = [&](void *dst, const void *src, size_t bytes) {
+            if (bytes) TPO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        };
+        h2d(Gd, G, sizeof(double) * d * d);
+        TPO_CUDA(cudaEventRecord(res.g_ready, st));
+        h2d(brp, B->row_ptr, sizeof(int64_t) * (n + 1));
+        h2d(bci, B->col_idx, sizeof(int32_t) * nnz);
+        h2d(trp, Bt->row_ptr, sizeof(int64_t) * (m + 1));
+        h2d(tci, Bt->col_idx, sizeof(int32_t) * nnz);
+        if (weighted) {
+            h2d(bv, B->val, sizeof(float) * nnz);
+            h2d(tv, Bt->val, sizeof(float) * nnz);
+        }
+        h2d(Xd, X, sizeof(float) * n * d);
+        const tpo_csr_t Bd{n, m, nnz, brp, bci, bv}, Btd{m, n, nnz, trp, tci, tv};
+        // the Haar rotation runs during the input copies: no SMs are held back for it
+        int res_sms = 0, res_launches = 0;
+        if (const char *e = getenv("TPO_HOST_RESERVE")) {
+            int a = 0, b = 0;
+            if (sscanf(e, "%d,%d", &a, &b) == 2 && a >= 0 && b >= 0) { res_sms = a; res_launches = b; }
+        }
+        run_body(&Bd, &Btd, Xd, d, alpha, T, k, Gd, true, res.g_ready, eig_mode, Omega, p, q, Tf, Tg, lab, timings_ms,
+                 ar, st, res, res_sms, res_launches);
+        TPO_CUDA(cudaMemcpyAsync(labels, lab, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         TPO_CUDA(cudaStreamSynchronize(st));
-        if (timings_ms)
-            for (int i = 0; i < 4; ++i) {
-                float ms = 0.f;
-                TPO_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-                timings_ms[i] = ms;
-            }
     });
 }
 

@@ -217,6 +217,57 @@ class Runner:
         return self.labels
 
 
+def _host(t, dtype, name, shape):
+    """A contiguous CPU tensor of `dtype` and `shape` (numpy arrays are wrapped, not copied)."""
+    if isinstance(t, np.ndarray):
+        t = torch.from_numpy(np.ascontiguousarray(t))
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a host (CPU) tensor or numpy array")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must be contiguous with shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
+class HostRunner:
+    """Whole hot path from HOST inputs (tpo_run_host): the inputs are copied inside the call,
+    the Haar QR of G runs beside their copies, the labels come back to a host array.  Pinned
+    host tensors make the copies asynchronous."""
+
+    def __init__(self, n_u: int, n_v: int, nnz: int, d: int, k: int, weighted: bool = False,
+                 mode: int = TPO_EIG_EXACT, p: int = 10, device="cuda"):
+        self.n_u, self.n_v, self.nnz, self.d, self.k = n_u, n_v, nnz, d, k
+        self.weighted, self.mode, self.p = weighted, mode, p
+        self.ws = _ws(lib().tpo_run_host_ws(n_u, n_v, nnz, d, k, mode, p, int(weighted)), device)
+        self.timings = np.zeros(4, np.float64)
+
+    def __call__(self, B_rowptr, B_col, Bt_rowptr, Bt_col, X, G, alpha: float, T: int, Tf: int = 5, Tg: int = 20,
+                 B_val=None, Bt_val=None, labels=None, q: int = 2, Omega: Optional[torch.Tensor] = None, stream=None):
+        n, m, e, d = self.n_u, self.n_v, self.nnz, self.d
+        brp = _host(B_rowptr, torch.int64, "B_rowptr", (n + 1,))
+        bci = _host(B_col, torch.int32, "B_col", (e,))
+        trp = _host(Bt_rowptr, torch.int64, "Bt_rowptr", (m + 1,))
+        tci = _host(Bt_col, torch.int32, "Bt_col", (e,))
+        Xh = _host(X, torch.float32, "X", (n, d))
+        Gh = _host(G, torch.float64, "G", (d, d))
+        if (B_val is None) != (not self.weighted) or (Bt_val is None) != (not self.weighted):
+            raise ValueError("weights must be given for both B and Bt exactly when the runner is weighted")
+        bv = None if B_val is None else _host(B_val, torch.float32, "B_val", (e,))
+        tv = None if Bt_val is None else _host(Bt_val, torch.float32, "Bt_val", (e,))
+        if labels is None:
+            labels = torch.empty(n, dtype=torch.int32)
+        labels = _host(labels, torch.int32, "labels", (n,))
+        B = CSR(n, m, e, brp.data_ptr(), bci.data_ptr(), None if bv is None else bv.data_ptr())
+        Bt = CSR(m, n, e, trp.data_ptr(), tci.data_ptr(), None if tv is None else tv.data_ptr())
+        check(lib().tpo_run_host(C.byref(B), C.byref(Bt), C.c_void_p(Xh.data_ptr()), d, float(alpha), int(T),
+                                 int(self.k), C.c_void_p(Gh.data_ptr()), int(self.mode), _ptr(Omega), int(self.p),
+                                 int(q), int(Tf), int(Tg), C.c_void_p(labels.data_ptr()),
+                                 self.timings.ctypes.data_as(C.c_void_p), _ptr(self.ws), self.ws.numel(),
+                                 _stream(stream)))
+        return labels
+
+
 def run(g: DeviceGraph, X: torch.Tensor, alpha: float, T: int, k: int, G: np.ndarray, mode=TPO_EIG_EXACT,
         Tf=5, Tg=20, p=10, q=2, Omega=None):
     """Whole hot path (tpo_run): returns (labels, timings_ms[4])."""

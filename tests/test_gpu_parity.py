@@ -315,3 +315,34 @@ def test_run_tiny_end_to_end(tpo, tiny_topk):
     assert DN.ari(labels, res["labels"]) >= 0.999
     assert labels.min() >= 0 and labels.max() < g.k
     assert np.all(tm > 0)
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_run_host_matches_device_inputs(tpo, weighted):
+    """tpo_run_host (host inputs copied inside the call, Haar beside the copies, no SMs held
+    back) runs the same kernels on the same data as tpo_run: identical labels."""
+    g = make_config("tiny")
+    rng = np.random.default_rng(5)
+    bval = tval = None
+    if weighted:   # weights of B and the matching entries of B^T
+        bval = rng.uniform(0.5, 2.0, g.nnz).astype(np.float32)
+        rows = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(g.B_rowptr))
+        key_b = rows * g.m + g.B_col
+        trows = np.repeat(np.arange(g.m, dtype=np.int64), np.diff(g.Bt_rowptr))
+        key_t = g.Bt_col.astype(np.int64) * g.m + trows
+        tval = bval[np.searchsorted(key_b, key_t)] if np.all(np.diff(key_b) > 0) else None
+        assert tval is not None
+    dg = tpo.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, bval, tval)
+    X = torch.from_numpy(g.X).cuda()
+    lab_d = tpo.Runner(dg, g.d, g.k)(X, g.alpha, g.T, g.G).cpu().numpy()
+    hr = tpo.HostRunner(g.n, g.m, g.nnz, g.d, g.k, weighted=weighted)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    lab_h = hr(pin(g.B_rowptr), pin(g.B_col), pin(g.Bt_rowptr), pin(g.Bt_col), pin(g.X),
+               pin(np.asarray(g.G, np.float64)), g.alpha, g.T,
+               B_val=None if bval is None else pin(bval), Bt_val=None if tval is None else pin(tval)).numpy()
+    assert np.array_equal(lab_h, lab_d)
+    assert np.all(hr.timings > 0)
+    # pageable numpy inputs work too (synchronous copies)
+    lab_h2 = hr(g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, g.X, np.asarray(g.G, np.float64), g.alpha, g.T,
+                B_val=bval, Bt_val=tval).numpy()
+    assert np.array_equal(lab_h2, lab_d)
