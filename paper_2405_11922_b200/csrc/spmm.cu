@@ -617,18 +617,22 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
 // of an edge over more bytes, fewer keep the gathered working set (SL x 512 B per row) small.
 // MINB: resident blocks per SM the register budget is sized for.  Encoded as SL * 10 + MINB
 // (or SL * 100 + MINB * 10 + edges-in-flight code); TPO_SPMM_VARIANT overrides it (tuning).
+// variant code: SL * 10 + MINB (edges in flight 8 / SL), SL * 100 + MINB * 10 + UE, or
+// SL * 1000 + MINB * 100 + UE (UE >= 10)
+int variant_sl(int v) { return v >= 1000 ? v / 1000 : v >= 100 ? v / 100 : v / 10; }
+int variant_minb(int v) { return v >= 1000 ? (v / 100) % 10 : v >= 100 ? (v / 10) % 10 : v % 10; }
 int spmm_variant(int nslices) {
-    int v = nslices >= 2 ? 23 : 14;      // measured best on small (d = 1000) and medium (d = 256)
+    int v = 14;   // measured best on small (d = 1000), medium (d = 256) and large (d = 128)
     if (const char *e = getenv("TPO_SPMM_VARIANT")) v = atoi(e);
-    if (v != 14 && v != 23 && v != 228) v = 14;
-    if (v / (v >= 100 ? 100 : 10) > nslices) v = 14;
+    if (v != 14 && v != 13 && v != 23 && v != 228) v = 14;
+    if (variant_sl(v) > nslices) v = 14;
     return v;
 }
 
 template <int EPI, bool W>
 void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
-    const int sl = var >= 100 ? var / 100 : var / 10;
-    const int minb = var >= 100 ? (var / 10) % 10 : var % 10;
+    const int sl = variant_sl(var);
+    const int minb = variant_minb(var);
     a.ngroups = (a.nslices + sl - 1) / sl;
     const int64_t blocks = cdiv(max_items * a.ngroups, WPB);
     // persistent warps: at most the resident capacity (SMs x MINB blocks of WPB warps)
@@ -640,6 +644,7 @@ void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
     switch (var) {
         case 23: spmm_kernel<EPI, W, 2, 3><<<grid, WPB * 32, 0, st>>>(a); break;
         case 228: spmm_kernel<EPI, W, 2, 2, 8><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 13: spmm_kernel<EPI, W, 1, 3><<<grid, WPB * 32, 0, st>>>(a); break;
         default: spmm_kernel<EPI, W, 1, 4><<<grid, WPB * 32, 0, st>>>(a); break;
     }
     TPO_LAUNCH_CHECK();
