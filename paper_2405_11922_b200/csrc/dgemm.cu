@@ -11,7 +11,8 @@
 //   chol_inv:  one CTA; for the b x b Gram g (b <= 112) of CholeskyQR: S = diag(g)^{-1/2},
 //              S g S = C^T C (upper C), writes Ci = S C^{-1} so that V <- V Ci has orthonormal
 //              columns; a non-SPD or non-finite pivot sets *flag (checked by the caller at its
-//              next synchronisation point -> TPO_ENUMERIC).
+//              next synchronisation point -> TPO_ENUMERIC).  A near-identity g (max|g - I| <=
+//              1e-8, the second CholeskyQR pass) takes the first-order inverse I - F instead.
 #include <algorithm>
 
 #include "tpo_internal.cuh"
@@ -299,8 +300,26 @@ __global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double *__restr
     double *sc = X + b * p;              // b
     double *T = sc + b;                  // CB x b scratch
     double *rd = T + CB * b;             // b: 1 / U[i][i] (no fp64 divisions on the dependency chains)
-    __shared__ int bad;
-    if (t == 0) bad = 0;
+    __shared__ int bad, far;
+    if (t == 0) bad = 0, far = 0;
+    __syncthreads();
+    // Near-identity fast path (the second pass of CholeskyQR2): g = I + E with max|E| <= 1e-8
+    // has the factor U = I + F + O(|E|^2), F = triu(E, 1) + diag(E) / 2, so U^{-1} = I - F to
+    // O(|E|^2) <= 1e-16 -- no sequential factorisation needed.
+    for (int i = t; i < b * b; i += 256) {
+        const int r = i / b, c = i - r * b;
+        const double e = g[i] - (r == c ? 1.0 : 0.0);
+        if (!(fabs(e) <= 1e-8)) far = 1;
+    }
+    __syncthreads();
+    if (!far) {
+        for (int i = t; i < b * b; i += 256) {
+            const int r = i / b, c = i - r * b;
+            const double e = g[i] - (r == c ? 1.0 : 0.0);
+            Ci[i] = c > r ? -e : (c == r ? 1.0 - 0.5 * e : 0.0);
+        }
+        return;
+    }
     for (int i = t; i < b; i += 256) {
         const double d = g[(int64_t)i * b + i];
         sc[i] = (d > 0.0 && isfinite(d)) ? rsqrt(d) : 0.0;
