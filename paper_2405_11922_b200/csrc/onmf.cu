@@ -12,6 +12,8 @@
 //              a-dimension (coalesced), RPW x KC accumulators per lane, fixed shuffle tree.
 //
 // Both are fp64-FMA bound on B200 (64 DFMA/clk/SM): n D k FMAs per pass.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "tpo_internal.cuh"
@@ -87,6 +89,125 @@ __global__ void __launch_bounds__(NTR, 4) onmf_rtu_kernel(const float *__restric
         }
     }
     // part[g][a][l] (the chunk's columns only)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        if (!cv[c]) continue;
+#pragma unroll
+        for (int l = 0; l < KC; ++l)
+            if (l < kc) part[(g * D + col[c]) * (int64_t)k + k0 + l] = acc[c][l];
+    }
+}
+
+// The same product with the R' rows and the Ups / dinv rows staged through an RS-stage cp.async
+// ring (RTS rows per stage): the loads of the next stages are in flight while a stage is
+// multiplied (the direct-load kernel keeps only 4 rows per thread in flight: MLP-bound on
+// HBM).  Per (column, l) the rows are accumulated in the same order as onmf_rtu_kernel, so the
+// results are bit-identical.
+constexpr int RTS = 8, RS = 4;
+__device__ __forceinline__ void cpa16(void *sm, const void *g, bool v) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(g), "r"(v ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa8(void *sm, const void *g, bool v) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(g), "r"(v ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa4(void *sm, const void *g, bool v) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(g), "r"(v ? 4 : 0) : "memory");
+}
+template <int CPT, int KC>
+constexpr size_t rtu_pipe_smem() {
+    return (size_t)RS * (RTS * NTR * CPT * 4 + RTS * KC * 8 + RTS * 4);
+}
+
+template <int CPT, int KC>
+__global__ void __launch_bounds__(NTR, 2) onmf_rtu_pipe_kernel(const float *__restrict__ Rp, int64_t n, int D,
+                                                              const float *__restrict__ dinv,
+                                                              const double *__restrict__ U, int k, int64_t rows_per,
+                                                              double *__restrict__ part) {
+    constexpr int W = NTR * CPT;                      // columns of the block
+    extern __shared__ __align__(16) uint8_t rsm[];
+    float *Rs = reinterpret_cast<float *>(rsm);                                   // [RS][RTS][W]
+    double *Ys = reinterpret_cast<double *>(rsm + (size_t)RS * RTS * W * 4);       // [RS][RTS][KC]
+    float *ds = reinterpret_cast<float *>(rsm + (size_t)RS * (RTS * W * 4 + RTS * KC * 8));   // [RS][RTS]
+    const int t = threadIdx.x;
+    const int64_t g = blockIdx.x;
+    const int a0 = blockIdx.y * W;
+    const int k0 = blockIdx.z * KC;
+    const int kc = min(KC, k - k0);
+    const int64_t r0 = g * rows_per, r1 = min(n, r0 + rows_per);
+    const int nst = (int)((r1 - r0 + RTS - 1) / RTS);
+    const bool vec = (D % 4 == 0) && (a0 % 4 == 0);
+    auto load = [&](int s) {
+        const int buf = s % RS;
+        const int64_t tb = r0 + (int64_t)s * RTS;
+        float *R = Rs + (size_t)buf * RTS * W;
+        if (vec) {
+            for (int e = t; e < RTS * W / 4; e += NTR) {
+                const int r = e / (W / 4), c4 = (e - r * (W / 4)) * 4;
+                const bool v = tb + r < r1 && a0 + c4 < D;
+                cpa16(R + r * W + c4, v ? (const void *)(Rp + (tb + r) * D + a0 + c4) : (const void *)Rp, v);
+            }
+        } else {
+            for (int e = t; e < RTS * W; e += NTR) {
+                const int r = e / W, c = e - r * W;
+                const bool v = tb + r < r1 && a0 + c < D;
+                cpa4(R + r * W + c, v ? (const void *)(Rp + (tb + r) * D + a0 + c) : (const void *)Rp, v);
+            }
+        }
+        double *Y = Ys + (size_t)buf * RTS * KC;
+        for (int e = t; e < RTS * KC; e += NTR) {
+            const int r = e / KC, l = e - r * KC;
+            const bool v = tb + r < r1 && l < kc;
+            cpa8(Y + e, v ? (const void *)(U + (tb + r) * k + k0 + l) : (const void *)U, v);
+        }
+        if (t < RTS) {
+            const bool v = tb + t < r1;
+            cpa4(ds + buf * RTS + t, v ? (const void *)(dinv + tb + t) : (const void *)dinv, v);
+        }
+    };
+    int col[CPT];
+    bool cv[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        col[c] = a0 + t + NTR * c;
+        cv[c] = col[c] < D;
+    }
+    double acc[CPT][KC];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int l = 0; l < KC; ++l) acc[c][l] = 0.0;
+#pragma unroll
+    for (int s = 0; s < RS - 1; ++s) {
+        if (s < nst) load(s);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int s = 0; s < nst; ++s) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(RS - 2) : "memory");
+        __syncthreads();
+        const int buf = s % RS;
+        double *Y = Ys + (size_t)buf * RTS * KC;
+        for (int e = t; e < RTS * KC; e += NTR) Y[e] = (double)ds[buf * RTS + e / KC] * Y[e];   // dinv . Ups
+        __syncthreads();
+        if (s + RS - 1 < nst) load(s + RS - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const float *R = Rs + (size_t)buf * RTS * W;
+#pragma unroll 2
+        for (int r = 0; r < RTS; ++r) {
+            double rv[CPT];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) rv[c] = (double)R[r * W + t + NTR * c];
+#pragma unroll
+            for (int l = 0; l < KC; ++l) {
+                const double y = Y[r * KC + l];
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) acc[c][l] = fma(rv[c], y, acc[c][l]);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
         if (!cv[c]) continue;
@@ -203,6 +324,27 @@ void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float
     const dim3 grid((unsigned)p.G, (unsigned)p.ncb, (unsigned)p.nkc);
     // only CPT x KC <= 64 (or CPT = 1) is planned (rtu_plan); the other combinations are not instantiated
     constexpr int C8 = 8 * KC <= 64 ? 8 : 1, C4 = 4 * KC <= 64 ? 4 : 1, C2 = 2 * KC <= 64 ? 2 : 1;
+    static const bool pipe = [] {
+        const char *e = getenv("TPO_RTU_PIPE");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (pipe) {
+#define TPO_RTU_PIPE(CPTV)                                                                                   \
+    {                                                                                                        \
+        constexpr size_t sm = rtu_pipe_smem<CPTV, KC>();                                                     \
+        TPO_CUDA(cudaFuncSetAttribute(onmf_rtu_pipe_kernel<CPTV, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+        onmf_rtu_pipe_kernel<CPTV, KC><<<grid, NTR, sm, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part);      \
+    }
+        switch (p.cpt) {
+            case 1: TPO_RTU_PIPE(1) break;
+            case 2: TPO_RTU_PIPE(C2) break;
+            case 4: TPO_RTU_PIPE(C4) break;
+            default: TPO_RTU_PIPE(C8) break;
+        }
+#undef TPO_RTU_PIPE
+        TPO_LAUNCH_CHECK();
+        return;
+    }
     switch (p.cpt) {
         case 1: onmf_rtu_kernel<1, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
         case 2: onmf_rtu_kernel<C2, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
