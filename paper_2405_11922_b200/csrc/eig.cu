@@ -14,6 +14,9 @@
 #include <algorithm>
 #include <vector>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "tpo_internal.cuh"
 
 namespace tpo {
@@ -383,6 +386,10 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         const std::vector<double> rh = to_host(res, k, st);
         double rmax = 0.0;
         for (int l = 0; l < k; ++l) rmax = std::max(rmax, rh[l]);
+        static const bool trace = getenv("TPO_TRACE_EIG") != nullptr;
+        if (trace)
+            fprintf(stderr, "[tpo eig] round %d degree %d rmax/w0 %.3e w0 %.6e wk %.6e wk+1 %.6e wb %.6e\n", round,
+                    round > 0 ? m : 0, rmax / fabs(w[0]), w[0], w[k - 1], w[k], w[bz - 1]);
         if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
             check_flag(flag, st, "top-k subspace iteration (CholeskyQR2)");
             lam.assign(w.begin(), w.begin() + k);
