@@ -230,6 +230,8 @@ struct SpmmArgs {
     float4 *out;              // Q (EPI_V), P (EPI_U), Z (EPI_FINAL)
     float4 *out_hat;          // Zhat (EPI_FINAL, fused when nslices == 1), else null
     unsigned long long *work; // persistent-warp work counter of this launch (zeroed)
+    unsigned *arrive;         // per (long row, column group) chunk-arrival counters (zeroed once per
+                              // propagation; each launch adds nchunks), or null: separate fix-up kernel
     int reserve_sms;          // SMs left free (blocks placed on them exit) for concurrent side-stream work
     int smid_limit;           // = SMs - reserve_sms, set at launch
 };
@@ -490,6 +492,25 @@ __device__ __forceinline__ void spmm_unit(const SpmmArgs &a, int grp, int64_t it
 #pragma unroll
     for (int q = 0; q < SL; ++q)
         if (act[q]) a.partials[(int64_t)it.z * a.d4 + c4[q]] = acc[q];
+    if (a.arrive == nullptr) return;
+    // the last chunk to arrive finishes the row: partials added in chunk order (the same sum as
+    // the fix-up kernel, whichever warp does it)
+    __threadfence();
+    const int slot0 = it.z - it.y;
+    unsigned old = 0;
+    if (lane == 0) old = atomicAdd(a.arrive + (int64_t)slot0 * a.ngroups + grp, 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if ((int)(old % (unsigned)it.w) != it.w - 1) return;
+    __threadfence();
+#pragma unroll
+    for (int q = 0; q < SL; ++q) {
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act[q]) {
+            const float4 *pp = a.partials + (int64_t)slot0 * a.d4 + c4[q];
+            for (int j = 0; j < it.w; ++j) s4 = f4add(s4, __ldcg(pp + (int64_t)j * a.d4));
+        }
+        epilogue<EPI>(a, it.x, c4[q], act[q], s4);
+    }
 }
 
 // Persistent warps: the grid is the resident capacity (SMs x MINB blocks); each warp takes the
@@ -655,6 +676,7 @@ void spmm_launch(const SpmmArgs &a, int64_t max_items, int64_t max_slots, bool w
     const int var = spmm_variant(a.nslices);
     if (weighted) spmm_launch_sl<EPI, true>(a, max_items, var, st);
     else spmm_launch_sl<EPI, false>(a, max_items, var, st);
+    if (a.arrive) return;                 // long rows finished by their last chunk (fused fix-up)
     const int64_t fw = max_slots * a.nslices;
     fixup_kernel<EPI><<<cdiv(fw, WPB), WPB * 32, 0, st>>>(a);
     TPO_LAUNCH_CHECK();
@@ -671,6 +693,9 @@ size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
     sched_alloc(ar, n_v, nnz);
     ar.take<float>((2 * (nnz / CHUNK) + 1) * d);  // partials (shared by both SpMMs)
     ar.take<unsigned long long>(kCounters);       // persistent-warp work counters
+    const int64_t nsl = (d / 4 + 31) / 32;
+    ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * nsl);   // chunk-arrival counters (U side)
+    ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * nsl);   // (V side)
     return ar.off + 256;
 }
 
@@ -687,6 +712,13 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     SchedBufs sbt = sched_alloc(ar, m, nnz);
     float *partials = ar.take<float>((2 * (nnz / CHUNK) + 1) * d);
     unsigned long long *work = ar.take<unsigned long long>(kCounters);
+    const int nsl_all = (d4 + 31) / 32;
+    unsigned *arr_u = ar.take<unsigned>(sb.s.max_slots * nsl_all), *arr_v = ar.take<unsigned>(sbt.s.max_slots * nsl_all);
+    const bool fused_fixup = getenv("TPO_SEPARATE_FIXUP") == nullptr;
+    if (fused_fixup) {
+        TPO_CUDA(cudaMemsetAsync(arr_u, 0, sizeof(unsigned) * sb.s.max_slots * nsl_all, st));
+        TPO_CUDA(cudaMemsetAsync(arr_v, 0, sizeof(unsigned) * sbt.s.max_slots * nsl_all, st));
+    }
     int launches = 0;
     auto counter = [&]() {        // a zeroed counter per SpMM launch (the pool is re-zeroed when it wraps)
         if (launches % kCounters == 0) TPO_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) * kCounters, st));
@@ -720,6 +752,7 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
             a.src = (const float4 *)Z; a.d4 = d4; a.nslices = nslices;
             a.sch = sbt.s; a.n_rows = m; a.partials = (float4 *)partials;
             a.scale = sv; a.out = (float4 *)Qv;
+            a.arrive = fused_fixup ? arr_v : nullptr;
             a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
             a.work = counter();
             spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
@@ -732,6 +765,7 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
         a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
         a.scale = su; a.X = (const float4 *)X; a.c = c; a.alpha = alpha;
         a.out = (float4 *)Z;
+        a.arrive = fused_fixup ? arr_u : nullptr;
         a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
         a.work = counter();
         if (last) {
