@@ -157,130 +157,12 @@ int64_t splits_for(int64_t M, int64_t N, int64_t K) {
     return std::max<int64_t>(1, std::min<int64_t>(want, cdiv(K, 4 * BK)));
 }
 
-// ---------------------------------------------------------------------------------------
-// chol_inv (one CTA of TPR threads per row, two b x b matrices in shared memory, b <= CI_MAX)
-//   Cholesky by Schur complements: step j updates rows r > j of the upper triangle with
-//   A[r][c] -= A[j][r] A[j][c] / A[j][j]; row j is final after step j (one barrier per step)
-//   and is scaled by 1/sqrt(A[j][j]) at the end.
-//   Inverse X = C^{-1} by back substitution on unscaled rows: for j = b-1 .. 0,
-//   X[r][c] -= C[r][j] X[j][c] / C[j][j] for r < j, c >= j (one barrier per step); row j
-//   is final once step j starts, and every row is divided by its pivot at the end.
-// ---------------------------------------------------------------------------------------
 constexpr int CI_MAX = 112;
-constexpr int TPR = 8;     // threads per row
-
-// 1/d by the hardware approximation refined with two Newton steps (the pivot reciprocal sits
-// on the critical path of every Cholesky step; an IEEE division is several times longer)
-__device__ __forceinline__ double fast_rcp(double d) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-    r = r * fma(-d, r, 2.0);
-    r = r * fma(-d, r, 2.0);
-    return r;
-}
-
-template <int PER>      // columns of a row a thread owns: ceil(b / TPR) <= PER
-__global__ void __launch_bounds__(CI_MAX * TPR) chol_inv_kernel(const double *__restrict__ g, int b,
-                                                                double *__restrict__ Ci, int *__restrict__ flag) {
-    extern __shared__ double sm[];
-    const int p = b + 1, t = threadIdx.x, nt = blockDim.x;
-    const int my_r = t / TPR, my_q = t % TPR;        // row owned, column phase
-    double *U = sm;                      // b x b (pitch p): equilibrated Gram -> Cholesky factor
-    double *X = sm + b * p;              // b x b (pitch p): inverse
-    double *sc = X + b * p;              // b: equilibration
-    double *pinv = sc + b;               // b: 1 / pivot
-    for (int i = t; i < b; i += nt) {
-        const double d = g[(int64_t)i * b + i];
-        sc[i] = (d > 0.0 && isfinite(d)) ? rsqrt(d) : 0.0;
-    }
-    __syncthreads();
-    for (int i = t; i < b * b; i += nt) {
-        const int r = i / b, c = i - r * b;
-        U[r * p + c] = c >= r ? g[i] * sc[r] * sc[c] : 0.0;
-        X[r * p + c] = r == c ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    if (t == 0) {
-        const double d = U[0];
-        pinv[0] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
-    }
-    __syncthreads();
-    for (int j = 0; j < b - 1; ++j) {
-        if (my_r > j && my_r < b) {
-            const double f = U[j * p + my_r] * pinv[j];
-            const double *uj = U + j * p;
-            double *ur = U + my_r * p;
-            // all loads first (U rows alias: keep the compiler from ordering loads after stores)
-            double xv[PER], yv[PER];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int c = my_r + my_q + TPR * q;
-                xv[q] = c < b ? ur[c] : 0.0;
-                yv[q] = c < b ? uj[c] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int c = my_r + my_q + TPR * q;
-                if (c < b) ur[c] = xv[q] - f * yv[q];
-            }
-            if (my_r == j + 1 && my_q == 0) {            // next pivot is final now: 1 / A_{j+1}[j+1][j+1]
-                const double d = xv[0] - f * yv[0];
-                pinv[my_r] = (d > 0.0 && isfinite(d)) ? fast_rcp(d) : 0.0;
-            }
-        }
-        __syncthreads();
-    }
-    int bad = 0;
-    if (my_r < b) {                                  // C[r][c] = A_r[r][c] / sqrt(A_r[r][r])
-        const double d = U[my_r * p + my_r];
-        const bool ok = d > 0.0 && isfinite(d);
-        bad = !ok;
-        const double s = ok ? rsqrt(d) : 1.0;
-        for (int c = my_r + 1 + my_q; c < b; c += TPR) U[my_r * p + c] *= s;
-    }
-    __syncthreads();
-    if (my_r < b && my_q == 0) {
-        const double d = U[my_r * p + my_r];
-        const double cd = (d > 0.0 && isfinite(d)) ? sqrt(d) : 1.0;
-        U[my_r * p + my_r] = cd;
-        pinv[my_r] = 1.0 / cd;
-    }
-    __syncthreads();
-    for (int j = b - 1; j > 0; --j) {
-        if (my_r < j) {
-            const double f = U[my_r * p + j] * pinv[j];
-            const double *xj = X + j * p;
-            double *xr = X + my_r * p;
-            double xv[PER], yv[PER];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int c = j + my_q + TPR * q;
-                xv[q] = c < b ? xr[c] : 0.0;
-                yv[q] = c < b ? xj[c] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int c = j + my_q + TPR * q;
-                if (c < b) xr[c] = xv[q] - f * yv[q];
-            }
-        }
-        __syncthreads();
-    }
-    for (int i = t; i < b * b; i += nt) {
-        const int r = i / b, c = i - r * b;
-        Ci[i] = c >= r ? X[r * p + c] * pinv[r] * sc[r] : 0.0;
-    }
-    bad = __syncthreads_or(bad);
-    if (t == 0) {
-        bool z = false;
-        for (int i = 0; i < b; ++i) z |= sc[i] == 0.0;
-        if ((bad || z) && flag) *flag = 1;
-    }
-}
 
 // ---------------------------------------------------------------------------------------
-// Blocked chol_inv (one CTA of 256 threads, 16 x 16 blocks, b <= CI_MAX): the same factor and
-// inverse as chol_inv_kernel with O(b / 16) block barriers instead of O(b) steps.
+// Blocked chol_inv (one CTA of 256 threads, 16 x 16 blocks, b <= CI_MAX): Cholesky and
+// triangular inverse with O(b / 16) block barriers (an unblocked one-barrier-per-step version
+// was 2-3x slower).
 //   Cholesky (upper, S g S = U^T U), per block column J = [j0, je):
 //     (1) warp 0 factors the diagonal block (warp-synchronous right-looking steps),
 //     (2) panel: U[J, c] <- U_JJ^{-T} U[J, c] for c >= je (thread per column, forward subst.),

@@ -7,9 +7,7 @@
 //              (coalesced loads, 4 rows in flight) and KC columns of Ups (dinv.Ups staged in
 //              shared memory, read as broadcasts): CPT x KC fp64 accumulators.  Each CTA writes
 //              an fp64 partial; onmf_reduce adds the row groups in order (deterministic).
-//   onmf_rh:   RH[i, l] = dinv_i sum_a R'[i, a] H[a, l]                (n x k)
-//              H (D x KC chunk) staged in shared memory; a warp owns RPW rows, lanes split the
-//              a-dimension (coalesced), RPW x KC accumulators per lane, fixed shuffle tree.
+//   (RH[i, l] = dinv_i sum_a R'[i, a] H[a, l] is tsgemm_AW_f64 in dense.cu.)
 //
 // Both are fp64-FMA bound on B200 (64 DFMA/clk/SM): n D k FMAs per pass.
 #include <stdlib.h>
@@ -21,7 +19,6 @@
 namespace tpo {
 namespace {
 
-constexpr int NT = 256;                     // onmf_rh block
 constexpr int NTR = 128;                    // onmf_rtu block: 128 threads x CPT columns
 constexpr int RT = 64;                      // rows of dinv.Ups staged per tile (onmf_rtu)
 
@@ -230,59 +227,6 @@ __global__ void onmf_reduce_kernel(const double *__restrict__ part, int64_t G, i
     out[i] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
-template <int RPW, int KC>
-__global__ void __launch_bounds__(NT) onmf_rh_kernel(const float *__restrict__ Rp, int64_t n, int D,
-                                                     const float *__restrict__ dinv, const double *__restrict__ H,
-                                                     int k, double *__restrict__ RH) {
-    extern __shared__ double Hs[];          // [D][KC]
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int k0 = blockIdx.y * KC;
-    const int kc = min(KC, k - k0);
-    for (int e = t; e < D * KC; e += NT) {
-        const int a = e / KC, l = e - a * KC;
-        Hs[e] = l < kc ? H[(int64_t)a * k + k0 + l] : 0.0;
-    }
-    __syncthreads();
-    const int64_t rows_per_block = (int64_t)(NT / 32) * RPW;
-    for (int64_t rb = (int64_t)blockIdx.x * rows_per_block + w * RPW; rb < n; rb += (int64_t)gridDim.x * rows_per_block) {
-        double acc[RPW][KC];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r)
-#pragma unroll
-            for (int l = 0; l < KC; ++l) acc[r][l] = 0.0;
-        bool rv_ok[RPW];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) rv_ok[r] = rb + r < n;
-        for (int a = lane; a < D; a += 32) {
-            float rv[RPW];
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) rv[r] = rv_ok[r] ? __ldg(Rp + (rb + r) * D + a) : 0.f;
-            const double *h = Hs + a * KC;
-#pragma unroll
-            for (int l = 0; l < KC; ++l) {
-                const double hv = h[l];
-#pragma unroll
-                for (int r = 0; r < RPW; ++r) acc[r][l] = fma((double)rv[r], hv, acc[r][l]);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RPW; ++r)
-#pragma unroll
-            for (int l = 0; l < KC; ++l)
-#pragma unroll
-                for (int o = 16; o; o >>= 1) acc[r][l] += __shfl_xor_sync(0xffffffffu, acc[r][l], o);
-        if (lane == 0) {
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                if (!rv_ok[r]) continue;
-                const double s = (double)dinv[rb + r];
-#pragma unroll
-                for (int l = 0; l < KC; ++l)
-                    if (l < kc) RH[(rb + r) * k + k0 + l] = s * acc[r][l];
-            }
-        }
-    }
-}
 
 // k-chunk widths that are instantiated (a chunk is padded up to the next one)
 constexpr int KCS[] = {2, 4, 5, 8, 10, 12, 16, 20, 26, 32, 50};
@@ -354,30 +298,6 @@ void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float
     TPO_LAUNCH_CHECK();
 }
 
-template <int KC>
-void launch_rh(int rpw, int nkc, const float *Rp, int64_t n, int D, const float *dinv, const double *H, int k, double *RH,
-               cudaStream_t st) {
-    const size_t smem = sizeof(double) * (size_t)D * KC;
-    const int64_t rows_per_block = (NT / 32) * rpw;
-    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, rows_per_block), 148 * 8));
-    const dim3 grid(gx, (unsigned)nkc);
-    constexpr int R4 = 4 * KC <= 64 ? 4 : 1, R2 = 2 * KC <= 64 ? 2 : 1;
-    switch (rpw) {
-        case 1:
-            TPO_CUDA(cudaFuncSetAttribute(onmf_rh_kernel<1, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            onmf_rh_kernel<1, KC><<<grid, NT, smem, st>>>(Rp, n, D, dinv, H, k, RH);
-            break;
-        case 2:
-            TPO_CUDA(cudaFuncSetAttribute(onmf_rh_kernel<R2, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            onmf_rh_kernel<R2, KC><<<grid, NT, smem, st>>>(Rp, n, D, dinv, H, k, RH);
-            break;
-        default:
-            TPO_CUDA(cudaFuncSetAttribute(onmf_rh_kernel<R4, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            onmf_rh_kernel<R4, KC><<<grid, NT, smem, st>>>(Rp, n, D, dinv, H, k, RH);
-            break;
-    }
-    TPO_LAUNCH_CHECK();
-}
 
 #define TPO_KC_SWITCH(kc, F, ...)                      \
     switch (kc) {                                      \
@@ -413,20 +333,5 @@ void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const do
     ar.off = mark;
 }
 
-// RH = dinv . (R' H)   (n x k, fp64); H: D x k fp64
-void onmf_rh(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *H, int k, double *RH,
-             cudaStream_t st) {
-    // the H chunk lives in shared memory: D * kc * 8 bytes <= 200 KB
-    TPO_REQUIRE((size_t)D * 2 * 8 <= 200 * 1024, "ONMF: D too large for the shared-memory H chunk");
-    int nkc = 1;
-    while (true) {
-        const int kc = pick_kc((k + nkc - 1) / nkc);
-        if ((size_t)D * kc * 8 <= 200 * 1024 && kc >= (k + nkc - 1) / nkc) break;
-        ++nkc;
-    }
-    const int kc = pick_kc((k + nkc - 1) / nkc);
-    const int rpw = 4 * kc <= 64 ? 4 : (2 * kc <= 64 ? 2 : 1);
-    TPO_KC_SWITCH(kc, launch_rh, rpw, nkc, Rp, n, (int)D, dinv, H, k, RH, st);
-}
 
 }  // namespace tpo

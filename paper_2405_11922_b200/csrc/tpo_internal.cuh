@@ -178,11 +178,9 @@ size_t tsgemm_ws(int64_t n, int64_t p, int64_t q);
 void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda,
            const double *B, int64_t ldb, double beta, double *C, int64_t ldc, Arena &ar, cudaStream_t st);
 size_t dgemm_ws(int64_t M, int64_t N, int64_t K);
-// ONMF passes over R' (onmf.cu): RtU = R'^T (dinv . U) (D x k) and RH = dinv . (R' H) (n x k), fp64.
+// ONMF passes over R' (onmf.cu): RtU = R'^T (dinv . U) (D x k), fp64 (RH = dinv . (R' H) is tsgemm_AW_f64).
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU,
               Arena &ar, cudaStream_t st);
-void onmf_rh(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *H, int k, double *RH,
-             cudaStream_t st);
 size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k);
 // Ci = S C^{-1} for the b x b Gram g (S g S = C^T C, S = diag(g)^{-1/2}), b <= 128; one CTA;
 // a failed pivot sets *flag (device int) instead of throwing (dgemm.cu).
