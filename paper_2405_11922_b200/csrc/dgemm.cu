@@ -173,7 +173,7 @@ constexpr int CI_MAX = 112;
 // ---------------------------------------------------------------------------------------
 constexpr int CB = 16;
 
-__global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double *__restrict__ g, int b,
+__global__ void __launch_bounds__(256, 1) chol_inv_blk_kernel(const double *__restrict__ g, int b,
                                                            double *__restrict__ Ci, int *__restrict__ flag) {
     extern __shared__ double sm[];
     const int p = b + 1, t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -216,43 +216,48 @@ __global__ void __launch_bounds__(256) chol_inv_blk_kernel(const double *__restr
     const int nb = (b + CB - 1) / CB;
     for (int J = 0; J < nb; ++J) {
         const int j0 = J * CB, je = min(b, j0 + CB);
-        if (w == 0) {                                    // (1) diagonal block, warp-synchronous
-            for (int j = j0; j < je; ++j) {
-                double d = U[j * p + j];
+        if (w == 0) {   // (1) diagonal block by warp 0, register-resident: lane owns column lane & 15 of
+                        //     every other row from lane >> 4; row jj is broadcast by shuffles
+            const int c = lane & 15, h = lane >> 4, bs = je - j0;
+            double a[CB / 2];
+#pragma unroll
+            for (int m = 0; m < CB / 2; ++m) {
+                const int r = h + 2 * m;
+                a[m] = (r < bs && c < bs) ? U[(j0 + r) * p + j0 + c] : 0.0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < CB; ++jj) {
+                if (jj >= bs) break;
+                const int sh = (jj & 1) * 16;             // lanes holding row jj
+                const double rowv = a[jj >> 1];
+                double d = __shfl_sync(0xffffffffu, rowv, sh + jj);
                 const bool ok = d > 0.0 && isfinite(d);
                 if (!ok) d = 1.0;
                 double inv = rsqrt(d);
                 inv = inv * fma(-0.5 * d * inv, inv, 1.5);      // one Newton step: full fp64 accuracy
                 const double piv = d * inv;
-                __syncwarp();
+                const double uc = __shfl_sync(0xffffffffu, rowv, sh + c) * inv;
+                double ur[CB / 2];
+#pragma unroll
+                for (int m = 0; m < CB / 2; ++m) ur[m] = __shfl_sync(0xffffffffu, rowv, sh + h + 2 * m) * inv;
+#pragma unroll
+                for (int m = 0; m < CB / 2; ++m) {
+                    const int r = h + 2 * m;
+                    if (r > jj && c >= r && c < bs) a[m] = fma(-ur[m], uc, a[m]);
+                }
+                if (h == (jj & 1)) {                      // the finished row jj of U
+                    if (c == jj) a[jj >> 1] = piv;
+                    else if (c > jj && c < bs) a[jj >> 1] = rowv * inv;
+                }
                 if (lane == 0) {
                     if (!ok) bad = 1;
-                    U[j * p + j] = piv;
-                    rd[j] = inv;
+                    rd[j0 + jj] = inv;
                 }
-                const int c1 = j + 1 + lane;
-                if (c1 < je) U[j * p + c1] *= inv;
-                __syncwarp();
-                // trailing pairs (r, c), j < r <= c < je: lane owns column j+1+(lane&15) and every
-                // other row from j+1+(lane>>4); all loads are issued before the stores
-                const int cc = j + 1 + (lane & 15), rp = lane >> 4;
-                if (cc < je) {
-                    const double ujc = U[j * p + cc];
-                    double uj[CB / 2], ur[CB / 2];
+            }
 #pragma unroll
-                    for (int m = 0; m < CB / 2; ++m) {
-                        const int r = j + 1 + rp + 2 * m;
-                        const bool v = r <= cc;
-                        uj[m] = v ? U[j * p + r] : 0.0;
-                        ur[m] = v ? U[r * p + cc] : 0.0;
-                    }
-#pragma unroll
-                    for (int m = 0; m < CB / 2; ++m) {
-                        const int r = j + 1 + rp + 2 * m;
-                        if (r <= cc) U[r * p + cc] = ur[m] - uj[m] * ujc;
-                    }
-                }
-                __syncwarp();
+            for (int m = 0; m < CB / 2; ++m) {
+                const int r = h + 2 * m;
+                if (r < bs && c < bs && c >= r) U[(j0 + r) * p + j0 + c] = a[m];
             }
         }
         __syncthreads();
