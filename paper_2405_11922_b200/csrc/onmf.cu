@@ -255,7 +255,7 @@ RtuPlan rtu_plan(int64_t n, int D, int k) {
     p.cpt = cpt;
     p.ncb = (D + NTR * cpt - 1) / (NTR * cpt);
     const int64_t tiles = (int64_t)p.ncb * p.nkc;
-    const int64_t want_g = std::max<int64_t>(1, (4 * 148 + tiles - 1) / tiles);   // one wave at 4 CTAs / SM
+    const int64_t want_g = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);   // one wave at 2 CTAs / SM (pipelined kernel)
     p.G = std::max<int64_t>(1, std::min<int64_t>(want_g, (std::max<int64_t>(n, 1) + RT - 1) / RT));
     p.rows_per = cdiv(cdiv(std::max<int64_t>(n, 1), p.G), 4) * 4;
     p.G = cdiv(std::max<int64_t>(n, 1), p.rows_per);
