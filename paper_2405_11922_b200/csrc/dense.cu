@@ -297,11 +297,16 @@ __global__ void __launch_bounds__(SN) aw2_stream_kernel(const float *__restrict_
             const bool ok = gi < n && k0 + kc < p;
             cp_async16(&As[buf][row * SP + kc], ok ? (const void *)(A + gi * lda + k0 + kc) : (const void *)A, ok);
         }
-        cp_async_commit();
-        for (int e = t; e < SK * QW; e += SN) {
+        for (int e = t; e < SK * QW; e += SN) {     // W slab by cp.async too (no synchronous loads)
             const int kk = e / QW, c = e - kk * QW;
-            Ws[buf][e] = (k0 + kk < p && b0 + c < q) ? W[(int64_t)(k0 + kk) * q + b0 + c] : 0.0;
+            const bool ok = k0 + kk < p && b0 + c < q;
+            const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(&Ws[buf][e]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
+                         "l"(ok ? (const void *)(W + (int64_t)(k0 + kk) * q + b0 + c) : (const void *)W),
+                         "r"(ok ? 8 : 0)
+                         : "memory");
         }
+        cp_async_commit();
     };
     load(0, 0);
     for (int s = 0; s < nslab; ++s) {
