@@ -15,7 +15,7 @@
 #include <vector>
 
 #include <stdio.h>
-#include <stdlib.h>
+#include <chrono>
 
 #include "tpo_internal.cuh"
 
@@ -348,7 +348,13 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     int m = 8;
     std::vector<double> w(bz), E(bz * bz);
     double bnd = 0.0;
+    static const bool trace = getenv("TPO_TRACE_EIG") != nullptr;
+    static cudaEvent_t tev[2] = {};   // trace only: created once, reused
+    if (trace && !tev[0])
+        for (auto &e : tev) TPO_CUDA(cudaEventCreate(&e));
     for (int round = 0; round <= max_rounds; ++round) {
+        const auto t_round = std::chrono::steady_clock::now();
+        if (trace) TPO_CUDA(cudaEventRecord(tev[0], st));
         if (round > 0) {   // Chebyshev filter p_m(Gd) V, damping [0, bnd]
             const double c = 0.5 * bnd, e = 0.5 * bnd;
             TPO_CUDA(cudaMemcpyAsync(Y0, V, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
@@ -386,10 +392,17 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         const std::vector<double> rh = to_host(res, k, st);
         double rmax = 0.0;
         for (int l = 0; l < k; ++l) rmax = std::max(rmax, rh[l]);
-        static const bool trace = getenv("TPO_TRACE_EIG") != nullptr;
-        if (trace)
-            fprintf(stderr, "[tpo eig] round %d degree %d rmax/w0 %.3e w0 %.6e wk %.6e wk+1 %.6e wb %.6e\n", round,
-                    round > 0 ? m : 0, rmax / fabs(w[0]), w[0], w[k - 1], w[k], w[bz - 1]);
+        if (trace) {
+            TPO_CUDA(cudaEventRecord(tev[1], st));
+            TPO_CUDA(cudaEventSynchronize(tev[1]));
+            float gpu_ms = 0.f;
+            TPO_CUDA(cudaEventElapsedTime(&gpu_ms, tev[0], tev[1]));
+            const double wall_ms =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_round).count();
+            fprintf(stderr, "[tpo eig] round %d degree %d rmax/w0 %.3e w0 %.6e wk %.6e wk+1 %.6e wb %.6e  "
+                            "stream %.3f ms wall %.3f ms\n", round, round > 0 ? m : 0, rmax / fabs(w[0]), w[0],
+                    w[k - 1], w[k], w[bz - 1], gpu_ms, wall_ms);
+        }
         if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
             check_flag(flag, st, "top-k subspace iteration (CholeskyQR2)");
             lam.assign(w.begin(), w.begin() + k);
