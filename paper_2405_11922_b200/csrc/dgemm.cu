@@ -14,6 +14,7 @@
 //              next synchronisation point -> TPO_ENUMERIC).  A near-identity g (max|g - I| <=
 //              1e-8, the second CholeskyQR pass) takes the first-order inverse I - F instead.
 #include <algorithm>
+#include <mutex>
 
 #include "tpo_internal.cuh"
 
@@ -346,6 +347,94 @@ __global__ void __launch_bounds__(256, 1) chol_inv_blk_kernel(const double *__re
     }
 }
 
+
+// ---- skinny C = A^T B (A: K x M, B: K x N, M, N <= 32, K large: the k x k products of Alg. 2)
+// The dgemm tile (64 x 32) keeps only 20 % of its FMAs for M = N = 20; here a CTA owns the whole
+// M x N output as a grid of TA x TB register tiles over its slice of the K rows, staged in
+// 32-row chunks through a double-buffered cp.async ring; each CTA writes an fp64 partial that
+// splitk_reduce adds in CTA order (deterministic).
+constexpr int TS_RC = 32, TS_ST = 4;   // rows per chunk, ring stages
+template <int TA, int TB>
+__global__ void __launch_bounds__(256) tsatb_kernel(const double *__restrict__ A, int64_t lda,
+                                                    const double *__restrict__ B, int64_t ldb, int64_t K, int M,
+                                                    int N, int64_t rows_per, double *__restrict__ part) {
+    extern __shared__ __align__(16) double tsm[];    // [TS_ST][TS_RC][M + N]
+    const int W = M + N, t = threadIdx.x;
+    const int QB = (N + TB - 1) / TB, PA = (M + TA - 1) / TA;
+    const int ta = t / QB, tb = t - ta * QB;
+    const bool active = ta < PA;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(K, r0 + rows_per);
+    const int nch = (int)((r1 - r0 + TS_RC - 1) / TS_RC);
+    auto load = [&](int c, int buf) {
+        double *S = tsm + (size_t)buf * TS_RC * W;
+        const int64_t rb = r0 + (int64_t)c * TS_RC;
+        for (int e = t; e < TS_RC * W; e += 256) {
+            const int r = e / W, col = e - r * W;
+            const bool v = rb + r < r1;
+            const double *src = col < M ? A + (rb + r) * lda + col : B + (rb + r) * ldb + (col - M);
+            const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(S + e));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
+                         "l"(v ? (const void *)src : (const void *)A), "r"(v ? 8 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[TA][TB];
+#pragma unroll
+    for (int i = 0; i < TA; ++i)
+#pragma unroll
+        for (int j = 0; j < TB; ++j) acc[i][j] = 0.0;
+#pragma unroll
+    for (int c = 0; c < TS_ST - 1; ++c) {
+        if (c < nch) load(c, c);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int c = 0; c < nch; ++c) {
+        const int buf = c % TS_ST;
+        asm volatile("cp.async.wait_group %0;" ::"n"(TS_ST - 2) : "memory");
+        __syncthreads();
+        if (c + TS_ST - 1 < nch) load(c + TS_ST - 1, (c + TS_ST - 1) % TS_ST);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        if (active) {
+            const double *S = tsm + (size_t)buf * TS_RC * W;
+#pragma unroll 8
+            for (int r = 0; r < TS_RC; ++r) {
+                double a[TA], b[TB];
+#pragma unroll
+                for (int i = 0; i < TA; ++i) a[i] = (ta * TA + i < M) ? S[r * W + ta * TA + i] : 0.0;
+#pragma unroll
+                for (int j = 0; j < TB; ++j) b[j] = (tb * TB + j < N) ? S[r * W + M + tb * TB + j] : 0.0;
+#pragma unroll
+                for (int i = 0; i < TA; ++i)
+#pragma unroll
+                    for (int j = 0; j < TB; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            }
+        }
+    }
+    if (!active) return;
+    double *P = part + (size_t)blockIdx.x * M * N;
+#pragma unroll
+    for (int i = 0; i < TA; ++i)
+#pragma unroll
+        for (int j = 0; j < TB; ++j) {
+            const int a = ta * TA + i, bcol = tb * TB + j;
+            if (a < M && bcol < N) P[(size_t)a * N + bcol] = acc[i][j];
+        }
+}
+
+template <int TA, int TB>
+void launch_tsatb(int64_t G, const double *A, int64_t lda, const double *B, int64_t ldb, int64_t K, int M, int N,
+                  int64_t rows_per, double *part, cudaStream_t st) {
+    const size_t smem = sizeof(double) * TS_ST * TS_RC * (M + N);
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(tsatb_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * TS_ST * TS_RC * 64));
+    });
+    tsatb_kernel<TA, TB><<<(unsigned)G, 256, smem, st>>>(A, lda, B, ldb, K, M, N, rows_per, part);
+    TPO_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 // Bound for every K and every M' <= M, N' <= N: S <= 296 / tiles + 1 and M N <= 4096 tiles,
@@ -361,6 +450,18 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
     if (K <= 0) {   // empty sum: C = beta C
         splitk_reduce_kernel<<<cdiv(M * N, 256), 256, 0, st>>>(nullptr, 0, M, N, alpha, beta, C, ldc);
         TPO_LAUNCH_CHECK();
+        return;
+    }
+    if (transA && M <= 32 && N <= 32 && K >= 8192) {    // skinny k x k products: tsatb
+        const int64_t G = std::min<int64_t>(2 * 148, cdiv(K, 256));
+        const int64_t rows_per = cdiv(K, G);
+        const int64_t Gr = cdiv(K, rows_per);
+        const size_t mark = ar.off;
+        double *part = ar.take<double>(Gr * M * N);
+        if (M <= 16 && N <= 16) launch_tsatb<1, 1>(Gr, A, lda, B, ldb, K, (int)M, (int)N, rows_per, part, st);
+        else launch_tsatb<2, 2>(Gr, A, lda, B, ldb, K, (int)M, (int)N, rows_per, part, st);
+        splitk_reduce(part, Gr, M, N, alpha, beta, C, ldc, st);
+        ar.off = mark;
         return;
     }
     const int64_t S = splits_for(M, N, K);
