@@ -606,8 +606,8 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const size_t sum_smem = (size_t)sum_nw * k * (32 * sizeof(double) + sizeof(int));
     TPO_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)phi_smem));
     TPO_CUDA(cudaFuncSetAttribute(cluster_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sum_smem));
-    // rows per block for the sums / fused passes: whole 32-row runs per warp, ~2 blocks per SM
-    const int64_t rpf = std::max<int64_t>(rpb, cdiv(cdiv(n, 2 * 148), 256) * 256);
+    // rows per block for the sums / fused passes: whole 32-row runs per warp, ~4 blocks per SM
+    const int64_t rpf = std::max<int64_t>(rpb, cdiv(cdiv(n, 4 * 148), 256) * 256);
     const int64_t nbf = cdiv(n, rpf);
     for (int t = 0; t < Tg; ++t) {
         const bool last = t == Tg - 1;           // the last Phi update is never used
