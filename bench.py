@@ -18,6 +18,7 @@ import json
 import os
 import statistics
 import subprocess
+import threading
 import sys
 import time
 
@@ -46,14 +47,47 @@ def propagation_bytes(n, m, nnz, d):
 
 
 class ClockSampler:
+    """SM clocks and clock-event reasons sampled DURING the timed region: NVML every 2 ms from a
+    background thread (a 50 ms region is shorter than nvidia-smi's start-up), with `nvidia-smi
+    -lms 100` as the fallback when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvmlClocksEventReason*)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index=0):
         self.index = index
         self.p = None
+        self.nv = None
+        self.samples = []
+        self.lines = []
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv = (pynvml, h)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.stop = threading.Event()
+
+            def loop():
+                while True:
+                    try:
+                        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        rs = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)) \
+                            if hasattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons") \
+                            else int(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+                        self.samples.append((sm, rs))
+                    except Exception:
+                        pass
+                    if self.stop.wait(0.002):
+                        break
+            self.th = threading.Thread(target=loop, daemon=True)
+            self.th.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -63,7 +97,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        if self.nv is not None:
+            self.stop.set()
+            self.th.join(timeout=1)
+            return
         if self.p is not None:
             self.p.terminate()
             try:
@@ -74,8 +111,17 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
+        if self.nv is not None:
+            mx = self.mx
+            for f, rs in self.samples:
+                sm.append(f)
+                for nm, bit in self.BITS.items():
+                    if rs & bit:
+                        reasons.add(nm)
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "nvml"}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
                 sm.append(float(f[0]))
@@ -86,7 +132,7 @@ class ClockSampler:
             except (ValueError, IndexError):
                 continue
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 def dist_env():
