@@ -346,3 +346,19 @@ def test_run_host_matches_device_inputs(tpo, weighted):
     lab_h2 = hr(g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, g.X, np.asarray(g.G, np.float64), g.alpha, g.T,
                 B_val=bval, Bt_val=tval).numpy()
     assert np.array_equal(lab_h2, lab_d)
+
+
+@pytest.mark.parametrize("n_p,k", [(20000, 7), (20000, 16), (12345, 20), (9000, 32), (20000, 40), (100, 20)])
+def test_skinny_atb64(tpo, n_p, k):
+    """A^T B of two n_p x k fp64 blocks (the k x k products of Alg. 2 and the Gamma polish):
+    the whole-output skinny kernel (k <= 32, n_p >= 8192) and the dgemm path both match
+    numpy's fp64 product to rounding."""
+    from paper_2405_11922_b200.sharded import GpuSolverOps
+    rng = np.random.default_rng(n_p + k)
+    A = rng.standard_normal((n_p, k))
+    B = rng.standard_normal((n_p, k))
+    ops = GpuSolverOps(n_p, 64, k, "cuda")
+    out = ops.atb(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    ref = A.T @ B
+    scale = np.abs(A).T @ np.abs(B)
+    assert np.max(np.abs(out - ref) / scale) <= 1e-13
