@@ -47,7 +47,7 @@ def propagation_bytes(n, m, nnz, d):
 
 
 class ClockSampler:
-    """SM clocks and clock-event reasons sampled DURING the timed region: NVML every 2 ms from a
+    """SM clocks and clock-event reasons sampled DURING the timed region: NVML every 10 ms from a
     background thread (a 50 ms region is shorter than nvidia-smi's start-up), with `nvidia-smi
     -lms 100` as the fallback when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -81,7 +81,7 @@ class ClockSampler:
                         self.samples.append((sm, rs))
                     except Exception:
                         pass
-                    if self.stop.wait(0.002):
+                    if self.stop.wait(0.010):
                         break
             self.th = threading.Thread(target=loop, daemon=True)
             self.th.start()

@@ -2,6 +2,8 @@
 // error translation.  All arithmetic lives in the module files.
 #include <string.h>
 
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -519,7 +521,7 @@ static void haar_reserve(int &sms, int &launches) {
 // The whole path on device inputs (B, Bt, X, G).  The Haar side stream starts after `g_ready`
 // (recorded on `st` once G is on the device); with `haar_first` its kernels are queued before
 // the propagation's (host inputs: the Haar QR runs while the CSRs and X are still being copied).
-struct RunRes {   // events and the Haar side stream, created before the timed start, released on every exit
+struct RunRes {   // events and the Haar side stream of tpo_run / tpo_run_host (see run_res)
     cudaEvent_t ev[5] = {}, join = nullptr, g_ready = nullptr;
     cudaStream_t side = nullptr;
     RunRes() {
@@ -537,6 +539,17 @@ struct RunRes {   // events and the Haar side stream, created before the timed s
         if (side) cudaStreamDestroy(side);
     }
 };
+
+// One RunRes per (host thread, device), created on first use and reused: no event / stream
+// creation inside a timed call.
+static RunRes &run_res() {
+    int dev = 0;
+    TPO_CUDA(cudaGetDevice(&dev));
+    thread_local std::map<int, std::unique_ptr<RunRes>> cache;
+    auto &r = cache[dev];
+    if (!r) r.reset(new RunRes());
+    return *r;
+}
 
 static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T,
                      int32_t k, const double *G, bool haar_first, cudaEvent_t g_ready, int32_t eig_mode,
@@ -604,7 +617,7 @@ int tpo_run(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, 
         check_ws(ws, ws_bytes, tpo_run_ws(B->n_rows, B->n_cols, B->nnz, d, k, eig_mode, p));
         cudaStream_t st = as_stream(stream);
         Arena ar(ws, ws_bytes);
-        RunRes res;
+        RunRes &res = run_res();
         TPO_CUDA(cudaEventRecord(res.ev[0], st));
         int res_sms = 0, res_launches = 0;
         haar_reserve(res_sms, res_launches);
@@ -642,7 +655,7 @@ int tpo_run_host(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_
         float *Xd = ar.take<float>(n * d);
         double *Gd = ar.take<double>(d * d);
         int32_t *lab = ar.take<int32_t>(n);
-        RunRes res;
+        RunRes &res = run_res();
         TPO_CUDA(cudaEventRecord(res.ev[0], st));
         // inputs in the order the path consumes them: G (the Haar QR starts as soon as it lands;
         // the copy engine serves the copies in issue order), the CSRs (degrees, schedules), X
