@@ -341,6 +341,33 @@ def test_onmf_hand_computed_step():
     assert np.allclose(U, [[math.sqrt(0.75)], [0.5]], atol=1e-9)
 
 
+def test_onmf_hand_computed_step_k2_weighted():
+    """One Alg. 2 step by hand at k = 2 with non-unit dinv, non-unit sigma and a NON-symmetric
+    M = Ups^T (R H), so that a transposed M, a dropped dinv (in R^T Ups or in R H) or Sigma applied
+    on the wrong side of Psi each change the result (Eqs. update-Q / update-Y, PAPER.md:553-560;
+    products bracketed as PAPER.md:564; init Eq. init-HY 571-574 with the R9 clamps).
+
+      R' = [[1,2],[3,1]], dinv = [1, 1/2]  ->  R = diag(dinv) R' = [[1,2],[3/2,1/2]]
+      Gamma = [[1,1],[2,1]]                ->  Ups0 = Gamma (+eps)
+      Psi = [[1/2,2],[1/2,4]], sigma = [2, 1/2]  ->  H0 = Psi Sigma = [[1,1],[1,2]] (+eps)
+    H step:  R^T Ups0 = [[4,5/2],[3,5/2]];  Ups0^T Ups0 = [[5,3],[3,2]];  H0 (Ups0^T Ups0) = [[8,5],[11,7]]
+             H1 = H0 . (R^T Ups0) / (H0 Ups0^T Ups0) = [[1/2,1/2],[3/11,5/7]]
+    Ups step: R H1 = [[23/22,27/14],[39/44,31/28]]
+              M = Ups0^T (R H1) = [[31/11,29/7],[85/44,85/28]]          (M != M^T)
+              Ups0 M = [[209/44,201/28],[333/44,317/28]]
+              Ups1 = Ups0 . sqrt(R H1 / (Ups0 M)) = [[sqrt(46/209), sqrt(54/201)],
+                                                    [2 sqrt(39/333), sqrt(31/317)]]"""
+    Rp = np.array([[1, 2], [3, 1]], np.float32)
+    dinv = np.array([1.0, 0.5], np.float32)
+    Gamma = np.array([[1, 1], [2, 1]], np.float32)
+    Psi = np.array([[0.5, 2], [0.5, 4]], np.float32)
+    sigma = np.array([2.0, 0.5])
+    U, H = O.onmf(Rp, dinv, Gamma, sigma, Psi, 1)
+    assert np.allclose(H, [[0.5, 0.5], [3 / 11, 5 / 7]], rtol=0, atol=1e-10)
+    assert np.allclose(U, [[math.sqrt(46 / 209), math.sqrt(54 / 201)],
+                           [2 * math.sqrt(39 / 333), math.sqrt(31 / 317)]], rtol=0, atol=1e-10)
+
+
 def test_onmf_clamps_negative_numerator():
     """R9: a negative (R H) entry is clamped to 0, so the Ups entry becomes exactly 0."""
     Rp = np.array([[-2, 0], [0, 1]], np.float32)
