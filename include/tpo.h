@@ -81,7 +81,8 @@ uint64_t tpo_launch_count(void);
  *   alpha in [0, 1], T >= 0.
  * Workspace: tpo_propagate_ws(n_u, n_v, nnz, d).
  * Errors: TPO_EINVAL (shapes of B/Bt/X disagree, Bt.nnz != B.nnz, alpha/T/d out of range,
- * null or misaligned pointers), TPO_ENOMEM, TPO_ECUDA.
+ * null or misaligned pointers, max(n_u, n_v) * d/4 >= 2^32: the SpMM gathers use 32-bit row
+ * offsets), TPO_ENOMEM, TPO_ECUDA.
  * --------------------------------------------------------------------------------------- */
 size_t tpo_propagate_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d);
 int tpo_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d,
@@ -128,7 +129,7 @@ int tpo_shard_uside(const tpo_csr_t *Bp, const float *Q, const float *Xp, int64_
  * --------------------------------------------------------------------------------------- */
 int tpo_haar_q(const double *G, int64_t d, double *Q);
 /* The same factor computed on the device (block Gram-Schmidt with re-orthogonalisation over
- * 64-column panels, each panel by CholeskyQR2; the QR with diag(R) > 0 is unique, so this is
+ * 112-column panels, each panel by CholeskyQR2; the QR with diag(R) > 0 is unique, so this is
  * the Q of tpo_haar_q up to rounding), written as fp32 for tpo_features.
  *   G: (host) d x d fp64;  Q: d x d fp32 out (device).  [sync].
  * Workspace: tpo_haar_q_dev_ws(d).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC. */
@@ -166,9 +167,11 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
  * a7  Top-k singular triplets of R = diag(dinv) R' -- "the top-k left and right singular
  * vectors of R" and its top-k singular values (Eq. init-HY).
  *   mode TPO_EIG_EXACT (R7): the exact top-k.  Gram G = R^T R (D x D, fp64 cross-block
- *     sums), host fp64 symmetric eigensolve, Gamma = R Psi Sigma^{-1}, CholeskyQR2 polish
- *     when ||Gamma^T Gamma - I||_max > 1e-6.  Equivalent to block subspace iteration on
- *     S~ with a full-rank block (b = D), which converges in one step.
+ *     sums), its top-k eigenpairs by a Chebyshev-filtered block subspace iteration on the
+ *     device (fp64; the trivial pair u = r/||r||, G r = R'^T 1 = r, deflated; Rayleigh-Ritz
+ *     with the full G; stop at max Ritz residual <= 1e-9 lambda_1, else TPO_ENUMERIC after
+ *     60 rounds), Gamma = R Psi Sigma^{-1}, CholeskyQR2 polish when
+ *     ||Gamma^T Gamma - I||_max > 1e-6.
  *   mode TPO_EIG_HALKO: the randomised truncated SVD the paper cites (Halko et al.,
  *     PAPER.md:574) with b = k + p columns, q power iterations, orthonormalisation by
  *     CholeskyQR2, Rayleigh-Ritz on the host.  Omega (D x b fp32) is its Gaussian test
@@ -177,12 +180,13 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
  *   Rp: n x D fp32;  dinv: n fp32;  1 <= k <= min(n, D) (HALKO: k + p <= min(n, D)).
  *   Gamma: n x k fp32 out;  sigma: (host) k fp64 out, descending;  Psi: D x k fp32 out.
  * [sync].  Workspace: tpo_topk_eig_ws(n, D, k, mode, p).
- * Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC (sigma_k == 0, non-SPD Gram).
+ * Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC (sigma_k == 0, non-SPD Gram, the
+ * subspace iteration not converged).
  * --------------------------------------------------------------------------------------- */
 enum { TPO_EIG_EXACT = 0, TPO_EIG_HALKO = 1 };
 /* a7 step 1 on its own: G = R^T R = R'^T diag(dinv^2) R' (D x D fp64 out, full symmetric
  * matrix), the Gram of the exact mode.  tcgen05 kind::tf32 with 3xTF32 splitting of R
- * (fp32-accurate products), fp32 accumulation over 256-row segments, fp64 across segments.
+ * (fp32-accurate products), fp32 accumulation over 128-row segments, fp64 across segments.
  *   Rp: n x D fp32, D % 4 == 0;  dinv: n fp32;  G: D x D fp64 out (device).
  * Workspace: tpo_gram_ws(n, D).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA. */
 size_t tpo_gram_ws(int64_t n, int64_t D);

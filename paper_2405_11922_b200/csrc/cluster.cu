@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(NW * 32) nci_fused_kernel(const double *__rest
             double sc = 0.0;
 #pragma unroll
             for (int a = 0; a < KM; ++a)
-                if (a < k) sc = fma(u[a], phs[a * k + l], sc);
+                if (a < k) sc = __dadd_rn(sc, __dmul_rn(u[a], phs[a * k + l]));   // unfused, as the oracle
             if (l == 0 || sc > best) { best = sc; arg = l; }
         }
         if (ok) {

@@ -196,80 +196,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// out[i, b0 + c] = rs_i * sum_j A[i, j] W[j, b0 + c]
-template <class TO, int QW>
-__global__ void __launch_bounds__(SN) aw_stream_kernel(const float *__restrict__ A, int64_t lda,
-                                                       const float *__restrict__ rs, const double *__restrict__ W,
-                                                       int64_t n, int p, int q, TO *__restrict__ out, int64_t ldo) {
-    constexpr int CW = QW / 4;
-    __shared__ __align__(16) float As[2][SR * SP];
-    __shared__ __align__(16) double Ws[2][SK * QW];
-    const int t = threadIdx.x, rg = t >> 2, cg = t & 3;
-    const int64_t i0 = (int64_t)blockIdx.x * SR;
-    const int b0 = blockIdx.y * QW;
-    const int nslab = (p + SK - 1) / SK;
-    double acc[4][CW];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-    auto load = [&](int s, int buf) {
-        const int k0 = s * SK;
-#pragma unroll
-        for (int m = 0; m < (SR * SK / 4) / SN; ++m) {
-            const int ch = t + SN * m, row = ch >> 3, kc = (ch & 7) * 4;
-            const int64_t gi = i0 + row;
-            const bool ok = gi < n && k0 + kc < p;
-            cp_async16(&As[buf][row * SP + kc], ok ? (const void *)(A + gi * lda + k0 + kc) : (const void *)A, ok);
-        }
-        cp_async_commit();
-        for (int e = t; e < SK * QW; e += SN) {
-            const int kk = e / QW, c = e - kk * QW;
-            Ws[buf][e] = (k0 + kk < p && b0 + c < q) ? W[(int64_t)(k0 + kk) * q + b0 + c] : 0.0;
-        }
-    };
-    load(0, 0);
-    for (int s = 0; s < nslab; ++s) {
-        const int buf = s & 1;
-        if (s + 1 < nslab) {
-            load(s + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const float *a = As[buf];
-        const double *w = Ws[buf];
-#pragma unroll 8
-        for (int kk = 0; kk < SK; ++kk) {
-            double av[4], wv[CW];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) av[r] = (double)a[(rg + 32 * r) * SP + kk];
-#pragma unroll
-            for (int c = 0; c < CW; ++c) wv[c] = w[kk * QW + cg * CW + c];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], wv[c], acc[r][c]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t row = i0 + rg + 32 * r;
-        if (row >= n) continue;
-        const double sc = rs ? (double)rs[row] : 1.0;
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-            const int col = b0 + cg * CW + c;
-            if (col < q) out[row * ldo + col] = (TO)(sc * acc[r][c]);
-        }
-    }
-}
-
-// The same product with 2 column groups instead of 4: a thread owns 2 rows (strided by 64) and
-// CW = QW / 2 columns, so each fp32 element of A is widened twice instead of four times (the
-// F2F widening runs on the quarter-rate XU pipe and bounded the 4-group tiling) and QW may be
+// out[i, b0 + c] = rs_i * sum_j A[i, j] W[j, b0 + c] with 2 column groups: a thread owns 2 rows
+// (strided by 64) and CW = QW / 2 columns, so each fp32 element of A is widened twice (the F2F
+// widening runs on the quarter-rate XU pipe; a 4-group tiling was bound by it) and QW may be
 // any even width (k = 10 needs 10 columns, not 12).
 template <class TO, int QW>
 __global__ void __launch_bounds__(SN) aw2_stream_kernel(const float *__restrict__ A, int64_t lda,
@@ -523,32 +452,17 @@ void aw_f32_run(const float *A, int64_t lda, const float *rs, const double *W, i
         aw_run<float, TO>(A, lda, rs, W, n, p, q, out, ldo, st);
         return;
     }
-    if (!getenv("TPO_AW4")) {   // 2 column groups, even chunk widths <= 22 (static smem) fitted to q
-        const int64_t nch2 = cdiv(q, 22);
-        const int QW2 = (int)(cdiv(cdiv(q, nch2), 2) * 2);
-        const dim3 grid2((unsigned)cdiv(n, SR), (unsigned)cdiv(q, QW2));
+    // 2 column groups, even chunk widths <= 22 (static smem) fitted to q
+    const int64_t nch2 = cdiv(q, 22);
+    const int QW2 = (int)(cdiv(cdiv(q, nch2), 2) * 2);
+    const dim3 grid2((unsigned)cdiv(n, SR), (unsigned)cdiv(q, QW2));
 #define TPO_AW2(QV) case QV: aw2_stream_kernel<TO, QV><<<grid2, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        switch (QW2) {
-            TPO_AW2(2) TPO_AW2(4) TPO_AW2(6) TPO_AW2(8) TPO_AW2(10) TPO_AW2(12) TPO_AW2(14) TPO_AW2(16)
-            TPO_AW2(18) TPO_AW2(20)
-            default: aw2_stream_kernel<TO, 22><<<grid2, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        }
+    switch (QW2) {
+        TPO_AW2(2) TPO_AW2(4) TPO_AW2(6) TPO_AW2(8) TPO_AW2(10) TPO_AW2(12) TPO_AW2(14) TPO_AW2(16)
+        TPO_AW2(18) TPO_AW2(20)
+        default: aw2_stream_kernel<TO, 22><<<grid2, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
+    }
 #undef TPO_AW2
-        TPO_LAUNCH_CHECK();
-        return;
-    }
-    // q chunk width QW (a multiple of 4, <= 24: static smem) fitted to q: little padding for any k
-    const int64_t nch = cdiv(q, 24);
-    const int QW = (int)(cdiv(cdiv(q, nch), 4) * 4);
-    const dim3 grid((unsigned)cdiv(n, SR), (unsigned)cdiv(q, QW));
-    switch (QW) {
-        case 4: aw_stream_kernel<TO, 4><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        case 8: aw_stream_kernel<TO, 8><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        case 12: aw_stream_kernel<TO, 12><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        case 16: aw_stream_kernel<TO, 16><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        case 20: aw_stream_kernel<TO, 20><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-        default: aw_stream_kernel<TO, 24><<<grid, SN, 0, st>>>(A, lda, rs, W, n, (int)p, (int)q, out, ldo); break;
-    }
     TPO_LAUNCH_CHECK();
 }
 

@@ -344,7 +344,12 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         cholqr2_f64(V, T, D, b, flag, ar, st);
     };
     orth_against_u();
-    const int max_rounds = 60;
+    // 60 rounds; TPO_EIG_MAX_ROUNDS lowers the cap (tests of the no-convergence error only)
+    const int max_rounds = [] {
+        const char *e = getenv("TPO_EIG_MAX_ROUNDS");
+        const int v = e ? atoi(e) : 60;
+        return v >= 0 && v <= 60 ? v : 60;
+    }();
     int m = 8;
     std::vector<double> w(bz), E(bz * bz);
     double bnd = 0.0;
@@ -405,6 +410,9 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
         }
         if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
             check_flag(flag, st, "top-k subspace iteration (CholeskyQR2)");
+            if (!(rmax <= 1e-9 * fabs(w[0])))
+                throw Error(TPO_ENUMERIC, "top-k subspace iteration did not converge in " + std::to_string(max_rounds) +
+                                              " rounds: max Ritz residual / lambda_1 = " + std::to_string(rmax / fabs(w[0])));
             lam.assign(w.begin(), w.begin() + k);
             ar.off = mark;
             return;
@@ -547,15 +555,8 @@ __global__ void copy2d_kernel(const double *__restrict__ src, int64_t lds, doubl
 
 // panel width of the device Haar QR (<= 112, the one-CTA Cholesky-inverse limit; since the
 // second CholeskyQR pass skips the factorisation, wide panels are fastest: d = 1000 takes
-// 2.8 / 3.2 / 5.2 ms with 112 / 64 / 32 columns); TPO_HAAR_PANEL overrides (tuning)
-int64_t haar_panel(int64_t d) {
-    int64_t bw = 112;
-    if (const char *e = getenv("TPO_HAAR_PANEL")) {
-        const int64_t v = atoll(e);
-        if (v >= 16 && v <= 112) bw = v;
-    }
-    return std::min<int64_t>(bw, d);
-}
+// 2.8 / 3.2 / 5.2 ms with 112 / 64 / 32 columns)
+int64_t haar_panel(int64_t d) { return std::min<int64_t>(112, d); }
 
 size_t haar_q_ws_bytes(int64_t d) {
     const int64_t bw = std::min<int64_t>(112, d);
@@ -564,7 +565,7 @@ size_t haar_q_ws_bytes(int64_t d) {
 }
 
 // Alg. 1 L6-7 on the device: Q of the unique QR (diag(R) > 0) of the d x d Gaussian G by
-// block classical Gram-Schmidt with re-orthogonalisation (BCGS2) over 64-column panels, each
+// block classical Gram-Schmidt with re-orthogonalisation (BCGS2) over 112-column panels, each
 // panel orthonormalised by CholeskyQR2.  R is block upper triangular with upper triangular,
 // positive-diagonal blocks, so Q is the same unique factor the host routine returns.  No
 // host round trip until the final failure-flag check.

@@ -85,11 +85,20 @@ void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cud
     ar.off = mark;
 }
 
+// r is staged in 8 * D bytes of dynamic shared memory: above the default 48 KB (D > 6144)
+// the kernel must opt in to the larger carve-out first.
+void launch_dinv(const float *Rp, int64_t n, int64_t D, const double *r, float *dinv, cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)D;
+    if (smem > 48 * 1024)
+        TPO_CUDA(cudaFuncSetAttribute(dinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dinv_kernel<<<cdiv(n * 32, 256), 256, smem, st>>>(Rp, n, (int)D, r, dinv);
+    TPO_LAUNCH_CHECK();
+}
+
 // dinv from a given (global) r: the per-row half of tpo_features (sharded path)
 void dinv_from_r(const float *Rp, int64_t n, int64_t D, const double *r, float *dinv, cudaStream_t st) {
     if (n == 0) return;
-    dinv_kernel<<<cdiv(n * 32, 256), 256, sizeof(double) * D, st>>>(Rp, n, (int)D, r, dinv);
-    TPO_LAUNCH_CHECK();
+    launch_dinv(Rp, n, D, r, dinv, st);
 }
 
 // R' of the given rows and their fp64 column sums (the shard's partial r)
@@ -131,9 +140,7 @@ void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, floa
         ar.off = mark;
     }
     colsum_run(Rp, n, D, G, part, r, st);
-    const int TB = 256;
-    dinv_kernel<<<cdiv(n * 32, TB), TB, sizeof(double) * D, st>>>(Rp, n, D, r, dinv);
-    TPO_LAUNCH_CHECK();
+    launch_dinv(Rp, n, D, r, dinv, st);
 }
 
 }  // namespace tpo

@@ -116,8 +116,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-__device__ float *g_gram_dbg = nullptr;   // debug dump (set by tpo__gram_debug), normally null
-
 struct GramArgs {
     int n_tiles;        // T = ceil(D / 128)
     int ksplit;         // row splits
@@ -211,12 +209,6 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant
                 const int s = kb % STAGES, j = kb / STAGES;
                 mbar_wait(smem_u32(&bars[s]), j & 1);
                 fence_after();
-                if (g_gram_dbg && blockIdx.x == 0 && kb == 0) {
-                    const float *st0 = reinterpret_cast<const float *>(smem);
-                    g_gram_dbg[lane] = st0[lane];
-                    g_gram_dbg[32 + lane] = st0[OPER / 4 + lane];
-                    g_gram_dbg[64 + lane] = st0[32 + lane];
-                }
                 if (lane == 0) {
                     const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
                     const uint32_t ahi = base, alo = base + OPER;
@@ -252,13 +244,6 @@ gram_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant
             const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + buf * TILE + 64 * h;
             float v[32];
             tmem_ld32(taddr, v);
-            if (g_gram_dbg && blockIdx.x == 0 && seg == 0 && warp == 2 && lane == 0)
-                for (int i = 0; i < 32; ++i) g_gram_dbg[96 + i] = v[i];
-            if (g_gram_dbg && blockIdx.x == 0 && seg == 0 && warp == 2 && lane == 0) {
-                g_gram_dbg[128] = __uint_as_float(tmem_base);
-                g_gram_dbg[129] = (float)nkb;
-                g_gram_dbg[130] = (float)nseg;
-            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] += (double)v[i];
             tmem_ld32(taddr + 32, v);
@@ -600,8 +585,6 @@ void features_tc(const float *Zhat, int64_t n, int64_t d, const float *Q, float 
     features_tc_kernel<<<grid, FT_THREADS, smem, st>>>(a_hi, a_lo, b_hi, b_lo, n, (int)d, Rp);
     TPO_LAUNCH_CHECK();
 }
-
-void gram_debug_set(float *p) { TPO_CUDA(cudaMemcpyToSymbol(g_gram_dbg, &p, sizeof(p))); }
 
 size_t gram_tc_ws(int64_t n, int64_t D) {
     const GramPlan p = plan(n, D);

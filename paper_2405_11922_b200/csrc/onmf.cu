@@ -22,84 +22,10 @@ namespace {
 constexpr int NTR = 128;                    // onmf_rtu block: 128 threads x CPT columns
 constexpr int RT = 64;                      // rows of dinv.Ups staged per tile (onmf_rtu)
 
-template <int CPT, int KC>
-__global__ void __launch_bounds__(NTR, 4) onmf_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
-                                                      const float *__restrict__ dinv,
-                                                      const double *__restrict__ U, int k, int64_t rows_per,
-                                                      double *__restrict__ part) {
-    __shared__ double Ys[RT][KC];
-    const int t = threadIdx.x;
-    const int64_t g = blockIdx.x;
-    const int a0 = blockIdx.y * (NTR * CPT);
-    const int k0 = blockIdx.z * KC;
-    const int kc = min(KC, k - k0);
-    const int64_t r0 = g * rows_per, r1 = min(n, r0 + rows_per);
-    int col[CPT];
-    bool cv[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-        col[c] = a0 + t + NTR * c;
-        cv[c] = col[c] < D;
-    }
-    double acc[CPT][KC];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c)
-#pragma unroll
-        for (int l = 0; l < KC; ++l) acc[c][l] = 0.0;
-    for (int64_t tb = r0; tb < r1; tb += RT) {
-        const int rows = (int)min((int64_t)RT, r1 - tb);
-        __syncthreads();
-        for (int e = t; e < RT * KC; e += NTR) {
-            const int r = e / KC, l = e - r * KC;
-            double v = 0.0;
-            if (r < rows && l < kc) v = (double)dinv[tb + r] * U[(tb + r) * k + k0 + l];
-            Ys[r][l] = v;
-        }
-        __syncthreads();
-        int r = 0;
-        for (; r + 4 <= rows; r += 4) {
-            float rv[4][CPT];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int c = 0; c < CPT; ++c) rv[u][c] = cv[c] ? __ldg(Rp + (tb + r + u) * D + col[c]) : 0.f;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-#pragma unroll
-                for (int l = 0; l < KC; ++l) {
-                    const double y = Ys[r + u][l];
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) acc[c][l] = fma((double)rv[u][c], y, acc[c][l]);
-                }
-            }
-        }
-        for (; r < rows; ++r) {
-            float rv[CPT];
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) rv[c] = cv[c] ? __ldg(Rp + (tb + r) * D + col[c]) : 0.f;
-#pragma unroll
-            for (int l = 0; l < KC; ++l) {
-                const double y = Ys[r][l];
-#pragma unroll
-                for (int c = 0; c < CPT; ++c) acc[c][l] = fma((double)rv[c], y, acc[c][l]);
-            }
-        }
-    }
-    // part[g][a][l] (the chunk's columns only)
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-        if (!cv[c]) continue;
-#pragma unroll
-        for (int l = 0; l < KC; ++l)
-            if (l < kc) part[(g * D + col[c]) * (int64_t)k + k0 + l] = acc[c][l];
-    }
-}
-
-// The same product with the R' rows and the Ups / dinv rows staged through an RS-stage cp.async
-// ring (RTS rows per stage): the loads of the next stages are in flight while a stage is
-// multiplied (the direct-load kernel keeps only 4 rows per thread in flight: MLP-bound on
-// HBM).  Per (column, l) the rows are accumulated in the same order as onmf_rtu_kernel, so the
-// results are bit-identical.
+// part[g] = R'^T (dinv . U) over the rows of split g, with the R' rows and the Ups / dinv rows
+// staged through an RS-stage cp.async ring (RTS rows per stage): the loads of the next stages
+// are in flight while a stage is multiplied (a direct-load kernel keeping 4 rows per thread in
+// flight was MLP-bound on HBM).  Per (column, l) the rows are accumulated in row order.
 constexpr int RTS = 8, RS = 4;
 __device__ __forceinline__ void cpa16(void *sm, const void *g, bool v) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
@@ -268,33 +194,19 @@ void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float
     const dim3 grid((unsigned)p.G, (unsigned)p.ncb, (unsigned)p.nkc);
     // only CPT x KC <= 64 (or CPT = 1) is planned (rtu_plan); the other combinations are not instantiated
     constexpr int C8 = 8 * KC <= 64 ? 8 : 1, C4 = 4 * KC <= 64 ? 4 : 1, C2 = 2 * KC <= 64 ? 2 : 1;
-    static const bool pipe = [] {
-        const char *e = getenv("TPO_RTU_PIPE");
-        return e ? atoi(e) != 0 : true;
-    }();
-    if (pipe) {
 #define TPO_RTU_PIPE(CPTV)                                                                                   \
     {                                                                                                        \
         constexpr size_t sm = rtu_pipe_smem<CPTV, KC>();                                                     \
         TPO_CUDA(cudaFuncSetAttribute(onmf_rtu_pipe_kernel<CPTV, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
         onmf_rtu_pipe_kernel<CPTV, KC><<<grid, NTR, sm, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part);      \
     }
-        switch (p.cpt) {
-            case 1: TPO_RTU_PIPE(1) break;
-            case 2: TPO_RTU_PIPE(C2) break;
-            case 4: TPO_RTU_PIPE(C4) break;
-            default: TPO_RTU_PIPE(C8) break;
-        }
-#undef TPO_RTU_PIPE
-        TPO_LAUNCH_CHECK();
-        return;
-    }
     switch (p.cpt) {
-        case 1: onmf_rtu_kernel<1, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
-        case 2: onmf_rtu_kernel<C2, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
-        case 4: onmf_rtu_kernel<C4, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
-        default: onmf_rtu_kernel<C8, KC><<<grid, NTR, 0, st>>>(Rp, n, D, dinv, U, k, p.rows_per, part); break;
+        case 1: TPO_RTU_PIPE(1) break;
+        case 2: TPO_RTU_PIPE(C2) break;
+        case 4: TPO_RTU_PIPE(C4) break;
+        default: TPO_RTU_PIPE(C8) break;
     }
+#undef TPO_RTU_PIPE
     TPO_LAUNCH_CHECK();
 }
 

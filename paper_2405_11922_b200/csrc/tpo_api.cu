@@ -16,7 +16,6 @@ namespace tpo {
 
 size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d);
 size_t features_ws_bytes(int64_t n, int64_t d);
-void gram_debug_set(float *p);
 size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p);
 size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k);
 
@@ -50,6 +49,14 @@ void check_csr(const tpo_csr_t *A, const char *name) {
     TPO_REQUIRE(A->nnz == 0 || A->col_idx != nullptr, std::string(name) + ".col_idx is NULL");
 }
 
+// The SpMM gathers address a row of the gathered table with a 32-bit float4 offset
+// (col * d/4 for a row-major table, col * group width for a column-group table), so every
+// gathered table must hold fewer than 2^32 float4.
+void check_gather_range(int64_t rows, int64_t d, const char *what) {
+    TPO_REQUIRE(rows * (d / 4) < (int64_t(1) << 32),
+                std::string(what) + ": rows x d/4 >= 2^32 exceeds the SpMM's 32-bit gather offsets");
+}
+
 void check_ws(void *ws, size_t have, size_t need) {
     if (have < need) throw Error(TPO_ENOMEM, "workspace too small: " + std::to_string(have) + " < " + std::to_string(need));
     TPO_REQUIRE(ws != nullptr || need == 0, "ws is NULL");
@@ -65,6 +72,8 @@ void check_propagate(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
     TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
     TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
     TPO_REQUIRE(T >= 0, "T must be >= 0");
+    check_gather_range(B->n_rows, d, "Z (gathered by the V-side SpMM)");
+    check_gather_range(B->n_cols, d, "the V-side block (gathered by the U-side SpMM)");
     if (B->n_rows > 0) {
         check_ptr(X, "X");
         check_ptr(Z, "Z");
@@ -134,6 +143,7 @@ int tpo_shard_vside(const tpo_csr_t *Btp, const float *Pp, int64_t d, float *Qpa
     return guarded([&] {
         check_csr(Btp, "Btp");
         TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        check_gather_range(Btp->n_cols, d, "Pp (gathered by the V-side SpMM)");
         if (Btp->n_rows) check_ptr(Qpart, "Qpart");
         if (Btp->n_cols) check_ptr(Pp, "Pp");
         check_ws(ws, ws_bytes, tpo_shard_ws(Btp->n_rows, Btp->nnz, d));
@@ -158,6 +168,7 @@ int tpo_shard_uside(const tpo_csr_t *Bp, const float *Q, const float *Xp, int64_
     return guarded([&] {
         check_csr(Bp, "Bp");
         TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        check_gather_range(Bp->n_cols, d, "Q (gathered by the U-side SpMM)");
         TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
         if (Bp->n_rows) {
             check_ptr(Xp, "Xp");
@@ -234,7 +245,6 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
 }
 
 // undocumented debugging hook (not part of include/tpo.h)
-int tpo__gram_debug(float *p) { return guarded([&] { tpo::gram_debug_set(p); }); }
 
 size_t tpo_gram_ws(int64_t n, int64_t D) { return gram_tc_ws(n, D) + 1024; }
 

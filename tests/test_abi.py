@@ -57,6 +57,20 @@ def test_validation_errors_without_gpu(L):
     assert rc == TPO_EINVAL and b"nnz" in L.tpo_last_error()
     rc = L.tpo_propagate(C.byref(B), C.byref(Bt), 16, 8, 0.5, 2, 16, None, 256, 10, None)
     assert rc == TPO_ENOMEM
+    # gathered tables of >= 2^32 float4 would wrap the SpMM's 32-bit gather offsets: rejected
+    # (20 M U rows at d = 1000 is 5e9 float4)
+    Bbig = CSR(20_000_000, 5, 0, 16, 0, None)
+    Btbig = CSR(5, 20_000_000, 0, 16, 0, None)
+    rc = L.tpo_propagate(C.byref(Bbig), C.byref(Btbig), 16, 1000, 0.5, 2, 16, None, None, 0, None)
+    assert rc == TPO_EINVAL and b"32-bit gather offsets" in L.tpo_last_error()
+    Bwide = CSR(5, 20_000_000, 0, 16, 0, None)       # V side too large (gathered by the U-side SpMM)
+    Btwide = CSR(20_000_000, 5, 0, 16, 0, None)
+    rc = L.tpo_propagate(C.byref(Bwide), C.byref(Btwide), 16, 1000, 0.5, 2, 16, None, None, 0, None)
+    assert rc == TPO_EINVAL and b"32-bit gather offsets" in L.tpo_last_error()
+    rc = L.tpo_shard_vside(C.byref(Btbig), 16, 1000, 16, None, 0, None)
+    assert rc == TPO_EINVAL and b"32-bit gather offsets" in L.tpo_last_error()
+    rc = L.tpo_shard_uside(C.byref(Bwide), 16, 16, 1000, 0.5, 16, 0, 16, None, None, 0, None)
+    assert rc == TPO_EINVAL and b"32-bit gather offsets" in L.tpo_last_error()
     rc = L.tpo_topk_eig(16, 16, 100, 8, 9, 0, 0, 0, None, 16, None, 16, 256, 1 << 30, None)
     assert rc == TPO_EINVAL and b"k must" in L.tpo_last_error()
     rc = L.tpo_topk_eig(16, 16, 100, 8, 2, 7, 0, 0, None, 16, None, 16, 256, 1 << 30, None)

@@ -227,6 +227,20 @@ def test_topk_exact_tiny(tpo, tiny_feats, tiny_topk):
     assert np.all(Gm.astype(np.float64).sum(0) >= 0)                 # R8
 
 
+def test_topk_not_converged_is_an_error(tpo, tiny_feats, monkeypatch):
+    """A subspace iteration that runs out of rounds before its Ritz residuals reach 1e-9 lambda_1
+    returns TPO_ENUMERIC instead of unconverged vectors (TPO_EIG_MAX_ROUNDS lowers the cap)."""
+    from paper_2405_11922_b200._lib import TPO_ENUMERIC, TpoError
+    g, Rp, dinv = tiny_feats
+    monkeypatch.setenv("TPO_EIG_MAX_ROUNDS", "0")
+    with pytest.raises(TpoError) as ei:
+        tpo.topk_eig(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), g.k)
+    assert ei.value.code == TPO_ENUMERIC and "did not converge" in str(ei.value)
+    monkeypatch.delenv("TPO_EIG_MAX_ROUNDS")
+    Gm, s, Ps = tpo.topk_eig(torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), g.k)
+    assert abs(s[0] - 1.0) < 1e-5
+
+
 def test_topk_planted_svd(tpo):
     """E8: R' = U diag(s) V^T with dinv = 1 -> Gamma = U[:, :k], sigma = s[:k]."""
     rng = np.random.default_rng(3)
