@@ -6,7 +6,9 @@
  * header, table or helper with the CUDA library under paper_2405_11922_b200/csrc/.
  *
  * Every function follows the paper's definition or algorithm in the paper's order,
- * in fp64, on fp32 inputs widened to double.  Citations are PAPER.md line numbers
+ * in fp64, on fp32 inputs widened to double.  OpenMP loops only split independent
+ * outputs across threads: every sum is accumulated by one thread in its serial order,
+ * so the results do not depend on the thread count.  Citations are PAPER.md line numbers
  * (LaTeX source) plus the equation / algorithm label.  Readings of silent or garbled
  * passages are the ones listed in DESIGN.md "Readings" (R1..R12).
  *
@@ -50,8 +52,10 @@ void oracle_degree_scales(int64_t n, int64_t m, const int64_t *rowptr, const int
  *      Z_0 = c X,   Z <- c X + alpha * L (L^T Z)   (T times),
  * c = (1 - alpha) (R1: Lemma 1's prefactor; c = 1 at alpha = 1, the Alg. 1 limit).
  * Then Zhat = row-L2-normalised Z (Eq. Z), zero rows stay zero (R4).
- * Only CSR(B) is used: L^T Z is formed by scattering over B's rows, so this oracle
- * never reads CSR(B^T).
+ * Only CSR(B) is used: for L^T Z the oracle builds its own transposed edge list of B by a
+ * stable counting sort (each v's incident edges in ascending u order) and sums
+ * Y[v] = sum_u L[u,v] Z[u] in that order -- the order a serial scatter over B's rows adds
+ * them in -- so it never reads the caller's CSR(B^T).
  * Z, Zhat: n x d row-major doubles (Zhat may be NULL).
  * ------------------------------------------------------------------------------------ */
 void oracle_propagate(int64_t n, int64_t m, const int64_t *rowptr, const int32_t *col,
@@ -61,18 +65,38 @@ void oracle_propagate(int64_t n, int64_t m, const int64_t *rowptr, const int32_t
     oracle_degree_scales(n, m, rowptr, col, val, s_u, s_v);
     const double c = (alpha < 1.0) ? (1.0 - alpha) : 1.0;
     for (int64_t i = 0; i < n * d; ++i) Z[i] = c * (double)X[i];
-    double *Y = dalloc((size_t)(m * d));
-    for (int32_t t = 0; t < T; ++t) {
-        /* Y = L^T Z :  Y[v] += L[u,v] * Z[u] */
-        memset(Y, 0, sizeof(double) * (size_t)(m * d));
+    /* transposed edge list: for each v, (u, L[u,v]) in ascending u */
+    const int64_t E = rowptr[n];
+    int64_t *tptr = (int64_t *)calloc((size_t)(m + 1), sizeof(int64_t));
+    int64_t *tu = (int64_t *)malloc(sizeof(int64_t) * (size_t)(E ? E : 1));
+    double *tL = dalloc((size_t)E);
+    for (int64_t e = 0; e < E; ++e) tptr[col[e] + 1]++;
+    for (int64_t v = 0; v < m; ++v) tptr[v + 1] += tptr[v];
+    {
+        int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m ? m : 1));
+        for (int64_t v = 0; v < m; ++v) fill[v] = tptr[v];
         for (int64_t u = 0; u < n; ++u)
             for (int64_t e = rowptr[u]; e < rowptr[u + 1]; ++e) {
                 const int64_t v = col[e];
-                const double L = (val ? (double)val[e] : 1.0) * s_u[u] * s_v[v];
-                const double *zu = Z + u * d;
-                double *yv = Y + v * d;
+                tu[fill[v]] = u;
+                tL[fill[v]] = (val ? (double)val[e] : 1.0) * s_u[u] * s_v[v];
+                fill[v]++;
+            }
+        free(fill);
+    }
+    double *Y = dalloc((size_t)(m * d));
+    for (int32_t t = 0; t < T; ++t) {
+        /* Y = L^T Z :  Y[v] = sum_u L[u,v] * Z[u] */
+#pragma omp parallel for schedule(static)
+        for (int64_t v = 0; v < m; ++v) {
+            double *yv = Y + v * d;
+            for (int64_t j = 0; j < d; ++j) yv[j] = 0.0;
+            for (int64_t q = tptr[v]; q < tptr[v + 1]; ++q) {
+                const double L = tL[q];
+                const double *zu = Z + tu[q] * d;
                 for (int64_t j = 0; j < d; ++j) yv[j] += L * zu[j];
             }
+        }
         /* Z = c X + alpha * L Y */
 #pragma omp parallel for schedule(static)
         for (int64_t u = 0; u < n; ++u) {
@@ -87,6 +111,7 @@ void oracle_propagate(int64_t n, int64_t m, const int64_t *rowptr, const int32_t
             for (int64_t j = 0; j < d; ++j) zu[j] = c * (double)X[u * d + j] + alpha * zu[j];
         }
     }
+    free(tptr); free(tu); free(tL);
     if (Zhat) {
         for (int64_t u = 0; u < n; ++u) {
             double s = 0.0;
@@ -122,6 +147,7 @@ static void householder_qr(int64_t rows, int64_t cols, double *A, double *Q, dou
         if (vn > 0.0) {
             const double inv = 1.0 / sqrt(vn);
             for (int64_t i = j; i < rows; ++i) V[i * cols + j] *= inv;
+#pragma omp parallel for schedule(static)
             for (int64_t c2 = j; c2 < cols; ++c2) {           /* A[j:, j:] <- (I - 2 v v^T) A */
                 double s = 0.0;
                 for (int64_t i = j; i < rows; ++i) s += V[i * cols + j] * A[i * cols + c2];
@@ -138,6 +164,7 @@ static void householder_qr(int64_t rows, int64_t cols, double *A, double *Q, dou
     for (int64_t i = 0; i < rows; ++i)
         for (int64_t j = 0; j < cols; ++j) Q[i * cols + j] = (i == j) ? 1.0 : 0.0;
     for (int64_t j = cols - 1; j >= 0; --j)
+#pragma omp parallel for schedule(static)
         for (int64_t c2 = 0; c2 < cols; ++c2) {
             double s = 0.0;
             for (int64_t i = j; i < rows; ++i) s += V[i * cols + j] * Q[i * cols + c2];
@@ -189,9 +216,13 @@ void oracle_features(int64_t n, int64_t d, const float *Zhat, const float *Q, do
             Rp[i * D + d + j] = amp * cos(zo);
         }
     }
-    for (int64_t j = 0; j < D; ++j) r[j] = 0.0;
-    for (int64_t i = 0; i < n; ++i)
-        for (int64_t j = 0; j < D; ++j) r[j] += Rp[i * D + j];
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < D; ++j) {
+        double rj = 0.0;
+        for (int64_t i = 0; i < n; ++i) rj += Rp[i * D + j];
+        r[j] = rj;
+    }
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         double t = 0.0;
         for (int64_t j = 0; j < D; ++j) t += Rp[i * D + j] * r[j];
@@ -207,8 +238,9 @@ void oracle_features(int64_t n, int64_t d, const float *Zhat, const float *Q, do
 void oracle_affinity_matvec(int64_t n, int64_t D, const float *Rp, const float *dinv,
                             const double *Y, int64_t b, double *out) {
     double *W = dalloc((size_t)(D * b));
-    for (int64_t i = 0; i < n; ++i)
-        for (int64_t j = 0; j < D; ++j) {
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < D; ++j)
+        for (int64_t i = 0; i < n; ++i) {
             const double rij = (double)dinv[i] * (double)Rp[i * D + j];
             for (int64_t c = 0; c < b; ++c) W[j * b + c] += rij * Y[i * b + c];
         }
@@ -388,15 +420,16 @@ void oracle_onmf(int64_t n, int64_t D, int32_t k, const float *Rp, const float *
         /* R^T Ups and Ups^T Ups */
         memset(RtU, 0, sizeof(double) * (size_t)(D * k));
         memset(UtU, 0, sizeof(double) * (size_t)(k * k));
-        for (int64_t i = 0; i < n; ++i) {
-            const double di = (double)dinv[i];
-            for (int64_t j = 0; j < D; ++j) {
-                const double rij = di * (double)Rp[i * D + j];
+#pragma omp parallel for schedule(static)
+        for (int64_t j = 0; j < D; ++j)
+            for (int64_t i = 0; i < n; ++i) {
+                const double rij = (double)dinv[i] * (double)Rp[i * D + j];
                 for (int32_t l = 0; l < k; ++l) RtU[j * k + l] += rij * Ups[i * k + l];
             }
-            for (int32_t a = 0; a < k; ++a)
+#pragma omp parallel for schedule(static)
+        for (int32_t a = 0; a < k; ++a)
+            for (int64_t i = 0; i < n; ++i)
                 for (int32_t b = 0; b < k; ++b) UtU[a * k + b] += Ups[i * k + a] * Ups[i * k + b];
-        }
         /* H (Ups^T Ups) then the H update (Eq. update-Q) */
         for (int64_t j = 0; j < D; ++j)
             for (int32_t l = 0; l < k; ++l) {
@@ -418,16 +451,19 @@ void oracle_onmf(int64_t n, int64_t D, int32_t k, const float *Rp, const float *
             }
         /* M = Ups^T (R H) */
         memset(M, 0, sizeof(double) * (size_t)(k * k));
-        for (int64_t i = 0; i < n; ++i)
-            for (int32_t a = 0; a < k; ++a)
+#pragma omp parallel for schedule(static)
+        for (int32_t a = 0; a < k; ++a)
+            for (int64_t i = 0; i < n; ++i)
                 for (int32_t b = 0; b < k; ++b) M[a * k + b] += Ups[i * k + a] * RH[i * k + b];
         /* den = Ups M ; Ups update (Eq. update-Y) */
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; ++i)
             for (int32_t l = 0; l < k; ++l) {
                 double s = 0.0;
                 for (int32_t a = 0; a < k; ++a) s += Ups[i * k + a] * M[a * k + l];
                 den[i * k + l] = s;
             }
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n * k; ++i) {
             const double num = RH[i] > 0.0 ? RH[i] : 0.0;
             const double dd = (den[i] > 0.0 ? den[i] : 0.0) + EPS_ONMF;
@@ -456,6 +492,7 @@ void oracle_nci(int64_t n, int32_t k, const double *Ups, int32_t Tg, int32_t *la
     int32_t it = 0;
     for (int32_t t = 0; t < Tg; ++t) {
         int changed = 0;
+#pragma omp parallel for schedule(static) reduction(|:changed)
         for (int64_t i = 0; i < n; ++i) {
             int32_t best = 0;
             double bv = 0.0;
