@@ -1,15 +1,19 @@
 #!/usr/bin/env python
 """bench.py -- the TPO hot path (arXiv 2405.11922) on B200: one step = one whole pass of
 propagate -> Haar Q -> features -> exact top-k -> ONMF + NCI over BASELINE.json's
-configs[1] ("small") by default, through libtpo's C-ABI (tpo_run).
+configs[3] ("large", the largest configuration that fits one GPU; xl is the 8-GPU config) by
+default, through libtpo's C-ABI (tpo_run).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config small]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config large]
 
-Prints ONE JSON line (rank 0).  `value` is the whole-step throughput in MSA-propagation work
-units (2 * nnz * d * T multiply-adds per step, i.e. nnz*d per SpMM) per second with inputs
-resident in HBM; `ms_per_step` is the end-to-end TPO time per step.  `e2e` is the same
-metric with host inputs copied in and labels copied out inside the timed region.
---impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
+Prints ONE JSON line (rank 0).  BASELINE.json's metric is the pair "MSA propagation GB/s &
+nnz*d/s; end-to-end TPO seconds": `value` is the MSA-propagation work of a step
+(2 * nnz * d * T multiply-adds, i.e. nnz*d per SpMM) per END-TO-END TPO second with inputs
+resident in HBM (so it moves with the whole step, not only with the propagation);
+`tpo_seconds` is the end-to-end step time, and `propagation_nnz_d_per_s` /
+`propagation_gb_per_s` the propagation alone.  `e2e` is the same metric with host inputs
+copied in and labels copied out inside the timed region.  --impl reference times the fp64
+CPU oracle (oracle/) on a bounded, stage-by-stage sample of the same workload.
 """
 from __future__ import annotations
 
@@ -142,56 +146,111 @@ def dist_env():
     return ws, rank, local
 
 
-def run_reference(args, g, ws, rank):
-    """The fp64 oracle as it stands, on a bounded sample: one propagation hop (a1-a3) over the
-    full graph per step (the stages a5-a9 are excluded: the oracle's D x D Jacobi alone would
-    take minutes at D = 2000)."""
-    if rank != 0:
-        return
+ORACLE_ROW_FRACTION = 32      # a5-a9 of the oracle sample run on n / 32 rows (their cost is linear in n)
+
+
+def oracle_stage_sample(g, args):
+    """One bounded, stage-by-stage sample of the whole oracle pipeline (a1-a9) on this workload,
+    extrapolated to one full step.  a1-a3: ONE of the T hops over the full graph (each hop costs
+    the same).  a4: the Haar QR of G (d x d, once per step).  a5-a9 on the first n/16 U rows
+    of that hop's Zhat (the ids are shuffled, so this is a random row sample; features, Gram,
+    Gamma, ONMF and NCI costs are linear in n): features, the exact top-k, ONE ONMF iteration and
+    ONE Alg. 3 iteration, scaled by 32 and by Tf / Tg -- except the top-k's D x D Jacobi
+    eigensolve, which does not depend on n and is timed on its own and counted once.  Returns (seconds per full step, stage
+    dict, sample text)."""
     from oracle import core as O
     O.lib()
-    cores = len(os.sched_getaffinity(0))
-    units = 2 * g.nnz * g.d * 1
-    times = []
+    t = {}
+    t0 = time.perf_counter()
+    _, Zh = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, 1, g.B_val)
+    t["propagate_hop"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Q = O.haar_q(g.G)
+    t["haar"] = time.perf_counter() - t0
+    ns = max(min(g.n, 4096), g.n // ORACLE_ROW_FRACTION)
+    scale = g.n / ns
+    Zs = np.ascontiguousarray(Zh[:ns], np.float32)
+    del Zh
+    t0 = time.perf_counter()
+    Rp, dinv, _ = O.features(Zs, Q.astype(np.float32))
+    t["features"] = time.perf_counter() - t0
+    Rp32, dv32 = Rp.astype(np.float32), dinv.astype(np.float32)
+    del Rp
+    t0 = time.perf_counter()
+    Gm, s, Ps, _ = O.topk(Rp32, dv32, g.k)
+    t["topk"] = time.perf_counter() - t0
+    Gs = O.gram(Rp32, dv32)
+    t0 = time.perf_counter()
+    O.sym_eig(Gs)
+    t_jac = min(time.perf_counter() - t0, t["topk"])
+    t0 = time.perf_counter()
+    U, _ = O.onmf(Rp32, dv32, Gm.astype(np.float32), s, Ps.astype(np.float32), 1)
+    t["onmf_iter"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.nci(U, 1)
+    t["nci_iter"] = time.perf_counter() - t0
+    stages = {"propagate": g.T * t["propagate_hop"] + t["haar"], "features": scale * t["features"],
+              "topk_eig": scale * (t["topk"] - t_jac) + t_jac, "cluster": scale * (args.tf * t["onmf_iter"] + args.tg * t["nci_iter"])}
+    step_s = sum(stages.values())
+    sample = (f"oracle (fp64 C, OpenMP) stage by stage on {g.name}: 1 of T={g.T} propagation hops over the full graph "
+              f"+ Haar QR; features, exact top-k, 1 of Tf={args.tf} ONMF and 1 of Tg={args.tg} NCI iterations on "
+              f"{ns:,} of {g.n:,} U rows; extrapolated to the full step (x T, x n/{ns} except the D x D "
+              f"Jacobi, x Tf, x Tg); "
+              f"measured {sum(t.values()):.1f} s")
+    return step_s, {k: round(v * 1e3, 1) for k, v in stages.items()}, sample
+
+
+def run_reference(args, g, ws, rank):
+    """The fp64 oracle as it stands (the reference arm of this tier), each step one bounded
+    stage-by-stage sample of the whole pipeline (oracle_stage_sample) on this workload; the
+    step's time is the extrapolated full-step time, so `value` is our arm's metric."""
+    if rank != 0:
+        return
+    cores = omp_cores()
+    units = 2.0 * g.nnz * g.d * g.T
+    times, stages, sample = [], None, ""
     for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, 1)
-        dt = time.perf_counter() - t0
+        step_s, stages, sample = oracle_stage_sample(g, args)
         if it >= args.warmup:
-            times.append(dt)
+            times.append(step_s)
     tot = sum(times)
     value = units * len(times) / tot
     unit = "nnz*d/s"
-    sample = f"oracle_propagate over the full {g.name} graph, 1 of T={g.T} hops per step (a1-a3 only)"
     line = {"impl": "reference", "metric": metric_name(), "value": value, "unit": unit, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(g, args, ws),
+            "config": config_dict(g, args, ws), "stages_ms": stages, "tpo_seconds": tot / len(times),
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def omp_cores():
+    """Threads the oracle's OpenMP loops use (OMP_NUM_THREADS, else every core of the affinity mask)."""
+    n = len(os.sched_getaffinity(0))
+    try:
+        return min(n, int(os.environ["OMP_NUM_THREADS"]))
+    except (KeyError, ValueError):
+        return n
+
+
 def metric_name():
-    return "MSA propagation nnz*d/s over the end-to-end TPO step"
+    return ("MSA-propagation nnz*d per end-to-end TPO second (pair: propagation_nnz_d_per_s / "
+            "propagation_gb_per_s and tpo_seconds)")
 
 
 def config_dict(g, args, ws):
     return {"workload": f"{g.name} planted ABG (BASELINE.json configs[{['tiny','small','medium','large','xl'].index(g.name)}])",
             "n_u": g.n, "n_v": g.m, "nnz": g.nnz, "d": g.d, "k": g.k, "alpha": g.alpha, "T": g.T, "Tf": args.tf,
             "Tg": args.tg, "eig": "exact", "seed": 0, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+            "units_per_step": "2*nnz*d*T (MSA-propagation multiply-adds)",
             "l2": "256 MiB L2 flush between timed steps; inputs also exceed L2"}
 
 
-def cpu_baseline_sample(g):
-    from oracle import core as O
-    O.lib()
-    t0 = time.perf_counter()
-    O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, 1)
-    dt = time.perf_counter() - t0
-    return {"value": 2 * g.nnz * g.d / dt, "unit": "nnz*d/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "oracle",
-            "sample": f"oracle_propagate, 1 of T={g.T} hops over the full {g.name} graph ({dt:.1f} s; a5-a9 excluded)"}
+def cpu_baseline_sample(g, args):
+    step_s, stages, sample = oracle_stage_sample(g, args)
+    return {"value": 2.0 * g.nnz * g.d * g.T / step_s, "unit": "nnz*d/s", "cores": omp_cores(), "kind": "oracle",
+            "sample": sample, "tpo_seconds": step_s, "stages_ms": stages}
 
 
 def run_sharded(args, g, ws, rank, local, dev):
@@ -265,17 +324,19 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="small")
+    ap.add_argument("--config", default="large")
     ap.add_argument("--tf", type=int, default=5)
     ap.add_argument("--tg", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
-                    help="N > 1: independent replicas (weak scaling, default) or one graph with its U rows "
-                         "sharded across the ranks (strong scaling: NCCL reduce-scatter / all-gather per hop, "
-                         "all-reduced solver partials)")
+    ap.add_argument("--mode", default=None, choices=["replicas", "sharded"],
+                    help="N > 1: one graph with its U rows sharded across the ranks (default: strong scaling, "
+                         "NCCL reduce-scatter / all-gather per hop, all-reduced solver partials) or N independent "
+                         "replicas (weak scaling, no data-path collective)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
+    if args.mode is None:
+        args.mode = "sharded" if ws > 1 else "replicas"
 
     from synth import make_config
     g = make_config(args.config)
@@ -426,10 +487,11 @@ def main():
                           "cluster": stage_ms[3]},
             "tpo_seconds": ms_step / 1e3,
             "propagation_nnz_d_per_s": 2.0 * g.nnz * g.d * g.T / (prop_ms / 1e3),
+            "propagation_gb_per_s": bytes_hop * g.T / (prop_ms / 1e3) / 1e9,
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": cs.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(g)
+        line["cpu_baseline"] = cpu_baseline_sample(g, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

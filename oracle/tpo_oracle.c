@@ -335,17 +335,19 @@ static int sign_rule(int64_t n, int64_t k, const double *Gamma, int64_t l) {
 /* G = R^T R with R = diag(dinv) R' (fp64 products of the widened fp32 inputs), step 1 of
  * oracle_topk; exported on its own for the parity test of the GPU Gram. */
 void oracle_gram(int64_t n, int64_t D, const float *Rp, const float *dinv, double *G) {
-#pragma omp parallel for schedule(static)
-    for (int64_t a = 0; a < D; ++a)
-        for (int64_t b = a; b < D; ++b) {
-            double s = 0.0;
-            for (int64_t i = 0; i < n; ++i) {
-                const double di = (double)dinv[i];
-                s += (di * (double)Rp[i * D + a]) * (di * (double)Rp[i * D + b]);
-            }
-            G[a * D + b] = s;
-            G[b * D + a] = s;
+    /* row a of the upper triangle per thread; each entry summed over i in ascending order */
+#pragma omp parallel for schedule(static, 1)
+    for (int64_t a = 0; a < D; ++a) {
+        double *g = G + a * D;
+        for (int64_t b = a; b < D; ++b) g[b] = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            const double di = (double)dinv[i];
+            const double ra = di * (double)Rp[i * D + a];
+            for (int64_t b = a; b < D; ++b) g[b] += ra * (di * (double)Rp[i * D + b]);
         }
+    }
+    for (int64_t a = 0; a < D; ++a)
+        for (int64_t b = a + 1; b < D; ++b) G[b * D + a] = G[a * D + b];
 }
 
 int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_t k,
