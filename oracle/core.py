@@ -43,6 +43,10 @@ def lib():
         L.oracle_gram.argtypes = [i64, i64, vp, vp, vp]
         L.oracle_topk.argtypes = [i64, i64, vp, vp, i32, vp, vp, vp, vp]
         L.oracle_topk.restype = C.c_int
+        L.oracle_topk_from_eig.argtypes = [i64, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.oracle_topk_from_eig.restype = C.c_int
+        L.oracle_svd_reduce.argtypes = [i64, i64, vp, i64, vp, vp]
+        L.oracle_svd_reduce_from_eig.argtypes = [i64, i64, vp, i64, vp, vp, vp, vp]
         L.oracle_onmf.argtypes = [i64, i64, i32, vp, vp, vp, vp, vp, i32, vp, vp]
         L.oracle_nci.argtypes = [i64, i32, vp, i32, vp, vp]
         _lib = L
@@ -125,15 +129,44 @@ def gram(Rp, dinv):
     return G
 
 
-def topk(Rp, dinv, k):
-    """Exact top-k singular triplets of R = diag(dinv) R' -> (Gamma, sigma, Psi, all eigenvalues of R^T R)."""
+def topk(Rp, dinv, k, eig="jacobi"):
+    """Exact top-k singular triplets of R = diag(dinv) R' -> (Gamma, sigma, Psi, all eigenvalues of R^T R).
+    eig="lapack" takes the eigenpairs of the D x D Gram from numpy.linalg.eigh (LAPACK, a library
+    eigensolver; the oracle's own cyclic Jacobi is pinned against it) instead of the Jacobi sweeps,
+    whose cost grows as D^3 per sweep -- for D = 2000 (small config)."""
     Rp, dinv = _c(Rp, np.float32), _c(dinv, np.float32)
     n, D = Rp.shape
     Gm, s, Ps, lam = np.zeros((n, k)), np.zeros(k), np.zeros((D, k)), np.zeros(D)
-    rc = lib().oracle_topk(n, D, _p(Rp), _p(dinv), int(k), _p(Gm), _p(s), _p(Ps), _p(lam))
+    if eig == "lapack":
+        w, V = np.linalg.eigh(gram(Rp, dinv))
+        w, V = np.ascontiguousarray(w), np.ascontiguousarray(V)
+        rc = lib().oracle_topk_from_eig(n, D, _p(Rp), _p(dinv), int(k), _p(w), _p(V), _p(Gm), _p(s), _p(Ps),
+                                        _p(lam))
+    else:
+        rc = lib().oracle_topk(n, D, _p(Rp), _p(dinv), int(k), _p(Gm), _p(s), _p(Ps), _p(lam))
     if rc != 0:
         raise ArithmeticError(f"oracle_topk rc={rc}")
     return Gm, s, Ps, lam
+
+
+def svd_reduce(X, d, eig="jacobi"):
+    """X' = Gamma Sigma of the exact top-d SVD of X (Eq. Xd), sign-fixed (R8); pass-through when
+    d >= d_U.  Returns (X' n x d fp64, sigma (d,) or None on pass-through).  eig="lapack" takes the
+    eigenpairs of X^T X from numpy.linalg.eigh (LAPACK) instead of the Jacobi sweeps."""
+    X = _c(X, np.float32)
+    n, dU = X.shape
+    if d >= dU:
+        Xr = np.zeros((n, dU))
+        lib().oracle_svd_reduce(n, dU, _p(X), int(d), _p(Xr), None)
+        return Xr, None
+    Xr, s = np.zeros((n, d)), np.zeros(d)
+    if eig == "lapack":
+        w, V = np.linalg.eigh(gram(X, np.ones(n, np.float32)))
+        w, V = np.ascontiguousarray(w), np.ascontiguousarray(V)
+        lib().oracle_svd_reduce_from_eig(n, dU, _p(X), int(d), _p(w), _p(V), _p(Xr), _p(s))
+    else:
+        lib().oracle_svd_reduce(n, dU, _p(X), int(d), _p(Xr), _p(s))
+    return Xr, s
 
 
 def onmf(Rp, dinv, Gamma, sigma, Psi, Tf):

@@ -350,12 +350,13 @@ void oracle_gram(int64_t n, int64_t D, const float *Rp, const float *dinv, doubl
         for (int64_t b = a + 1; b < D; ++b) G[b * D + a] = G[a * D + b];
 }
 
-int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_t k,
-                double *Gamma, double *sigma, double *Psi, double *lam_all) {
-    double *G = dalloc((size_t)(D * D));
-    oracle_gram(n, D, Rp, dinv, G);
-    double *w = dalloc((size_t)D), *V = dalloc((size_t)(D * D));
-    jacobi_eig(D, G, w, V);
+/* Steps 2 (sorting) to 4 of oracle_topk from a given eigendecomposition of G = R^T R:
+ * w (D eigenvalues, any order) and V (D x D, eigenvector j in column j).  Exported so that a
+ * test may supply the eigenpairs of G from LAPACK (a library eigensolver, pinned against
+ * jacobi_eig by the tests) where the O(D^3)-per-sweep Jacobi would be too slow (D = 2000). */
+int oracle_topk_from_eig(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_t k,
+                         const double *w, const double *V, double *Gamma, double *sigma, double *Psi,
+                         double *lam_all) {
     int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (size_t)D);
     for (int64_t i = 0; i < D; ++i) ord[i] = i;
     for (int64_t i = 1; i < D; ++i) {                 /* insertion sort, descending */
@@ -387,8 +388,72 @@ int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_
                 for (int64_t j = 0; j < D; ++j) Psi[j * k + l] = -Psi[j * k + l];
             }
     }
-    free(Gm); free(ord); free(V); free(w); free(G);
+    free(Gm); free(ord);
     return rc;
+}
+
+int oracle_topk(int64_t n, int64_t D, const float *Rp, const float *dinv, int32_t k,
+                double *Gamma, double *sigma, double *Psi, double *lam_all) {
+    double *G = dalloc((size_t)(D * D));
+    oracle_gram(n, D, Rp, dinv, G);
+    double *w = dalloc((size_t)D), *V = dalloc((size_t)(D * D));
+    jacobi_eig(D, G, w, V);
+    const int rc = oracle_topk_from_eig(n, D, Rp, dinv, k, w, V, Gamma, sigma, Psi, lam_all);
+    free(V); free(w); free(G);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------------------
+ * f1: SVD-based attribute dimension reduction, Sec. 3.2.1 Eq. Xd:
+ *   X' = Gamma Sigma  for the exact top-d SVD X ~ Gamma Sigma Psi^T of the n x d_U matrix X
+ * (R14: the exact top-d, the unique result the paper's randomised SVD approximates, as R7),
+ * evaluated as X' = X Psi, because X Psi = Gamma Sigma Psi^T Psi = Gamma Sigma for the exact
+ * right singular vectors Psi = the top-d eigenvectors of X^T X.  The sign of each column pair is
+ * fixed by R8 (column sum of X' >= 0, near-zero sums by the largest-magnitude entry), since
+ * X' columns = sigma_l * Gamma columns.  d >= d_U is the pass-through X' = X.
+ * oracle_svd_reduce_from_eig takes the eigendecomposition of X^T X (w: d_U eigenvalues in any
+ * order, V: eigenvector j in column j); oracle_svd_reduce forms X^T X (fp64 products of the
+ * widened fp32 X) and uses the cyclic Jacobi solver.  Xr: n x d doubles; sigma: d (descending).
+ * ------------------------------------------------------------------------------------ */
+void oracle_svd_reduce_from_eig(int64_t n, int64_t dU, const float *X, int64_t d, const double *w,
+                                const double *V, double *Xr, double *sigma) {
+    if (d >= dU) {
+        for (int64_t i = 0; i < n * dU; ++i) Xr[i] = (double)X[i];
+        return;
+    }
+    int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (size_t)dU);
+    for (int64_t i = 0; i < dU; ++i) ord[i] = i;
+    for (int64_t i = 1; i < dU; ++i) {                /* insertion sort, descending */
+        int64_t x = ord[i], j = i - 1;
+        while (j >= 0 && w[ord[j]] < w[x]) { ord[j + 1] = ord[j]; --j; }
+        ord[j + 1] = x;
+    }
+    for (int64_t l = 0; l < d; ++l) sigma[l] = sqrt(w[ord[l]] > 0.0 ? w[ord[l]] : 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t l = 0; l < d; ++l) {
+            double s = 0.0;
+            for (int64_t j = 0; j < dU; ++j) s += (double)X[i * dU + j] * V[j * dU + ord[l]];
+            Xr[i * d + l] = s;
+        }
+    for (int64_t l = 0; l < d; ++l)
+        if (sign_rule(n, d, Xr, l) < 0)
+            for (int64_t i = 0; i < n; ++i) Xr[i * d + l] = -Xr[i * d + l];
+    free(ord);
+}
+
+void oracle_svd_reduce(int64_t n, int64_t dU, const float *X, int64_t d, double *Xr, double *sigma) {
+    if (d >= dU) {
+        oracle_svd_reduce_from_eig(n, dU, X, d, NULL, NULL, Xr, sigma);
+        return;
+    }
+    float *ones = (float *)malloc(sizeof(float) * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) ones[i] = 1.0f;
+    double *G = dalloc((size_t)(dU * dU)), *w = dalloc((size_t)dU), *V = dalloc((size_t)(dU * dU));
+    oracle_gram(n, dU, X, ones, G);                  /* X^T X (dinv = 1) */
+    jacobi_eig(dU, G, w, V);
+    oracle_svd_reduce_from_eig(n, dU, X, d, w, V, Xr, sigma);
+    free(ones); free(G); free(w); free(V);
 }
 
 /* ------------------------------------------------------------------------------------
@@ -482,7 +547,10 @@ void oracle_onmf(int64_t n, int64_t D, int32_t k, const float *Rp, const float *
  *     Y[i] = e_{l*}                         (Eq. Y-update)
  *     columns of Y scaled to unit L2 norm   (Eq. y-norm; empty -> zero)
  *     Phi = Ups^T Y
- *   early stop when the labels repeat (result-neutral).  labels: n int32;
+ *   early stop when the labels repeat (result-neutral).  R13: each score (Ups Phi)[i,l] is
+ *   accumulated over a = 0..k-1 with one correctly rounded fused multiply-add per term (C99
+ *   fma(); the paper fixes no rounding), the same operation the GPU argmax uses, so near-tie
+ *   rows are decided identically.  labels: n int32;
  *   *iters_used = iterations run.
  * ------------------------------------------------------------------------------------ */
 void oracle_nci(int64_t n, int32_t k, const double *Ups, int32_t Tg, int32_t *labels,
@@ -500,7 +568,7 @@ void oracle_nci(int64_t n, int32_t k, const double *Ups, int32_t Tg, int32_t *la
             double bv = 0.0;
             for (int32_t l = 0; l < k; ++l) {
                 double s = 0.0;
-                for (int32_t a = 0; a < k; ++a) s += Ups[i * k + a] * Phi[a * k + l];
+                for (int32_t a = 0; a < k; ++a) s = fma(Ups[i * k + a], Phi[a * k + l], s);   /* R13 */
                 if (l == 0 || s > bv) { bv = s; best = l; }
             }
             if (labels[i] != best) changed = 1;

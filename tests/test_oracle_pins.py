@@ -285,6 +285,21 @@ def test_sym_eig_vs_lapack():
     assert np.linalg.norm(V.T @ V - np.eye(40)) < 1e-12
 
 
+def test_topk_lapack_eigensolver_matches_jacobi():
+    """The oracle's top-k with the Gram's eigenpairs taken from LAPACK (eig="lapack", used where the
+    Jacobi sweeps are too slow, D = 2000) equals the Jacobi route: same sigma, the same subspaces, and
+    the same signs (the sign rule R8 is applied after either eigensolver)."""
+    n, d, k = 600, 20, 6
+    Zh = random_unit_rows(n, d, seed=21)
+    Q = O.haar_q(np.random.default_rng(22).standard_normal((d, d))).astype(np.float32)
+    Rp, dinv, _ = O.features(Zh, Q)
+    Rp32, dv32 = Rp.astype(np.float32), dinv.astype(np.float32)
+    Gj, sj, Pj, lj = O.topk(Rp32, dv32, k)
+    Gl, sl, Pl, ll = O.topk(Rp32, dv32, k, eig="lapack")
+    assert np.allclose(sj, sl, rtol=1e-12) and np.allclose(lj, ll, rtol=1e-9, atol=1e-13)
+    assert np.allclose(Gj, Gl, atol=1e-9) and np.allclose(Pj, Pl, atol=1e-9)
+
+
 def test_topk_planted_svd_and_eckart_young():
     """E8 / E4 / E2: the exact top-k of R' = U diag(s) V^T is (U[:, :k], s[:k], V[:, :k]) up to the
     sign rule; ||R - Gamma Sigma Psi^T||_2 = s_{k+1} (Eckart-Young)."""
@@ -487,3 +502,73 @@ def test_halko_power_iterations_converge_to_the_exact_top_k():
     assert errs[3] < 1e-8
     Gm, s, _ = DN.halko_topk(Rp, np.ones(n), k, p, 6, Om)
     assert np.allclose(s, sig[:k], rtol=1e-10)
+
+
+# ----------------------------------------------------------------------------------------------
+# f1 SVD-based attribute dimension reduction: Eq. Xd, Lemma 3 (519-527)
+# ----------------------------------------------------------------------------------------------
+
+def test_svd_reduce_pass_through():
+    """d >= d_U disables the reduction: X' = X exactly."""
+    X = random_unit_rows(30, 12, seed=31)
+    for d in (12, 20):
+        Xr, s = O.svd_reduce(X, d)
+        assert s is None and np.array_equal(Xr, X.astype(np.float64))
+
+
+def test_svd_reduce_exact_on_low_rank_X():
+    """A rank-r X (exact small-integer product, so fp32 holds it exactly) loses nothing at d >= r:
+    X' X'^T = X X^T (Eq. Xd: X X^T = Gamma Sigma^2 Gamma^T when sigma_{d+1} = 0), and the
+    singular values beyond r vanish."""
+    rng = np.random.default_rng(32)
+    A = rng.integers(-3, 4, (40, 3)).astype(np.float64)
+    B = rng.integers(-3, 4, (3, 24)).astype(np.float64)
+    X = (A @ B).astype(np.float32)
+    XX = X.astype(np.float64) @ X.astype(np.float64).T
+    for d in (3, 5):
+        Xr, s = O.svd_reduce(X, d)
+        assert np.max(np.abs(Xr @ Xr.T - XX)) <= 1e-9 * np.max(np.abs(XX))
+        if d > 3:
+            assert np.all(s[3:] <= 1e-6 * s[0])
+
+
+def test_svd_reduce_eckart_young_orthogonality_and_signs():
+    """Random 50 x 40 X, d = 10: sigma = the top-10 singular values of an independent
+    LAPACK SVD; X'^T X' = diag(sigma^2) (orthogonal columns Gamma Sigma); Eckart-Young
+    ||X X^T - X' X'^T||_2 = sigma_11^2 and entrywise <= sigma_11^2; column sums >= 0 (R8)."""
+    X = np.random.default_rng(33).random((50, 40)).astype(np.float32)
+    X64 = X.astype(np.float64)
+    S = np.linalg.svd(X64, compute_uv=False)
+    Xr, s = O.svd_reduce(X, 10)
+    assert np.allclose(s, S[:10], rtol=1e-11)
+    assert np.allclose(Xr.T @ Xr, np.diag(S[:10] ** 2), atol=1e-9 * S[0] ** 2)
+    E = X64 @ X64.T - Xr @ Xr.T
+    assert abs(np.linalg.norm(E, 2) - S[10] ** 2) <= 1e-9 * S[0] ** 2
+    assert np.max(np.abs(E)) <= S[10] ** 2 + 1e-6
+    assert np.all(Xr.sum(0) >= 0)
+    # X' spans the top-10 left singular subspace
+    U = np.linalg.svd(X64, full_matrices=False)[0][:, :10]
+    assert DN.sin_theta(Xr, U) < 1e-9
+
+
+def test_lemma3_bound_on_reduced_propagation():
+    """Lemma 3: |Z'[i].Z'[j] - Z[i].Z[j]| <= sigma_{d+1}^2 sqrt(D_U[i] D_U[j]) / (1 - alpha)
+    for the propagation of X' = Gamma Sigma vs of X (T = 300 hops: the series has converged to
+    fp64 precision at alpha = 0.5, 0.8); graphs without isolated U nodes."""
+    worst = 0.0
+    for seed in range(6):
+        g = small_graph(seed=40 + seed, n=60, m=40, k=4, d=5, deg=("poisson", 5.0))
+        du = np.diff(g.B_rowptr).astype(np.float64)
+        if np.any(du == 0):
+            continue
+        X = np.random.default_rng(seed).random((g.n, 24)).astype(np.float32)
+        S = np.linalg.svd(X.astype(np.float64), compute_uv=False)
+        for d in (4, 10):
+            Xr, _ = O.svd_reduce(X, d)
+            for alpha in (0.5, 0.8):
+                Z, _ = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, X, alpha, 300)
+                Zr, _ = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, Xr.astype(np.float32), alpha, 300)
+                lhs = np.abs(Zr @ Zr.T - Z @ Z.T)
+                rhs = S[d] ** 2 * np.sqrt(np.outer(du, du)) / (1 - alpha)
+                worst = max(worst, float(np.max(lhs / rhs)))
+    assert 0.0 < worst <= 1.0
