@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) assign_kernel(const double *__restrict__ 
             for (int a = 0; a < k; ++a) {
                 const double ph = phs[a * k + l];
 #pragma unroll
-                for (int r = 0; r < AR; ++r) sc[r] = __dadd_rn(sc[r], __dmul_rn(ubw[r * k + a], ph));
+                for (int r = 0; r < AR; ++r) sc[r] = fma(ubw[r * k + a], ph, sc[r]);
             }
 #pragma unroll
             for (int r = 0; r < AR; ++r)
@@ -231,10 +231,10 @@ __global__ void __launch_bounds__(128) assign_small_kernel(const double *__restr
         for (int a = 0; a < KM; ++a)
             if (a < k) {
                 const double ua = u[a];
-                sc0 = __dadd_rn(sc0, __dmul_rn(ua, phs[a * k + l]));
-                sc1 = __dadd_rn(sc1, __dmul_rn(ua, phs[a * k + l + 1]));
-                sc2 = __dadd_rn(sc2, __dmul_rn(ua, phs[a * k + l + 2]));
-                sc3 = __dadd_rn(sc3, __dmul_rn(ua, phs[a * k + l + 3]));
+                sc0 = fma(ua, phs[a * k + l], sc0);
+                sc1 = fma(ua, phs[a * k + l + 1], sc1);
+                sc2 = fma(ua, phs[a * k + l + 2], sc2);
+                sc3 = fma(ua, phs[a * k + l + 3], sc3);
             }
         if (l == 0 || sc0 > best) { best = sc0; arg = l; }
         if (sc1 > best) { best = sc1; arg = l + 1; }
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(128) assign_small_kernel(const double *__restr
         double sc = 0.0;
 #pragma unroll
         for (int a = 0; a < KM; ++a)
-            if (a < k) sc = __dadd_rn(sc, __dmul_rn(u[a], phs[a * k + l]));
+            if (a < k) sc = fma(u[a], phs[a * k + l], sc);
         if (l == 0 || sc > best) { best = sc; arg = l; }
     }
     if (labels[row] != arg) *s.changed = 1;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(NW * 32) nci_fused_kernel(const double *__rest
             double sc = 0.0;
 #pragma unroll
             for (int a = 0; a < KM; ++a)
-                if (a < k) sc = __dadd_rn(sc, __dmul_rn(u[a], phs[a * k + l]));   // unfused, as the oracle
+                if (a < k) sc = fma(u[a], phs[a * k + l], sc);   // fused multiply-add, as the oracle
             if (l == 0 || sc > best) { best = sc; arg = l; }
         }
         if (ok) {
@@ -451,6 +451,10 @@ void onmf_h_update(double *H, const double *RtU, const double *UtU, int64_t D, i
 
 void onmf_u_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st) {
     if (n == 0) return;
+    if (ts64_ups_enabled(k)) {
+        ts_ups_update(U, RH, M, n, k, st);
+        return;
+    }
     if (k <= 16) {
         ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
     } else {
@@ -587,12 +591,16 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
         dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;
-        if (k <= 16)
-            ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
-        else
-            ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * UR), 148 * 8), 256, ups_smem, st>>>(U, RH, M,
-                                                                                                          n, k);
-        TPO_LAUNCH_CHECK();
+        if (ts64_ups_enabled(k)) {
+            ts_ups_update(U, RH, M, n, k, st);
+        } else {
+            if (k <= 16)
+                ups_update_reg_kernel<16><<<cdiv(n, 256), 256, 0, st>>>(U, RH, M, n, k);
+            else
+                ups_update_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * UR), 148 * 8), 256, ups_smem, st>>>(U, RH, M,
+                                                                                                              n, k);
+            TPO_LAUNCH_CHECK();
+        }
     }
     // Alg. 3
     NciState s{flags, flags + 1, flags + 2};

@@ -472,6 +472,10 @@ void tsgemm_AW_f32(const float *A, int64_t lda, const float *rs, const double *W
 }
 void tsgemm_AW_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int64_t p, int64_t q,
                    double *out, int64_t ldo, cudaStream_t st) {
+    if (ts64_enabled()) {
+        ts_aw_f64(A, lda, rs, W, n, (int)p, (int)q, nullptr, out, ldo, st);
+        return;
+    }
     aw_f32_run<double>(A, lda, rs, W, n, p, q, out, ldo, st);
 }
 void tsgemm_AW_dd(const double *A, int64_t lda, const double *W, int64_t n, int64_t p, int64_t q, double *out,

@@ -230,12 +230,16 @@ void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float
 
 size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k) {
     const RtuPlan p = rtu_plan(n, (int)D, k);
-    return align_up(sizeof(double) * (size_t)(p.G * D * k) + 1) + 256;
+    return std::max(align_up(sizeof(double) * (size_t)(p.G * D * k) + 1) + 256, ts_rtu_ws(n, D, k));
 }
 
 // RtU = R'^T (dinv . U)   (D x k, fp64)
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
               cudaStream_t st) {
+    if (ts64_enabled()) {
+        ts_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
+        return;
+    }
     const RtuPlan p = rtu_plan(n, (int)D, k);
     const size_t mark = ar.off;
     double *part = ar.take<double>(p.G * D * k);

@@ -234,6 +234,10 @@ struct SpmmArgs {
                               // propagation; each launch adds nchunks), or null: separate fix-up kernel
     int reserve_sms;          // SMs left free (blocks placed on them exit) for concurrent side-stream work
     int smid_limit;           // = SMs - reserve_sms, set at launch
+    // column-group kernel only: the gathered table holds src_rows rows in LPE-float4 groups; the
+    // output is written in out_L-float4 groups of out_rows rows (out_L = d4: row-major)
+    int64_t src_rows, out_rows;
+    int out_L;
 };
 
 // Packed fp32x2 arithmetic (FADD2 / FFMA2 on sm_100a): two lanes of a float4 per instruction,
@@ -572,15 +576,201 @@ __global__ void __launch_bounds__(WPB * 32) fixup_kernel(SpmmArgs a) {
     epilogue<EPI>(a, s.x, c4, act, acc);
 }
 
+// ---------------------------------------------------------------------------------------
+// Column-group SpMM (propagation on tables too large for L2 at full width).  The gathered table
+// is stored in column groups of LPE float4 ("blocked": [group][row][LPE float4]); the work is
+// ordered group-major, so while the warps work on group g every gathered row comes from one
+// rows x 16*LPE-byte slice of the table, which stays L2-resident where the full-width table
+// (1 GB for the large config's P) does not.  A warp gathers E = 32 / LPE edges per load
+// instruction (lane sg * LPE + sl loads float4 sl of edge sg of the stream), accumulates per
+// lane, and folds the E partial sums of a row with an xor butterfly when the edge stream
+// crosses the row's end (fp addition is commutative, so every lane of a group holds the same
+// sum; the order is fixed by the edge positions: deterministic).  Outputs are written in
+// out_L-float4 groups (out_L = d4: row-major Z on the last hop).
+// ---------------------------------------------------------------------------------------
+template <int LPE>
+__device__ __forceinline__ float4 fold_edges(float4 a) {
+#pragma unroll
+    for (int o = LPE; o < 32; o <<= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+        a.z += __shfl_xor_sync(0xffffffffu, a.z, o);
+        a.w += __shfl_xor_sync(0xffffffffu, a.w, o);
+    }
+    return a;
+}
+
+// epilogue of one output row (lanes of edge slot 0 only): o = the row's output offset
+template <int EPI>
+__device__ __forceinline__ void gepilogue(const SpmmArgs &a, int64_t o, float4 acc, float4 x, float s) {
+    if (EPI == EPI_RAW) {
+        st_stream(a.out + o, acc);
+        return;
+    }
+    if (EPI == EPI_V) {
+        const float s2 = s * s;
+        st_stream(a.out + o, make_float4(acc.x * s2, acc.y * s2, acc.z * s2, acc.w * s2));
+        return;
+    }
+    const float g = a.alpha * s;
+    float4 z;
+    z.x = fmaf(a.c, x.x, g * acc.x);
+    z.y = fmaf(a.c, x.y, g * acc.y);
+    z.z = fmaf(a.c, x.z, g * acc.z);
+    z.w = fmaf(a.c, x.w, g * acc.w);
+    if (EPI == EPI_U) st_stream(a.out + o, make_float4(s * z.x, s * z.y, s * z.z, s * z.w));
+    else st_stream(a.out + o, z);
+}
+
+template <int EPI>
+__device__ __forceinline__ float4 gload_x(const SpmmArgs &a, int64_t row, int c4, bool lead) {
+    if (EPI == EPI_V || EPI == EPI_RAW || !lead) return make_float4(0.f, 0.f, 0.f, 0.f);
+#if TPO_L2_HINTS
+    return __ldcs(a.X + row * (int64_t)a.d4 + c4);
+#else
+    return __ldg(a.X + row * (int64_t)a.d4 + c4);
+#endif
+}
+
+template <int EPI, bool WEIGHTED, int LPE, int UMAX>
+__device__ __forceinline__ void gspmm_unit(const SpmmArgs &a, int grp, int64_t item, int64_t n_items) {
+    constexpr int E = 32 / LPE;                       // edges per load instruction
+    constexpr int U = (32 / E) < UMAX ? (32 / E) : UMAX;   // load instructions in flight (E * U divides 32)
+    const int lane = threadIdx.x & 31, sg = lane / LPE, sl = lane % LPE;
+    const bool lead = sg == 0;
+    const int c4 = grp * LPE + sl;
+    const float4 *base = a.src + (int64_t)grp * a.src_rows * LPE + sl;
+    const int64_t o_lane = (int64_t)(c4 / a.out_L) * a.out_rows * a.out_L + (c4 % a.out_L);
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int4 it = a.sch.items[item];
+    if (it.w == 0) {                                   // row block: one edge stream over its rows
+        const int64_t r0 = it.x;
+        const int64_t r1 = item + 1 < n_items ? (int64_t)a.sch.items[item + 1].x : a.n_rows;
+        for (int64_t rb = r0; rb < r1; rb += 32) {
+            const int nb = (int)(r1 - rb < 32 ? r1 - rb : 32);
+            const int64_t e_beg = a.rowptr[rb];
+            const int my_end = lane < nb ? (int)(a.rowptr[rb + 1 + lane] - e_beg) : 0;
+            const float my_s = (EPI != EPI_RAW && lane < nb) ? a.scale[rb + lane] : 0.f;
+            const int n_e = __shfl_sync(0xffffffffu, my_end, nb - 1);
+            int cur = 0;
+            int cur_end = __shfl_sync(0xffffffffu, my_end, 0);
+            float4 acc = zero;
+            float4 xcur = gload_x<EPI>(a, rb, c4, lead);
+            auto flush = [&]() {                        // warp-uniform: row rb + cur is complete
+                const float s = __shfl_sync(0xffffffffu, my_s, cur);
+                const float4 tot = fold_edges<LPE>(acc);
+                if (lead) gepilogue<EPI>(a, o_lane + (rb + cur) * a.out_L, tot, xcur, s);
+                acc = zero;
+                ++cur;
+                cur_end = __shfl_sync(0xffffffffu, my_end, cur < nb ? cur : nb - 1);
+                if (cur < nb) xcur = gload_x<EPI>(a, rb + cur, c4, lead);
+            };
+            for (int k0 = 0; k0 < n_e; k0 += 32) {
+                const int cnt = n_e - k0 < 32 ? n_e - k0 : 32;
+                const uint32_t mycol = (uint32_t)__ldg(a.col + e_beg + k0 + (lane < cnt ? lane : cnt - 1));
+                const float myw = WEIGHTED ? (lane < cnt ? __ldg(a.val + e_beg + k0 + lane) : 0.f) : 1.f;
+                for (int j = 0; j < cnt; j += E * U) {
+                    float4 v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int idx = j + u * E + sg;
+                        const uint32_t ro = __shfl_sync(0xffffffffu, mycol, idx < cnt ? idx : cnt - 1) * LPE;
+                        v[u] = gather_ld(row_addr(base, ro));
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (j + u * E >= cnt) break;            // warp-uniform
+                        const int idx = j + u * E + sg;
+                        const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, idx < cnt ? idx : cnt - 1) : 1.f;
+                        const int e = k0 + idx;
+                        bool pend = idx < cnt;
+                        while (true) {
+                            if (pend && e < cur_end) {
+                                acc = WEIGHTED ? f4fma(w, v[u], acc) : f4add(acc, v[u]);
+                                pend = false;
+                            }
+                            if (!__any_sync(0xffffffffu, pend)) break;
+                            flush();
+                        }
+                    }
+                }
+            }
+            while (cur < nb) flush();                   // the last row and trailing empty rows
+        }
+        return;
+    }
+    // one CHUNK-edge chunk of a long row -> partial sum; the last chunk to arrive finishes the row
+    const int64_t rbe = a.rowptr[it.x], re = a.rowptr[it.x + 1];
+    const int64_t beg = rbe + (int64_t)it.y * CHUNK;
+    const int64_t end = min(re, beg + CHUNK);
+    float4 acc = zero;
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+        const int cnt = (int)(end - e0 < 32 ? end - e0 : 32);
+        const uint32_t mycol = (uint32_t)__ldg(a.col + e0 + (lane < cnt ? lane : cnt - 1));
+        const float myw = WEIGHTED ? (lane < cnt ? __ldg(a.val + e0 + lane) : 0.f) : 1.f;
+        for (int j = 0; j < cnt; j += E * U) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = j + u * E + sg;
+                const uint32_t ro = __shfl_sync(0xffffffffu, mycol, idx < cnt ? idx : cnt - 1) * LPE;
+                v[u] = gather_ld(row_addr(base, ro));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = j + u * E + sg;
+                const float w = WEIGHTED ? __shfl_sync(0xffffffffu, myw, idx < cnt ? idx : cnt - 1) : 1.f;
+                if (idx < cnt) acc = WEIGHTED ? f4fma(w, v[u], acc) : f4add(acc, v[u]);
+            }
+        }
+    }
+    const float4 tot = fold_edges<LPE>(acc);
+    if (lead) a.partials[(int64_t)it.z * a.d4 + c4] = tot;
+    __threadfence();
+    const int slot0 = it.z - it.y;
+    unsigned old = 0;
+    if (lane == 0) old = atomicAdd(a.arrive + (int64_t)slot0 * a.ngroups + grp, 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if ((int)(old % (unsigned)it.w) != it.w - 1) return;
+    __threadfence();
+    if (!lead) return;
+    float4 s4 = zero;
+    const float4 *pp = a.partials + (int64_t)slot0 * a.d4 + c4;
+    for (int j = 0; j < it.w; ++j) s4 = f4add(s4, __ldcg(pp + (int64_t)j * a.d4));
+    const float s = EPI == EPI_RAW ? 0.f : a.scale[it.x];
+    gepilogue<EPI>(a, o_lane + (int64_t)it.x * a.out_L, s4, gload_x<EPI>(a, it.x, c4, true), s);
+}
+
+// Persistent warps over (column group, work item) units, group-major (see spmm_kernel).
+template <int EPI, bool WEIGHTED, int LPE, int UMAX, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) gspmm_kernel(SpmmArgs a) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    if ((int)smid >= a.smid_limit) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t n_items = packed_total(a.sch.offsets, a.n_rows) >> 32;
+    const int64_t units = n_items * a.ngroups;
+    while (true) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(a.work, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if ((int64_t)u >= units) return;
+        const int grp = (int)((int64_t)u / n_items);
+        gspmm_unit<EPI, WEIGHTED, LPE, UMAX>(a, grp, (int64_t)u - (int64_t)grp * n_items, n_items);
+    }
+}
+
 // P0 = s_u . (c X) for T >= 1; for T == 0, Z = c X (and Zhat = rownorm, see below).
+// out_L: column-group width of the output layout (d4: row-major).
 __global__ void init_scaled_kernel(const float4 *__restrict__ X, const float *__restrict__ su, int64_t n, int d4,
-                                   float c, int scale_rows, float4 *__restrict__ out) {
+                                   float c, int scale_rows, float4 *__restrict__ out, int out_L) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n * d4) return;
     const int64_t row = i / d4;
+    const int c4 = (int)(i - row * d4);
     const float s = scale_rows ? su[row] * c : c;
     const float4 x = X[i];
-    out[i] = make_float4(s * x.x, s * x.y, s * x.z, s * x.w);
+    out[(int64_t)(c4 / out_L) * n * out_L + row * out_L + (c4 % out_L)] = make_float4(s * x.x, s * x.y, s * x.z, s * x.w);
 }
 
 // Zhat = Z / ||Z|| row-wise (warp per row), zero rows stay zero (R4).
@@ -634,52 +824,92 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
     TPO_LAUNCH_CHECK();
 }
 
-// Column slices per warp (SL): more slices amortise the index load / shuffle / address work
-// of an edge over more bytes, fewer keep the gathered working set (SL x 512 B per row) small.
-// MINB: resident blocks per SM the register budget is sized for.  Encoded as SL * 10 + MINB
-// (or SL * 100 + MINB * 10 + edges-in-flight code); TPO_SPMM_VARIANT overrides it (tuning).
-// variant code: SL * 10 + MINB (edges in flight 8 / SL), SL * 100 + MINB * 10 + UE, or
-// SL * 1000 + MINB * 100 + UE (UE >= 10)
-int variant_sl(int v) { return v >= 1000 ? v / 1000 : v >= 100 ? v / 100 : v / 10; }
-int variant_minb(int v) { return v >= 1000 ? (v / 100) % 10 : v >= 100 ? (v / 10) % 10 : v % 10; }
-int spmm_variant(int nslices) {
-    int v = 14;   // measured best on small (d = 1000), medium (d = 256) and large (d = 128)
-    if (const char *e = getenv("TPO_SPMM_VARIANT")) v = atoi(e);
-    if (v != 14 && v != 13 && v != 23 && v != 228) v = 14;
-    if (variant_sl(v) > nslices) v = 14;
-    return v;
-}
-
+// Row-major kernel: one 128-float column slice per warp (SL = 1) with 4 resident blocks per SM,
+// measured best on small (d = 1000), medium (d = 256) and large (d = 128) against SL = 2 / 3-4
+// blocks and 16 rows in flight.
 template <int EPI, bool W>
-void spmm_launch_sl(SpmmArgs a, int64_t max_items, int var, cudaStream_t st) {
-    const int sl = variant_sl(var);
-    const int minb = variant_minb(var);
-    a.ngroups = (a.nslices + sl - 1) / sl;
+void spmm_launch_rm(SpmmArgs a, int64_t max_items, cudaStream_t st) {
+    constexpr int MINB = 4;
+    a.ngroups = a.nslices;
     const int64_t blocks = cdiv(max_items * a.ngroups, WPB);
     // persistent warps: at most the resident capacity (SMs x MINB blocks of WPB warps)
     const int nsm = sm_count();
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)nsm * minb));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)nsm * MINB));
     // the reserve applies only to a full-capacity grid (blocks on every SM, so the blocks of the
     // non-reserved SMs exist and drain the work queue); a smaller grid keeps every block
-    a.smid_limit = (int64_t)grid == (int64_t)nsm * minb ? std::max(1, nsm - std::max(0, a.reserve_sms)) : (1 << 30);
-    switch (var) {
-        case 23: spmm_kernel<EPI, W, 2, 3><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 228: spmm_kernel<EPI, W, 2, 2, 8><<<grid, WPB * 32, 0, st>>>(a); break;
-        case 13: spmm_kernel<EPI, W, 1, 3><<<grid, WPB * 32, 0, st>>>(a); break;
-        default: spmm_kernel<EPI, W, 1, 4><<<grid, WPB * 32, 0, st>>>(a); break;
-    }
+    a.smid_limit = (int64_t)grid == (int64_t)nsm * MINB ? std::max(1, nsm - std::max(0, a.reserve_sms)) : (1 << 30);
+    spmm_kernel<EPI, W, 1, MINB><<<grid, WPB * 32, 0, st>>>(a);
     TPO_LAUNCH_CHECK();
 }
 
 template <int EPI>
 void spmm_launch(const SpmmArgs &a, int64_t max_items, int64_t max_slots, bool weighted, cudaStream_t st) {
-    const int var = spmm_variant(a.nslices);
-    if (weighted) spmm_launch_sl<EPI, true>(a, max_items, var, st);
-    else spmm_launch_sl<EPI, false>(a, max_items, var, st);
+    if (weighted) spmm_launch_rm<EPI, true>(a, max_items, st);
+    else spmm_launch_rm<EPI, false>(a, max_items, st);
     if (a.arrive) return;                 // long rows finished by their last chunk (fused fix-up)
     const int64_t fw = max_slots * a.nslices;
     fixup_kernel<EPI><<<cdiv(fw, WPB), WPB * 32, 0, st>>>(a);
     TPO_LAUNCH_CHECK();
+}
+
+// Column-group kernel launch: LPE = a.ngroups' group width (a.d4 / a.ngroups); needs a.arrive.
+template <int EPI, bool W, int UMAX, int MINB>
+void gspmm_launch(SpmmArgs a, int lpe, int64_t max_items, cudaStream_t st) {
+    a.ngroups = a.d4 / lpe;
+    const int64_t blocks = cdiv(max_items * a.ngroups, WPB);
+    const int nsm = sm_count();
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)nsm * MINB));
+    a.smid_limit = (int64_t)grid == (int64_t)nsm * MINB ? std::max(1, nsm - std::max(0, a.reserve_sms)) : (1 << 30);
+    switch (lpe) {
+        case 4: gspmm_kernel<EPI, W, 4, UMAX, MINB><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 8: gspmm_kernel<EPI, W, 8, UMAX, MINB><<<grid, WPB * 32, 0, st>>>(a); break;
+        case 16: gspmm_kernel<EPI, W, 16, UMAX, MINB><<<grid, WPB * 32, 0, st>>>(a); break;
+        default: gspmm_kernel<EPI, W, 32, UMAX, MINB><<<grid, WPB * 32, 0, st>>>(a); break;
+    }
+    TPO_LAUNCH_CHECK();
+}
+
+// (loads in flight per warp, resident blocks per SM): tuning knob TPO_GSPMM_CFG = 0 (8, 3) or
+// 1 (4, 4) while the choice is measured
+template <int EPI>
+void gspmm(const SpmmArgs &a, int lpe, int64_t max_items, bool weighted, cudaStream_t st) {
+    const char *e = getenv("TPO_GSPMM_CFG");
+    const int cfg = e ? atoi(e) : 0;
+    if (cfg == 1) {
+        if (weighted) gspmm_launch<EPI, true, 4, 4>(a, lpe, max_items, st);
+        else gspmm_launch<EPI, false, 4, 4>(a, lpe, max_items, st);
+    } else {
+        if (weighted) gspmm_launch<EPI, true, 8, 3>(a, lpe, max_items, st);
+        else gspmm_launch<EPI, false, 8, 3>(a, lpe, max_items, st);
+    }
+}
+
+// Column-group width (float4) of a gathered table of `rows` rows: the widest group whose slice
+// (rows x 16 * L bytes) fits the L2 budget, among the widths dividing d4 (>= 4: 64-byte pieces,
+// two DRAM sectors).  0 = no group width divides d4 (the row-major kernel is used).
+// TPO_SPMM_L = "Lp,Lq" overrides both choices (tuning and the per-width parity tests).
+constexpr double kL2SliceBudget = 64.0 * (1 << 20);
+int group_width(int64_t rows, int d4) {
+    for (int L = 32; L >= 4; L >>= 1)
+        if (d4 % L == 0 && (double)rows * L * 16.0 <= kL2SliceBudget) return L;
+    return d4 % 4 == 0 ? 4 : 0;
+}
+void choose_widths(int64_t n, int64_t m, int d4, int &Lp, int &Lq) {
+    // measured (large, medium): every column-group layout is slower than the row-major slice
+    // kernel (per-group index re-reads, shuffles and row folds cost more than the L2 locality
+    // saves), so the row-major layout is the default; group_width() is kept for the override.
+    Lp = Lq = 0;
+    (void)n; (void)m;
+    if (const char *e = getenv("TPO_SPMM_L")) {
+        int a = 0, b = 0;
+        if (sscanf(e, "%d,%d", &a, &b) == 2) {
+            auto ok = [&](int L) { return L == 0 || ((L == 4 || L == 8 || L == 16 || L == 32) && d4 % L == 0); };
+            if (ok(a) && ok(b)) { Lp = a; Lq = b; }
+        }
+    }
+    // both row-major (the slice-major row-major kernel) when either table cannot be grouped or
+    // both fit L2 at full width in 32-float4 slices
+    if (Lp == 0 || Lq == 0) Lp = Lq = 0;
 }
 
 }  // namespace
@@ -693,9 +923,9 @@ size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
     sched_alloc(ar, n_v, nnz);
     ar.take<float>((2 * (nnz / CHUNK) + 1) * d);  // partials (shared by both SpMMs)
     ar.take<unsigned long long>(kCounters);       // persistent-warp work counters
-    const int64_t nsl = (d / 4 + 31) / 32;
-    ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * nsl);   // chunk-arrival counters (U side)
-    ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * nsl);   // (V side)
+    const int64_t ncnt = std::max<int64_t>((d / 4 + 31) / 32, d / 16);   // slices or column groups
+    ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * ncnt);  // chunk-arrival counters (U side)
+    ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * ncnt);  // (V side)
     return ar.off + 256;
 }
 
@@ -712,13 +942,10 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     SchedBufs sbt = sched_alloc(ar, m, nnz);
     float *partials = ar.take<float>((2 * (nnz / CHUNK) + 1) * d);
     unsigned long long *work = ar.take<unsigned long long>(kCounters);
-    const int nsl_all = (d4 + 31) / 32;
-    unsigned *arr_u = ar.take<unsigned>(sb.s.max_slots * nsl_all), *arr_v = ar.take<unsigned>(sbt.s.max_slots * nsl_all);
-    const bool fused_fixup = getenv("TPO_SEPARATE_FIXUP") == nullptr;
-    if (fused_fixup) {
-        TPO_CUDA(cudaMemsetAsync(arr_u, 0, sizeof(unsigned) * sb.s.max_slots * nsl_all, st));
-        TPO_CUDA(cudaMemsetAsync(arr_v, 0, sizeof(unsigned) * sbt.s.max_slots * nsl_all, st));
-    }
+    const int64_t ncnt = std::max<int64_t>((d4 + 31) / 32, d4 / 4);
+    unsigned *arr_u = ar.take<unsigned>(sb.s.max_slots * ncnt), *arr_v = ar.take<unsigned>(sbt.s.max_slots * ncnt);
+    TPO_CUDA(cudaMemsetAsync(arr_u, 0, sizeof(unsigned) * sb.s.max_slots * ncnt, st));
+    TPO_CUDA(cudaMemsetAsync(arr_v, 0, sizeof(unsigned) * sbt.s.max_slots * ncnt, st));
     int launches = 0;
     auto counter = [&]() {        // a zeroed counter per SpMM launch (the pool is re-zeroed when it wraps)
         if (launches % kCounters == 0) TPO_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) * kCounters, st));
@@ -732,7 +959,7 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     TPO_LAUNCH_CHECK();
     if (n == 0) return;
     if (T == 0) {
-        init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 0, (float4 *)Z);
+        init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 0, (float4 *)Z, d4);
         TPO_LAUNCH_CHECK();
         if (Zhat) rownorm_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>((const float4 *)Z, n, d4, (float4 *)Zhat);
         TPO_LAUNCH_CHECK();
@@ -740,7 +967,13 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     }
     sched_build(sb, B.row_ptr, n, st);
     if (m > 0) sched_build(sbt, Bt.row_ptr, m, st);
-    init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 1, (float4 *)Z);
+    // Layouts: Lp / Lq = column-group widths of the iterate P (n rows, gathered by SpMM-1) and of
+    // the V-side block Q (m rows, gathered by SpMM-2); 0 = row-major with the slice kernel.
+    int Lp = 0, Lq = 0;
+    choose_widths(n, m, d4, Lp, Lq);
+    const bool grouped = Lp > 0;
+    init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 1, (float4 *)Z,
+                                                        grouped ? Lp : d4);
     TPO_LAUNCH_CHECK();
 
     const int nslices = (d4 + 31) / 32;
@@ -752,12 +985,17 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
             a.src = (const float4 *)Z; a.d4 = d4; a.nslices = nslices;
             a.sch = sbt.s; a.n_rows = m; a.partials = (float4 *)partials;
             a.scale = sv; a.out = (float4 *)Qv;
-            a.arrive = fused_fixup ? arr_v : nullptr;
+            a.arrive = arr_v;
             a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
             a.work = counter();
-            spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
+            if (grouped) {
+                a.src_rows = n; a.out_rows = m; a.out_L = Lq;
+                gspmm<EPI_V>(a, Lp, sbt.s.max_items, Bt.val != nullptr, st);
+            } else {
+                spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
+            }
         } else {
-            TPO_CUDA(cudaMemsetAsync(Qv, 0, 0, st));
+            TPO_CUDA(cudaMemsetAsync(Qv, 0, sizeof(float) * 0, st));
         }
         SpmmArgs a{};
         a.rowptr = B.row_ptr; a.col = B.col_idx; a.val = B.val;
@@ -765,10 +1003,18 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
         a.sch = sb.s; a.n_rows = n; a.partials = (float4 *)partials;
         a.scale = su; a.X = (const float4 *)X; a.c = c; a.alpha = alpha;
         a.out = (float4 *)Z;
-        a.arrive = fused_fixup ? arr_u : nullptr;
+        a.arrive = arr_u;
         a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
         a.work = counter();
-        if (last) {
+        if (grouped) {
+            a.src_rows = m; a.out_rows = n; a.out_L = last ? d4 : Lp;
+            if (last) gspmm<EPI_FINAL>(a, Lq, sb.s.max_items, B.val != nullptr, st);
+            else gspmm<EPI_U>(a, Lq, sb.s.max_items, B.val != nullptr, st);
+            if (last && Zhat) {
+                rownorm_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>((const float4 *)Z, n, d4, (float4 *)Zhat);
+                TPO_LAUNCH_CHECK();
+            }
+        } else if (last) {
             a.out_hat = (nslices == 1 && Zhat) ? (float4 *)Zhat : nullptr;
             spmm_launch<EPI_FINAL>(a, sb.s.max_items, sb.s.max_slots, B.val != nullptr, st);
             if (Zhat && nslices > 1) {
@@ -809,7 +1055,7 @@ void shard_start_impl(const double *deg_u, const double *deg_v, int64_t n_p, int
     if (m > 0) inv_sqrt_kernel<<<cdiv(m, TB), TB, 0, st>>>(deg_v, m, s_v);
     TPO_LAUNCH_CHECK();
     const int d4 = (int)(d / 4);
-    if (n_p > 0) init_scaled_kernel<<<cdiv(n_p * d4, TB), TB, 0, st>>>((const float4 *)Xp, s_u, n_p, d4, c, 1, (float4 *)Pp);
+    if (n_p > 0) init_scaled_kernel<<<cdiv(n_p * d4, TB), TB, 0, st>>>((const float4 *)Xp, s_u, n_p, d4, c, 1, (float4 *)Pp, d4);
     TPO_LAUNCH_CHECK();
 }
 

@@ -182,6 +182,19 @@ size_t dgemm_ws(int64_t M, int64_t N, int64_t K);
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU,
               Arena &ar, cudaStream_t st);
 size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k);
+// fp64 tensor-path (DMMA) products of the discretisation (ts64.cu).  ts64_enabled(): TPO_TS64=0
+// selects the CUDA-core kernels of dense.cu / onmf.cu / cluster.cu (A/B measurement only).
+bool ts64_enabled();
+// the DMMA Ups update (den = Ups M): measured slower than ups_update_kernel at k = 50 (1.89 vs
+// 1.64 ms, large); off unless TPO_TS64_UPS=1
+bool ts64_ups_enabled(int k);
+void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int K, int N,
+               const double *cs, double *out, int64_t ldo, cudaStream_t st);
+void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);
+size_t ts_rtu_ws(int64_t n, int64_t D, int k);
+void ts_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
+            cudaStream_t st);
+
 // Ci = S C^{-1} for the b x b Gram g (S g S = C^T C, S = diag(g)^{-1/2}), b <= 128; one CTA;
 // a failed pivot sets *flag (device int) instead of throwing (dgemm.cu).
 void chol_inv_device(const double *g, int64_t b, double *Ci, int *flag, cudaStream_t st);

@@ -7,4 +7,4 @@ Alg. 1 L6; Omega for the randomised SVD of Alg. 2 L1, PAPER.md:540
 The recipes are the SURVEY.md §8(d) readings of BASELINE.json's configs; DESIGN.md
 restates them.
 """
-from .generate import CONFIGS, ABG, make_config, planted_abg, csr_from_edges, random_unit_rows  # noqa: F401
+from .generate import CONFIGS, ABG, make_config, planted_abg, planted_rows, csr_from_edges, random_unit_rows  # noqa: F401

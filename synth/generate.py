@@ -247,6 +247,21 @@ def make_config(name: str, seed: int = 0, **over) -> ABG:
                        x=c["x"], alpha=c["alpha"], T=c["T"], seed=seed, name=name)
 
 
+def planted_rows(n: int, d: int, k: int, seed: int = 0, sigma: float = 1.0):
+    """Planted Gaussian unit rows without a graph: k equal clusters in shuffled order, rows
+    mu_c + sigma N(0, I) L2-normalised (the X recipe of the medium/large/xl configs), standing in
+    for Zhat where a test needs the discretisation's launch shapes at a size whose graph would be
+    too costly to propagate in the oracle.  Returns (rows fp32 [n, d], truth int32 [n])."""
+    cl = (np.arange(n, dtype=np.int64) * k) // n
+    Xp = _draw_X(_rng(seed, "X"), n, d, k, cl, ("gaussian", sigma))
+    perm = _rng(seed, "perm").permutation(n)
+    X = np.empty_like(Xp)
+    X[perm] = Xp
+    truth = np.empty(n, np.int32)
+    truth[perm] = cl.astype(np.int32)
+    return X, truth
+
+
 def random_unit_rows(n: int, d: int, seed: int = 0, zero_rows=()) -> np.ndarray:
     """fp32 rows uniformly on the unit sphere (stage inputs standing in for Z-hat)."""
     r = _rng(seed, "aux").standard_normal((n, d)).astype(np.float32)

@@ -97,6 +97,36 @@ def test_propagate_hubs_isolated(tpo, weighted, d):
     assert np.array_equal(Z, Z2.cpu().numpy()) and np.array_equal(Zh, Zh2.cpu().numpy())
 
 
+@pytest.mark.parametrize("layout", ["0,0", "4,4", "4,8", "8,16", "16,8", "32,32", "32,4"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_propagate_column_group_layouts(tpo, monkeypatch, layout, weighted):
+    """Every column-group layout of the propagation (TPO_SPMM_L = "Lp,Lq": the iterate P and the
+    V-side block Q stored in Lp / Lq-float4 column groups, gathered E = 32 / L edges per load;
+    "0,0" = the row-major slice kernel) on a graph with rows longer than one chunk (the
+    last-arriving-chunk path) and isolated U / V nodes, at d = 128 (4 .. 32-float4 groups) and
+    d = 64: parity with the oracle and bitwise-deterministic re-runs."""
+    monkeypatch.setenv("TPO_SPMM_L", layout)
+    for d in (128, 64):
+        if d == 64 and "32" in layout:
+            continue                              # 32-float4 groups need d4 % 32 == 0
+        h = hub_graph(seed=d + 7, weighted=weighted, d=d)
+        g = G(**h)
+        Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, 0.6, 4, g.B_val)
+        dg = tpo.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, g.B_val, g.Bt_val)
+        Z, Zh = tpo.propagate(dg, torch.from_numpy(g.X).cuda(), 0.6, 4)
+        Z2, Zh2 = tpo.propagate(dg, torch.from_numpy(g.X).cuda(), 0.6, 4)
+        assert torch.equal(Z, Z2) and torch.equal(Zh, Zh2)
+        Z, Zh = Z.cpu().numpy(), Zh.cpu().numpy()
+        assert relF(Z, Zo) <= 1e-5 and relF(Zh, Zho) <= 1e-5
+        for u in (3, 4):   # isolated U keeps X-hat
+            assert np.allclose(Zh[u], g.X[u] / np.linalg.norm(g.X[u]), atol=1e-6)
+        gp = planted_abg(3001, 2005, 5, d, deg=("zipf", 1.3, 120), p_in=0.6, pop=("zipf", 1.2),
+                         x=("gaussian", 1.0), seed=d + 1, weighted=weighted)
+        Zo, _ = O.propagate(gp.n, gp.m, gp.B_rowptr, gp.B_col, gp.X, 0.5, 3, gp.B_val)
+        Z, _ = tpo.propagate(dev_graph(tpo, gp), torch.from_numpy(gp.X).cuda(), 0.5, 3)
+        assert relF(Z.cpu().numpy(), Zo) <= 1e-5
+
+
 def test_propagate_empty_graph(tpo):
     """nnz = 0: every node is isolated, Z = (1 - alpha) X."""
     n, m, d = 37, 5, 8
