@@ -294,6 +294,48 @@ int tpo_shard_nci_assign(const double *U_p, const double *Phi, int64_t n_p, int3
 int tpo_nci_phi(const double *sums, const double *counts, int32_t k, double *Phi, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Evaluation and monitors.
+ * tpo_eval: ARI, NMI and ACC of a predicted labelling against ground truth (Evaluation Metrics,
+ *   PAPER.md:2448-2462): the k_pred x k_true contingency table is counted on the device (exact
+ *   integer counts), the metrics are evaluated from it on the host in fp64; ACC matches
+ *   predicted to true labels with the Hungarian algorithm; NMI is the standard
+ *   sqrt-normalised form (reading R15: the printed numerator omits |U| inside the logarithm).
+ *   pred, truth: n int32 (device), values in [0, k_pred) / [0, k_true);
+ *   metrics: (host) 3 fp64 out {ARI, NMI, ACC}.  k_pred * k_true <= 49152.  [sync]
+ *   Workspace: tpo_eval_ws(k_pred, k_true).  Errors: TPO_EINVAL (also a label out of range).
+ * tpo_objective: the Lemma 4 monitor (Eq. obj5) of a labelling: out[0] =
+ *   ||R^T Y||_F^2 = Tr(Y^T R R^T Y) for the NCI matrix Y of `labels` (columns 1/sqrt|C_l| on C_l;
+ *   the discretisation's objective, <= sum_{l<=k} sigma_l^2 by Ky Fan), and, when Ups (n x k fp64,
+ *   device) is given, out[1] = ||R^T Ups||_F^2, so that |Tr((Y Y^T - Ups Ups^T) R R^T)| =
+ *   |out[0] - out[1]|.  R = diag(dinv) R' as in tpo_cluster.  out: (host) 1 or 2 fp64.  [sync]
+ *   Workspace: tpo_objective_ws(n, D, k).  Errors: TPO_EINVAL (also a label out of range).
+ * Target side V: clustering V instead of U is the same calls with the roles of B
+ *   and B^T swapped and X = X_V: tpo_run(Bt, B, X_V, ...).
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_eval_ws(int32_t k_pred, int32_t k_true);
+int tpo_eval(const int32_t *pred, const int32_t *truth, int64_t n, int32_t k_pred, int32_t k_true, double *metrics,
+             void *ws, size_t ws_bytes, void *stream);
+size_t tpo_objective_ws(int64_t n, int64_t D, int32_t k);
+int tpo_objective(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const int32_t *labels,
+                  const double *Ups, double *out, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * SVD-based attribute dimension reduction (Sec. 3.2.1, Eq. Xd; the step the
+ * paper's default "TPO" runs before Alg. 1): X' = Gamma Sigma of the exact
+ * top-d SVD X ~ Gamma Sigma Psi^T (R14: exact, as R7), computed as X Psi (Psi = top-d
+ * eigenvectors of X^T X; tcgen05 3xTF32 Gram, device subspace iteration, fp64 product), each
+ * column's sign fixed by R8 (column sum >= 0).  Lemma 3 bounds the MSA
+ * error of propagating X' instead of X by sigma_{d+1}^2.  d == d_u copies X (pass-through).
+ *   X: n x d_u fp32 (d_u % 4 == 0);  Xr: n x d fp32 out (the input X of tpo_propagate / tpo_run);
+ *   sigma: (host) d fp64 out (descending singular values of X), or NULL.  1 <= d <= min(n, d_u).
+ * [sync].  Workspace: tpo_svd_reduce_ws(n, d_u, d).
+ * Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA, TPO_ENUMERIC (subspace iteration not converged).
+ * --------------------------------------------------------------------------------------- */
+size_t tpo_svd_reduce_ws(int64_t n, int64_t d_u, int64_t d);
+int tpo_svd_reduce(const float *X, int64_t n, int64_t d_u, int64_t d, float *Xr, double *sigma, void *ws,
+                   size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * Whole hot path (Fig. overview): propagate -> Haar Q from G -> features ->
  * top-k (mode) -> cluster.  G: d x d fp64 on the DEVICE (the Gaussian input of Alg. 1 L6,
  * resident like X; the Haar QR of Alg. 1 L7 runs inside the call, beside the propagation).  Omega: D x (k+p) fp32 (HALKO only, else

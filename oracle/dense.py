@@ -145,6 +145,56 @@ def ari(a, b):
     return float((s_ij - exp) / (mx - exp))
 
 
+def contingency(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    ua, ia = np.unique(a, return_inverse=True)
+    ub, ib = np.unique(b, return_inverse=True)
+    ct = np.zeros((ua.size, ub.size), np.int64)
+    np.add.at(ct, (ia, ib), 1)
+    return ct
+
+
+def nmi(a, b):
+    """Normalised mutual information in the standard sqrt-normalised form
+    sum n_ij log(n n_ij / (a_i b_j)) / sqrt(sum a_i log(a_i / n) * sum b_j log(b_j / n)) (reading R15:
+    the printed numerator omits n inside the logarithm)."""
+    ct = contingency(a, b).astype(np.float64)
+    n = ct.sum()
+    ra, rb = ct.sum(1), ct.sum(0)
+    nz = ct > 0
+    mi = (ct[nz] * np.log(n * ct[nz] / np.outer(ra, rb)[nz])).sum()
+    ha, hb = (ra * np.log(ra / n)).sum(), (rb * np.log(rb / n)).sum()
+    if ha == 0.0 or hb == 0.0:
+        return 1.0 if ha == hb else 0.0
+    return float(mi / np.sqrt(ha * hb))
+
+
+def acc(pred, truth):
+    """Clustering accuracy: the fraction of nodes whose predicted label maps to
+    their true label under the best one-to-one mapping (Hungarian algorithm; scipy's
+    linear_sum_assignment, a library primitive)."""
+    from scipy.optimize import linear_sum_assignment
+    ct = contingency(pred, truth)
+    r, c = linear_sum_assignment(-ct)
+    return float(ct[r, c].sum() / ct.sum())
+
+
+def nci_objective(Rp, dinv, labels, k, Ups=None):
+    """Lemma 4's quantities (Eq. obj5) by explicit construction: S~ = R R^T (n x n),
+    Y the NCI matrix of labels; returns (Tr(Y^T S~ Y), Tr(Ups^T S~ Ups) or None)."""
+    R = np.asarray(dinv, np.float64)[:, None] * np.asarray(Rp, np.float64)
+    S = R @ R.T
+    n = R.shape[0]
+    Y = np.zeros((n, k))
+    for l in range(k):
+        idx = labels == l
+        if idx.any():
+            Y[idx, l] = 1.0 / np.sqrt(idx.sum())
+    t1 = float(np.trace(Y.T @ S @ Y))
+    t2 = None if Ups is None else float(np.trace(np.asarray(Ups).T @ S @ np.asarray(Ups)))
+    return t1, t2
+
+
 def sign_rule(Gm, Ps):
     """R8: flip each pair so that sum_i Gamma[i, l] >= 0; when |sum| < 1e-6 ||.||_1 use
     the sign of the largest-magnitude entry (smallest index among ties)."""

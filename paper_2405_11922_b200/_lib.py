@@ -24,6 +24,7 @@ SYMBOLS = [
     "tpo_shard_atb64", "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final",
     "tpo_shard_onmf_init", "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh",
     "tpo_shard_onmf_u_update", "tpo_shard_nci_assign", "tpo_nci_phi",
+    "tpo_svd_reduce_ws", "tpo_svd_reduce", "tpo_eval_ws", "tpo_eval", "tpo_objective_ws", "tpo_objective",
 ]
 
 TPO_OK, TPO_EINVAL, TPO_ECUDA, TPO_ENOMEM, TPO_ENCCL, TPO_ENUMERIC = 0, -1, -2, -3, -4, -5
@@ -110,6 +111,18 @@ def lib():
     L.tpo_shard_onmf_u_update.argtypes = [vp, vp, vp, i64, i32, vp]
     L.tpo_shard_nci_assign.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp, sz, vp]
     L.tpo_nci_phi.argtypes = [vp, vp, i32, vp, vp]
+    L.tpo_svd_reduce_ws.argtypes = [i64, i64, i64]
+    L.tpo_svd_reduce_ws.restype = sz
+    L.tpo_svd_reduce.argtypes = [vp, i64, i64, i64, vp, vp, vp, sz, vp]
+    L.tpo_svd_reduce.restype = C.c_int
+    L.tpo_eval_ws.argtypes = [i32, i32]
+    L.tpo_eval_ws.restype = sz
+    L.tpo_eval.argtypes = [vp, vp, i64, i32, i32, vp, vp, sz, vp]
+    L.tpo_eval.restype = C.c_int
+    L.tpo_objective_ws.argtypes = [i64, i64, i32]
+    L.tpo_objective_ws.restype = sz
+    L.tpo_objective.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp, sz, vp]
+    L.tpo_objective.restype = C.c_int
     for name in ["tpo_shard_features", "tpo_shard_dinv", "tpo_eig_from_gram", "tpo_shard_gamma", "tpo_shard_atb64",
                  "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final", "tpo_shard_onmf_init",
                  "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh", "tpo_shard_onmf_u_update",

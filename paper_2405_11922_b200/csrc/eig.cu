@@ -303,7 +303,7 @@ __global__ void stack_kernel(const double *__restrict__ u, const double *__restr
 //    = smallest Ritz value of the block) and amplifies the wanted end of the spectrum; the
 //    deflation keeps the lambda = 1 direction from swamping the block.
 void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
-               Arena &ar, cudaStream_t st) {
+               Arena &ar, cudaStream_t st, int power_steps = 6) {
     const int64_t b = std::min<int64_t>(D - 1, k + std::max<int64_t>(k, 16));
     if (b + 1 >= D || D <= 64) {
         std::vector<double> gh = to_host(G, D * D, st), w(D), V(D * k);
@@ -325,7 +325,7 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     double *lam1 = ar.take<double>(1);
     int *flag = ar.take<int>(1);
     TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    for (int it = 0; it < 6; ++it) {
+    for (int it = 0; it < power_steps; ++it) {
         dgemm(false, D, 1, D, 1.0, G, D, u, 1, 0.0, Y0, 1, ar, st);
         power_step_kernel<<<1, 1024, 0, st>>>(Y0, u, D, lam1);
         TPO_LAUNCH_CHECK();
@@ -823,6 +823,70 @@ void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t
     double *W = ar.take<double>(D * b);
     tsgemm_AtB_f32f32(Rp, D, dinv, Y, b, nullptr, n, D, b, W, ar, st);
     tsgemm_AW_f32(Rp, D, dinv, W, n, D, b, out, b, st);
+}
+
+// ---------------------------------------------------------------------------------------
+// f1: SVD-based attribute dimension reduction (Sec. 3.2.1, Eq. Xd):
+// X' = Gamma Sigma of the exact top-d SVD of X (R14), computed as X Psi with Psi the top-d
+// eigenvectors of the d_U x d_U Gram X^T X: the tcgen05 3xTF32 Gram (gram_tc with unit row
+// weights), the device subspace iteration of the top-k solver started from the normalised
+// column sums of X (refined by 30 power steps, then deflated), X Psi on the fp64 tensor path,
+// the sign rule R8 on the columns of X' (X' = Gamma Sigma, so Gamma's rule), rounded to fp32.
+// d == d_U is the pass-through X' = X.
+// ---------------------------------------------------------------------------------------
+__global__ void fill_f32_kernel(float *p, int64_t n, float v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+size_t svd_reduce_ws_bytes(int64_t n, int64_t du, int64_t d) {
+    return topk_eig_ws_bytes(n, du, (int32_t)d, TPO_EIG_EXACT, 0) + align_up(sizeof(double) * n * d) +
+           align_up(sizeof(float) * n) + align_up(sizeof(float) * du * d) + align_up(sizeof(double) * du * d) + 4096;
+}
+
+void svd_reduce_impl(const float *X, int64_t n, int64_t du, int64_t d, float *Xr, double *sigma_host, Arena &ar,
+                     cudaStream_t st) {
+    if (d >= du) {
+        TPO_CUDA(cudaMemcpyAsync(Xr, X, sizeof(float) * n * du, cudaMemcpyDeviceToDevice, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    float *ones = ar.take<float>(n);
+    double *G = ar.take<double>(du * du), *u = ar.take<double>(du), *r = ar.take<double>(du);
+    double *Psi64 = ar.take<double>(du * d), *X64 = ar.take<double>(n * d);
+    float *Psi32 = ar.take<float>(du * d);
+    int *zflag = ar.take<int>(1);
+    fill_f32_kernel<<<cdiv(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(ones, n, 1.0f);
+    TPO_LAUNCH_CHECK();
+    {
+        const size_t mark = ar.off;
+        gram_tc(X, ones, n, du, G, ar, st);              // X^T X
+        ar.off = mark;
+        colsum_f64(X, n, du, r, ar, st);                  // start direction: X^T 1
+        ar.off = mark;
+    }
+    TPO_CUDA(cudaMemsetAsync(zflag, 0, sizeof(int), st));
+    unit_vec_kernel<<<1, 1024, 0, st>>>(r, u, du, zflag);
+    TPO_LAUNCH_CHECK();
+    int zh = 0;
+    TPO_CUDA(cudaMemcpyAsync(&zh, zflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    if (zh) {                                             // zero column sums: start from e_0-ish uniform
+        std::vector<double> h((size_t)du, 1.0 / sqrt((double)du));
+        TPO_CUDA(cudaMemcpyAsync(u, h.data(), sizeof(double) * du, cudaMemcpyHostToDevice, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+    }
+    std::vector<double> lam;
+    gram_topk(G, u, du, (int32_t)d, lam, Psi64, ar, st, 30);
+    if (sigma_host)
+        for (int64_t l = 0; l < d; ++l) sigma_host[l] = sqrt(std::max(lam[l], 0.0));
+    tsgemm_AW_f64(X, du, nullptr, Psi64, n, du, d, X64, d, st);   // X Psi = Gamma Sigma
+    cast_f64_f32<<<cdiv(du * d, 256), 256, 0, st>>>(Psi64, du * d, Psi32);
+    TPO_LAUNCH_CHECK();
+    apply_sign_rule(X64, n, (int)d, Psi32, du, ar, st);
+    cast_f64_f32<<<cdiv(n * d, 256), 256, 0, st>>>(X64, n * d, Xr);
+    TPO_LAUNCH_CHECK();
+    TPO_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace tpo

@@ -312,6 +312,59 @@ int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_
     });
 }
 
+size_t tpo_eval_ws(int32_t k_pred, int32_t k_true) { return eval_ws_bytes(k_pred, k_true); }
+
+int tpo_eval(const int32_t *pred, const int32_t *truth, int64_t n, int32_t k_pred, int32_t k_true, double *metrics,
+             void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 0, "n must be >= 0");
+        TPO_REQUIRE(k_pred >= 1 && k_true >= 1 && (int64_t)k_pred * k_true <= 48 * 1024,
+                    "k_pred, k_true must be >= 1 with k_pred * k_true <= 49152");
+        TPO_REQUIRE(metrics != nullptr, "metrics is NULL");
+        if (n > 0) {
+            TPO_REQUIRE(pred != nullptr, "pred is NULL");
+            TPO_REQUIRE(truth != nullptr, "truth is NULL");
+        }
+        check_ws(ws, ws_bytes, tpo_eval_ws(k_pred, k_true));
+        Arena ar(ws, ws_bytes);
+        eval_impl(pred, truth, n, k_pred, k_true, metrics, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_objective_ws(int64_t n, int64_t D, int32_t k) { return objective_ws_bytes(n, D, k); }
+
+int tpo_objective(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const int32_t *labels,
+                  const double *Ups, double *out, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && D >= 4 && D % 4 == 0, "need n >= 1 and D a positive multiple of 4");
+        TPO_REQUIRE(k >= 1, "k must be >= 1");
+        check_ptr(Rp, "Rp");
+        check_ptr(dinv, "dinv", false);
+        TPO_REQUIRE(labels != nullptr, "labels is NULL");
+        TPO_REQUIRE(out != nullptr, "out is NULL");
+        if (Ups) check_ptr(Ups, "Ups");
+        check_ws(ws, ws_bytes, tpo_objective_ws(n, D, k));
+        Arena ar(ws, ws_bytes);
+        objective_impl(Rp, dinv, n, D, k, labels, Ups, out, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_svd_reduce_ws(int64_t n, int64_t d_u, int64_t d) { return svd_reduce_ws_bytes(n, d_u, d); }
+
+int tpo_svd_reduce(const float *X, int64_t n, int64_t d_u, int64_t d, float *Xr, double *sigma, void *ws,
+                   size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1, "n must be >= 1");
+        TPO_REQUIRE(d_u >= 4 && d_u % 4 == 0, "d_u must be a positive multiple of 4");
+        TPO_REQUIRE(d >= 1 && d <= d_u && d <= n, "d must lie in [1, min(n, d_u)]");
+        check_ptr(X, "X");
+        check_ptr(Xr, "Xr");
+        check_ws(ws, ws_bytes, tpo_svd_reduce_ws(n, d_u, d));
+        Arena ar(ws, ws_bytes);
+        svd_reduce_impl(X, n, d_u, d, Xr, sigma, ar, as_stream(stream));
+    });
+}
+
 size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, int32_t mode, int32_t p) {
     const int64_t D = 2 * d;
     size_t s = 0;

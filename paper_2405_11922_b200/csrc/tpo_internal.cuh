@@ -145,6 +145,17 @@ void nci_assign_part(const double *U, const double *Phi, int64_t n, int k, int32
 size_t nci_assign_part_ws(int64_t n, int k);
 void nci_phi(const double *sums, const double *counts, int k, double *Phi, cudaStream_t st);
 size_t haar_q_ws_bytes(int64_t d);
+// f4 evaluation and monitors (eval.cu)
+size_t eval_ws_bytes(int32_t ka, int32_t kb);
+void eval_impl(const int32_t *pred, const int32_t *truth, int64_t n, int32_t ka, int32_t kb, double *metrics, Arena &ar,
+               cudaStream_t st);
+size_t objective_ws_bytes(int64_t n, int64_t D, int32_t k);
+void objective_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const int32_t *labels,
+                    const double *Ups, double *out, Arena &ar, cudaStream_t st);
+// f1 SVD attribute reduction (eig.cu)
+size_t svd_reduce_ws_bytes(int64_t n, int64_t du, int64_t d);
+void svd_reduce_impl(const float *X, int64_t n, int64_t du, int64_t d, float *Xr, double *sigma_host, Arena &ar,
+                     cudaStream_t st);
 
 // ----------------------------------------------------------------------------------------
 // Dense building blocks (dense.cu)

@@ -62,6 +62,16 @@ class DeviceGraph:
                  None if self.Bt_val is None else self.Bt_val.data_ptr())
         return B, Bt
 
+    def target(self, side: str = "U") -> "DeviceGraph":
+        """The graph oriented for clustering `side`: U as given, or V (the roles of B
+        and B^T swap, X is then X_V).  No copy: the same device CSRs."""
+        if side == "U":
+            return self
+        if side != "V":
+            raise ValueError("target side must be 'U' or 'V'")
+        return DeviceGraph(self.n_v, self.n_u, self.nnz, self.Bt_rowptr, self.Bt_col, self.B_rowptr, self.B_col,
+                           self.Bt_val, self.B_val)
+
 
 def to_device_graph(n_u, n_v, B_rowptr, B_col, Bt_rowptr, Bt_col, B_val=None, Bt_val=None,
                     device="cuda", non_blocking=False) -> DeviceGraph:
@@ -172,6 +182,50 @@ def topk_eig(Rp: torch.Tensor, dinv: torch.Tensor, k: int, mode: int = TPO_EIG_E
     check(L.tpo_topk_eig(_ptr(Rp), _ptr(dinv), n, D, int(k), int(mode), int(p), int(q), _ptr(Omega), _ptr(Gamma),
                          sigma.ctypes.data_as(C.c_void_p), _ptr(Psi), _ptr(ws), ws.numel(), _stream(stream)))
     return Gamma, sigma, Psi
+
+
+def svd_reduce(X: torch.Tensor, d: int, out=None, stream=None):
+    """Sec. 3.2.1 (tpo_svd_reduce): X' = Gamma Sigma of the exact top-d SVD of X (Eq. Xd), sign-fixed;
+    returns (X' [n, d] fp32, sigma np.float64[d] or None on pass-through d == d_u)."""
+    n, du = X.shape
+    _need(X, torch.float32, "X")
+    d = int(d)
+    out = torch.empty((n, du if d >= du else d), dtype=torch.float32, device=X.device) if out is None else out
+    sigma = np.zeros(max(d, 1), np.float64)
+    L = lib()
+    ws = _ws(L.tpo_svd_reduce_ws(n, du, d), X.device)
+    check(L.tpo_svd_reduce(_ptr(X), n, du, d, _ptr(out), sigma.ctypes.data_as(C.c_void_p), _ptr(ws), ws.numel(),
+                           _stream(stream)))
+    return out, (None if d >= du else sigma[:d])
+
+
+def evaluate(pred: torch.Tensor, truth: torch.Tensor, k_pred: int, k_true: int, stream=None) -> dict:
+    """Clustering metrics (tpo_eval): {'ari', 'nmi', 'acc'} of pred vs truth."""
+    _need(pred, torch.int32, "pred")
+    _need(truth, torch.int32, "truth", pred.shape)
+    m = np.zeros(3, np.float64)
+    L = lib()
+    ws = _ws(L.tpo_eval_ws(int(k_pred), int(k_true)), pred.device)
+    check(L.tpo_eval(_ptr(pred), _ptr(truth), pred.numel(), int(k_pred), int(k_true), m.ctypes.data_as(C.c_void_p),
+                     _ptr(ws), ws.numel(), _stream(stream)))
+    return {"ari": float(m[0]), "nmi": float(m[1]), "acc": float(m[2])}
+
+
+def objective(Rp: torch.Tensor, dinv: torch.Tensor, labels: torch.Tensor, k: int, Ups: Optional[torch.Tensor] = None,
+              stream=None):
+    """Lemma 4 monitor (tpo_objective): (||R^T Y||_F^2, ||R^T Ups||_F^2 or None) for the NCI Y of labels."""
+    n, D = Rp.shape
+    _need(Rp, torch.float32, "Rp")
+    _need(dinv, torch.float32, "dinv", (n,))
+    _need(labels, torch.int32, "labels", (n,))
+    if Ups is not None:
+        _need(Ups, torch.float64, "Ups", (n, k))
+    out = np.zeros(2, np.float64)
+    L = lib()
+    ws = _ws(L.tpo_objective_ws(n, D, int(k)), Rp.device)
+    check(L.tpo_objective(_ptr(Rp), _ptr(dinv), n, D, int(k), _ptr(labels), _ptr(Ups), out.ctypes.data_as(C.c_void_p),
+                          _ptr(ws), ws.numel(), _stream(stream)))
+    return float(out[0]), (float(out[1]) if Ups is not None else None)
 
 
 def cluster(Rp: torch.Tensor, dinv: torch.Tensor, Gamma: torch.Tensor, sigma: np.ndarray, Psi: torch.Tensor,

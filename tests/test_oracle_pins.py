@@ -572,3 +572,24 @@ def test_lemma3_bound_on_reduced_propagation():
                 rhs = S[d] ** 2 * np.sqrt(np.outer(du, du)) / (1 - alpha)
                 worst = max(worst, float(np.max(lhs / rhs)))
     assert 0.0 < worst <= 1.0
+
+
+# ----------------------------------------------------------------------------------------------
+# f4 evaluation metrics
+# ----------------------------------------------------------------------------------------------
+
+def test_metrics_worked_examples():
+    """Hand-worked: a = [0,0,1,1], b = [0,1,0,1]: contingency [[1,1],[1,1]] -> ARI = (0 - 2*2/6) /
+    (2 - 2/3) = -1/2, MI = 0 -> NMI = 0, best matching 2 of 4 -> ACC = 1/2.  A relabelled copy
+    scores 1 on all three.  a = [0,0,0,1,1,2], b = [1,1,1,0,0,0]: contingency rows (0: 3 in b=1),
+    (1: 2 in b=0), (2: 1 in b=0) -> ACC = (3 + 2) / 6."""
+    a, b = np.array([0, 0, 1, 1]), np.array([0, 1, 0, 1])
+    assert abs(DN.ari(a, b) + 0.5) < 1e-15 and abs(DN.nmi(a, b)) < 1e-15 and DN.acc(a, b) == 0.5
+    c = np.array([2, 2, 0, 0, 1, 1, 1])
+    d = np.array([0, 0, 1, 1, 2, 2, 2])
+    assert DN.ari(c, d) == 1.0 and abs(DN.nmi(c, d) - 1.0) < 1e-15 and DN.acc(c, d) == 1.0
+    assert abs(DN.acc(np.array([0, 0, 0, 1, 1, 2]), np.array([1, 1, 1, 0, 0, 0])) - 5 / 6) < 1e-15
+    # NMI by hand for a = [0,0,1,1], b = [0,0,0,1]: a_i = (2,2), b_j = (3,1), n_ij = [[2,0],[1,1]]
+    mi = 2 * math.log(4 * 2 / (2 * 3)) + 1 * math.log(4 * 1 / (2 * 3)) + 1 * math.log(4 * 1 / (2 * 1))
+    ha, hb = 2 * 2 * math.log(2 / 4), 3 * math.log(3 / 4) + math.log(1 / 4)
+    assert abs(DN.nmi(np.array([0, 0, 1, 1]), np.array([0, 0, 0, 1])) - mi / math.sqrt(ha * hb)) < 1e-15
