@@ -277,7 +277,7 @@ def run_sharded(args, g, ws, rank, local, dev):
 
     def step():
         Q = T.haar_q_dev(g.G, device=dev)
-        _, Zh = propagate_sharded(ops, coll, Xp, g.alpha, g.T)
+        _, Zh = propagate_sharded(ops, coll, Xp, g.alpha, g.T, exchange=args.exchange)
         lab, _ = solve_sharded(sops, coll, Zh, Q, sh.u0, args.tf, args.tg)
         return lab
 
@@ -308,7 +308,9 @@ def run_sharded(args, g, ws, rank, local, dev):
     tot_ms = float(t.item())
     units = 2.0 * g.nnz * g.d * g.T
     cfg = config_dict(g, args, ws)
-    cfg["parallelism"] = f"U-rows sharded over {ws} rank(s) (NCCL RS/AG per hop, all-reduced solver partials)"
+    cfg["parallelism"] = (f"U-rows sharded over {ws} rank(s) ("
+                          + ("NCCL RS/AG of the V block" if args.exchange == "full" else "NCCL all-to-all of touched V rows")
+                          + " per hop, all-reduced solver partials)")
     line = {"metric": metric_name(), "value": units * args.steps / (tot_ms / 1e3), "unit": "nnz*d/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic", "config": cfg,
@@ -328,6 +330,9 @@ def main():
     ap.add_argument("--tf", type=int, default=5)
     ap.add_argument("--tg", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="full", choices=["full", "touched"],
+                    help="sharded mode: per-hop exchange of the whole V block (reduce-scatter + all-gather) or of "
+                         "the touched V rows only (all-to-all, SURVEY.md §8f #2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default=None, choices=["replicas", "sharded"],
                     help="N > 1: one graph with its U rows sharded across the ranks (default: strong scaling, "

@@ -122,6 +122,21 @@ int tpo_shard_uside(const tpo_csr_t *Bp, const float *Q, const float *Xp, int64_
                     size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Touched-row exchange of the sharded propagation: instead of reduce-scattering
+ * and all-gathering the whole m x d V-side block, rank p sends only the rows of V its U slice
+ * touches (the non-empty rows of Btp) to their owners and receives back only those rows of Q;
+ * the caller runs the all-to-all exchanges (NCCL / gloo) and these row movers pack / unpack them.
+ *   tpo_rows_gather:  dst[i] = src[idx[i]]            (nidx rows of d floats)
+ *   tpo_rows_scatter: dst[idx[i]] = src[i], or += when accumulate != 0; idx must not repeat
+ *                     within one call (the caller adds the ranks' blocks one call at a time, in
+ *                     rank order: a fixed summation order).
+ * d % 4 == 0; src / dst 16-byte aligned device pointers; idx device int32.  Errors: TPO_EINVAL.
+ * --------------------------------------------------------------------------------------- */
+int tpo_rows_gather(const float *src, const int32_t *idx, int64_t nidx, int64_t d, float *dst, void *stream);
+int tpo_rows_scatter(float *dst, const int32_t *idx, int64_t nidx, int64_t d, const float *src, int32_t accumulate,
+                     void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * a4  Haar rotation, Alg. 1 L6-7: Q = the Q factor of the QR
  * decomposition of the d x d Gaussian matrix G, sign-fixed so that diag(R) > 0, which
  * makes Q Haar-distributed and unique.  Host-only, fp64.

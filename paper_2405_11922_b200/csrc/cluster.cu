@@ -555,7 +555,7 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     const int64_t nb = cdiv(std::max<int64_t>(n, 1), cluster_rows_per_block(n));
     ar.take<double>(nb * k * k);
     ar.take<int64_t>(nb * k);
-    return ar.off + std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)) + 4096;
+    return ar.off + std::max(std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)), ts_atb_ws(k, k)) + 4096;
 }
 
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
@@ -583,13 +583,15 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     for (int t = 0; t < Tf; ++t) {
         onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
         ar.off = mark;
-        dgemm(true, k, k, n, 1.0, U, k, U, k, 0.0, UtU, k, ar, st);
+        if (ts64_enabled() && k <= 104) ts_atb_f64(U, k, U, k, n, k, k, UtU, ar, st);
+        else dgemm(true, k, k, n, 1.0, U, k, U, k, 0.0, UtU, k, ar, st);
         ar.off = mark;
         h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
         TPO_LAUNCH_CHECK();
         std::swap(H, Hn);
         tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
-        dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
+        if (ts64_enabled() && k <= 104) ts_atb_f64(U, k, RH, k, n, k, k, M, ar, st);
+        else dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;
         if (ts64_ups_enabled(k)) {
             ts_ups_update(U, RH, M, n, k, st);

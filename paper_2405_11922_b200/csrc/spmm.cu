@@ -1076,6 +1076,45 @@ void shard_vside_impl(const tpo_csr_t &Btp, const float *Pp, int64_t d, float *Q
     spmm_launch<EPI_RAW>(a, sb.s.max_items, sb.s.max_slots, Btp.val != nullptr, st);
 }
 
+// Row movers of the touched-row exchange: dst[i] = src[idx[i]] and
+// dst[idx[i]] (+)= src[i] for d/4 float4 per row (idx unique within one call: no races).
+namespace {
+__global__ void rows_gather_kernel(const float4 *__restrict__ src, const int32_t *__restrict__ idx, int64_t nidx,
+                                   int d4, float4 *__restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nidx * d4) return;
+    const int64_t r = i / d4;
+    const int c = (int)(i - r * d4);
+    dst[i] = src[(int64_t)idx[r] * d4 + c];
+}
+__global__ void rows_scatter_kernel(float4 *__restrict__ dst, const int32_t *__restrict__ idx, int64_t nidx, int d4,
+                                    const float4 *__restrict__ src, int accumulate) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nidx * d4) return;
+    const int64_t r = i / d4;
+    const int c = (int)(i - r * d4);
+    float4 *p = dst + (int64_t)idx[r] * d4 + c;
+    const float4 v = src[i];
+    if (accumulate) *p = f4add(*p, v);
+    else *p = v;
+}
+}  // namespace
+
+void rows_gather_impl(const float *src, const int32_t *idx, int64_t nidx, int64_t d, float *dst, cudaStream_t st) {
+    if (nidx == 0) return;
+    const int d4 = (int)(d / 4);
+    rows_gather_kernel<<<cdiv(nidx * d4, 256), 256, 0, st>>>((const float4 *)src, idx, nidx, d4, (float4 *)dst);
+    TPO_LAUNCH_CHECK();
+}
+void rows_scatter_impl(float *dst, const int32_t *idx, int64_t nidx, int64_t d, const float *src, bool accumulate,
+                       cudaStream_t st) {
+    if (nidx == 0) return;
+    const int d4 = (int)(d / 4);
+    rows_scatter_kernel<<<cdiv(nidx * d4, 256), 256, 0, st>>>((float4 *)dst, idx, nidx, d4, (const float4 *)src,
+                                                               accumulate ? 1 : 0);
+    TPO_LAUNCH_CHECK();
+}
+
 void shard_vscale_impl(float *Q, const float *s_v, int64_t rows, int64_t d, cudaStream_t st) {
     const int d4 = (int)(d / 4);
     if (rows == 0) return;

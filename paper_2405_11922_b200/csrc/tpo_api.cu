@@ -312,6 +312,31 @@ int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_
     });
 }
 
+int tpo_rows_gather(const float *src, const int32_t *idx, int64_t nidx, int64_t d, float *dst, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(nidx >= 0 && d >= 4 && d % 4 == 0, "need nidx >= 0 and d a positive multiple of 4");
+        if (nidx > 0) {
+            check_ptr(src, "src");
+            check_ptr(dst, "dst");
+            TPO_REQUIRE(idx != nullptr, "idx is NULL");
+        }
+        rows_gather_impl(src, idx, nidx, d, dst, as_stream(stream));
+    });
+}
+
+int tpo_rows_scatter(float *dst, const int32_t *idx, int64_t nidx, int64_t d, const float *src, int32_t accumulate,
+                     void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(nidx >= 0 && d >= 4 && d % 4 == 0, "need nidx >= 0 and d a positive multiple of 4");
+        if (nidx > 0) {
+            check_ptr(src, "src");
+            check_ptr(dst, "dst");
+            TPO_REQUIRE(idx != nullptr, "idx is NULL");
+        }
+        rows_scatter_impl(dst, idx, nidx, d, src, accumulate != 0, as_stream(stream));
+    });
+}
+
 size_t tpo_eval_ws(int32_t k_pred, int32_t k_true) { return eval_ws_bytes(k_pred, k_true); }
 
 int tpo_eval(const int32_t *pred, const int32_t *truth, int64_t n, int32_t k_pred, int32_t k_true, double *metrics,

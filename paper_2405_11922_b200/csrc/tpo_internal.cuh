@@ -145,6 +145,10 @@ void nci_assign_part(const double *U, const double *Phi, int64_t n, int k, int32
 size_t nci_assign_part_ws(int64_t n, int k);
 void nci_phi(const double *sums, const double *counts, int k, double *Phi, cudaStream_t st);
 size_t haar_q_ws_bytes(int64_t d);
+// touched-row exchange row movers (spmm.cu)
+void rows_gather_impl(const float *src, const int32_t *idx, int64_t nidx, int64_t d, float *dst, cudaStream_t st);
+void rows_scatter_impl(float *dst, const int32_t *idx, int64_t nidx, int64_t d, const float *src, bool accumulate,
+                       cudaStream_t st);
 // f4 evaluation and monitors (eval.cu)
 size_t eval_ws_bytes(int32_t ka, int32_t kb);
 void eval_impl(const int32_t *pred, const int32_t *truth, int64_t n, int32_t ka, int32_t kb, double *metrics, Arena &ar,
@@ -199,6 +203,10 @@ bool ts64_enabled();
 // the DMMA Ups update (den = Ups M): measured slower than ups_update_kernel at k = 50 (1.89 vs
 // 1.64 ms, large); off unless TPO_TS64_UPS=1
 bool ts64_ups_enabled(int k);
+size_t ts_atb_ws(int p, int q);
+// out (p x q) = A^T B for n x p / n x q fp64 A, B (p, q <= 104) on the fp64 tensor path
+void ts_atb_f64(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, double *out,
+                Arena &ar, cudaStream_t st);
 void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int K, int N,
                const double *cs, double *out, int64_t ldo, cudaStream_t st);
 void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);

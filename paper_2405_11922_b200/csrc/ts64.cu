@@ -291,6 +291,94 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restric
     }
 }
 
+// part[b] = A^T B over the rows of split b (A: n x p, B: n x q, fp64, p, q <= 128): the k x k
+// products of Alg. 2 (Ups^T Ups, Ups^T (R H)).  Output tiles (mt, nt) of 8 x 8: warp w owns the
+// m-tiles w, w + 8 (< ceil(p/8)) against every n-tile; the row index is the reduction dimension,
+// staged 32 rows at a time.
+constexpr int AB_BK = 32;
+constexpr int AB_MAXT = 16;         // up to 128 columns
+template <int MT, int NTT>          // m-tiles per warp (1 or 2), n-tiles (<= 16)
+__global__ void __launch_bounds__(DM_NT, 1) dm_atb_kernel(const double *__restrict__ A, int64_t lda,
+                                                          const double *__restrict__ B, int64_t ldb, int64_t n, int p,
+                                                          int q, int64_t rows_per, double *__restrict__ part) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr int PW = 8 * AB_MAXT + 4, QW = 8 * NTT + 4;      // padded widths (fragment reads)
+    double *As = reinterpret_cast<double *>(dsm);               // [2][AB_BK][PW]
+    double *Bs = As + 2 * AB_BK * PW;                           // [2][AB_BK][QW]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+    const int64_t i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
+    auto load = [&](int64_t b, int buf) {
+        double *as = As + (size_t)buf * AB_BK * PW, *bs = Bs + (size_t)buf * AB_BK * QW;
+        for (int idx = tid; idx < AB_BK * p; idx += DM_NT) {
+            const int r = idx / p, c = idx - (idx / p) * p;
+            const bool v = b + r < i1;
+            cp8(as + r * PW + c, v ? A + (b + r) * lda + c : A, v);
+        }
+        for (int idx = tid; idx < AB_BK * q; idx += DM_NT) {
+            const int r = idx / q, c = idx - (idx / q) * q;
+            const bool v = b + r < i1;
+            cp8(bs + r * QW + c, v ? B + (b + r) * ldb + c : B, v);
+        }
+        cp_commit();
+    };
+    // zero the padding columns once (never written by the loads)
+    for (int idx = tid; idx < 2 * AB_BK * PW; idx += DM_NT) As[idx] = 0.0;
+    for (int idx = tid; idx < 2 * AB_BK * QW; idx += DM_NT) Bs[idx] = 0.0;
+    __syncthreads();
+    double acc[MT][NTT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int t = 0; t < NTT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+    const int mtiles = (p + 7) / 8;
+    if (i0 < i1) {
+        load(i0, 0);
+        cp_wait_all();
+        __syncthreads();
+        int buf = 0;
+        for (int64_t b = i0; b < i1; b += AB_BK) {
+            const bool more = b + AB_BK < i1;
+            if (more) load(b + AB_BK, buf ^ 1);
+            const double *as = As + (size_t)buf * AB_BK * PW + gc * PW + gr;
+            const double *bs = Bs + (size_t)buf * AB_BK * QW + gc * QW + gr;
+#pragma unroll
+            for (int k4 = 0; k4 < AB_BK / 4; ++k4) {
+                double af[MT], bf[NTT];
+#pragma unroll
+                for (int m = 0; m < MT; ++m) {
+                    const int mt = w + 8 * m;
+                    af[m] = mt < mtiles ? as[k4 * 4 * PW + mt * 8] : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < NTT; ++t) bf[t] = bs[k4 * 4 * QW + t * 8];
+#pragma unroll
+                for (int m = 0; m < MT; ++m)
+#pragma unroll
+                    for (int t = 0; t < NTT; ++t) dmma(acc[m][t], af[m], bf[t]);
+            }
+            if (more) {
+                cp_wait_all();
+                __syncthreads();
+                buf ^= 1;
+            }
+        }
+    }
+    double *pp = part + (int64_t)blockIdx.x * p * q;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+        const int row = (w + 8 * m) * 8 + gr;
+        if (row >= p) continue;
+#pragma unroll
+        for (int t = 0; t < NTT; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = t * 8 + 2 * gc + h;
+                if (col < q) pp[(int64_t)row * q + col] = acc[m][t][h];
+            }
+    }
+}
+
 __global__ void reduce_parts_kernel(const double *__restrict__ part, int64_t G, int64_t len, double *__restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= len) return;
@@ -354,6 +442,39 @@ void dm_rtu_launch(const float *Rp, int64_t n, int D, const float *dinv, const d
 }
 
 }  // namespace
+
+namespace {
+template <int MT, int NTT>
+void dm_atb_launch(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, int64_t rows_per,
+                   int G, double *part, cudaStream_t st) {
+    const size_t sm = 2 * sizeof(double) * ((size_t)AB_BK * (8 * AB_MAXT + 4) + (size_t)AB_BK * (8 * NTT + 4));
+    TPO_CUDA(cudaFuncSetAttribute(dm_atb_kernel<MT, NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dm_atb_kernel<MT, NTT><<<G, DM_NT, sm, st>>>(A, lda, B, ldb, n, p, q, rows_per, part);
+    TPO_LAUNCH_CHECK();
+}
+template <int NTT>
+void dm_atb_mt(int mt, const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q,
+               int64_t rows_per, int G, double *part, cudaStream_t st) {
+    if (mt <= 8) dm_atb_launch<1, NTT>(A, lda, B, ldb, n, p, q, rows_per, G, part, st);
+    else dm_atb_launch<2, NTT>(A, lda, B, ldb, n, p, q, rows_per, G, part, st);
+}
+}  // namespace
+
+size_t ts_atb_ws(int p, int q) { return align_up(sizeof(double) * (size_t)sm_count_cached() * p * q) + 256; }
+
+// out (p x q fp64) = A^T B, A n x p, B n x q fp64 (p, q <= 128): fixed-order split over rows
+void ts_atb_f64(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, double *out,
+                Arena &ar, cudaStream_t st) {
+    const int64_t rows_per = cdiv(cdiv(std::max<int64_t>(n, 1), sm_count_cached()), AB_BK) * AB_BK;
+    const int G = (int)cdiv(std::max<int64_t>(n, 1), rows_per);
+    const size_t mark = ar.off;
+    double *part = ar.take<double>((size_t)G * p * q);
+    const int mt = (p + 7) / 8;
+    TPO_NT13(dm_atb_mt, (q + 7) / 8, mt, A, lda, B, ldb, n, p, q, rows_per, G, part, st);
+    reduce_parts_kernel<<<cdiv((int64_t)p * q, 256), 256, 0, st>>>(part, G, (int64_t)p * q, out);
+    TPO_LAUNCH_CHECK();
+    ar.off = mark;
+}
 
 bool ts64_enabled() {
     const char *e = getenv("TPO_TS64");
