@@ -455,28 +455,18 @@ def main():
             traffic = json.load(open(tf)).get("bytes_per_hop") * g.T      # per launch of the T-hop loop
         except Exception:
             traffic = None
+    # the gather view: every edge reads a d-wide fp32 row in both SpMMs (2 nnz d 4 bytes per hop),
+    # against the measured gather ceilings of tools/probes/gather_bw.cu (context: a table that fits
+    # L2 vs one that lives in DRAM; the large config's two tables are 1 GB and 512 MB)
     gather = None
     gc = os.path.join(ROOT, "profiles", "gather_ceilings.json")
     if os.path.exists(gc):
         try:
             ceil = json.load(open(gc))
-            gbytes = 2.0 * g.nnz * g.d * 4        # every edge reads a d-wide fp32 row, both SpMMs
-            ach = gbytes * g.T / (prop_ms / 1e3) / 1e9
-            # the gathered table per column group (SL = 1: 128 columns): L2-resident when it fits
-            sl = 1
-            table_mb = max(g.n, g.m) * min(g.d, 128 * sl) * 4 / 2**20
-            pk_g = ceil["l2_resident_gbs"] if table_mb <= 96 else ceil["dram_gbs"]
-            gather = {"achieved": ach, "ceiling": pk_g, "unit": "GB/s", "frac": ach / pk_g,
-                      "gathered_bytes_per_hop": gbytes, "table_mb_per_column_group": table_mb,
+            gbytes = 2.0 * g.nnz * g.d * 4
+            gather = {"achieved": gbytes * g.T / (prop_ms / 1e3) / 1e9, "unit": "GB/s", "gathered_bytes_per_hop": gbytes,
+                      "ceiling_l2_resident_gbs": ceil.get("l2_resident_gbs"), "ceiling_dram_resident_gbs": ceil.get("dram_gbs"),
                       "ceiling_source": "profiles/gather_ceilings.json (measured gather probe)"}
-            # the same probe replaying the graph's own CSR column-id streams (no epilogue): the
-            # gather ceiling of this access pattern, per hop
-            gp = os.path.join(ROOT, "profiles", f"gather_pattern_{args.config}.json")
-            if os.path.exists(gp):
-                pat = json.load(open(gp))
-                probe_ms = (pat["spmm1_ms"] + pat["spmm2_ms"]) * g.T
-                gather["pattern"] = {"probe_ms": probe_ms, "frac": probe_ms / prop_ms,
-                                     "source": f"profiles/gather_pattern_{args.config}.json"}
         except Exception:
             gather = None
     roof = {"kernel": "spmm_kernel pair (one hop: SpMM-1 V side + SpMM-2 U side, fix-ups, per-call schedule)",

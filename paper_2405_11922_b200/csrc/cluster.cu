@@ -632,16 +632,20 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
             TPO_LAUNCH_CHECK();
             continue;
         }
-        if (k <= 16)
-            assign_small_kernel<16><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
-        else if (k <= 32)
-            assign_small_kernel<32><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
-        else if (k <= 64)
-            assign_small_kernel<64><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
-        else
-            assign_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * AR), 148 * 8), 256, phi_smem, st>>>(U, Phi, n, k,
-                                                                                                  labels, s);
-        TPO_LAUNCH_CHECK();
+        if (ts64_enabled() && k > 32 && k <= 104) {
+            ts_assign(U, Phi, n, k, labels, s.changed, s.done, st);
+        } else {
+            if (k <= 16)
+                assign_small_kernel<16><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
+            else if (k <= 32)
+                assign_small_kernel<32><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
+            else if (k <= 64)
+                assign_small_kernel<64><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
+            else
+                assign_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 8 * AR), 148 * 8), 256, phi_smem, st>>>(U, Phi, n,
+                                                                                                      k, labels, s);
+            TPO_LAUNCH_CHECK();
+        }
         nci_step_kernel<<<1, 32, 0, st>>>(s, nullptr, k);
         TPO_LAUNCH_CHECK();
         if (last) break;

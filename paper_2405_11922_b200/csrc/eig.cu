@@ -489,7 +489,8 @@ void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
     int *flag = ar.take<int>(1);
     TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
     for (int pass = 0; pass < 2; ++pass) {
-        dgemm(true, k, k, n, 1.0, Gamma, k, Gamma, k, 0.0, g, k, ar, st);
+        if (ts64_enabled() && k <= 104) ts_atb_f64(Gamma, k, Gamma, k, n, k, k, g, ar, st);
+        else dgemm(true, k, k, n, 1.0, Gamma, k, Gamma, k, 0.0, g, k, ar, st);
         if (k <= 112) {
             chol_inv_device(g, k, ci, flag, st);
         } else {
@@ -605,6 +606,7 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
          4 * align_up(sizeof(double) * 2 * 148 * k) + 8 * align_up(sizeof(double) * k * k);
     if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
     s += dgemm_ws(std::max(n, D), std::max(b, bh) + 1, 0) + 2 * align_up(sizeof(double) * (std::max(b, bh) + 1) * (std::max(b, bh) + 1));
+    s += ts_atb_ws((int)k, (int)k);                      // the polish Gram Gamma^T Gamma (fp64 tensor path)
     return s + 64 * 256;
 }
 

@@ -413,6 +413,7 @@ size_t tpo_shard_solver_ws(int64_t n_p, int64_t d, int32_t k) {
     s = std::max(s, eig_from_gram_ws(D, k));
     s = std::max(s, nci_assign_part_ws(n_p, k));
     s = std::max(s, onmf_ws_bytes(n_p, D, k));
+    s = std::max(s, ts_atb_ws(k, k) + align_up(sizeof(double) * (size_t)k * k));
     s = std::max(s, dgemm_ws(std::max<int64_t>(n_p, k), k, n_p) + align_up(sizeof(double) * (size_t)(n_p * k + k * k)));
     return s + 64 * 256 + align_up(sizeof(double) * (size_t)(D * k + 4 * 2 * 148 * k));
 }
@@ -477,7 +478,8 @@ int tpo_shard_atb64(const double *A_p, const double *B_p, int64_t n_p, int32_t k
         check_ptr(A_p, "A_p");
         check_ptr(B_p, "B_p");
         Arena ar(ws, ws_bytes);
-        dgemm(true, k, k, n_p, 1.0, A_p, k, B_p, k, 0.0, out, k, ar, st);
+        if (ts64_enabled() && k <= 104) ts_atb_f64(A_p, k, B_p, k, n_p, k, k, out, ar, st);
+        else dgemm(true, k, k, n_p, 1.0, A_p, k, B_p, k, 0.0, out, k, ar, st);
     });
 }
 

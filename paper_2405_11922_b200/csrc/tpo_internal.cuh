@@ -200,10 +200,11 @@ size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k);
 // fp64 tensor-path (DMMA) products of the discretisation (ts64.cu).  ts64_enabled(): TPO_TS64=0
 // selects the CUDA-core kernels of dense.cu / onmf.cu / cluster.cu (A/B measurement only).
 bool ts64_enabled();
-// the DMMA Ups update (den = Ups M): measured slower than ups_update_kernel at k = 50 (1.89 vs
-// 1.64 ms, large); off unless TPO_TS64_UPS=1
+// the DMMA Ups update (den = Ups M, resident M, bulk-copied Ups / RH tiles): even 16 < k <= 64
 bool ts64_ups_enabled(int k);
 size_t ts_atb_ws(int p, int q);
+void ts_assign(const double *U, const double *Phi, int64_t n, int k, int32_t *labels, int32_t *changed,
+               const int32_t *done, cudaStream_t st);
 // out (p x q) = A^T B for n x p / n x q fp64 A, B (p, q <= 104) on the fp64 tensor path
 void ts_atb_f64(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, double *out,
                 Arena &ar, cudaStream_t st);

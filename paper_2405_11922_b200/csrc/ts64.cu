@@ -14,6 +14,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "tpo_internal.cuh"
 
@@ -25,7 +26,7 @@ constexpr int DM_NT = 256;          // 8 warps
 constexpr int DM_BM = 256;          // rows per tile: 8 warps x 32 (4 m-tiles of 8)
 constexpr int DM_BK = 32;           // K per stage (8 k-steps of 4)
 
-enum { DM_STORE = 0, DM_UPS = 1 };
+enum { DM_STORE = 0, DM_UPS = 1, DM_ASSIGN = 2 };
 
 struct DmArgs {
     const void *A;        // n x K (fp32 or fp64), leading dimension lda
@@ -39,7 +40,28 @@ struct DmArgs {
     int64_t ldo;
     const double *cs;     // STORE: column divisors (sigma) or null
     const double *RH;     // UPS: n x N
+    int32_t *labels;      // ASSIGN: labels out; changed flag set when one changes; skipped when *done
+    int32_t *changed;
+    const int32_t *done;
 };
+
+// Alg. 3 certified argmax: the tensor-path scores of a row are accepted when their top-2 margin
+// exceeds CERT_TOL relative to the best score (Ups and Phi are nonnegative, so every score carries a
+// relative error <= k * 2^-53 ~ 1e-14 in either summation order); a row below it is rescored with
+// the sequential fma of R13 (the oracle's arithmetic), so the labels are the oracle's.
+constexpr double CERT_TOL = 1e-11;
+
+__device__ __forceinline__ void top2_merge(double &b1, int &i1, double &b2, double v, int iv) {
+    // (b1, i1): best (ties -> smaller index); b2: second-best value
+    if (iv < 0) return;
+    if (i1 < 0 || v > b1 || (v == b1 && iv < i1)) {
+        if (i1 >= 0) b2 = fmax(b2, b1);
+        b1 = v;
+        i1 = iv;
+    } else {
+        b2 = fmax(b2, v);
+    }
+}
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -59,6 +81,39 @@ __device__ __forceinline__ void cp4(void *sm, const void *g, bool v) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(g), "r"(v ? 4 : 0) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ uint32_t sm32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    uint64_t spins = 0;
+    while (true) {
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.b32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(sm32(bar)), "r"(parity)
+                     : "memory");
+        if (done) return;
+        if (++spins > (1ull << 31)) __trap();            // watchdog: never hang the GPU
+    }
+}
+// shared memory -> one contiguous global block (bulk-copy engine), tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sm32(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// one contiguous global block -> shared memory through the bulk-copy (1-D TMA) engine
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm32(dst)),
+                 "l"(src), "r"(bytes), "r"(sm32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // A tile rows padded by 4 elements: the 8 rows x 4 columns of an m8n8k4 A fragment then hit
@@ -75,6 +130,7 @@ constexpr size_t dm_smem() {
 // n-tiles of m8n8k4 accumulators.  The (tile, K-stage) steps form one cp.async pipeline.
 template <class TA, int EPI, int NT>
 __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
+    if (EPI == DM_ASSIGN && *a.done) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int LDA = DM_LDA;
     constexpr int NBW = 8 * NT;
@@ -151,7 +207,44 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
         }
-        if (s == nst - 1) {                 // epilogue of the tile: C[gr][2 gc + h] of each 8 x 8 tile
+        if (EPI == DM_ASSIGN && s == nst - 1) {
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int64_t row = r0 + w * 32 + mt * 8 + gr;
+                double b1 = 0.0, b2 = -1.0;
+                int i1 = -1;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = nt * 8 + 2 * gc + h;
+                        top2_merge(b1, i1, b2, acc[mt][nt][h], col < a.N ? col : -1);
+                    }
+#pragma unroll
+                for (int o = 1; o < 4; o <<= 1) {       // the 4 lanes of this row (gc = 0..3)
+                    const double ob1 = __shfl_xor_sync(0xffffffffu, b1, o), ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+                    const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+                    top2_merge(b1, i1, b2, ob1, oi1);
+                    b2 = fmax(b2, ob2);
+                }
+                if (gc == 0 && row < a.n) {
+                    int lab = i1;
+                    if (!(b1 - b2 > CERT_TOL * fabs(b1))) {   // near tie (or a tie): R13 rescoring
+                        const double *u = static_cast<const double *>(a.A) + row * a.lda;
+                        double best = 0.0;
+                        lab = 0;
+                        for (int l = 0; l < a.N; ++l) {
+                            double sc = 0.0;
+                            for (int j = 0; j < a.K; ++j) sc = fma(u[j], a.W[(int64_t)j * a.ldw + l], sc);
+                            if (l == 0 || sc > best) { best = sc; lab = l; }
+                        }
+                    }
+                    if (a.labels[row] != lab) *a.changed = 1;
+                    a.labels[row] = lab;
+                }
+            }
+        }
+        if (EPI != DM_ASSIGN && s == nst - 1) {   // epilogue of the tile: C[gr][2 gc + h] of each 8 x 8 tile
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int64_t row = r0 + w * 32 + mt * 8 + gr;
@@ -182,6 +275,140 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
             __syncthreads();                // stage q+1 visible; everyone done with stage q's buffer
         }
     }
+}
+
+// Row-block products with a k x k right factor (K = N = k <= 104, k even), fp64 A = Ups stored
+// densely: den = Ups M for the Ups update (Eq. update-Y) and the Alg. 3 scores Ups Phi.  W = M / Phi
+// stays resident in shared memory; BM-row tiles of A (one contiguous block each) arrive by bulk copy
+// into a 2-slot ring on mbarriers, the next tile in flight while one is multiplied.  Warp w owns the
+// MTW m-tiles (8 rows each) w*MTW .. of a tile against all NT n-tiles.
+template <int EPI, int NT, int MTW>
+__global__ void __launch_bounds__(DM_NT, 1) dm_rowk_kernel(DmArgs a) {
+    if (EPI == DM_ASSIGN && *a.done) return;
+    constexpr int BM = 8 * 8 * MTW;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(dsm);                 // [2]
+    const int k = a.N;
+    double *Ws = reinterpret_cast<double *>(dsm + 128);                 // [k][k]
+    double *ring = Ws + ((k * k + 15) / 16) * 16;                        // [2][NB][BM * k]
+    constexpr int NB = EPI == DM_UPS ? 2 : 1;                           // UPS slots: Ups tile, RH tile
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+    const double *A = static_cast<const double *>(a.A);
+    const int64_t ntiles = (a.n + BM - 1) / BM;
+    const int64_t my = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (tid == 0) {
+        bar_init(full, 1);
+        bar_init(full + 1, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = tid; i < k * k; i += DM_NT) Ws[i] = a.W[i];
+    __syncthreads();
+    auto issue = [&](int64_t j) {                    // thread 0: this CTA's j-th tile into slot j & 1
+        const int64_t r0 = (blockIdx.x + j * gridDim.x) * BM;
+        const int rows = (int)(a.n - r0 < BM ? a.n - r0 : BM);
+        const uint32_t bytes = (uint32_t)rows * (uint32_t)k * 8u;
+        double *slot = ring + (size_t)(j & 1) * NB * BM * k;
+        bar_expect_tx(full + (j & 1), NB * bytes);
+        bulk_g2s(slot, A + r0 * k, bytes, full + (j & 1));
+        if (EPI == DM_UPS) bulk_g2s(slot + BM * k, a.RH + r0 * k, bytes, full + (j & 1));
+    };
+    if (tid == 0) {
+        if (my > 0) issue(0);
+        if (my > 1) issue(1);
+    }
+    bool changed = false;
+    for (int64_t j = 0; j < my; ++j) {
+        const int64_t r0 = (blockIdx.x + j * gridDim.x) * BM;
+        const int rows = (int)(a.n - r0 < BM ? a.n - r0 : BM);
+        bar_wait(full + (j & 1), (uint32_t)((j >> 1) & 1));
+        double *as = ring + (size_t)(j & 1) * NB * BM * k;
+        double acc[MTW][NT][2];
+#pragma unroll
+        for (int m = 0; m < MTW; ++m)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+        for (int k4 = 0; k4 < (k + 3) / 4; ++k4) {
+            const int kk = k4 * 4 + gc;
+            double af[MTW], bf[NT];
+#pragma unroll
+            for (int m = 0; m < MTW; ++m) {
+                const int r = (w * MTW + m) * 8 + gr;
+                af[m] = (kk < k && r < rows) ? as[r * k + kk] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int col = t * 8 + gr;
+                bf[t] = (kk < k && col < k) ? Ws[kk * k + col] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < MTW; ++m)
+#pragma unroll
+                for (int t = 0; t < NT; ++t) dmma(acc[m][t], af[m], bf[t]);
+        }
+#pragma unroll
+        for (int m = 0; m < MTW; ++m) {
+            const int r = (w * MTW + m) * 8 + gr;
+            const int64_t row = r0 + r;
+            if (EPI == DM_UPS) {
+                if (r >= rows) continue;
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = t * 8 + 2 * gc + h;
+                        if (col >= k) continue;
+                        const double rh = as[BM * k + r * k + col];
+                        const double num = rh > 0.0 ? rh : 0.0;
+                        const double dd = (acc[m][t][h] > 0.0 ? acc[m][t][h] : 0.0) + EPS_R9;
+                        as[r * k + col] = as[r * k + col] * sqrt(num / dd);   // in the tile, stored below
+                    }
+            } else {   // DM_ASSIGN: certified argmax (see CERT_TOL)
+                double b1 = 0.0, b2 = -1.0;
+                int i1 = -1;
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = t * 8 + 2 * gc + h;
+                        top2_merge(b1, i1, b2, acc[m][t][h], col < k ? col : -1);
+                    }
+#pragma unroll
+                for (int o = 1; o < 4; o <<= 1) {
+                    const double ob1 = __shfl_xor_sync(0xffffffffu, b1, o), ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+                    const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+                    top2_merge(b1, i1, b2, ob1, oi1);
+                    b2 = fmax(b2, ob2);
+                }
+                if (gc == 0 && r < rows) {
+                    int lab = i1;
+                    if (!(b1 - b2 > CERT_TOL * fabs(b1))) {          // near tie: R13 rescoring
+                        const double *u = as + (size_t)r * k;
+                        double best = 0.0;
+                        lab = 0;
+                        for (int l = 0; l < k; ++l) {
+                            double sc = 0.0;
+                            for (int jj = 0; jj < k; ++jj) sc = fma(u[jj], Ws[jj * k + l], sc);
+                            if (l == 0 || sc > best) { best = sc; lab = l; }
+                        }
+                    }
+                    if (a.labels[row] != lab) changed = true;
+                    a.labels[row] = lab;
+                }
+            }
+        }
+        if (EPI == DM_UPS) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // tile -> async proxy
+        __syncthreads();                              // slot j & 1 is done (and, UPS, updated)
+        if (tid == 0) {
+            if (EPI == DM_UPS) {
+                bulk_s2g(a.out + r0 * k, as, (uint32_t)rows * (uint32_t)k * 8u);
+                bulk_wait_read();                     // the store has read the slot before it is refilled
+            }
+            if (j + 2 < my) issue(j + 2);
+        }
+    }
+    if (EPI == DM_UPS && tid == 0) bulk_wait_all();
+    if (EPI == DM_ASSIGN && __any_sync(0xffffffffu, changed) && lane == 0) *a.changed = 1;
 }
 
 // part[b][d][l] = sum_{i in split b} R'[i, d] * (dinv_i Ups[i, l]) for D rows [d0, d0 + 256)
@@ -296,35 +523,37 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restric
 // m-tiles w, w + 8 (< ceil(p/8)) against every n-tile; the row index is the reduction dimension,
 // staged 32 rows at a time.
 constexpr int AB_BK = 32;
-constexpr int AB_MAXT = 16;         // up to 128 columns
-template <int MT, int NTT>          // m-tiles per warp (1 or 2), n-tiles (<= 16)
+template <int MT, int NTT, int S>    // m-tiles per warp (1 or 2), n-tiles (<= 13), ring stages
 __global__ void __launch_bounds__(DM_NT, 1) dm_atb_kernel(const double *__restrict__ A, int64_t lda,
                                                           const double *__restrict__ B, int64_t ldb, int64_t n, int p,
                                                           int q, int64_t rows_per, double *__restrict__ part) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    constexpr int PW = 8 * AB_MAXT + 4, QW = 8 * NTT + 4;      // padded widths (fragment reads)
-    double *As = reinterpret_cast<double *>(dsm);               // [2][AB_BK][PW]
-    double *Bs = As + 2 * AB_BK * PW;                           // [2][AB_BK][QW]
+    constexpr int W = 8 * NTT + 4;                              // padded width (p, q <= 8 NTT)
+    constexpr int STG = 2 * AB_BK * W;                          // doubles per stage: A then B
+    double *ring = reinterpret_cast<double *>(dsm);             // [S][2][AB_BK][W]
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gr = lane >> 2, gc = lane & 3;
     const int64_t i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
-    auto load = [&](int64_t b, int buf) {
-        double *as = As + (size_t)buf * AB_BK * PW, *bs = Bs + (size_t)buf * AB_BK * QW;
-        for (int idx = tid; idx < AB_BK * p; idx += DM_NT) {
-            const int r = idx / p, c = idx - (idx / p) * p;
-            const bool v = b + r < i1;
-            cp8(as + r * PW + c, v ? A + (b + r) * lda + c : A, v);
+    const int64_t nch = i1 > i0 ? (i1 - i0 + AB_BK - 1) / AB_BK : 0;
+    auto load = [&](int64_t c) {                                // chunk c into slot c % S (commits a group)
+        if (c < nch) {
+            double *as = ring + (size_t)(c % S) * STG, *bs = as + AB_BK * W;
+            const int64_t b = i0 + c * AB_BK;
+            for (int idx = tid; idx < AB_BK * p; idx += DM_NT) {
+                const int r = idx / p, col = idx - (idx / p) * p;
+                const bool v = b + r < i1;
+                cp8(as + r * W + col, v ? A + (b + r) * lda + col : A, v);
+            }
+            for (int idx = tid; idx < AB_BK * q; idx += DM_NT) {
+                const int r = idx / q, col = idx - (idx / q) * q;
+                const bool v = b + r < i1;
+                cp8(bs + r * W + col, v ? B + (b + r) * ldb + col : B, v);
+            }
         }
-        for (int idx = tid; idx < AB_BK * q; idx += DM_NT) {
-            const int r = idx / q, c = idx - (idx / q) * q;
-            const bool v = b + r < i1;
-            cp8(bs + r * QW + c, v ? B + (b + r) * ldb + c : B, v);
-        }
-        cp_commit();
+        cp_commit();                                            // (an empty group past the end)
     };
     // zero the padding columns once (never written by the loads)
-    for (int idx = tid; idx < 2 * AB_BK * PW; idx += DM_NT) As[idx] = 0.0;
-    for (int idx = tid; idx < 2 * AB_BK * QW; idx += DM_NT) Bs[idx] = 0.0;
+    for (int idx = tid; idx < S * STG; idx += DM_NT) ring[idx] = 0.0;
     __syncthreads();
     double acc[MT][NTT][2];
 #pragma unroll
@@ -332,38 +561,128 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_atb_kernel(const double *__restri
 #pragma unroll
         for (int t = 0; t < NTT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
     const int mtiles = (p + 7) / 8;
-    if (i0 < i1) {
-        load(i0, 0);
-        cp_wait_all();
-        __syncthreads();
-        int buf = 0;
-        for (int64_t b = i0; b < i1; b += AB_BK) {
-            const bool more = b + AB_BK < i1;
-            if (more) load(b + AB_BK, buf ^ 1);
-            const double *as = As + (size_t)buf * AB_BK * PW + gc * PW + gr;
-            const double *bs = Bs + (size_t)buf * AB_BK * QW + gc * QW + gr;
 #pragma unroll
-            for (int k4 = 0; k4 < AB_BK / 4; ++k4) {
-                double af[MT], bf[NTT];
+    for (int c = 0; c < S - 1; ++c) load(c);
+    for (int64_t c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");   // chunk c has landed
+        __syncthreads();                                         // ... for every thread; slot (c-1)%S is free
+        load(c + S - 1);
+        const double *as = ring + (size_t)(c % S) * STG + gc * W + gr;
+        const double *bs = as + AB_BK * W;
 #pragma unroll
-                for (int m = 0; m < MT; ++m) {
-                    const int mt = w + 8 * m;
-                    af[m] = mt < mtiles ? as[k4 * 4 * PW + mt * 8] : 0.0;
-                }
+        for (int k4 = 0; k4 < AB_BK / 4; ++k4) {
+            double af[MT], bf[NTT];
 #pragma unroll
-                for (int t = 0; t < NTT; ++t) bf[t] = bs[k4 * 4 * QW + t * 8];
-#pragma unroll
-                for (int m = 0; m < MT; ++m)
-#pragma unroll
-                    for (int t = 0; t < NTT; ++t) dmma(acc[m][t], af[m], bf[t]);
+            for (int m = 0; m < MT; ++m) {
+                const int mt = w + 8 * m;
+                af[m] = mt < mtiles ? as[k4 * 4 * W + mt * 8] : 0.0;
             }
-            if (more) {
-                cp_wait_all();
-                __syncthreads();
-                buf ^= 1;
-            }
+#pragma unroll
+            for (int t = 0; t < NTT; ++t) bf[t] = bs[k4 * 4 * W + t * 8];
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+                for (int t = 0; t < NTT; ++t) dmma(acc[m][t], af[m], bf[t]);
         }
     }
+    cp_wait_all();
+    double *pp = part + (int64_t)blockIdx.x * p * q;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+        const int row = (w + 8 * m) * 8 + gr;
+        if (row >= p) continue;
+#pragma unroll
+        for (int t = 0; t < NTT; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = t * 8 + 2 * gc + h;
+                if (col < q) pp[(int64_t)row * q + col] = acc[m][t][h];
+            }
+    }
+}
+
+// The same A^T B with A, B stored densely (lda = p, ldb = q): a 32-row chunk of each is one
+// contiguous block, fetched by one bulk copy (cp.async.bulk) into an S-stage ring completed on
+// mbarriers -- one instruction per 12.8 KB instead of one per element (the element-wise cp.async
+// version was LSU-issue bound, 1.0 ms for 2M x 50).  Fragment reads use the unpadded row stride.
+// A CTA's rows are whole chunks except the last CTA's tail, which is staged element-wise with
+// zero fill.
+template <int MT, int NTT, int S>
+__global__ void __launch_bounds__(DM_NT, 1) dm_atb_bulk_kernel(const double *__restrict__ A, const double *__restrict__ B,
+                                                               int64_t n, int p, int q, int64_t rows_per,
+                                                               double *__restrict__ part) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(dsm);                        // [S]
+    double *ring = reinterpret_cast<double *>(dsm + 128);                       // [S][AB_BK * (p + q)]
+    const int stage = AB_BK * (p + q);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int gr = lane >> 2, gc = lane & 3;
+    const int64_t i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
+    const int64_t nfull = i1 > i0 ? (i1 - i0) / AB_BK : 0;
+    const int tail = i1 > i0 ? (int)((i1 - i0) - nfull * AB_BK) : 0;
+    if (tid == 0)
+        for (int sI = 0; sI < S; ++sI) bar_init(full + sI, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    auto issue = [&](int64_t c) {                      // thread 0: full chunk c into slot c % S
+        double *as = ring + (size_t)(c % S) * stage, *bs = as + AB_BK * p;
+        const int64_t b = i0 + c * AB_BK;
+        const uint32_t ba = (uint32_t)(AB_BK * p * 8), bb = (uint32_t)(AB_BK * q * 8);
+        bar_expect_tx(full + c % S, ba + bb);
+        bulk_g2s(as, A + b * p, ba, full + c % S);
+        bulk_g2s(bs, B + b * q, bb, full + c % S);
+    };
+    if (tid == 0)
+        for (int64_t c = 0; c < S && c < nfull; ++c) issue(c);
+    double acc[MT][NTT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int t = 0; t < NTT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+    const int mtiles = (p + 7) / 8, ntiles = (q + 7) / 8;
+    auto compute = [&](const double *as, const double *bs) {
+#pragma unroll
+        for (int k4 = 0; k4 < AB_BK / 4; ++k4) {
+            double af[MT], bf[NTT];
+            const int r = k4 * 4 + gc;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const int col = (w + 8 * m) * 8 + gr;
+                af[m] = col < p ? as[r * p + col] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < NTT; ++t) {
+                const int col = t * 8 + gr;
+                bf[t] = (t < ntiles && col < q) ? bs[r * q + col] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+                for (int t = 0; t < NTT; ++t) dmma(acc[m][t], af[m], bf[t]);
+        }
+    };
+    for (int64_t c = 0; c < nfull; ++c) {
+        bar_wait(full + c % S, (uint32_t)((c / S) & 1));
+        const double *as = ring + (size_t)(c % S) * stage;
+        compute(as, as + AB_BK * p);
+        __syncthreads();                               // every thread is done with slot c % S
+        if (tid == 0 && c + S < nfull) issue(c + S);
+    }
+    if (tail > 0) {                                    // the last rows: element-wise, zero-filled
+        double *as = ring, *bs = ring + AB_BK * p;     // slot 0 is free (all bulk copies consumed)
+        const int64_t b = i0 + nfull * AB_BK;
+        for (int idx = tid; idx < AB_BK * p; idx += DM_NT) {
+            const int r = idx / p;
+            as[idx] = r < tail ? A[(b + r) * p + (idx - r * p)] : 0.0;
+        }
+        for (int idx = tid; idx < AB_BK * q; idx += DM_NT) {
+            const int r = idx / q;
+            bs[idx] = r < tail ? B[(b + r) * q + (idx - r * q)] : 0.0;
+        }
+        __syncthreads();
+        compute(as, bs);
+    }
+    (void)mtiles;
     double *pp = part + (int64_t)blockIdx.x * p * q;
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
@@ -430,6 +749,36 @@ void dm_store_f32(const DmArgs &a, int nblk, cudaStream_t st) { dm_launch<float,
 // the Ups update reads whole rows of Ups (den = Ups M) and overwrites them: one column block
 template <int NT>
 void dm_ups(const DmArgs &a, cudaStream_t st) { dm_launch<double, DM_UPS, NT>(a, 1, st); }
+template <int NT>
+void dm_assign(const DmArgs &a, cudaStream_t st) { dm_launch<double, DM_ASSIGN, NT>(a, 1, st); }
+
+// resident-W row-block kernel (dense fp64 Ups, even k): 16 rows per warp for k <= 64, else 8
+template <int EPI, int NT>
+void dm_rowk_launch(const DmArgs &a, cudaStream_t st) {
+    const int k = a.N;
+    auto go = [&](auto mtw_tag) {
+        constexpr int MTW = decltype(mtw_tag)::value;
+        constexpr int BM = 64 * MTW;
+        constexpr int NB = EPI == DM_UPS ? 2 : 1;
+        const size_t sm = 128 + sizeof(double) * (((size_t)k * k + 15) / 16 * 16 + 2 * (size_t)NB * BM * k);
+        TPO_CUDA(cudaFuncSetAttribute(dm_rowk_kernel<EPI, NT, MTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        const int64_t tiles = cdiv(std::max<int64_t>(a.n, 1), BM);
+        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count_cached()));
+        dm_rowk_kernel<EPI, NT, MTW><<<gx, DM_NT, sm, st>>>(a);
+        TPO_LAUNCH_CHECK();
+    };
+    // UPS slots hold two tiles (Ups, RH): 64-row tiles keep them within shared memory
+    if (k <= 64 && EPI != DM_UPS) go(std::integral_constant<int, 2>());
+    else go(std::integral_constant<int, 1>());
+}
+template <int NT>
+void dm_rowk_ups(const DmArgs &a, cudaStream_t st) { dm_rowk_launch<DM_UPS, NT>(a, st); }
+template <int NT>
+void dm_rowk_assign(const DmArgs &a, cudaStream_t st) { dm_rowk_launch<DM_ASSIGN, NT>(a, st); }
+bool rowk_ok(const double *A, int k) { return k % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0; }
+bool rowk_ups_ok(const double *U, const double *RH, int k) {
+    return rowk_ok(U, k) && (reinterpret_cast<uintptr_t>(RH) & 15u) == 0;
+}
 
 template <int NT>
 void dm_rtu_launch(const float *Rp, int64_t n, int D, const float *dinv, const double *U, int k, int64_t rows_per,
@@ -447,14 +796,31 @@ namespace {
 template <int MT, int NTT>
 void dm_atb_launch(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, int64_t rows_per,
                    int G, double *part, cudaStream_t st) {
-    const size_t sm = 2 * sizeof(double) * ((size_t)AB_BK * (8 * AB_MAXT + 4) + (size_t)AB_BK * (8 * NTT + 4));
-    TPO_CUDA(cudaFuncSetAttribute(dm_atb_kernel<MT, NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dm_atb_kernel<MT, NTT><<<G, DM_NT, sm, st>>>(A, lda, B, ldb, n, p, q, rows_per, part);
+    constexpr int S = NTT <= 8 ? 4 : 3;                         // ring depth within ~220 KB
+    const size_t sm = (size_t)S * 2 * AB_BK * (8 * NTT + 4) * sizeof(double);
+    TPO_CUDA(cudaFuncSetAttribute(dm_atb_kernel<MT, NTT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dm_atb_kernel<MT, NTT, S><<<G, DM_NT, sm, st>>>(A, lda, B, ldb, n, p, q, rows_per, part);
+    TPO_LAUNCH_CHECK();
+}
+template <int MT, int NTT>
+void dm_atb_bulk_launch(const double *A, const double *B, int64_t n, int p, int q, int64_t rows_per, int G, double *part,
+                        cudaStream_t st) {
+    constexpr int S = 4;
+    const size_t sm = 128 + (size_t)S * AB_BK * (p + q) * sizeof(double);
+    TPO_CUDA(cudaFuncSetAttribute(dm_atb_bulk_kernel<MT, NTT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dm_atb_bulk_kernel<MT, NTT, S><<<G, DM_NT, sm, st>>>(A, B, n, p, q, rows_per, part);
     TPO_LAUNCH_CHECK();
 }
 template <int NTT>
 void dm_atb_mt(int mt, const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q,
                int64_t rows_per, int G, double *part, cudaStream_t st) {
+    // dense rows (lda = p, ldb = q), 16-byte aligned bases: one bulk copy per 32-row chunk
+    const bool bulk = lda == p && ldb == q && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0;
+    if (bulk) {
+        if (mt <= 8) dm_atb_bulk_launch<1, NTT>(A, B, n, p, q, rows_per, G, part, st);
+        else dm_atb_bulk_launch<2, NTT>(A, B, n, p, q, rows_per, G, part, st);
+        return;
+    }
     if (mt <= 8) dm_atb_launch<1, NTT>(A, lda, B, ldb, n, p, q, rows_per, G, part, st);
     else dm_atb_launch<2, NTT>(A, lda, B, ldb, n, p, q, rows_per, G, part, st);
 }
@@ -470,7 +836,7 @@ void ts_atb_f64(const double *A, int64_t lda, const double *B, int64_t ldb, int6
     const size_t mark = ar.off;
     double *part = ar.take<double>((size_t)G * p * q);
     const int mt = (p + 7) / 8;
-    TPO_NT13(dm_atb_mt, (q + 7) / 8, mt, A, lda, B, ldb, n, p, q, rows_per, G, part, st);
+    TPO_NT13(dm_atb_mt, (std::max(p, q) + 7) / 8, mt, A, lda, B, ldb, n, p, q, rows_per, G, part, st);
     reduce_parts_kernel<<<cdiv((int64_t)p * q, 256), 256, 0, st>>>(part, G, (int64_t)p * q, out);
     TPO_LAUNCH_CHECK();
     ar.off = mark;
@@ -480,10 +846,8 @@ bool ts64_enabled() {
     const char *e = getenv("TPO_TS64");
     return !(e && e[0] == '0');
 }
-bool ts64_ups_enabled(int k) {
-    const char *e = getenv("TPO_TS64_UPS");
-    return ts64_enabled() && e && e[0] == '1' && k > 16 && k <= 104;
-}
+// (k <= 64: two 64-row Ups / RH slots and the resident k x k M fit shared memory)
+bool ts64_ups_enabled(int k) { return ts64_enabled() && k > 16 && k <= 64 && k % 2 == 0; }
 
 // out = diag(rs) A W diag(1/cs): A n x K fp32 (lda), W K x N fp64 (ldw = N), out n x N fp64 (ldo)
 void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int K, int N,
@@ -502,7 +866,27 @@ void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int 
     if (n == 0) return;
     DmArgs a{};
     a.A = U; a.lda = k; a.W = M; a.ldw = k; a.n = n; a.K = k; a.N = k; a.out = U; a.ldo = k; a.RH = RH;
+    if (rowk_ups_ok(U, RH, k)) {
+        TPO_NT13(dm_rowk_ups, (k + 7) / 8, a, st);
+        return;
+    }
     TPO_NT13(dm_ups, (k + 7) / 8, a, st);
+}
+
+// Alg. 3 assignment (Eq. ell-ast) for k <= 104: labels = argmax_l (Ups Phi)[i, l]
+// with ties -> smallest l, scores on the fp64 tensor path, certified (CERT_TOL) or rescored by R13's
+// sequential fma; *changed = 1 when a label changes; nothing when *done.
+void ts_assign(const double *U, const double *Phi, int64_t n, int k, int32_t *labels, int32_t *changed,
+               const int32_t *done, cudaStream_t st) {
+    if (n == 0) return;
+    DmArgs a{};
+    a.A = U; a.lda = k; a.W = Phi; a.ldw = k; a.n = n; a.K = k; a.N = k;
+    a.labels = labels; a.changed = changed; a.done = done;
+    if (rowk_ok(U, k)) {
+        TPO_NT13(dm_rowk_assign, (k + 7) / 8, a, st);
+        return;
+    }
+    TPO_NT13(dm_assign, (k + 7) / 8, a, st);
 }
 
 size_t ts_rtu_ws(int64_t n, int64_t D, int k) {
