@@ -12,7 +12,8 @@
  *    Dense float/double device buffers must be 16-byte aligned.
  *  - Ownership: the caller allocates and owns every buffer; the library never frees
  *    caller memory and keeps no pointer after a call returns.  The only objects the
- *    library owns are the opaque communicator handles of tpo_comm_create.
+ *    library owns are the opaque communicator handles of tpo_comm_create (freed by
+ *    tpo_comm_destroy).
  *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Calls enqueue on it and return without synchronising, except those marked [sync],
  *    which copy small fp64 matrices to the host, factor them there and copy back; [sync]
@@ -135,6 +136,27 @@ int tpo_shard_uside(const tpo_csr_t *Bp, const float *Q, const float *Xp, int64_
 int tpo_rows_gather(const float *src, const int32_t *idx, int64_t nidx, int64_t d, float *dst, void *stream);
 int tpo_rows_scatter(float *dst, const int32_t *idx, int64_t nidx, int64_t d, const float *src, int32_t accumulate,
                      void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Library-owned NCCL communicator and the sharded propagation with its
+ * collectives inside the library (§8e).  NCCL is resolved at run time (libnccl.so.2, e.g. the copy
+ * PyTorch loaded); TPO_ENCCL when it is unavailable or a call fails.
+ *   tpo_comm_unique_id: (host) 128-byte ncclUniqueId out (rank 0 creates it and shares it).
+ *   tpo_comm_create:    one communicator per rank on `device`; *comm is an opaque handle owned by
+ *                       the library until tpo_comm_destroy.
+ *   tpo_propagate_sharded: a1-a3 for the rank's U slice (Bp = its rows of B with global V ids,
+ *                       Btp = Bp^T with local U ids, Xp its rows of X) on `stream`: all-reduce of the
+ *                       V degrees, then per hop B_p^T P_p -> ncclReduceScatter over V slices ->
+ *                       s_v^2 -> ncclAllGather -> U side; Zp (n_p x d) raw Z, Zhat_p rownorm or NULL.
+ *                       The same result as tpo_propagate on the whole graph.  Workspace:
+ *                       tpo_propagate_sharded_ws(n_p, n_v, nnz_p, d, world).
+ * --------------------------------------------------------------------------------------- */
+int tpo_comm_unique_id(void *id);
+int tpo_comm_create(const void *id, int32_t rank, int32_t world, int32_t device, void **comm);
+int tpo_comm_destroy(void *comm);
+size_t tpo_propagate_sharded_ws(int64_t n_p, int64_t n_v, int64_t nnz_p, int64_t d, int32_t world);
+int tpo_propagate_sharded(void *comm, const tpo_csr_t *Bp, const tpo_csr_t *Btp, const float *Xp, int64_t d, float alpha,
+                          int32_t T, float *Zp, float *Zhat_p, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * a4  Haar rotation, Alg. 1 L6-7: Q = the Q factor of the QR

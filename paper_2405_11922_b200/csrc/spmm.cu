@@ -1115,6 +1115,17 @@ void rows_scatter_impl(float *dst, const int32_t *idx, int64_t nidx, int64_t d, 
     TPO_LAUNCH_CHECK();
 }
 
+// T = 0 on a shard: Z = c X, Zhat = rownorm(Z) (no exchange)
+void propagate_local_t0(const float *Xp, int64_t n_p, int64_t d, float alpha, float *Zp, float *Zhat_p, cudaStream_t st) {
+    if (n_p == 0) return;
+    const int d4 = (int)(d / 4);
+    const float c = alpha < 1.0f ? 1.0f - alpha : 1.0f;
+    init_scaled_kernel<<<cdiv(n_p * d4, 256), 256, 0, st>>>((const float4 *)Xp, nullptr, n_p, d4, c, 0, (float4 *)Zp, d4);
+    TPO_LAUNCH_CHECK();
+    if (Zhat_p) rownorm_kernel<<<cdiv(n_p * 32, 256), 256, 0, st>>>((const float4 *)Zp, n_p, d4, (float4 *)Zhat_p);
+    TPO_LAUNCH_CHECK();
+}
+
 void shard_vscale_impl(float *Q, const float *s_v, int64_t rows, int64_t d, cudaStream_t st) {
     const int d4 = (int)(d / 4);
     if (rows == 0) return;

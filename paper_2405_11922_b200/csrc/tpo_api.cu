@@ -312,6 +312,53 @@ int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_
     });
 }
 
+int tpo_comm_unique_id(void *id) {
+    return guarded([&] {
+        TPO_REQUIRE(id != nullptr, "id is NULL");
+        comm_unique_id(id);
+    });
+}
+
+int tpo_comm_create(const void *id, int32_t rank, int32_t world, int32_t device, void **comm) {
+    return guarded([&] {
+        TPO_REQUIRE(id != nullptr && comm != nullptr, "id / comm is NULL");
+        TPO_REQUIRE(world >= 1 && rank >= 0 && rank < world, "need 0 <= rank < world");
+        *comm = comm_create(id, rank, world, device);
+    });
+}
+
+int tpo_comm_destroy(void *comm) {
+    return guarded([&] { comm_destroy(comm); });
+}
+
+size_t tpo_propagate_sharded_ws(int64_t n_p, int64_t n_v, int64_t nnz_p, int64_t d, int32_t world) {
+    return propagate_sharded_ws_bytes(n_p, n_v, nnz_p, d, std::max<int32_t>(world, 1));
+}
+
+int tpo_propagate_sharded(void *comm, const tpo_csr_t *Bp, const tpo_csr_t *Btp, const float *Xp, int64_t d, float alpha,
+                          int32_t T, float *Zp, float *Zhat_p, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(comm != nullptr, "comm is NULL");
+        check_csr(Bp, "Bp");
+        check_csr(Btp, "Btp");
+        TPO_REQUIRE(Bp->n_rows == Btp->n_cols && Bp->n_cols == Btp->n_rows && Bp->nnz == Btp->nnz,
+                    "Btp is not shaped as the transpose of Bp");
+        TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
+        TPO_REQUIRE(T >= 0, "T must be >= 0");
+        check_gather_range(Btp->n_cols, d, "Pp (gathered by the V-side SpMM)");
+        check_gather_range(Bp->n_cols, d, "Q (gathered by the U-side SpMM)");
+        if (Bp->n_rows) {
+            check_ptr(Xp, "Xp");
+            check_ptr(Zp, "Zp");
+        }
+        if (Zhat_p) check_ptr(Zhat_p, "Zhat_p");
+        check_ws(ws, ws_bytes, tpo_propagate_sharded_ws(Bp->n_rows, Bp->n_cols, Bp->nnz, d, comm_world(comm)));
+        Arena ar(ws, ws_bytes);
+        propagate_sharded_impl(comm, *Bp, *Btp, Xp, d, alpha, T, Zp, Zhat_p, ar, as_stream(stream));
+    });
+}
+
 int tpo_rows_gather(const float *src, const int32_t *idx, int64_t nidx, int64_t d, float *dst, void *stream) {
     return guarded([&] {
         TPO_REQUIRE(nidx >= 0 && d >= 4 && d % 4 == 0, "need nidx >= 0 and d a positive multiple of 4");

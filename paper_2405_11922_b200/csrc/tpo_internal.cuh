@@ -96,6 +96,16 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
                     int reserve_launches = 1 << 30);
 // sharded propagation pieces (spmm.cu)
 size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d);
+void propagate_local_t0(const float *Xp, int64_t n_p, int64_t d, float alpha, float *Zp, float *Zhat_p, cudaStream_t st);
+// library-owned NCCL communicator (comm.cu)
+void comm_unique_id(void *id);
+void *comm_create(const void *id, int rank, int world, int device);
+void comm_destroy(void *comm);
+int comm_world(const void *comm);
+int comm_rank(const void *comm);
+size_t propagate_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, int world);
+void propagate_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, const float *Xp, int64_t d,
+                            float alpha, int32_t T, float *Zp, float *Zhat_p, Arena &ar, cudaStream_t st);
 void shard_degrees_impl(const tpo_csr_t &Bp, const tpo_csr_t &Btp, double *deg_u, double *deg_v, cudaStream_t st);
 void shard_start_impl(const double *deg_u, const double *deg_v, int64_t n_p, int64_t m, const float *Xp, int64_t d,
                       float alpha, float *s_u, float *s_v, float *Pp, cudaStream_t st);

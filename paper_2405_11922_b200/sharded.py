@@ -319,6 +319,54 @@ def _propagate_touched(ops, coll, Xp, alpha, T, want_zhat):
     return Z, Zhat
 
 
+class NcclComm:
+    """A libtpo-owned NCCL communicator (tpo_comm_create / tpo_comm_destroy).  `uid` is the 128-byte
+    ncclUniqueId rank 0 created with NcclComm.unique_id() and shared with the other ranks."""
+
+    def __init__(self, rank: int, world: int, device, uid: bytes):
+        self.rank, self.world = rank, world
+        self.device = torch.device(device)
+        buf = C.create_string_buffer(bytes(uid), 128)
+        h = C.c_void_p()
+        check(lib().tpo_comm_create(buf, int(rank), int(world), int(self.device.index or 0), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().tpo_comm_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.h:
+            check(lib().tpo_comm_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def propagate_sharded_lib(comm: NcclComm, ops: "GpuShardOps", Xp: torch.Tensor, alpha: float, T: int,
+                          want_zhat: bool = True, stream=None):
+    """Sharded a1-a3 with the collectives inside libtpo (tpo_propagate_sharded on the library's NCCL
+    communicator): returns (Z_p, Zhat_p)."""
+    s = ops.s
+    d = Xp.shape[1]
+    Z = torch.empty_like(Xp)
+    Zh = torch.empty_like(Xp) if want_zhat else None
+    L = lib()
+    ws = torch.empty(max(int(L.tpo_propagate_sharded_ws(s.n_p, s.m, s.nnz, d, comm.world)), 256), dtype=torch.uint8,
+                     device=Xp.device)
+    B, Bt = ops._csr("B"), ops._csr("Bt")
+    st = C.c_void_p((stream or torch.cuda.current_stream(Xp.device)).cuda_stream)
+    check(L.tpo_propagate_sharded(comm.h, C.byref(B), C.byref(Bt), ops._p(Xp), d, float(alpha), int(T), ops._p(Z),
+                                  ops._p(Zh), ops._p(ws), ws.numel(), st))
+    return Z, Zh
+
+
 # ------------------------------------------------------------------------------------------
 # a5-a9 on row shards (SURVEY.md §8e: "an all-reduce of the d x k Gram matrices"): every
 # D x D, D x k and k x k quantity is the all-reduced sum of the shards' partials, so each rank

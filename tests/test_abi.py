@@ -73,6 +73,9 @@ def test_validation_errors_without_gpu(L):
     assert rc == TPO_EINVAL and b"32-bit gather offsets" in L.tpo_last_error()
     rc = L.tpo_topk_eig(16, 16, 100, 8, 9, 0, 0, 0, None, 16, None, 16, 256, 1 << 30, None)
     assert rc == TPO_EINVAL and b"k must" in L.tpo_last_error()
+    h = C.c_void_p()
+    rc = L.tpo_comm_create(C.create_string_buffer(128), 2, 2, 0, C.byref(h))   # rank >= world
+    assert rc == TPO_EINVAL and b"rank" in L.tpo_last_error()
     rc = L.tpo_svd_reduce(16, 100, 64, 65, 16, None, 256, 1 << 30, None)       # d > d_u
     assert rc == TPO_EINVAL and b"d must" in L.tpo_last_error()
     rc = L.tpo_svd_reduce(16, 100, 62, 8, 16, None, 256, 1 << 30, None)        # d_u % 4

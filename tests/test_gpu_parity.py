@@ -190,6 +190,23 @@ def test_features(tpo, n, d):
     assert torch.equal(Rp, Rp2) and torch.equal(dv, dv2)
 
 
+def test_features_wide_d(tpo):
+    """d = 4096 (D = 8192): dinv's r staging needs 64 KB of dynamic shared memory, above the default
+    48 KB opt-in limit.  Q is any orthogonal matrix (numpy QR of a Gaussian; features take Q as input)."""
+    n, d = 300, 4096
+    Zh = random_unit_rows(n, d, seed=41)
+    Q = np.linalg.qr(np.random.default_rng(42).standard_normal((d, d)))[0].astype(np.float32)
+    Rpo, dvo, ro = O.features(Zh, Q)
+    Rp, dv, r = tpo.features(torch.from_numpy(Zh).cuda(), torch.from_numpy(Q).cuda(), want_r=True)
+    # the sin / cos arguments sqrt(d) Zhat Q^T grow as sqrt(d) (up to 64 here) and their fp32 rounding
+    # with them: the fp32-vs-fp64 tolerance is scaled from the 1e-5 of d <= 256 by sqrt(d / 256)
+    tol = 1e-5 * np.sqrt(d / 256)
+    assert relF(Rp.cpu().numpy(), Rpo) <= tol
+    assert relF(dv.cpu().numpy(), dvo) <= tol
+    assert relF(r.cpu().numpy(), ro) <= tol
+    assert np.allclose(np.sum(Rp.double().cpu().numpy() ** 2, axis=1), np.e, rtol=1e-5)   # F1
+
+
 # ------------------------------------------------------------------------------------------
 # a6-a7 implicit affinity and top-k
 # ------------------------------------------------------------------------------------------

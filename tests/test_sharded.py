@@ -236,3 +236,28 @@ def test_row_movers_gpu():
     ops.unpack(dst, idx, out, False)
     ref[idx.long()] = out
     assert torch.equal(dst, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T,weighted", [(3, False), (2, True), (0, False)])
+def test_propagate_sharded_library_nccl(T, weighted):
+    """tpo_propagate_sharded with a libtpo-owned NCCL communicator (world 1 on one GPU: the
+    all-reduce / reduce-scatter / all-gather run through NCCL) equals the oracle's propagation."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_11922_b200 import build
+    build.build()
+    from paper_2405_11922_b200.sharded import GpuShardOps, NcclComm, propagate_sharded_lib
+    g = planted_abg(3001, 1005, 5, 64, deg=("zipf", 1.3, 300), p_in=0.6, pop=("zipf", 1.2), x=("gaussian", 1.0),
+                    seed=T + 11, weighted=weighted)
+    sh = shard_graph(g.n, g.m, g.B_rowptr, g.B_col, 0, 1, g.B_val)
+    ops = GpuShardOps(sh, "cuda:0", 64)
+    comm = NcclComm(0, 1, "cuda:0", NcclComm.unique_id())
+    try:
+        Z, Zh = propagate_sharded_lib(comm, ops, torch.from_numpy(g.X).cuda(), 0.5, T)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, 0.5, T, g.B_val)
+    assert np.linalg.norm(Z.cpu().numpy() - Zo) <= 1e-5 * np.linalg.norm(Zo)
+    assert np.linalg.norm(Zh.cpu().numpy() - Zho) <= 1e-5 * np.linalg.norm(Zho)
