@@ -261,8 +261,8 @@ def run_sharded(args, g, ws, rank, local, dev):
     import torch.distributed as dist
     import paper_2405_11922_b200 as T
     from paper_2405_11922_b200._lib import lib
-    from paper_2405_11922_b200.sharded import (GpuShardOps, GpuSolverOps, TorchCollectives, propagate_sharded,
-                                               shard_graph, solve_sharded)
+    from paper_2405_11922_b200.sharded import (GpuShardOps, GpuSolverOps, LibRunner, NcclComm, TorchCollectives,
+                                               propagate_sharded, shard_graph, solve_sharded)
     if ws == 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
@@ -275,7 +275,18 @@ def run_sharded(args, g, ws, rank, local, dev):
     L = lib()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    lib_run, comm = None, None
+    if args.comm == "lib" and args.exchange == "full":
+        # collectives inside libtpo (tpo_run_sharded on a library-owned NCCL communicator)
+        uid = [NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = NcclComm(rank, ws, dev, uid[0])
+        lib_run = LibRunner(comm, ops, g.d, g.k)
+        Gd = torch.from_numpy(np.ascontiguousarray(g.G, np.float64)).to(dev)
+
     def step():
+        if lib_run is not None:
+            return lib_run(Xp, g.alpha, g.T, Gd, args.tf, args.tg)
         Q = T.haar_q_dev(g.G, device=dev)
         _, Zh = propagate_sharded(ops, coll, Xp, g.alpha, g.T, exchange=args.exchange)
         lab, _ = solve_sharded(sops, coll, Zh, Q, sh.u0, args.tf, args.tg)
@@ -310,13 +321,57 @@ def run_sharded(args, g, ws, rank, local, dev):
     cfg = config_dict(g, args, ws)
     cfg["parallelism"] = (f"U-rows sharded over {ws} rank(s) ("
                           + ("NCCL RS/AG of the V block" if args.exchange == "full" else "NCCL all-to-all of touched V rows")
-                          + " per hop, all-reduced solver partials)")
+                          + " per hop, all-reduced solver partials; collectives "
+                          + ("inside libtpo: tpo_run_sharded" if lib_run is not None else "through torch.distributed") + ")")
+    # end to end: this rank's shard (X_p, CSR(B_p), CSR(B_p^T), G) copied in from pinned host memory
+    # and its labels copied out inside the timed region, every step
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hX = pin(g.X[sh.u0:sh.u1])
+        hB = [pin(sh.Bp_rowptr), pin(sh.Bp_col), pin(sh.Btp_rowptr), pin(sh.Btp_col)]
+        hG = pin(np.ascontiguousarray(g.G, np.float64))
+        dB = [ops.Bp[0], ops.Bp[1], ops.Btp[0], ops.Btp[1]]
+        Gd_e = torch.empty_like(hG, device=dev)
+        hlab = torch.empty(max(sh.n_p, 1), dtype=torch.int32).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in [hX, hG] + hB)
+        et = []
+        for it in range(max(2, args.steps // 2) + 1):
+            flush.zero_()
+            dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            Xp.copy_(hX, non_blocking=True)
+            for dsrc, ddst in zip(hB, dB):
+                ddst.copy_(dsrc, non_blocking=True)
+            Gd_e.copy_(hG, non_blocking=True)
+            if lib_run is not None:
+                lab = lib_run(Xp, g.alpha, g.T, Gd_e, args.tf, args.tg)
+            else:
+                lab = step()
+            hlab[: sh.n_p].copy_(lab[: sh.n_p], non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if it > 0:
+                et.append(e0.elapsed_time(e1))
+        t2 = torch.tensor([float(np.mean(et))], device=dev, dtype=torch.float64)
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t2.item())
+        e2e = {"value": units / (e2e_ms / 1e3), "unit": "nnz*d/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(sh.n_p * 4)}
     line = {"metric": metric_name(), "value": units * args.steps / (tot_ms / 1e3), "unit": "nnz*d/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic", "config": cfg,
-            "e2e": None, "gpu_launches": int(launches), "clocks": cs.summary(), "mode": "sharded"}
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": cs.summary(), "mode": "sharded",
+            "tpo_seconds": tot_ms / args.steps / 1e3}
+    if lib_run is not None:
+        line["stages_ms"] = dict(zip(["propagate", "features", "topk_eig", "cluster"],
+                                     [float(x) for x in lib_run.timings]))
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     dist.destroy_process_group()
 
 
@@ -330,6 +385,9 @@ def main():
     ap.add_argument("--tf", type=int, default=5)
     ap.add_argument("--tg", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", default="lib", choices=["lib", "torch"],
+                    help="sharded mode: collectives inside libtpo (tpo_run_sharded on its own NCCL communicator) or "
+                         "issued from Python through torch.distributed")
     ap.add_argument("--exchange", default="full", choices=["full", "touched"],
                     help="sharded mode: per-hop exchange of the whole V block (reduce-scatter + all-gather) or of "
                          "the touched V rows only (all-to-all, SURVEY.md §8f #2)")

@@ -157,6 +157,19 @@ int tpo_comm_destroy(void *comm);
 size_t tpo_propagate_sharded_ws(int64_t n_p, int64_t n_v, int64_t nnz_p, int64_t d, int32_t world);
 int tpo_propagate_sharded(void *comm, const tpo_csr_t *Bp, const tpo_csr_t *Btp, const float *Xp, int64_t d, float alpha,
                           int32_t T, float *Zp, float *Zhat_p, void *ws, size_t ws_bytes, void *stream);
+/* tpo_run_sharded: the whole hot path (as tpo_run) on the rank's U slice [row0, row0 + n_p) with every
+ * collective inside the library: the sharded propagation, then features, the exact top-k, ONMF and
+ * NCI with the fp64 partials all-reduced in between (r, the Gram, Gamma^T Gamma and the polish
+ * decision, the sign rule's column statistics and largest entries, R'^T Ups, Ups^T Ups, Ups^T RH,
+ * the cluster sums, counts and changed flag), so every rank's replicated factors are identical and
+ * its labels are the single-GPU path's.  G: d x d fp64 (device), the same on every rank.
+ * labels_p: n_p int32 out; iters_used: (host) Alg. 3 iterations or NULL; timings_ms: (host) 4
+ * stage times {propagate, features, topk, cluster} or NULL.  [sync]
+ * Workspace: tpo_run_sharded_ws(n_p, n_v, nnz_p, d, k, world). */
+size_t tpo_run_sharded_ws(int64_t n_p, int64_t n_v, int64_t nnz_p, int64_t d, int32_t k, int32_t world);
+int tpo_run_sharded(void *comm, const tpo_csr_t *Bp, const tpo_csr_t *Btp, const float *Xp, int64_t d, float alpha,
+                    int32_t T, int32_t k, const double *G, int64_t row0, int32_t Tf, int32_t Tg, int32_t *labels_p,
+                    int32_t *iters_used, double *timings_ms, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * a4  Haar rotation, Alg. 1 L6-7: Q = the Q factor of the QR
@@ -192,13 +205,23 @@ int tpo_features(const float *Zhat, int64_t n, int64_t d, const float *Q, float 
  * (R R^T approximates the MSA matrix S, Theorem 1); evaluated as
  * dinv . (R' (R'^T (dinv . Y))) so the n x n matrix is never formed.
  *   Rp: n x D fp32;  dinv: n fp32;  Y: n x b fp32;  out: n x b fp32 out (may not alias Y).
- *   The D x b intermediate R'^T (dinv . Y) is reduced across the GPU in fp64.
+ *   Both products run on the fp64 tensor path (DMMA); the D x b intermediate R'^T (dinv . Y) is
+ *   fp64 and reduced across the GPU in a fixed order.
  * Workspace: tpo_affinity_matvec_ws(n, D, b).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA.
  * --------------------------------------------------------------------------------------- */
 size_t tpo_affinity_matvec_ws(int64_t n, int64_t D, int64_t b);
 int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D,
                         const float *Y, int64_t b, float *out, void *ws, size_t ws_bytes,
                         void *stream);
+
+/* "R-free" a6: the same S~Y from Zhat and Q instead of R' -- R' rows are
+ * recomputed (tcgen05 features GEMM + sincos) in chunks of chunk_rows rows (<= 0: 262,144) in three
+ * sweeps (r, then W = R^T Y, then dinv . R'W), so only chunk_rows x 2d floats of R' ever exist.
+ *   Zhat: n x d fp32 (d % 4 == 0);  Q: d x d fp32;  Y, out: n x b fp32.
+ * Workspace: tpo_affinity_matvec_rfree_ws(n, d, b, chunk_rows).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA. */
+size_t tpo_affinity_matvec_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk_rows);
+int tpo_affinity_matvec_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *Y, int64_t b,
+                              float *out, int64_t chunk_rows, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * a7  Top-k singular triplets of R = diag(dinv) R' -- "the top-k left and right singular

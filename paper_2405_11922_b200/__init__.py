@@ -4,6 +4,6 @@ The product is libtpo.so (C-ABI in include/tpo.h, CUDA sources in csrc/); this p
 its thin Python binding.  There is no CPU fallback: importing the binding functions needs
 the built library (`python -m paper_2405_11922_b200.build`).
 """
-from .tpo import (DeviceGraph, HostRunner, Runner, affinity_matvec, cluster, evaluate, features, gram, haar_q,  # noqa: F401
+from .tpo import (DeviceGraph, HostRunner, Runner, affinity_matvec, affinity_matvec_rfree, cluster, evaluate, features, gram, haar_q,  # noqa: F401
                   haar_q_dev, objective, propagate, run, svd_reduce, to_device_graph, topk_eig)
 from ._lib import TPO_EIG_EXACT, TPO_EIG_HALKO, TpoError, lib  # noqa: F401

@@ -27,6 +27,7 @@ SYMBOLS = [
     "tpo_svd_reduce_ws", "tpo_svd_reduce", "tpo_eval_ws", "tpo_eval", "tpo_objective_ws", "tpo_objective",
     "tpo_rows_gather", "tpo_rows_scatter",
     "tpo_comm_unique_id", "tpo_comm_create", "tpo_comm_destroy", "tpo_propagate_sharded_ws", "tpo_propagate_sharded",
+    "tpo_affinity_matvec_rfree_ws", "tpo_affinity_matvec_rfree", "tpo_run_sharded_ws", "tpo_run_sharded",
 ]
 
 TPO_OK, TPO_EINVAL, TPO_ECUDA, TPO_ENOMEM, TPO_ENCCL, TPO_ENUMERIC = 0, -1, -2, -3, -4, -5
@@ -139,6 +140,14 @@ def lib():
     L.tpo_propagate_sharded_ws.restype = sz
     L.tpo_propagate_sharded.argtypes = [vp, P, P, vp, i64, f32, i32, vp, vp, vp, sz, vp]
     L.tpo_propagate_sharded.restype = C.c_int
+    L.tpo_affinity_matvec_rfree_ws.argtypes = [i64, i64, i64, i64]
+    L.tpo_affinity_matvec_rfree_ws.restype = sz
+    L.tpo_affinity_matvec_rfree.argtypes = [vp, i64, i64, vp, vp, i64, vp, i64, vp, sz, vp]
+    L.tpo_affinity_matvec_rfree.restype = C.c_int
+    L.tpo_run_sharded_ws.argtypes = [i64, i64, i64, i64, i32, i32]
+    L.tpo_run_sharded_ws.restype = sz
+    L.tpo_run_sharded.argtypes = [vp, P, P, vp, i64, f32, i32, i32, vp, i64, i32, i32, vp, vp, vp, vp, sz, vp]
+    L.tpo_run_sharded.restype = C.c_int
     for name in ["tpo_shard_features", "tpo_shard_dinv", "tpo_eig_from_gram", "tpo_shard_gamma", "tpo_shard_atb64",
                  "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final", "tpo_shard_onmf_init",
                  "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh", "tpo_shard_onmf_u_update",

@@ -13,9 +13,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <math.h>
+
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "tpo_internal.cuh"
 
@@ -151,6 +154,191 @@ void propagate_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Bt
         shard_uside_impl(Bp, Q, Xp, d, alpha, s_u, last, Zp, last ? Zhat_p : nullptr, ar, st);
         ar.off = mark;
     }
+}
+
+// ---------------------------------------------------------------------------------------
+// The whole hot path on a rank's U slice with every collective inside the library (SURVEY.md
+// §8e "an all-reduce of the d x k Gram matrices"): sharded propagation, then a5-a9 with the fp64
+// partials all-reduced in between -- r, the Gram R^T R, Gamma^T Gamma for the CholeskyQR polish
+// (and its decision), the sign rule's column statistics (all-reduce) and largest-magnitude entries
+// (all-gather; R8 applied identically on every rank), R'^T Ups, Ups^T Ups, Ups^T (R H) per Alg. 2
+// iteration, and the cluster sums, counts and changed flag per Alg. 3 iteration.  Every D x D,
+// D x k and k x k quantity is replicated, so each rank's steps are the single-GPU ones.
+// ---------------------------------------------------------------------------------------
+namespace {
+__global__ void eye_f64_kernel(double *P, int k) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k * k) P[i] = (i / k == i % k) ? 1.0 : 0.0;
+}
+__global__ void fill_i32_kernel(int32_t *p, int64_t n, int32_t v) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+}  // namespace
+
+size_t run_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, int32_t k, int world) {
+    const int64_t D = 2 * d;
+    size_t s = propagate_sharded_ws_bytes(n_p, m, nnz_p, d, world);
+    s += 2 * align_up(sizeof(float) * (size_t)n_p * d) + align_up(sizeof(float) * (size_t)d * d);
+    s += align_up(sizeof(float) * (size_t)n_p * D) + align_up(sizeof(float) * (size_t)n_p + 1) + align_up(sizeof(double) * D);
+    s += align_up(sizeof(double) * (size_t)D * D) + 3 * align_up(sizeof(double) * (size_t)D * k) + align_up(sizeof(float) * D * k);
+    s += 3 * align_up(sizeof(double) * (size_t)n_p * k) + align_up(sizeof(float) * (size_t)n_p * k);
+    s += 8 * align_up(sizeof(double) * (size_t)k * k) + 8 * align_up(sizeof(double) * (size_t)k) + 1024;
+    size_t inner = std::max(features_ws_bytes(n_p, d), gram_tc_ws(std::max<int64_t>(n_p, 1), D));
+    inner = std::max(inner, eig_from_gram_ws(D, k));
+    inner = std::max(inner, haar_q_ws_bytes(d));
+    inner = std::max(inner, nci_assign_part_ws(n_p, k));
+    inner = std::max(inner, onmf_ws_bytes(n_p, D, k));
+    inner = std::max(inner, ts_atb_ws(k, k) + dgemm_ws(k, k, std::max<int64_t>(n_p, 1)));
+    inner = std::max(inner, align_up(sizeof(double) * (size_t)(4 * 2 * 148 * k)) + 4096);
+    return s + inner + 64 * 256;
+}
+
+void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, const float *Xp, int64_t d, float alpha,
+                      int32_t T, int32_t k, const double *Gdev, int64_t row0, int32_t Tf, int32_t Tg, int32_t *labels_p,
+                      int32_t *iters_used, double *timings_ms, Arena &ar, cudaStream_t st) {
+    Comm *c = static_cast<Comm *>(comm);
+    const NcclApi &api = nccl();
+    const int64_t n_p = Bp.n_rows, D = 2 * d;
+    const int world = c->world;
+    cudaEvent_t ev[5];
+    for (auto &e : ev) TPO_CUDA(cudaEventCreate(&e));
+    auto allreduce = [&](double *p, size_t len) { TPO_NCCL(api.AllReduce(p, p, len, ncclFloat64, ncclSum, c->nc, st)); };
+    float *Zp = ar.take<float>(n_p * d), *Zh = ar.take<float>(n_p * d), *Q = ar.take<float>(d * d);
+    float *Rp = ar.take<float>(n_p * D), *dinv = ar.take<float>(n_p + 1);
+    double *r = ar.take<double>(D), *Gd = ar.take<double>(D * D), *Psi64 = ar.take<double>(D * k);
+    double *RtU = ar.take<double>(D * k), *H = ar.take<double>(D * k);
+    float *Psi = ar.take<float>(D * k);
+    double *G64 = ar.take<double>(n_p * k), *U = ar.take<double>(n_p * k), *RH = ar.take<double>(n_p * k);
+    float *Gam = ar.take<float>(n_p * k);
+    double *g = ar.take<double>(k * k), *UtU = ar.take<double>(k * k), *M = ar.take<double>(k * k),
+           *Phi = ar.take<double>(k * k), *sums = ar.take<double>(k * k);
+    double *cs = ar.take<double>(k), *ca = ar.take<double>(k), *cmax = ar.take<double>(k), *counts = ar.take<double>(k);
+    int64_t *carg = ar.take<int64_t>(k);
+    double *vals_all = ar.take<double>((size_t)world * k);
+    int64_t *idx_all = ar.take<int64_t>((size_t)world * k);
+    int32_t *changed = ar.take<int32_t>(2);
+    const size_t mark = ar.off;
+    auto atb = [&](const double *A, const double *B, double *out) {
+        if (n_p == 0) { TPO_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * k * k, st)); return; }
+        if (ts64_enabled() && k <= 104) ts_atb_f64(A, k, B, k, n_p, k, k, out, ar, st);
+        else dgemm(true, k, k, n_p, 1.0, A, k, B, k, 0.0, out, k, ar, st);
+        ar.off = mark;
+    };
+    TPO_CUDA(cudaEventRecord(ev[0], st));
+    // a1-a3
+    propagate_sharded_impl(comm, Bp, Btp, Xp, d, alpha, T, Zp, Zh, ar, st);
+    ar.off = mark;
+    TPO_CUDA(cudaEventRecord(ev[1], st));
+    // a4-a5: Q replicated from G; R'_p, r (all-reduce), dinv_p
+    haar_q_device(Gdev, true, d, Q, ar, st);
+    ar.off = mark;
+    features_part(Zh, n_p, d, Q, Rp, r, ar, st);
+    ar.off = mark;
+    allreduce(r, (size_t)D);
+    if (n_p > 0) dinv_from_r(Rp, n_p, D, r, dinv, st);
+    TPO_CUDA(cudaEventRecord(ev[2], st));
+    // a7: Gram (all-reduce), replicated eigensolve, Gamma rows, polish, sign rule
+    if (n_p > 0) gram_tc(Rp, dinv, n_p, D, Gd, ar, st);
+    else TPO_CUDA(cudaMemsetAsync(Gd, 0, sizeof(double) * D * D, st));
+    ar.off = mark;
+    allreduce(Gd, (size_t)(D * D));
+    std::vector<double> sigma(k);
+    eig_from_gram(Gd, r, D, k, Psi64, sigma.data(), ar, st);
+    ar.off = mark;
+    gamma_rows(Rp, dinv, n_p, D, k, Psi64, sigma.data(), G64, ar, st);
+    ar.off = mark;
+    std::vector<double> gh((size_t)k * k);
+    for (int p = 0; p < 3; ++p) {                         // CholeskyQR polish while ||G^T G - I|| > 1e-6
+        atb(G64, G64, g);
+        allreduce(g, (size_t)k * k);
+        TPO_CUDA(cudaMemcpyAsync(gh.data(), g, sizeof(double) * k * k, cudaMemcpyDeviceToHost, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        double dev = 0.0;
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < k; ++j) dev = std::max(dev, fabs(gh[(size_t)i * k + j] - (i == j ? 1.0 : 0.0)));
+        if (dev <= 1e-6 || p == 2) break;
+        apply_chol(G64, n_p, k, g, ar, st);
+        ar.off = mark;
+    }
+    colstats_rows(G64, n_p, k, row0, cs, ca, cmax, carg, ar, st);
+    ar.off = mark;
+    allreduce(cs, (size_t)k);
+    allreduce(ca, (size_t)k);
+    TPO_NCCL(api.AllGather(cmax, vals_all, (size_t)k, ncclFloat64, c->nc, st));
+    TPO_NCCL(api.AllGather(carg, idx_all, (size_t)k, ncclInt64, c->nc, st));
+    std::vector<double> hs(k), ha(k), hv((size_t)world * k);
+    std::vector<int64_t> hi((size_t)world * k);
+    TPO_CUDA(cudaMemcpyAsync(hs.data(), cs, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(ha.data(), ca, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(hv.data(), vals_all, sizeof(double) * world * k, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(hi.data(), idx_all, sizeof(int64_t) * world * k, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> signs(k, 1);                          // R8 from the global statistics
+    for (int l = 0; l < k; ++l) {
+        if (fabs(hs[l]) < 1e-6 * ha[l]) {
+            double best = -1.0, bv = 0.0;
+            int64_t bi = INT64_MAX;
+            for (int q = 0; q < world; ++q) {
+                const double mv = fabs(hv[(size_t)q * k + l]);
+                const int64_t iv = hi[(size_t)q * k + l];
+                if (mv > best || (mv == best && iv < bi)) { best = mv; bi = iv; bv = hv[(size_t)q * k + l]; }
+            }
+            signs[l] = bv < 0.0 ? -1 : 1;
+        } else {
+            signs[l] = hs[l] < 0.0 ? -1 : 1;
+        }
+    }
+    gamma_final(G64, n_p, k, signs.data(), Psi, Psi64, D, Gam, ar, st);
+    ar.off = mark;
+    TPO_CUDA(cudaEventRecord(ev[3], st));
+    // a8 (Alg. 2)
+    onmf_init(Gam, n_p, Psi, sigma.data(), D, k, U, H, ar, st);
+    ar.off = mark;
+    for (int t = 0; t < Tf; ++t) {
+        if (n_p > 0) onmf_rtu(Rp, n_p, D, dinv, U, k, RtU, ar, st);
+        else TPO_CUDA(cudaMemsetAsync(RtU, 0, sizeof(double) * D * k, st));
+        ar.off = mark;
+        allreduce(RtU, (size_t)(D * k));
+        atb(U, U, UtU);
+        allreduce(UtU, (size_t)k * k);
+        onmf_h_update(H, RtU, UtU, D, k, ar, st);
+        ar.off = mark;
+        if (n_p > 0) tsgemm_AW_f64(Rp, D, dinv, H, n_p, D, k, RH, k, st);
+        atb(U, RH, M);
+        allreduce(M, (size_t)k * k);
+        onmf_u_update(U, RH, M, n_p, k, st);
+    }
+    // a9 (Alg. 3)
+    eye_f64_kernel<<<cdiv((int64_t)k * k, 256), 256, 0, st>>>(Phi, k);
+    TPO_LAUNCH_CHECK();
+    if (n_p > 0) fill_i32_kernel<<<cdiv(n_p, 256), 256, 0, st>>>(labels_p, n_p, -1);
+    TPO_LAUNCH_CHECK();
+    int32_t iters = 0;
+    for (int t = 0; t < Tg; ++t) {
+        TPO_CUDA(cudaMemsetAsync(changed, 0, sizeof(int32_t), st));
+        nci_assign_part(U, Phi, n_p, k, labels_p, changed, sums, counts, ar, st);
+        ar.off = mark;
+        TPO_NCCL(api.AllReduce(changed, changed, 1, ncclInt32, ncclSum, c->nc, st));
+        int32_t ch = 0;
+        TPO_CUDA(cudaMemcpyAsync(&ch, changed, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        ++iters;
+        if (ch == 0 || t == Tg - 1) break;
+        allreduce(sums, (size_t)k * k);
+        allreduce(counts, (size_t)k);
+        nci_phi(sums, counts, k, Phi, st);
+    }
+    TPO_CUDA(cudaEventRecord(ev[4], st));
+    TPO_CUDA(cudaEventSynchronize(ev[4]));
+    if (iters_used) *iters_used = iters;
+    if (timings_ms)
+        for (int i = 0; i < 4; ++i) {
+            float ms = 0.f;
+            TPO_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            timings_ms[i] = ms;
+        }
+    for (auto &e : ev) cudaEventDestroy(e);
 }
 
 }  // namespace tpo

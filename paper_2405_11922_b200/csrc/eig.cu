@@ -822,6 +822,10 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
 // a6: out = dinv . R' (R'^T (dinv . Y)), the D x b intermediate summed in fp64.
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b,
                           float *out, Arena &ar, cudaStream_t st) {
+    if (ts64_enabled() && D % 4 == 0) {                  // fp64 tensor path (DMMA)
+        ts_affinity(Rp, dinv, n, D, Y, b, out, ar, st);
+        return;
+    }
     double *W = ar.take<double>(D * b);
     tsgemm_AtB_f32f32(Rp, D, dinv, Y, b, nullptr, n, D, b, W, ar, st);
     tsgemm_AW_f32(Rp, D, dinv, W, n, D, b, out, b, st);

@@ -226,7 +226,7 @@ int tpo_features(const float *Zhat, int64_t n, int64_t d, const float *Q, float 
 }
 
 size_t tpo_affinity_matvec_ws(int64_t n, int64_t D, int64_t b) {
-    return align_up(sizeof(double) * D * b) + tsgemm_ws(n, D, b) + 1024;
+    return std::max(align_up(sizeof(double) * D * b) + tsgemm_ws(n, D, b), ts_affinity_ws(D, b)) + 1024;
 }
 
 int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b,
@@ -245,6 +245,25 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
 }
 
 // undocumented debugging hook (not part of include/tpo.h)
+
+size_t tpo_affinity_matvec_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk_rows) {
+    return ts_affinity_rfree_ws(n, d, b, chunk_rows > 0 ? chunk_rows : (int64_t)1 << 18);
+}
+
+int tpo_affinity_matvec_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *Y, int64_t b,
+                              float *out, int64_t chunk_rows, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && d >= 4 && d % 4 == 0 && b >= 1, "need n >= 1, d a positive multiple of 4, b >= 1");
+        check_ptr(Zhat, "Zhat");
+        check_ptr(Q, "Q");
+        check_ptr(Y, "Y", false);
+        check_ptr(out, "out", false);
+        const int64_t chunk = chunk_rows > 0 ? chunk_rows : (int64_t)1 << 18;
+        check_ws(ws, ws_bytes, tpo_affinity_matvec_rfree_ws(n, d, b, chunk));
+        Arena ar(ws, ws_bytes);
+        ts_affinity_rfree(Zhat, n, d, Q, Y, b, out, chunk, ar, as_stream(stream));
+    });
+}
 
 size_t tpo_gram_ws(int64_t n, int64_t D) { return gram_tc_ws(n, D) + 1024; }
 
@@ -356,6 +375,37 @@ int tpo_propagate_sharded(void *comm, const tpo_csr_t *Bp, const tpo_csr_t *Btp,
         check_ws(ws, ws_bytes, tpo_propagate_sharded_ws(Bp->n_rows, Bp->n_cols, Bp->nnz, d, comm_world(comm)));
         Arena ar(ws, ws_bytes);
         propagate_sharded_impl(comm, *Bp, *Btp, Xp, d, alpha, T, Zp, Zhat_p, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_run_sharded_ws(int64_t n_p, int64_t n_v, int64_t nnz_p, int64_t d, int32_t k, int32_t world) {
+    return run_sharded_ws_bytes(n_p, n_v, nnz_p, d, k, std::max<int32_t>(world, 1));
+}
+
+int tpo_run_sharded(void *comm, const tpo_csr_t *Bp, const tpo_csr_t *Btp, const float *Xp, int64_t d, float alpha,
+                    int32_t T, int32_t k, const double *G, int64_t row0, int32_t Tf, int32_t Tg, int32_t *labels_p,
+                    int32_t *iters_used, double *timings_ms, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(comm != nullptr, "comm is NULL");
+        check_csr(Bp, "Bp");
+        check_csr(Btp, "Btp");
+        TPO_REQUIRE(Bp->n_rows == Btp->n_cols && Bp->n_cols == Btp->n_rows && Bp->nnz == Btp->nnz,
+                    "Btp is not shaped as the transpose of Bp");
+        TPO_REQUIRE(d >= 4 && d % 4 == 0, "d must be a positive multiple of 4");
+        TPO_REQUIRE(alpha >= 0.0f && alpha <= 1.0f, "alpha must lie in [0, 1]");
+        TPO_REQUIRE(T >= 0 && Tf >= 0 && Tg >= 1 && row0 >= 0, "T, Tf >= 0, Tg >= 1, row0 >= 0");
+        TPO_REQUIRE(k >= 1 && k <= 2 * d && k <= 128, "need 1 <= k <= min(2d, 128)");
+        check_gather_range(Btp->n_cols, d, "Pp (gathered by the V-side SpMM)");
+        check_gather_range(Bp->n_cols, d, "Q (gathered by the U-side SpMM)");
+        check_ptr(G, "G");
+        if (Bp->n_rows) {
+            check_ptr(Xp, "Xp");
+            TPO_REQUIRE(labels_p != nullptr, "labels_p is NULL");
+        }
+        check_ws(ws, ws_bytes, tpo_run_sharded_ws(Bp->n_rows, Bp->n_cols, Bp->nnz, d, k, comm_world(comm)));
+        Arena ar(ws, ws_bytes);
+        run_sharded_impl(comm, *Bp, *Btp, Xp, d, alpha, T, k, G, row0, Tf, Tg, labels_p, iters_used, timings_ms, ar,
+                         as_stream(stream));
     });
 }
 

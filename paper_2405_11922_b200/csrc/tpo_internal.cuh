@@ -106,6 +106,10 @@ int comm_rank(const void *comm);
 size_t propagate_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, int world);
 void propagate_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, const float *Xp, int64_t d,
                             float alpha, int32_t T, float *Zp, float *Zhat_p, Arena &ar, cudaStream_t st);
+size_t run_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, int32_t k, int world);
+void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, const float *Xp, int64_t d, float alpha,
+                      int32_t T, int32_t k, const double *Gdev, int64_t row0, int32_t Tf, int32_t Tg, int32_t *labels_p,
+                      int32_t *iters_used, double *timings_ms, Arena &ar, cudaStream_t st);
 void shard_degrees_impl(const tpo_csr_t &Bp, const tpo_csr_t &Btp, double *deg_u, double *deg_v, cudaStream_t st);
 void shard_start_impl(const double *deg_u, const double *deg_v, int64_t n_p, int64_t m, const float *Xp, int64_t d,
                       float alpha, float *s_u, float *s_v, float *Pp, cudaStream_t st);
@@ -122,6 +126,7 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
                    int32_t p, int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi,
                    Arena &ar, cudaStream_t st, const double *r_colsum = nullptr);
 void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cudaStream_t st);
+size_t features_ws_bytes(int64_t n, int64_t d);
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
                   int32_t *iters_used, Arena &ar, cudaStream_t st);
@@ -222,6 +227,12 @@ void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, in
                const double *cs, double *out, int64_t ldo, cudaStream_t st);
 void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);
 size_t ts_rtu_ws(int64_t n, int64_t D, int k);
+size_t ts_affinity_ws(int64_t D, int64_t b);
+size_t ts_affinity_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk);
+void ts_affinity_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *Y, int64_t b, float *out,
+                       int64_t chunk, Arena &ar, cudaStream_t st);
+void ts_affinity(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b, float *out,
+                 Arena &ar, cudaStream_t st);
 void ts_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
             cudaStream_t st);
 

@@ -37,6 +37,7 @@ struct DmArgs {
     int64_t n;
     int K, N;
     double *out;          // STORE: n x N (ldo); UPS: Ups itself (= A, updated in place)
+    float *out32;         // STORE: when set, the product is written as fp32 here instead of out
     int64_t ldo;
     const double *cs;     // STORE: column divisors (sigma) or null
     const double *RH;     // UPS: n x N
@@ -259,7 +260,8 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
                         if (EPI == DM_STORE) {
                             double v = rsv * acc[mt][nt][h];
                             if (a.cs) v = v / a.cs[col];
-                            a.out[row * a.ldo + col] = v;
+                            if (a.out32) a.out32[row * a.ldo + col] = (float)v;
+                            else a.out[row * a.ldo + col] = v;
                         } else {
                             const double rh = a.RH[row * a.N + col];
                             const double num = rh > 0.0 ? rh : 0.0;
@@ -423,15 +425,18 @@ constexpr size_t rt_smem() {
     return 2 * ((size_t)RT_BK * RT_LDR * sizeof(float) + (size_t)RT_BK * 8 * NT * sizeof(double) + RT_BK * sizeof(float));
 }
 
-template <int NT>
+// TU: the right factor's type (fp64 Ups in Alg. 2; fp32 Y in the a6 product), staged as is and
+// widened at the fragment load
+template <int NT, class TU>
 __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restrict__ Rp, int64_t n, int D,
-                                                          const float *__restrict__ dinv, const double *__restrict__ U,
+                                                          const float *__restrict__ dinv, const TU *__restrict__ U,
                                                           int k, int64_t rows_per, double *__restrict__ part) {
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int NBW = 8 * NT;
     float *Rs = reinterpret_cast<float *>(dsm);                                         // [2][RT_BK][RT_LDR]
-    double *Us = reinterpret_cast<double *>(dsm + 2 * (size_t)RT_BK * RT_LDR * sizeof(float));   // [2][RT_BK][NBW]
-    float *Ds = reinterpret_cast<float *>(Us + 2 * RT_BK * NBW);                       // [2][RT_BK]
+    TU *Us = reinterpret_cast<TU *>(dsm + 2 * (size_t)RT_BK * RT_LDR * sizeof(float));   // [2][RT_BK][NBW]
+    float *Ds = reinterpret_cast<float *>(dsm + 2 * (size_t)RT_BK * RT_LDR * sizeof(float) +
+                                          2 * (size_t)RT_BK * NBW * sizeof(double));    // [2][RT_BK]
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gr = lane >> 2, gc = lane & 3;
     const int col0 = blockIdx.y * NBW, d0 = blockIdx.z * RT_DB;
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restric
     const bool r16 = (D % 4) == 0 && ((reinterpret_cast<uintptr_t>(Rp) & 15u) == 0);
     auto load = [&](int64_t b, int buf) {
         float *rs = Rs + (size_t)buf * RT_BK * RT_LDR;
-        double *us = Us + (size_t)buf * RT_BK * NBW;
+        TU *us = Us + (size_t)buf * RT_BK * NBW;
         float *ds = Ds + buf * RT_BK;
         if (r16) {
 #pragma unroll
@@ -462,7 +467,8 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restric
             const int r = idx / NBW, c = idx - (idx / NBW) * NBW;
             const int64_t row = b + r;
             const bool v = row < i1 && col0 + c < k;
-            cp8(us + idx, v ? (const void *)(U + row * k + col0 + c) : (const void *)U, v);
+            if (sizeof(TU) == 8) cp8(us + idx, v ? (const void *)(U + row * k + col0 + c) : (const void *)U, v);
+            else cp4(us + idx, v ? (const void *)(U + row * k + col0 + c) : (const void *)U, v);
         }
         if (tid < RT_BK) cp4(ds + tid, (b + tid < i1) ? (const void *)(dinv + b + tid) : (const void *)dinv, b + tid < i1);
         cp_commit();
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restric
             const bool more = b + RT_BK < i1;
             if (more) load(b + RT_BK, buf ^ 1);
             const float *rs = Rs + (size_t)buf * RT_BK * RT_LDR + gc * RT_LDR + w * 32 + gr;
-            const double *us = Us + (size_t)buf * RT_BK * NBW + gc * NBW + gr;
+            const TU *us = Us + (size_t)buf * RT_BK * NBW + gc * NBW + gr;
             const float *ds = Ds + buf * RT_BK + gc;
 #pragma unroll
             for (int k4 = 0; k4 < RT_BK / 4; ++k4) {
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rtu_kernel(const float *__restric
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) af[mt] = (double)rs[k4 * 4 * RT_LDR + mt * 8];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) bf[nt] = dv * us[k4 * 4 * NBW + nt * 8];
+                for (int nt = 0; nt < NT; ++nt) bf[nt] = dv * (double)us[k4 * 4 * NBW + nt * 8];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -780,14 +786,20 @@ bool rowk_ups_ok(const double *U, const double *RH, int k) {
     return rowk_ok(U, k) && (reinterpret_cast<uintptr_t>(RH) & 15u) == 0;
 }
 
-template <int NT>
-void dm_rtu_launch(const float *Rp, int64_t n, int D, const float *dinv, const double *U, int k, int64_t rows_per,
-                   int G, int nblk, double *part, cudaStream_t st) {
+template <int NT, class TU>
+void dm_rtu_launch_t(const float *Rp, int64_t n, int D, const float *dinv, const TU *U, int k, int64_t rows_per, int G,
+                     int nblk, double *part, cudaStream_t st) {
     const size_t sm = rt_smem<NT>();
-    TPO_CUDA(cudaFuncSetAttribute(dm_rtu_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dm_rtu_kernel<NT><<<dim3((unsigned)G, (unsigned)nblk, (unsigned)cdiv(D, RT_DB)), DM_NT, sm, st>>>(Rp, n, D, dinv, U, k,
-                                                                                                   rows_per, part);
+    TPO_CUDA(cudaFuncSetAttribute(dm_rtu_kernel<NT, TU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dm_rtu_kernel<NT, TU><<<dim3((unsigned)G, (unsigned)nblk, (unsigned)cdiv(D, RT_DB)), DM_NT, sm, st>>>(Rp, n, D, dinv,
+                                                                                                       U, k, rows_per, part);
     TPO_LAUNCH_CHECK();
+}
+template <int NT>
+void dm_rtu_launch(const float *Rp, int64_t n, int D, const float *dinv, const double *U, const float *U32, int k,
+                   int64_t rows_per, int G, int nblk, double *part, cudaStream_t st) {
+    if (U32) dm_rtu_launch_t<NT, float>(Rp, n, D, dinv, U32, k, rows_per, G, nblk, part, st);
+    else dm_rtu_launch_t<NT, double>(Rp, n, D, dinv, U, k, rows_per, G, nblk, part, st);
 }
 
 }  // namespace
@@ -894,9 +906,9 @@ size_t ts_rtu_ws(int64_t n, int64_t D, int k) {
     return align_up(sizeof(double) * (size_t)sm_count_cached() * D * k) + 256;   // >= G * D * k
 }
 
-// RtU = R'^T (dinv . Ups) (D x k fp64)
-void ts_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
-            cudaStream_t st) {
+namespace {
+void rtu_run(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, const float *U32, int k,
+             double *RtU, Arena &ar, cudaStream_t st) {
     int NT, nblk;
     col_tiling(k, NT, nblk);
     const int nz = (int)cdiv(D, RT_DB);
@@ -905,10 +917,95 @@ void ts_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const doub
     const int G = (int)cdiv(std::max<int64_t>(n, 1), rows_per);
     const size_t mark = ar.off;
     double *part = ar.take<double>((size_t)G * D * k);
-    TPO_NT13(dm_rtu_launch, NT, Rp, n, (int)D, dinv, U, k, rows_per, G, nblk, part, st);
+    TPO_NT13(dm_rtu_launch, NT, Rp, n, (int)D, dinv, U, U32, k, rows_per, G, nblk, part, st);
     reduce_parts_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(part, G, D * k, RtU);
     TPO_LAUNCH_CHECK();
     ar.off = mark;
+}
+}  // namespace
+
+// RtU = R'^T (dinv . Ups) (D x k fp64)
+void ts_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
+            cudaStream_t st) {
+    rtu_run(Rp, n, D, dinv, U, nullptr, k, RtU, ar, st);
+}
+
+// a6 on the fp64 tensor path (Theorem 1, bracketing 564): W = R'^T (dinv . Y)
+// (D x b, fp64), out = dinv . (R' W) rounded to fp32
+size_t ts_affinity_ws(int64_t D, int64_t b) {
+    return align_up(sizeof(double) * (size_t)D * b) + ts_rtu_ws(0, D, (int)b) + 256;
+}
+void ts_affinity(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b, float *out,
+                 Arena &ar, cudaStream_t st) {
+    double *W = ar.take<double>((size_t)D * b);
+    rtu_run(Rp, n, D, dinv, nullptr, Y, (int)b, W, ar, st);
+    if (n == 0) return;
+    DmArgs a{};
+    a.A = Rp; a.lda = D; a.rs = dinv; a.W = W; a.ldw = b; a.n = n; a.K = (int)D; a.N = (int)b; a.out32 = out; a.ldo = b;
+    int NT, nblk;
+    col_tiling((int)b, NT, nblk);
+    TPO_NT13(dm_store_f32, NT, a, nblk, st);
+}
+
+namespace {
+__global__ void add_f64_kernel(double *__restrict__ acc, const double *__restrict__ x, int64_t len) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < len) acc[i] += x[i];
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// f3 "R-free" a6: S~Y without materialising R' for all n rows.  R' rows are
+// recomputed from Zhat (Eq. R-prime: tcgen05 3xTF32 GEMM + sincos) in chunks of
+// `chunk` rows in each of three sweeps -- r = sum_i R'[i]; W = sum_chunks R'_c^T (dinv_c . Y_c);
+// out_c = dinv_c . (R'_c W) -- so the working set is chunk x 2d floats instead of n x 2d (10 GB at
+// xl).  The chunk sums of r and W are added in chunk order (deterministic).  The cost is three
+// feature evaluations per application (an O(n d^2) GEMM + 2nd sincos each) for half the bytes.
+// ---------------------------------------------------------------------------------------
+size_t ts_affinity_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk) {
+    const int64_t D = 2 * d, C = std::max<int64_t>(1, std::min(n, chunk));
+    return align_up(sizeof(float) * (size_t)C * D) + align_up(sizeof(float) * (size_t)C) + 3 * align_up(sizeof(double) * D) +
+           2 * align_up(sizeof(double) * (size_t)D * b) + std::max(features_ws_bytes(C, d), ts_rtu_ws(0, D, (int)b)) + 4096;
+}
+
+void ts_affinity_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *Y, int64_t b, float *out,
+                       int64_t chunk, Arena &ar, cudaStream_t st) {
+    const int64_t D = 2 * d, C = std::max<int64_t>(1, std::min(n, chunk));
+    float *Rc = ar.take<float>((size_t)C * D), *dc = ar.take<float>((size_t)C);
+    double *r = ar.take<double>(D), *rp = ar.take<double>(D);
+    double *W = ar.take<double>((size_t)D * b), *Wc = ar.take<double>((size_t)D * b);
+    const size_t mark = ar.off;
+    TPO_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * D, st));
+    TPO_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * D * b, st));
+    for (int64_t c0 = 0; c0 < n; c0 += C) {                // sweep 1: r
+        const int64_t nc = std::min(C, n - c0);
+        features_part(Zhat + c0 * d, nc, d, Q, Rc, rp, ar, st);
+        ar.off = mark;
+        add_f64_kernel<<<cdiv(D, 256), 256, 0, st>>>(r, rp, D);
+        TPO_LAUNCH_CHECK();
+    }
+    for (int64_t c0 = 0; c0 < n; c0 += C) {                // sweep 2: W = R^T Y
+        const int64_t nc = std::min(C, n - c0);
+        features_part(Zhat + c0 * d, nc, d, Q, Rc, rp, ar, st);
+        ar.off = mark;
+        dinv_from_r(Rc, nc, D, r, dc, st);
+        rtu_run(Rc, nc, D, dc, nullptr, Y + c0 * b, (int)b, Wc, ar, st);
+        ar.off = mark;
+        add_f64_kernel<<<cdiv(D * b, 256), 256, 0, st>>>(W, Wc, D * b);
+        TPO_LAUNCH_CHECK();
+    }
+    for (int64_t c0 = 0; c0 < n; c0 += C) {                // sweep 3: out = R W
+        const int64_t nc = std::min(C, n - c0);
+        features_part(Zhat + c0 * d, nc, d, Q, Rc, rp, ar, st);
+        ar.off = mark;
+        dinv_from_r(Rc, nc, D, r, dc, st);
+        DmArgs a{};
+        a.A = Rc; a.lda = D; a.rs = dc; a.W = W; a.ldw = b; a.n = nc; a.K = (int)D; a.N = (int)b;
+        a.out32 = out + c0 * b; a.ldo = b;
+        int NT, nblk;
+        col_tiling((int)b, NT, nblk);
+        TPO_NT13(dm_store_f32, NT, a, nblk, st);
+    }
 }
 
 }  // namespace tpo

@@ -367,6 +367,34 @@ def propagate_sharded_lib(comm: NcclComm, ops: "GpuShardOps", Xp: torch.Tensor, 
     return Z, Zh
 
 
+class LibRunner:
+    """The whole hot path on this rank's U slice with the collectives inside libtpo
+    (tpo_run_sharded on a NcclComm).  Workspace and label buffers are kept across calls."""
+
+    def __init__(self, comm: NcclComm, ops: "GpuShardOps", d: int, k: int):
+        self.comm, self.ops, self.d, self.k = comm, ops, d, k
+        s = ops.s
+        L = lib()
+        self.ws = torch.empty(max(int(L.tpo_run_sharded_ws(s.n_p, s.m, s.nnz, d, k, comm.world)), 256), dtype=torch.uint8,
+                              device=ops.device)
+        self.labels = torch.empty(max(s.n_p, 1), dtype=torch.int32, device=ops.device)
+        self.timings = np.zeros(4, np.float64)
+        self.iters = 0
+
+    def __call__(self, Xp: torch.Tensor, alpha: float, T: int, Gdev: torch.Tensor, Tf: int = 5, Tg: int = 20,
+                 stream=None):
+        s = self.ops.s
+        B, Bt = self.ops._csr("B"), self.ops._csr("Bt")
+        it = C.c_int32(0)
+        st = C.c_void_p((stream or torch.cuda.current_stream(self.ops.device)).cuda_stream)
+        check(lib().tpo_run_sharded(self.comm.h, C.byref(B), C.byref(Bt), self.ops._p(Xp), self.d, float(alpha), int(T),
+                                    int(self.k), self.ops._p(Gdev), int(s.u0), int(Tf), int(Tg),
+                                    self.ops._p(self.labels), C.byref(it), self.timings.ctypes.data_as(C.c_void_p),
+                                    self.ops._p(self.ws), self.ws.numel(), st))
+        self.iters = int(it.value)
+        return self.labels[: s.n_p]
+
+
 # ------------------------------------------------------------------------------------------
 # a5-a9 on row shards (SURVEY.md §8e: "an all-reduce of the d x k Gram matrices"): every
 # D x D, D x k and k x k quantity is the all-reduced sum of the shards' partials, so each rank

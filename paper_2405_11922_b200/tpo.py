@@ -154,6 +154,22 @@ def affinity_matvec(Rp: torch.Tensor, dinv: torch.Tensor, Y: torch.Tensor, out=N
     return out
 
 
+def affinity_matvec_rfree(Zhat: torch.Tensor, Q: torch.Tensor, Y: torch.Tensor, chunk_rows: int = 0, out=None,
+                          stream=None):
+    """a6 without materialising R' (tpo_affinity_matvec_rfree): R' rows recomputed from Zhat in chunks."""
+    n, d = Zhat.shape
+    _need(Zhat, torch.float32, "Zhat")
+    _need(Q, torch.float32, "Q", (d, d))
+    _need(Y, torch.float32, "Y")
+    b = Y.shape[1]
+    out = torch.empty_like(Y) if out is None else out
+    L = lib()
+    ws = _ws(L.tpo_affinity_matvec_rfree_ws(n, d, b, int(chunk_rows)), Zhat.device)
+    check(L.tpo_affinity_matvec_rfree(_ptr(Zhat), n, d, _ptr(Q), _ptr(Y), b, _ptr(out), int(chunk_rows), _ptr(ws),
+                                      ws.numel(), _stream(stream)))
+    return out
+
+
 def gram(Rp: torch.Tensor, dinv: torch.Tensor, stream=None) -> torch.Tensor:
     """a7 step 1 (tpo_gram): G = R'^T diag(dinv^2) R' as a D x D fp64 tensor."""
     n, D = Rp.shape

@@ -118,6 +118,18 @@ class TestFullSize:
         nr = np.sum(Rp[torch.from_numpy(rows).cuda()].double().cpu().numpy() ** 2, axis=1)
         assert np.allclose(nr, np.e, rtol=1e-5)
 
+    def test_affinity_matvec_full_vs_oracle(self, tpo, st):
+        """a6 at full size (b = k + 10 columns, the Halko block width): S~Y vs the oracle's fp64 product;
+        F5: S~ (1/dinv) = 1/dinv."""
+        g = st["g"]
+        Rp, dinv = torch.from_numpy(st["Rp32"]).cuda(), torch.from_numpy(st["dinv32"]).cuda()
+        Y = np.random.default_rng(3).standard_normal((g.n, g.k + 10)).astype(np.float32)
+        out = tpo.affinity_matvec(Rp, dinv, torch.from_numpy(Y).cuda())
+        assert relF(out.cpu().numpy(), O.affinity_matvec(st["Rp32"], st["dinv32"], Y)) <= 1e-5
+        v = (1.0 / st["dinv32"].astype(np.float64))[:, None].astype(np.float32)
+        o2 = tpo.affinity_matvec(Rp, dinv, torch.from_numpy(v).cuda())
+        assert relF(o2.cpu().numpy(), v) <= 1e-5
+
     def test_topk_full_vs_oracle(self, tpo, st):
         g = st["g"]
         Rp = torch.from_numpy(st["Rp32"]).cuda()

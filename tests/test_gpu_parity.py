@@ -255,6 +255,26 @@ def test_affinity_matvec(tpo, tiny_feats):
     assert relF(o2.cpu().numpy(), v) <= 1e-5
 
 
+@pytest.mark.parametrize("chunk", [0, 700, 2000, 64])
+def test_affinity_matvec_rfree(tpo, chunk):
+    """f3: S~Y from Zhat and Q with R' recomputed in row chunks (ragged last chunk)
+    vs the oracle's features -> affinity chain, and vs the materialised GPU product."""
+    g = make_config("tiny")
+    _, Zh = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, g.alpha, g.T)
+    Zh32 = Zh.astype(np.float32)
+    Q = O.haar_q(g.G).astype(np.float32)
+    Rp, dinv, _ = O.features(Zh32, Q)
+    Rp32, dv32 = Rp.astype(np.float32), dinv.astype(np.float32)
+    Y = np.random.default_rng(5).standard_normal((g.n, 15)).astype(np.float32)
+    ref = O.affinity_matvec(Rp32, dv32, Y)
+    out = tpo.affinity_matvec_rfree(torch.from_numpy(Zh32).cuda(), torch.from_numpy(Q).cuda(), torch.from_numpy(Y).cuda(),
+                                    chunk_rows=chunk)
+    assert relF(out.cpu().numpy(), ref) <= 1e-5
+    Rg, dg_, _ = tpo.features(torch.from_numpy(Zh32).cuda(), torch.from_numpy(Q).cuda())
+    mat = tpo.affinity_matvec(Rg, dg_, torch.from_numpy(Y).cuda())
+    assert relF(out.cpu().numpy(), mat.cpu().numpy()) <= 1e-6
+
+
 @pytest.fixture(scope="module")
 def tiny_topk(tiny_feats):
     g, Rp, dinv = tiny_feats

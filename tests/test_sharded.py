@@ -261,3 +261,33 @@ def test_propagate_sharded_library_nccl(T, weighted):
     Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, 0.5, T, g.B_val)
     assert np.linalg.norm(Z.cpu().numpy() - Zo) <= 1e-5 * np.linalg.norm(Zo)
     assert np.linalg.norm(Zh.cpu().numpy() - Zho) <= 1e-5 * np.linalg.norm(Zho)
+
+
+@pytest.mark.gpu
+def test_run_sharded_library_nccl():
+    """tpo_run_sharded (the whole hot path with every collective inside libtpo) at world 1 through
+    NCCL: labels equal the oracle's end-to-end labels on the tiny config, and tpo_run's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_11922_b200 import build
+    build.build()
+    import paper_2405_11922_b200 as T
+    from oracle import dense as DN
+    from paper_2405_11922_b200.sharded import GpuShardOps, LibRunner, NcclComm
+    from synth import make_config
+    g = make_config("tiny")
+    sh = shard_graph(g.n, g.m, g.B_rowptr, g.B_col, 0, 1, g.B_val)
+    ops = GpuShardOps(sh, "cuda:0", g.d)
+    comm = NcclComm(0, 1, "cuda:0", NcclComm.unique_id())
+    try:
+        run = LibRunner(comm, ops, g.d, g.k)
+        Gd = torch.from_numpy(np.ascontiguousarray(g.G, np.float64)).cuda()
+        lab = run(torch.from_numpy(g.X).cuda(), g.alpha, g.T, Gd, 5, 20).cpu().numpy()
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    ref = O.run(g)
+    assert np.array_equal(lab, ref["labels"]) or DN.ari(lab, ref["labels"]) >= 0.999
+    dg = T.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col)
+    lab1, _ = T.run(dg, torch.from_numpy(g.X).cuda(), g.alpha, g.T, g.k, g.G)
+    assert DN.ari(lab, lab1.cpu().numpy()) >= 0.999
