@@ -302,9 +302,21 @@ __global__ void stack_kernel(const double *__restrict__ u, const double *__restr
 //    orders of magnitude below the 1e-4 parity bound and the fp32 rounding of Gamma).  The filter damps [0, theta_min] (theta_min
 //    = smallest Ritz value of the block) and amplifies the wanted end of the spectrum; the
 //    deflation keeps the lambda = 1 direction from swamping the block.
+// Extra columns of the subspace block beyond k (b = k + extra).  The host Rayleigh-Ritz
+// eigensolve costs O((b+1)^3) per round; on large (k = 50) extra = 50 / 32 / 24 / 16 all converged in
+// the same 5 rounds while the top-k stage took 16.9 / 14.7 / 13.9 / 13.9 ms, so extra = 24 (16 for
+// k < 24).  TPO_EIG_EXTRA overrides it within the workspace's bound max(k, 16) (measurement).
+int64_t eig_block_extra(int64_t k) {
+    if (const char *e = getenv("TPO_EIG_EXTRA")) {
+        const int64_t v = atoll(e);
+        if (v >= 8 && v <= std::max<int64_t>(k, 16)) return v;   // the workspace is sized for max(k, 16)
+    }
+    return std::max<int64_t>(16, std::min<int64_t>(k, 24));
+}
+
 void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<double> &lam, double *Psi64,
                Arena &ar, cudaStream_t st, int power_steps = 6) {
-    const int64_t b = std::min<int64_t>(D - 1, k + std::max<int64_t>(k, 16));
+    const int64_t b = std::min<int64_t>(D - 1, k + eig_block_extra(k));
     if (b + 1 >= D || D <= 64) {
         std::vector<double> gh = to_host(G, D * D, st), w(D), V(D * k);
         host_sym_eig_top(D, gh.data(), k, w.data(), V.data());

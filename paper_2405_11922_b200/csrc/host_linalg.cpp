@@ -106,7 +106,8 @@ void tridiagonalise(int n, std::vector<double> &a, std::vector<double> &d, std::
     }
 }
 
-// Implicit-shift QL on the tridiagonal (d, e), accumulating rotations into z (n x n).
+// Implicit-shift QL on the tridiagonal (d, e), accumulating rotations into z (n x n, TRANSPOSED:
+// z[i * n + k] = component k of vector i).
 void tridiag_ql(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> &z) {
     for (int i = 1; i < n; ++i) e[i - 1] = e[i];
     e[n - 1] = 0.0;
@@ -139,10 +140,12 @@ void tridiag_ql(int n, std::vector<double> &d, std::vector<double> &e, std::vect
                     r = (d[i] - g) * s + 2.0 * c * b;
                     d[i + 1] = g + (p = s * r);
                     g = c * r - b;
+                    // z is held transposed (row i = eigenvector column i): contiguous rows
+                    double *zi = &z[(size_t)i * n], *zi1 = &z[(size_t)(i + 1) * n];
                     for (int k = 0; k < n; ++k) {
-                        f = z[(size_t)k * n + i + 1];
-                        z[(size_t)k * n + i + 1] = s * z[(size_t)k * n + i] + c * f;
-                        z[(size_t)k * n + i] = c * z[(size_t)k * n + i] - s * f;
+                        f = zi1[k];
+                        zi1[k] = s * zi[k] + c * f;
+                        zi[k] = c * zi[k] - s * f;
                     }
                 }
                 if (r == 0.0 && i >= l) continue;
@@ -171,7 +174,12 @@ void host_sym_eig_top(int64_t D, const double *Ain, int64_t nvec, double *w, dou
         return;
     }
     tridiagonalise(n, a, d, e);
-    tridiag_ql(n, d, e, a);
+    std::vector<double> zt((size_t)n * n);                  // the transform, transposed for tridiag_ql
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) zt[(size_t)c * n + r] = a[(size_t)r * n + c];
+    tridiag_ql(n, d, e, zt);
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) a[(size_t)r * n + c] = zt[(size_t)c * n + r];
     std::vector<int> ord(n);
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return d[x] > d[y]; });
