@@ -353,16 +353,17 @@ __global__ void cluster_sums_kernel(const double *__restrict__ U, const int32_t 
     double *my = acc + (size_t)w * k * 32 + lane;
     int *myc = cnt + w * k;
     int64_t i = w0;
-    for (; i + 4 <= w1; i += 4) {
-        int l[4];
-        double v[4];
+    constexpr int CU = 16;                 // rows in flight per warp (the pass is memory-latency bound)
+    for (; i + CU <= w1; i += CU) {
+        int l[CU];
+        double v[CU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < CU; ++u) {
             l[u] = labels[i + u];
             v[u] = act ? U[(i + u) * k + a] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < CU; ++u) {
             my[l[u] * 32] += v[u];
             if (lane == 0 && blockIdx.y == 0) myc[l[u]] += 1;
         }

@@ -215,7 +215,7 @@ size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k);
 // fp64 tensor-path (DMMA) products of the discretisation (ts64.cu).  ts64_enabled(): TPO_TS64=0
 // selects the CUDA-core kernels of dense.cu / onmf.cu / cluster.cu (A/B measurement only).
 bool ts64_enabled();
-// the DMMA Ups update (den = Ups M, resident M, bulk-copied Ups / RH tiles): even 16 < k <= 64
+// the DMMA Ups update (den = Ups M, resident M, bulk-copied Ups / RH tiles): even 16 < k <= 104
 bool ts64_ups_enabled(int k);
 size_t ts_atb_ws(int p, int q);
 void ts_assign(const double *U, const double *Phi, int64_t n, int k, int32_t *labels, int32_t *changed,

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
 // stays resident in shared memory; BM-row tiles of A (one contiguous block each) arrive by bulk copy
 // into a 2-slot ring on mbarriers, the next tile in flight while one is multiplied.  Warp w owns the
 // MTW m-tiles (8 rows each) w*MTW .. of a tile against all NT n-tiles.
-template <int EPI, int NT, int MTW>
+template <int EPI, int NT, int MTW, int NS>           // NS: ring slots (2, or 1 when the tiles are large)
 __global__ void __launch_bounds__(DM_NT, 1) dm_rowk_kernel(DmArgs a) {
     if (EPI == DM_ASSIGN && *a.done) return;
     constexpr int BM = 8 * 8 * MTW;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowk_kernel(DmArgs a) {
     uint64_t *full = reinterpret_cast<uint64_t *>(dsm);                 // [2]
     const int k = a.N;
     double *Ws = reinterpret_cast<double *>(dsm + 128);                 // [k][k]
-    double *ring = Ws + ((k * k + 15) / 16) * 16;                        // [2][NB][BM * k]
+    double *ring = Ws + ((k * k + 15) / 16) * 16;                        // [NS][NB][BM * k]
     constexpr int NB = EPI == DM_UPS ? 2 : 1;                           // UPS slots: Ups tile, RH tile
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gr = lane >> 2, gc = lane & 3;
@@ -310,21 +310,21 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowk_kernel(DmArgs a) {
         const int64_t r0 = (blockIdx.x + j * gridDim.x) * BM;
         const int rows = (int)(a.n - r0 < BM ? a.n - r0 : BM);
         const uint32_t bytes = (uint32_t)rows * (uint32_t)k * 8u;
-        double *slot = ring + (size_t)(j & 1) * NB * BM * k;
-        bar_expect_tx(full + (j & 1), NB * bytes);
-        bulk_g2s(slot, A + r0 * k, bytes, full + (j & 1));
-        if (EPI == DM_UPS) bulk_g2s(slot + BM * k, a.RH + r0 * k, bytes, full + (j & 1));
+        double *slot = ring + (size_t)(j % NS) * NB * BM * k;
+        bar_expect_tx(full + (j % NS), NB * bytes);
+        bulk_g2s(slot, A + r0 * k, bytes, full + (j % NS));
+        if (EPI == DM_UPS) bulk_g2s(slot + BM * k, a.RH + r0 * k, bytes, full + (j % NS));
     };
     if (tid == 0) {
         if (my > 0) issue(0);
-        if (my > 1) issue(1);
+        if (NS > 1 && my > 1) issue(1);
     }
     bool changed = false;
     for (int64_t j = 0; j < my; ++j) {
         const int64_t r0 = (blockIdx.x + j * gridDim.x) * BM;
         const int rows = (int)(a.n - r0 < BM ? a.n - r0 : BM);
-        bar_wait(full + (j & 1), (uint32_t)((j >> 1) & 1));
-        double *as = ring + (size_t)(j & 1) * NB * BM * k;
+        bar_wait(full + (j % NS), (uint32_t)((j / NS) & 1));
+        double *as = ring + (size_t)(j % NS) * NB * BM * k;
         double acc[MTW][NT][2];
 #pragma unroll
         for (int m = 0; m < MTW; ++m)
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowk_kernel(DmArgs a) {
                 bulk_s2g(a.out + r0 * k, as, (uint32_t)rows * (uint32_t)k * 8u);
                 bulk_wait_read();                     // the store has read the slot before it is refilled
             }
-            if (j + 2 < my) issue(j + 2);
+            if (j + NS < my) issue(j + NS);
         }
     }
     if (EPI == DM_UPS && tid == 0) bulk_wait_all();
@@ -762,20 +762,29 @@ void dm_assign(const DmArgs &a, cudaStream_t st) { dm_launch<double, DM_ASSIGN, 
 template <int EPI, int NT>
 void dm_rowk_launch(const DmArgs &a, cudaStream_t st) {
     const int k = a.N;
-    auto go = [&](auto mtw_tag) {
-        constexpr int MTW = decltype(mtw_tag)::value;
+    auto go = [&](auto mtw_tag, auto ns_tag) {
+        constexpr int MTW = decltype(mtw_tag)::value, NS = decltype(ns_tag)::value;
         constexpr int BM = 64 * MTW;
         constexpr int NB = EPI == DM_UPS ? 2 : 1;
-        const size_t sm = 128 + sizeof(double) * (((size_t)k * k + 15) / 16 * 16 + 2 * (size_t)NB * BM * k);
-        TPO_CUDA(cudaFuncSetAttribute(dm_rowk_kernel<EPI, NT, MTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        const size_t sm = 128 + sizeof(double) * (((size_t)k * k + 15) / 16 * 16 + (size_t)NS * NB * BM * k);
+        TPO_CUDA(cudaFuncSetAttribute(dm_rowk_kernel<EPI, NT, MTW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sm));
         const int64_t tiles = cdiv(std::max<int64_t>(a.n, 1), BM);
         const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count_cached()));
-        dm_rowk_kernel<EPI, NT, MTW><<<gx, DM_NT, sm, st>>>(a);
+        dm_rowk_kernel<EPI, NT, MTW, NS><<<gx, DM_NT, sm, st>>>(a);
         TPO_LAUNCH_CHECK();
     };
-    // UPS slots hold two tiles (Ups, RH): 64-row tiles keep them within shared memory
-    if (k <= 64 && EPI != DM_UPS) go(std::integral_constant<int, 2>());
-    else go(std::integral_constant<int, 1>());
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    // ASSIGN: 128-row tiles for k <= 64; UPS slots hold two tiles (Ups, RH): 64-row tiles, and a
+    // single slot once the k x k factor and two double-buffered tile pairs exceed shared memory
+    if (EPI != DM_UPS) {
+        if (k <= 64) go(I2(), I2());
+        else go(I1(), I2());
+    } else {
+        if (k <= 64) go(I1(), I2());
+        else go(I1(), I1());
+    }
 }
 template <int NT>
 void dm_rowk_ups(const DmArgs &a, cudaStream_t st) { dm_rowk_launch<DM_UPS, NT>(a, st); }
@@ -858,8 +867,8 @@ bool ts64_enabled() {
     const char *e = getenv("TPO_TS64");
     return !(e && e[0] == '0');
 }
-// (k <= 64: two 64-row Ups / RH slots and the resident k x k M fit shared memory)
-bool ts64_ups_enabled(int k) { return ts64_enabled() && k > 16 && k <= 64 && k % 2 == 0; }
+// (k <= 64: two 64-row Ups / RH slots and the resident k x k M fit shared memory; up to 104 with one)
+bool ts64_ups_enabled(int k) { return ts64_enabled() && k > 16 && k <= 104 && k % 2 == 0; }
 
 // out = diag(rs) A W diag(1/cs): A n x K fp32 (lda), W K x N fp64 (ldw = N), out n x N fp64 (ldo)
 void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int K, int N,
