@@ -259,7 +259,40 @@ def cpu_baseline_sample(g, args):
             "sample": sample, "tpo_seconds": step_s, "stages_ms": stages}
 
 
-def run_sharded(args, g, ws, rank, local, dev):
+def shard_inputs(args, ws, rank):
+    """Every rank's share of the workload without every rank materialising the whole graph: rank 0
+    generates it, writes each rank's U slice (CSR(B_p), CSR(B_p^T), X_p) to /dev/shm, and each rank
+    loads only its own (host memory per rank ~ 1/ws of the graph; xl is ~22 GB whole)."""
+    import shutil
+    import types
+    import torch.distributed as dist
+    from paper_2405_11922_b200.sharded import HostShard, shard_graph
+    from synth import make_config
+    base = f"/dev/shm/tpo_bench_{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        g = make_config(args.config)
+        os.makedirs(base, exist_ok=True)
+        for r in range(ws):
+            sh = shard_graph(g.n, g.m, g.B_rowptr, g.B_col, r, ws, g.B_val)
+            np.savez(f"{base}/shard{r}.npz", Bp_rowptr=sh.Bp_rowptr, Bp_col=sh.Bp_col, Btp_rowptr=sh.Btp_rowptr,
+                     Btp_col=sh.Btp_col, X=g.X[sh.u0:sh.u1], u0=sh.u0, u1=sh.u1)
+        np.savez(f"{base}/meta.npz", G=g.G, n=g.n, m=g.m, nnz=g.nnz, d=g.d, k=g.k, alpha=g.alpha, T=g.T)
+        del g
+    dist.barrier()
+    z = np.load(f"{base}/shard{rank}.npz")
+    mt = np.load(f"{base}/meta.npz")
+    meta = types.SimpleNamespace(name=args.config, G=mt["G"], n=int(mt["n"]), m=int(mt["m"]), nnz=int(mt["nnz"]),
+                                 d=int(mt["d"]), k=int(mt["k"]), alpha=float(mt["alpha"]), T=int(mt["T"]))
+    sh = HostShard(rank, ws, meta.n, meta.m, int(z["u0"]), int(z["u1"]), z["Bp_rowptr"], z["Bp_col"], z["Btp_rowptr"],
+                   z["Btp_col"])
+    Xp = np.ascontiguousarray(z["X"])
+    dist.barrier()
+    if rank == 0:
+        shutil.rmtree(base, ignore_errors=True)
+    return meta, sh, Xp
+
+
+def run_sharded(args, g, ws, rank, local, dev, pre=None):
     """One graph, U rows split over the ranks: sharded propagation (NCCL
     reduce-scatter / all-gather of the V-side block per hop) and the sharded solver (fp64
     partials all-reduced); every rank computes the Haar rotation from G (replicated)."""
@@ -274,10 +307,14 @@ def run_sharded(args, g, ws, rank, local, dev):
         os.environ.setdefault("MASTER_PORT", "29531")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     coll = TorchCollectives()
-    sh = shard_graph(g.n, g.m, g.B_rowptr, g.B_col, rank, ws, g.B_val)
+    if pre is not None:                       # (meta, shard, X_p) from shard_inputs
+        g, sh, Xp_host = pre
+    else:
+        sh = shard_graph(g.n, g.m, g.B_rowptr, g.B_col, rank, ws, g.B_val)
+        Xp_host = g.X[sh.u0:sh.u1]
     ops = GpuShardOps(sh, dev, g.d)
     sops = GpuSolverOps(sh.n_p, g.d, g.k, dev)
-    Xp = torch.from_numpy(g.X[sh.u0:sh.u1]).to(dev)
+    Xp = torch.from_numpy(np.ascontiguousarray(Xp_host)).to(dev)
     L = lib()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -334,7 +371,7 @@ def run_sharded(args, g, ws, rank, local, dev):
     e2e = None
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        hX = pin(g.X[sh.u0:sh.u1])
+        hX = pin(Xp_host)
         hB = [pin(sh.Bp_rowptr), pin(sh.Bp_col), pin(sh.Btp_rowptr), pin(sh.Btp_col)]
         hG = pin(np.ascontiguousarray(g.G, np.float64))
         dB = [ops.Bp[0], ops.Bp[1], ops.Btp[0], ops.Btp[1]]
@@ -408,6 +445,14 @@ def main():
         args.mode = "sharded" if ws > 1 else "replicas"
 
     from synth import make_config
+    if args.impl != "reference" and args.mode == "sharded" and ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        dist.init_process_group("nccl", device_id=dev)
+        run_sharded(args, None, ws, rank, local, dev, pre=shard_inputs(args, ws, rank))
+        return
     g = make_config(args.config)
 
     if args.impl == "reference":

@@ -291,3 +291,40 @@ def test_run_sharded_library_nccl():
     dg = T.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col)
     lab1, _ = T.run(dg, torch.from_numpy(g.X).cuda(), g.alpha, g.T, g.k, g.G)
     assert DN.ari(lab, lab1.cpu().numpy()) >= 0.999
+
+
+def _shard_inputs_worker(rank, world, port, q):
+    import types
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        meta, sh, Xp = bench.shard_inputs(types.SimpleNamespace(config="tiny"), world, rank)
+        q.put((rank, meta.n, meta.nnz, sh.u0, sh.u1, sh.Bp_col.copy(), Xp.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_shard_inputs_gloo():
+    """bench.py's multi-rank input path: rank 0 generates the graph once and every rank loads only
+    its own U slice; the slices reassemble the generator's graph and X exactly."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_shard_inputs_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict()
+    for _ in range(2):
+        r, n, nnz, u0, u1, col, Xp = q.get(timeout=180)
+        res[r] = (u0, u1, col, Xp)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from synth import make_config
+    g = make_config("tiny")
+    assert np.array_equal(np.concatenate([res[r][2] for r in range(2)]), g.B_col)
+    assert np.array_equal(np.concatenate([res[r][3] for r in range(2)]), g.X)
+    assert res[0][1] == res[1][0] and res[1][1] == g.n
