@@ -23,6 +23,7 @@ SYMBOLS = [
     "tpo_shard_solver_ws", "tpo_shard_features", "tpo_shard_dinv", "tpo_eig_from_gram", "tpo_shard_gamma",
     "tpo_shard_atb64", "tpo_shard_apply_chol", "tpo_shard_colstats", "tpo_shard_gamma_final",
     "tpo_shard_onmf_init", "tpo_shard_onmf_rtu", "tpo_onmf_h_update", "tpo_shard_onmf_rh",
+    "tpo_rowgemm_f64_ws", "tpo_rowgemm_f64",
     "tpo_shard_onmf_u_update", "tpo_shard_nci_assign", "tpo_nci_phi",
     "tpo_svd_reduce_ws", "tpo_svd_reduce", "tpo_eval_ws", "tpo_eval", "tpo_objective_ws", "tpo_objective",
     "tpo_rows_gather", "tpo_rows_scatter",
@@ -144,6 +145,10 @@ def lib():
     L.tpo_affinity_matvec_rfree_ws.restype = sz
     L.tpo_affinity_matvec_rfree.argtypes = [vp, i64, i64, vp, vp, i64, vp, i64, vp, sz, vp]
     L.tpo_affinity_matvec_rfree.restype = C.c_int
+    L.tpo_rowgemm_f64_ws.argtypes = [i64, i64, i32]
+    L.tpo_rowgemm_f64_ws.restype = sz
+    L.tpo_rowgemm_f64.argtypes = [vp, i64, i64, vp, vp, i32, vp, vp, sz, vp]
+    L.tpo_rowgemm_f64.restype = C.c_int
     L.tpo_run_sharded_ws.argtypes = [i64, i64, i64, i64, i32, i32]
     L.tpo_run_sharded_ws.restype = sz
     L.tpo_run_sharded.argtypes = [vp, P, P, vp, i64, f32, i32, i32, vp, i64, i32, i32, vp, vp, vp, vp, sz, vp]

@@ -556,7 +556,9 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     const int64_t nb = cdiv(std::max<int64_t>(n, 1), cluster_rows_per_block(n));
     ar.take<double>(nb * k * k);
     ar.take<int64_t>(nb * k);
-    return ar.off + std::max(std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)), ts_atb_ws(k, k)) + 4096;
+    ar.take<char>(rh_plan_ws(n));
+    return ar.off + std::max(std::max(std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)), ts_atb_ws(k, k)),
+                             rh_apply_ws(D, k)) + 4096;
 }
 
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
@@ -573,6 +575,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const int64_t nb = cdiv(std::max<int64_t>(n, 1), rpb);
     double *part = ar.take<double>(nb * k * k);
     int64_t *cpart = ar.take<int64_t>(nb * k);
+    const RhPlan rhp = rh_plan(Rp, n, D, k, ar, st);
     const size_t mark = ar.off;
 
     TPO_CUDA(cudaMemcpyAsync(sig, sigma, sizeof(double) * k, cudaMemcpyHostToDevice, st));
@@ -590,7 +593,8 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
         TPO_LAUNCH_CHECK();
         std::swap(H, Hn);
-        tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
+        rh_apply(rhp, Rp, dinv, H, n, D, k, RH, ar, st);
+        ar.off = mark;
         if (ts64_enabled() && k <= 104) ts_atb_f64(U, k, RH, k, n, k, k, M, ar, st);
         else dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
         ar.off = mark;

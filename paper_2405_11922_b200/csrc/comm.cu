@@ -184,11 +184,13 @@ size_t run_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, in
     s += align_up(sizeof(double) * (size_t)D * D) + 3 * align_up(sizeof(double) * (size_t)D * k) + align_up(sizeof(float) * D * k);
     s += 3 * align_up(sizeof(double) * (size_t)n_p * k) + align_up(sizeof(float) * (size_t)n_p * k);
     s += 8 * align_up(sizeof(double) * (size_t)k * k) + 8 * align_up(sizeof(double) * (size_t)k) + 1024;
+    s += rh_plan_ws(n_p);
     size_t inner = std::max(features_ws_bytes(n_p, d), gram_tc_ws(std::max<int64_t>(n_p, 1), D));
     inner = std::max(inner, eig_from_gram_ws(D, k));
     inner = std::max(inner, haar_q_ws_bytes(d));
     inner = std::max(inner, nci_assign_part_ws(n_p, k));
     inner = std::max(inner, onmf_ws_bytes(n_p, D, k));
+    inner = std::max(inner, rh_apply_ws(D, k));
     inner = std::max(inner, ts_atb_ws(k, k) + dgemm_ws(k, k, std::max<int64_t>(n_p, 1)));
     inner = std::max(inner, align_up(sizeof(double) * (size_t)(4 * 2 * 148 * k)) + 4096);
     return s + inner + 64 * 256;
@@ -218,6 +220,7 @@ void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, con
     double *vals_all = ar.take<double>((size_t)world * k);
     int64_t *idx_all = ar.take<int64_t>((size_t)world * k);
     int32_t *changed = ar.take<int32_t>(2);
+    int32_t *rowE = ar.take<int32_t>(std::max<int64_t>(n_p, 1));
     const size_t mark = ar.off;
     auto atb = [&](const double *A, const double *B, double *out) {
         if (n_p == 0) { TPO_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * k * k, st)); return; }
@@ -295,6 +298,7 @@ void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, con
     // a8 (Alg. 2)
     onmf_init(Gam, n_p, Psi, sigma.data(), D, k, U, H, ar, st);
     ar.off = mark;
+    const RhPlan rhp = rh_plan_at(rowE, Rp, n_p, D, k, st);
     for (int t = 0; t < Tf; ++t) {
         if (n_p > 0) onmf_rtu(Rp, n_p, D, dinv, U, k, RtU, ar, st);
         else TPO_CUDA(cudaMemsetAsync(RtU, 0, sizeof(double) * D * k, st));
@@ -304,7 +308,8 @@ void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, con
         allreduce(UtU, (size_t)k * k);
         onmf_h_update(H, RtU, UtU, D, k, ar, st);
         ar.off = mark;
-        if (n_p > 0) tsgemm_AW_f64(Rp, D, dinv, H, n_p, D, k, RH, k, st);
+        rh_apply(rhp, Rp, dinv, H, n_p, D, k, RH, ar, st);
+        ar.off = mark;
         atb(U, RH, M);
         allreduce(M, (size_t)k * k);
         onmf_u_update(U, RH, M, n_p, k, st);

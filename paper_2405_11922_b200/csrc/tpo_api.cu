@@ -653,6 +653,30 @@ int tpo_onmf_h_update(double *H, const double *RtU, const double *UtU, int64_t D
     });
 }
 
+size_t tpo_rowgemm_f64_ws(int64_t n, int64_t K, int32_t N) {
+    if (n < 0 || K < 1 || N < 1) return 0;
+    return align_up(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1)) + oz_aw_ws(K, N) + 1024;
+}
+
+int tpo_rowgemm_f64(const float *A, int64_t n, int64_t K, const float *rs, const double *W, int32_t N, double *out,
+                    void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 0 && K >= 1 && N >= 1 && K % 4 == 0, "bad shapes (K % 4 == 0 required)");
+        check_ptr(W, "W");
+        if (n == 0) return;
+        check_ptr(A, "A"); check_ptr(out, "out");
+        cudaStream_t st = as_stream(stream);
+        if (oz_enabled() && oz_aw_supported(K, N)) {
+            Arena ar(ws, ws_bytes);
+            int32_t *rowE = ar.take<int32_t>(n);
+            oz_rowexp(A, K, n, (int)K, rowE, st);
+            oz_aw_f64(A, K, rs, rowE, W, n, (int)K, N, out, N, ar, st);
+        } else {
+            tsgemm_AW_f64(A, K, rs, W, n, K, N, out, N, st);
+        }
+    });
+}
+
 int tpo_shard_onmf_rh(const float *Rp_p, const float *dinv_p, const double *H, int64_t n_p, int64_t D, int32_t k,
                       double *RH_p, void *stream) {
     return guarded([&] {

@@ -223,6 +223,25 @@ void ts_assign(const double *U, const double *Phi, int64_t n, int k, int32_t *la
 // out (p x q) = A^T B for n x p / n x q fp64 A, B (p, q <= 104) on the fp64 tensor path
 void ts_atb_f64(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, double *out,
                 Arena &ar, cudaStream_t st);
+// fp64-accurate out = diag(rs) A W on the integer tensor cores (oz.cu; Ozaki digit splitting):
+// A n x K fp32 (lda % 4 == 0, 16-byte aligned), W K x N fp64, out n x N fp64; N <= 64 and the
+// digit image of W (7 x N x K bytes) <= 112 KB.  rowE = oz_rowexp(A) (per-row exponents).
+bool oz_enabled();
+bool oz_aw_supported(int64_t K, int N);
+size_t oz_aw_ws(int64_t K, int N);
+void oz_rowexp(const float *A, int64_t lda, int64_t n, int K, int32_t *E, cudaStream_t st);
+void oz_aw_f64(const float *A, int64_t lda, const float *rs, const int32_t *rowE, const double *W, int64_t n, int K,
+               int N, double *out, int64_t ldo, Arena &ar, cudaStream_t st);
+struct RhPlan {
+    bool oz = false;
+    int32_t *rowE = nullptr;
+};
+RhPlan rh_plan(const float *Rp, int64_t n, int64_t D, int k, Arena &ar, cudaStream_t st);
+RhPlan rh_plan_at(int32_t *rowE, const float *Rp, int64_t n, int64_t D, int k, cudaStream_t st);
+size_t rh_plan_ws(int64_t n);
+size_t rh_apply_ws(int64_t D, int k);
+void rh_apply(const RhPlan &p, const float *Rp, const float *dinv, const double *H, int64_t n, int64_t D, int k,
+              double *RH, Arena &ar, cudaStream_t st);
 void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int K, int N,
                const double *cs, double *out, int64_t ldo, cudaStream_t st);
 void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);

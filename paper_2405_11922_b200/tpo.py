@@ -154,6 +154,22 @@ def affinity_matvec(Rp: torch.Tensor, dinv: torch.Tensor, Y: torch.Tensor, out=N
     return out
 
 
+def rowgemm_f64(A: torch.Tensor, W: torch.Tensor, rs=None, out=None, stream=None):
+    """tpo_rowgemm_f64: out = diag(rs) A W in fp64 (A n x K fp32, W K x N fp64)."""
+    n, K = A.shape
+    _need(A, torch.float32, "A")
+    _need(W, torch.float64, "W")
+    N = W.shape[1]
+    if rs is not None:
+        _need(rs, torch.float32, "rs", (n,))
+    out = torch.empty(n, N, dtype=torch.float64, device=A.device) if out is None else out
+    L = lib()
+    ws = _ws(L.tpo_rowgemm_f64_ws(n, K, N), A.device)
+    check(L.tpo_rowgemm_f64(_ptr(A), n, K, _ptr(rs) if rs is not None else None, _ptr(W), N, _ptr(out), _ptr(ws),
+                            ws.numel(), _stream(stream)))
+    return out
+
+
 def affinity_matvec_rfree(Zhat: torch.Tensor, Q: torch.Tensor, Y: torch.Tensor, chunk_rows: int = 0, out=None,
                           stream=None):
     """a6 without materialising R' (tpo_affinity_matvec_rfree): R' rows recomputed from Zhat in chunks."""
