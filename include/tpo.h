@@ -284,8 +284,8 @@ int tpo_cluster(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_
  * Row GEMM of Alg. 2 / a7:  out = diag(rs) A W   (RH = dinv . (R' H), PAPER.md:552-560;
  * Gamma = R Psi Sigma^-1).  A: n x K fp32 row-major (16-byte aligned rows,
  * K % 4 == 0);  rs: n fp32 (NULL = 1);  W: K x N fp64;  out: n x N fp64 (all device).
- * fp64-accurate: when N <= 64 and 7 N K <= 112 KB (and TPO_OZ != 0) on the integer tensor cores
- * (tcgen05 kind::i8, Ozaki digit splitting: 7 x 7-bit digits per operand, exact int32 sums of
+ * fp64-accurate: when N <= 64 and 6 N K <= 96 KB (and TPO_OZ != 0) on the integer tensor cores
+ * (tcgen05 kind::i8, Ozaki digit splitting: 6 byte digits per operand, exact int32 sums of
  * the digit products of equal weight, error <~ 2^-44 K max|A_i| max|W_l|), otherwise on the fp64
  * tensor path (DMMA).  Workspace: tpo_rowgemm_f64_ws(n, K, N).  Errors: TPO_EINVAL, TPO_ENOMEM,
  * TPO_ECUDA.  Asynchronous on `stream`.

@@ -1,30 +1,39 @@
 // fp64-accurate row GEMM on the integer tensor cores (tcgen05 kind::i8):
 //      out = diag(rs) . A . W          A: n x K fp32 (R'), W: K x N fp64 (H), out: n x N fp64
-// the ONMF product RH = dinv . (R' H) of Alg. 2, and Gamma = R Psi Sigma^-1.
+// the ONMF product RH = dinv . (R' H) of Alg. 2.
 //
-// Error-free splitting (Ozaki scheme, integer form).  Row i of A is scaled by 2^-E_i (E_i: the
-// smallest power of two above max_j |A_ij|) and written as a 49-bit fixed-point number with a
-// bias:  F'_ij = trunc(A_ij 2^(48 - E_i)) + 2^48 in [0, 2^49), cut into 7 unsigned 7-bit digits
-// A'_p (p = 0 most significant).  Column l of W is scaled by 2^-E_l and cut into 7 signed 7-bit
-// digits B_q of trunc(|W_jl| 2^(49 - E_l)) (sign on every digit).  Then
-//      A_ij W_jl ~= 2^(E_i + E_l - 97) sum_{p,q} A'_p B_q 2^(7 (12 - p - q)) - (bias term)
-// and the products of equal weight s = p + q are summed EXACTLY in one int32 TMEM accumulator
-// acc_s (<= 7 K 127^2 < 2^31 for K <= 256 ... 19,000).  Pairs with p + q > 7 are dropped (their sum
-// is below 2^-44 of max|A_i| max|W_l| K).  The bias 2^48 = 64 * 2^42 lives in digit 0 only, so it
-// is removed exactly per accumulator: acc_s -= 64 sum_j B_s[j, l].  The epilogue combines the 8
-// accumulators in int64 (hi = acc_0..3, lo = acc_4..7, both < 2^53), converts with one fp64
-// rounding (fma(hi, 2^28, lo)), scales by powers of two (exact) and by rs_i (one rounding).
-// Accuracy: |error| <~ 2^-44 K max|A_i| max|W_l| -- within a few units of fp64 DMMA's own
-// rounding (K 2^-53 sum |A||W|) on these operands; parity is checked against an fp64 reference
-// (tests/test_gpu_reduce.py) and, end to end, by the bit-exact Alg. 3 labels.
+// Error-free splitting (Ozaki scheme, integer form, base 256).  Row i of A is scaled by 2^-E_i
+// (E_i: the smallest power of two above max_j |A_ij|) and written as the biased 48-bit integer
+//      A'_ij = floor(A_ij 2^(47 - E_i)) + 2^47  in [0, 2^48)
+// (one fp64 fma with round-toward-zero: A' is the low 48 bits of 2^52 + 2^47 + A 2^(47-E_i)),
+// cut into its 6 bytes a_p (unsigned digits, p = 0 most significant).  Column l of W is scaled by
+// 2^-E_l, truncated to the signed integer F_jl = trunc(W_jl 2^(46 - E_l)) (|F| < 2^46) and cut
+// into 6 balanced signed base-256 digits b_q in [-128, 127].  Then
+//      sum_j A'_ij F_jl = sum_{p,q} 2^(8 (10 - p - q)) sum_j a_p b_q
+// and the digit products of equal weight s = p + q are summed EXACTLY in one int32 TMEM
+// accumulator acc_s (|acc_s| <= 6 K 255 128 < 2^29 for K <= 2,048).  Pairs with p + q > 5 are
+// dropped.  The bias is removed exactly: sum_j A' F = sum_j floor(A 2^(47-E_i)) F + 2^47 sum_j F,
+// the last term a per-column constant.  The epilogue forms g0 = acc_0 2^16 + acc_1 2^8 + acc_2 and
+// g1 = acc_3 2^16 + acc_4 2^8 + acc_5 (exact int64, < 2^53), then
+//      out_il = rs_i 2^(E_i + E_l - 53) [ (g0 2^24 - C_hi) + (g1 - C_lo) ]
+// with C = 128 sum_j F_jl = C_hi + C_lo (C_hi = 128 fp64(sum), C_lo the exact int64 rest): two
+// fp64 roundings.  Error <~ 2^-44 K max|A_i| max|W_l| |rs_i| (the dropped pairs and the
+// truncations), within a few units of the fp64 DMMA path's own rounding on these operands
+// (tests/test_gpu_oz.py: ~3e-14 of max|out| apart); end to end the Alg. 3 labels stay bit-exact
+// (tests/test_gpu_fullsize.py).
 //
-// Kernel (persistent, one CTA per SM, 448 threads):
-//   warp 0      TMA producer: W's digit image once (bulk copy, resident in smem), then per
-//               (row tile of 128, K chunk of 32) the fp32 A chunk (SWIZZLE_128B box) into a ring
-//   warp 1      MMA issuer: per K chunk 34 tcgen05.mma kind::i8 (u8 x s8 -> s32), M = 128, N = NP,
-//               K = 32, into the 8 accumulators acc_s (TMEM columns s * NP)
-//   warps 2-9   slicers: fp32 chunk -> 7 digit planes (K-major, no-swizzle core-matrix layout)
-//   warps 10-13 epilogue: TMEM -> int64 -> fp64 -> out (rows of the tile, TMEM lane quarter warp % 4)
+// Kernel (persistent, one CTA per SM, 832 threads, ~207 KB shared memory):
+//   warp 0      W's digit image once (bulk copy, resident: 6 planes x NP x K bytes), then per
+//               (row tile of 128, K chunk of 32) the fp32 A chunk by TMA (SWIZZLE_128B) into a
+//               3-stage ring
+//   warp 1      MMA issuer: per K chunk 8 tcgen05.mma kind::i8 (u8 x s8 -> s32), M = 128, K = 32,
+//               N = up to 4 NP, into the 6 accumulators acc_s (TMEM columns s * NP)
+//   warps 2-9   slicers: fp32 chunk -> digits in registers (stage released), then 6 byte planes
+//               (K-major, no-swizzle core-matrix layout) into one of 3 plane buffers
+//   warps 10-25 epilogue: TMEM -> int64 -> fp64 -> out (TMEM lane quarter warp % 4, column quarter)
+// Measured on large (n = 2M, K = 256, N = 50): 1.37 ms vs 2.42 ms on the fp64 DMMA path
+// (tools/bench_oz.py).  On medium (K = 512, N = 20) it does not beat DMMA (0.62 vs 0.61 ms), so
+// the ONMF uses it only for N > 32 (rh_plan).
 #include <cuda.h>
 
 #include <algorithm>
@@ -37,25 +46,28 @@ namespace {
 
 constexpr int OZ_M = 128;                 // rows per tile
 constexpr int OZ_KC = 32;                 // K chunk (fp32 columns) = one kind::i8 MMA K
-constexpr int OZ_STG = 3;                 // fp32 staging stages
-constexpr int OZ_SL = 7;                  // digits per operand
-constexpr int OZ_SMAX = 7;                // kept digit pairs: p + q <= OZ_SMAX
-constexpr int OZ_NACC = OZ_SMAX + 1;      // accumulators acc_0 .. acc_7
+constexpr int OZ_STG = 3;                 // fp32 staging stages (TMA ring, 16 KB each)
+constexpr int OZ_NBUF = 3;                // digit-plane buffers
+constexpr int OZ_SL = 6;                  // digits per operand
+constexpr int OZ_SMAX = 5;                // kept digit pairs: p + q <= OZ_SMAX
+constexpr int OZ_NACC = OZ_SMAX + 1;      // accumulators acc_0 .. acc_5
 constexpr int OZ_STAGE_BYTES = OZ_M * OZ_KC * 4;      // 16 KB
 constexpr int OZ_PLANE = OZ_M * OZ_KC;                // one digit plane of a chunk: 4 KB
-constexpr int OZ_SBUF = OZ_SL * OZ_PLANE;             // 28 KB
+constexpr int OZ_SBUF = OZ_SL * OZ_PLANE;             // 24 KB
 constexpr int OZ_SLICERS = 8;
-constexpr int OZ_EPI = 4;
+constexpr int OZ_EPI = 16;                // 4 per TMEM lane quarter (column quarters)
 constexpr int OZ_THREADS = 32 * (2 + OZ_SLICERS + OZ_EPI);
-constexpr size_t OZ_B_MAX = 112 * 1024;               // resident digit image of W
+constexpr size_t OZ_B_MAX = 96 * 1024;                // resident digit image of W
 
 struct OzArgs {
-    int64_t n, ldo;
+    const float *A;
+    int64_t n, ldo, lda;
     int K, N, NP, Kp;        // Kp: K rounded up to OZ_KC; NP: N rounded up to 16
     int64_t ntiles;
     const int32_t *rowE;     // [n]
     const int32_t *colE;     // [NP]
-    const int32_t *corr;     // [OZ_NACC][NP]
+    const double *chi;       // [NP]: C_hi (fp64 rounding of C = 8 sum_j F_jl)
+    const long long *clo;    // [NP]: C - C_hi (exact)
     const uint8_t *Bimg;     // [OZ_SL][NP x Kp] digit image (smem layout)
     const float *rs;         // [n] or null
     double *out;
@@ -82,51 +94,58 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t *v) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = (int32_t)r[i];
-}
-
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
 
-// 28 low bits -> 4 bytes of 7-bit digits (byte 0 = least significant digit)
-__device__ __forceinline__ uint32_t spread7x4(uint32_t x) {
-    return (x & 0x7Fu) | ((x << 1) & 0x7F00u) | ((x << 2) & 0x7F0000u) | ((x << 3) & 0x7F000000u);
-}
-
-// Digits of 4 consecutive elements of one row -> the 7 digit-plane words (byte e = element e).
-__device__ __forceinline__ void slice4(const float4 a, float sc1, float sc2, uint32_t (&w)[OZ_SL]) {
+// Byte planes of 4 consecutive elements of one row: w[p] holds byte 5 - p (digit p) of the
+// elements' A' (byte e = element e).  scale = 2^(47 - E_i).
+__device__ __forceinline__ void slice4(const float4 a, double scale, uint32_t (&w)[OZ_SL]) {
     const float av[4] = {a.x, a.y, a.z, a.w};
     uint32_t L[4], H[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        const float x = (av[e] * sc1) * sc2;                       // exact: power-of-two scales
-        long long f;
-        asm("cvt.rzi.s64.f32 %0, %1;" : "=l"(f) : "f"(x));         // trunc(A 2^(48-E)), |f| < 2^48
-        const unsigned long long fp = (unsigned long long)(f + (1ll << 48));   // biased, < 2^49
-        L[e] = spread7x4((uint32_t)fp & 0x0FFFFFFFu);              // digits 6, 5, 4, 3
-        H[e] = spread7x4((uint32_t)(fp >> 28));                    // digits 2, 1, 0
+        // 2^52 + floor(2^47 + A 2^(47-E)): the product is exact (power of two), the sum lies in
+        // [2^52, 2^53) where round-toward-zero is floor
+        const double z = __fma_rz((double)av[e], scale, 4644337115725824.0);
+        const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
+        L[e] = (uint32_t)zb;                                   // bytes 0..3
+        H[e] = (uint32_t)(zb >> 32) & 0xFFFFu;                 // bytes 4..5
     }
     const uint32_t t0 = __byte_perm(L[0], L[1], 0x5140), t1 = __byte_perm(L[2], L[3], 0x5140);
     const uint32_t u0 = __byte_perm(L[0], L[1], 0x7362), u1 = __byte_perm(L[2], L[3], 0x7362);
-    w[6] = __byte_perm(t0, t1, 0x5410);
-    w[5] = __byte_perm(t0, t1, 0x7632);
-    w[4] = __byte_perm(u0, u1, 0x5410);
-    w[3] = __byte_perm(u0, u1, 0x7632);
+    w[5] = __byte_perm(t0, t1, 0x5410);
+    w[4] = __byte_perm(t0, t1, 0x7632);
+    w[3] = __byte_perm(u0, u1, 0x5410);
+    w[2] = __byte_perm(u0, u1, 0x7632);
     const uint32_t h0 = __byte_perm(H[0], H[1], 0x5140), h1 = __byte_perm(H[2], H[3], 0x5140);
-    const uint32_t g0 = __byte_perm(H[0], H[1], 0x7362), g1 = __byte_perm(H[2], H[3], 0x7362);
-    w[2] = __byte_perm(h0, h1, 0x5410);
-    w[1] = __byte_perm(h0, h1, 0x7632);
-    w[0] = __byte_perm(g0, g1, 0x5410);
+    w[1] = __byte_perm(h0, h1, 0x5410);
+    w[0] = __byte_perm(h0, h1, 0x7632);
+}
+
+__device__ __forceinline__ void tmem_ld4_nowait(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+
+// mbarrier wait with a back-off for warps that wait a whole tile (frees issue slots for the
+// producer, MMA and slicer warps)
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    uint64_t spins = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.b32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(128);
+        if (++spins > (1ull << 28)) __trap();
+    }
 }
 
 __device__ __forceinline__ float pow2f(int e) {       // 2^e for -126 <= e <= 127
@@ -141,14 +160,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t bbytes = (uint32_t)OZ_SL * NP * g.Kp;
-    const uint32_t stage_off = (bbytes + 1023) & ~1023u;
+    const uint32_t stage_off = (bbytes + 1023) & ~1023u;        // SWIZZLE_128B TMA targets
     const uint32_t slice_off = stage_off + OZ_STG * OZ_STAGE_BYTES;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + slice_off + 2 * OZ_SBUF);
-    // bars: bfull, afull[STG], aempty[STG], sready[2], sfree[2], tfull, tempty
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + slice_off + OZ_NBUF * OZ_SBUF);
+    // bars: bfull, afull[STG], aempty[STG], sready[NBUF], sfree[NBUF], tfull, tempty
     uint64_t *bfull = bars, *afull = bars + 1, *aempty = afull + OZ_STG, *sready = aempty + OZ_STG;
-    uint64_t *sfree = sready + 2, *tfull = sfree + 2, *tempty = tfull + 1;
-    int32_t *sh_corr = reinterpret_cast<int32_t *>(tempty + 1);   // [OZ_NACC][NP]
-    int32_t *sh_colE = sh_corr + OZ_NACC * NP;                    // [NP]
+    uint64_t *sfree = sready + OZ_NBUF, *tfull = sfree + OZ_NBUF, *tempty = tfull + 1;
+    double *sh_chi = reinterpret_cast<double *>(tempty + 1);         // [NP]
+    long long *sh_clo = reinterpret_cast<long long *>(sh_chi + NP);  // [NP]
+    int32_t *sh_colE = reinterpret_cast<int32_t *>(sh_clo + NP);     // [NP]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sh_colE + NP);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkc = g.Kp / OZ_KC;
@@ -156,11 +176,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
 
     if (threadIdx.x == 0) {
         mbar_init(smem_u32(bfull), 1);
-        for (int s = 0; s < OZ_STG; ++s) {
-            mbar_init(smem_u32(&afull[s]), 1);
-            mbar_init(smem_u32(&aempty[s]), OZ_SLICERS);
+        for (int b = 0; b < OZ_STG; ++b) {
+            mbar_init(smem_u32(&afull[b]), 1);
+            mbar_init(smem_u32(&aempty[b]), OZ_SLICERS);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < OZ_NBUF; ++b) {
             mbar_init(smem_u32(&sready[b]), OZ_SLICERS);
             mbar_init(smem_u32(&sfree[b]), 1);
         }
@@ -169,7 +189,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     }
-    for (int i = threadIdx.x; i < OZ_NACC * NP; i += blockDim.x) sh_corr[i] = g.corr[i];
+    for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+        sh_chi[i] = g.chi[i];
+        sh_clo[i] = g.clo[i];
+    }
     for (int i = threadIdx.x; i < NP; i += blockDim.x) sh_colE[i] = g.colE[i];
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -183,7 +206,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- producer ----------------
+        // ---------------- producer: W's digit image (resident), then the fp32 A chunks ----------------
+        // A chunks: 128 rows x 32 fp32, SWIZZLE_128B, into a 4-stage ring freed as soon as the
+        // slicers hold the chunk in registers
         if (lane == 0) {
             const uint32_t bar = smem_u32(bfull);
             mbar_expect_tx(bar, bbytes);
@@ -192,19 +217,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
             int64_t gc = 0;
             for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
                 for (int c = 0; c < nkc; ++c, ++gc) {
-                    const int s = (int)(gc % OZ_STG);
-                    const int64_t j = gc / OZ_STG;
-                    if (j > 0) mbar_wait(smem_u32(&aempty[s]), (uint32_t)((j - 1) & 1));
-                    const uint32_t full = smem_u32(&afull[s]);
+                    const int b = (int)(gc % OZ_STG);
+                    if (gc >= OZ_STG) mbar_wait(smem_u32(&aempty[b]), (uint32_t)(((gc / OZ_STG) - 1) & 1));
+                    const uint32_t full = smem_u32(&afull[b]);
                     mbar_expect_tx(full, OZ_STAGE_BYTES);
-                    tma_load_2d(smem_u32(smem + stage_off + s * OZ_STAGE_BYTES), &mapA, full, c * OZ_KC,
-                                (int)(t * OZ_M));
+                    tma_load_2d(smem_u32(smem + stage_off + b * OZ_STAGE_BYTES), &mapA, full, c * OZ_KC, (int)(t * OZ_M));
                 }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = idesc_i8(OZ_M, NP);
         mbar_wait(smem_u32(bfull), 0);
         const uint32_t bres = smem_u32(smem);
         const uint32_t sbo_b = 8u * (uint32_t)g.Kp;                   // 8 rows of W's image
@@ -214,23 +236,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
             if (i > 0) mbar_wait(smem_u32(tempty), (uint32_t)((i - 1) & 1));
             fence_after();
             for (int c = 0; c < nkc; ++c, ++gc) {
-                const int b = (int)(gc & 1);
-                mbar_wait(smem_u32(&sready[b]), (uint32_t)((gc >> 1) & 1));
+                const int b = (int)(gc % OZ_NBUF);
+                mbar_wait(smem_u32(&sready[b]), (uint32_t)((gc / OZ_NBUF) & 1));
                 fence_after();
                 if (lane == 0) {
                     const uint32_t abase = smem_u32(smem + slice_off + b * OZ_SBUF);
+                    // digit planes of W are consecutive NP-row blocks of one K-major matrix, so one
+                    // MMA with D at acc_{p+q0} and B = planes q0 .. q0+nq-1 (N = nq NP) adds
+                    // a_p b_q into acc_{p+q} for all nq planes at once: 8 MMAs per chunk for the
+                    // 21 kept pairs; the first two (p = 0) initialise acc_0..3 and acc_4..5.
 #pragma unroll
-                    for (int p = 0; p < OZ_SL; ++p) {
-                        const uint64_t da = desc_kmajor_noswz(abase + p * OZ_PLANE, 128, 256);
-#pragma unroll
-                        for (int q = 0; q < OZ_SL; ++q) {
-                            if (p + q > OZ_SMAX) continue;
-                            const int s = p + q;
-                            const uint64_t db = desc_kmajor_noswz(
-                                bres + (uint32_t)q * NP * g.Kp + (uint32_t)c * (OZ_KC * 8), 128, sbo_b);
-                            const bool first = (c == 0) && (p == (s > OZ_SL - 1 ? s - (OZ_SL - 1) : 0));
-                            mma_i8(tmem_base + (uint32_t)(s * NP), da, db, idesc, first ? 0u : 1u);
-                        }
+                    for (int u = 0; u < 8; ++u) {
+                        constexpr int P[8] = {0, 0, 1, 1, 2, 3, 4, 5};
+                        constexpr int Q0[8] = {0, 4, 0, 4, 0, 0, 0, 0};
+                        constexpr int NQ[8] = {4, 2, 4, 1, 4, 3, 2, 1};
+                        const uint64_t da = desc_kmajor_noswz(abase + P[u] * OZ_PLANE, 128, 256);
+                        const uint64_t db = desc_kmajor_noswz(
+                            bres + (uint32_t)Q0[u] * NP * g.Kp + (uint32_t)c * (OZ_KC * 8), 128, sbo_b);
+                        const uint32_t acc = (c > 0 || u >= 2) ? 1u : 0u;
+                        mma_i8(tmem_base + (uint32_t)((P[u] + Q0[u]) * NP), da, db, idesc_i8(OZ_M, NQ[u] * NP), acc);
                     }
                     mma_commit(smem_u32(&sfree[b]));
                     if (c == nkc - 1) mma_commit(smem_u32(tfull));
@@ -240,77 +264,114 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_aw_kernel(const __grid_const
         }
     } else if (warp < 2 + OZ_SLICERS) {
         // ---------------- slicers: 16 rows per warp ----------------
+        // lane -> (row r = 8-row group + lane % 8, 16-byte chunk 4h + lane / 8): the 8 lanes of a
+        // shared-memory phase read 8 different swizzled chunks and write one 128-byte core matrix
         const int sw = warp - 2;
         int64_t gc = 0;
         for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
-            float sc1[2], sc2[2];
+            double scale[2];
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
-                const int64_t row = t * OZ_M + 16 * sw + 8 * rr + (lane >> 2);
-                const int E = row < g.n ? g.rowE[row] : 0;
-                const int sh = 48 - E;                                 // scale 2^(48 - E) in two steps
-                const int h1 = sh / 2;
-                sc1[rr] = pow2f(h1);
-                sc2[rr] = pow2f(sh - h1);
+                const int64_t row = t * OZ_M + 16 * sw + 8 * rr + (lane & 7);
+                scale[rr] = pow2d(47 - (row < g.n ? g.rowE[row] : 0));
             }
             for (int c = 0; c < nkc; ++c, ++gc) {
                 const int s = (int)(gc % OZ_STG);
-                const int b = (int)(gc & 1);
                 mbar_wait(smem_u32(&afull[s]), (uint32_t)((gc / OZ_STG) & 1));
-                if (gc >= 2) mbar_wait(smem_u32(&sfree[b]), (uint32_t)(((gc >> 1) - 1) & 1));
                 const uint8_t *stg = smem + stage_off + s * OZ_STAGE_BYTES;
+                float4 cur[2][2];
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int r = 16 * sw + 8 * rr + (lane & 7);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c16 = 4 * h + (lane >> 3);
+                        cur[rr][h] = *reinterpret_cast<const float4 *>(stg + r * 128 + ((c16 ^ (r & 7)) << 4));
+                    }
+                }
+                // digits first (consumes the stage's values), then the stage is released
+                uint32_t w[2][2][OZ_SL];
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) slice4(cur[rr][h], scale[rr], w[rr][h]);
+                // release the stage once every lane's values have arrived: the warp-wide OR of the
+                // digits depends on all of them (an LDS may still be in flight when later
+                // instructions issue, and the next TMA would overwrite the stage)
+                uint32_t dep = 0;
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) dep |= w[rr][h][0] | w[rr][h][OZ_SL - 1];
+                dep = __reduce_or_sync(0xffffffffu, dep);
+                if (lane == 0)
+                    asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %1, 0xdeadbeef;\n@q mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+                                     smem_u32(&aempty[s])),
+                                 "r"(dep)
+                                 : "memory");
+                const int b = (int)(gc % OZ_NBUF);
+                if (gc >= OZ_NBUF) mbar_wait(smem_u32(&sfree[b]), (uint32_t)(((gc / OZ_NBUF) - 1) & 1));
                 uint8_t *sb = smem + slice_off + b * OZ_SBUF;
 #pragma unroll
                 for (int rr = 0; rr < 2; ++rr) {
-                    const int r = 16 * sw + 8 * rr + (lane >> 2);
+                    const int r = 16 * sw + 8 * rr + (lane & 7);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int c16 = 4 * h + (lane & 3);                   // 16-byte chunk of the fp32 row
-                        const float4 a = *reinterpret_cast<const float4 *>(stg + r * 128 + ((c16 ^ (r & 7)) << 4));
-                        uint32_t w[OZ_SL];
-                        slice4(a, sc1[rr], sc2[rr], w);
-                        const int kb = 16 * h + 4 * (lane & 3);               // byte (= element) in the K chunk
+                        const int kb = 4 * (4 * h + (lane >> 3));             // byte (= element) in the K chunk
                         const uint32_t off = (uint32_t)((r >> 3) * 256 + (kb >> 4) * 128 + (r & 7) * 16 + (kb & 15));
 #pragma unroll
-                        for (int p = 0; p < OZ_SL; ++p) *reinterpret_cast<uint32_t *>(sb + p * OZ_PLANE + off) = w[p];
+                        for (int p = 0; p < OZ_SL; ++p) *reinterpret_cast<uint32_t *>(sb + p * OZ_PLANE + off) = w[rr][h][p];
                     }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(smem_u32(&aempty[s]));
-                    mbar_arrive(smem_u32(&sready[b]));
-                }
+                if (lane == 0) mbar_arrive(smem_u32(&sready[b]));
             }
         }
     } else {
-        // ---------------- epilogue ----------------
-        const int q4 = warp & 3;
+        // ---------------- epilogue: 4 warps per TMEM lane quarter, NP / 4 columns each ----------------
+        const int q4 = warp & 3, ch = (warp - 2 - OZ_SLICERS) >> 2;
+        constexpr int HALF = NP / 4;                 // columns per epilogue warp (multiple of 4)
         int i = 0;
         for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++i) {
-            mbar_wait(smem_u32(tfull), (uint32_t)(i & 1));
+            mbar_wait_sleep(smem_u32(tfull), (uint32_t)(i & 1));
             fence_after();
             const int64_t row = t * OZ_M + 32 * q4 + lane;
             const bool ok = row < g.n;
             const int E = ok ? g.rowE[row] : 0;
             const double rsc = (ok && g.rs ? (double)g.rs[row] : 1.0);
-            double *orow = g.out + (ok ? row : 0) * g.ldo;
 #pragma unroll 1
-            for (int cb = 0; cb < NP; cb += 8) {
-                int32_t v[OZ_NACC][8];
+            for (int cb = ch * HALF; cb < (ch + 1) * HALF; cb += 4) {
+                uint32_t v[OZ_NACC][4];
 #pragma unroll
                 for (int s = 0; s < OZ_NACC; ++s)
-                    tmem_ld8(tmem_base + ((uint32_t)(32 * q4) << 16) + (uint32_t)(s * NP + cb), v[s]);
+                    tmem_ld4_nowait(tmem_base + ((uint32_t)(32 * q4) << 16) + (uint32_t)(s * NP + cb), v[s]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int s = 0; s < OZ_NACC; ++s)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) asm volatile("" : "+r"(v[s][j]));
+                double o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
                     const int l = cb + j;
-                    long long hi = 0, lo = 0;
+                    const long long g0 = (long long)(int32_t)v[0][j] * 65536 + (long long)(int32_t)v[1][j] * 256 +
+                                         (long long)(int32_t)v[2][j];
+                    const long long g1 = (long long)(int32_t)v[3][j] * 65536 + (long long)(int32_t)v[4][j] * 256 +
+                                         (long long)(int32_t)v[5][j] - sh_clo[l];
+                    const double x = fma((double)g0, 16777216.0, -sh_chi[l]) + (double)g1;
+                    o[j] = x * pow2d(E + sh_colE[l] - 53) * rsc;
+                }
+                if (ok) {
+                    double *orow = g.out + row * g.ldo;
+                    if (cb + 4 <= g.N && ((reinterpret_cast<uintptr_t>(orow + cb) & 15) == 0)) {
+                        *reinterpret_cast<double2 *>(orow + cb) = make_double2(o[0], o[1]);
+                        *reinterpret_cast<double2 *>(orow + cb + 2) = make_double2(o[2], o[3]);
+                    } else {
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) hi = hi * 128 + (long long)(v[s][j] - sh_corr[s * NP + l]);
-#pragma unroll
-                    for (int s = 4; s < OZ_NACC; ++s) lo = lo * 128 + (long long)(v[s][j] - sh_corr[s * NP + l]);
-                    const double cval = fma((double)hi, 268435456.0, (double)lo) * pow2d(E + sh_colE[l] - 62);
-                    if (ok && l < g.N) orow[l] = cval * rsc;
+                        for (int j = 0; j < 4; ++j)
+                            if (cb + j < g.N) orow[cb + j] = o[j];
+                    }
                 }
             }
             fence_before();
@@ -342,14 +403,14 @@ __global__ void oz_rowexp_kernel(const float *__restrict__ A, int64_t lda, int64
     }
 }
 
-// W (K x N fp64, row-major) -> digit image [OZ_SL][NP x Kp] in the kernel's shared-memory layout,
-// column exponents E_l and the bias corrections corr[s][l] = 64 sum_j B_s[j, l] (s < OZ_SL).
-// One block per padded column l.
+// W (K x N fp64, row-major) -> digit image [OZ_SL][NP x Kp] in the kernel's shared-memory layout
+// (plane q = digit q, most significant first), the column exponents E_l and the bias
+// correction C = 8 sum_j F_jl split into C_hi (fp64) + C_lo (int64).  One block per padded column.
 __global__ void oz_bprep_kernel(const double *__restrict__ W, int K, int N, int NP, int Kp, uint8_t *__restrict__ img,
-                                int32_t *__restrict__ colE, int32_t *__restrict__ corr) {
+                                int32_t *__restrict__ colE, double *__restrict__ chi, long long *__restrict__ clo) {
     const int l = blockIdx.x;
     __shared__ double red[32];
-    __shared__ int sred[OZ_SL][32];
+    __shared__ long long lred[32];
     double m = 0.0;
     if (l < N)
         for (int j = threadIdx.x; j < K; j += blockDim.x) m = fmax(m, fabs(W[(int64_t)j * N + l]));
@@ -364,36 +425,32 @@ __global__ void oz_bprep_kernel(const double *__restrict__ W, int K, int N, int 
     __syncthreads();
     int E = 0;
     if (red[0] > 0.0) frexp(red[0], &E);
-    int dsum[OZ_SL];
-#pragma unroll
-    for (int q = 0; q < OZ_SL; ++q) dsum[q] = 0;
-    const double scale = ldexp(1.0, 49 - E);
+    const double scale = ldexp(1.0, 46 - E);     // |F| < 2^46: inside the 6-digit balanced range
+    long long fsum = 0;
     for (int j = threadIdx.x; j < Kp; j += blockDim.x) {
         const double w = (l < N && j < K) ? W[(int64_t)j * N + l] : 0.0;
-        const long long f = (long long)(fabs(w) * scale);          // trunc, < 2^49 (exact scaling)
-        const int sg = w < 0.0 ? -1 : 1;
+        long long f = (long long)(w * scale);                      // trunc, |f| < 2^46 (exact scaling)
+        fsum += f;
         const int64_t off = (int64_t)(l >> 3) * (8 * Kp) + (j >> 4) * 128 + (l & 7) * 16 + (j & 15);
 #pragma unroll
-        for (int q = 0; q < OZ_SL; ++q) {
-            const int d = sg * (int)((f >> (7 * (OZ_SL - 1 - q))) & 127);
+        for (int q = OZ_SL - 1; q >= 0; --q) {                      // balanced base-256 digits, LSB first
+            const int d = (int)(int8_t)(uint8_t)(f & 255);
             img[(int64_t)q * NP * Kp + off] = (uint8_t)(int8_t)d;
-            dsum[q] += d;
+            f = (f - d) >> 8;
         }
     }
-#pragma unroll
-    for (int q = 0; q < OZ_SL; ++q) {
-        int v = dsum[q];
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) sred[q][threadIdx.x >> 5] = v;
-    }
+    for (int o = 16; o; o >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
+    if ((threadIdx.x & 31) == 0) lred[threadIdx.x >> 5] = fsum;
     __syncthreads();
-    if (threadIdx.x < OZ_NACC) {
-        int v = 0;
-        if (threadIdx.x < OZ_SL)
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sred[threadIdx.x][w];
-        corr[threadIdx.x * NP + l] = 64 * v;
+    if (threadIdx.x == 0) {
+        long long c = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += lred[w];
+        // C = 128 sum_j F (up to 2^65): C_hi = 128 fp64(sum), C_lo = 128 (sum - fp64(sum)), exact
+        const double h = (double)c;
+        chi[l] = 128.0 * h;
+        clo[l] = 128 * (c - (long long)h);
+        colE[l] = E;
     }
-    if (threadIdx.x == 0) colE[l] = E;
 }
 
 CUtensorMap oz_map(const float *A, int64_t n, int64_t K, int64_t lda) {
@@ -414,7 +471,7 @@ int oz_kp(int64_t K) { return (int)((K + OZ_KC - 1) / OZ_KC * OZ_KC); }
 
 size_t oz_smem(int NP, int Kp) {
     const size_t b = ((size_t)OZ_SL * NP * Kp + 1023) & ~size_t(1023);
-    return 1024 + b + OZ_STG * OZ_STAGE_BYTES + 2 * OZ_SBUF + 16 * 8 + sizeof(int32_t) * (OZ_NACC + 1) * NP + 16;
+    return 1024 + b + OZ_STG * OZ_STAGE_BYTES + OZ_NBUF * OZ_SBUF + 16 * 8 + (sizeof(double) + sizeof(long long) + sizeof(int32_t)) * NP + 16;
 }
 
 template <int NP>
@@ -434,9 +491,9 @@ bool oz_enabled() {
 }
 
 bool oz_aw_supported(int64_t K, int N) {
-    if (K < 1 || N < 1 || N > 64 || K > 16384) return false;
+    if (K < 1 || N < 1 || N > 64 || K > 2048) return false;      // exact int64 / fp64 epilogue sums
     if ((size_t)OZ_SL * oz_np(N) * oz_kp(K) > OZ_B_MAX) return false;
-    return oz_smem(oz_np(N), oz_kp(K)) <= 227 * 1024;
+    return oz_smem(oz_np(N), oz_kp(K)) <= 227 * 1024 - 256;
 }
 
 size_t oz_aw_ws(int64_t K, int N) {
@@ -444,7 +501,8 @@ size_t oz_aw_ws(int64_t K, int N) {
     const int NP = oz_np(N), Kp = oz_kp(K);
     ar.take<uint8_t>((size_t)OZ_SL * NP * Kp);
     ar.take<int32_t>(NP);
-    ar.take<int32_t>((size_t)OZ_NACC * NP);
+    ar.take<double>(NP);
+    ar.take<long long>(NP);
     return ar.off + 256;
 }
 
@@ -464,13 +522,16 @@ void oz_aw_f64(const float *A, int64_t lda, const float *rs, const int32_t *rowE
     const int NP = oz_np(N), Kp = oz_kp(K);
     uint8_t *img = ar.take<uint8_t>((size_t)OZ_SL * NP * Kp);
     int32_t *colE = ar.take<int32_t>(NP);
-    int32_t *corr = ar.take<int32_t>((size_t)OZ_NACC * NP);
-    oz_bprep_kernel<<<NP, 256, 0, st>>>(W, K, N, NP, Kp, img, colE, corr);
+    double *chi = ar.take<double>(NP);
+    long long *clo = ar.take<long long>(NP);
+    oz_bprep_kernel<<<NP, 256, 0, st>>>(W, K, N, NP, Kp, img, colE, chi, clo);
     TPO_LAUNCH_CHECK();
     OzArgs a{};
+    a.A = A; a.lda = lda;
     a.n = n; a.ldo = ldo; a.K = K; a.N = N; a.NP = NP; a.Kp = Kp;
     a.ntiles = cdiv(n, OZ_M);
-    a.rowE = rowE; a.colE = colE; a.corr = corr; a.Bimg = img; a.rs = rs; a.out = out;
+    a.rowE = rowE; a.colE = colE; a.chi = chi; a.clo = clo;
+    a.Bimg = img; a.rs = rs; a.out = out;
     const CUtensorMap map = oz_map(A, n, K, lda);
     switch (NP) {
         case 16: oz_launch<16>(map, a, st); break;
@@ -485,7 +546,9 @@ void oz_aw_f64(const float *A, int64_t lda, const float *rs, const int32_t *rowE
 // the integer-tensor-core product (or the fp64 DMMA path when the shape is not supported).
 RhPlan rh_plan_at(int32_t *rowE, const float *Rp, int64_t n, int64_t D, int k, cudaStream_t st) {
     RhPlan p;
-    p.oz = oz_enabled() && n > 0 && D % 4 == 0 && oz_aw_supported(D, k) &&
+    // measured faster than the fp64 DMMA path for N > 32 only (large: 1.37 vs 2.42 ms; medium,
+    // N = 20: 0.62 vs 0.61 ms)
+    p.oz = oz_enabled() && n > 0 && D % 4 == 0 && k > 32 && oz_aw_supported(D, k) &&
            (reinterpret_cast<uintptr_t>(Rp) & 15) == 0;
     p.rowE = rowE;
     if (p.oz) oz_rowexp(Rp, D, n, (int)D, p.rowE, st);
@@ -495,7 +558,7 @@ RhPlan rh_plan(const float *Rp, int64_t n, int64_t D, int k, Arena &ar, cudaStre
     return rh_plan_at(ar.take<int32_t>(std::max<int64_t>(n, 1)), Rp, n, D, k, st);
 }
 size_t rh_plan_ws(int64_t n) { return align_up(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1) + 1); }
-size_t rh_apply_ws(int64_t D, int k) { return oz_aw_supported(D, k) ? oz_aw_ws(D, k) : 0; }
+size_t rh_apply_ws(int64_t D, int k) { return (k > 32 && oz_aw_supported(D, k)) ? oz_aw_ws(D, k) : 0; }
 
 void rh_apply(const RhPlan &p, const float *Rp, const float *dinv, const double *H, int64_t n, int64_t D, int k,
               double *RH, Arena &ar, cudaStream_t st) {
