@@ -543,7 +543,8 @@ void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, in
         scale_cols_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D, k, sd, w);
         TPO_LAUNCH_CHECK();
         G64 = ar.take<double>((size_t)n * k);
-        tsgemm_AW_f64(Rp, D, dinv, w, n, D, k, G64, k, st);
+        const RhPlan gp = rh_plan(Rp, n, D, k, ar, st);     // integer tensor cores when k > 32
+        rh_apply(gp, Rp, dinv, w, n, D, k, G64, ar, st);
     }
     cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
     TPO_LAUNCH_CHECK();
@@ -619,6 +620,7 @@ size_t topk_eig_ws_bytes(int64_t n, int64_t D, int32_t k, int32_t mode, int32_t 
     if (mode == TPO_EIG_HALKO) s += 3 * align_up(sizeof(double) * n * bh) + tsgemm_ws(n, D, bh) + tsgemm_ws(n, bh, bh);
     s += dgemm_ws(std::max(n, D), std::max(b, bh) + 1, 0) + 2 * align_up(sizeof(double) * (std::max(b, bh) + 1) * (std::max(b, bh) + 1));
     s += ts_atb_ws((int)k, (int)k);                      // the polish Gram Gamma^T Gamma (fp64 tensor path)
+    s += rh_plan_ws(n) + rh_apply_ws(D, k);              // Gamma = R Psi Sigma^-1 on the integer tensor cores
     return s + 64 * 256;
 }
 
