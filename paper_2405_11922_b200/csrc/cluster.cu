@@ -557,8 +557,10 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     ar.take<double>(nb * k * k);
     ar.take<int64_t>(nb * k);
     ar.take<char>(rh_plan_ws(n));
-    return ar.off + std::max(std::max(std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)), ts_atb_ws(k, k)),
-                             rh_apply_ws(D, k)) + 4096;
+    size_t inner = std::max(std::max(std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)), ts_atb_ws(k, k)),
+                            rh_apply_ws(D, k));
+    if (oz_assign_supported(k)) inner = std::max(inner, oz_assign_ws(n, k));
+    return ar.off + inner + 4096;
 }
 
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
@@ -610,6 +612,10 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         }
     }
     // Alg. 3
+    ar.off = mark;
+    const bool oa_on = oz_assign_supported(k);
+    OzAssign oa;
+    if (oa_on) oa = oz_assign_prepare(U, n, k, ar, st);      // Ups is fixed during Alg. 3
     NciState s{flags, flags + 1, flags + 2};
     TPO_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 8, st));
     fill_i32<<<cdiv(n, 256), 256, 0, st>>>(labels, n, -1);
@@ -637,7 +643,9 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
             TPO_LAUNCH_CHECK();
             continue;
         }
-        if (ts64_enabled() && k > 32 && k <= 104) {
+        if (oa_on) {
+            oz_assign(oa, U, Phi, labels, s.changed, s.done, st);
+        } else if (ts64_enabled() && k > 32 && k <= 104) {
             ts_assign(U, Phi, n, k, labels, s.changed, s.done, st);
         } else {
             if (k <= 16)

@@ -567,4 +567,359 @@ void rh_apply(const RhPlan &p, const float *Rp, const float *dinv, const double 
     else tsgemm_AW_f64(Rp, D, dinv, H, n, D, k, RH, k, st);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Alg. 3 assignment on the integer tensor cores (Eq. ell-ast; R13 certified):
+//      l*_i = argmax_l sum_a Ups[i,a] Phi[a,l]
+// Ups and Phi are nonnegative, so both are cut into UNSIGNED byte digits without a bias: row i of
+// Ups -> A'_ia = floor(Ups_ia 2^(48-E_i)) (6 bytes; computed ONCE per Alg. 3, Ups is fixed while
+// Phi changes), column l of Phi -> B'_al = floor(Phi_al 2^(48-E_l)) (per iteration).  The kept
+// digit pairs (p + q <= 5) give c_il = 2^(E_i+E_l-56) [acc_0..2 2^24 + acc_3..5] <= the exact
+// score, below it by at most U_il = k 2^(E_i+E_l) (2^-45 + k 2^-52) (dropped pairs, truncation,
+// and the slack that keeps the certified argmax equal to R13's sequential-fma argmax).  A row's
+// argmax is accepted when its best computed score exceeds every other c_il + U_il; otherwise the
+// row is rescored with R13's sequential fma from Ups and Phi (rare).  Labels are the oracle's.
+//   warp 0     Phi's digit image once (bulk copy, resident), then per row tile of 128 its precomputed
+//              Ups digit planes (one bulk copy) into a 3-slot ring
+//   warp 1     MMA issuer: per 32-wide K chunk the 8 N-concatenated kind::i8 MMAs (u8 x u8 -> s32)
+//   warps 2-17 epilogue: 4 per TMEM lane quarter (a quarter of the columns each), per row a running
+//              certified top-2, merged in column order
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int OA_NBUF = 3;
+constexpr int OA_EPI = 16;                // 4 per TMEM lane quarter (column quarters)
+constexpr int OA_THREADS = 32 * (2 + OA_EPI);
+
+struct OaArgs {
+    int64_t n;
+    int k, NP, Kp;
+    int64_t ntiles;
+    const uint8_t *Ud;       // [ntiles][Kp/32][6][4 KB] digit planes of Ups
+    const int32_t *rowE;     // [n]
+    const uint8_t *Bimg;     // [6][NP x Kp] digit image of Phi
+    const int32_t *colE;     // [NP]
+    const double *U, *Phi;   // fp64 (R13 rescoring)
+    int32_t *labels, *changed;
+    const int32_t *done;
+};
+
+// (once per Alg. 3) row exponents E_i and the Ups digit planes in the MMA layout.  Half a warp
+// per row (Kp <= 64: 16 lanes x 4 columns), two rows per warp; coalesced 32-byte reads.
+__global__ void oa_prep_kernel(const double *__restrict__ U, int64_t n, int k, int Kp, int32_t *__restrict__ rowE,
+                               uint8_t *__restrict__ Ud) {
+    const int64_t row = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 2 + ((threadIdx.x >> 4) & 1);
+    const int hl = threadIdx.x & 15;
+    const int64_t ntiles = (n + OZ_M - 1) / OZ_M;
+    if (row >= ntiles * OZ_M) return;                    // uniform per half warp
+    const int a0 = 4 * hl;
+    double u[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) u[e] = (row < n && a0 + e < k) ? U[row * k + a0 + e] : 0.0;
+    double m = fmax(fmax(u[0], u[1]), fmax(u[2], u[3]));
+    for (int o = 8; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int E = 0;
+    if (m > 0.0) frexp(m, &E);
+    if (hl == 0 && row < n) rowE[row] = E;
+    if (a0 >= Kp) return;
+    const double scale = pow2d(48 - E);
+    uint32_t L[4], H[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const double z = __fma_rz(u[e], scale, 4503599627370496.0);    // 2^52 + floor(Ups 2^(48-E))
+        const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
+        L[e] = (uint32_t)zb;
+        H[e] = (uint32_t)(zb >> 32) & 0xFFFFu;
+    }
+    uint32_t w[OZ_SL];
+    const uint32_t t0 = __byte_perm(L[0], L[1], 0x5140), t1 = __byte_perm(L[2], L[3], 0x5140);
+    const uint32_t u0 = __byte_perm(L[0], L[1], 0x7362), u1 = __byte_perm(L[2], L[3], 0x7362);
+    w[5] = __byte_perm(t0, t1, 0x5410);
+    w[4] = __byte_perm(t0, t1, 0x7632);
+    w[3] = __byte_perm(u0, u1, 0x5410);
+    w[2] = __byte_perm(u0, u1, 0x7632);
+    const uint32_t h0 = __byte_perm(H[0], H[1], 0x5140), h1 = __byte_perm(H[2], H[3], 0x5140);
+    w[1] = __byte_perm(h0, h1, 0x5410);
+    w[0] = __byte_perm(h0, h1, 0x7632);
+    const int64_t t = row / OZ_M;
+    const int r = (int)(row - t * OZ_M), c = a0 / OZ_KC, kb = a0 % OZ_KC;
+    uint8_t *base = Ud + ((t * (Kp / OZ_KC) + c) * OZ_SL) * (int64_t)OZ_PLANE;
+    const uint32_t off = (uint32_t)((r >> 3) * 256 + (kb >> 4) * 128 + (r & 7) * 16 + (kb & 15));
+#pragma unroll
+    for (int p = 0; p < OZ_SL; ++p) *reinterpret_cast<uint32_t *>(base + p * OZ_PLANE + off) = w[p];
+}
+
+// Phi (k x k fp64, Phi[a][l]) -> unsigned digit image [6][NP x Kp] (row l = column of Phi), E_l
+__global__ void oa_phidigits_kernel(const double *__restrict__ Phi, int k, int NP, int Kp, uint8_t *__restrict__ img,
+                                    int32_t *__restrict__ colE, const int32_t *__restrict__ done) {
+    if (*done) return;
+    const int l = blockIdx.x;
+    __shared__ double red[32];
+    double m = 0.0;
+    if (l < k)
+        for (int a = threadIdx.x; a < k; a += blockDim.x) m = fmax(m, Phi[(int64_t)a * k + l]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+        red[0] = v;
+    }
+    __syncthreads();
+    int E = 0;
+    if (red[0] > 0.0) frexp(red[0], &E);
+    const double scale = ldexp(1.0, 48 - E);
+    for (int a = threadIdx.x; a < Kp; a += blockDim.x) {
+        const double v = (l < k && a < k) ? Phi[(int64_t)a * k + l] : 0.0;
+        const unsigned long long f = (unsigned long long)(v * scale);     // floor (v >= 0), < 2^48
+        const int64_t off = (int64_t)(l >> 3) * (8 * Kp) + (a >> 4) * 128 + (l & 7) * 16 + (a & 15);
+#pragma unroll
+        for (int q = 0; q < OZ_SL; ++q) img[(int64_t)q * NP * Kp + off] = (uint8_t)((f >> (8 * (OZ_SL - 1 - q))) & 255);
+    }
+    if (threadIdx.x == 0) colE[l] = E;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(OA_THREADS, 1) oa_assign_kernel(OaArgs g) {
+    if (*g.done) return;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    const int nkc = g.Kp / OZ_KC;
+    const uint32_t bbytes = (uint32_t)OZ_SL * NP * g.Kp;
+    const uint32_t tbytes = (uint32_t)nkc * OZ_SBUF;                 // one tile's Ups planes
+    const uint32_t ring_off = (bbytes + 127) & ~127u;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ring_off + OA_NBUF * tbytes);
+    uint64_t *bfull = bars, *afull = bars + 1, *afree = afull + OA_NBUF, *tfull = afree + OA_NBUF, *tempty = tfull + 1;
+    double *sh_c1 = reinterpret_cast<double *>(tempty + 1);         // [4 column quarters][128 rows]
+    double *sh_cu = sh_c1 + 4 * OZ_M, *sh_w2 = sh_cu + 4 * OZ_M;
+    int32_t *sh_i1 = reinterpret_cast<int32_t *>(sh_w2 + 4 * OZ_M);
+    int32_t *sh_colE = sh_i1 + 4 * OZ_M;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sh_colE + NP);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t TMEM_COLS = (OZ_NACC * NP <= 128) ? 128 : (OZ_NACC * NP <= 256 ? 256 : 512);
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(bfull), 1);
+        for (int b = 0; b < OA_NBUF; ++b) {
+            mbar_init(smem_u32(&afull[b]), 1);
+            mbar_init(smem_u32(&afree[b]), 1);
+        }
+        mbar_init(smem_u32(tfull), 1);
+        mbar_init(smem_u32(tempty), OA_EPI);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < NP; i += blockDim.x) sh_colE[i] = g.colE[i];
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(smem_u32(bfull), bbytes);
+            for (uint32_t o = 0; o < bbytes; o += 32768)
+                bulk_g2s(smem_u32(smem) + o, g.Bimg + o, std::min<uint32_t>(32768, bbytes - o), smem_u32(bfull));
+            int j = 0;
+            for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++j) {
+                const int b = j % OA_NBUF;
+                if (j >= OA_NBUF) mbar_wait(smem_u32(&afree[b]), (uint32_t)(((j / OA_NBUF) - 1) & 1));
+                mbar_expect_tx(smem_u32(&afull[b]), tbytes);
+                bulk_g2s(smem_u32(smem + ring_off + b * tbytes), g.Ud + t * (int64_t)tbytes, tbytes, smem_u32(&afull[b]));
+            }
+        }
+    } else if (warp == 1) {
+        mbar_wait(smem_u32(bfull), 0);
+        const uint32_t bres = smem_u32(smem);
+        const uint32_t sbo_b = 8u * (uint32_t)g.Kp;
+        int j = 0;
+        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++j) {
+            const int b = j % OA_NBUF;
+            if (j > 0) mbar_wait(smem_u32(tempty), (uint32_t)((j - 1) & 1));
+            mbar_wait(smem_u32(&afull[b]), (uint32_t)((j / OA_NBUF) & 1));
+            fence_after();
+            if (lane == 0) {
+                for (int c = 0; c < nkc; ++c) {
+                    const uint32_t abase = smem_u32(smem + ring_off + b * tbytes + c * OZ_SBUF);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        constexpr int P[8] = {0, 0, 1, 1, 2, 3, 4, 5};
+                        constexpr int Q0[8] = {0, 4, 0, 4, 0, 0, 0, 0};
+                        constexpr int NQ[8] = {4, 2, 4, 1, 4, 3, 2, 1};
+                        const uint64_t da = desc_kmajor_noswz(abase + P[u] * OZ_PLANE, 128, 256);
+                        const uint64_t db = desc_kmajor_noswz(
+                            bres + (uint32_t)Q0[u] * NP * g.Kp + (uint32_t)c * (OZ_KC * 8), 128, sbo_b);
+                        const uint32_t acc = (c > 0 || u >= 2) ? 1u : 0u;
+                        // u8 x u8 (both digit sets unsigned)
+                        const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) |
+                                               ((uint32_t)((NQ[u] * NP) >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
+                        mma_i8(tmem_base + (uint32_t)((P[u] + Q0[u]) * NP), da, db, idesc, acc);
+                    }
+                }
+                mma_commit(smem_u32(&afree[b]));
+                mma_commit(smem_u32(tfull));
+            }
+            __syncwarp();
+        }
+    } else {
+        // 4 warps per lane quarter, NP / 4 columns each; per row a local certified top-2, merged
+        // in column order by the quarter's first warp (ties keep the smallest index)
+        const int q4 = warp & 3, ch = (warp - 2) >> 2;
+        constexpr int CW = NP / 4;
+        const double kf = (double)g.k;
+        const double urel = kf * (2.8421709430404007e-14 + kf * 2.220446049250313e-16);   // k (2^-45 + k 2^-52)
+        bool changed = false;
+        int j = 0;
+        for (int64_t t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++j) {
+            mbar_wait_sleep(smem_u32(tfull), (uint32_t)(j & 1));
+            fence_after();
+            const int rloc = 32 * q4 + lane;
+            const int64_t row = t * OZ_M + rloc;
+            const bool ok = row < g.n;
+            const int E = ok ? g.rowE[row] : 0;
+            double c1 = -1.0, w2 = -1.0, u1 = 0.0;      // best computed score, max over others of c + U
+            int i1 = -1;
+#pragma unroll 1
+            for (int cb = ch * CW; cb < (ch + 1) * CW; cb += 4) {
+                uint32_t v[OZ_NACC][4];
+#pragma unroll
+                for (int s = 0; s < OZ_NACC; ++s)
+                    tmem_ld4_nowait(tmem_base + ((uint32_t)(32 * q4) << 16) + (uint32_t)(s * NP + cb), v[s]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int s = 0; s < OZ_NACC; ++s)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) asm volatile("" : "+r"(v[s][jj]));
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int l = cb + jj;
+                    if (l >= g.k) break;
+                    const long long g0 = (long long)v[0][jj] * 65536 + (long long)v[1][jj] * 256 + (long long)v[2][jj];
+                    const long long g1 = (long long)v[3][jj] * 65536 + (long long)v[4][jj] * 256 + (long long)v[5][jj];
+                    const double c = fma((double)g0, 16777216.0, (double)g1) * pow2d(E + sh_colE[l] - 56);
+                    const double U = urel * pow2d(E + sh_colE[l]);
+                    if (i1 < 0 || c > c1) {
+                        if (i1 >= 0) w2 = fmax(w2, c1 + u1);
+                        c1 = c; i1 = l; u1 = U;
+                    } else {
+                        w2 = fmax(w2, c + U);
+                    }
+                }
+            }
+            fence_before();
+            sh_c1[ch * OZ_M + rloc] = c1;
+            sh_cu[ch * OZ_M + rloc] = i1 >= 0 ? c1 + u1 : -1.0;
+            sh_w2[ch * OZ_M + rloc] = w2;
+            sh_i1[ch * OZ_M + rloc] = i1;
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + q4) : "memory");     // the quarter's 4 warps
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(tempty));      // TMEM may be refilled; rescoring uses fp64
+            if (ch == 0 && ok) {
+                double bc = -1.0, bw = -1.0;
+                int bi = -1, bq = -1;
+                for (int q = 0; q < 4; ++q) {
+                    const int qi = sh_i1[q * OZ_M + rloc];
+                    if (qi < 0) continue;
+                    const double qc = sh_c1[q * OZ_M + rloc];
+                    if (bi < 0 || qc > bc) { bc = qc; bi = qi; bq = q; }
+                }
+                for (int q = 0; q < 4; ++q) {
+                    if (sh_i1[q * OZ_M + rloc] < 0) continue;
+                    bw = fmax(bw, sh_w2[q * OZ_M + rloc]);
+                    if (q != bq) bw = fmax(bw, sh_cu[q * OZ_M + rloc]);
+                }
+                int lab = bi;
+                if (!(bc > bw)) {                               // not certified: R13 sequential fma
+                    const double *u = g.U + row * g.k;
+                    double best = 0.0;
+                    lab = 0;
+                    for (int l = 0; l < g.k; ++l) {
+                        double sc = 0.0;
+                        for (int a = 0; a < g.k; ++a) sc = fma(u[a], g.Phi[(int64_t)a * g.k + l], sc);
+                        if (l == 0 || sc > best) { best = sc; lab = l; }
+                    }
+                }
+                if (g.labels[row] != lab) changed = true;
+                g.labels[row] = lab;
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + q4) : "memory");     // merge read before the next tile's writes
+        }
+        if (__any_sync(0xffffffffu, changed) && lane == 0) *g.changed = 1;
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+size_t oa_smem(int NP, int Kp) {
+    return 128 + (((size_t)OZ_SL * NP * Kp + 127) & ~size_t(127)) + (size_t)OA_NBUF * (Kp / OZ_KC) * OZ_SBUF + 16 * 8 +
+           4 * OZ_M * (3 * sizeof(double) + sizeof(int32_t)) + sizeof(int32_t) * NP + 16;
+}
+
+template <int NP>
+void oa_launch(const OaArgs &a, cudaStream_t st) {
+    const size_t sm = oa_smem(NP, a.Kp);
+    TPO_CUDA(cudaFuncSetAttribute(oa_assign_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int grid = (int)std::min<int64_t>(a.ntiles, sm_count());
+    oa_assign_kernel<NP><<<grid, OA_THREADS, sm, st>>>(a);
+    TPO_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// k in (32, 64]: the Ups digit planes fit (3 tiles of 6 x 128 x Kp bytes + Phi's image)
+bool oz_assign_supported(int k) { return oz_enabled() && k > 32 && k <= 64 && oa_smem(oz_np(k), oz_kp(k)) <= 227 * 1024 - 256; }
+
+size_t oz_assign_ws(int64_t n, int k) {
+    const int NP = oz_np(k), Kp = oz_kp(k);
+    const int64_t ntiles = cdiv(std::max<int64_t>(n, 1), OZ_M);
+    Arena ar(nullptr, 0);
+    ar.take<uint8_t>((size_t)ntiles * (Kp / OZ_KC) * OZ_SBUF);
+    ar.take<int32_t>(std::max<int64_t>(n, 1));
+    ar.take<uint8_t>((size_t)OZ_SL * NP * Kp);
+    ar.take<int32_t>(NP);
+    return ar.off + 256;
+}
+
+OzAssign oz_assign_prepare(const double *U, int64_t n, int k, Arena &ar, cudaStream_t st) {
+    OzAssign p;
+    p.n = n;
+    p.k = k;
+    p.NP = oz_np(k);
+    p.Kp = oz_kp(k);
+    const int64_t ntiles = cdiv(std::max<int64_t>(n, 1), OZ_M);
+    p.Ud = ar.take<uint8_t>((size_t)ntiles * (p.Kp / OZ_KC) * OZ_SBUF);
+    p.rowE = ar.take<int32_t>(std::max<int64_t>(n, 1));
+    p.Bimg = ar.take<uint8_t>((size_t)OZ_SL * p.NP * p.Kp);
+    p.colE = ar.take<int32_t>(p.NP);
+    if (n == 0) return p;
+    const int64_t rows = ntiles * OZ_M;
+    oa_prep_kernel<<<cdiv(rows * 16, 256), 256, 0, st>>>(U, n, k, p.Kp, p.rowE, p.Ud);
+    TPO_LAUNCH_CHECK();
+    return p;
+}
+
+void oz_assign(const OzAssign &p, const double *U, const double *Phi, int32_t *labels, int32_t *changed,
+               const int32_t *done, cudaStream_t st) {
+    if (p.n == 0) return;
+    oa_phidigits_kernel<<<p.NP, 128, 0, st>>>(Phi, p.k, p.NP, p.Kp, p.Bimg, p.colE, done);
+    TPO_LAUNCH_CHECK();
+    OaArgs a{};
+    a.n = p.n; a.k = p.k; a.NP = p.NP; a.Kp = p.Kp;
+    a.ntiles = cdiv(p.n, OZ_M);
+    a.Ud = p.Ud; a.rowE = p.rowE; a.Bimg = p.Bimg; a.colE = p.colE;
+    a.U = U; a.Phi = Phi; a.labels = labels; a.changed = changed; a.done = done;
+    switch (p.NP) {
+        case 48: oa_launch<48>(a, st); break;
+        default: oa_launch<64>(a, st); break;
+    }
+}
+
 }  // namespace tpo

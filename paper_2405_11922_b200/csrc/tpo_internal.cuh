@@ -232,6 +232,19 @@ size_t oz_aw_ws(int64_t K, int N);
 void oz_rowexp(const float *A, int64_t lda, int64_t n, int K, int32_t *E, cudaStream_t st);
 void oz_aw_f64(const float *A, int64_t lda, const float *rs, const int32_t *rowE, const double *W, int64_t n, int K,
                int N, double *out, int64_t ldo, Arena &ar, cudaStream_t st);
+// Alg. 3 assignment on the integer tensor cores (oz.cu), 32 < k <= 64: Ups digits prepared once
+// per solve (Ups is fixed during Alg. 3), then one certified argmax per iteration.
+struct OzAssign {
+    int64_t n = 0;
+    int k = 0, NP = 0, Kp = 0;
+    uint8_t *Ud = nullptr, *Bimg = nullptr;
+    int32_t *rowE = nullptr, *colE = nullptr;
+};
+bool oz_assign_supported(int k);
+size_t oz_assign_ws(int64_t n, int k);
+OzAssign oz_assign_prepare(const double *U, int64_t n, int k, Arena &ar, cudaStream_t st);
+void oz_assign(const OzAssign &p, const double *U, const double *Phi, int32_t *labels, int32_t *changed,
+               const int32_t *done, cudaStream_t st);
 struct RhPlan {
     bool oz = false;
     int32_t *rowE = nullptr;

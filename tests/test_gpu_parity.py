@@ -412,6 +412,38 @@ def test_cluster_bit_exact_k_over_32(tpo, k, Tf, Tg):
     assert it == it_o and np.array_equal(lab.cpu().numpy(), lab_o)
 
 
+@pytest.mark.parametrize("k", [40, 50])
+def test_cluster_exact_ties_k_over_32(tpo, k):
+    """Exact ties in Alg. 3 on the k > 32 path (integer-tensor-core scores, certified argmax):
+    columns j and j+1 of Gamma and Psi are made identical with sigma_{j+1} = sigma_j, so the ONMF
+    keeps Upsilon's columns j and j+1 identical and every row whose best cluster is j ties.  Those
+    rows fail certification and are rescored with R13's sequential fma: ties -> smallest index,
+    labels bit-exact vs the oracle."""
+    g = planted_abg(6000, 4000, k, 48, deg=("poisson", 10.0), p_in=0.8, x=("gaussian", 1.0), alpha=0.5, T=2,
+                    seed=k + 3)
+    Rp, dinv = oracle_features_of(g)
+    Gmo, so, Pso, _ = O.topk(Rp, dinv, k)
+    for j in range(2, k - 1):                      # the first non-trivial pair whose tie is exercised
+        Gm32, Ps32 = Gmo.astype(np.float32).copy(), Pso.astype(np.float32).copy()
+        sj = np.array(so, np.float64).copy()
+        Gm32[:, j + 1] = Gm32[:, j]
+        Ps32[:, j + 1] = Ps32[:, j]
+        sj[j + 1] = sj[j]
+        lab_o, it_o, _ = O.cluster(Rp, dinv, Gm32, sj, Ps32, 3, 1)       # first assignment: Phi = I
+        if np.any(lab_o == j):
+            break
+    so = sj
+    assert np.any(lab_o == j)                      # the tie is exercised
+    assert not np.any(lab_o == j + 1)              # ... and resolved to the smaller index
+    args = (torch.from_numpy(Rp).cuda(), torch.from_numpy(dinv).cuda(), torch.from_numpy(Gm32).cuda(), so,
+            torch.from_numpy(Ps32).cuda(), 3)
+    lab, it = tpo.cluster(*args, 1)
+    assert it == it_o and np.array_equal(lab.cpu().numpy(), lab_o)
+    lab_o, it_o, _ = O.cluster(Rp, dinv, Gm32, so, Ps32, 3, 10)        # and through the later iterations
+    lab, it = tpo.cluster(*args, 10)
+    assert it == it_o and np.array_equal(lab.cpu().numpy(), lab_o)
+
+
 # ------------------------------------------------------------------------------------------
 # end to end
 # ------------------------------------------------------------------------------------------
