@@ -557,7 +557,8 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     ar.take<double>(nb * k * k);
     ar.take<int64_t>(nb * k);
     ar.take<char>(rh_plan_ws(n));
-    size_t inner = std::max(std::max(std::max(onmf_ws_bytes(n, D, k), dgemm_ws(k, k, n)), ts_atb_ws(k, k)),
+    size_t inner = std::max(std::max(std::max(onmf_ws_bytes(n, D, k), std::max(dgemm_ws(k, k, n), dgemm_ws(k, k, D))),
+                                     ts_atb_ws(k, k)),
                             rh_apply_ws(D, k));
     if (oz_assign_supported(k)) inner = std::max(inner, oz_assign_ws(n, k));
     return ar.off + inner + 4096;
@@ -597,8 +598,9 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         std::swap(H, Hn);
         rh_apply(rhp, Rp, dinv, H, n, D, k, RH, ar, st);
         ar.off = mark;
-        if (ts64_enabled() && k <= 104) ts_atb_f64(U, k, RH, k, n, k, k, M, ar, st);
-        else dgemm(true, k, k, n, 1.0, U, k, RH, k, 0.0, M, k, ar, st);
+        // M = Ups^T (R H) = (R^T Ups)^T H = RtU^T H: the same product by associativity, from the
+        // D x k factors instead of a pass over the n x k rows (RtU was formed from this Ups)
+        dgemm(true, k, k, D, 1.0, RtU, k, H, k, 0.0, M, k, ar, st);
         ar.off = mark;
         if (ts64_ups_enabled(k)) {
             ts_ups_update(U, RH, M, n, k, st);

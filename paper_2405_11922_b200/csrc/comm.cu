@@ -192,6 +192,7 @@ size_t run_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, in
     inner = std::max(inner, onmf_ws_bytes(n_p, D, k));
     inner = std::max(inner, rh_apply_ws(D, k));
     inner = std::max(inner, ts_atb_ws(k, k) + dgemm_ws(k, k, std::max<int64_t>(n_p, 1)));
+    inner = std::max(inner, dgemm_ws(k, k, D));
     inner = std::max(inner, align_up(sizeof(double) * (size_t)(4 * 2 * 148 * k)) + 4096);
     return s + inner + 64 * 256;
 }
@@ -310,8 +311,10 @@ void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, con
         ar.off = mark;
         rh_apply(rhp, Rp, dinv, H, n_p, D, k, RH, ar, st);
         ar.off = mark;
-        atb(U, RH, M);
-        allreduce(M, (size_t)k * k);
+        // M = Ups^T R H = RtU^T H (RtU is already the all-reduced global product): no pass over
+        // the rows and no all-reduce
+        dgemm(true, k, k, D, 1.0, RtU, k, H, k, 0.0, M, k, ar, st);
+        ar.off = mark;
         onmf_u_update(U, RH, M, n_p, k, st);
     }
     // a9 (Alg. 3)
