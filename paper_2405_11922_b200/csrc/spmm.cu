@@ -238,9 +238,6 @@ struct SpmmArgs {
     // output is written in out_L-float4 groups of out_rows rows (out_L = d4: row-major)
     int64_t src_rows, out_rows;
     int out_L;
-    // column-range passes (row-major kernel): the earlier passes' partial sum of this output
-    // row (pass > 0; read from `out` itself before it is overwritten), else null
-    const float4 *acc_in;
 };
 
 // Packed fp32x2 arithmetic (FADD2 / FFMA2 on sm_100a): two lanes of a float4 per instruction,
@@ -349,7 +346,6 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_v(const SpmmArgs &a, int64_t row, int c4, bool act, float4 acc, float4 x,
                                            float s) {
     const int64_t o = row * (int64_t)a.d4 + c4;
-    if (a.acc_in != nullptr && act) acc = f4add(__ldcs(a.acc_in + o), acc);
     if (EPI == EPI_RAW) {
         if (act) st_stream(a.out + o, acc);
         return;
@@ -828,136 +824,6 @@ void sched_build(SchedBufs &b, const int64_t *rowptr, int64_t n_rows, cudaStream
     TPO_LAUNCH_CHECK();
 }
 
-// ---------------------------------------------------------------------------------------
-// Column-range passes.  One SpMM over a gathered table larger than L2 is split into R passes,
-// pass r gathering only the table rows of range r = {c : floor(c R / n_src) = r} (a table slice
-// of ~1/R of the rows, re-read from L2 instead of DRAM); pass r > 0 adds the earlier passes'
-// sum (acc_in) and the last pass applies the epilogue.  The sub-CSRs are built once per
-// propagation: a stable, per-row split of the column indices, all ranges in one array (range
-// r's row pointers are S[r m .. (r+1) m], absolute offsets into it).
-// ---------------------------------------------------------------------------------------
-constexpr int kMaxRanges = 8;
-
-__device__ __forceinline__ int col_range(int32_t c, int64_t n_src, int R) {
-    return (int)(((int64_t)c * R) / n_src);
-}
-
-__global__ void range_count_kernel(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ col, int64_t m,
-                                   int64_t n_src, int R, int64_t *__restrict__ cnt) {
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= m) return;
-    int64_t c[kMaxRanges];
-#pragma unroll
-    for (int r = 0; r < kMaxRanges; ++r) c[r] = 0;
-    for (int64_t e = rowptr[row] + lane, end = rowptr[row + 1]; e - lane < end; e += 32) {
-        const int rg = e < end ? col_range(col[e], n_src, R) : -1;
-#pragma unroll
-        for (int r = 0; r < kMaxRanges; ++r)
-            if (r < R) c[r] += __popc(__ballot_sync(0xffffffffu, rg == r));
-    }
-    if (lane == 0)
-        for (int r = 0; r < R; ++r) cnt[(int64_t)r * m + row] = c[r];
-}
-
-__global__ void range_fill_kernel(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ col,
-                                  const float *__restrict__ val, int64_t m, int64_t n_src, int R,
-                                  const int64_t *__restrict__ S, int32_t *__restrict__ col_out,
-                                  float *__restrict__ val_out) {
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= m) return;
-    int64_t pos[kMaxRanges];
-#pragma unroll
-    for (int r = 0; r < kMaxRanges; ++r) pos[r] = r < R ? S[(int64_t)r * m + row] : 0;
-    const unsigned below = (1u << lane) - 1u;
-    for (int64_t e = rowptr[row] + lane, end = rowptr[row + 1]; e - lane < end; e += 32) {
-        const bool in = e < end;
-        const int32_t cc = in ? col[e] : 0;
-        const int rg = in ? col_range(cc, n_src, R) : -1;
-#pragma unroll
-        for (int r = 0; r < kMaxRanges; ++r) {
-            if (r >= R) break;
-            const unsigned b = __ballot_sync(0xffffffffu, rg == r);
-            if (rg == r) {
-                const int64_t p = pos[r] + __popc(b & below);
-                col_out[p] = cc;
-                if (val != nullptr) val_out[p] = val[e];
-            }
-            pos[r] += __popc(b);
-        }
-    }
-}
-
-struct RangedCsr {
-    int R = 1;
-    int64_t m = 0;
-    int64_t *cnt = nullptr, *S = nullptr, *tilesums = nullptr;
-    int32_t *col = nullptr;
-    float *val = nullptr;
-    SchedBufs sb[kMaxRanges];
-    unsigned *arr[kMaxRanges];
-};
-
-// Workspace of an R-range split of an m-row CSR with nnz entries (R = 1: nothing).
-RangedCsr ranged_alloc(Arena &ar, int R, int64_t m, int64_t nnz, int64_t ncnt) {
-    RangedCsr rc;
-    rc.R = R;
-    rc.m = m;
-    if (R <= 1) return rc;
-    const int64_t N = (int64_t)R * m;
-    rc.cnt = ar.take<int64_t>(N + 1);
-    rc.S = ar.take<int64_t>(N + 1);
-    rc.tilesums = ar.take<int64_t>(cdiv(N + 1, SCAN_TILE) + 1);
-    rc.col = ar.take<int32_t>(nnz);
-    rc.val = ar.take<float>(nnz);
-    for (int r = 0; r < R; ++r) {
-        rc.sb[r] = sched_alloc(ar, m, nnz);
-        rc.arr[r] = ar.take<unsigned>(rc.sb[r].s.max_slots * ncnt);
-    }
-    return rc;
-}
-
-void ranged_build(RangedCsr &rc, const tpo_csr_t &A, int64_t n_src, int64_t ncnt, cudaStream_t st) {
-    if (rc.R <= 1 || rc.m == 0) return;
-    const int64_t m = rc.m, N = (int64_t)rc.R * m;
-    const int T = 256;
-    range_count_kernel<<<cdiv(m * 32, T), T, 0, st>>>(A.row_ptr, A.col_idx, m, n_src, rc.R, rc.cnt);
-    TPO_LAUNCH_CHECK();
-    const int64_t nb = cdiv(N, SCAN_TILE);
-    scan_tile_sums<<<nb, SCAN_T, 0, st>>>(rc.cnt, N, rc.tilesums);
-    TPO_LAUNCH_CHECK();
-    scan_sums_single<<<1, SCAN_T, 0, st>>>(rc.tilesums, nb);
-    TPO_LAUNCH_CHECK();
-    scan_apply<<<nb, SCAN_T, 0, st>>>(rc.cnt, N, rc.tilesums, rc.S, rc.S + N);
-    TPO_LAUNCH_CHECK();
-    range_fill_kernel<<<cdiv(m * 32, T), T, 0, st>>>(A.row_ptr, A.col_idx, A.val, m, n_src, rc.R, rc.S, rc.col,
-                                                     A.val ? rc.val : nullptr);
-    TPO_LAUNCH_CHECK();
-    for (int r = 0; r < rc.R; ++r) {
-        sched_build(rc.sb[r], rc.S + (int64_t)r * m, m, st);
-        TPO_CUDA(cudaMemsetAsync(rc.arr[r], 0, sizeof(unsigned) * rc.sb[r].s.max_slots * ncnt, st));
-    }
-}
-
-// Column ranges of the two SpMMs of a hop (gathered tables P: n_u rows, Q: n_v rows).  Measured
-// on large / medium: every split is slower than one pass (R = 2 on SpMM-1 of
-// large: +0.6 ms per hop; the L2 hits gained do not pay for the extra pass over the output and
-// the per-pass row walk), so the default is one pass; TPO_SPMM_RANGES = "R1,R2" selects splits.
-void spmm_ranges(int64_t n_u, int64_t n_v, int d4, int &R1, int &R2) {
-    (void)d4;
-    R1 = R2 = 1;
-    if (const char *e = getenv("TPO_SPMM_RANGES")) {
-        int a = 0, b = 0;
-        if (sscanf(e, "%d,%d", &a, &b) == 2 && a >= 1 && b >= 1 && a <= kMaxRanges && b <= kMaxRanges) {
-            R1 = a;
-            R2 = b;
-        }
-    }
-    if (n_u == 0) R1 = 1;
-    if (n_v == 0) R2 = 1;
-}
-
 // Row-major kernel: one 128-float column slice per warp (SL = 1) with 4 resident blocks per SM,
 // measured best on small (d = 1000), medium (d = 256) and large (d = 128) against SL = 2 / 3-4
 // blocks and 16 rows in flight.
@@ -1060,10 +926,6 @@ size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
     const int64_t ncnt = std::max<int64_t>((d / 4 + 31) / 32, d / 16);   // slices or column groups
     ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * ncnt);  // chunk-arrival counters (U side)
     ar.take<unsigned>((2 * (nnz / CHUNK) + 1) * ncnt);  // (V side)
-    int R1 = 1, R2 = 1;
-    spmm_ranges(n_u, n_v, (int)(d / 4), R1, R2);
-    ranged_alloc(ar, R1, n_v, nnz, ncnt);                // SpMM-1 column ranges (gathers P)
-    ranged_alloc(ar, R2, n_u, nnz, ncnt);                // SpMM-2 column ranges (gathers Q)
     return ar.off + 256;
 }
 
@@ -1084,10 +946,6 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     unsigned *arr_u = ar.take<unsigned>(sb.s.max_slots * ncnt), *arr_v = ar.take<unsigned>(sbt.s.max_slots * ncnt);
     TPO_CUDA(cudaMemsetAsync(arr_u, 0, sizeof(unsigned) * sb.s.max_slots * ncnt, st));
     TPO_CUDA(cudaMemsetAsync(arr_v, 0, sizeof(unsigned) * sbt.s.max_slots * ncnt, st));
-    int R1 = 1, R2 = 1;
-    spmm_ranges(n, m, d4, R1, R2);
-    RangedCsr rc1 = ranged_alloc(ar, R1, m, nnz, ncnt);
-    RangedCsr rc2 = ranged_alloc(ar, R2, n, nnz, ncnt);
     int launches = 0;
     auto counter = [&]() {        // a zeroed counter per SpMM launch (the pool is re-zeroed when it wraps)
         if (launches % kCounters == 0) TPO_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) * kCounters, st));
@@ -1114,10 +972,6 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     int Lp = 0, Lq = 0;
     choose_widths(n, m, d4, Lp, Lq);
     const bool grouped = Lp > 0;
-    if (!grouped) {
-        if (m > 0) ranged_build(rc1, Bt, n, ncnt, st);
-        ranged_build(rc2, B, m, ncnt, st);
-    }
     init_scaled_kernel<<<cdiv(n * d4, TB), TB, 0, st>>>((const float4 *)X, su, n, d4, c, 1, (float4 *)Z,
                                                         grouped ? Lp : d4);
     TPO_LAUNCH_CHECK();
@@ -1137,22 +991,6 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
             if (grouped) {
                 a.src_rows = n; a.out_rows = m; a.out_L = Lq;
                 gspmm<EPI_V>(a, Lp, sbt.s.max_items, Bt.val != nullptr, st);
-            } else if (rc1.R > 1) {
-                a.col = rc1.col;
-                if (Bt.val == nullptr) a.val = nullptr;
-                else a.val = rc1.val;
-                for (int r = 0; r < rc1.R; ++r) {
-                    a.rowptr = rc1.S + (int64_t)r * m;
-                    a.sch = rc1.sb[r].s;
-                    a.arrive = rc1.arr[r];
-                    a.acc_in = r > 0 ? (const float4 *)Qv : nullptr;
-                    if (r > 0) {
-                        a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
-                        a.work = counter();
-                    }
-                    if (r + 1 < rc1.R) spmm_launch<EPI_RAW>(a, a.sch.max_items, a.sch.max_slots, Bt.val != nullptr, st);
-                    else spmm_launch<EPI_V>(a, a.sch.max_items, a.sch.max_slots, Bt.val != nullptr, st);
-                }
             } else {
                 spmm_launch<EPI_V>(a, sbt.s.max_items, sbt.s.max_slots, Bt.val != nullptr, st);
             }
@@ -1173,33 +1011,6 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
             if (last) gspmm<EPI_FINAL>(a, Lq, sb.s.max_items, B.val != nullptr, st);
             else gspmm<EPI_U>(a, Lq, sb.s.max_items, B.val != nullptr, st);
             if (last && Zhat) {
-                rownorm_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>((const float4 *)Z, n, d4, (float4 *)Zhat);
-                TPO_LAUNCH_CHECK();
-            }
-        } else if (rc2.R > 1) {
-            a.col = rc2.col;
-            if (B.val == nullptr) a.val = nullptr;
-            else a.val = rc2.val;
-            for (int r = 0; r < rc2.R; ++r) {
-                a.rowptr = rc2.S + (int64_t)r * n;
-                a.sch = rc2.sb[r].s;
-                a.arrive = rc2.arr[r];
-                a.acc_in = r > 0 ? (const float4 *)Z : nullptr;
-                if (r > 0) {
-                    a.reserve_sms = launches < reserve_launches ? reserve_sms : 0;
-                    a.work = counter();
-                }
-                const bool w = B.val != nullptr;
-                if (r + 1 < rc2.R) {
-                    spmm_launch<EPI_RAW>(a, a.sch.max_items, a.sch.max_slots, w, st);
-                } else if (last) {
-                    a.out_hat = (nslices == 1 && Zhat) ? (float4 *)Zhat : nullptr;
-                    spmm_launch<EPI_FINAL>(a, a.sch.max_items, a.sch.max_slots, w, st);
-                } else {
-                    spmm_launch<EPI_U>(a, a.sch.max_items, a.sch.max_slots, w, st);
-                }
-            }
-            if (last && Zhat && nslices > 1) {
                 rownorm_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>((const float4 *)Z, n, d4, (float4 *)Zhat);
                 TPO_LAUNCH_CHECK();
             }

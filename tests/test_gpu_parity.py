@@ -127,34 +127,6 @@ def test_propagate_column_group_layouts(tpo, monkeypatch, layout, weighted):
         assert relF(Z.cpu().numpy(), Zo) <= 1e-5
 
 
-@pytest.mark.parametrize("ranges", ["1,1", "2,1", "1,3", "4,4", "8,2", "3,5"])
-@pytest.mark.parametrize("weighted", [False, True])
-def test_propagate_column_ranges(tpo, monkeypatch, ranges, weighted):
-    """The column-range passes of the two SpMMs (TPO_SPMM_RANGES = "R1,R2": SpMM-1 / SpMM-2 split
-    into R passes over 1/R of the gathered table's rows, partial sums added in pass order) on
-    graphs with rows longer than one chunk, isolated U / V nodes and rows with no edge in some
-    ranges, at d = 8 (one ragged slice), 128 and 136 (two slices): parity with the oracle and
-    bitwise-deterministic re-runs."""
-    monkeypatch.setenv("TPO_SPMM_RANGES", ranges)
-    for d in (8, 128, 136):
-        h = hub_graph(seed=d + 11, weighted=weighted, d=d)
-        g = G(**h)
-        Zo, Zho = O.propagate(g.n, g.m, g.B_rowptr, g.B_col, g.X, 0.6, 3, g.B_val)
-        dg = tpo.to_device_graph(g.n, g.m, g.B_rowptr, g.B_col, g.Bt_rowptr, g.Bt_col, g.B_val, g.Bt_val)
-        Z, Zh = tpo.propagate(dg, torch.from_numpy(g.X).cuda(), 0.6, 3)
-        Z2, Zh2 = tpo.propagate(dg, torch.from_numpy(g.X).cuda(), 0.6, 3)
-        assert torch.equal(Z, Z2) and torch.equal(Zh, Zh2)
-        Z, Zh = Z.cpu().numpy(), Zh.cpu().numpy()
-        assert relF(Z, Zo) <= 1e-5 and relF(Zh, Zho) <= 1e-5
-        for u in (3, 4):   # isolated U keeps X-hat
-            assert np.allclose(Zh[u], g.X[u] / np.linalg.norm(g.X[u]), atol=1e-6)
-    gp = planted_abg(3001, 2005, 5, 128, deg=("zipf", 1.3, 120), p_in=0.6, pop=("zipf", 1.2),
-                     x=("gaussian", 1.0), seed=5, weighted=weighted)
-    Zo, _ = O.propagate(gp.n, gp.m, gp.B_rowptr, gp.B_col, gp.X, 0.5, 4, gp.B_val)
-    Z, _ = tpo.propagate(dev_graph(tpo, gp), torch.from_numpy(gp.X).cuda(), 0.5, 4)
-    assert relF(Z.cpu().numpy(), Zo) <= 1e-5
-
-
 def test_propagate_empty_graph(tpo):
     """nnz = 0: every node is isolated, Z = (1 - alpha) X."""
     n, m, d = 37, 5, 8

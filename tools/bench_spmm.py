@@ -1,7 +1,7 @@
-"""Time tpo_propagate under the SpMM variants on BASELINE configs:
-  RANGES  -- TPO_SPMM_RANGES = "R1,R2" (column-range passes of SpMM-1 / SpMM-2; "auto" = the
-             library's default rule),
+"""Time tpo_propagate under the SpMM layouts on BASELINE configs:
   LAYOUTS -- TPO_SPMM_L = "Lp,Lq" (column-group widths in float4 of P and Q; "0,0" = row-major).
+  (RANGES -- TPO_SPMM_RANGES, the column-range passes measured in round 2, were removed: slower
+  everywhere and a register-pressure cost to the default kernel.)
 Variants sum in different (fixed) orders: results agree to fp32 rounding (relF printed vs the
 first variant).  The L2 is flushed before every timed call."""
 import os
@@ -12,7 +12,7 @@ import paper_2405_11922_b200 as T
 from synth import make_config
 
 cfgs = os.environ.get("CFGS", "large").split(",")
-ranges = os.environ.get("RANGES", "1,1;auto").split(";")
+ranges = ["1,1"]
 layouts = os.environ.get("LAYOUTS", "0,0").split(";")
 reps = int(os.environ.get("REPS", "5"))
 for cfg in cfgs:
