@@ -557,6 +557,7 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     ar.take<double>(nb * k * k);
     ar.take<int64_t>(nb * k);
     ar.take<char>(rh_plan_ws(n));
+    ar.take<uint32_t>(D);
     size_t inner = std::max(std::max(std::max(onmf_ws_bytes(n, D, k), std::max(dgemm_ws(k, k, n), dgemm_ws(k, k, D))),
                                      ts_atb_ws(k, k)),
                             rh_apply_ws(D, k));
@@ -566,7 +567,7 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
 
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
-                  int32_t *iters_used, Arena &ar, cudaStream_t st) {
+                  int32_t *iters_used, Arena &ar, cudaStream_t st, RStats rs) {
     double *U = ar.take<double>(n * k);
     double *RH = ar.take<double>(n * k);
     double *H = ar.take<double>(D * k), *Hn = ar.take<double>(D * k);
@@ -578,7 +579,17 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const int64_t nb = cdiv(std::max<int64_t>(n, 1), rpb);
     double *part = ar.take<double>(nb * k * k);
     int64_t *cpart = ar.take<int64_t>(nb * k);
-    const RhPlan rhp = rh_plan(Rp, n, D, k, ar, st);
+    const RhPlan rhp = rh_plan_pre(rs.rowE, Rp, n, D, k, ar, st);
+    const uint32_t *featmax = nullptr;                     // R''s per-feature maxima (oz R^T Ups), once per solve
+    if (oz_rtu_supported(n, D, k)) {
+        if (rs.featmax) {
+            featmax = rs.featmax;
+        } else {
+            uint32_t *fm = ar.take<uint32_t>(D);
+            oz_featmax(Rp, n, D, fm, st);
+            featmax = fm;
+        }
+    }
     const size_t mark = ar.off;
 
     TPO_CUDA(cudaMemcpyAsync(sig, sigma, sizeof(double) * k, cudaMemcpyHostToDevice, st));
@@ -588,7 +599,7 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const size_t ups_smem = sizeof(double) * ((size_t)k * k + 1 + (size_t)8 * UR * k);
     TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
     for (int t = 0; t < Tf; ++t) {
-        onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
+        onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st, featmax);
         ar.off = mark;
         if (ts64_enabled() && k <= 104) ts_atb_f64(U, k, U, k, n, k, k, UtU, ar, st);
         else dgemm(true, k, k, n, 1.0, U, k, U, k, 0.0, UtU, k, ar, st);

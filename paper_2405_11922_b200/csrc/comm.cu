@@ -184,7 +184,7 @@ size_t run_sharded_ws_bytes(int64_t n_p, int64_t m, int64_t nnz_p, int64_t d, in
     s += align_up(sizeof(double) * (size_t)D * D) + 3 * align_up(sizeof(double) * (size_t)D * k) + align_up(sizeof(float) * D * k);
     s += 3 * align_up(sizeof(double) * (size_t)n_p * k) + align_up(sizeof(float) * (size_t)n_p * k);
     s += 8 * align_up(sizeof(double) * (size_t)k * k) + 8 * align_up(sizeof(double) * (size_t)k) + 1024;
-    s += rh_plan_ws(n_p);
+    s += rh_plan_ws(n_p) + align_up(sizeof(uint32_t) * (size_t)D + 1);
     size_t inner = std::max(features_ws_bytes(n_p, d), gram_tc_ws(std::max<int64_t>(n_p, 1), D));
     inner = std::max(inner, eig_from_gram_ws(D, k));
     inner = std::max(inner, haar_q_ws_bytes(d));
@@ -222,6 +222,7 @@ void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, con
     int64_t *idx_all = ar.take<int64_t>((size_t)world * k);
     int32_t *changed = ar.take<int32_t>(2);
     int32_t *rowE = ar.take<int32_t>(std::max<int64_t>(n_p, 1));
+    uint32_t *featmax = ar.take<uint32_t>(D);           // R''s per-feature maxima (oz R^T Ups), once per solve
     const size_t mark = ar.off;
     auto atb = [&](const double *A, const double *B, double *out) {
         if (n_p == 0) { TPO_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * k * k, st)); return; }
@@ -300,8 +301,10 @@ void run_sharded_impl(void *comm, const tpo_csr_t &Bp, const tpo_csr_t &Btp, con
     onmf_init(Gam, n_p, Psi, sigma.data(), D, k, U, H, ar, st);
     ar.off = mark;
     const RhPlan rhp = rh_plan_at(rowE, Rp, n_p, D, k, st);
+    if (oz_rtu_supported(n_p, D, k)) oz_featmax(Rp, n_p, D, featmax, st);
+    else featmax = nullptr;
     for (int t = 0; t < Tf; ++t) {
-        if (n_p > 0) onmf_rtu(Rp, n_p, D, dinv, U, k, RtU, ar, st);
+        if (n_p > 0) onmf_rtu(Rp, n_p, D, dinv, U, k, RtU, ar, st, featmax);
         else TPO_CUDA(cudaMemsetAsync(RtU, 0, sizeof(double) * D * k, st));
         ar.off = mark;
         allreduce(RtU, (size_t)(D * k));

@@ -106,6 +106,15 @@ __global__ void flip_cols_f64(double *__restrict__ A, int64_t n, int k, const in
     if (sgn[i % k] < 0) A[i] = -A[i];
 }
 
+// out = sgn(l) A (rounded to fp32): R8's column flips fused with the fp32 rounding of Gamma
+__global__ void flip_cast_f64_f32(const double *__restrict__ A, int64_t n, int k, const int *__restrict__ sgn,
+                                  float *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * k) return;
+    const double v = A[i];
+    out[i] = (float)(sgn[i % k] < 0 ? -v : v);
+}
+
 __global__ void cast_f64_f32_k(const double *__restrict__ a, int64_t len, float *__restrict__ b) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < len) b[i] = (float)a[i];
@@ -365,6 +374,13 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     int m = 8;
     std::vector<double> w(bz), E(bz * bz);
     double bnd = 0.0;
+    // Rayleigh-Ritz (a host eigensolve of the (b+1) x (b+1) projection) only where it can stop the
+    // iteration: the residual falls by a steady factor per filter round (measured between the last
+    // two Rayleigh-Ritz steps), so rounds whose predicted residual is still above the tolerance
+    // filter and re-orthonormalise only; Rayleigh-Ritz runs when the predicted residual reaches the
+    // tolerance.  Stopping is always decided on explicit residuals.
+    int last_rr = -1;
+    double last_rel = 0.0, rate = 0.0;
     static const bool trace = getenv("TPO_TRACE_EIG") != nullptr;
     static cudaEvent_t tev[2] = {};   // trace only: created once, reused
     if (trace && !tev[0])
@@ -386,6 +402,9 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
             }
             TPO_CUDA(cudaMemcpyAsync(V, Y1, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
             orth_against_u();
+            if (round < max_rounds && last_rr >= 1 && rate > 1.0 &&
+                last_rel / pow(rate, (double)(round - last_rr)) > 1e-9)
+                continue;                                  // predicted residual still above 1e-9
         }
         // Rayleigh-Ritz with the full G on Z = [u, V]
         stack_kernel<<<cdiv(D * bz, 256), 256, 0, st>>>(u, V, D, (int)b, Z);
@@ -419,6 +438,13 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
             fprintf(stderr, "[tpo eig] round %d degree %d rmax/w0 %.3e w0 %.6e wk %.6e wk+1 %.6e wb %.6e  "
                             "stream %.3f ms wall %.3f ms\n", round, round > 0 ? m : 0, rmax / fabs(w[0]), w[0],
                     w[k - 1], w[k], w[bz - 1], gpu_ms, wall_ms);
+        }
+        {
+            const double rel = rmax / fabs(w[0]);
+            if (last_rr >= 0 && rel > 0.0 && rel < last_rel)
+                rate = pow(last_rel / rel, 1.0 / (double)(round - last_rr));
+            last_rr = round;
+            last_rel = rel;
         }
         if (rmax <= 1e-9 * fabs(w[0]) || round == max_rounds) {
             check_flag(flag, st, "top-k subspace iteration (CholeskyQR2)");
@@ -454,7 +480,9 @@ __global__ void sign_rule_kernel(const double *__restrict__ s, const double *__r
 
 // Sign rule R8 on (Gamma, Psi): sum_i Gamma[i,l] >= 0, else (near-zero sums) the sign of the
 // largest-magnitude entry (smallest index among ties).  Flips are applied to both factors.
-void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Arena &ar, cudaStream_t st) {
+// out32 (optional): write sgn . Gamma rounded to fp32 there instead of flipping Gamma in place.
+void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Arena &ar, cudaStream_t st,
+                     float *out32 = nullptr) {
     const size_t mark = ar.off;
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>(2 * 148, cdiv(n, 64)));
     const int64_t rows_per = cdiv(n, G);
@@ -469,35 +497,100 @@ void apply_sign_rule(double *Gamma, int64_t n, int k, float *Psi, int64_t D, Are
     TPO_LAUNCH_CHECK();
     sign_rule_kernel<<<cdiv(k, 128), 128, 0, st>>>(s, a, arg, Gamma, k, dsg);
     TPO_LAUNCH_CHECK();
-    flip_cols_f64<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
+    if (out32) flip_cast_f64_f32<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg, out32);
+    else flip_cols_f64<<<cdiv(n * k, 256), 256, 0, st>>>(Gamma, n, k, dsg);
     TPO_LAUNCH_CHECK();
     flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
     TPO_LAUNCH_CHECK();
     ar.off = mark;
 }
 
-// ci <- I when the Gram g is already within 1e-6 of I (then X ci = X exactly): the polish
-// decision taken on the device
-__global__ void polish_select_kernel(const double *__restrict__ g, int k, double *__restrict__ ci) {
-    __shared__ int need;
-    if (threadIdx.x == 0) need = 0;
-    __syncthreads();
+// *dev = max |g - I| (one CTA, order-free max)
+__global__ void gram_dev_kernel(const double *__restrict__ g, int k, double *__restrict__ dev) {
+    __shared__ double sm[256];
+    double m = 0.0;
     for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
         const double dv = fabs(g[i] - ((i / k) == (i % k) ? 1.0 : 0.0));
-        if (!(dv <= 1e-6)) need = 1;
+        m = (dv > m || dv != dv) ? dv : m;                 // NaN propagates
     }
+    sm[threadIdx.x] = m;
     __syncthreads();
-    if (need) return;
-    for (int i = threadIdx.x; i < k * k; i += blockDim.x) ci[i] = (i / k) == (i % k) ? 1.0 : 0.0;
+    for (int o = 128; o; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            const double a = sm[threadIdx.x], b = sm[threadIdx.x + o];
+            sm[threadIdx.x] = (b > a || b != b) ? b : a;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *dev = sm[0];
+}
+
+// X[i, :] <- X[i, :] Ci in place for an upper-triangular k x k Ci (k <= 128): a warp per row, the
+// row in registers (lane: columns lane + 32 c), Ci in shared memory (entries below the diagonal
+// read as 0)
+template <int C>
+__global__ void __launch_bounds__(256) apply_upper_rows_kernel(double *__restrict__ X, int64_t n, int k,
+                                                               const double *__restrict__ Ci) {
+    extern __shared__ double cs[];
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) cs[i] = ((i / k) <= (i % k)) ? Ci[i] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = wid; row < n; row += nw) {
+        double x[C], acc[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int l = lane + 32 * c;
+            x[c] = l < k ? X[row * k + l] : 0.0;
+            acc[c] = 0.0;
+        }
+#pragma unroll
+        for (int c0 = 0; c0 < C; ++c0) {
+            for (int j = 0; j < 32; ++j) {
+                const int a = 32 * c0 + j;
+                if (a >= k) break;
+                const double xa = __shfl_sync(0xffffffffu, x[c0], j);
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const int l = lane + 32 * c;
+                    if (l < k) acc[c] = fma(xa, cs[a * k + l], acc[c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int l = lane + 32 * c;
+            if (l < k) X[row * k + l] = acc[c];
+        }
+    }
+}
+
+void apply_upper_rows(double *X, int64_t n, int k, const double *Ci, cudaStream_t st) {
+    if (n == 0) return;
+    const size_t smem = sizeof(double) * (size_t)k * k;
+    const unsigned grid = (unsigned)std::min<int64_t>(8 * sm_count(), cdiv(n, 8));
+#define TPO_AUR(CV)                                                                                          \
+    {                                                                                                        \
+        TPO_CUDA(cudaFuncSetAttribute(apply_upper_rows_kernel<CV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        apply_upper_rows_kernel<CV><<<grid, 256, smem, st>>>(X, n, k, Ci);                                \
+    }
+    if (k <= 32) TPO_AUR(1)
+    else if (k <= 64) TPO_AUR(2)
+    else TPO_AUR(4)
+#undef TPO_AUR
+    TPO_LAUNCH_CHECK();
 }
 
 // CholeskyQR polish of the fp64 n x k Gamma while its Gram is off identity by > 1e-6 (at most
-// two corrections): G = Gamma^T Gamma (dgemm), Ci = S C^{-1} (chol_inv), Gamma <- Gamma Ci, with
-// Ci replaced by I on the device when the Gram is already within 1e-6 of I.
+// two corrections): G = Gamma^T Gamma, Ci = S C^{-1} (chol_inv), Gamma <- Gamma Ci (in place).
+// The deviation max|G - I| is read back after each Gram: within 1e-6 Gamma is left as is; below
+// 1e-2 one correction suffices (CholeskyQR leaves ||Gamma^T Gamma - I|| ~ kappa^2 u with kappa^2
+// < 1.03, far below 1e-6), so the second Gram is skipped.
 void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
     const size_t mark = ar.off;
     double *g = ar.take<double>((size_t)k * k), *ci = ar.take<double>((size_t)k * k);
-    double *tmp = ar.take<double>((size_t)n * k);
+    double *dev = ar.take<double>(1);
     int *flag = ar.take<int>(1);
     TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
     for (int pass = 0; pass < 2; ++pass) {
@@ -512,10 +605,14 @@ void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
             host_upper_inverse(k, C.data(), Ci.data());
             TPO_CUDA(cudaMemcpyAsync(ci, Ci.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
         }
-        polish_select_kernel<<<1, 256, 0, st>>>(g, k, ci);
+        gram_dev_kernel<<<1, 256, 0, st>>>(g, k, dev);
         TPO_LAUNCH_CHECK();
-        dgemm(false, n, k, k, 1.0, Gamma, k, ci, k, 0.0, tmp, k, ar, st);
-        TPO_CUDA(cudaMemcpyAsync(Gamma, tmp, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
+        double hdev = 1.0;
+        TPO_CUDA(cudaMemcpyAsync(&hdev, dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+        TPO_CUDA(cudaStreamSynchronize(st));
+        if (hdev <= 1e-6) break;
+        if (!ts_xw_inplace_f64(Gamma, n, k, ci, st)) apply_upper_rows(Gamma, n, k, ci, st);
+        if (hdev < 1e-2) break;
     }
     check_flag(flag, st, "CholeskyQR2 polish of Gamma");
     ar.off = mark;
@@ -535,7 +632,7 @@ __global__ void scale_cols_kernel(const double *__restrict__ A, int64_t rows, in
 // otherwise Gamma = R Psi Sigma^{-1} (exact mode: the same factor, the block being full rank).
 void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
                     const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st,
-                    double *Gamma_in = nullptr) {
+                    double *Gamma_in = nullptr, const int32_t *rowE = nullptr) {
     double *G64 = Gamma_in;
     if (!G64) {
         double *sd = to_dev(ar, sig, st);
@@ -543,15 +640,13 @@ void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, in
         scale_cols_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D, k, sd, w);
         TPO_LAUNCH_CHECK();
         G64 = ar.take<double>((size_t)n * k);
-        const RhPlan gp = rh_plan(Rp, n, D, k, ar, st);     // integer tensor cores when k > 32
+        const RhPlan gp = rh_plan_pre(rowE, Rp, n, D, k, ar, st);     // integer tensor cores when k > 32
         rh_apply(gp, Rp, dinv, w, n, D, k, G64, ar, st);
     }
     cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
     TPO_LAUNCH_CHECK();
     polish_gamma(G64, n, k, ar, st);
-    apply_sign_rule(G64, n, k, Psi, D, ar, st);
-    cast_f64_f32_k<<<cdiv(n * k, 256), 256, 0, st>>>(G64, n * k, Gamma);
-    TPO_LAUNCH_CHECK();
+    apply_sign_rule(G64, n, k, Psi, D, ar, st, Gamma);
     TPO_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -755,7 +850,7 @@ void gamma_final(double *G64, int64_t n, int k, const int *signs_host, float *Ps
 
 void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode, int32_t p,
                    int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi, Arena &ar,
-                   cudaStream_t st, const double *r_colsum) {
+                   cudaStream_t st, const double *r_colsum, RStats rs) {
     std::vector<double> lam;
     double *Psi64 = ar.take<double>(D * k);
     double *halko_gamma = nullptr;              // Halko mode: Gamma = Y E_k
@@ -830,7 +925,7 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
         if (!(sig[l] > 0.0)) throw Error(TPO_ENUMERIC, "top-k: sigma_k is zero (rank(R) < k)");
         sigma[l] = sig[l];
     }
-    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st, halko_gamma);
+    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st, halko_gamma, rs.rowE);
 }
 
 // a6: out = dinv . R' (R'^T (dinv . Y)), the D x b intermediate summed in fp64.
@@ -903,9 +998,7 @@ void svd_reduce_impl(const float *X, int64_t n, int64_t du, int64_t d, float *Xr
     tsgemm_AW_f64(X, du, nullptr, Psi64, n, du, d, X64, d, st);   // X Psi = Gamma Sigma
     cast_f64_f32<<<cdiv(du * d, 256), 256, 0, st>>>(Psi64, du * d, Psi32);
     TPO_LAUNCH_CHECK();
-    apply_sign_rule(X64, n, (int)d, Psi32, du, ar, st);
-    cast_f64_f32<<<cdiv(n * d, 256), 256, 0, st>>>(X64, n * d, Xr);
-    TPO_LAUNCH_CHECK();
+    apply_sign_rule(X64, n, (int)d, Psi32, du, ar, st, Xr);
     TPO_CUDA(cudaStreamSynchronize(st));
 }
 

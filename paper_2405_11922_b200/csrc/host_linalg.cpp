@@ -47,63 +47,93 @@ void host_qr_positive(int64_t rows, int64_t cols, const double *A, double *Q, do
 
 namespace {
 
-// Householder reduction of symmetric a (n x n, row-major, overwritten by the orthogonal
-// transform Z with Z^T A Z = tridiag(d, e)); e[i] couples i-1 and i, e[0] = 0.
-void tridiagonalise(int n, std::vector<double> &a, std::vector<double> &d, std::vector<double> &e) {
+// Householder tridiagonalisation of symmetric a (n x n, row-major, full storage): T = Q^T A Q
+// with Q = H_0 H_1 ... H_{n-3}, H_k = I - beta_k v_k v_k^T acting on rows / columns k+1 .. n-1.
+// d = diag(T), e[i] couples i-1 and i (e[0] = 0); zt = Q^T (row i of zt = column i of Q), the
+// transposed start of the QL eigenvector accumulation.  Every inner loop runs over contiguous
+// rows (the symmetric rank-2 update keeps the full matrix), so it vectorises and stays in cache.
+void tridiagonalise(int n, std::vector<double> &a, std::vector<double> &d, std::vector<double> &e,
+                    std::vector<double> &zt) {
     auto A = [&](int i, int j) -> double & { return a[(size_t)i * n + j]; };
-    for (int i = n - 1; i > 0; --i) {
-        const int l = i - 1;
-        double h = 0.0, scale = 0.0;
-        if (l > 0) {
-            for (int k = 0; k <= l; ++k) scale += fabs(A(i, k));
-            if (scale == 0.0) {
-                e[i] = A(i, l);
-            } else {
-                for (int k = 0; k <= l; ++k) {
-                    A(i, k) /= scale;
-                    h += A(i, k) * A(i, k);
-                }
-                double f = A(i, l);
-                double g = (f >= 0.0) ? -sqrt(h) : sqrt(h);
-                e[i] = scale * g;
-                h -= f * g;
-                A(i, l) = f - g;
-                f = 0.0;
-                for (int j = 0; j <= l; ++j) {
-                    A(j, i) = A(i, j) / h;
-                    g = 0.0;
-                    for (int k = 0; k <= j; ++k) g += A(j, k) * A(i, k);
-                    for (int k = j + 1; k <= l; ++k) g += A(k, j) * A(i, k);
-                    e[j] = g / h;
-                    f += e[j] * A(i, j);
-                }
-                const double hh = f / (h + h);
-                for (int j = 0; j <= l; ++j) {
-                    f = A(i, j);
-                    e[j] = g = e[j] - hh * f;
-                    for (int k = 0; k <= j; ++k) A(j, k) -= (f * e[k] + g * A(i, k));
-                }
-            }
-        } else {
-            e[i] = A(i, l);
-        }
-        d[i] = h;
-    }
-    d[0] = 0.0;
+    std::vector<double> v(n), p(n), w(n), beta(n, 0.0), V((size_t)n * n, 0.0);   // V row k: v_k
     e[0] = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const int l = i - 1;
-        if (d[i] != 0.0) {
-            for (int j = 0; j <= l; ++j) {
-                double g = 0.0;
-                for (int k = 0; k <= l; ++k) g += A(i, k) * A(k, j);
-                for (int k = 0; k <= l; ++k) A(k, j) -= g * A(k, i);
-            }
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m0 = k + 1;
+        double *x = &A(k, m0);                         // row k right of the diagonal = column k below it
+        double scale = 0.0;
+        for (int i = 0; i < n - m0; ++i) scale = std::max(scale, fabs(x[i]));
+        d[k] = A(k, k);
+        if (scale == 0.0) {
+            e[m0] = 0.0;
+            continue;
         }
-        d[i] = A(i, i);
-        A(i, i) = 1.0;
-        for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
+        double sig = 0.0;
+        for (int i = 0; i < n - m0; ++i) {
+            v[i] = x[i] / scale;
+            sig += v[i] * v[i];
+        }
+        const double nrm = sqrt(sig);
+        const double alpha = v[0] >= 0.0 ? -nrm : nrm;       // H x = alpha scale e_0
+        v[0] -= alpha;
+        const double vtv = sig - 2.0 * alpha * (v[0] + alpha) + alpha * alpha;   // |x/scale - alpha e0|^2
+        const double b = 2.0 / vtv;
+        e[m0] = alpha * scale;
+        beta[k] = b;
+        const int m = n - m0;
+        // p = b A22 v (rows of A22 contiguous)
+        double pv = 0.0;
+        for (int i = 0; i < m; ++i) {
+            const double *ri = &A(m0 + i, m0);
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j) acc += ri[j] * v[j];
+            p[i] = b * acc;
+            pv += p[i] * v[i];
+        }
+        const double K = 0.5 * b * pv;
+        for (int i = 0; i < m; ++i) w[i] = p[i] - K * v[i];
+        // A22 -= v w^T + w v^T
+        for (int i = 0; i < m; ++i) {
+            double *ri = &A(m0 + i, m0);
+            const double vi = v[i], wi = w[i];
+            for (int j = 0; j < m; ++j) ri[j] -= vi * w[j] + wi * v[j];
+        }
+        double *vk = &V[(size_t)k * n + m0];
+        for (int i = 0; i < m; ++i) vk[i] = v[i];
     }
+    if (n >= 2) {
+        d[n - 2] = A(n - 2, n - 2);
+        e[n - 1] = A(n - 1, n - 2);
+    }
+    d[n - 1] = A(n - 1, n - 1);
+    // zt = Q^T = H_{n-3} ... H_1 H_0: start from I, apply H_0 first (each H_k changes rows k+1..)
+    std::fill(zt.begin(), zt.end(), 0.0);
+    for (int i = 0; i < n; ++i) zt[(size_t)i * n + i] = 1.0;
+    std::vector<double> y(n);
+    for (int k = 0; k + 2 < n; ++k) {
+        if (beta[k] == 0.0) continue;
+        const int m0 = k + 1;
+        const double *vk = &V[(size_t)k * n];
+        std::fill(y.begin(), y.end(), 0.0);                // y^T = v^T M (rows m0..n-1 of M)
+        for (int i = m0; i < n; ++i) {
+            const double vi = vk[i];
+            const double *mi = &zt[(size_t)i * n];
+            for (int j = 0; j < n; ++j) y[j] += vi * mi[j];
+        }
+        for (int i = m0; i < n; ++i) {
+            const double c = beta[k] * vk[i];
+            double *mi = &zt[(size_t)i * n];
+            for (int j = 0; j < n; ++j) mi[j] -= c * y[j];
+        }
+    }
+}
+
+// sqrt(a^2 + b^2) without libm's hypot (which dominated the QL sweeps: one call per rotation);
+// rescaled only when a square could over- or underflow
+inline double fast_hypot(double a, double b) {
+    const double fa = fabs(a), fb = fabs(b);
+    const double m = fa > fb ? fa : fb;
+    if (m > 1e150 || (m < 1e-150 && m > 0.0)) return hypot(a, b);
+    return sqrt(a * a + b * b);
 }
 
 // Implicit-shift QL on the tridiagonal (d, e), accumulating rotations into z (n x n, TRANSPOSED:
@@ -121,14 +151,14 @@ void tridiag_ql(int n, std::vector<double> &d, std::vector<double> &e, std::vect
             if (m != l) {
                 if (iter++ == 200) throw Error(TPO_ENUMERIC, "tridiagonal QL did not converge");
                 double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-                double r = hypot(g, 1.0);
+                double r = fast_hypot(g, 1.0);
                 g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? fabs(r) : -fabs(r)));
                 double s = 1.0, c = 1.0, p = 0.0;
                 int i;
                 for (i = m - 1; i >= l; --i) {
                     double f = s * e[i];
                     const double b = c * e[i];
-                    e[i + 1] = (r = hypot(f, g));
+                    e[i + 1] = (r = fast_hypot(f, g));
                     if (r == 0.0) {
                         d[i + 1] -= p;
                         e[m] = 0.0;
@@ -173,10 +203,8 @@ void host_sym_eig_top(int64_t D, const double *Ain, int64_t nvec, double *w, dou
         if (nvec > 0) V[0] = 1.0;
         return;
     }
-    tridiagonalise(n, a, d, e);
     std::vector<double> zt((size_t)n * n);                  // the transform, transposed for tridiag_ql
-    for (int r = 0; r < n; ++r)
-        for (int c = 0; c < n; ++c) zt[(size_t)c * n + r] = a[(size_t)r * n + c];
+    tridiagonalise(n, a, d, e, zt);
     tridiag_ql(n, d, e, zt);
     for (int r = 0; r < n; ++r)
         for (int c = 0; c < n; ++c) a[(size_t)r * n + c] = zt[(size_t)c * n + r];

@@ -230,12 +230,26 @@ void launch_rtu(const RtuPlan &p, const float *Rp, int64_t n, int D, const float
 
 size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k) {
     const RtuPlan p = rtu_plan(n, (int)D, k);
-    return std::max(align_up(sizeof(double) * (size_t)(p.G * D * k) + 1) + 256, ts_rtu_ws(n, D, k));
+    return std::max(std::max(align_up(sizeof(double) * (size_t)(p.G * D * k) + 1) + 256, ts_rtu_ws(n, D, k)),
+                    align_up(sizeof(uint32_t) * (size_t)D + 1) + oz_rtu_ws(n, D, k));
 }
 
-// RtU = R'^T (dinv . U)   (D x k, fp64)
+// RtU = R'^T (dinv . U)   (D x k, fp64).  featmax (optional, from oz_featmax): R''s per-feature
+// maxima when the caller keeps them across the iterations of one solve.
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
-              cudaStream_t st) {
+              cudaStream_t st, const uint32_t *featmax) {
+    if (dinv && oz_rtu_supported(n, D, k) && (reinterpret_cast<uintptr_t>(Rp) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(U) & 15) == 0 && (reinterpret_cast<uintptr_t>(dinv) & 15) == 0) {
+        const size_t mark = ar.off;
+        if (!featmax) {
+            uint32_t *fm = ar.take<uint32_t>(D);
+            oz_featmax(Rp, n, D, fm, st);
+            featmax = fm;
+        }
+        oz_rtu(Rp, n, D, dinv, U, k, featmax, RtU, ar, st);    // integer tensor cores (R16)
+        ar.off = mark;
+        return;
+    }
     if (ts64_enabled()) {
         ts_rtu(Rp, n, D, dinv, U, k, RtU, ar, st);
         return;

@@ -37,6 +37,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <numeric>
 
 #include "tc_ptx.cuh"
 #include "tpo_internal.cuh"
@@ -557,6 +558,14 @@ RhPlan rh_plan_at(int32_t *rowE, const float *Rp, int64_t n, int64_t D, int k, c
 RhPlan rh_plan(const float *Rp, int64_t n, int64_t D, int k, Arena &ar, cudaStream_t st) {
     return rh_plan_at(ar.take<int32_t>(std::max<int64_t>(n, 1)), Rp, n, D, k, st);
 }
+RhPlan rh_plan_pre(const int32_t *rowE, const float *Rp, int64_t n, int64_t D, int k, Arena &ar, cudaStream_t st) {
+    if (!rowE) return rh_plan(Rp, n, D, k, ar, st);
+    RhPlan p;
+    p.oz = oz_enabled() && n > 0 && D % 4 == 0 && k > 32 && oz_aw_supported(D, k) &&
+           (reinterpret_cast<uintptr_t>(Rp) & 15) == 0;
+    p.rowE = const_cast<int32_t *>(rowE);
+    return p;
+}
 size_t rh_plan_ws(int64_t n) { return align_up(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1) + 1); }
 size_t rh_apply_ws(int64_t D, int k) { return (k > 32 && oz_aw_supported(D, k)) ? oz_aw_ws(D, k) : 0; }
 
@@ -920,6 +929,617 @@ void oz_assign(const OzAssign &p, const double *U, const double *Phi, int32_t *l
         case 48: oa_launch<48>(a, st); break;
         default: oa_launch<64>(a, st); break;
     }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Alg. 2's R^T Ups = R'^T (dinv . Ups) (D x k, reduced over the n rows; Eq. update-Q)
+// fp64-accurate on the integer tensor cores (R16), 32 < k <= 64:
+//   A = R'^T (M = 128 features per tile, K = rows): feature j scaled by 2^(46 - EA_j) (EA_j: the
+//       smallest e with max_i |R'_ij| < 2^e), F = round(R' 2^(46-EA)) (|F| <= 2^46; nearest, so the
+//       truncation is unbiased) cut into 6 balanced signed byte digits.  One fp64 fma gives V = F +
+//       beta (beta = 0x808080808080, so V in [0, 2^48)) in the low 48 bits of 2^52 + beta + R' 2^(46-EA);
+//       the digits are V's bytes xor 0x80 (byte b stands for b - 128).
+//   B = dinv . Ups (N = k padded to 16, K = rows; Ups >= 0): column l scaled by 2^(47 - EB_l), G =
+//       round(dinv_i Ups_il 2^(47-EB_l)) <= 2^47 (one fma rounds the exact product), 6 unsigned digits.
+//   The 26 kept digit pairs (p + q <= 6: a sum over K = n rows needs one digit weight more than
+//   the row products of oz_aw) are summed exactly in 7 int32 TMEM accumulators over one item of
+//   <= 8192 rows (per 32-row chunk |acc_s| grows by <= 6 x 32 x 128 x 255 < 2^23), then flushed as
+//   the exact int64 pair g0 = acc0 2^16 + acc1 2^8 + acc2, g1 = (acc3 2^16 + acc4 2^8 + acc5) 2^8
+//   + acc6 per (feature, column, item).  oz_rtu_reduce adds the items in 128-bit integers (exact,
+//   so the result does not depend on the order) and rounds once:
+//        RtU_jl = 2^(EA_j + EB_l - 61) sum_items (g0 2^32 + g1).
+//   Error per row <~ 2^-52 2^EA_j 2^EB_l (dropped pairs) + the roundings 2^-47 2^EA_j (dinv_i Ups_il)
+//   + 2^-48 2^EB_l |R'_ij| (both unbiased): the class of the fp64 products' own rounding
+//   (tests/test_gpu_oz.py).
+// Kernel (persistent, 704 threads, ~214 KB shared memory), items = (row block, feature tile):
+//   warp 0       producer: per 32-row chunk the fp32 R' tile (4 TMA boxes of 32 x 32, SWIZZLE_128B),
+//                the Ups rows (bulk copy) and dinv (bulk copy) into a 4-stage ring
+//   warp 1       MMA issuer: 9 N-concatenated tcgen05.mma kind::i8 (s8 x u8 -> s32) per chunk
+//   warps 2-9    A slicers: one feature x 16 rows per thread (conflict-free swizzled reads,
+//                16-byte core-matrix row stores)
+//   warps 10-13  B slicers: one column x 16 rows per thread
+//   warps 14-21  epilogue: TMEM -> exact int64 partials of the item
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int RT_ASL = 8, RT_BSL = 4, RT_EPI = 8;
+constexpr int RT_THREADS = 32 * (2 + RT_ASL + RT_BSL + RT_EPI);
+constexpr int RT_STG = 4, RT_NBUF = 2;             // input ring depth covers the load latency
+constexpr int RT_ITEM_MAX = 8192;                      // rows per item (int32 accumulators)
+constexpr int RT_NACC = 7;                             // acc_0 .. acc_6 (p + q <= 6)
+constexpr uint32_t RT_A_BYTES = 4 * 4096;              // 32 rows x 128 fp32 (4 swizzled boxes)
+constexpr uint32_t RT_U_BYTES = 32 * 64 * 8;           // 32 rows x k <= 64 fp64
+constexpr uint32_t RT_STAGE = 33 * 1024;               // A + Ups + dinv (128 B), 1024-aligned stride
+
+struct RtArgs {
+    int64_t n;
+    int D, k, NP, nD;
+    int64_t RB, nitems;
+    const double *U;
+    const float *dinv;
+    const uint32_t *featmax;                           // [D] bits of max_i |R'_ij|
+    const unsigned long long *colmax;                  // [k] bits of max_i dinv_i Ups_il
+    long long *g0, *g1;                                // [nitems][NP][128]
+};
+
+__device__ __forceinline__ int exp_f32bits(uint32_t b) {       // smallest e with m < 2^e (0 for m = 0)
+    const float m = __uint_as_float(b);
+    int e = 0;
+    if (m > 0.f) frexpf(m, &e);
+    return e;
+}
+__device__ __forceinline__ int exp_f64bits(unsigned long long b) {
+    const double m = __longlong_as_double((long long)b);
+    int e = 0;
+    if (m > 0.0) frexp(m, &e);
+    return max(e, -900);                                // tiny / zero columns: any scale works
+}
+
+// bytes 0..5 of the 48-bit integers in the low mantissa bits of z[0..3] -> w[p] = byte 5 - p of
+// each (byte e = element e)
+__device__ __forceinline__ void pack6(const double (&z)[4], uint32_t (&w)[OZ_SL]) {
+    uint32_t L[4], H[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const unsigned long long zb = (unsigned long long)__double_as_longlong(z[e]);
+        L[e] = (uint32_t)zb;
+        H[e] = (uint32_t)(zb >> 32) & 0xFFFFu;
+    }
+    const uint32_t t0 = __byte_perm(L[0], L[1], 0x5140), t1 = __byte_perm(L[2], L[3], 0x5140);
+    const uint32_t u0 = __byte_perm(L[0], L[1], 0x7362), u1 = __byte_perm(L[2], L[3], 0x7362);
+    w[5] = __byte_perm(t0, t1, 0x5410);
+    w[4] = __byte_perm(t0, t1, 0x7632);
+    w[3] = __byte_perm(u0, u1, 0x5410);
+    w[2] = __byte_perm(u0, u1, 0x7632);
+    const uint32_t h0 = __byte_perm(H[0], H[1], 0x5140), h1 = __byte_perm(H[2], H[3], 0x5140);
+    w[1] = __byte_perm(h0, h1, 0x5410);
+    w[0] = __byte_perm(h0, h1, 0x7632);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(RT_THREADS, 1) oz_rtu_kernel(const __grid_constant__ CUtensorMap mapA, RtArgs g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr uint32_t BPLANE = NP * 32;                           // one B digit plane (NP x 32 bytes)
+    constexpr uint32_t BUF = OZ_SL * OZ_PLANE + OZ_SL * BPLANE;    // A planes then B planes
+    const uint32_t buf_off = RT_STG * RT_STAGE;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + buf_off + RT_NBUF * BUF);
+    uint64_t *afull = bars, *aempty = afull + RT_STG, *sready = aempty + RT_STG, *sfree = sready + RT_NBUF;
+    uint64_t *tfull = sfree + RT_NBUF, *tempty = tfull + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t TMEM_COLS = (RT_NACC * NP <= 128) ? 128 : (RT_NACC * NP <= 256 ? 256 : 512);
+    constexpr int NSL = RT_ASL + RT_BSL;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < RT_STG; ++b) {
+            mbar_init(smem_u32(&afull[b]), 1);
+            mbar_init(smem_u32(&aempty[b]), NSL);
+        }
+        for (int b = 0; b < RT_NBUF; ++b) {
+            mbar_init(smem_u32(&sready[b]), NSL);
+            mbar_init(smem_u32(&sfree[b]), 1);
+        }
+        mbar_init(smem_u32(tfull), 1);
+        mbar_init(smem_u32(tempty), RT_EPI);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            int64_t gc = 0;
+            for (int64_t w = blockIdx.x; w < g.nitems; w += gridDim.x) {
+                const int64_t rb = w / g.nD;
+                const int t = (int)(w - rb * g.nD);
+                const int64_t row0 = rb * g.RB, rows = min(g.RB, g.n - row0);
+                const int nch = (int)((rows + 31) / 32);
+                for (int c = 0; c < nch; ++c, ++gc) {
+                    const int s = (int)(gc % RT_STG);
+                    if (gc >= RT_STG) mbar_wait(smem_u32(&aempty[s]), (uint32_t)(((gc / RT_STG) - 1) & 1));
+                    const int64_t r0 = row0 + 32 * c;
+                    const int nv = (int)(g.n - r0 < 32 ? g.n - r0 : 32);
+                    uint8_t *st = smem + s * RT_STAGE;
+                    double *su = reinterpret_cast<double *>(st + RT_A_BYTES);
+                    float *sd = reinterpret_cast<float *>(st + RT_A_BYTES + RT_U_BYTES);
+                    const uint32_t ub = (uint32_t)nv * g.k * 8, ubulk = ub & ~15u;
+                    const uint32_t db = (uint32_t)nv * 4, dbulk = db & ~15u;
+                    // tails that are not 16-byte multiples: plain copies before the arrive (release)
+                    if (ub != ubulk) su[ubulk / 8] = g.U[r0 * g.k + ubulk / 8];
+                    for (uint32_t o = dbulk; o < db; o += 4) sd[o / 4] = g.dinv[r0 + o / 4];
+                    const uint32_t full = smem_u32(&afull[s]);
+                    mbar_expect_tx(full, RT_A_BYTES + ubulk + dbulk);
+#pragma unroll
+                    for (int bx = 0; bx < 4; ++bx) tma_load_2d(smem_u32(st + bx * 4096), &mapA, full, t * 128 + 32 * bx, (int)r0);
+                    if (ubulk) bulk_g2s(smem_u32(su), g.U + r0 * g.k, ubulk, full);
+                    if (dbulk) bulk_g2s(smem_u32(sd), g.dinv + r0, dbulk, full);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        int64_t gc = 0;
+        int i = 0;
+        for (int64_t w = blockIdx.x; w < g.nitems; w += gridDim.x, ++i) {
+            const int64_t rb = w / g.nD;
+            const int64_t row0 = rb * g.RB, rows = min(g.RB, g.n - row0);
+            const int nch = (int)((rows + 31) / 32);
+            if (i > 0) mbar_wait(smem_u32(tempty), (uint32_t)((i - 1) & 1));
+            fence_after();
+            for (int c = 0; c < nch; ++c, ++gc) {
+                const int b = (int)(gc % RT_NBUF);
+                mbar_wait(smem_u32(&sready[b]), (uint32_t)((gc / RT_NBUF) & 1));
+                fence_after();
+                if (lane == 0) {
+                    const uint32_t abase = smem_u32(smem + buf_off + b * BUF);
+                    const uint32_t bbase = abase + OZ_SL * OZ_PLANE;
+                    // the 26 pairs p + q <= 6 in 9 MMAs; the first three initialise acc_0..3,
+                    // acc_4..5 and acc_6 (an MMA's accumulate flag covers all of its N columns)
+#pragma unroll
+                    for (int u = 0; u < 9; ++u) {
+                        constexpr int P[9] = {0, 0, 2, 1, 1, 2, 3, 4, 5};
+                        constexpr int Q0[9] = {0, 4, 4, 0, 4, 0, 0, 0, 0};
+                        constexpr int NQ[9] = {4, 2, 1, 4, 2, 4, 4, 3, 2};
+                        const uint64_t da = desc_kmajor_noswz(abase + P[u] * OZ_PLANE, 128, 256);
+                        const uint64_t dbd = desc_kmajor_noswz(bbase + (uint32_t)Q0[u] * BPLANE, 128, 256);
+                        const uint32_t acc = (c > 0 || u >= 3) ? 1u : 0u;
+                        // s8 (R' digits) x u8 (dinv.Ups digits) -> s32
+                        const uint32_t idesc = (2u << 4) | (1u << 7) | (0u << 10) |
+                                               ((uint32_t)((NQ[u] * NP) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+                        mma_i8(tmem_base + (uint32_t)((P[u] + Q0[u]) * NP), da, dbd, idesc, acc);
+                    }
+                    mma_commit(smem_u32(&sfree[b]));
+                    if (c == nch - 1) mma_commit(smem_u32(tfull));
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp < 2 + NSL) {
+        // ---------------- slicers ----------------
+        const bool is_a = warp < 2 + RT_ASL;
+        const int sw = is_a ? warp - 2 : warp - 2 - RT_ASL;
+        const int bx = sw & 3, h = is_a ? (sw >> 2) : (sw >> 1), ch = sw & 1;
+        const int l = 32 * ch + lane;                              // B: column
+        const bool lok = !is_a && l < g.k;
+        double sB = 0.0;
+        if (lok) sB = pow2d(47 - exp_f64bits(g.colmax[l]));
+        int64_t gc = 0;
+        for (int64_t w = blockIdx.x; w < g.nitems; w += gridDim.x) {
+            const int64_t rb = w / g.nD;
+            const int t = (int)(w - rb * g.nD);
+            const int64_t row0 = rb * g.RB, rows = min(g.RB, g.n - row0);
+            const int nch = (int)((rows + 31) / 32);
+            const int f = t * 128 + 32 * bx + lane;                // A: feature
+            const double sA = pow2d(46 - (is_a && f < g.D ? exp_f32bits(g.featmax[f]) : 0));
+            for (int c = 0; c < nch; ++c, ++gc) {
+                const int s = (int)(gc % RT_STG);
+                mbar_wait(smem_u32(&afull[s]), (uint32_t)((gc / RT_STG) & 1));
+                const uint8_t *st = smem + s * RT_STAGE;
+                uint32_t wd[4][OZ_SL];
+                if (is_a) {
+                    const uint8_t *box = st + bx * 4096;
+                    float x[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int r = 16 * h + u;
+                        x[u] = *reinterpret_cast<const float *>(box + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        double z[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) z[e] = __fma_rn((double)x[4 * q + e], sA, 4644889027444864.0);   // 2^52 + beta
+                        pack6(z, wd[q]);
+#pragma unroll
+                        for (int p = 0; p < OZ_SL; ++p) wd[q][p] ^= 0x80808080u;
+                    }
+                } else {
+                    const double *su = reinterpret_cast<const double *>(st + RT_A_BYTES);
+                    const float *sd = reinterpret_cast<const float *>(st + RT_A_BYTES + RT_U_BYTES);
+                    const int64_t r0 = row0 + 32 * c;
+                    const int nv = (int)(g.n - r0 < 32 ? g.n - r0 : 32);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        double z[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int r = 16 * h + 4 * q + e;
+                            const bool ok = lok && r < nv;
+                            const double v = ok ? su[r * g.k + l] : 0.0;
+                            const double sc = ok ? (double)sd[r] * sB : 0.0;
+                            z[e] = __fma_rn(v, sc, 4503599627370496.0);                                  // 2^52 + G
+                        }
+                        pack6(z, wd[q]);
+                    }
+                }
+                uint32_t dep = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dep |= wd[q][0] | wd[q][OZ_SL - 1];
+                dep = __reduce_or_sync(0xffffffffu, dep);
+                if (lane == 0)
+                    asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %1, 0xdeadbeef;\n@q mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+                                     smem_u32(&aempty[s])),
+                                 "r"(dep)
+                                 : "memory");
+                const int b = (int)(gc % RT_NBUF);
+                if (gc >= RT_NBUF) mbar_wait(smem_u32(&sfree[b]), (uint32_t)(((gc / RT_NBUF) - 1) & 1));
+                uint8_t *sb = smem + buf_off + b * BUF;
+                if (is_a) {
+                    const int m = 32 * bx + lane;
+                    const uint32_t off = (uint32_t)((m >> 3) * 256 + h * 128 + (m & 7) * 16);
+#pragma unroll
+                    for (int p = 0; p < OZ_SL; ++p)
+                        *reinterpret_cast<uint4 *>(sb + p * OZ_PLANE + off) = make_uint4(wd[0][p], wd[1][p], wd[2][p], wd[3][p]);
+                } else if (l < NP) {
+                    const uint32_t off = (uint32_t)((l >> 3) * 256 + h * 128 + (l & 7) * 16);
+#pragma unroll
+                    for (int p = 0; p < OZ_SL; ++p)
+                        *reinterpret_cast<uint4 *>(sb + OZ_SL * OZ_PLANE + p * BPLANE + off) =
+                            make_uint4(wd[0][p], wd[1][p], wd[2][p], wd[3][p]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&sready[b]));
+            }
+        }
+    } else {
+        // ---------------- epilogue: item partials (exact int64) ----------------
+        const int e = warp - 2 - NSL;
+        const int q4 = warp & 3, chh = e >> 2;
+        constexpr int HALF = NP / 2;
+        int i = 0;
+        for (int64_t w = blockIdx.x; w < g.nitems; w += gridDim.x, ++i) {
+            mbar_wait_sleep(smem_u32(tfull), (uint32_t)(i & 1));
+            fence_after();
+            const int jj = 32 * q4 + lane;
+#pragma unroll 1
+            for (int cb = chh * HALF; cb < (chh + 1) * HALF; cb += 4) {
+                uint32_t v[RT_NACC][4];
+#pragma unroll
+                for (int s = 0; s < RT_NACC; ++s)
+                    tmem_ld4_nowait(tmem_base + ((uint32_t)(32 * q4) << 16) + (uint32_t)(s * NP + cb), v[s]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const long long a0 = (long long)(int32_t)v[0][j] * 65536 + (long long)(int32_t)v[1][j] * 256 +
+                                         (long long)(int32_t)v[2][j];
+                    const long long a1 = ((long long)(int32_t)v[3][j] * 65536 + (long long)(int32_t)v[4][j] * 256 +
+                                          (long long)(int32_t)v[5][j]) * 256 + (long long)(int32_t)v[6][j];
+                    const int64_t o = (w * NP + cb + j) * 128 + jj;
+                    g.g0[o] = a0;
+                    g.g1[o] = a1;
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(tempty));
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// bits of max_i |A_ij| per column (atomicMax on the bit patterns of nonnegative floats: order free)
+__global__ void oz_featmax_kernel(const float *__restrict__ A, int64_t n, int D, int64_t rows_per,
+                                  uint32_t *__restrict__ mx) {
+    const int64_t r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+        int64_t r = r0;
+        for (; r + 4 <= r1; r += 4) {
+            m0 = fmaxf(m0, fabsf(A[r * D + c]));
+            m1 = fmaxf(m1, fabsf(A[(r + 1) * D + c]));
+            m2 = fmaxf(m2, fabsf(A[(r + 2) * D + c]));
+            m3 = fmaxf(m3, fabsf(A[(r + 3) * D + c]));
+        }
+        for (; r < r1; ++r) m0 = fmaxf(m0, fabsf(A[r * D + c]));
+        atomicMax(&mx[c], __float_as_uint(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3))));
+    }
+}
+
+// bits of max_i fl(dinv_i U_il) per column (U >= 0, k <= 64): a warp per row (lane: columns l and
+// l + 32, coalesced), 4 rows in flight per warp, block maxima combined by atomicMax (order free)
+__global__ void __launch_bounds__(256) oz_colmax_kernel(const double *__restrict__ U, const float *__restrict__ dinv,
+                                                        int64_t n, int k, int64_t rows_per,
+                                                        unsigned long long *__restrict__ mx) {
+    __shared__ double sm[8][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+    const bool v0 = lane < k, v1 = lane + 32 < k;
+    double m0 = 0.0, m1 = 0.0;
+    int64_t r = r0 + w;
+    for (; r + 24 < r1; r += 32) {
+        double a[4], b[4];
+        float dv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t rr = r + 8 * u;
+            dv[u] = dinv[rr];
+            a[u] = v0 ? U[rr * k + lane] : 0.0;
+            b[u] = v1 ? U[rr * k + lane + 32] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            m0 = fmax(m0, (double)dv[u] * a[u]);
+            m1 = fmax(m1, (double)dv[u] * b[u]);
+        }
+    }
+    for (; r < r1; r += 8) {
+        const double dv = (double)dinv[r];
+        if (v0) m0 = fmax(m0, dv * U[r * k + lane]);
+        if (v1) m1 = fmax(m1, dv * U[r * k + lane + 32]);
+    }
+    sm[w][lane] = m0;
+    sm[w][lane + 32] = m1;
+    __syncthreads();
+    if (threadIdx.x < 64 && (int)threadIdx.x < k) {
+        double m = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m = fmax(m, sm[i][threadIdx.x]);
+        atomicMax(&mx[threadIdx.x], (unsigned long long)__double_as_longlong(m));
+    }
+}
+
+// one block per (feature tile t, column l): 128 features x 8 groups of row blocks, exact 128-bit
+// sums (the order does not matter), one rounding
+__global__ void __launch_bounds__(1024) oz_rtu_reduce_kernel(const long long *__restrict__ g0,
+                                                             const long long *__restrict__ g1, int D, int k, int NP,
+                                                             int nD, int64_t nrb, const uint32_t *__restrict__ featmax,
+                                                             const unsigned long long *__restrict__ colmax,
+                                                             double *__restrict__ out) {
+    __shared__ __int128 sh[8][128];
+    const int t = blockIdx.x, l = blockIdx.y;
+    const int jj = threadIdx.x & 127, grp = threadIdx.x >> 7;
+    __int128 T = 0;                                     // sum (g0 2^32 + g1): < 2^88, exact
+    for (int64_t rb = grp; rb < nrb; rb += 8) {
+        const int64_t o = ((rb * nD + t) * NP + l) * 128 + jj;
+        T += ((__int128)g0[o] << 32) + (__int128)g1[o];
+    }
+    sh[grp][jj] = T;
+    __syncthreads();
+    const int j = t * 128 + jj;
+    if (grp != 0 || j >= D) return;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) T += sh[i][jj];
+    // T = a 2^40 + b with a (< 2^48), b (< 2^40) exact in fp64: one rounding
+    const long long a = (long long)(T >> 40);
+    const long long b = (long long)(T - ((__int128)a << 40));
+    const double x = (double)a * 1099511627776.0 + (double)b;
+    out[(int64_t)j * k + l] = ldexp(x, exp_f32bits(featmax[j]) + exp_f64bits(colmax[l]) - 61);
+}
+
+CUtensorMap oz_rtu_map(const float *A, int64_t n, int64_t D) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)D * sizeof(float)};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(A), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(TPO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+size_t oz_rtu_smem(int NP) {
+    return 1024 + RT_STG * RT_STAGE + RT_NBUF * (size_t)(OZ_SL * OZ_PLANE + OZ_SL * NP * 32) + 16 * 8 + 16;
+}
+
+struct RtuShape {
+    int NP, nD;
+    int64_t RB, nrb, nitems;
+};
+
+RtuShape rtu_shape(int64_t n, int64_t D, int k) {
+    RtuShape s;
+    s.NP = oz_np(k);
+    s.nD = (int)cdiv(D, 128);
+    // row blocks of <= 8192 rows (multiples of 32), their count rounded so that the items fill
+    // whole waves of the SMs
+    const int64_t sms = sm_count();
+    const int64_t base = cdiv(std::max<int64_t>(n, 1), RT_ITEM_MAX);
+    const int64_t step = sms / std::gcd<int64_t>(sms, (int64_t)s.nD);
+    int64_t nrb = cdiv(base, step) * step;
+    s.RB = std::max<int64_t>(32, cdiv(cdiv(std::max<int64_t>(n, 1), nrb), 32) * 32);
+    s.nrb = cdiv(std::max<int64_t>(n, 1), s.RB);
+    s.nitems = s.nrb * s.nD;
+    return s;
+}
+
+}  // namespace
+
+bool oz_rtu_supported(int64_t n, int64_t D, int k) {
+    return oz_enabled() && n > 0 && k > 32 && k <= 64 && D % 4 == 0 && D >= 4 &&
+           oz_rtu_smem(oz_np(k)) <= 227 * 1024;
+}
+
+size_t oz_rtu_ws(int64_t n, int64_t D, int k) {
+    if (!(k > 32 && k <= 64)) return 0;
+    const RtuShape s = rtu_shape(n, D, k);
+    Arena ar(nullptr, 0);
+    ar.take<long long>((size_t)s.nitems * s.NP * 128);
+    ar.take<long long>((size_t)s.nitems * s.NP * 128);
+    ar.take<unsigned long long>(k);
+    return ar.off + 256;
+}
+
+// bits of max_i |R'_ij| per feature (once per solve: R' is fixed during Alg. 2)
+void oz_featmax(const float *Rp, int64_t n, int64_t D, uint32_t *featmax, cudaStream_t st) {
+    TPO_CUDA(cudaMemsetAsync(featmax, 0, sizeof(uint32_t) * D, st));
+    if (n == 0) return;
+    const int64_t blocks = std::min<int64_t>(8 * sm_count(), cdiv(n, 64));
+    const int64_t rows_per = cdiv(n, blocks);
+    oz_featmax_kernel<<<(unsigned)cdiv(n, rows_per), 256, 0, st>>>(Rp, n, (int)D, rows_per, featmax);
+    TPO_LAUNCH_CHECK();
+}
+
+// RtU = R'^T (dinv . U) (D x k fp64) on the integer tensor cores; featmax from oz_featmax(R').
+void oz_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, const uint32_t *featmax,
+            double *RtU, Arena &ar, cudaStream_t st) {
+    TPO_REQUIRE(oz_rtu_supported(n, D, k), "oz_rtu: unsupported shape");
+    TPO_REQUIRE((reinterpret_cast<uintptr_t>(Rp) & 15) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(dinv) & 15) == 0,
+                "oz_rtu: R', Ups and dinv must be 16-byte aligned");
+    const RtuShape s = rtu_shape(n, D, k);
+    const size_t mark = ar.off;
+    long long *g0 = ar.take<long long>((size_t)s.nitems * s.NP * 128);
+    long long *g1 = ar.take<long long>((size_t)s.nitems * s.NP * 128);
+    unsigned long long *colmax = ar.take<unsigned long long>(k);
+    TPO_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * k, st));
+    {
+        const int64_t blocks = std::min<int64_t>(8 * sm_count(), cdiv(n, 256));
+        const int64_t rows_per = cdiv(n, blocks);
+        oz_colmax_kernel<<<(unsigned)cdiv(n, rows_per), 256, 0, st>>>(U, dinv, n, k, rows_per, colmax);
+        TPO_LAUNCH_CHECK();
+    }
+    RtArgs a{};
+    a.n = n; a.D = (int)D; a.k = k; a.NP = s.NP; a.nD = s.nD;
+    a.RB = s.RB; a.nitems = s.nitems;
+    a.U = U; a.dinv = dinv; a.featmax = featmax; a.colmax = colmax; a.g0 = g0; a.g1 = g1;
+    const CUtensorMap map = oz_rtu_map(Rp, n, D);
+    const size_t sm = oz_rtu_smem(s.NP);
+    const int grid = (int)std::min<int64_t>(s.nitems, sm_count());
+    switch (s.NP) {
+        case 48:
+            TPO_CUDA(cudaFuncSetAttribute(oz_rtu_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            oz_rtu_kernel<48><<<grid, RT_THREADS, sm, st>>>(map, a);
+            break;
+        default:
+            TPO_CUDA(cudaFuncSetAttribute(oz_rtu_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            oz_rtu_kernel<64><<<grid, RT_THREADS, sm, st>>>(map, a);
+            break;
+    }
+    TPO_LAUNCH_CHECK();
+    oz_rtu_reduce_kernel<<<dim3((unsigned)s.nD, (unsigned)k), 1024, 0, st>>>(g0, g1, (int)D, k, s.NP, s.nD, s.nrb,
+                                                                             featmax, colmax, RtU);
+    TPO_LAUNCH_CHECK();
+    ar.off = mark;
+}
+
+
+namespace {
+// rowE (row exponents, as oz_rowexp_kernel) and featmax (bits of per-feature max |A|, as
+// oz_featmax_kernel) in one pass: a warp per row (16-byte loads, 4 rows in flight), a lane keeps
+// the maxima of its 4 NF4 features in registers over all of its rows; block maxima -> atomicMax
+// (order free).  D % 4 == 0, D <= 128 NF4.
+template <int NF4>
+__global__ void __launch_bounds__(256) oz_rstats_kernel(const float *__restrict__ A, int64_t n, int D,
+                                                        int32_t *__restrict__ rowE, uint32_t *__restrict__ featmax) {
+    __shared__ float sm[8][128 * NF4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int D4 = D / 4;
+    float fm[NF4][4];
+#pragma unroll
+    for (int i = 0; i < NF4; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) fm[i][e] = 0.f;
+    const float4 *A4 = reinterpret_cast<const float4 *>(A);
+    const int64_t stride = (int64_t)gridDim.x * 32;
+    for (int64_t r0 = (int64_t)blockIdx.x * 32 + w; r0 < n; r0 += stride) {
+        float m[4];
+        float4 v[4][NF4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t r = r0 + 8 * u;
+#pragma unroll
+            for (int i = 0; i < NF4; ++i) {
+                const int q = lane + 32 * i;
+                v[u][i] = (q < D4 && r < n) ? A4[r * D4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float mm = 0.f;
+#pragma unroll
+            for (int i = 0; i < NF4; ++i) {
+                const float a0 = fabsf(v[u][i].x), a1 = fabsf(v[u][i].y), a2 = fabsf(v[u][i].z), a3 = fabsf(v[u][i].w);
+                fm[i][0] = fmaxf(fm[i][0], a0);
+                fm[i][1] = fmaxf(fm[i][1], a1);
+                fm[i][2] = fmaxf(fm[i][2], a2);
+                fm[i][3] = fmaxf(fm[i][3], a3);
+                mm = fmaxf(mm, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
+            }
+            m[u] = mm;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            for (int o = 16; o; o >>= 1) m[u] = fmaxf(m[u], __shfl_xor_sync(0xffffffffu, m[u], o));
+        if (lane < 4) {
+            const int64_t r = r0 + 8 * lane;
+            const float mu = lane == 0 ? m[0] : lane == 1 ? m[1] : lane == 2 ? m[2] : m[3];
+            if (r < n) {
+                int e = 0;
+                if (mu > 0.f) frexpf(mu, &e);
+                rowE[r] = e;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NF4; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sm[w][4 * (lane + 32 * i) + e] = fm[i][e];
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        float mm = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mm = fmaxf(mm, sm[q][j]);
+        atomicMax(&featmax[j], __float_as_uint(mm));
+    }
+}
+}  // namespace
+
+bool oz_rstats_wanted(int64_t n, int64_t D, int k) {
+    return oz_enabled() && n > 0 && k > 32 && D % 4 == 0 && D <= 512;
+}
+
+void oz_rstats(const float *Rp, int64_t n, int64_t D, int32_t *rowE, uint32_t *featmax, cudaStream_t st) {
+    TPO_REQUIRE(D >= 1 && D <= 512, "oz_rstats: D out of range");
+    TPO_CUDA(cudaMemsetAsync(featmax, 0, sizeof(uint32_t) * D, st));
+    if (n == 0) return;
+    TPO_REQUIRE(D % 4 == 0 && (reinterpret_cast<uintptr_t>(Rp) & 15) == 0, "oz_rstats: R' must be 16-byte aligned rows");
+    const unsigned grid = (unsigned)std::min<int64_t>(8 * sm_count(), cdiv(n, 32));
+    const int nf4 = (int)cdiv(D, 128);
+    if (nf4 <= 1) oz_rstats_kernel<1><<<grid, 256, 0, st>>>(Rp, n, (int)D, rowE, featmax);
+    else if (nf4 <= 2) oz_rstats_kernel<2><<<grid, 256, 0, st>>>(Rp, n, (int)D, rowE, featmax);
+    else oz_rstats_kernel<4><<<grid, 256, 0, st>>>(Rp, n, (int)D, rowE, featmax);
+    TPO_LAUNCH_CHECK();
 }
 
 }  // namespace tpo

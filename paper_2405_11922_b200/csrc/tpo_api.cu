@@ -495,6 +495,7 @@ size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, i
     s += align_up(sizeof(float) * d * d);                // Q
     s += align_up(sizeof(float) * n_u * k) + align_up(sizeof(float) * D * k);   // Gamma, Psi
     s += align_up(sizeof(double) * D);                                           // r
+    s += align_up(sizeof(int32_t) * n_u + 1) + align_up(sizeof(uint32_t) * D + 1);  // R' row exponents, feature maxima
     s += align_up(haar_q_ws_bytes(d));                   // Haar Q runs beside the propagation
     size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d), tpo_features_ws(n_u, d)),
                             std::max(tpo_topk_eig_ws(n_u, D, k, mode, p), tpo_cluster_ws(n_u, D, k)));
@@ -772,6 +773,8 @@ static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
     float *Qd = ar.take<float>(d * d);
     float *Gamma = ar.take<float>(n * k), *Psi = ar.take<float>(D * k);
     double *r = ar.take<double>(D);
+    int32_t *rowE = ar.take<int32_t>(n);
+    uint32_t *featmax = ar.take<uint32_t>(D);
     const size_t haar_bytes = align_up(haar_q_ws_bytes(d));
     Arena har(ar.dry ? nullptr : ar.base + ar.off, haar_bytes);
     ar.take<char>(haar_bytes - 256);
@@ -794,13 +797,19 @@ static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
     TPO_CUDA(cudaEventRecord(ev[1], st));
     TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
     features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
+    RStats rs;                  // R''s row exponents / feature maxima: one pass, shared by a7 and a8
+    if (oz_rstats_wanted(n, D, k)) {
+        oz_rstats(Rp, n, D, rowE, featmax, st);
+        rs.rowE = rowE;
+        rs.featmax = featmax;
+    }
     ar.off = mark;
     TPO_CUDA(cudaEventRecord(ev[2], st));
     std::vector<double> sig(k);
-    topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st, r);
+    topk_eig_impl(Rp, dinv, n, D, k, eig_mode, p, q, Omega, Gamma, sig.data(), Psi, ar, st, r, rs);
     ar.off = mark;
     TPO_CUDA(cudaEventRecord(ev[3], st));
-    cluster_impl(Rp, dinv, n, D, k, Gamma, sig.data(), Psi, Tf, Tg, labels, nullptr, ar, st);
+    cluster_impl(Rp, dinv, n, D, k, Gamma, sig.data(), Psi, Tf, Tg, labels, nullptr, ar, st, rs);
     TPO_CUDA(cudaEventRecord(ev[4], st));
     TPO_CUDA(cudaStreamSynchronize(st));
     if (timings_ms)

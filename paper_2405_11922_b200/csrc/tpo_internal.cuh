@@ -121,15 +121,25 @@ void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, floa
                    double *r_out, Arena &ar, cudaStream_t st);
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y,
                           int64_t b, float *out, Arena &ar, cudaStream_t st);
+// Per-R' statistics of the integer-tensor-core products (oz.cu), computed once per R' inside
+// tpo_run and shared by the top-k (Gamma = R Psi Sigma^-1) and the discretisation (RH, R^T Ups):
+// rowE[i] = row exponents of R', featmax[j] = bits of max_i |R'_ij|; NULL members: not computed.
+struct RStats {
+    const int32_t *rowE = nullptr;
+    const uint32_t *featmax = nullptr;
+};
+// one pass over R' for both (rowE: n, featmax: D); only when k > 32 and D <= 512
+bool oz_rstats_wanted(int64_t n, int64_t D, int k);
+void oz_rstats(const float *Rp, int64_t n, int64_t D, int32_t *rowE, uint32_t *featmax, cudaStream_t st);
 // r_colsum: r = sum_i R'[i] (2d fp64, device) from tpo_features, or NULL to recompute it.
 void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, int32_t mode,
                    int32_t p, int32_t q, const float *Omega, float *Gamma, double *sigma, float *Psi,
-                   Arena &ar, cudaStream_t st, const double *r_colsum = nullptr);
+                   Arena &ar, cudaStream_t st, const double *r_colsum = nullptr, RStats rs = RStats());
 void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cudaStream_t st);
 size_t features_ws_bytes(int64_t n, int64_t d);
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
-                  int32_t *iters_used, Arena &ar, cudaStream_t st);
+                  int32_t *iters_used, Arena &ar, cudaStream_t st, RStats rs = RStats());
 
 // G: d x d fp64, on the device when G_on_device, else host memory
 void haar_q_device(const double *G, bool G_on_device, int64_t d, float *Q_out, Arena &ar, cudaStream_t st);
@@ -210,7 +220,7 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
 size_t dgemm_ws(int64_t M, int64_t N, int64_t K);
 // ONMF passes over R' (onmf.cu): RtU = R'^T (dinv . U) (D x k), fp64 (RH = dinv . (R' H) is tsgemm_AW_f64).
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU,
-              Arena &ar, cudaStream_t st);
+              Arena &ar, cudaStream_t st, const uint32_t *featmax = nullptr);
 size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k);
 // fp64 tensor-path (DMMA) products of the discretisation (ts64.cu).  ts64_enabled(): TPO_TS64=0
 // selects the CUDA-core kernels of dense.cu / onmf.cu / cluster.cu (A/B measurement only).
@@ -232,6 +242,13 @@ size_t oz_aw_ws(int64_t K, int N);
 void oz_rowexp(const float *A, int64_t lda, int64_t n, int K, int32_t *E, cudaStream_t st);
 void oz_aw_f64(const float *A, int64_t lda, const float *rs, const int32_t *rowE, const double *W, int64_t n, int K,
                int N, double *out, int64_t ldo, Arena &ar, cudaStream_t st);
+// Alg. 2's RtU = R'^T (dinv . Ups) (D x k fp64) on the integer tensor cores (oz.cu), 32 < k <= 64:
+// featmax = bits of R''s per-feature max |R'| (oz_featmax, once per solve).
+bool oz_rtu_supported(int64_t n, int64_t D, int k);
+size_t oz_rtu_ws(int64_t n, int64_t D, int k);
+void oz_featmax(const float *Rp, int64_t n, int64_t D, uint32_t *featmax, cudaStream_t st);
+void oz_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, const uint32_t *featmax,
+            double *RtU, Arena &ar, cudaStream_t st);
 // Alg. 3 assignment on the integer tensor cores (oz.cu), 32 < k <= 64: Ups digits prepared once
 // per solve (Ups is fixed during Alg. 3), then one certified argmax per iteration.
 struct OzAssign {
@@ -251,6 +268,8 @@ struct RhPlan {
 };
 RhPlan rh_plan(const float *Rp, int64_t n, int64_t D, int k, Arena &ar, cudaStream_t st);
 RhPlan rh_plan_at(int32_t *rowE, const float *Rp, int64_t n, int64_t D, int k, cudaStream_t st);
+// the plan with precomputed row exponents (oz_rstats), or computed into the arena when NULL
+RhPlan rh_plan_pre(const int32_t *rowE, const float *Rp, int64_t n, int64_t D, int k, Arena &ar, cudaStream_t st);
 size_t rh_plan_ws(int64_t n);
 size_t rh_apply_ws(int64_t D, int k);
 void rh_apply(const RhPlan &p, const float *Rp, const float *dinv, const double *H, int64_t n, int64_t D, int k,
@@ -258,6 +277,7 @@ void rh_apply(const RhPlan &p, const float *Rp, const float *dinv, const double 
 void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, int64_t n, int K, int N,
                const double *cs, double *out, int64_t ldo, cudaStream_t st);
 void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);
+bool ts_xw_inplace_f64(double *X, int64_t n, int k, const double *W, cudaStream_t st);
 size_t ts_rtu_ws(int64_t n, int64_t D, int k);
 size_t ts_affinity_ws(int64_t D, int64_t b);
 size_t ts_affinity_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk);

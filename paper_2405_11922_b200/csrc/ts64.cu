@@ -752,6 +752,8 @@ void dm_launch(const DmArgs &a, int nblk, cudaStream_t st) {
 }
 template <int NT>
 void dm_store_f32(const DmArgs &a, int nblk, cudaStream_t st) { dm_launch<float, DM_STORE, NT>(a, nblk, st); }
+template <int NT>
+void dm_store_f64(const DmArgs &a, int nblk, cudaStream_t st) { dm_launch<double, DM_STORE, NT>(a, nblk, st); }
 // the Ups update reads whole rows of Ups (den = Ups M) and overwrites them: one column block
 template <int NT>
 void dm_ups(const DmArgs &a, cudaStream_t st) { dm_launch<double, DM_UPS, NT>(a, 1, st); }
@@ -879,6 +881,21 @@ void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, in
     int NT, nblk;
     col_tiling(N, NT, nblk);
     TPO_NT13(dm_store_f32, NT, a, nblk, st);
+}
+
+// X <- X W in place (X n x k fp64, W k x k fp64) on the fp64 tensor path when the k columns form
+// one column block (k <= 56: every CTA reads its rows whole before writing them, like the Ups
+// update); returns false (nothing done) otherwise.
+bool ts_xw_inplace_f64(double *X, int64_t n, int k, const double *W, cudaStream_t st) {
+    if (!ts64_enabled()) return false;
+    int NT, nblk;
+    col_tiling(k, NT, nblk);
+    if (nblk != 1) return false;
+    if (n == 0) return true;
+    DmArgs a{};
+    a.A = X; a.lda = k; a.W = W; a.ldw = k; a.n = n; a.K = k; a.N = k; a.out = X; a.ldo = k;
+    TPO_NT13(dm_store_f64, NT, a, 1, st);
+    return true;
 }
 
 // Ups <- Ups . sqrt(max(RH,0) / (max(Ups M,0) + eps))  (Eq. update-Y with the R9 clamps), in place;

@@ -170,6 +170,21 @@ def rowgemm_f64(A: torch.Tensor, W: torch.Tensor, rs=None, out=None, stream=None
     return out
 
 
+def onmf_rtu(Rp: torch.Tensor, dinv: torch.Tensor, U: torch.Tensor, out=None, stream=None):
+    """tpo_shard_onmf_rtu over all rows: RtU = R'^T (dinv . U) (D x k fp64; Alg. 2's R^T Ups)."""
+    n, D = Rp.shape
+    _need(Rp, torch.float32, "Rp")
+    _need(dinv, torch.float32, "dinv", (n,))
+    _need(U, torch.float64, "U")
+    k = U.shape[1]
+    out = torch.empty(D, k, dtype=torch.float64, device=Rp.device) if out is None else out
+    L = lib()
+    ws = _ws(L.tpo_shard_solver_ws(n, D // 2, k), Rp.device)
+    check(L.tpo_shard_onmf_rtu(_ptr(Rp), _ptr(dinv), _ptr(U), n, D, k, _ptr(out), _ptr(ws), ws.numel(),
+                               _stream(stream)))
+    return out
+
+
 def affinity_matvec_rfree(Zhat: torch.Tensor, Q: torch.Tensor, Y: torch.Tensor, chunk_rows: int = 0, out=None,
                           stream=None):
     """a6 without materialising R' (tpo_affinity_matvec_rfree): R' rows recomputed from Zhat in chunks."""

@@ -93,3 +93,46 @@ def test_rowgemm_f64_many_tiles(tpo):
     idx = np.concatenate([idx, np.arange(n - 200, n)])
     ref = _ref(A[idx], W, rs[idx])
     assert np.all(np.abs(out[idx] - ref) <= _bound(A[idx], W, rs[idx]))
+
+
+# --------------------------------------------------------------------------------------------
+# Alg. 2's R^T Ups = R'^T (dinv . Ups) on the integer tensor cores (oz_rtu_kernel, 32 < k <= 64)
+# --------------------------------------------------------------------------------------------
+def _rtu_case(rng, n, D, k, kind):
+    A = (np.sqrt(np.e / (D // 2)) * np.sin(rng.uniform(-6, 6, (n, D)))).astype(np.float32)
+    if kind == "cos":                                  # mostly positive columns: coherent sums
+        A[:, D // 2:] = np.abs(A[:, D // 2:])
+    U = np.abs(rng.normal(size=(n, k))) / np.sqrt(n) + 1e-12
+    if kind == "range":
+        U *= 10.0 ** rng.uniform(-9, 2, (n, k))
+        U[:, 0] = 1e-12                               # R9 floor column
+        A[::13] = 0.0
+    dinv = rng.uniform(0.2, 3.0, n).astype(np.float32)
+    return A, U, dinv
+
+
+@pytest.mark.parametrize("n,D,k,kind", [(5000, 256, 50, "sin"), (70001, 260, 33, "cos"), (4099, 256, 49, "range"),
+                                        (7, 256, 64, "sin"), (40000, 512, 64, "range"), (148 * 32 + 5, 128, 40, "cos")])
+def test_onmf_rtu_integer_tensor_cores(tpo, monkeypatch, n, D, k, kind):
+    """oz R^T Ups (B = dinv . Ups): within the kernel's rigorous bound of the exact sum, per row
+    2^-52 2^EA 2^EB (dropped digit pairs, 2^E <= 2 max) + 2^-47 2^EA B_il + 2^-48 2^EB |R'_ij|
+    (roundings); within 4e-14 of the L1 mass sum_i |R'_ij| B_il; close to the fp64 DMMA path;
+    bitwise deterministic; ragged rows / feature tiles / odd k (the 8-byte Ups tail copy)."""
+    rng = np.random.default_rng(n + D + k)
+    A, U, dinv = _rtu_case(rng, n, D, k, kind)
+    B = dinv.astype(np.float64)[:, None] * U
+    ref = A.astype(np.float64).T @ B
+    l1 = np.abs(A.astype(np.float64)).T @ B
+    dA, dU, dd = torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda(), torch.from_numpy(dinv).cuda()
+    out = tpo.onmf_rtu(dA, dd, dU).cpu().numpy()
+    err = np.abs(out - ref)
+    mA, mB = 2 * np.abs(A).max(axis=0).astype(np.float64), 2 * B.max(axis=0)
+    rig = (2.0 ** -52 * n * np.outer(mA, mB) + 2.0 ** -47 * np.outer(mA, B.sum(axis=0)) +
+           2.0 ** -48 * np.outer(np.abs(A.astype(np.float64)).sum(axis=0), mB)) * 1.01 + 1e-300
+    assert np.all(err <= rig), (err / rig).max()
+    assert np.all(err <= 4e-14 * l1 + 1e-300), (err / (l1 + 1e-300)).max()
+    assert np.array_equal(out, tpo.onmf_rtu(dA, dd, dU).cpu().numpy())     # deterministic
+    monkeypatch.setenv("TPO_OZ", "0")
+    dm = tpo.onmf_rtu(dA, dd, dU).cpu().numpy()
+    monkeypatch.delenv("TPO_OZ")
+    assert np.all(np.abs(dm - out) <= 4e-14 * l1 + 1e-300)
