@@ -965,12 +965,10 @@ namespace {
 
 constexpr int RT_ASL = 8, RT_BSL = 4, RT_EPI = 8;
 constexpr int RT_THREADS = 32 * (2 + RT_ASL + RT_BSL + RT_EPI);
-constexpr int RT_STG = 4, RT_NBUF = 2;             // input ring depth covers the load latency
+constexpr int RT_STG = 4;                          // input ring depth covers the load latency
 constexpr int RT_ITEM_MAX = 8192;                      // rows per item (int32 accumulators)
 constexpr int RT_NACC = 7;                             // acc_0 .. acc_6 (p + q <= 6)
 constexpr uint32_t RT_A_BYTES = 4 * 4096;              // 32 rows x 128 fp32 (4 swizzled boxes)
-constexpr uint32_t RT_U_BYTES = 32 * 64 * 8;           // 32 rows x k <= 64 fp64
-constexpr uint32_t RT_STAGE = 33 * 1024;               // A + Ups + dinv (128 B), 1024-aligned stride
 
 struct RtArgs {
     int64_t n;
@@ -981,7 +979,12 @@ struct RtArgs {
     const uint32_t *featmax;                           // [D] bits of max_i |R'_ij|
     const unsigned long long *colmax;                  // [k] bits of max_i dinv_i Ups_il
     long long *g0, *g1;                                // [nitems][NP][128]
+    uint32_t stage, ubytes;                            // ring stage stride (A + Ups + dinv), Ups region
 };
+
+// stage = R' tile (16 KB) + 32 Ups rows + 32 dinv, 1024-aligned (the TMA boxes use SWIZZLE_128B)
+inline uint32_t rt_ubytes(int k) { return (uint32_t)((32 * k * 8 + 15) / 16 * 16); }
+inline uint32_t rt_stage(int k) { return (RT_A_BYTES + rt_ubytes(k) + 128 + 1023) / 1024 * 1024; }
 
 __device__ __forceinline__ int exp_f32bits(uint32_t b) {       // smallest e with m < 2^e (0 for m = 0)
     const float m = __uint_as_float(b);
@@ -1017,12 +1020,13 @@ __device__ __forceinline__ void pack6(const double (&z)[4], uint32_t (&w)[OZ_SL]
     w[0] = __byte_perm(h0, h1, 0x7632);
 }
 
-template <int NP>
+template <int NP, int RT_NBUF>
 __global__ void __launch_bounds__(RT_THREADS, 1) oz_rtu_kernel(const __grid_constant__ CUtensorMap mapA, RtArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr uint32_t BPLANE = NP * 32;                           // one B digit plane (NP x 32 bytes)
     constexpr uint32_t BUF = OZ_SL * OZ_PLANE + OZ_SL * BPLANE;    // A planes then B planes
+    const uint32_t RT_STAGE = g.stage, RT_U_BYTES = g.ubytes;
     const uint32_t buf_off = RT_STG * RT_STAGE;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + buf_off + RT_NBUF * BUF);
     uint64_t *afull = bars, *aempty = afull + RT_STG, *sready = aempty + RT_STG, *sfree = sready + RT_NBUF;
@@ -1358,9 +1362,12 @@ CUtensorMap oz_rtu_map(const float *A, int64_t n, int64_t D) {
     return m;
 }
 
-size_t oz_rtu_smem(int NP) {
-    return 1024 + RT_STG * RT_STAGE + RT_NBUF * (size_t)(OZ_SL * OZ_PLANE + OZ_SL * NP * 32) + 16 * 8 + 16;
+size_t oz_rtu_smem(int NP, int k, int nbuf) {
+    return 1024 + RT_STG * (size_t)rt_stage(k) + nbuf * (size_t)(OZ_SL * OZ_PLANE + OZ_SL * NP * 32) + 16 * 8 + 16;
 }
+// two digit-plane buffers: a third one (it fits beside the 4-stage ring for k <= 50) measured
+// slower on large (1.51 vs 1.45 ms)
+int rt_nbuf(int NP, int k) { (void)NP; (void)k; return 2; }
 
 struct RtuShape {
     int NP, nD;
@@ -1387,7 +1394,7 @@ RtuShape rtu_shape(int64_t n, int64_t D, int k) {
 
 bool oz_rtu_supported(int64_t n, int64_t D, int k) {
     return oz_enabled() && n > 0 && k > 32 && k <= 64 && D % 4 == 0 && D >= 4 &&
-           oz_rtu_smem(oz_np(k)) <= 227 * 1024;
+           oz_rtu_smem(oz_np(k), k, 2) <= 227 * 1024;
 }
 
 size_t oz_rtu_ws(int64_t n, int64_t D, int k) {
@@ -1433,19 +1440,22 @@ void oz_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const doub
     a.n = n; a.D = (int)D; a.k = k; a.NP = s.NP; a.nD = s.nD;
     a.RB = s.RB; a.nitems = s.nitems;
     a.U = U; a.dinv = dinv; a.featmax = featmax; a.colmax = colmax; a.g0 = g0; a.g1 = g1;
+    a.stage = rt_stage(k); a.ubytes = rt_ubytes(k);
     const CUtensorMap map = oz_rtu_map(Rp, n, D);
-    const size_t sm = oz_rtu_smem(s.NP);
+    const int nbuf = rt_nbuf(s.NP, k);
+    const size_t sm = oz_rtu_smem(s.NP, k, nbuf);
     const int grid = (int)std::min<int64_t>(s.nitems, sm_count());
-    switch (s.NP) {
-        case 48:
-            TPO_CUDA(cudaFuncSetAttribute(oz_rtu_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            oz_rtu_kernel<48><<<grid, RT_THREADS, sm, st>>>(map, a);
-            break;
-        default:
-            TPO_CUDA(cudaFuncSetAttribute(oz_rtu_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            oz_rtu_kernel<64><<<grid, RT_THREADS, sm, st>>>(map, a);
-            break;
+#define TPO_RTU_LAUNCH(NPV, NB)                                                                                    \
+    {                                                                                                              \
+        TPO_CUDA(cudaFuncSetAttribute(oz_rtu_kernel<NPV, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+        oz_rtu_kernel<NPV, NB><<<grid, RT_THREADS, sm, st>>>(map, a);                                            \
     }
+    if (s.NP == 48) {
+        TPO_RTU_LAUNCH(48, 2)
+    } else {
+        TPO_RTU_LAUNCH(64, 2)
+    }
+#undef TPO_RTU_LAUNCH
     TPO_LAUNCH_CHECK();
     oz_rtu_reduce_kernel<<<dim3((unsigned)s.nD, (unsigned)k), 1024, 0, st>>>(g0, g1, (int)D, k, s.NP, s.nD, s.nrb,
                                                                              featmax, colmax, RtU);
