@@ -378,7 +378,8 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
     // iteration: the residual falls by a steady factor per filter round (measured between the last
     // two Rayleigh-Ritz steps), so rounds whose predicted residual is still above the tolerance
     // filter and re-orthonormalise only; Rayleigh-Ritz runs when the predicted residual reaches the
-    // tolerance.  Stopping is always decided on explicit residuals.
+    // tolerance.  Only for b + 1 >= 64, where the O(b^3) host eigensolve outweighs a filter round
+    // (a wrong prediction costs one more round).  Stopping is always decided on explicit residuals.
     int last_rr = -1;
     double last_rel = 0.0, rate = 0.0;
     static const bool trace = getenv("TPO_TRACE_EIG") != nullptr;
@@ -402,7 +403,7 @@ void gram_topk(const double *G, double *u, int64_t D, int32_t k, std::vector<dou
             }
             TPO_CUDA(cudaMemcpyAsync(V, Y1, sizeof(double) * D * b, cudaMemcpyDeviceToDevice, st));
             orth_against_u();
-            if (round < max_rounds && last_rr >= 1 && rate > 1.0 &&
+            if (bz >= 64 && round < max_rounds && last_rr >= 1 && rate > 1.0 &&
                 last_rel / pow(rate, (double)(round - last_rr)) > 1e-9)
                 continue;                                  // predicted residual still above 1e-9
         }
@@ -611,7 +612,15 @@ void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
         TPO_CUDA(cudaMemcpyAsync(&hdev, dev, sizeof(double), cudaMemcpyDeviceToHost, st));
         TPO_CUDA(cudaStreamSynchronize(st));
         if (hdev <= 1e-6) break;
-        if (!ts_xw_inplace_f64(Gamma, n, k, ci, st)) apply_upper_rows(Gamma, n, k, ci, st);
+        if (!ts_xw_inplace_f64(Gamma, n, k, ci, st)) {       // k > 56: two column blocks, out of place
+            const size_t m2 = ar.off;
+            double *tmp = ar.take<double>((size_t)n * k);
+            if (ts_xw_f64(Gamma, n, k, ci, tmp, st))
+                TPO_CUDA(cudaMemcpyAsync(Gamma, tmp, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
+            else
+                apply_upper_rows(Gamma, n, k, ci, st);
+            ar.off = m2;
+        }
         if (hdev < 1e-2) break;
     }
     check_flag(flag, st, "CholeskyQR2 polish of Gamma");

@@ -73,6 +73,65 @@ void colsum_run(const float *Rp, int64_t n, int D, int G, double *part, double *
     TPO_LAUNCH_CHECK();
 }
 
+// dinv_kernel fused with R''s row exponents and per-feature maxima (the integer-tensor-core
+// products' statistics, see oz_rstats): a persistent warp per row (D = 32 NF), lane j reads the
+// columns j + 32 i in the same order as dinv_kernel (so dinv is bit-identical), keeps its NF
+// feature maxima in registers over all of its rows; block maxima -> atomicMax (order free).
+template <int NF>
+__global__ void __launch_bounds__(256) dinv_stats_kernel(const float *__restrict__ Rp, int64_t n, int D,
+                                                         const double *__restrict__ r, float *__restrict__ dinv,
+                                                         int32_t *__restrict__ rowE, uint32_t *__restrict__ featmax) {
+    __shared__ double rsh[32 * NF];
+    __shared__ float fsm[8][32 * NF];
+    for (int j = threadIdx.x; j < D; j += blockDim.x) rsh[j] = r[j];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float fm[NF];
+#pragma unroll
+    for (int i = 0; i < NF; ++i) fm[i] = 0.f;
+    for (int64_t r0 = (int64_t)blockIdx.x * 16 + w; r0 < n; r0 += (int64_t)gridDim.x * 16) {
+        float x[2][NF];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t row = r0 + 8 * u;
+#pragma unroll
+            for (int i = 0; i < NF; ++i) x[u][i] = row < n ? Rp[row * D + lane + 32 * i] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t row = r0 + 8 * u;
+            double acc = 0.0;
+            float m = 0.f;
+#pragma unroll
+            for (int i = 0; i < NF; ++i) {
+                acc = fma((double)x[u][i], rsh[lane + 32 * i], acc);
+                const float a = fabsf(x[u][i]);
+                m = fmaxf(m, a);
+                fm[i] = fmaxf(fm[i], a);
+            }
+            for (int o = 16; o; o >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            }
+            if (lane == 0 && row < n) {
+                dinv[row] = (float)(1.0 / sqrt(acc > 1e-12 ? acc : 1e-12));   // R6 floor
+                int e = 0;
+                if (m > 0.f) frexpf(m, &e);
+                rowE[row] = e;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NF; ++i) fsm[w][lane + 32 * i] = fm[i];
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        float mm = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mm = fmaxf(mm, fsm[q][j]);
+        atomicMax(&featmax[j], __float_as_uint(mm));
+    }
+}
+
 }  // namespace
 
 // r = sum_i R'[i] (fp64, deterministic), the same routine tpo_features uses.
@@ -125,7 +184,7 @@ size_t features_ws_bytes(int64_t n, int64_t d) {
 }
 
 void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv, double *r_out,
-                   Arena &ar, cudaStream_t st) {
+                   Arena &ar, cudaStream_t st, int32_t *rowE, uint32_t *featmax) {
     const int D = (int)(2 * d);
     const int G = row_groups_for(n, (int)d);
     double *part = ar.take<double>((size_t)G * D);
@@ -140,7 +199,20 @@ void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, floa
         ar.off = mark;
     }
     colsum_run(Rp, n, D, G, part, r, st);
+    if (rowE && featmax && D % 32 == 0 && D <= 512) {   // dinv + R' statistics in one pass
+        TPO_CUDA(cudaMemsetAsync(featmax, 0, sizeof(uint32_t) * D, st));
+        const unsigned grid = (unsigned)std::min<int64_t>(8 * sm_count(), cdiv(n, 16));
+        switch (D / 32) {
+#define TPO_DS(NFV) case NFV: dinv_stats_kernel<NFV><<<grid, 256, 0, st>>>(Rp, n, D, r, dinv, rowE, featmax); break;
+            TPO_DS(1) TPO_DS(2) TPO_DS(3) TPO_DS(4) TPO_DS(5) TPO_DS(6) TPO_DS(7) TPO_DS(8)
+            TPO_DS(9) TPO_DS(10) TPO_DS(11) TPO_DS(12) TPO_DS(13) TPO_DS(14) TPO_DS(15) TPO_DS(16)
+#undef TPO_DS
+        }
+        TPO_LAUNCH_CHECK();
+        return;
+    }
     launch_dinv(Rp, n, D, r, dinv, st);
+    if (rowE && featmax) oz_rstats(Rp, n, D, rowE, featmax, st);
 }
 
 }  // namespace tpo

@@ -285,7 +285,8 @@ GramPlan plan(int64_t n, int64_t D) {
 constexpr int FT_M = 128, FT_N = 128, FT_KB = 32, FT_STAGES = 3;
 constexpr int FT_OPER = FT_M * FT_KB * 4;          // 16 KB: 128 rows x 32 fp32 (128 B rows)
 constexpr int FT_STAGE = 4 * FT_OPER;              // A_hi, A_lo, B_hi, B_lo
-constexpr int FT_THREADS = 192;
+constexpr int FT_EPI = 8;                          // epilogue warps: 2 per TMEM lane quarter
+constexpr int FT_THREADS = 32 * (2 + FT_EPI);
 
 // K-major operand, 128-byte swizzle: 8-row x 128-byte atoms stacked along M/N at SBO = 1 KB.
 __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t addr) {
@@ -304,10 +305,11 @@ constexpr uint32_t idesc_tf32_kmajor(int M, int N) {
 
 // Persistent: grid = min(tiles, SMs); a CTA walks the 128 x 128 output tiles t = blockIdx.x +
 // i * gridDim.x (row tile = t / ncol, so the concurrently running CTAs share A row tiles in
-// L2).  Two TMEM accumulators (2 x 128 columns): the MMA warp fills buffer i & 1 while the four
-// epilogue warps drain the other one (sincos + stores), so the epilogue overlaps the MMAs.
+// L2).  Two TMEM accumulators (2 x 128 columns): the MMA warp fills buffer i & 1 while the eight
+// epilogue warps (two per TMEM lane quarter, half of the 32-column chunks each) drain the other
+// one (sincos + stores), so the epilogue overlaps the MMAs.
 // Barriers: full[s] / empty[s] per smem stage (TMA <-> MMA), tfull[a] (MMA commit -> epilogue),
-// tempty[a] (4 epilogue warps -> MMA).
+// tempty[a] (8 epilogue warps -> MMA).
 __global__ void __launch_bounds__(FT_THREADS, 1)
 features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_constant__ CUtensorMap mz_lo,
                    const __grid_constant__ CUtensorMap mq_hi, const __grid_constant__ CUtensorMap mq_lo, int64_t n,
@@ -328,7 +330,7 @@ features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_const
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&bars[2 * FT_STAGES + a]), 1);
-            mbar_init(smem_u32(&bars[2 * FT_STAGES + 2 + a]), 4);
+            mbar_init(smem_u32(&bars[2 * FT_STAGES + 2 + a]), FT_EPI);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -397,7 +399,7 @@ features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_const
             }
         }
     } else {
-        const int q = warp & 3;
+        const int q = warp & 3, half = (warp - 2) >> 2;
         const float sd = sqrtf((float)d);
         const float amp = (float)sqrt(exp(1.0) / (double)d);
         const int64_t D = 2 * (int64_t)d;
@@ -410,7 +412,7 @@ features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_const
             fence_after();
             const int64_t row = i0 + 32 * q + lane;
 #pragma unroll 1
-            for (int c = 0; c < FT_N / 32; ++c) {
+            for (int c = half * (FT_N / 64); c < (half + 1) * (FT_N / 64); ++c) {
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * FT_N) + 32 * c, v);
                 const int jb = j0 + 32 * c;

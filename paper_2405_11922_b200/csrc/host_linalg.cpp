@@ -136,6 +136,15 @@ inline double fast_hypot(double a, double b) {
     return sqrt(a * a + b * b);
 }
 
+// (zi, zi1) <- (c zi - s zi1, s zi + c zi1): two distinct rows (restrict: vectorised)
+inline void rotate_rows(double *__restrict__ zi, double *__restrict__ zi1, int n, double c, double s) {
+    for (int k = 0; k < n; ++k) {
+        const double f = zi1[k], g = zi[k];
+        zi1[k] = s * g + c * f;
+        zi[k] = c * g - s * f;
+    }
+}
+
 // Implicit-shift QL on the tridiagonal (d, e), accumulating rotations into z (n x n, TRANSPOSED:
 // z[i * n + k] = component k of vector i).
 void tridiag_ql(int n, std::vector<double> &d, std::vector<double> &e, std::vector<double> &z) {
@@ -171,12 +180,7 @@ void tridiag_ql(int n, std::vector<double> &d, std::vector<double> &e, std::vect
                     d[i + 1] = g + (p = s * r);
                     g = c * r - b;
                     // z is held transposed (row i = eigenvector column i): contiguous rows
-                    double *zi = &z[(size_t)i * n], *zi1 = &z[(size_t)(i + 1) * n];
-                    for (int k = 0; k < n; ++k) {
-                        f = zi1[k];
-                        zi1[k] = s * zi[k] + c * f;
-                        zi[k] = c * zi[k] - s * f;
-                    }
+                    rotate_rows(&z[(size_t)i * n], &z[(size_t)(i + 1) * n], n, c, s);
                 }
                 if (r == 0.0 && i >= l) continue;
                 d[l] -= p;

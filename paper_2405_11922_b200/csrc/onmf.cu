@@ -237,7 +237,7 @@ size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k) {
 // RtU = R'^T (dinv . U)   (D x k, fp64).  featmax (optional, from oz_featmax): R''s per-feature
 // maxima when the caller keeps them across the iterations of one solve.
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU, Arena &ar,
-              cudaStream_t st, const uint32_t *featmax) {
+              cudaStream_t st, const uint32_t *featmax, const unsigned long long *colmax) {
     if (dinv && oz_rtu_supported(n, D, k) && (reinterpret_cast<uintptr_t>(Rp) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(U) & 15) == 0 && (reinterpret_cast<uintptr_t>(dinv) & 15) == 0) {
         const size_t mark = ar.off;
@@ -246,7 +246,7 @@ void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const do
             oz_featmax(Rp, n, D, fm, st);
             featmax = fm;
         }
-        oz_rtu(Rp, n, D, dinv, U, k, featmax, RtU, ar, st);    // integer tensor cores (R16)
+        oz_rtu(Rp, n, D, dinv, U, k, featmax, RtU, ar, st, colmax);    // integer tensor cores (R16)
         ar.off = mark;
         return;
     }

@@ -1419,7 +1419,7 @@ void oz_featmax(const float *Rp, int64_t n, int64_t D, uint32_t *featmax, cudaSt
 
 // RtU = R'^T (dinv . U) (D x k fp64) on the integer tensor cores; featmax from oz_featmax(R').
 void oz_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, const uint32_t *featmax,
-            double *RtU, Arena &ar, cudaStream_t st) {
+            double *RtU, Arena &ar, cudaStream_t st, const unsigned long long *colmax_pre) {
     TPO_REQUIRE(oz_rtu_supported(n, D, k), "oz_rtu: unsupported shape");
     TPO_REQUIRE((reinterpret_cast<uintptr_t>(Rp) & 15) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(dinv) & 15) == 0,
@@ -1429,8 +1429,10 @@ void oz_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const doub
     long long *g0 = ar.take<long long>((size_t)s.nitems * s.NP * 128);
     long long *g1 = ar.take<long long>((size_t)s.nitems * s.NP * 128);
     unsigned long long *colmax = ar.take<unsigned long long>(k);
-    TPO_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * k, st));
-    {
+    if (colmax_pre) {
+        colmax = const_cast<unsigned long long *>(colmax_pre);
+    } else {
+        TPO_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * k, st));
         const int64_t blocks = std::min<int64_t>(8 * sm_count(), cdiv(n, 256));
         const int64_t rows_per = cdiv(n, blocks);
         oz_colmax_kernel<<<(unsigned)cdiv(n, rows_per), 256, 0, st>>>(U, dinv, n, k, rows_per, colmax);

@@ -796,12 +796,13 @@ static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
     if (!haar_first) haar();
     TPO_CUDA(cudaEventRecord(ev[1], st));
     TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
-    features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
-    RStats rs;                  // R''s row exponents / feature maxima: one pass, shared by a7 and a8
+    RStats rs;                  // R''s row exponents / feature maxima (in the dinv pass), shared by a7 and a8
     if (oz_rstats_wanted(n, D, k)) {
-        oz_rstats(Rp, n, D, rowE, featmax, st);
+        features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st, rowE, featmax);
         rs.rowE = rowE;
         rs.featmax = featmax;
+    } else {
+        features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
     }
     ar.off = mark;
     TPO_CUDA(cudaEventRecord(ev[2], st));

@@ -117,8 +117,10 @@ void shard_vside_impl(const tpo_csr_t &Btp, const float *Pp, int64_t d, float *Q
 void shard_vscale_impl(float *Q, const float *s_v, int64_t rows, int64_t d, cudaStream_t st);
 void shard_uside_impl(const tpo_csr_t &Bp, const float *Q, const float *Xp, int64_t d, float alpha, const float *s_u,
                       bool last, float *Zp, float *Zhat_p, Arena &ar, cudaStream_t st);
+// rowE / featmax (optional, both or neither): R''s row exponents and per-feature maxima (see
+// oz_rstats), formed in the dinv pass when D % 32 == 0 and D <= 512
 void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv,
-                   double *r_out, Arena &ar, cudaStream_t st);
+                   double *r_out, Arena &ar, cudaStream_t st, int32_t *rowE = nullptr, uint32_t *featmax = nullptr);
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y,
                           int64_t b, float *out, Arena &ar, cudaStream_t st);
 // Per-R' statistics of the integer-tensor-core products (oz.cu), computed once per R' inside
@@ -220,7 +222,8 @@ void dgemm(bool transA, int64_t M, int64_t N, int64_t K, double alpha, const dou
 size_t dgemm_ws(int64_t M, int64_t N, int64_t K);
 // ONMF passes over R' (onmf.cu): RtU = R'^T (dinv . U) (D x k), fp64 (RH = dinv . (R' H) is tsgemm_AW_f64).
 void onmf_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, double *RtU,
-              Arena &ar, cudaStream_t st, const uint32_t *featmax = nullptr);
+              Arena &ar, cudaStream_t st, const uint32_t *featmax = nullptr,
+              const unsigned long long *colmax = nullptr);
 size_t onmf_ws_bytes(int64_t n, int64_t D, int32_t k);
 // fp64 tensor-path (DMMA) products of the discretisation (ts64.cu).  ts64_enabled(): TPO_TS64=0
 // selects the CUDA-core kernels of dense.cu / onmf.cu / cluster.cu (A/B measurement only).
@@ -247,8 +250,9 @@ void oz_aw_f64(const float *A, int64_t lda, const float *rs, const int32_t *rowE
 bool oz_rtu_supported(int64_t n, int64_t D, int k);
 size_t oz_rtu_ws(int64_t n, int64_t D, int k);
 void oz_featmax(const float *Rp, int64_t n, int64_t D, uint32_t *featmax, cudaStream_t st);
+// colmax_pre (optional): bits of max_i dinv_i U_il already formed (the Ups update's fused maxima)
 void oz_rtu(const float *Rp, int64_t n, int64_t D, const float *dinv, const double *U, int k, const uint32_t *featmax,
-            double *RtU, Arena &ar, cudaStream_t st);
+            double *RtU, Arena &ar, cudaStream_t st, const unsigned long long *colmax_pre = nullptr);
 // Alg. 3 assignment on the integer tensor cores (oz.cu), 32 < k <= 64: Ups digits prepared once
 // per solve (Ups is fixed during Alg. 3), then one certified argmax per iteration.
 struct OzAssign {
@@ -278,6 +282,7 @@ void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, in
                const double *cs, double *out, int64_t ldo, cudaStream_t st);
 void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);
 bool ts_xw_inplace_f64(double *X, int64_t n, int k, const double *W, cudaStream_t st);
+bool ts_xw_f64(const double *X, int64_t n, int k, const double *W, double *out, cudaStream_t st);
 size_t ts_rtu_ws(int64_t n, int64_t D, int k);
 size_t ts_affinity_ws(int64_t D, int64_t b);
 size_t ts_affinity_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk);
