@@ -268,7 +268,10 @@ int tpo_topk_eig(const float *Rp, const float *dinv, int64_t n, int64_t D, int32
  * T_f times (H first), then NCI generation (Alg. 3): Phi = I; T_g times
  * l*_i = argmax_l Ups[i].Phi[:,l] (Eq. ell-ast, ties -> smallest l), Y one-hot with unit
  * columns (Eqs. Y-update, y-norm), Phi = Ups^T Y; early stop on a
- * repeated labelling (R10).  All arithmetic fp64.
+ * repeated labelling (R10).  All arithmetic fp64 or fp64-accurate: for 32 < k <= 64 the products
+ * R H, R^T Ups and Alg. 3's scores run on the integer tensor cores (error-free byte-digit
+ * splitting, R16; R^T Ups keeps the 26 digit pairs p + q <= 6, exact 128-bit cross-block sums),
+ * the Alg. 3 argmax certified against the sequential fma of R13.
  *   Rp: n x D fp32;  dinv: n fp32;  Gamma: n x k fp32;  sigma: (host) k fp64;
  *   Psi: D x k fp32;  Tf >= 0, Tg >= 1;  labels: n int32 out in [0,k);
  *   iters_used: (host) int32 out, iterations of Alg. 3 actually run (may be NULL).

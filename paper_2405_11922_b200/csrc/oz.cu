@@ -47,7 +47,7 @@ namespace {
 
 constexpr int OZ_M = 128;                 // rows per tile
 constexpr int OZ_KC = 32;                 // K chunk (fp32 columns) = one kind::i8 MMA K
-constexpr int OZ_STG = 3;                 // fp32 staging stages (TMA ring, 16 KB each)
+constexpr int OZ_STG = 3;                 // fp32 staging stages (TMA ring, 16 KB each; 4-5 measured no faster)
 constexpr int OZ_NBUF = 3;                // digit-plane buffers
 constexpr int OZ_SL = 6;                  // digits per operand
 constexpr int OZ_SMAX = 5;                // kept digit pairs: p + q <= OZ_SMAX

@@ -430,6 +430,24 @@ def test_run_tiny_end_to_end(tpo, tiny_topk):
     assert np.all(tm > 0)
 
 
+@pytest.mark.parametrize("k", [40, 50])
+def test_run_matches_stage_calls_k_over_32(tpo, k):
+    """tpo_run shares R''s row exponents / feature maxima between a7 and a8 (formed in the dinv pass
+    of a5, dinv bit-identical) and runs the integer-tensor-core Gamma, RH and R^T Ups: the same
+    labels, bit for bit, as the stage-by-stage ABI calls (tpo_propagate, tpo_haar_q_dev,
+    tpo_features, tpo_topk_eig, tpo_cluster), which compute those statistics themselves."""
+    g = planted_abg(9000, 5000, k, 64, deg=("poisson", 10.0), p_in=0.8, x=("gaussian", 1.0), alpha=0.5, T=2,
+                    seed=k + 11)
+    dg = dev_graph(tpo, g)
+    X = torch.from_numpy(g.X).cuda()
+    lab_run, _ = tpo.run(dg, X, g.alpha, g.T, k, g.G)
+    _, Zh = tpo.propagate(dg, X, g.alpha, g.T)
+    Rp, dinv, _ = tpo.features(Zh, tpo.haar_q_dev(g.G))
+    Gm, sig, Ps = tpo.topk_eig(Rp, dinv, k)
+    lab, _ = tpo.cluster(Rp, dinv, Gm, sig, Ps, 5, 20)
+    assert np.array_equal(lab_run.cpu().numpy(), lab.cpu().numpy())
+
+
 @pytest.mark.parametrize("weighted", [False, True])
 def test_run_host_matches_device_inputs(tpo, weighted):
     """tpo_run_host (host inputs copied inside the call, Haar beside the copies, no SMs held

@@ -33,3 +33,10 @@ for e in ev:
     print(f"{(e.time_range.start - t0) / 1000.0:9.3f} ms  +gap {gap:7.3f}  {d * 1000:8.1f} us  {e.name[:90]}")
     prev_end = e.time_range.end
 print(f"kernels {len(ev)}  busy {tot:.3f} ms  span {(ev[-1].time_range.end - t0) / 1000.0:.3f} ms")
+api = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CPU],
+             key=lambda e: e.time_range.start)
+print("host-side runtime calls longer than 20 us:")
+for e in api:
+    d = (e.time_range.end - e.time_range.start) / 1000.0
+    if d > 0.02:
+        print(f"  {(e.time_range.start - t0) / 1000.0:9.3f} ms  {d:8.3f} ms  {e.name[:80]}")
