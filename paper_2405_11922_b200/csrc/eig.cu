@@ -627,6 +627,72 @@ void polish_gamma(double *Gamma, int64_t n, int k, Arena &ar, cudaStream_t st) {
     ar.off = mark;
 }
 
+// One-pass finish of the exact mode when s = 1^T R (D fp64) is known (tpo_run forms it in the dinv
+// pass): the polish decision as polish_gamma (one Gram; within 1e-6 of I: W = I, below 1e-2: W =
+// Ci, else not handled), R8's column sums of the final Gamma = G64 W from D-space,
+// sum_i Gamma[i,l] = ((s^T Psi Sigma^-1) W)_l (exact arithmetic identity), decided on the host; a
+// column whose |sum| is below 1e-6 sqrt(n) (where R8's fallback to the largest entry could apply:
+// ||Gamma_l||_1 <= sqrt(n) for a unit column) is not handled.  Then Gamma = fp32(G64 W diag(sgn))
+// in one fp64-tensor pass (or the sign flip fused with the rounding when W = I), no column-
+// statistics pass.  Returns false (nothing written to Gamma) when not handled.
+bool finish_fast(double *G64, int64_t n, int k, const double *Psi64, const std::vector<double> &sig,
+                 const double *s_colsum, int64_t D, float *Psi, float *Gamma, Arena &ar, cudaStream_t st) {
+    if (!ts64_enabled() || k > 104 || n == 0) return false;
+    const size_t mark = ar.off;
+    double *g = ar.take<double>((size_t)k * k), *ci = ar.take<double>((size_t)k * k);
+    double *dev = ar.take<double>(1);
+    int *flag = ar.take<int>(1);
+    TPO_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    ts_atb_f64(G64, k, G64, k, n, k, k, g, ar, st);
+    if (k > 112) { ar.off = mark; return false; }
+    chol_inv_device(g, k, ci, flag, st);
+    gram_dev_kernel<<<1, 256, 0, st>>>(g, k, dev);
+    TPO_LAUNCH_CHECK();
+    double hdev = 1.0;
+    int hflag = 0;
+    std::vector<double> hs(D), hps((size_t)D * k), hci((size_t)k * k);
+    TPO_CUDA(cudaMemcpyAsync(&hdev, dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(hs.data(), s_colsum, sizeof(double) * D, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(hps.data(), Psi64, sizeof(double) * D * k, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaMemcpyAsync(hci.data(), ci, sizeof(double) * k * k, cudaMemcpyDeviceToHost, st));
+    TPO_CUDA(cudaStreamSynchronize(st));
+    const bool ident = hdev <= 1e-6;
+    if (!(hdev < 1e-2) || (!ident && hflag)) { ar.off = mark; return false; }   // NaN, far from I, failed pivot
+    std::vector<double> t(k, 0.0), cs(k, 0.0);
+    for (int64_t j = 0; j < D; ++j) {
+        if (!std::isfinite(hs[j])) { ar.off = mark; return false; }           // s not formed
+        for (int a = 0; a < k; ++a) t[a] += hs[j] * hps[(size_t)j * k + a];
+    }
+    for (int a = 0; a < k; ++a) t[a] /= sig[a];
+    for (int l = 0; l < k; ++l) {
+        if (ident) cs[l] = t[l];
+        else
+            for (int a = 0; a <= l; ++a) cs[l] += t[a] * hci[(size_t)a * k + l];   // Ci upper triangular
+    }
+    const double thr = 1e-6 * sqrt((double)n) * 1.01;
+    std::vector<int> sg(k);
+    for (int l = 0; l < k; ++l) {
+        if (!(fabs(cs[l]) >= thr)) { ar.off = mark; return false; }
+        sg[l] = cs[l] < 0.0 ? -1 : 1;
+    }
+    int *dsg = to_dev(ar, sg, st);
+    flip_cols_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi, D, k, dsg);
+    TPO_LAUNCH_CHECK();
+    if (ident) {
+        flip_cast_f64_f32<<<cdiv(n * k, 256), 256, 0, st>>>(G64, n, k, dsg, Gamma);
+        TPO_LAUNCH_CHECK();
+    } else {
+        for (int a = 0; a < k; ++a)
+            for (int l = 0; l < k; ++l) hci[(size_t)a * k + l] = (a <= l ? hci[(size_t)a * k + l] : 0.0) * sg[l];
+        double *w = to_dev(ar, hci, st);
+        if (!ts_xw_f32out(G64, n, k, w, Gamma, st)) throw Error(TPO_ECUDA, "finish_fast: fp64 tensor path unavailable");
+    }
+    TPO_CUDA(cudaStreamSynchronize(st));
+    ar.off = mark;
+    return true;
+}
+
 // Psi / sigma column scaling on the device
 __global__ void scale_cols_kernel(const double *__restrict__ A, int64_t rows, int k, const double *__restrict__ sig,
                                   double *__restrict__ out) {
@@ -641,7 +707,7 @@ __global__ void scale_cols_kernel(const double *__restrict__ A, int64_t rows, in
 // otherwise Gamma = R Psi Sigma^{-1} (exact mode: the same factor, the block being full rank).
 void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, int k, const double *Psi64,
                     const std::vector<double> &sig, float *Gamma, float *Psi, Arena &ar, cudaStream_t st,
-                    double *Gamma_in = nullptr, const int32_t *rowE = nullptr) {
+                    double *Gamma_in = nullptr, const int32_t *rowE = nullptr, const double *s_colsum = nullptr) {
     double *G64 = Gamma_in;
     if (!G64) {
         double *sd = to_dev(ar, sig, st);
@@ -654,6 +720,7 @@ void finish_factors(const float *Rp, const float *dinv, int64_t n, int64_t D, in
     }
     cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
     TPO_LAUNCH_CHECK();
+    if (s_colsum && !Gamma_in && finish_fast(G64, n, k, Psi64, sig, s_colsum, D, Psi, Gamma, ar, st)) return;
     polish_gamma(G64, n, k, ar, st);
     apply_sign_rule(G64, n, k, Psi, D, ar, st, Gamma);
     TPO_CUDA(cudaStreamSynchronize(st));
@@ -934,7 +1001,7 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
         if (!(sig[l] > 0.0)) throw Error(TPO_ENUMERIC, "top-k: sigma_k is zero (rank(R) < k)");
         sigma[l] = sig[l];
     }
-    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st, halko_gamma, rs.rowE);
+    finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st, halko_gamma, rs.rowE, rs.s_colsum);
 }
 
 // a6: out = dinv . R' (R'^T (dinv . Y)), the D x b intermediate summed in fp64.

@@ -496,6 +496,7 @@ size_t tpo_run_ws(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d, int32_t k, i
     s += align_up(sizeof(float) * n_u * k) + align_up(sizeof(float) * D * k);   // Gamma, Psi
     s += align_up(sizeof(double) * D);                                           // r
     s += align_up(sizeof(int32_t) * n_u + 1) + align_up(sizeof(uint32_t) * D + 1);  // R' row exponents, feature maxima
+    s += align_up(sizeof(double) * D + 1);                                        // s = 1^T R
     s += align_up(haar_q_ws_bytes(d));                   // Haar Q runs beside the propagation
     size_t stage = std::max(std::max(tpo_propagate_ws(n_u, n_v, nnz, d), tpo_features_ws(n_u, d)),
                             std::max(tpo_topk_eig_ws(n_u, D, k, mode, p), tpo_cluster_ws(n_u, D, k)));
@@ -775,6 +776,7 @@ static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
     double *r = ar.take<double>(D);
     int32_t *rowE = ar.take<int32_t>(n);
     uint32_t *featmax = ar.take<uint32_t>(D);
+    double *s_colsum = ar.take<double>(D);
     const size_t haar_bytes = align_up(haar_q_ws_bytes(d));
     Arena har(ar.dry ? nullptr : ar.base + ar.off, haar_bytes);
     ar.take<char>(haar_bytes - 256);
@@ -798,9 +800,10 @@ static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
     TPO_CUDA(cudaStreamWaitEvent(st, join, 0));
     RStats rs;                  // R''s row exponents / feature maxima (in the dinv pass), shared by a7 and a8
     if (oz_rstats_wanted(n, D, k)) {
-        features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st, rowE, featmax);
+        features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st, rowE, featmax, s_colsum);
         rs.rowE = rowE;
         rs.featmax = featmax;
+        rs.s_colsum = s_colsum;
     } else {
         features_impl(Zh, n, d, Qd, Rp, dinv, r, ar, st);
     }

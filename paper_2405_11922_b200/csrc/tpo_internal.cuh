@@ -119,8 +119,10 @@ void shard_uside_impl(const tpo_csr_t &Bp, const float *Q, const float *Xp, int6
                       bool last, float *Zp, float *Zhat_p, Arena &ar, cudaStream_t st);
 // rowE / featmax (optional, both or neither): R''s row exponents and per-feature maxima (see
 // oz_rstats), formed in the dinv pass when D % 32 == 0 and D <= 512
+// s_out (optional, with rowE / featmax): s = sum_i dinv_i R'[i] (D fp64); NaN-filled when not formed
 void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, float *Rp, float *dinv,
-                   double *r_out, Arena &ar, cudaStream_t st, int32_t *rowE = nullptr, uint32_t *featmax = nullptr);
+                   double *r_out, Arena &ar, cudaStream_t st, int32_t *rowE = nullptr, uint32_t *featmax = nullptr,
+                   double *s_out = nullptr);
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y,
                           int64_t b, float *out, Arena &ar, cudaStream_t st);
 // Per-R' statistics of the integer-tensor-core products (oz.cu), computed once per R' inside
@@ -129,6 +131,7 @@ void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t
 struct RStats {
     const int32_t *rowE = nullptr;
     const uint32_t *featmax = nullptr;
+    const double *s_colsum = nullptr;   // s = sum_i dinv_i R'[i] = 1^T R (D fp64): a7's sign rule from D-space
 };
 // one pass over R' for both (rowE: n, featmax: D); only when k > 32 and D <= 512
 bool oz_rstats_wanted(int64_t n, int64_t D, int k);
@@ -283,6 +286,7 @@ void ts_aw_f64(const float *A, int64_t lda, const float *rs, const double *W, in
 void ts_ups_update(double *U, const double *RH, const double *M, int64_t n, int k, cudaStream_t st);
 bool ts_xw_inplace_f64(double *X, int64_t n, int k, const double *W, cudaStream_t st);
 bool ts_xw_f64(const double *X, int64_t n, int k, const double *W, double *out, cudaStream_t st);
+bool ts_xw_f32out(const double *X, int64_t n, int k, const double *W, float *out32, cudaStream_t st);
 size_t ts_rtu_ws(int64_t n, int64_t D, int k);
 size_t ts_affinity_ws(int64_t D, int64_t b);
 size_t ts_affinity_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk);

@@ -898,6 +898,18 @@ bool ts_xw_inplace_f64(double *X, int64_t n, int k, const double *W, cudaStream_
     return true;
 }
 
+// out32 = fp32(X W) (X n x k fp64, W k x k) on the fp64 tensor path, k <= 104
+bool ts_xw_f32out(const double *X, int64_t n, int k, const double *W, float *out32, cudaStream_t st) {
+    if (!ts64_enabled() || k > 104) return false;
+    if (n == 0) return true;
+    int NT, nblk;
+    col_tiling(k, NT, nblk);
+    DmArgs a{};
+    a.A = X; a.lda = k; a.W = W; a.ldw = k; a.n = n; a.K = k; a.N = k; a.out32 = out32; a.ldo = k;
+    TPO_NT13(dm_store_f64, NT, a, nblk, st);
+    return true;
+}
+
 // out = X W (X n x k fp64, W k x k, out n x k; out != X) on the fp64 tensor path, k <= 104
 bool ts_xw_f64(const double *X, int64_t n, int k, const double *W, double *out, cudaStream_t st) {
     if (!ts64_enabled() || k > 104) return false;
