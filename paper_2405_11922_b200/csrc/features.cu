@@ -165,16 +165,16 @@ __global__ void __launch_bounds__(256) dinv_stats_kernel(const float *__restrict
         fm[i] = 0.f;
         sa[i] = 0.0;
     }
-    for (int64_t r0 = (int64_t)blockIdx.x * 16 + w; r0 < n; r0 += (int64_t)gridDim.x * 16) {
-        float x[2][NF];
+    for (int64_t r0 = (int64_t)blockIdx.x * 32 + w; r0 < n; r0 += (int64_t)gridDim.x * 32) {
+        float x[4][NF];                                 // 4 rows in flight per warp
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int64_t row = r0 + 8 * u;
 #pragma unroll
             for (int i = 0; i < NF; ++i) x[u][i] = row < n ? Rp[row * D + lane + 32 * i] : 0.f;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int64_t row = r0 + 8 * u;
             double acc = 0.0;
             float m = 0.f;
@@ -292,7 +292,7 @@ void features_impl(const float *Zhat, int64_t n, int64_t d, const float *Q, floa
     colsum_run(Rp, n, D, G, part, r, st);
     if (rowE && featmax && D % 32 == 0 && D <= 512) {   // dinv + R' statistics in one pass
         TPO_CUDA(cudaMemsetAsync(featmax, 0, sizeof(uint32_t) * D, st));
-        const unsigned grid = (unsigned)std::min<int64_t>(8 * sm_count(), cdiv(n, 16));
+        const unsigned grid = (unsigned)std::min<int64_t>(8 * sm_count(), cdiv(n, 32));
         double *spart = s_out ? ar.take<double>((size_t)grid * D) : nullptr;
         switch (D / 32) {
 #define TPO_DS(NFV) case NFV: dinv_stats_kernel<NFV><<<grid, 256, 0, st>>>(Rp, n, D, r, dinv, rowE, featmax, spart); break;
