@@ -68,6 +68,14 @@ __global__ void degree_scale_kernel(const int64_t *__restrict__ rowptr, const fl
     if (lane == 0) s[row] = deg > 0.0 ? (float)(1.0 / sqrt(deg)) : 0.0f;
 }
 
+// unweighted degrees: a thread per row (deg = row length; the same value as degree_scale_kernel)
+__global__ void degree_scale_unw_kernel(const int64_t *__restrict__ rowptr, int64_t n, float *__restrict__ s) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    const double deg = (double)(rowptr[row + 1] - rowptr[row]);
+    s[row] = deg > 0.0 ? (float)(1.0 / sqrt(deg)) : 0.0f;
+}
+
 // weighted degrees in fp64 (sharded path: the V-side sums are all-reduced across ranks)
 __global__ void degree_kernel(const int64_t *__restrict__ rowptr, const float *__restrict__ val, int64_t n,
                               double *__restrict__ deg) {
@@ -953,9 +961,15 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
     };
 
     const int TB = 256;
-    if (n > 0) degree_scale_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>(B.row_ptr, B.val, n, su);
+    if (n > 0) {
+        if (B.val) degree_scale_kernel<<<cdiv(n * 32, TB), TB, 0, st>>>(B.row_ptr, B.val, n, su);
+        else degree_scale_unw_kernel<<<cdiv(n, TB), TB, 0, st>>>(B.row_ptr, n, su);
+    }
     TPO_LAUNCH_CHECK();
-    if (m > 0) degree_scale_kernel<<<cdiv(m * 32, TB), TB, 0, st>>>(Bt.row_ptr, Bt.val, m, sv);
+    if (m > 0) {
+        if (Bt.val) degree_scale_kernel<<<cdiv(m * 32, TB), TB, 0, st>>>(Bt.row_ptr, Bt.val, m, sv);
+        else degree_scale_unw_kernel<<<cdiv(m, TB), TB, 0, st>>>(Bt.row_ptr, m, sv);
+    }
     TPO_LAUNCH_CHECK();
     if (n == 0) return;
     if (T == 0) {
