@@ -3,7 +3,7 @@
 //   features_tc (gram_tc.cu): Zo = sqrt(d) Zhat Q^T on tcgen05 with 3xTF32 splitting
 //     (fp32-accurate), epilogue R' = sqrt(e/d) (sin Zo || cos Zo) (accurate sincosf, the
 //     arguments reach sqrt(d)) straight from TMEM.
-//   colsum_part_kernel + colsum_reduce_kernel: r = sum_i R'[i] in fp64, fixed row ranges per
+//   colsum(4)_part_kernel + colsum_reduce_wide_kernel: r = sum_i R'[i] in fp64, fixed row ranges per
 //     block and a fixed-order sum over blocks.
 //   dinv_kernel: dinv_i = 1 / sqrt(max(R'[i] . r, 1e-12)) with r (fp64) staged in smem.
 #include <algorithm>
@@ -100,13 +100,6 @@ __global__ void __launch_bounds__(1024) colsum_reduce_wide_kernel(const double *
     }
 }
 
-__global__ void colsum_reduce_kernel(const double *__restrict__ part, int G, int D, double *__restrict__ r) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= D) return;
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += part[(int64_t)g * D + j];
-    r[j] = s;
-}
 
 __global__ void dinv_kernel(const float *__restrict__ Rp, int64_t n, int D, const double *__restrict__ r,
                             float *__restrict__ dinv) {
@@ -138,7 +131,7 @@ void colsum_run(const float *Rp, int64_t n, int D, int G, double *part, double *
     else
         colsum_part_kernel<<<dim3(G, cdiv(D, 256)), 256, 0, st>>>(Rp, n, D, rows_per, part);
     TPO_LAUNCH_CHECK();
-    colsum_reduce_kernel<<<cdiv(D, 256), 256, 0, st>>>(part, G, D, r);
+    colsum_reduce_wide_kernel<<<cdiv(D, 32), 1024, 0, st>>>(part, G, D, r);
     TPO_LAUNCH_CHECK();
 }
 
@@ -149,7 +142,7 @@ void colsum_run(const float *Rp, int64_t n, int D, int G, double *part, double *
 // Also (spart != NULL) the block's partial s = sum_i dinv_i R'[i] (fp64, rows in a fixed order per
 // lane, warps combined in order), the column sums 1^T R that a7's sign rule needs.
 template <int NF>
-__global__ void __launch_bounds__(256) dinv_stats_kernel(const float *__restrict__ Rp, int64_t n, int D,
+__global__ void __launch_bounds__(256, 3) dinv_stats_kernel(const float *__restrict__ Rp, int64_t n, int D,
                                                          const double *__restrict__ r, float *__restrict__ dinv,
                                                          int32_t *__restrict__ rowE, uint32_t *__restrict__ featmax,
                                                          double *__restrict__ spart) {

@@ -288,6 +288,30 @@ constexpr int FT_STAGE = 4 * FT_OPER;              // A_hi, A_lo, B_hi, B_lo
 constexpr int FT_EPI = 8;                          // epilogue warps: 2 per TMEM lane quarter
 constexpr int FT_THREADS = 32 * (2 + FT_EPI);
 
+// sin / cos of an fp32 argument without the XU conversions of sincosf's reduction: k = rint(x 2/pi)
+// by the 1.5 2^23 magic addition (the quadrant is the low bits of its pattern), r = x - k pi/2 with a
+// two-part pi/2 (fma; |k| small, so r is accurate to ~1e-15), Cephes minimax polynomials on
+// [-pi/4, pi/4] (~1 ulp).  |x| >= 2^17 (never reached here: |x| <= sqrt(d) for unit rows) falls
+// back to sincosf.
+__device__ __forceinline__ void sincos_fast(float x, float *sn, float *cs) {
+    if (!(fabsf(x) < 131072.f)) {
+        sincosf(x, sn, cs);
+        return;
+    }
+    const float t = fmaf(x, 0.636619772367581343f, 12582912.f);       // 1.5 * 2^23 + rint(x 2/pi)
+    const int q = __float_as_int(t) & 3;
+    const float k = t - 12582912.f;
+    float r = fmaf(-k, 1.57079637050628662109375f, x);
+    r = fmaf(-k, -4.37113900018624283e-8f, r);
+    const float z = r * r;
+    const float sr = fmaf(r * z, fmaf(z, fmaf(z, -1.9515295891e-4f, 8.3321608736e-3f), -1.6666654611e-1f), r);
+    const float cr = fmaf(z * z, fmaf(z, fmaf(z, 2.443315711809948e-5f, -1.388731625493765e-3f), 4.166664568298827e-2f),
+                          fmaf(-0.5f, z, 1.0f));
+    const float a = (q & 1) ? cr : sr, b = (q & 1) ? sr : cr;
+    *sn = (q & 2) ? -a : a;
+    *cs = ((q + 1) & 2) ? -b : b;
+}
+
 // K-major operand, 128-byte swizzle: 8-row x 128-byte atoms stacked along M/N at SBO = 1 KB.
 __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t addr) {
     uint64_t d = 0;
@@ -400,6 +424,7 @@ features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_const
         }
     } else {
         const int q = warp & 3, half = (warp - 2) >> 2;
+        float *tb = reinterpret_cast<float *>(smem + FT_STAGES * FT_STAGE + 256) + (warp - 2) * 1024;   // 32 x 32
         const float sd = sqrtf((float)d);
         const float amp = (float)sqrt(exp(1.0) / (double)d);
         const int64_t D = 2 * (int64_t)d;
@@ -416,25 +441,38 @@ features_tc_kernel(const __grid_constant__ CUtensorMap mz_hi, const __grid_const
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * FT_N) + 32 * c, v);
                 const int jb = j0 + 32 * c;
-                if (row >= n) continue;
+                if (jb + 32 > d && row >= n) continue;     // (the full-width path stores whole rows)
                 float *ps = Rp + row * D + jb, *pc = Rp + row * D + d + jb;
                 if (jb + 32 <= d) {
+                    // lane = row: transpose the 32 x 32 block through the warp's smem buffer (XOR
+                    // swizzle, conflict-free) so that every store writes one row's 128 contiguous
+                    // bytes instead of 32 rows x 16 bytes
 #pragma unroll
-                    for (int tt = 0; tt < 32; tt += 4) {
-                        float s0, c0, s1, c1, s2, c2, s3, c3;
-                        sincosf(sd * v[tt], &s0, &c0);
-                        sincosf(sd * v[tt + 1], &s1, &c1);
-                        sincosf(sd * v[tt + 2], &s2, &c2);
-                        sincosf(sd * v[tt + 3], &s3, &c3);
-                        *reinterpret_cast<float4 *>(ps + tt) = make_float4(amp * s0, amp * s1, amp * s2, amp * s3);
-                        *reinterpret_cast<float4 *>(pc + tt) = make_float4(amp * c0, amp * c1, amp * c2, amp * c3);
+                    for (int tt = 0; tt < 32; ++tt) {
+                        float sn, cs;
+                        sincos_fast(sd * v[tt], &sn, &cs);
+                        tb[lane * 32 + (tt ^ lane)] = amp * sn;
+                        v[tt] = amp * cs;
                     }
+                    __syncwarp();
+                    const int64_t rb0 = i0 + 32 * q;
+#pragma unroll 4
+                    for (int rr = 0; rr < 32; ++rr)
+                        if (rb0 + rr < n) Rp[(rb0 + rr) * D + jb + lane] = tb[rr * 32 + (lane ^ rr)];
+                    __syncwarp();
+#pragma unroll
+                    for (int tt = 0; tt < 32; ++tt) tb[lane * 32 + (tt ^ lane)] = v[tt];
+                    __syncwarp();
+#pragma unroll 4
+                    for (int rr = 0; rr < 32; ++rr)
+                        if (rb0 + rr < n) Rp[(rb0 + rr) * D + d + jb + lane] = tb[rr * 32 + (lane ^ rr)];
+                    __syncwarp();
                 } else {
 #pragma unroll
                     for (int tt = 0; tt < 32; ++tt) {
                         if (jb + tt < d) {
                             float sn, cs;
-                            sincosf(sd * v[tt], &sn, &cs);
+                            sincos_fast(sd * v[tt], &sn, &cs);
                             ps[tt] = amp * sn;
                             pc[tt] = amp * cs;
                         }
@@ -504,7 +542,7 @@ void features_tc(const float *Zhat, int64_t n, int64_t d, const float *Q, float 
     TPO_LAUNCH_CHECK();
     const CUtensorMap a_hi = make_map_kmajor(zh, n, d, FT_M), a_lo = make_map_kmajor(zl, n, d, FT_M);
     const CUtensorMap b_hi = make_map_kmajor(qh, d, d, FT_N), b_lo = make_map_kmajor(ql, d, d, FT_N);
-    const size_t smem = FT_STAGES * FT_STAGE + 1024 + 256;
+    const size_t smem = FT_STAGES * FT_STAGE + 1024 + 256 + FT_EPI * 4096;   // + the epilogue transpose buffers
     static std::once_flag once;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(features_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
