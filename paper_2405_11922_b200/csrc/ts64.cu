@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
     const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t Q = my_tiles * nst;
     const bool a16 = sizeof(TA) == 4 && (a.lda % 4) == 0 && ((reinterpret_cast<uintptr_t>(A) & 15u) == 0);
+    const bool d16 = sizeof(TA) == 8 && (a.lda % 2) == 0 && ((reinterpret_cast<uintptr_t>(A) & 15u) == 0);
     auto load = [&](int64_t q, int buf) {
         const int64_t r0 = (blockIdx.x + (q / nst) * gridDim.x) * DM_BM;
         const int k0 = (int)(q % nst) * DM_BK;
@@ -160,7 +161,16 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
                 const int bytes = row < a.n ? 4 * max(0, min(4, a.K - kc)) : 0;
                 cp16(as + r * LDA + part * 4, bytes ? (const void *)(A + row * a.lda + kc) : (const void *)A, bytes);
             }
-        } else {                            // element copies (fp64 A, or unaligned fp32)
+        } else if (d16) {                   // fp64 rows in 16-byte chunks (16 per row): half the copies
+#pragma unroll 4
+            for (int i = 0; i < DM_BM * 16 / DM_NT; ++i) {
+                const int c = tid + DM_NT * i, r = c >> 4, part = c & 15;
+                const int64_t row = r0 + r;
+                const int kc = k0 + part * 2;
+                const int bytes = row < a.n ? 8 * max(0, min(2, a.K - kc)) : 0;
+                cp16(as + r * LDA + part * 2, bytes ? (const void *)(A + row * a.lda + kc) : (const void *)A, bytes);
+            }
+        } else {                            // element copies (unaligned fp64 or fp32)
 #pragma unroll 4
             for (int i = 0; i < DM_BM * DM_BK / DM_NT; ++i) {
                 const int idx = tid + DM_NT * i, r = idx >> 5, c = idx & 31;
@@ -284,8 +294,8 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_rowgemm_kernel(DmArgs a) {
 // stays resident in shared memory; BM-row tiles of A (one contiguous block each) arrive by bulk copy
 // into a 2-slot ring on mbarriers, the next tile in flight while one is multiplied.  Warp w owns the
 // MTW m-tiles (8 rows each) w*MTW .. of a tile against all NT n-tiles.
-template <int EPI, int NT, int MTW, int NS>           // NS: ring slots (2, or 1 when the tiles are large)
-__global__ void __launch_bounds__(DM_NT, 1) dm_rowk_kernel(DmArgs a) {
+template <int EPI, int NT, int MTW, int NS, int MINB>  // NS: ring slots; MINB: resident CTAs per SM
+__global__ void __launch_bounds__(DM_NT, MINB) dm_rowk_kernel(DmArgs a) {
     if (EPI == DM_ASSIGN && *a.done) return;
     constexpr int BM = 8 * 8 * MTW;
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -612,15 +622,15 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_atb_kernel(const double *__restri
 // mbarriers -- one instruction per 12.8 KB instead of one per element (the element-wise cp.async
 // version was LSU-issue bound, 1.0 ms for 2M x 50).  Fragment reads use the unpadded row stride.
 // A CTA's rows are whole chunks except the last CTA's tail, which is staged element-wise with
-// zero fill.
+// zero fill.  A Gram (B == A, `same`) stages each chunk once and reads both fragments from it.
 template <int MT, int NTT, int S>
 __global__ void __launch_bounds__(DM_NT, 1) dm_atb_bulk_kernel(const double *__restrict__ A, const double *__restrict__ B,
-                                                               int64_t n, int p, int q, int64_t rows_per,
+                                                               int64_t n, int p, int q, int64_t rows_per, bool same,
                                                                double *__restrict__ part) {
     extern __shared__ __align__(128) unsigned char dsm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(dsm);                        // [S]
-    double *ring = reinterpret_cast<double *>(dsm + 128);                       // [S][AB_BK * (p + q)]
-    const int stage = AB_BK * (p + q);
+    double *ring = reinterpret_cast<double *>(dsm + 128);                       // [S][AB_BK * (p + q)] (same: p)
+    const int stage = AB_BK * (same ? p : p + q);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int gr = lane >> 2, gc = lane & 3;
     const int64_t i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
@@ -634,9 +644,9 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_atb_bulk_kernel(const double *__r
         double *as = ring + (size_t)(c % S) * stage, *bs = as + AB_BK * p;
         const int64_t b = i0 + c * AB_BK;
         const uint32_t ba = (uint32_t)(AB_BK * p * 8), bb = (uint32_t)(AB_BK * q * 8);
-        bar_expect_tx(full + c % S, ba + bb);
+        bar_expect_tx(full + c % S, same ? ba : ba + bb);
         bulk_g2s(as, A + b * p, ba, full + c % S);
-        bulk_g2s(bs, B + b * q, bb, full + c % S);
+        if (!same) bulk_g2s(bs, B + b * q, bb, full + c % S);
     };
     if (tid == 0)
         for (int64_t c = 0; c < S && c < nfull; ++c) issue(c);
@@ -670,12 +680,12 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_atb_bulk_kernel(const double *__r
     for (int64_t c = 0; c < nfull; ++c) {
         bar_wait(full + c % S, (uint32_t)((c / S) & 1));
         const double *as = ring + (size_t)(c % S) * stage;
-        compute(as, as + AB_BK * p);
+        compute(as, same ? as : as + AB_BK * p);
         __syncthreads();                               // every thread is done with slot c % S
         if (tid == 0 && c + S < nfull) issue(c + S);
     }
     if (tail > 0) {                                    // the last rows: element-wise, zero-filled
-        double *as = ring, *bs = ring + AB_BK * p;     // slot 0 is free (all bulk copies consumed)
+        double *as = ring, *bs = ring + AB_BK * p;     // slots 0 (and 1) are free: all bulk copies consumed
         const int64_t b = i0 + nfull * AB_BK;
         for (int idx = tid; idx < AB_BK * p; idx += DM_NT) {
             const int r = idx / p;
@@ -764,28 +774,34 @@ void dm_assign(const DmArgs &a, cudaStream_t st) { dm_launch<double, DM_ASSIGN, 
 template <int EPI, int NT>
 void dm_rowk_launch(const DmArgs &a, cudaStream_t st) {
     const int k = a.N;
-    auto go = [&](auto mtw_tag, auto ns_tag) {
+    auto go = [&](auto mtw_tag, auto ns_tag, auto minb_tag) {
         constexpr int MTW = decltype(mtw_tag)::value, NS = decltype(ns_tag)::value;
+        constexpr int MINB = decltype(minb_tag)::value;
         constexpr int BM = 64 * MTW;
         constexpr int NB = EPI == DM_UPS ? 2 : 1;
         const size_t sm = 128 + sizeof(double) * (((size_t)k * k + 15) / 16 * 16 + (size_t)NS * NB * BM * k);
-        TPO_CUDA(cudaFuncSetAttribute(dm_rowk_kernel<EPI, NT, MTW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sm));
+        TPO_CUDA(cudaFuncSetAttribute(dm_rowk_kernel<EPI, NT, MTW, NS, MINB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         const int64_t tiles = cdiv(std::max<int64_t>(a.n, 1), BM);
-        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count_cached()));
-        dm_rowk_kernel<EPI, NT, MTW, NS><<<gx, DM_NT, sm, st>>>(a);
+        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)MINB * sm_count_cached()));
+        dm_rowk_kernel<EPI, NT, MTW, NS, MINB><<<gx, DM_NT, sm, st>>>(a);
         TPO_LAUNCH_CHECK();
     };
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
-    // ASSIGN: 128-row tiles for k <= 64; UPS slots hold two tiles (Ups, RH): 64-row tiles, and a
-    // single slot once the k x k factor and two double-buffered tile pairs exceed shared memory
+    using I3 = std::integral_constant<int, 3>;
+    // ASSIGN: 128-row tiles for k <= 64.  UPS: 64-row tile pairs (Ups, RH).  The UPS epilogue (an fp64
+    // divide and square root per element) is as long as the tile's DMMA product, so several CTAs per SM
+    // with one slot each (one CTA's epilogue and store beside another's product and load) beat one CTA
+    // with a two-slot ring: as many CTAs as the k x k factor and one tile pair let fit (<= 227 KB / SM).
     if (EPI != DM_UPS) {
-        if (k <= 64) go(I2(), I2());
-        else go(I1(), I2());
+        if (k <= 64) go(I2(), I2(), I1());
+        else go(I1(), I2(), I1());
     } else {
-        if (k <= 64) go(I1(), I2());
-        else go(I1(), I1());
+        const size_t per = 1024 + 128 + sizeof(double) * (((size_t)k * k + 15) / 16 * 16 + (size_t)2 * 64 * k);
+        if (3 * per <= 227 * 1024) go(I1(), I1(), I3());
+        else if (2 * per <= 227 * 1024) go(I1(), I1(), I2());
+        else go(I1(), I1(), I1());
     }
 }
 template <int NT>
@@ -829,9 +845,11 @@ template <int MT, int NTT>
 void dm_atb_bulk_launch(const double *A, const double *B, int64_t n, int p, int q, int64_t rows_per, int G, double *part,
                         cudaStream_t st) {
     constexpr int S = 4;
-    const size_t sm = 128 + (size_t)S * AB_BK * (p + q) * sizeof(double);
+    const bool same = A == B && p == q;
+    // the tail's element-wise staging uses AB_BK * (p + q) doubles of the (S-slot) ring in either case
+    const size_t sm = 128 + (size_t)std::max(S * AB_BK * (same ? p : p + q), AB_BK * (p + q)) * sizeof(double);
     TPO_CUDA(cudaFuncSetAttribute(dm_atb_bulk_kernel<MT, NTT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dm_atb_bulk_kernel<MT, NTT, S><<<G, DM_NT, sm, st>>>(A, B, n, p, q, rows_per, part);
+    dm_atb_bulk_kernel<MT, NTT, S><<<G, DM_NT, sm, st>>>(A, B, n, p, q, rows_per, same, part);
     TPO_LAUNCH_CHECK();
 }
 template <int NTT>
@@ -849,12 +867,18 @@ void dm_atb_mt(int mt, const double *A, int64_t lda, const double *B, int64_t ld
 }
 }  // namespace
 
-size_t ts_atb_ws(int p, int q) { return align_up(sizeof(double) * (size_t)sm_count_cached() * p * q) + 256; }
+// two row splits per SM: a Gram chunk ring is small enough for two resident CTAs, whose DMMA chains
+// and bulk copies interleave
+constexpr int AB_SPLITS_PER_SM = 2;
+size_t ts_atb_ws(int p, int q) {
+    return align_up(sizeof(double) * (size_t)AB_SPLITS_PER_SM * sm_count_cached() * p * q) + 256;
+}
 
 // out (p x q fp64) = A^T B, A n x p, B n x q fp64 (p, q <= 128): fixed-order split over rows
 void ts_atb_f64(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t n, int p, int q, double *out,
                 Arena &ar, cudaStream_t st) {
-    const int64_t rows_per = cdiv(cdiv(std::max<int64_t>(n, 1), sm_count_cached()), AB_BK) * AB_BK;
+    const int64_t rows_per =
+        cdiv(cdiv(std::max<int64_t>(n, 1), (int64_t)AB_SPLITS_PER_SM * sm_count_cached()), AB_BK) * AB_BK;
     const int G = (int)cdiv(std::max<int64_t>(n, 1), rows_per);
     const size_t mark = ar.off;
     double *part = ar.take<double>((size_t)G * p * q);
