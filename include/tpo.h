@@ -223,6 +223,36 @@ size_t tpo_affinity_matvec_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chu
 int tpo_affinity_matvec_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *Y, int64_t b,
                               float *out, int64_t chunk_rows, void *ws, size_t ws_bytes, void *stream);
 
+/* "R-free" a7: tpo_topk_eig's exact mode (R7) from Zhat and Q instead of R' --
+ * R' rows are recomputed (Eq. R-prime; tcgen05 features GEMM + sincos, row-local,
+ * so each recomputed row equals the materialised one bit for bit) in chunks of chunk_rows rows
+ * (<= 0: 262,144) in three sweeps: r = R'^T 1; dinv = (R' r)^{-1/2} and the Gram G = R^T R (fp64
+ * chunk sums added in chunk order); Gamma = R Psi Sigma^-1 (Eq. init-HY).  Then
+ * the same eigensolver of G, CholeskyQR polish and R8 sign rule as tpo_topk_eig.
+ *   Zhat: n x d fp32 device (d % 4 == 0);  Q: d x d fp32 device;  Gamma: n x k fp32 device out;
+ *   sigma: k fp64 HOST out;  Psi: 2d x k fp32 device out;  dinv: n fp32 device out (Eq. dinv).
+ * Workspace: tpo_topk_eig_rfree_ws(n, d, k, chunk_rows).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA,
+ * TPO_ENUMERIC (as tpo_topk_eig).  Synchronises the stream. */
+size_t tpo_topk_eig_rfree_ws(int64_t n, int64_t d, int32_t k, int64_t chunk_rows);
+int tpo_topk_eig_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, int32_t k, float *Gamma,
+                       double *sigma, float *Psi, float *dinv, int64_t chunk_rows, void *ws, size_t ws_bytes,
+                       void *stream);
+
+/* "R-free" a8-a9: tpo_cluster (Alg. 2 ONMF, then Alg. 3 NCI rounding,
+ * PAPER.md:536-604) with R' rows recomputed from Zhat and Q in chunks of chunk_rows rows in each of
+ * the two R' passes of an ONMF iteration (R'^T (dinv . Ups), then dinv . (R' H)); the chunks' fp64
+ * partials of R'^T (dinv . Ups) are added in chunk order (deterministic).  Both products run on the
+ * fp64 tensor path (DMMA).  Alg. 3 does not touch R'.
+ *   Zhat: n x d fp32;  Q: d x d fp32;  dinv: n fp32 (e.g. from tpo_topk_eig_rfree);  Gamma: n x k
+ *   fp32;  sigma: k fp64 HOST;  Psi: 2d x k fp32;  labels: n int32 device out;  iters_used: host
+ *   int32 out (Alg. 3 iterations), may be NULL.
+ * Workspace: tpo_cluster_rfree_ws(n, d, k, chunk_rows).  Errors: TPO_EINVAL, TPO_ENOMEM, TPO_ECUDA. */
+size_t tpo_cluster_rfree_ws(int64_t n, int64_t d, int32_t k, int64_t chunk_rows);
+int tpo_cluster_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *dinv, int32_t k,
+                      const float *Gamma, const double *sigma, const float *Psi, int32_t Tf, int32_t Tg,
+                      int32_t *labels, int32_t *iters_used, int64_t chunk_rows, void *ws, size_t ws_bytes,
+                      void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * a7  Top-k singular triplets of R = diag(dinv) R' -- "the top-k left and right singular
  * vectors of R" and its top-k singular values (Eq. init-HY).

@@ -29,6 +29,7 @@ SYMBOLS = [
     "tpo_rows_gather", "tpo_rows_scatter",
     "tpo_comm_unique_id", "tpo_comm_create", "tpo_comm_destroy", "tpo_propagate_sharded_ws", "tpo_propagate_sharded",
     "tpo_affinity_matvec_rfree_ws", "tpo_affinity_matvec_rfree", "tpo_run_sharded_ws", "tpo_run_sharded",
+    "tpo_topk_eig_rfree_ws", "tpo_topk_eig_rfree", "tpo_cluster_rfree_ws", "tpo_cluster_rfree",
 ]
 
 TPO_OK, TPO_EINVAL, TPO_ECUDA, TPO_ENOMEM, TPO_ENCCL, TPO_ENUMERIC = 0, -1, -2, -3, -4, -5
@@ -145,6 +146,14 @@ def lib():
     L.tpo_affinity_matvec_rfree_ws.restype = sz
     L.tpo_affinity_matvec_rfree.argtypes = [vp, i64, i64, vp, vp, i64, vp, i64, vp, sz, vp]
     L.tpo_affinity_matvec_rfree.restype = C.c_int
+    L.tpo_topk_eig_rfree_ws.argtypes = [i64, i64, i32, i64]
+    L.tpo_topk_eig_rfree_ws.restype = sz
+    L.tpo_topk_eig_rfree.argtypes = [vp, i64, i64, vp, i32, vp, vp, vp, vp, i64, vp, sz, vp]
+    L.tpo_topk_eig_rfree.restype = C.c_int
+    L.tpo_cluster_rfree_ws.argtypes = [i64, i64, i32, i64]
+    L.tpo_cluster_rfree_ws.restype = sz
+    L.tpo_cluster_rfree.argtypes = [vp, i64, i64, vp, vp, i32, vp, vp, vp, i32, i32, vp, vp, i64, vp, sz, vp]
+    L.tpo_cluster_rfree.restype = C.c_int
     L.tpo_rowgemm_f64_ws.argtypes = [i64, i64, i32]
     L.tpo_rowgemm_f64_ws.restype = sz
     L.tpo_rowgemm_f64.argtypes = [vp, i64, i64, vp, vp, i32, vp, vp, sz, vp]

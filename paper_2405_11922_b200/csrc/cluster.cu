@@ -565,9 +565,65 @@ size_t cluster_ws_bytes(int64_t n, int64_t D, int32_t k) {
     return ar.off + inner + 4096;
 }
 
+namespace {
+__global__ void acc_f64_kernel(double *__restrict__ acc, const double *__restrict__ x, int64_t len) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < len) acc[i] += x[i];
+}
+
+int64_t rfree_chunk(const RSource &s, int64_t n) { return std::max<int64_t>(1, std::min(n, s.chunk)); }
+
+// f3 Alg. 2 RtU = R'^T (dinv . Ups) (Eq. update-Q / update-Y) with R' rows
+// recomputed from Zhat chunk by chunk (bit-identical rows: the features GEMM is row-local); the
+// chunks' fp64 partials (fp64 tensor path) are added in chunk order, so the sum is deterministic
+void rfree_rtu(const RSource &s, const float *dinv, const double *U, int64_t n, int64_t D, int k, double *RtU, Arena &ar,
+               cudaStream_t st) {
+    const int64_t C = rfree_chunk(s, n);
+    const size_t mark0 = ar.off;
+    float *Rc = ar.take<float>((size_t)C * D);
+    double *rp = ar.take<double>(D), *Pc = ar.take<double>((size_t)D * k);
+    const size_t mark = ar.off;
+    TPO_CUDA(cudaMemsetAsync(RtU, 0, sizeof(double) * D * k, st));
+    for (int64_t c0 = 0; c0 < n; c0 += C) {
+        const int64_t nc = std::min(C, n - c0);
+        features_part(s.Zhat + c0 * s.d, nc, s.d, s.Q, Rc, rp, ar, st);
+        ar.off = mark;
+        ts_rtu(Rc, nc, D, dinv + c0, U + c0 * k, k, Pc, ar, st);
+        ar.off = mark;
+        acc_f64_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(RtU, Pc, D * k);
+        TPO_LAUNCH_CHECK();
+    }
+    ar.off = mark0;
+}
+
+// f3 Alg. 2 RH = dinv . (R'H), row-local: each chunk's rows from its recomputed R' rows
+void rfree_rh(const RSource &s, const float *dinv, const double *H, int64_t n, int64_t D, int k, double *RH, Arena &ar,
+              cudaStream_t st) {
+    const int64_t C = rfree_chunk(s, n);
+    const size_t mark0 = ar.off;
+    float *Rc = ar.take<float>((size_t)C * D);
+    double *rp = ar.take<double>(D);
+    const size_t mark = ar.off;
+    for (int64_t c0 = 0; c0 < n; c0 += C) {
+        const int64_t nc = std::min(C, n - c0);
+        features_part(s.Zhat + c0 * s.d, nc, s.d, s.Q, Rc, rp, ar, st);
+        ar.off = mark;
+        rh_apply(RhPlan(), Rc, dinv + c0, H, nc, D, k, RH + c0 * k, ar, st);
+        ar.off = mark;
+    }
+    ar.off = mark0;
+}
+}  // namespace
+
+size_t rfree_pass_ws(int64_t n, int64_t d, int32_t k, int64_t chunk) {
+    const int64_t D = 2 * d, C = std::max<int64_t>(1, std::min(n, chunk));
+    return align_up(sizeof(float) * (size_t)C * D) + align_up(sizeof(double) * D) + align_up(sizeof(double) * D * k) +
+           std::max(features_ws_bytes(C, d), ts_rtu_ws(0, D, k)) + 4096;
+}
+
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
-                  int32_t *iters_used, Arena &ar, cudaStream_t st, RStats rs) {
+                  int32_t *iters_used, Arena &ar, cudaStream_t st, RStats rs, const RSource *src) {
     double *U = ar.take<double>(n * k);
     double *RH = ar.take<double>(n * k);
     double *H = ar.take<double>(D * k), *Hn = ar.take<double>(D * k);
@@ -579,9 +635,9 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const int64_t nb = cdiv(std::max<int64_t>(n, 1), rpb);
     double *part = ar.take<double>(nb * k * k);
     int64_t *cpart = ar.take<int64_t>(nb * k);
-    const RhPlan rhp = rh_plan_pre(rs.rowE, Rp, n, D, k, ar, st);
+    const RhPlan rhp = src ? RhPlan() : rh_plan_pre(rs.rowE, Rp, n, D, k, ar, st);
     const uint32_t *featmax = nullptr;                     // R''s per-feature maxima (oz R^T Ups), once per solve
-    if (oz_rtu_supported(n, D, k)) {
+    if (!src && oz_rtu_supported(n, D, k)) {
         if (rs.featmax) {
             featmax = rs.featmax;
         } else {
@@ -599,7 +655,8 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
     const size_t ups_smem = sizeof(double) * ((size_t)k * k + 1 + (size_t)8 * UR * k);
     TPO_CUDA(cudaFuncSetAttribute(ups_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ups_smem));
     for (int t = 0; t < Tf; ++t) {
-        onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st, featmax);
+        if (src) rfree_rtu(*src, dinv, U, n, D, k, RtU, ar, st);
+        else onmf_rtu(Rp, n, D, dinv, U, k, RtU, ar, st, featmax);
         ar.off = mark;
         if (ts64_enabled() && k <= 104) ts_atb_f64(U, k, U, k, n, k, k, UtU, ar, st);
         else dgemm(true, k, k, n, 1.0, U, k, U, k, 0.0, UtU, k, ar, st);
@@ -607,7 +664,8 @@ void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int3
         h_update_kernel<<<cdiv(D * k, 256), 256, 0, st>>>(H, RtU, UtU, D, k, Hn);
         TPO_LAUNCH_CHECK();
         std::swap(H, Hn);
-        rh_apply(rhp, Rp, dinv, H, n, D, k, RH, ar, st);
+        if (src) rfree_rh(*src, dinv, H, n, D, k, RH, ar, st);
+        else rh_apply(rhp, Rp, dinv, H, n, D, k, RH, ar, st);
         ar.off = mark;
         // M = Ups^T (R H) = (R^T Ups)^T H = RtU^T H: the same product by associativity, from the
         // D x k factors instead of a pass over the n x k rows (RtU was formed from this Ups)

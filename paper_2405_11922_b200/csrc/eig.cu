@@ -1004,6 +1004,75 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
     finish_factors(Rp, dinv, n, D, k, Psi64, sig, Gamma, Psi, ar, st, halko_gamma, rs.rowE, rs.s_colsum);
 }
 
+// ---------------------------------------------------------------------------------------
+// f3 "R-free" a7: the exact top-k (R7) of R = diag(dinv) R' without a
+// materialised R'.  R' rows are recomputed from Zhat (Eq. R-prime; the features
+// GEMM is row-local, so every recomputed row is bit-identical to the materialised one) in three
+// sweeps of `chunk` rows: (1) r = R'^T 1; (2) dinv = (R' r)^{-1/2} (written out: the ONMF needs
+// it) and G = sum_chunks R_c^T R_c (tcgen05 3xTF32 Gram per chunk, fp64 chunk sums added in chunk
+// order); (3) Gamma = R Psi Sigma^-1 row by row.  Then the same device eigensolver of G, CholeskyQR
+// polish and R8 sign rule as the materialised path.
+// ---------------------------------------------------------------------------------------
+size_t topk_rfree_ws(int64_t n, int64_t d, int32_t k, int64_t chunk) {
+    const int64_t D = 2 * d, C = std::max<int64_t>(1, std::min(n, chunk));
+    size_t s = align_up(sizeof(float) * (size_t)C * D) + 3 * align_up(sizeof(double) * D) +
+               2 * align_up(sizeof(double) * D * D) + align_up(sizeof(double) * D * k) + align_up(sizeof(double) * n * k);
+    s += std::max(std::max(features_ws_bytes(C, d), gram_tc_ws(C, D)), eig_from_gram_ws(D, k));
+    s += 2 * align_up(sizeof(double) * n * k) + ts_atb_ws(k, k) + dgemm_ws(n, k, k) + 8 * align_up(sizeof(double) * k * k) +
+         8 * align_up(sizeof(double) * 2 * 148 * k) + align_up(sizeof(double) * D * k);
+    return s + 64 * 256;
+}
+
+namespace {
+__global__ void add_to_f64_kernel(double *__restrict__ acc, const double *__restrict__ x, int64_t len) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < len) acc[i] += x[i];
+}
+}  // namespace
+
+void topk_rfree_impl(const RSource &src, int64_t n, int32_t k, float *Gamma, double *sigma, float *Psi, float *dinv,
+                     Arena &ar, cudaStream_t st) {
+    const int64_t d = src.d, D = 2 * d, C = std::max<int64_t>(1, std::min(n, src.chunk));
+    float *Rc = ar.take<float>((size_t)C * D);
+    double *r = ar.take<double>(D), *rp = ar.take<double>(D);
+    double *G = ar.take<double>((size_t)D * D), *Gc = ar.take<double>((size_t)D * D);
+    double *Psi64 = ar.take<double>((size_t)D * k), *G64 = ar.take<double>((size_t)n * k);
+    const size_t mark = ar.off;
+    TPO_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * D, st));
+    TPO_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * D * D, st));
+    for (int64_t c0 = 0; c0 < n; c0 += C) {                 // sweep 1: r = R'^T 1
+        const int64_t nc = std::min(C, n - c0);
+        features_part(src.Zhat + c0 * d, nc, d, src.Q, Rc, rp, ar, st);
+        ar.off = mark;
+        add_to_f64_kernel<<<cdiv(D, 256), 256, 0, st>>>(r, rp, D);
+        TPO_LAUNCH_CHECK();
+    }
+    for (int64_t c0 = 0; c0 < n; c0 += C) {                 // sweep 2: dinv, G = R^T R
+        const int64_t nc = std::min(C, n - c0);
+        features_part(src.Zhat + c0 * d, nc, d, src.Q, Rc, rp, ar, st);
+        ar.off = mark;
+        dinv_from_r(Rc, nc, D, r, dinv + c0, st);
+        gram_tc(Rc, dinv + c0, nc, D, Gc, ar, st);
+        ar.off = mark;
+        add_to_f64_kernel<<<cdiv(D * D, 256), 256, 0, st>>>(G, Gc, D * D);
+        TPO_LAUNCH_CHECK();
+    }
+    eig_from_gram(G, r, D, k, Psi64, sigma, ar, st);
+    ar.off = mark;
+    for (int64_t c0 = 0; c0 < n; c0 += C) {                 // sweep 3: Gamma = R Psi Sigma^-1
+        const int64_t nc = std::min(C, n - c0);
+        features_part(src.Zhat + c0 * d, nc, d, src.Q, Rc, rp, ar, st);
+        ar.off = mark;
+        gamma_rows(Rc, dinv + c0, nc, D, k, Psi64, sigma, G64 + c0 * k, ar, st);
+        ar.off = mark;
+    }
+    cast_f64_f32<<<cdiv(D * k, 256), 256, 0, st>>>(Psi64, D * k, Psi);
+    TPO_LAUNCH_CHECK();
+    polish_gamma(G64, n, k, ar, st);
+    apply_sign_rule(G64, n, k, Psi, D, ar, st, Gamma);
+    TPO_CUDA(cudaStreamSynchronize(st));
+}
+
 // a6: out = dinv . R' (R'^T (dinv . Y)), the D x b intermediate summed in fp64.
 void affinity_matvec_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, const float *Y, int64_t b,
                           float *out, Arena &ar, cudaStream_t st) {

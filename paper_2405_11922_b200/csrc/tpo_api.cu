@@ -244,8 +244,6 @@ int tpo_affinity_matvec(const float *Rp, const float *dinv, int64_t n, int64_t D
     });
 }
 
-// undocumented debugging hook (not part of include/tpo.h)
-
 size_t tpo_affinity_matvec_rfree_ws(int64_t n, int64_t d, int64_t b, int64_t chunk_rows) {
     return ts_affinity_rfree_ws(n, d, b, chunk_rows > 0 ? chunk_rows : (int64_t)1 << 18);
 }
@@ -262,6 +260,60 @@ int tpo_affinity_matvec_rfree(const float *Zhat, int64_t n, int64_t d, const flo
         check_ws(ws, ws_bytes, tpo_affinity_matvec_rfree_ws(n, d, b, chunk));
         Arena ar(ws, ws_bytes);
         ts_affinity_rfree(Zhat, n, d, Q, Y, b, out, chunk, ar, as_stream(stream));
+    });
+}
+
+static int64_t rfree_chunk_rows(int64_t chunk_rows) { return chunk_rows > 0 ? chunk_rows : (int64_t)1 << 18; }
+
+size_t tpo_topk_eig_rfree_ws(int64_t n, int64_t d, int32_t k, int64_t chunk_rows) {
+    return topk_rfree_ws(n, d, k, rfree_chunk_rows(chunk_rows));
+}
+
+int tpo_topk_eig_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, int32_t k, float *Gamma, double *sigma,
+                       float *Psi, float *dinv, int64_t chunk_rows, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && d >= 4 && d % 4 == 0, "need n >= 1 and d a positive multiple of 4");
+        TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= 2 * d, "k must lie in [1, min(n, 2d, 128)]");
+        check_ptr(Zhat, "Zhat");
+        check_ptr(Q, "Q");
+        check_ptr(Gamma, "Gamma");
+        check_ptr(Psi, "Psi");
+        check_ptr(dinv, "dinv");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        const int64_t chunk = rfree_chunk_rows(chunk_rows);
+        check_ws(ws, ws_bytes, tpo_topk_eig_rfree_ws(n, d, k, chunk));
+        Arena ar(ws, ws_bytes);
+        RSource src;
+        src.Zhat = Zhat; src.d = d; src.Q = Q; src.chunk = chunk;
+        topk_rfree_impl(src, n, k, Gamma, sigma, Psi, dinv, ar, as_stream(stream));
+    });
+}
+
+size_t tpo_cluster_rfree_ws(int64_t n, int64_t d, int32_t k, int64_t chunk_rows) {
+    return cluster_ws_bytes(n, 2 * d, k) + rfree_pass_ws(n, d, k, rfree_chunk_rows(chunk_rows));
+}
+
+int tpo_cluster_rfree(const float *Zhat, int64_t n, int64_t d, const float *Q, const float *dinv, int32_t k,
+                      const float *Gamma, const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
+                      int32_t *iters_used, int64_t chunk_rows, void *ws, size_t ws_bytes, void *stream) {
+    return guarded([&] {
+        TPO_REQUIRE(n >= 1 && d >= 4 && d % 4 == 0, "need n >= 1 and d a positive multiple of 4");
+        TPO_REQUIRE(k >= 1 && k <= 128 && k <= n && k <= 2 * d, "k must lie in [1, min(n, 2d, 128)]");
+        TPO_REQUIRE(Tf >= 0 && Tg >= 1, "need Tf >= 0 and Tg >= 1");
+        check_ptr(Zhat, "Zhat");
+        check_ptr(Q, "Q");
+        check_ptr(dinv, "dinv");
+        check_ptr(Gamma, "Gamma");
+        check_ptr(Psi, "Psi");
+        check_ptr(labels, "labels");
+        TPO_REQUIRE(sigma != nullptr, "sigma (host) is NULL");
+        const int64_t chunk = rfree_chunk_rows(chunk_rows);
+        check_ws(ws, ws_bytes, tpo_cluster_rfree_ws(n, d, k, chunk));
+        Arena ar(ws, ws_bytes);
+        RSource src;
+        src.Zhat = Zhat; src.d = d; src.Q = Q; src.chunk = chunk;
+        cluster_impl(nullptr, dinv, n, 2 * d, k, Gamma, sigma, Psi, Tf, Tg, labels, iters_used, ar, as_stream(stream),
+                     RStats(), &src);
     });
 }
 

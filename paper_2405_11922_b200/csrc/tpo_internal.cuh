@@ -142,9 +142,23 @@ void topk_eig_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int
                    Arena &ar, cudaStream_t st, const double *r_colsum = nullptr, RStats rs = RStats());
 void colsum_f64(const float *Rp, int64_t n, int64_t D, double *r, Arena &ar, cudaStream_t st);
 size_t features_ws_bytes(int64_t n, int64_t d);
+// f3 "R-free": R' rows recomputed from Zhat (Eq. R-prime) in chunks of `chunk`
+// rows wherever a pass needs them, instead of a materialised n x 2d R'
+struct RSource {
+    const float *Zhat = nullptr;   // n x d fp32
+    int64_t d = 0;
+    const float *Q = nullptr;      // d x d fp32 (the Haar rotation)
+    int64_t chunk = 0;
+};
+size_t rfree_pass_ws(int64_t n, int64_t d, int32_t k, int64_t chunk);
 void cluster_impl(const float *Rp, const float *dinv, int64_t n, int64_t D, int32_t k, const float *Gamma,
                   const double *sigma, const float *Psi, int32_t Tf, int32_t Tg, int32_t *labels,
-                  int32_t *iters_used, Arena &ar, cudaStream_t st, RStats rs = RStats());
+                  int32_t *iters_used, Arena &ar, cudaStream_t st, RStats rs = RStats(),
+                  const RSource *src = nullptr);
+// f3 a7: the exact top-k with R' recomputed from Zhat (sweeps: r, then dinv and the Gram, then Gamma)
+size_t topk_rfree_ws(int64_t n, int64_t d, int32_t k, int64_t chunk);
+void topk_rfree_impl(const RSource &src, int64_t n, int32_t k, float *Gamma, double *sigma, float *Psi, float *dinv,
+                     Arena &ar, cudaStream_t st);
 
 // G: d x d fp64, on the device when G_on_device, else host memory
 void haar_q_device(const double *G, bool G_on_device, int64_t d, float *Q_out, Arena &ar, cudaStream_t st);

@@ -294,6 +294,44 @@ def cluster(Rp: torch.Tensor, dinv: torch.Tensor, Gamma: torch.Tensor, sigma: np
     return labels, int(it.value)
 
 
+def topk_eig_rfree(Zhat: torch.Tensor, Q: torch.Tensor, k: int, chunk_rows: int = 0, stream=None):
+    """a7 without materialising R' (tpo_topk_eig_rfree, exact mode): returns (Gamma [n,k] fp32,
+    sigma np.float64[k], Psi [2d,k] fp32, dinv [n] fp32)."""
+    n, d = Zhat.shape
+    _need(Zhat, torch.float32, "Zhat")
+    _need(Q, torch.float32, "Q", (d, d))
+    Gamma = torch.empty((n, k), dtype=torch.float32, device=Zhat.device)
+    Psi = torch.empty((2 * d, k), dtype=torch.float32, device=Zhat.device)
+    dinv = torch.empty(n, dtype=torch.float32, device=Zhat.device)
+    sigma = np.zeros(k, np.float64)
+    L = lib()
+    ws = _ws(L.tpo_topk_eig_rfree_ws(n, d, int(k), int(chunk_rows)), Zhat.device)
+    check(L.tpo_topk_eig_rfree(_ptr(Zhat), n, d, _ptr(Q), int(k), _ptr(Gamma), sigma.ctypes.data_as(C.c_void_p),
+                               _ptr(Psi), _ptr(dinv), int(chunk_rows), _ptr(ws), ws.numel(), _stream(stream)))
+    return Gamma, sigma, Psi, dinv
+
+
+def cluster_rfree(Zhat: torch.Tensor, Q: torch.Tensor, dinv: torch.Tensor, Gamma: torch.Tensor, sigma: np.ndarray,
+                  Psi: torch.Tensor, Tf: int = 5, Tg: int = 20, chunk_rows: int = 0, labels=None, stream=None):
+    """a8-a9 without materialising R' (tpo_cluster_rfree): returns (labels int32 [n], Alg. 3 iterations)."""
+    n, d = Zhat.shape
+    k = Gamma.shape[1]
+    _need(Zhat, torch.float32, "Zhat")
+    _need(Q, torch.float32, "Q", (d, d))
+    _need(dinv, torch.float32, "dinv", (n,))
+    _need(Gamma, torch.float32, "Gamma", (n, k))
+    _need(Psi, torch.float32, "Psi", (2 * d, k))
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+    labels = torch.empty(n, dtype=torch.int32, device=Zhat.device) if labels is None else labels
+    it = C.c_int32(0)
+    L = lib()
+    ws = _ws(L.tpo_cluster_rfree_ws(n, d, int(k), int(chunk_rows)), Zhat.device)
+    check(L.tpo_cluster_rfree(_ptr(Zhat), n, d, _ptr(Q), _ptr(dinv), int(k), _ptr(Gamma),
+                              sigma.ctypes.data_as(C.c_void_p), _ptr(Psi), int(Tf), int(Tg), _ptr(labels), C.byref(it),
+                              int(chunk_rows), _ptr(ws), ws.numel(), _stream(stream)))
+    return labels, int(it.value)
+
+
 class Runner:
     """Whole hot path (tpo_run) with a workspace kept across calls."""
 
