@@ -714,11 +714,22 @@ __global__ void __launch_bounds__(DM_NT, 1) dm_atb_bulk_kernel(const double *__r
     }
 }
 
+// out[i] = sum_g part[g][i] in g order; 16 partials loaded ahead of their (in-order) adds, so the
+// few threads of a k x k reduction are not bound by one L2 round trip per partial
 __global__ void reduce_parts_kernel(const double *__restrict__ part, int64_t G, int64_t len, double *__restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= len) return;
+    constexpr int U = 16;
     double s = 0.0;
-    for (int64_t g = 0; g < G; ++g) s += part[g * len + i];
+    int64_t g = 0;
+    for (; g + U <= G; g += U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcg(part + (g + u) * len + i);
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += v[u];
+    }
+    for (; g < G; ++g) s += part[g * len + i];
     out[i] = s;
 }
 

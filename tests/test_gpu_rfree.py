@@ -94,7 +94,7 @@ def test_topk_rfree_matches_materialised_gpu(tpo, k40):
     Gm, s, Ps, dv = tpo.topk_eig_rfree(Zh, Q, g.k, chunk_rows=1000)
     assert float(((dv - dg).abs() / dg.abs()).max()) <= 1e-6
     assert DN.sin_theta(Gm.cpu().numpy(), Gm_m.cpu().numpy()) <= 1e-5
-    assert np.allclose(s, s_m, rtol=1e-9)
+    assert np.allclose(s, s_m, rtol=1e-6)       # the Gram's fp32 tile sums flush at other row boundaries
 
 
 @pytest.mark.parametrize("chunk", [0, 700])
