@@ -939,7 +939,7 @@ size_t propagate_ws_bytes(int64_t n_u, int64_t n_v, int64_t nnz, int64_t d) {
 
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
                     int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms,
-                    int reserve_launches) {
+                    int reserve_launches, cudaEvent_t b_cols_ready) {
     const int64_t n = B.n_rows, m = B.n_cols, nnz = B.nnz;
     const int d4 = (int)(d / 4);
     const float c = alpha < 1.0f ? 1.0f - alpha : 1.0f;    // R1
@@ -1011,6 +1011,8 @@ void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int
         } else {
             TPO_CUDA(cudaMemsetAsync(Qv, 0, sizeof(float) * 0, st));
         }
+        // B's column ids may still be in flight (host inputs): nothing before the first U-side SpMM reads them
+        if (t == 0 && b_cols_ready) TPO_CUDA(cudaStreamWaitEvent(st, b_cols_ready, 0));
         SpmmArgs a{};
         a.rowptr = B.row_ptr; a.col = B.col_idx; a.val = B.val;
         a.src = (const float4 *)Qv; a.d4 = d4; a.nslices = nslices;

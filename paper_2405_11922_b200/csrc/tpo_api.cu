@@ -787,12 +787,15 @@ static void haar_reserve(int &sms, int &launches) {
 // (recorded on `st` once G is on the device); with `haar_first` its kernels are queued before
 // the propagation's (host inputs: the Haar QR runs while the CSRs and X are still being copied).
 struct RunRes {   // events and the Haar side stream of tpo_run / tpo_run_host (see run_res)
-    cudaEvent_t ev[5] = {}, join = nullptr, g_ready = nullptr;
-    cudaStream_t side = nullptr;
+    cudaEvent_t ev[5] = {}, join = nullptr, g_ready = nullptr, x_done = nullptr, b_ready = nullptr;
+    cudaStream_t side = nullptr, copy = nullptr;
     RunRes() {
         for (auto &e : ev) TPO_CUDA(cudaEventCreate(&e));
         TPO_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
         TPO_CUDA(cudaEventCreateWithFlags(&g_ready, cudaEventDisableTiming));
+        TPO_CUDA(cudaEventCreateWithFlags(&x_done, cudaEventDisableTiming));
+        TPO_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming));
+        TPO_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
         int lo = 0, hi = 0;   // highest priority: the latency-bound Haar chain interleaves with the SpMMs
         TPO_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         TPO_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
@@ -801,7 +804,10 @@ struct RunRes {   // events and the Haar side stream of tpo_run / tpo_run_host (
         for (auto &e : ev) if (e) cudaEventDestroy(e);
         if (join) cudaEventDestroy(join);
         if (g_ready) cudaEventDestroy(g_ready);
+        if (x_done) cudaEventDestroy(x_done);
+        if (b_ready) cudaEventDestroy(b_ready);
         if (side) cudaStreamDestroy(side);
+        if (copy) cudaStreamDestroy(copy);
     }
 };
 
@@ -819,7 +825,8 @@ static RunRes &run_res() {
 static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_t d, float alpha, int32_t T,
                      int32_t k, const double *G, bool haar_first, cudaEvent_t g_ready, int32_t eig_mode,
                      const float *Omega, int32_t p, int32_t q, int32_t Tf, int32_t Tg, int32_t *labels,
-                     double *timings_ms, Arena &ar, cudaStream_t st, RunRes &res, int res_sms, int res_launches) {
+                     double *timings_ms, Arena &ar, cudaStream_t st, RunRes &res, int res_sms, int res_launches,
+                     cudaEvent_t b_cols_ready = nullptr) {
     const int64_t n = B->n_rows, D = 2 * d;
     float *Z = ar.take<float>(n * d), *Zh = ar.take<float>(n * d);
     float *Rp = ar.take<float>(n * D), *dinv = ar.take<float>(n);
@@ -845,7 +852,7 @@ static void run_body(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, in
         TPO_CUDA(cudaEventRecord(join, side));
     };
     if (haar_first) haar();
-    propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, res_sms, res_launches);
+    propagate_impl(*B, *Bt, X, d, alpha, T, Z, Zh, ar, st, res_sms, res_launches, b_cols_ready);
     ar.off = mark;
     if (!haar_first) haar();
     TPO_CUDA(cudaEventRecord(ev[1], st));
@@ -941,7 +948,9 @@ int tpo_run_host(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_
         h2d(Gd, G, sizeof(double) * d * d);
         TPO_CUDA(cudaEventRecord(res.g_ready, st));
         h2d(brp, B->row_ptr, sizeof(int64_t) * (n + 1));
-        h2d(bci, B->col_idx, sizeof(int32_t) * nnz);
+        // unweighted: B's column ids are first read by hop 1's U-side SpMM, so they are copied on a
+        // side copy stream after X, during the degrees, schedules and hop 1's V-side SpMM
+        if (weighted) h2d(bci, B->col_idx, sizeof(int32_t) * nnz);
         h2d(trp, Bt->row_ptr, sizeof(int64_t) * (m + 1));
         h2d(tci, Bt->col_idx, sizeof(int32_t) * nnz);
         if (weighted) {
@@ -949,6 +958,14 @@ int tpo_run_host(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_
             h2d(tv, Bt->val, sizeof(float) * nnz);
         }
         h2d(Xd, X, sizeof(float) * n * d);
+        cudaEvent_t b_cols_ready = nullptr;
+        if (!weighted && nnz > 0) {
+            TPO_CUDA(cudaEventRecord(res.x_done, st));
+            TPO_CUDA(cudaStreamWaitEvent(res.copy, res.x_done, 0));
+            TPO_CUDA(cudaMemcpyAsync(bci, B->col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, res.copy));
+            TPO_CUDA(cudaEventRecord(res.b_ready, res.copy));
+            b_cols_ready = res.b_ready;
+        }
         const tpo_csr_t Bd{n, m, nnz, brp, bci, bv}, Btd{m, n, nnz, trp, tci, tv};
         // the Haar rotation runs during the input copies: no SMs are held back for it
         int res_sms = 0, res_launches = 0;
@@ -957,7 +974,8 @@ int tpo_run_host(const tpo_csr_t *B, const tpo_csr_t *Bt, const float *X, int64_
             if (sscanf(e, "%d,%d", &a, &b) == 2 && a >= 0 && b >= 0) { res_sms = a; res_launches = b; }
         }
         run_body(&Bd, &Btd, Xd, d, alpha, T, k, Gd, true, res.g_ready, eig_mode, Omega, p, q, Tf, Tg, lab, timings_ms,
-                 ar, st, res, res_sms, res_launches);
+                 ar, st, res, res_sms, res_launches, b_cols_ready);
+        if (b_cols_ready) TPO_CUDA(cudaStreamWaitEvent(st, b_cols_ready, 0));   // joined even when T = 0
         TPO_CUDA(cudaMemcpyAsync(labels, lab, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         TPO_CUDA(cudaStreamSynchronize(st));
     });

@@ -93,7 +93,7 @@ int sm_count();
 // free (tpo_run keeps some for the Haar rotation running beside the propagation on a side stream).
 void propagate_impl(const tpo_csr_t &B, const tpo_csr_t &Bt, const float *X, int64_t d, float alpha,
                     int32_t T, float *Z, float *Zhat, Arena &ar, cudaStream_t st, int reserve_sms = 0,
-                    int reserve_launches = 1 << 30);
+                    int reserve_launches = 1 << 30, cudaEvent_t b_cols_ready = nullptr);
 // sharded propagation pieces (spmm.cu)
 size_t shard_spmm_ws_bytes(int64_t n_rows, int64_t nnz, int64_t d);
 void propagate_local_t0(const float *Xp, int64_t n_p, int64_t d, float alpha, float *Zp, float *Zhat_p, cudaStream_t st);
