@@ -32,10 +32,15 @@ def main(rep):
                 except ValueError:
                     pass
         stalls.sort(reverse=True)
+        pipes = sorted((k, v) for k, v in d.items()
+                       if k.startswith("sm__pipe_") and k.endswith("_cycles_active.avg.pct_of_peak_sustained_active")
+                       and v not in ("0", "0.000000"))
         print(f"{name:48s} t={t} dram_rd={rd} dram_wr={wr} "
               f"dram%={f(d, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} "
               f"l2hit={f(d, 'lts__t_sector_hit_rate.pct'):.1f} occ={f(d, 'sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} "
               f"regs={d.get('launch__registers_per_thread')} stalls={[(round(a, 2), b) for a, b in stalls[:4]]}")
+        if pipes:
+            print("    pipes: " + ", ".join(f"{k[len('sm__pipe_'):-len('_cycles_active.avg.pct_of_peak_sustained_active')]}={v}%" for k, v in pipes))
 
 
 if __name__ == "__main__":
