@@ -453,6 +453,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         run_sharded(args, None, ws, rank, local, dev, pre=shard_inputs(args, ws, rank))
         return
+    if args.impl == "reference" and rank != 0:
+        return      # rank 0 alone runs and prints the oracle arm; the other ranks exit 0 without work
     g = make_config(args.config)
 
     if args.impl == "reference":
