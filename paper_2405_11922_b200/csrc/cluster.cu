@@ -517,7 +517,9 @@ void nci_assign_part(const double *U, const double *Phi, int64_t n, int k, int32
         else nci_fused_kernel<32, 4><<<nbf, 128, 0, st>>>(U, Phi, n, k, rpf, labels, s, part, cpart);
         TPO_LAUNCH_CHECK();
     } else {
-        if (k <= 64) {
+        if (ts64_enabled() && k <= 104) {   // certified argmax on the fp64 tensor path (R13), as tpo_run's loop
+            ts_assign(U, Phi, n, k, labels, s.changed, s.done, st);
+        } else if (k <= 64) {
             assign_small_kernel<64><<<cdiv(n, 128), 128, 0, st>>>(U, Phi, n, k, labels, s);
         } else {
             const size_t phi_smem = sizeof(double) * ((size_t)k * k + (size_t)8 * AR * k);

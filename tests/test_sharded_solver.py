@@ -274,3 +274,34 @@ def test_sharded_solver_gpu_emulated(world):
     Gmo, so, Pso, _ = O.topk(Rp32, dinv32, g.k)
     lab_o, _, _ = O.cluster(Rp32, dinv32, Gmo.astype(np.float32), so, Pso.astype(np.float32), 5, 20)
     assert DN.ari(lab, lab_o) >= 0.999
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [40, 50, 100])
+def test_shard_nci_assign_tensor_path_gpu(k):
+    """Alg. 3 through the sharded solver's per-rank step tpo_shard_nci_assign at
+    32 < k <= 104, where the assignment runs the certified fp64-tensor-path argmax (R13): labels equal
+    the oracle's bit for bit on a ragged row count (equal rows and exact ties included)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_11922_b200 import build
+    build.build()
+    from paper_2405_11922_b200.sharded import GpuSolverOps
+    n, Tg = 20011, 20
+    rng = np.random.default_rng(100 + k)
+    Ups = np.abs(rng.standard_normal((n, k))) * 0.3
+    Ups[np.arange(n), rng.integers(0, k, n)] += 1.0          # a dominant cluster per row, noisy
+    Ups[:64] = Ups[0]                                         # equal rows
+    Ups[64:96] = 0.25                                         # exact ties -> smallest l
+    ref, it_ref = O.nci(Ups, Tg)
+    ops = GpuSolverOps(n, 8, k, "cuda")
+    U = torch.from_numpy(Ups).cuda()
+    Phi, labels, iters = ops.eye(), ops.labels(), 0
+    for t in range(Tg):
+        changed, sums, counts = ops.nci_assign(U, Phi, labels)
+        iters += 1
+        if int(changed.item()) == 0 or t == Tg - 1:
+            break
+        Phi = ops.phi(sums, counts)
+    assert np.array_equal(labels.cpu().numpy(), ref)
+    assert abs(iters - it_ref) <= 1      # the oracle counts the iterations it used; the fix-point check is one more pass here
